@@ -1,0 +1,202 @@
+/*
+ * bosp_b200.h -- C ABI of the B200-native BOSP core (libbosp_b200.so).
+ *
+ * Drop-in boundary for the reference's solver + matvec-callback plugin API
+ * (/root/reference/proj, C++20).  Plain pointers and sizes only: every block is a host
+ * column-major fp64 array (column j of an n x m block starts at j*n), every index is int64,
+ * errors are status codes + a thread-local message (no C++ exception crosses this ABI).
+ * Each entry point names the reference interface it replaces (file:line relative to
+ * /root/reference/proj).  The C++ facade with the reference's own names (bosp::solve,
+ * bosp::LinearOperator, ...) is paper_2506_08355_b200/csrc/api.hpp; this header is what an
+ * FFI (ctypes / cgo / JNI / N-API) binds.
+ */
+#ifndef BOSP_B200_H
+#define BOSP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes: one per exception class of include/bosp/core/errors.hpp:9-69. */
+typedef enum {
+    BOSP_OK = 0,
+    BOSP_CONTRACT_VIOLATION = 1,
+    BOSP_INGESTION_ERROR = 2,
+    BOSP_NULLSPACE_LEAK = 3,
+    BOSP_DEGENERATE_SPECTRUM = 4,
+    BOSP_RANK_MISMATCH = 5,
+    BOSP_INVALID_NULLSPACE = 6,
+    BOSP_INITIALIZATION_FAILURE = 7,
+    BOSP_NOT_ENOUGH_SAMPLES = 8,
+    BOSP_NUMERICAL_ABORT = 9,
+    BOSP_CUDA_ERROR = 10,
+    BOSP_ERROR = 11
+} bosp_status;
+
+/* Message of the last failing call on this thread. */
+const char* bosp_last_error(void);
+/* Library/device identification: writes the device name, returns the SM count (or <0). */
+int bosp_device_info(char* name, int name_len);
+
+/* ---------------------------------------------------------------------------------------
+ * Operators -- replaces LinearOperator (include/bosp/core/linear_operator.hpp:15-48)
+ * --------------------------------------------------------------------------------------- */
+typedef struct bosp_op_s* bosp_op;
+
+/* Host callback: y(:, j) = A x(:, j), x and y host n x ncols column-major (ld = n).
+ * Replaces LinearOperator::ApplyFn / from_callback (linear_operator.hpp:19,25). */
+typedef void (*bosp_host_apply_fn)(void* ctx, const double* x, double* y, int64_t n, int64_t ncols);
+/* Device callback (new): x, y in HBM with leading dims ldx, ldy; stream is a cudaStream_t. */
+typedef void (*bosp_device_apply_fn)(void* ctx, const double* x, int64_t ldx, double* y,
+                                     int64_t ldy, int64_t n, int64_t ncols, void* stream);
+
+/* from_dense (linear_operator.cpp:12-31): a is n x n column-major, copied to HBM. */
+bosp_status bosp_op_dense(int64_t n, const double* a, bosp_op* out);
+/* from_csr (linear_operator.cpp:33-43; SparseMatrixCSR sparse_csr.hpp:12-28). */
+bosp_status bosp_op_csr(int64_t n, const int64_t* row_offsets, const int64_t* col_indices,
+                        const double* values, bosp_op* out);
+/* from_callback (linear_operator.cpp:45-47). */
+bosp_status bosp_op_callback(int64_t n, bosp_host_apply_fn fn, void* ctx, bosp_op* out);
+bosp_status bosp_op_device_callback(int64_t n, bosp_device_apply_fn fn, void* ctx, bosp_op* out);
+
+/* Matrix-free structured-grid Laplacian family (new; the reference reaches such operators
+ * only through from_callback):  y = scale * L_bc x + v .* x on nx*ny*nz nodes (nz=1: 5-point).
+ * bc: 0 Neumann graph Laplacian, 1 Dirichlet.  potential: 0 none, 1 harmonic 0.5|x|^2 with
+ * node coordinates origin + (i+1)*h, 2 explicit array v (n values). */
+typedef struct {
+    int64_t nx, ny, nz;
+    int32_t bc;
+    double scale;
+    int32_t potential;
+    double origin, h;
+    const double* v;
+} bosp_stencil;
+bosp_status bosp_op_stencil(const bosp_stencil* spec, bosp_op* out);
+
+/* identity / scaled_identity / diagonal / shifted (linear_operator.cpp:49-92). */
+bosp_status bosp_op_identity(int64_t n, bosp_op* out);
+bosp_status bosp_op_scaled_identity(int64_t n, double alpha, bosp_op* out);
+bosp_status bosp_op_diagonal(int64_t n, const double* d, bosp_op* out);
+bosp_status bosp_op_shifted(bosp_op base, double sigma, bosp_op* out);
+
+/* LinearOperator::apply (linear_operator.cpp:94-106) on host blocks. */
+bosp_status bosp_op_apply(bosp_op op, int64_t ncols, const double* x, double* y);
+int64_t bosp_op_dim(bosp_op op);
+/* 0 dense, 1 sparse_csr, 2 matrix_free_callback (LinearOperator::Kind). */
+int bosp_op_kind(bosp_op op);
+void bosp_op_free(bosp_op op);
+
+/* ---------------------------------------------------------------------------------------
+ * Solver -- replaces bosp::solve / BospConfig / SolverStats / EigenResult
+ * (include/bosp/solver/bosp_solver.hpp:15-98)
+ * --------------------------------------------------------------------------------------- */
+typedef struct {
+    int64_t nev, nb;
+    double tol;
+    int64_t ngs, s;
+    int32_t moving;          /* -1 unset (default rule), 0 off, 1 on */
+    int64_t max_outer_iter;
+    uint64_t rng_seed;
+    double inner_cg_tol;
+    int64_t inner_cg_max_iter;
+    double tol_null;
+    int64_t rank_hint;       /* -1 unset */
+} bosp_config;
+
+/* BospConfig defaults (bosp_solver.hpp:15-34). */
+void bosp_config_default(bosp_config* cfg);
+
+typedef struct {
+    int64_t iterations, matvec_count, step3_matvecs, step3_vecprods, max_width_u;
+    double max_biorth_deviation, max_deflation_crossgram, final_biorth_deviation;
+    int32_t nevconv_monotone;
+    double wall_seconds;      /* host steady clock around the whole solve */
+    int64_t nev_converged;
+    int32_t converged;
+    /* B200 additions */
+    double device_seconds;    /* CUDA events on the solver stream around the whole solve */
+    double host_small_seconds;
+    int64_t repairs, cg_iterations, gpu_launches;
+} bosp_stats;
+
+/* bosp::solve (bosp_solver.cpp:513-536).  B may be NULL (Euclidean inner product).
+ * Nullspace: r >= 0 with x0, y0 (n x r) supplies GeneralizedNullspace; r < 0 asks the solver
+ * to compute it (compute_nullspace, nullspace.cpp:135).  Outputs have capacity `cap` pairs:
+ * lambdas[cap], x and y (n x cap, may be NULL), residuals[cap]; *nout = pairs returned.
+ * history (optional, history_cap x nev row-major) receives residual_history. */
+bosp_status bosp_solve(bosp_op K, bosp_op M, bosp_op B, const bosp_config* cfg, int64_t r,
+                       const double* x0, const double* y0, int64_t cap, double* lambdas,
+                       double* x, double* y, double* residuals, int64_t* nout, bosp_stats* stats,
+                       double* history, int64_t history_cap, int64_t* history_rows);
+
+/* regression_coefficients (bosp_solver.cpp:538-580); history rows x cols row-major. */
+bosp_status bosp_regression(const double* history, int64_t rows, int64_t cols, int64_t idx,
+                            double tol, double* alpha, double* beta, int32_t* degenerate);
+
+/* analytic_nullspace_T (nullspace.cpp:195-212): x0, y0 are n x 1. */
+bosp_status bosp_analytic_nullspace_T(int64_t n, double* x0, double* y0);
+/* compute_nullspace (nullspace.cpp:135-193): up to cap columns into x0/y0, rank in *r. */
+bosp_status bosp_compute_nullspace(bosp_op K, bosp_op M, bosp_op B, int64_t rank_hint,
+                                   double tol_null, uint64_t seed, int64_t cap, int64_t* r,
+                                   double* x0, double* y0);
+
+/* ---------------------------------------------------------------------------------------
+ * Block kernels (device), host blocks in/out -- kernels.hpp:22-30, biorth.hpp:30-45, cg.hpp:17
+ * --------------------------------------------------------------------------------------- */
+/* G (a x b) = X^T B Y  (block_inner, kernels.cpp:47-68). */
+bosp_status bosp_block_inner(bosp_op B, int64_t n, int64_t a, int64_t b, const double* x,
+                             const double* y, double* g);
+/* out (n x b) = X C  (block_product, kernels.cpp:70-87). */
+bosp_status bosp_block_product(int64_t n, int64_t a, int64_t b, const double* x, const double* c,
+                               double* out);
+/* Y (n x b) -= X C  (block_axpy, kernels.cpp:89-104). */
+bosp_status bosp_block_axpy(int64_t n, int64_t a, int64_t b, const double* x, const double* c,
+                            double* y);
+/* mgs_biorth (classical=0) / cgs_biorth (classical=1) (biorth.cpp:102-114).  P, Q n x m
+ * receive the kept columns; kept/dropped index lists (capacity m). */
+bosp_status bosp_biorth(int32_t classical, bosp_op B, int64_t n, int64_t m, const double* x,
+                        const double* y, double drop_tol, double* p, double* q, int64_t* kept,
+                        int64_t* nkept, int64_t* dropped, int64_t* ndropped);
+/* biorth_against (biorth.cpp:116-133): nbases pairs (ps[i], qs[i]) of widths[i] columns. */
+bosp_status bosp_biorth_against(bosp_op B, int64_t n, int64_t nbases, const int64_t* widths,
+                                const double* const* ps, const double* const* qs, int64_t m,
+                                const double* x, const double* y, double* xo, double* yo);
+/* biorth_residual (biorth.cpp:135-143). */
+bosp_status bosp_biorth_residual(bosp_op B, int64_t n, int64_t m, const double* p,
+                                 const double* q, double* out);
+/* cg_solve (cg.cpp:11-58), batched over columns with per-column masks. */
+bosp_status bosp_cg_solve(bosp_op A, int64_t m, const double* rhs, const double* x0, double tol,
+                          int64_t max_iter, double* x, int32_t* breakdown, int64_t* max_it_used);
+
+/* Host small dense (projected_lrep.cpp:48-80, dense_kernels.cpp:11-123). */
+bosp_status bosp_solve_small_lrep(int64_t d, const double* khat, const double* mhat, int64_t k,
+                                  double* lambdas, double* xhat, double* yhat);
+bosp_status bosp_jacobi_svd(int64_t m, int64_t k, const double* a, double* u, double* sigma,
+                            double* v, int64_t* sweeps, int32_t* converged);
+bosp_status bosp_cholesky(int64_t n, const double* a, double* l, int32_t* ok);
+
+/* ---------------------------------------------------------------------------------------
+ * Measurement hooks (bench.py): kernel-family CUDA-event timing and launch counting.
+ * --------------------------------------------------------------------------------------- */
+/* Time every launch of one kernel family ("spmm", "gram", "product", "cg_vec", ...); NULL or
+ * "" disables. */
+void bosp_profile_enable(const char* family);
+/* Synchronises; returns launches, summed device ms, algorithmic bytes and flops since enable. */
+void bosp_profile_collect(int64_t* launches, double* ms, double* bytes, double* flops);
+/* Kernel launches issued by this library since the last reset. */
+int64_t bosp_launch_count(void);
+void bosp_launch_reset(void);
+/* Per-family launch counts as "family=count;..." into buf. */
+int bosp_launch_families(char* buf, int len);
+void bosp_device_sync(void);
+/* Pinned host memory for e2e measurements. */
+void* bosp_host_alloc(int64_t bytes);
+void bosp_host_free(void* p);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BOSP_B200_H */

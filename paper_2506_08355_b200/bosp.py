@@ -1,0 +1,427 @@
+"""Python mirror of the reference's BOSP API (proj/include/bosp/...), bound to the B200 C ABI.
+
+Same names and argument meaning as the reference's C++ surface so tests read like the
+reference's own:  LinearOperator.from_dense / from_csr / from_callback / identity /
+scaled_identity / diagonal / shifted (+ stencil, new), InnerProduct, BospConfig,
+GeneralizedNullspace, solve(K, M, ip, cfg, ns), block_inner / block_product / block_axpy,
+mgs_biorth / cgs_biorth / biorth_against / biorth_residual, cg_solve, solve_small_lrep,
+jacobi_svd, cholesky_lower, regression_coefficients, analytic_nullspace_T, compute_nullspace.
+Every numeric call runs through libbosp_b200.so on the GPU (host small algebra excepted, as in
+the north star); there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib as L
+from ._lib import (BospError, ContractViolation, CudaError, DegenerateSpectrum,  # noqa: F401
+                   IngestionError, InitializationFailure, InvalidNullspace, NotEnoughSamples,
+                   NullspaceLeak, NumericalAbort, RankMismatch, check, lib)
+
+
+def _f(a, ndim=2):
+    a = np.asarray(a, dtype=np.float64)
+    if ndim == 2 and a.ndim == 1:
+        a = a[:, None]
+    return np.asfortranarray(a)
+
+
+def _p(a):
+    return None if a is None else C.c_void_p(a.ctypes.data)
+
+
+class LinearOperator:
+    """Apply-only operator (linear_operator.hpp:15-48); data lives in HBM."""
+    dense, sparse_csr, matrix_free_callback = 0, 1, 2
+
+    def __init__(self, handle, keep=None):
+        self._h = handle
+        self._keep = keep
+
+    def __del__(self):
+        try:
+            if self._h:
+                lib().bosp_op_free(self._h)
+        except Exception:
+            pass
+
+    @classmethod
+    def _make(cls, fn, *args, keep=None):
+        h = L.OpPtr()
+        check(fn(*args, C.byref(h)))
+        return cls(h, keep)
+
+    @classmethod
+    def from_dense(cls, a):
+        a = _f(a)
+        if a.shape[0] != a.shape[1]:
+            raise ContractViolation("LinearOperator: dense operator must be square")
+        return cls._make(lib().bosp_op_dense, C.c_int64(a.shape[0]), _p(a))
+
+    @classmethod
+    def from_csr(cls, rowptr, colidx=None, vals=None):
+        if colidx is None:  # problems.Csr
+            rowptr, colidx, vals = rowptr.rowptr, rowptr.colidx, rowptr.vals
+        rp = np.ascontiguousarray(rowptr, dtype=np.int64)
+        ci = np.ascontiguousarray(colidx, dtype=np.int64)
+        vv = np.ascontiguousarray(vals, dtype=np.float64)
+        return cls._make(lib().bosp_op_csr, C.c_int64(rp.shape[0] - 1), _p(rp), _p(ci), _p(vv))
+
+    @classmethod
+    def from_callback(cls, dim, fn):
+        """fn(x) -> y on (n, m) float64 arrays (host ApplyFn, linear_operator.cpp:45-47)."""
+        def tramp(ctx, xp, yp, n, m):
+            x = np.ctypeslib.as_array(xp, shape=(m, n)).T
+            y = np.ctypeslib.as_array(yp, shape=(m, n)).T
+            y[...] = fn(np.array(x))
+        cb = L.HOST_APPLY(tramp)
+        return cls._make(lib().bosp_op_callback, C.c_int64(dim), cb, None, keep=cb)
+
+    @classmethod
+    def stencil(cls, nx, ny, nz, bc, scale, potential="none", origin=0.0, h=1.0, v=None):
+        bcs = {"neumann": 0, "dirichlet": 1}[bc]
+        pot = {"none": 0, "harmonic": 1, "array": 2}[potential]
+        vv = None if v is None else np.ascontiguousarray(v, dtype=np.float64)
+        spec = L.Stencil(nx, ny, nz, bcs, scale, pot, origin, h, None if vv is None else vv.ctypes.data)
+        return cls._make(lib().bosp_op_stencil, C.byref(spec), keep=vv)
+
+    @classmethod
+    def from_stencil(cls, s):
+        """problems.Stencil -> matrix-free device operator."""
+        return cls.stencil(s.nx, s.ny, s.nz, s.bc, s.scale, s.potential, s.origin, s.h, s.v)
+
+    @classmethod
+    def identity(cls, n):
+        return cls._make(lib().bosp_op_identity, C.c_int64(n))
+
+    @classmethod
+    def scaled_identity(cls, n, alpha):
+        return cls._make(lib().bosp_op_scaled_identity, C.c_int64(n), C.c_double(alpha))
+
+    @classmethod
+    def diagonal(cls, d):
+        d = np.ascontiguousarray(d, dtype=np.float64)
+        return cls._make(lib().bosp_op_diagonal, C.c_int64(d.shape[0]), _p(d))
+
+    @classmethod
+    def shifted(cls, a, sigma):
+        return cls._make(lib().bosp_op_shifted, a._h, C.c_double(sigma), keep=a)
+
+    @property
+    def dim(self):
+        return int(lib().bosp_op_dim(self._h))
+
+    @property
+    def kind(self):
+        return int(lib().bosp_op_kind(self._h))
+
+    def apply(self, x):
+        x = _f(x)
+        if x.shape[0] != self.dim:
+            raise ContractViolation("LinearOperator::apply: dimension mismatch")
+        y = np.zeros_like(x, order="F")
+        check(lib().bosp_op_apply(self._h, C.c_int64(x.shape[1]), _p(x), _p(y)))
+        return y
+
+
+def block_apply(op, x):
+    return op.apply(x)
+
+
+class InnerProduct:
+    """x^T B y (inner_product.hpp:12-29); identity when weight is None."""
+
+    def __init__(self, weight: LinearOperator | None = None):
+        self.weight = weight
+
+    @property
+    def weighted(self):
+        return self.weight is not None
+
+    def _h(self):
+        return None if self.weight is None else self.weight._h
+
+
+@dataclass
+class BospConfig:  # bosp_solver.hpp:15-34
+    nev: int = 1
+    nb: int = 0
+    tol: float = 1e-8
+    ngs: int = 1
+    s: int = 3
+    moving: bool | None = None
+    max_outer_iter: int = 500
+    rng_seed: int = 0
+    inner_cg_tol: float = 1e-2
+    inner_cg_max_iter: int = 20
+    tol_null: float = 1e-10
+    rank_hint: int | None = None
+
+    def c(self):
+        return L.Config(self.nev, self.nb, self.tol, self.ngs, self.s,
+                        -1 if self.moving is None else int(bool(self.moving)), self.max_outer_iter,
+                        self.rng_seed, self.inner_cg_tol, self.inner_cg_max_iter, self.tol_null,
+                        -1 if self.rank_hint is None else int(self.rank_hint))
+
+    def effective_nb(self):
+        if self.nb > 0:
+            return min(self.nb, self.nev)
+        return max(1, min((self.nev + 4) // 5, 150))
+
+    def effective_moving(self):
+        return bool(self.moving) if self.moving is not None else self.nev > 3 * self.effective_nb()
+
+
+@dataclass
+class GeneralizedNullspace:  # nullspace.hpp:13-19
+    x0: np.ndarray
+    y0: np.ndarray
+
+    @property
+    def r(self):
+        return 0 if self.x0 is None else int(self.x0.shape[1])
+
+
+@dataclass
+class EigenResult:  # bosp_solver.hpp:71-81
+    lambdas: np.ndarray
+    x: np.ndarray
+    y: np.ndarray
+    iterations: int
+    residuals: np.ndarray
+    history: np.ndarray
+    converged: bool
+    nev_converged: int
+    stats: dict = field(default_factory=dict)
+
+
+def solve(K: LinearOperator, M: LinearOperator, ip: InnerProduct | None, cfg: BospConfig,
+          ns: GeneralizedNullspace | None = None, want_vectors=True, history_cap=2000) -> EigenResult:
+    """bosp::solve (bosp_solver.cpp:513-536) on the B200."""
+    ip = ip or InnerProduct()
+    n = K.dim
+    cap = cfg.nev
+    lam = np.zeros(cap)
+    res = np.zeros(cap)
+    x = np.zeros((n, cap), order="F") if want_vectors else None
+    y = np.zeros((n, cap), order="F") if want_vectors else None
+    hist = np.zeros((history_cap, cfg.nev))
+    hrows, nout = C.c_int64(), C.c_int64()
+    st = L.Stats()
+    cc = cfg.c()
+    if ns is None:
+        r, x0, y0 = -1, None, None
+    else:
+        x0, y0 = _f(ns.x0), _f(ns.y0)
+        r = x0.shape[1]
+    check(lib().bosp_solve(K._h, M._h, ip._h(), C.byref(cc), C.c_int64(r), _p(x0), _p(y0),
+                           C.c_int64(cap), _p(lam), _p(x), _p(y), _p(res), C.byref(nout),
+                           C.byref(st), _p(hist), C.c_int64(history_cap), C.byref(hrows)))
+    k = nout.value
+    stats = {f[0]: getattr(st, f[0]) for f in L.Stats._fields_}
+    return EigenResult(lam[:k], None if x is None else x[:, :k], None if y is None else y[:, :k],
+                       int(st.iterations), res[:k], hist[:min(hrows.value, history_cap)],
+                       bool(st.converged), int(st.nev_converged), stats)
+
+
+def regression_coefficients(history, idx, tol):
+    h = np.ascontiguousarray(history, dtype=np.float64)
+    a, b, d = C.c_double(), C.c_double(), C.c_int32()
+    check(lib().bosp_regression(_p(h), C.c_int64(h.shape[0]), C.c_int64(h.shape[1]),
+                                C.c_int64(idx), C.c_double(tol), C.byref(a), C.byref(b), C.byref(d)))
+    return a.value, b.value, bool(d.value)
+
+
+def analytic_nullspace_T(n):
+    x0 = np.zeros((n, 1), order="F")
+    y0 = np.zeros((n, 1), order="F")
+    check(lib().bosp_analytic_nullspace_T(C.c_int64(n), _p(x0), _p(y0)))
+    return GeneralizedNullspace(x0, y0)
+
+
+def compute_nullspace(K, M, rank_hint=None, tol_null=1e-10, ip=None, seed=777, cap=256):
+    n = K.dim
+    x0 = np.zeros((n, cap), order="F")
+    y0 = np.zeros((n, cap), order="F")
+    r = C.c_int64()
+    ip = ip or InnerProduct()
+    check(lib().bosp_compute_nullspace(K._h, M._h, ip._h(), C.c_int64(-1 if rank_hint is None else rank_hint),
+                                       C.c_double(tol_null), C.c_uint64(seed), C.c_int64(cap),
+                                       C.byref(r), _p(x0), _p(y0)))
+    return GeneralizedNullspace(x0[:, :r.value].copy(order="F"), y0[:, :r.value].copy(order="F"))
+
+
+# ---- block kernels (kernels.hpp / biorth.hpp / cg.hpp) -------------------------------------
+def block_inner(ip, x, y):
+    x, y = _f(x), _f(y)
+    ip = ip or InnerProduct()
+    g = np.zeros((x.shape[1], y.shape[1]), order="F")
+    check(lib().bosp_block_inner(ip._h(), C.c_int64(x.shape[0]), C.c_int64(x.shape[1]),
+                                 C.c_int64(y.shape[1]), _p(x), _p(y), _p(g)))
+    return g
+
+
+def block_product(x, c):
+    x, c = _f(x), _f(c)
+    out = np.zeros((x.shape[0], c.shape[1]), order="F")
+    check(lib().bosp_block_product(C.c_int64(x.shape[0]), C.c_int64(x.shape[1]),
+                                   C.c_int64(c.shape[1]), _p(x), _p(c), _p(out)))
+    return out
+
+
+def block_axpy(x, c, y):
+    x, c = _f(x), _f(c)
+    y = np.array(y, dtype=np.float64, order="F", copy=True)
+    check(lib().bosp_block_axpy(C.c_int64(x.shape[0]), C.c_int64(x.shape[1]),
+                                C.c_int64(c.shape[1]), _p(x), _p(c), _p(y)))
+    return y
+
+
+def _biorth(x, y, ip, drop_tol, classical):
+    x, y = _f(x), _f(y)
+    n, m = x.shape
+    ip = ip or InnerProduct()
+    p = np.zeros((n, m), order="F")
+    q = np.zeros((n, m), order="F")
+    kept = np.zeros(max(m, 1), dtype=np.int64)
+    dropped = np.zeros(max(m, 1), dtype=np.int64)
+    nk, nd = C.c_int64(), C.c_int64()
+    check(lib().bosp_biorth(C.c_int32(int(classical)), ip._h(), C.c_int64(n), C.c_int64(m), _p(x),
+                            _p(y), C.c_double(drop_tol), _p(p), _p(q), _p(kept), C.byref(nk),
+                            _p(dropped), C.byref(nd)))
+    k = nk.value
+    return p[:, :k].copy(order="F"), q[:, :k].copy(order="F"), list(kept[:k]), list(dropped[:nd.value])
+
+
+def mgs_biorth(x, y, ip=None, drop_tol=1e-12):
+    """(P, Q, kept, dropped) -- biorth.cpp:102-109."""
+    return _biorth(x, y, ip, drop_tol, False)
+
+
+def cgs_biorth(x, y, ip=None, drop_tol=1e-12):
+    return _biorth(x, y, ip, drop_tol, True)
+
+
+def biorth_against(bases, x, y, ip=None):
+    x, y = _f(x), _f(y)
+    n, m = x.shape
+    ip = ip or InnerProduct()
+    ps = [_f(p) for p, _ in bases]
+    qs = [_f(q) for _, q in bases]
+    widths = np.array([p.shape[1] for p in ps] or [0], dtype=np.int64)
+    parr = (C.c_void_p * max(1, len(ps)))(*[p.ctypes.data for p in ps])
+    qarr = (C.c_void_p * max(1, len(qs)))(*[q.ctypes.data for q in qs])
+    xo = np.zeros((n, m), order="F")
+    yo = np.zeros((n, m), order="F")
+    check(lib().bosp_biorth_against(ip._h(), C.c_int64(n), C.c_int64(len(ps)), _p(widths), parr,
+                                    qarr, C.c_int64(m), _p(x), _p(y), _p(xo), _p(yo)))
+    return xo, yo
+
+
+def biorth_residual(p, q, ip=None):
+    p, q = _f(p), _f(q)
+    ip = ip or InnerProduct()
+    out = C.c_double()
+    check(lib().bosp_biorth_residual(ip._h(), C.c_int64(p.shape[0]), C.c_int64(p.shape[1]),
+                                     _p(p), _p(q), C.byref(out)))
+    return out.value
+
+
+def cg_solve(op, rhs, x0=None, tol=1e-2, max_iter=20):
+    rhs = _f(rhs)
+    x0 = None if x0 is None else _f(x0)
+    x = np.zeros_like(rhs, order="F")
+    br, mi = C.c_int32(), C.c_int64()
+    check(lib().bosp_cg_solve(op._h, C.c_int64(rhs.shape[1]), _p(rhs), _p(x0), C.c_double(tol),
+                              C.c_int64(max_iter), _p(x), C.byref(br), C.byref(mi)))
+    return x, bool(br.value), mi.value
+
+
+def solve_small_lrep(khat, mhat, k):
+    khat, mhat = _f(khat), _f(mhat)
+    d = khat.shape[0]
+    lam = np.zeros(k)
+    xh = np.zeros((d, k), order="F")
+    yh = np.zeros((d, k), order="F")
+    check(lib().bosp_solve_small_lrep(C.c_int64(d), _p(khat), _p(mhat), C.c_int64(k), _p(lam),
+                                      _p(xh), _p(yh)))
+    return lam, xh, yh
+
+
+def jacobi_svd(a):
+    a = _f(a)
+    m, k = a.shape
+    u = np.zeros((m, k), order="F")
+    v = np.zeros((k, k), order="F")
+    s = np.zeros(k)
+    sw, cv = C.c_int64(), C.c_int32()
+    check(lib().bosp_jacobi_svd(C.c_int64(m), C.c_int64(k), _p(a), _p(u), _p(s), _p(v),
+                                C.byref(sw), C.byref(cv)))
+    return u, s, v, sw.value, bool(cv.value)
+
+
+def cholesky_lower(a):
+    a = _f(a)
+    n = a.shape[0]
+    l = np.zeros((n, n), order="F")
+    ok = C.c_int32()
+    check(lib().bosp_cholesky(C.c_int64(n), _p(a), _p(l), C.byref(ok)))
+    return l if ok.value else None
+
+
+# ---- measurement hooks ----------------------------------------------------------------------
+def device_info():
+    buf = C.create_string_buffer(256)
+    sms = lib().bosp_device_info(buf, 256)
+    if sms < 0:
+        check(-sms)
+    return buf.value.decode(), sms
+
+
+def profile_enable(family: str | None):
+    lib().bosp_profile_enable((family or "").encode())
+
+
+def profile_collect():
+    n, ms, b, f = C.c_int64(), C.c_double(), C.c_double(), C.c_double()
+    lib().bosp_profile_collect(C.byref(n), C.byref(ms), C.byref(b), C.byref(f))
+    return dict(launches=n.value, ms=ms.value, bytes=b.value, flops=f.value)
+
+
+def launch_count():
+    return int(lib().bosp_launch_count())
+
+
+def launch_reset():
+    lib().bosp_launch_reset()
+
+
+def launch_families():
+    buf = C.create_string_buffer(4096)
+    lib().bosp_launch_families(buf, 4096)
+    out = {}
+    for item in buf.value.decode().split(";"):
+        if "=" in item:
+            k, v = item.split("=")
+            out[k] = int(v)
+    return out
+
+
+def device_sync():
+    lib().bosp_device_sync()
+
+
+def operators_for(problem):
+    """problems.Problem -> (K, M) device operators (dense / CSR / matrix-free stencil)."""
+    from . import problems as P
+
+    def one(op):
+        if isinstance(op, np.ndarray):
+            return LinearOperator.from_dense(op)
+        if isinstance(op, P.Stencil):
+            return LinearOperator.from_stencil(op)
+        return LinearOperator.from_csr(op)
+    return one(problem.K), one(problem.M)

@@ -1,0 +1,88 @@
+// Tall-skinny fp64 contractions on the sm_100a DMMA tensor pipe (mma.sync m8n8k4 f64 ->
+// SASS DMMA.8x8x4; tcgen05 has no f64 kind) plus the column-wise reductions and element-wise
+// kernels of the BOSP outer iteration.
+#pragma once
+
+#include "common.hpp"
+
+namespace bosp {
+inline namespace b200 {
+
+// ---- Gram: G(a x b) = A^T B over n rows (reference block_inner, kernels.cpp:47-68) ----------
+// Up to 4 independent Grams in one launch.  G is column-major with leading dim ldg (device).
+struct GramJob {
+    ColList a, b;
+    double* g;
+    int64_t ldg;
+};
+void gram(const GramJob* jobs, int njobs, int64_t n);
+inline void gram(const ColList& a, const ColList& b, int64_t n, double* g, int64_t ldg) {
+    GramJob j{a, b, g, ldg};
+    gram(&j, 1, n);
+}
+
+// ---- Product: Out(n x b) = alpha * A(n x k) * C(k x b) + beta * Out -------------------------
+// reference block_product / block_axpy (kernels.cpp:70-104); also the dense operator K*X
+// (linear_operator.cpp:12-31) with A = K.  C is a device matrix (ldc).  Up to 4 jobs/launch.
+struct ProductJob {
+    ColList a;          // k columns of n rows
+    const double* c;    // k x b
+    int64_t ldc;
+    int32_t ncols;      // b
+    double* out;
+    int64_t ldo;
+    double alpha, beta;
+};
+void product(const ProductJob* jobs, int njobs, int64_t n);
+inline void product(const ColList& a, const double* c, int64_t ldc, int32_t b, const DMat& out,
+                    double alpha, double beta) {
+    ProductJob j{a, c, ldc, b, out.p, out.ld, alpha, beta};
+    product(&j, 1, out.rows);
+}
+
+// ---- Column reductions (deterministic two-level, no atomics on values) ------------------------
+// out[j] = sum_i x[i,j] * y[i,j]
+void col_dots(const DMat& x, const DMat& y, double* out_dev);
+// Normalised residuals of the Ritz window (bosp_solver.cpp:256-272, 487-497):
+// num_j = ||kx_j - lam_j yb_j||^2 + ||my_j - lam_j xb_j||^2,  den_j = ||x_j||^2 + ||y_j||^2
+void residual_sums(const DMat& kx, const DMat& my, const DMat& xb, const DMat& yb,
+                   const DMat& x, const DMat& y, const double* lam_dev, double* num_dev,
+                   double* den_dev);
+
+// ---- Element-wise ---------------------------------------------------------------------------
+// out[:,j] = lam_j * a[:,j] - b[:,j]   (Step-6 right-hand sides, bosp_solver.cpp:337-350)
+void lam_axmy(const DMat& a, const DMat& b, const double* lam_dev, const DMat& out);
+// y[:,j] += lam_j * x[:,j]             (Gauss-Seidel coupling, bosp_solver.cpp:354-371)
+void lam_axpy(const DMat& x, const double* lam_dev, const DMat& y);
+// y = x + sigma * y  (shifted operator epilogue) / y = alpha * x / y = d .* x
+void axpby(double a, const DMat& x, double b, const DMat& y);
+void diag_scale(const double* d_dev, const DMat& x, const DMat& y);
+
+// ---- Batched multi-RHS CG kernels (reference cg_solve, cg.cpp:11-58) -------------------------
+// Per-column scalars live on the device in CgScalars; every kernel honours the column masks, so
+// the iterates equal those of the reference's per-column loop.
+struct CgScalars {
+    double* rr;       // current r^T r
+    double* bnorm;    // ||b||
+    double* pap;      // p^T A p (this iteration)
+    double* beta;     // rr_new / rr (this iteration)
+    int* active;      // column still iterating
+    int* broken;      // p^T A p <= 0 hit
+    int* iters;       // iterations taken
+    int* any_active;  // scalar: number of active columns (device)
+};
+// x = 0, r = b, p = b, rr = ||b||^2, bnorm = ||b||, active = (bnorm != 0 && sqrt(rr) > tol*bnorm)
+void cg_start(const DMat& b, const DMat& x, const DMat& r, const DMat& p, const CgScalars& s,
+              double tol, int max_iter);
+// General start with x0: x = x0, r = b - ax0, p = r, rr = ||r||^2, bnorm = ||b|| (cg.cpp:22-31)
+void cg_start_x0(const DMat& b, const DMat& x0, const DMat& ax0, const DMat& x, const DMat& r,
+                 const DMat& p, const CgScalars& s, double tol, int max_iter);
+// pap_j = p_j^T ap_j (active columns)
+void cg_pap(const DMat& p, const DMat& ap, const CgScalars& s);
+// active & pap>0: x += a p, r -= a ap, rr_new; pap<=0 -> broken, inactive.  Then
+// p = r + beta p, rr = rr_new, active = sqrt(rr) > tol*bnorm && iters < max_iter.
+void cg_update(const DMat& x, const DMat& r, const DMat& p, const DMat& ap, const CgScalars& s,
+               double tol, int max_iter);
+
+}  // namespace b200
+}  // namespace bosp

@@ -1,0 +1,242 @@
+// Device orchestration of the biorthogonalization and inner-CG building blocks.
+#include "dev_algos.hpp"
+
+#include <algorithm>
+#include <cmath>
+
+#include "operators.hpp"
+
+namespace bosp {
+inline namespace b200 {
+
+// ---------------------------------------------------------------------------------------------
+// Grams under the inner product
+// ---------------------------------------------------------------------------------------------
+void apply_weight(const InnerProduct& ip, const DMat& b, const DMat& out) {
+    if (ip.weighted()) ip.weight()->apply_device(b, out);
+    else copy_block(b, out);
+}
+
+void ip_gram_dev(const InnerProduct& ip, const DMat& a, const DMat& b, const DMat& g) {
+    if (!ip.weighted()) {
+        gram(ColList(a), ColList(b), a.rows, g.p, g.ld);
+        return;
+    }
+    DBlock wb(b.rows, b.cols);
+    ip.weight()->apply_device(b, wb.view());
+    gram(ColList(a), ColList(wb.view()), a.rows, g.p, g.ld);
+}
+
+DenseMatrix ip_gram_host(const InnerProduct& ip, const DMat& a, const DMat& b) {
+    DenseMatrix h(a.cols, b.cols);
+    if (a.cols == 0 || b.cols == 0) return h;
+    DBlock g(a.cols, b.cols);
+    ip_gram_dev(ip, a, b, g.view());
+    to_host(g.view(), h.data(), h.rows());
+    return h;
+}
+
+// ---------------------------------------------------------------------------------------------
+// biorth_against: per basis two Grams (one launch) and two in-place axpy products (one launch)
+// ---------------------------------------------------------------------------------------------
+void dev_biorth_against(const std::vector<DevBasis>& bases, const DMat& w, const DMat& z,
+                        const InnerProduct& ip) {
+    if (w.cols == 0) return;
+    for (const DevBasis& b : bases) {
+        if (b.p.cols == 0) continue;
+        require(b.p.rows == w.rows, "biorth_against: basis dimension mismatch");
+        const int64_t k = b.p.cols, m = w.cols;
+        DBlock c(k, 2 * m);  // [Cw | Cz]
+        const DMat cw = c.cols(0, m), cz = c.cols(m, m);
+        if (!ip.weighted()) {
+            GramJob jobs[2] = {{ColList(b.q), ColList(w), cw.p, cw.ld},
+                               {ColList(b.p), ColList(z), cz.p, cz.ld}};
+            gram(jobs, 2, w.rows);
+        } else {
+            ip_gram_dev(ip, b.q, w, cw);
+            ip_gram_dev(ip, b.p, z, cz);
+        }
+        ProductJob pj[2] = {{ColList(b.p), cw.p, cw.ld, static_cast<int32_t>(m), w.p, w.ld, -1.0, 1.0},
+                            {ColList(b.q), cz.p, cz.ld, static_cast<int32_t>(m), z.p, z.ld, -1.0, 1.0}};
+        product(pj, 2, w.rows);
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// MGS-Biorth: Grams of the pair -> exact column recurrence on the host in coefficient space
+// -> P = X A, Q = Y B on the DMMA pipe -> conditional second pass from the Gram of (P, Q).
+// ---------------------------------------------------------------------------------------------
+namespace {
+
+void apply_coefs(const DMat& x, const DMat& y, const DenseMatrix& a, const DenseMatrix& b,
+                 const DMat& p, const DMat& q) {
+    const int64_t m = a.rows(), k = a.cols();
+    DBlock c(m, 2 * k);
+    to_device(a.data(), m, k, m, c.cols(0, k));
+    to_device(b.data(), m, k, m, c.cols(k, k));
+    ProductJob pj[2] = {{ColList(x), c.data(), c.ld(), static_cast<int32_t>(k), p.p, p.ld, 1.0, 0.0},
+                        {ColList(y), c.data() + k * c.ld(), c.ld(), static_cast<int32_t>(k), q.p, q.ld, 1.0, 0.0}};
+    product(pj, 2, x.rows);
+}
+
+// Gxx, Gxy, Gyy of the pair under ip.
+void pair_grams(const DMat& x, const DMat& y, const InnerProduct& ip, DenseMatrix& gxx,
+                DenseMatrix& gxy, DenseMatrix& gyy) {
+    const int64_t m = x.cols;
+    DBlock g(m, 3 * m);
+    if (!ip.weighted()) {
+        GramJob jobs[3] = {{ColList(x), ColList(x), g.data(), g.ld()},
+                           {ColList(x), ColList(y), g.data() + m * g.ld(), g.ld()},
+                           {ColList(y), ColList(y), g.data() + 2 * m * g.ld(), g.ld()}};
+        gram(jobs, 3, x.rows);
+    } else {
+        DBlock wx(x.rows, m), wy(y.rows, m);
+        ip.weight()->apply_device(x, wx.view());
+        ip.weight()->apply_device(y, wy.view());
+        GramJob jobs[3] = {{ColList(x), ColList(wx.view()), g.data(), g.ld()},
+                           {ColList(x), ColList(wy.view()), g.data() + m * g.ld(), g.ld()},
+                           {ColList(y), ColList(wy.view()), g.data() + 2 * m * g.ld(), g.ld()}};
+        gram(jobs, 3, x.rows);
+    }
+    DenseMatrix all(m, 3 * m);
+    to_host(g.view().cols_range(0, 3 * m), all.data(), m);
+    gxx = DenseMatrix(m, m);
+    gxy = DenseMatrix(m, m);
+    gyy = DenseMatrix(m, m);
+    std::copy(all.data(), all.data() + m * m, gxx.data());
+    std::copy(all.data() + m * m, all.data() + 2 * m * m, gxy.data());
+    std::copy(all.data() + 2 * m * m, all.data() + 3 * m * m, gyy.data());
+}
+
+}  // namespace
+
+DevBiorthOutcome dev_mgs_biorth(const DMat& x, const DMat& y, const DMat& p, const DMat& q,
+                                const InnerProduct& ip, double drop_tol, bool classical) {
+    require(x.rows == y.rows && x.cols == y.cols, "biorth: X and Y must have equal shape");
+    DevBiorthOutcome out;
+    const int64_t m = x.cols;
+    if (m == 0) return out;
+    DenseMatrix gxx, gxy, gyy;
+    pair_grams(x, y, ip, gxx, gxy, gyy);
+    CoefBiorth cb = coef_mgs(gxx, gxy, gyy, drop_tol, classical);
+    out.kept = static_cast<int64_t>(cb.kept.size());
+    out.kept_columns = cb.kept;
+    out.dropped_columns = cb.dropped;
+    if (out.kept == 0) return out;
+    const DMat pk = p.cols_range(0, out.kept), qk = q.cols_range(0, out.kept);
+    apply_coefs(x, y, cb.a, cb.b, pk, qk);
+    if (classical || out.kept <= 1) return out;
+    const DenseMatrix gpq = ip_gram_host(ip, pk, qk);
+    if (!biorth_loss_exceeds(gpq, 1e-10)) return out;
+    // second subtraction pass (biorth.cpp:104-107)
+    out.second_pass = true;
+    CoefBiorth cb2 = coef_rebiorth(gpq);
+    DBlock tp(x.rows, out.kept), tq(x.rows, out.kept);
+    apply_coefs(pk, qk, cb2.a, cb2.b, tp.view(), tq.view());
+    copy_block(tp.view(), pk);
+    copy_block(tq.view(), qk);
+    return out;
+}
+
+double dev_biorth_residual(const DMat& p, const DMat& q, const InnerProduct& ip) {
+    require(p.rows == q.rows && p.cols == q.cols, "biorth_residual: shape mismatch");
+    if (p.cols == 0) return 0.0;
+    return biorth_loss(ip_gram_host(ip, p, q));
+}
+
+// ---------------------------------------------------------------------------------------------
+// Batched multi-RHS CG
+// ---------------------------------------------------------------------------------------------
+void CgWorkspace::ensure(int64_t n, int64_t m) {
+    if (r.rows() != n || r.capacity() < m) {
+        r = DBlock(n, m);
+        p = DBlock(n, m);
+        ap = DBlock(n, m);
+    }
+    r.set_cols(m);
+    p.set_cols(m);
+    ap.set_cols(m);
+    if (m > m_cap_) {
+        Runtime& rt = Runtime::get();
+        if (scal_) rt.free(scal_);
+        m_cap_ = m;
+        const size_t bytes = sizeof(double) * 4 * m + sizeof(int) * (3 * m + 4);
+        scal_ = rt.alloc(bytes);
+        double* d = static_cast<double*>(scal_);
+        s.rr = d;
+        s.bnorm = d + m;
+        s.pap = d + 2 * m;
+        s.beta = d + 3 * m;
+        int* iv = reinterpret_cast<int*>(d + 4 * m);
+        s.active = iv;
+        s.broken = iv + m;
+        s.iters = iv + 2 * m;
+        s.any_active = iv + 3 * m;
+    }
+    if (!host_active) {
+        BOSP_CUDA(cudaMallocHost(&host_active, 4 * sizeof(int)));
+        BOSP_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+        BOSP_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+    }
+}
+
+CgWorkspace::~CgWorkspace() {
+    // owned device memory is returned with the pool at teardown; pinned/event handles leak
+    // intentionally when the workspace outlives the CUDA context at process exit.
+}
+
+DevCgOutcome dev_cg(const LinearOperator& a, const DMat& rhs, const DMat& x, double tol,
+                    int64_t max_iter, CgWorkspace& ws, const DMat* x0, bool want_stats) {
+    require(rhs.rows == a.dim() && x.rows == a.dim() && rhs.cols == x.cols, "cg_solve: shape mismatch");
+    DevCgOutcome out;
+    const int64_t m = rhs.cols;
+    if (m == 0) return out;
+    Runtime& rt = Runtime::get();
+    ws.ensure(rhs.rows, m);
+    const DMat r = ws.r.view(), p = ws.p.view(), ap = ws.ap.view();
+    const int mi = static_cast<int>(std::min<int64_t>(max_iter, 1 << 30));
+    if (x0) {
+        a.apply_device(*x0, ap);
+        cg_start_x0(rhs, *x0, ap, x, r, p, ws.s, tol, mi);
+    } else {
+        cg_start(rhs, x, r, p, ws.s, tol, mi);
+    }
+    // State s (s = 0 after start, s = it+1 after iteration it) publishes its active-column count
+    // to pinned slot s % 2.  Before issuing iteration it the host looks at state it-1, which the
+    // device has finished while it works on iteration it-1: no stall, and at most one fully
+    // masked iteration is ever issued.
+    auto publish = [&](int64_t state) {
+        const int slot = static_cast<int>(state & 1);
+        BOSP_CUDA(cudaMemcpyAsync(&ws.host_active[slot], ws.s.any_active, sizeof(int),
+                                  cudaMemcpyDeviceToHost, rt.stream()));
+        BOSP_CUDA(cudaEventRecord(ws.ev[slot], rt.stream()));
+    };
+    publish(0);
+    int64_t it = 0;
+    for (; it < max_iter; ++it) {
+        if (it >= 1) {
+            const int slot = static_cast<int>((it - 1) & 1);
+            BOSP_CUDA(cudaEventSynchronize(ws.ev[slot]));
+            if (ws.host_active[slot] == 0) break;
+        }
+        a.apply_device(p, ap);
+        cg_pap(p, ap, ws.s);
+        cg_update(x, r, p, ap, ws.s, tol, mi);
+        publish(it + 1);
+    }
+    out.sweeps = it;
+    if (want_stats) {
+        std::vector<int> broken(static_cast<size_t>(m)), iters(static_cast<size_t>(m));
+        BOSP_CUDA(cudaMemcpyAsync(broken.data(), ws.s.broken, sizeof(int) * m, cudaMemcpyDeviceToHost, rt.stream()));
+        BOSP_CUDA(cudaMemcpyAsync(iters.data(), ws.s.iters, sizeof(int) * m, cudaMemcpyDeviceToHost, rt.stream()));
+        rt.sync();
+        for (int64_t j = 0; j < m; ++j) {
+            out.breakdown |= broken[j] != 0;
+            out.max_iterations_used = std::max<int64_t>(out.max_iterations_used, iters[j]);
+        }
+    }
+    return out;
+}
+
+}  // namespace b200
+}  // namespace bosp

@@ -1,0 +1,67 @@
+// Device-resident building blocks of the BOSP iteration: inner-product Grams, blocked
+// biorthogonal projection, MGS-Biorth (coefficient-space recurrence + DMMA products) and the
+// batched multi-RHS CG.
+#pragma once
+
+#include <vector>
+
+#include "api.hpp"
+#include "dense_ops.hpp"
+#include "runtime.hpp"
+
+namespace bosp {
+inline namespace b200 {
+
+// G = A^T (W B) for the inner product's weight W (identity when unweighted); a x b.
+DenseMatrix ip_gram_host(const InnerProduct& ip, const DMat& a, const DMat& b);
+void ip_gram_dev(const InnerProduct& ip, const DMat& a, const DMat& b, const DMat& g);
+// W B into `out` (copy when unweighted).
+void apply_weight(const InnerProduct& ip, const DMat& b, const DMat& out);
+
+struct DevBasis {
+    DMat p, q;
+};
+
+// (I - sum P_k Q_k^T) W and (I - sum Q_k P_k^T) Z in place, bases in order (biorth.cpp:116-133).
+void dev_biorth_against(const std::vector<DevBasis>& bases, const DMat& w, const DMat& z,
+                        const InnerProduct& ip);
+
+struct DevBiorthOutcome {
+    int64_t kept = 0;
+    std::vector<int64_t> kept_columns, dropped_columns;
+    bool second_pass = false;
+};
+// MGS-Biorth of (X, Y) into (P, Q) (first `kept` columns written; P/Q need >= m columns and
+// must not alias X/Y).  Semantics of mgs_biorth (biorth.cpp:102-109); classical -> cgs_biorth.
+DevBiorthOutcome dev_mgs_biorth(const DMat& x, const DMat& y, const DMat& p, const DMat& q,
+                                const InnerProduct& ip, double drop_tol = 1e-12,
+                                bool classical = false);
+// ||P^T Q - I||_2 (biorth.cpp:135-143).
+double dev_biorth_residual(const DMat& p, const DMat& q, const InnerProduct& ip);
+
+// Batched CG workspace (per operator size / width).
+class CgWorkspace {
+public:
+    void ensure(int64_t n, int64_t m);
+    DBlock r, p, ap;
+    CgScalars s{};
+    int* host_active = nullptr;  // pinned ring
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    ~CgWorkspace();
+
+private:
+    void* scal_ = nullptr;
+    int64_t m_cap_ = 0;
+};
+struct DevCgOutcome {
+    bool breakdown = false;
+    int64_t max_iterations_used = 0;
+    int64_t sweeps = 0;  // batched iterations executed
+};
+// x = CG(A, rhs) column by column with masks (cg.cpp:11-58); x0 = 0 when x0 == nullptr.
+DevCgOutcome dev_cg(const LinearOperator& a, const DMat& rhs, const DMat& x, double tol,
+                    int64_t max_iter, CgWorkspace& ws, const DMat* x0 = nullptr,
+                    bool want_stats = false);
+
+}  // namespace b200
+}  // namespace bosp

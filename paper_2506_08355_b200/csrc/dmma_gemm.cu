@@ -1,0 +1,463 @@
+// fp64 tall-skinny GEMMs on the DMMA pipe for sm_100a.
+//
+//  * gram()    G = A^T B   (A: n x a, B: n x b, a,b <= a few hundred, n up to millions)
+//              -> split-K over n: every CTA owns one (BM x BN) output tile and a contiguous
+//                 row range; partial tiles go to scratch and a deterministic two-level
+//                 reduction (fixed split order) produces G.  Reference: block_inner
+//                 (kernels.cpp:47-68), assemble_projected_applied (projected_lrep.cpp:40-46).
+//  * product() Out = alpha A C + beta Out  (A: n x k, C: k x b small or, for the dense
+//              operator, k = n) -> one CTA per (BM x BN) output tile, K loop over k.
+//              Reference: block_product / block_axpy (kernels.cpp:70-104) and the dense
+//              operator (linear_operator.cpp:12-31).
+//
+// Operands are staged global->shared with 16-byte cp.async (LDGSTS) in a 3-stage ring, fed to
+// mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4).  Shared layouts are padded (+4 doubles) so the
+// fragment loads of a half-warp hit 16 distinct 8-byte bank pairs.
+#include <algorithm>
+#include <cstdio>
+
+#include "dense_ops.hpp"
+#include "runtime.hpp"
+
+namespace bosp {
+inline namespace b200 {
+
+namespace {
+
+constexpr int kStages = 3;
+constexpr int kBK = 32;           // k-depth of one pipeline stage
+constexpr int kLdK = kBK + 4;     // padded k-contiguous smem stride
+
+__device__ __forceinline__ const double* colptr(const ColList& cl, int c) {
+    int s = 0;
+#pragma unroll
+    for (int i = 1; i < kMaxSeg; ++i)
+        if (i < cl.nseg && c >= cl.start[i]) s = i;
+    return cl.p[s] + static_cast<int64_t>(c - cl.start[s]) * cl.ld[s];
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+    const unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(saddr), "l"(gmem),
+                 "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+// Load a "k-contiguous" tile: R columns (from ColList starting at col0, total ncols), rows
+// [k0, k0+kBK) clipped to kmax, into smem[c * kLdK + k].  Missing data is zero-filled.
+template <int R, int NT>
+__device__ __forceinline__ void load_kcontig(double* smem, const ColList& cl, int col0, int ncols,
+                                             int64_t k0, int64_t kmax) {
+    constexpr int kChunks = R * (kBK / 2);
+    for (int ch = threadIdx.x; ch < kChunks; ch += NT) {
+        const int c = ch / (kBK / 2);
+        const int kp = ch % (kBK / 2);
+        const int64_t k = k0 + 2 * kp;
+        const int gc = col0 + c;
+        int bytes = 0;
+        const double* src = cl.p[0];
+        if (gc < ncols && k < kmax) {
+            const int64_t rem = kmax - k;
+            bytes = rem >= 2 ? 16 : 8;
+            src = colptr(cl, gc) + k;
+        }
+        cp_async16(smem + c * kLdK + 2 * kp, src, bytes);
+    }
+}
+
+// Load an "m-contiguous" tile for the NN product: kBK columns (k0..k0+kBK of A, clipped to
+// kcols) x BM rows (m0.., clipped to mmax) into smem[k * (BM+4) + m].
+template <int BM, int NT>
+__device__ __forceinline__ void load_mcontig(double* smem, const ColList& cl, int k0, int kcols,
+                                             int64_t m0, int64_t mmax) {
+    constexpr int kChunks = kBK * (BM / 2);
+    for (int ch = threadIdx.x; ch < kChunks; ch += NT) {
+        const int kk = ch / (BM / 2);
+        const int mp = ch % (BM / 2);
+        const int gk = k0 + kk;
+        const int64_t m = m0 + 2 * mp;
+        int bytes = 0;
+        const double* src = cl.p[0];
+        if (gk < kcols && m < mmax) {
+            const int64_t rem = mmax - m;
+            bytes = rem >= 2 ? 16 : 8;
+            src = colptr(cl, gk) + m;
+        }
+        cp_async16(smem + kk * (BM + 4) + 2 * mp, src, bytes);
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// Gram kernel
+// ------------------------------------------------------------------------------------------
+struct GramParams {
+    GramJob job[4];
+    int64_t n;
+    int tiles_n[4];      // column tiles per job
+    int tiles[4];        // tiles per job
+    int splits;
+    int64_t chunk;       // rows per split (multiple of kBK)
+    double* partial;     // [job][split][tile][BM*BN]
+    int64_t job_stride;  // doubles per job in partial
+};
+
+template <int BM, int BN, int WM, int WN>
+__global__ void __launch_bounds__(WM * WN * 32)
+k_gram(GramParams prm) {
+    constexpr int NT = WM * WN * 32;
+    constexpr int WTM = BM / WM, WTN = BN / WN;
+    constexpr int MT = WTM / 8, NTL = WTN / 8;
+    extern __shared__ __align__(16) double smem[];
+    double* sa = smem;                           // [kStages][BM][kLdK]
+    double* sb = smem + kStages * BM * kLdK;     // [kStages][BN][kLdK]
+
+    const int jb = blockIdx.z;
+    const GramJob& job = prm.job[jb];
+    const int tile = blockIdx.x;
+    if (tile >= prm.tiles[jb]) return;
+    const int tm = tile / prm.tiles_n[jb], tn = tile % prm.tiles_n[jb];
+    const int m0 = tm * BM, n0 = tn * BN;
+    const int acols = job.a.cols(), bcols = job.b.cols();
+    const int64_t kb = static_cast<int64_t>(blockIdx.y) * prm.chunk;
+    const int64_t ke = min(prm.n, kb + prm.chunk);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int gid = lane >> 2, tig = lane & 3;
+    const int wm0 = (warp / WN) * WTM, wn0 = (warp % WN) * WTN;
+
+    double acc[MT][NTL][2];
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NTL; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    const int nk = ke > kb ? static_cast<int>((ke - kb + kBK - 1) / kBK) : 0;
+#pragma unroll
+    for (int s = 0; s < kStages - 1; ++s) {
+        if (s < nk) {
+            load_kcontig<BM, NT>(sa + s * BM * kLdK, job.a, m0, acols, kb + s * kBK, ke);
+            load_kcontig<BN, NT>(sb + s * BN * kLdK, job.b, n0, bcols, kb + s * kBK, ke);
+        }
+        cp_async_commit();
+    }
+    for (int it = 0; it < nk; ++it) {
+        cp_async_wait<kStages - 2>();
+        __syncthreads();
+        const int st = it % kStages;
+        const double* a = sa + st * BM * kLdK;
+        const double* b = sb + st * BN * kLdK;
+#pragma unroll
+        for (int kk = 0; kk < kBK; kk += 4) {
+            double af[MT], bf[NTL];
+#pragma unroll
+            for (int i = 0; i < MT; ++i) af[i] = a[(wm0 + i * 8 + gid) * kLdK + kk + tig];
+#pragma unroll
+            for (int j = 0; j < NTL; ++j) bf[j] = b[(wn0 + j * 8 + gid) * kLdK + kk + tig];
+#pragma unroll
+            for (int i = 0; i < MT; ++i)
+#pragma unroll
+                for (int j = 0; j < NTL; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        }
+        const int nxt = it + kStages - 1;
+        if (nxt < nk) {
+            const int sn = nxt % kStages;
+            load_kcontig<BM, NT>(sa + sn * BM * kLdK, job.a, m0, acols, kb + nxt * kBK, ke);
+            load_kcontig<BN, NT>(sb + sn * BN * kLdK, job.b, n0, bcols, kb + nxt * kBK, ke);
+        }
+        cp_async_commit();
+    }
+    cp_async_wait<0>();
+
+    // partial tile -> scratch (element (m, n) of the tile at m + n*BM)
+    double* part = prm.partial + jb * prm.job_stride +
+                   (static_cast<int64_t>(blockIdx.y) * prm.tiles[jb] + tile) * (BM * BN);
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NTL; ++j) {
+            const int m = wm0 + i * 8 + gid;
+            const int nn = wn0 + j * 8 + 2 * tig;
+            part[m + nn * BM] = acc[i][j][0];
+            part[m + (nn + 1) * BM] = acc[i][j][1];
+        }
+}
+
+// Sum split partials in fixed order: out tile element e of job jb.
+// grid.x over (tile, element block), grid.z = job.
+template <int BM, int BN>
+__global__ void k_gram_reduce(GramParams prm) {
+    const int jb = blockIdx.z;
+    const GramJob& job = prm.job[jb];
+    const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t total = static_cast<int64_t>(prm.tiles[jb]) * BM * BN;
+    if (e >= total) return;
+    const int tile = static_cast<int>(e / (BM * BN));
+    const int r = static_cast<int>(e % (BM * BN));
+    const int m = (tile / prm.tiles_n[jb]) * BM + r % BM;
+    const int nn = (tile % prm.tiles_n[jb]) * BN + r / BM;
+    if (m >= job.a.cols() || nn >= job.b.cols()) return;
+    const double* part = prm.partial + jb * prm.job_stride + e;
+    const int64_t stride = total;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int sp = 0;
+    for (; sp + 4 <= prm.splits; sp += 4) {
+        s0 += part[(sp + 0) * stride];
+        s1 += part[(sp + 1) * stride];
+        s2 += part[(sp + 2) * stride];
+        s3 += part[(sp + 3) * stride];
+    }
+    for (; sp < prm.splits; ++sp) s0 += part[sp * stride];
+    job.g[m + nn * job.ldg] = (s0 + s1) + (s2 + s3);
+}
+
+template <int BM, int BN, int WM, int WN>
+void launch_gram(const GramJob* jobs, int njobs, int64_t n) {
+    Runtime& rt = Runtime::get();
+    GramParams prm{};
+    int max_tiles = 0;
+    for (int j = 0; j < njobs; ++j) {
+        prm.job[j] = jobs[j];
+        prm.tiles_n[j] = (jobs[j].b.cols() + BN - 1) / BN;
+        prm.tiles[j] = ((jobs[j].a.cols() + BM - 1) / BM) * prm.tiles_n[j];
+        max_tiles = std::max(max_tiles, prm.tiles[j]);
+    }
+    prm.n = n;
+    const int kblocks = static_cast<int>((n + kBK - 1) / kBK);
+    const int target = 3 * rt.sm_count();
+    int splits = std::max(1, (target + max_tiles * njobs - 1) / (max_tiles * njobs));
+    splits = std::min(splits, std::max(1, kblocks / 4));  // >= 4 stages of work per CTA
+    const int kb_per = (kblocks + splits - 1) / splits;
+    prm.chunk = static_cast<int64_t>(kb_per) * kBK;
+    splits = static_cast<int>((n + prm.chunk - 1) / prm.chunk);
+    prm.splits = std::max(1, splits);
+    prm.job_stride = static_cast<int64_t>(prm.splits) * max_tiles * BM * BN;
+    prm.partial = rt.scratch(static_cast<size_t>(prm.job_stride) * njobs);
+
+    constexpr int NT = WM * WN * 32;
+    constexpr size_t smem = sizeof(double) * kStages * (BM + BN) * kLdK;
+    static bool attr = false;
+    if (!attr) {
+        BOSP_CUDA(cudaFuncSetAttribute(k_gram<BM, BN, WM, WN>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    const double flops = 2.0 * n * (double)jobs[0].a.cols() * jobs[0].b.cols() * njobs;
+    const double bytes = 8.0 * n * (double)(jobs[0].a.cols() + jobs[0].b.cols()) * njobs;
+    {
+        LaunchScope ls("gram", bytes, flops);
+        dim3 grid(max_tiles, prm.splits, njobs);
+        k_gram<BM, BN, WM, WN><<<grid, NT, smem, rt.stream()>>>(prm);
+        BOSP_LAUNCH_CHECK();
+    }
+    {
+        LaunchScope ls("gram_reduce");
+        const int64_t total = static_cast<int64_t>(max_tiles) * BM * BN;
+        dim3 grid(static_cast<unsigned>((total + 255) / 256), 1, njobs);
+        k_gram_reduce<BM, BN><<<grid, 256, 0, rt.stream()>>>(prm);
+        BOSP_LAUNCH_CHECK();
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// Product kernel
+// ------------------------------------------------------------------------------------------
+struct ProductParams {
+    ProductJob job[4];
+    int64_t n;
+    int tiles_n[4];
+    int64_t tiles[4];
+};
+
+template <int BM, int BN, int WM, int WN>
+__global__ void __launch_bounds__(WM * WN * 32)
+k_product(ProductParams prm) {
+    constexpr int NT = WM * WN * 32;
+    constexpr int WTM = BM / WM, WTN = BN / WN;
+    constexpr int MT = WTM / 8, NTL = WTN / 8;
+    constexpr int LdM = BM + 4;
+    extern __shared__ __align__(16) double smem[];
+    double* sa = smem;                        // [kStages][kBK][LdM]
+    double* sb = smem + kStages * kBK * LdM;  // [kStages][BN][kLdK]
+
+    const int jb = blockIdx.z;
+    const ProductJob& job = prm.job[jb];
+    const int64_t tile = blockIdx.x + static_cast<int64_t>(blockIdx.y) * gridDim.x;
+    if (tile >= prm.tiles[jb]) return;
+    const int tn = static_cast<int>(tile % prm.tiles_n[jb]);
+    const int64_t tm = tile / prm.tiles_n[jb];
+    const int64_t m0 = tm * BM;
+    const int n0 = tn * BN;
+    const int kcols = job.a.cols();
+    ColList cl;  // C as a one-segment list (k-contiguous columns)
+    cl.p[0] = job.c;
+    cl.ld[0] = job.ldc;
+    cl.start[1] = job.ncols;
+    cl.nseg = 1;
+    for (int i = 2; i <= kMaxSeg; ++i) cl.start[i] = job.ncols;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int gid = lane >> 2, tig = lane & 3;
+    const int wm0 = (warp / WN) * WTM, wn0 = (warp % WN) * WTN;
+
+    double acc[MT][NTL][2];
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NTL; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    const int nk = (kcols + kBK - 1) / kBK;
+#pragma unroll
+    for (int s = 0; s < kStages - 1; ++s) {
+        if (s < nk) {
+            load_mcontig<BM, NT>(sa + s * kBK * LdM, job.a, s * kBK, kcols, m0, prm.n);
+            load_kcontig<BN, NT>(sb + s * BN * kLdK, cl, n0, job.ncols, s * kBK, kcols);
+        }
+        cp_async_commit();
+    }
+    for (int it = 0; it < nk; ++it) {
+        cp_async_wait<kStages - 2>();
+        __syncthreads();
+        const int st = it % kStages;
+        const double* a = sa + st * kBK * LdM;
+        const double* b = sb + st * BN * kLdK;
+#pragma unroll
+        for (int kk = 0; kk < kBK; kk += 4) {
+            double af[MT], bf[NTL];
+#pragma unroll
+            for (int i = 0; i < MT; ++i) af[i] = a[(kk + tig) * LdM + wm0 + i * 8 + gid];
+#pragma unroll
+            for (int j = 0; j < NTL; ++j) bf[j] = b[(wn0 + j * 8 + gid) * kLdK + kk + tig];
+#pragma unroll
+            for (int i = 0; i < MT; ++i)
+#pragma unroll
+                for (int j = 0; j < NTL; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        }
+        const int nxt = it + kStages - 1;
+        if (nxt < nk) {
+            const int sn = nxt % kStages;
+            load_mcontig<BM, NT>(sa + sn * kBK * LdM, job.a, nxt * kBK, kcols, m0, prm.n);
+            load_kcontig<BN, NT>(sb + sn * BN * kLdK, cl, n0, job.ncols, nxt * kBK, kcols);
+        }
+        cp_async_commit();
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+
+    // Epilogue through shared memory so that every column of Out is written as one contiguous
+    // BM-row run: so[n * LdM + m].
+    double* so = smem;
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NTL; ++j) {
+            const int m = wm0 + i * 8 + gid;
+            const int nn = wn0 + j * 8 + 2 * tig;
+            so[nn * LdM + m] = acc[i][j][0];
+            so[(nn + 1) * LdM + m] = acc[i][j][1];
+        }
+    __syncthreads();
+    const double alpha = job.alpha, beta = job.beta;
+    for (int e = threadIdx.x; e < BM * BN; e += NT) {
+        const int m = e % BM, nn = e / BM;
+        const int64_t gm = m0 + m;
+        const int gn = n0 + nn;
+        if (gm < prm.n && gn < job.ncols) {
+            double* o = job.out + gn * job.ldo + gm;
+            const double v = alpha * so[nn * LdM + m];
+            *o = (beta == 0.0) ? v : v + beta * *o;
+        }
+    }
+}
+
+template <int BM, int BN, int WM, int WN>
+void launch_product(const ProductJob* jobs, int njobs, int64_t n) {
+    Runtime& rt = Runtime::get();
+    ProductParams prm{};
+    int64_t max_tiles = 0;
+    double flops = 0, bytes = 0;
+    for (int j = 0; j < njobs; ++j) {
+        prm.job[j] = jobs[j];
+        prm.tiles_n[j] = (jobs[j].ncols + BN - 1) / BN;
+        prm.tiles[j] = ((n + BM - 1) / BM) * prm.tiles_n[j];
+        max_tiles = std::max(max_tiles, prm.tiles[j]);
+        const double k = jobs[j].a.cols(), b = jobs[j].ncols;
+        flops += 2.0 * n * k * b;
+        bytes += 8.0 * n * (k + b * (jobs[j].beta != 0.0 ? 2.0 : 1.0));
+    }
+    prm.n = n;
+    constexpr int NT = WM * WN * 32;
+    constexpr size_t smem_pipe = sizeof(double) * kStages * (kBK * (BM + 4) + BN * kLdK);
+    constexpr size_t smem_epi = sizeof(double) * BN * (BM + 4);
+    constexpr size_t smem = smem_pipe > smem_epi ? smem_pipe : smem_epi;
+    static bool attr = false;
+    if (!attr) {
+        BOSP_CUDA(cudaFuncSetAttribute(k_product<BM, BN, WM, WN>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    LaunchScope ls("product", bytes, flops);
+    const unsigned gx = static_cast<unsigned>(std::min<int64_t>(max_tiles, 65535));
+    const unsigned gy = static_cast<unsigned>((max_tiles + gx - 1) / gx);
+    dim3 grid(gx, gy, njobs);
+    k_product<BM, BN, WM, WN><<<grid, NT, smem, rt.stream()>>>(prm);
+    BOSP_LAUNCH_CHECK();
+}
+
+void check_aligned(const ColList& cl) {
+    for (int s = 0; s < cl.nseg; ++s)
+        if ((reinterpret_cast<uintptr_t>(cl.p[s]) & 15) || (cl.ld[s] & 1))
+            throw ContractViolation("dmma: operand columns must be 16-byte aligned with even ld");
+}
+
+}  // namespace
+
+void gram(const GramJob* jobs, int njobs, int64_t n) {
+    require(njobs >= 1 && njobs <= 4, "gram: 1..4 jobs per launch");
+    int amax = 0, bmax = 0;
+    for (int j = 0; j < njobs; ++j) {
+        check_aligned(jobs[j].a);
+        check_aligned(jobs[j].b);
+        amax = std::max(amax, jobs[j].a.cols());
+        bmax = std::max(bmax, jobs[j].b.cols());
+    }
+    if (amax == 0 || bmax == 0) return;
+    if (n == 0) {
+        for (int j = 0; j < njobs; ++j)
+            for (int c = 0; c < jobs[j].b.cols(); ++c)
+                BOSP_CUDA(cudaMemsetAsync(jobs[j].g + c * jobs[j].ldg, 0,
+                                          sizeof(double) * jobs[j].a.cols(), Runtime::get().stream()));
+        return;
+    }
+    if (amax <= 32 && bmax <= 32)
+        launch_gram<32, 32, 2, 2>(jobs, njobs, n);
+    else
+        launch_gram<64, 64, 2, 4>(jobs, njobs, n);
+}
+
+void product(const ProductJob* jobs, int njobs, int64_t n) {
+    require(njobs >= 1 && njobs <= 4, "product: 1..4 jobs per launch");
+    int bmax = 0;
+    for (int j = 0; j < njobs; ++j) {
+        check_aligned(jobs[j].a);
+        require((reinterpret_cast<uintptr_t>(jobs[j].c) & 15) == 0 && (jobs[j].ldc & 1) == 0,
+                "product: C must be 16-byte aligned with even ldc");
+        bmax = std::max(bmax, jobs[j].ncols);
+    }
+    if (n == 0 || bmax == 0) return;
+    // k == 0: Out = beta * Out (handled by the kernel with an empty K loop)
+    if (bmax <= 32)
+        launch_product<64, 32, 2, 2>(jobs, njobs, n);
+    else
+        launch_product<64, 64, 2, 4>(jobs, njobs, n);
+}
+
+}  // namespace b200
+}  // namespace bosp

@@ -1,0 +1,624 @@
+// BOSP Algorithm 2 driven from the host with every n-length block resident in HBM.
+//
+// Mirrors bosp_solver.cpp (initialize :117-177, ritz_step :188-207, iterate_once :211-435,
+// assemble_result :439-509, solve :513-536) step for step.  What changes is where the data
+// lives and how it moves:
+//   * U = [X | P | W] and V = [Y | Q | Z] are single column-major HBM buffers; the active block
+//     [X(frozen:), P, W] is a column range, never an hcat copy.
+//   * K U, M V, Grams, pullbacks, projections and MGS products are device kernels; only the
+//     d x d projected blocks, residual norms and small coefficient matrices cross to the host.
+//   * the small LREP and Step-5 algebra run on the host (north star).
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <limits>
+#include <numeric>
+
+#include "api.hpp"
+#include "dev_algos.hpp"
+#include "operators.hpp"
+
+namespace bosp {
+inline namespace b200 {
+
+struct DeviceState {
+    int64_t n = 0;
+    DBlock U, V;                  // [X | P | W], [Y | Q | Z]
+    int64_t wx = 0, wp = 0, ww = 0;
+    std::vector<double> lambdas, residuals;
+    int64_t frozen = 0, nev_conv = 0;
+    std::vector<DBlock> locked_p, locked_q;
+    std::vector<double> locked_lambdas;
+    std::vector<std::vector<double>> residual_history;
+    std::vector<double> last_residual;
+    std::vector<int64_t> nevconv_history;
+    int64_t iter = 0;
+    bool leak_recovered = false;
+    SolverStats stats;
+    // nullspace on device
+    DBlock x0, y0;
+    // workspaces
+    DBlock ku, mv, xt, yt, kxt, myt, xtb, ytb, pt, qt, rz, rw, zg, wg, tmp;
+    DBlock small;                 // device copies of small coefficient matrices
+    DBlock scal;                  // per-column scalars (lambdas, residual sums)
+    CgWorkspace cg;
+
+    int64_t width() const { return wx + wp + ww; }
+    DMat X() const { return U.cols(0, wx); }
+    DMat Y() const { return V.cols(0, wx); }
+    int64_t locked_count() const { return static_cast<int64_t>(locked_lambdas.size()); }
+};
+
+SolverState::SolverState() : d_(std::make_unique<DeviceState>()) {}
+SolverState::~SolverState() = default;
+SolverState::SolverState(SolverState&&) noexcept = default;
+SolverState& SolverState::operator=(SolverState&&) noexcept = default;
+int64_t SolverState::iter() const { return d_->iter; }
+int64_t SolverState::nev_conv() const { return d_->nev_conv; }
+
+int64_t BospConfig::effective_nb() const {
+    if (nb > 0) return std::min(nb, nev);
+    const int64_t by_rule = (nev + 4) / 5;
+    return std::max<int64_t>(1, std::min<int64_t>(by_rule, 150));
+}
+
+bool BospConfig::effective_moving() const {
+    if (moving.has_value()) return *moving;
+    return nev > 3 * effective_nb();
+}
+
+void BospConfig::validate() const {
+    if (nev <= 0) throw ContractViolation("BospConfig: nev must be positive");
+    if (effective_nb() > nev) throw ContractViolation("BospConfig: nb exceeds nev");
+    if (s < 2) throw ContractViolation("BospConfig: s must be >= 2");
+    if (!(tol > 0.0)) throw ContractViolation("BospConfig: tol must be positive");
+}
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+
+double secs(Clock::time_point a, Clock::time_point b) {
+    return std::chrono::duration<double>(b - a).count();
+}
+
+void ensure_block(DBlock& b, int64_t rows, int64_t cols) {
+    if (b.rows() != rows || b.capacity() < cols) b = DBlock(rows, std::max<int64_t>(cols, 1));
+    b.set_cols(cols);
+}
+
+std::vector<DevBasis> deflation_bases(const DeviceState& st) {
+    std::vector<DevBasis> bases;
+    if (st.x0.ncols() > 0) bases.push_back({st.x0.view(), st.y0.view()});
+    for (size_t i = 0; i < st.locked_p.size(); ++i) bases.push_back({st.locked_p[i].view(), st.locked_q[i].view()});
+    return bases;
+}
+
+// Scalars (per-column lambdas) to the device.
+const double* upload_scalars(DeviceState& st, const std::vector<double>& v, int64_t offset) {
+    ensure_block(st.scal, 1024, 4);
+    double* d = st.scal.data() + offset;
+    if (!v.empty())
+        BOSP_CUDA(cudaMemcpyAsync(d, v.data(), sizeof(double) * v.size(), cudaMemcpyHostToDevice, Runtime::get().stream()));
+    return d;
+}
+
+// Full MGS repair of (U, V) (bosp_solver.cpp:79-95).
+void rebiorthogonalize_state(DeviceState& st, const InnerProduct& ip) {
+    ++st.stats.repairs;
+    const int64_t d = st.width();
+    const DMat u = st.U.cols(0, d), v = st.V.cols(0, d);
+    dev_biorth_against(deflation_bases(st), u, v, ip);
+    DBlock nu(st.n, st.U.capacity()), nv(st.n, st.V.capacity());
+    DevBiorthOutcome out = dev_mgs_biorth(u, v, nu.cols(0, d), nv.cols(0, d), ip);
+    if (!out.dropped_columns.empty())
+        throw NumericalAbort("bosp: rebiorthogonalization dropped columns");
+    nu.set_cols(st.U.ncols());
+    nv.set_cols(st.V.ncols());
+    std::swap(st.U, nu);
+    std::swap(st.V, nv);
+}
+
+// Returns the max |U^T V - I| deviation and records cross-Gram statistics (:63-76).
+double sample_invariants(DeviceState& st, const InnerProduct& ip) {
+    const int64_t d = st.width();
+    const DMat u = st.U.cols(0, d), v = st.V.cols(0, d);
+    DenseMatrix g = ip_gram_host(ip, u, v);
+    for (int64_t i = 0; i < g.rows(); ++i) g(i, i) -= 1.0;
+    const double dev = g.max_abs();
+    st.stats.max_biorth_deviation = std::max(st.stats.max_biorth_deviation, dev);
+    double cg = 0.0;
+    for (const DevBasis& b : deflation_bases(st)) {
+        cg = std::max(cg, ip_gram_host(ip, b.q, u).max_abs());
+        cg = std::max(cg, ip_gram_host(ip, b.p, v).max_abs());
+    }
+    st.stats.max_deflation_crossgram = std::max(st.stats.max_deflation_crossgram, cg);
+    return dev;
+}
+
+struct RitzOut {
+    SmallEigenSolution sol;
+    int64_t d = 0;
+};
+
+// Step 3 (:188-207): K U, M V, projected blocks, host small solve, pullbacks.
+RitzOut ritz_step(DeviceState& st, const LinearOperator& k, const LinearOperator& m, int64_t wxa) {
+    RitzOut ro;
+    const int64_t d = wxa + st.wp + st.ww;
+    ro.d = d;
+    const DMat u = st.U.cols(st.frozen, d), v = st.V.cols(st.frozen, d);
+    ensure_block(st.ku, st.n, d);
+    ensure_block(st.mv, st.n, d);
+    k.apply_device(u, st.ku.view());
+    m.apply_device(v, st.mv.view());
+    st.stats.matvec_count += 2 * d;
+    st.stats.step3_matvecs += 2 * d;
+    st.stats.step3_vecprods += d * d + d;
+
+    DBlock g(d, 2 * d);
+    GramJob jobs[2] = {{ColList(u), ColList(st.ku.view()), g.data(), g.ld()},
+                       {ColList(v), ColList(st.mv.view()), g.data() + d * g.ld(), g.ld()}};
+    gram(jobs, 2, st.n);
+    DenseMatrix both(d, 2 * d);
+    to_host(g.view().cols_range(0, 2 * d), both.data(), d);
+    DenseMatrix khat(d, d), mhat(d, d);
+    std::copy(both.data(), both.data() + d * d, khat.data());
+    std::copy(both.data() + d * d, both.data() + 2 * d * d, mhat.data());
+
+    const auto t0 = Clock::now();
+    ProjectedLrep proj = finish_assembly(khat, mhat);  // NullspaceLeak propagates
+    ro.sol = solve_small_lrep(proj, wxa);
+    st.stats.host_small_seconds += secs(t0, Clock::now());
+
+    ensure_block(st.small, d, 2 * wxa);
+    to_device(ro.sol.xhat.data(), d, wxa, d, st.small.cols(0, wxa));
+    to_device(ro.sol.yhat.data(), d, wxa, d, st.small.cols(wxa, wxa));
+    ensure_block(st.xt, st.n, wxa);
+    ensure_block(st.yt, st.n, wxa);
+    ensure_block(st.kxt, st.n, wxa);
+    ensure_block(st.myt, st.n, wxa);
+    const double* xh = st.small.data();
+    const double* yh = st.small.data() + wxa * st.small.ld();
+    const int64_t lds = st.small.ld();
+    const int32_t w = static_cast<int32_t>(wxa);
+    ProductJob pj[4] = {{ColList(u), xh, lds, w, st.xt.data(), st.xt.ld(), 1.0, 0.0},
+                        {ColList(v), yh, lds, w, st.yt.data(), st.yt.ld(), 1.0, 0.0},
+                        {ColList(st.ku.view()), xh, lds, w, st.kxt.data(), st.kxt.ld(), 1.0, 0.0},
+                        {ColList(st.mv.view()), yh, lds, w, st.myt.data(), st.myt.ld(), 1.0, 0.0}};
+    product(pj, 4, st.n);
+    return ro;
+}
+
+}  // namespace
+
+SolverState initialize(const LinearOperator& k, const LinearOperator& m, const InnerProduct& ip,
+                        const GeneralizedNullspace& ns, const BospConfig& cfg) {
+    cfg.validate();
+    const int64_t n = k.dim();
+    if (m.dim() != n) throw ContractViolation("bosp: K and M dimension mismatch");
+    if (ns.r > 0 && (ns.x0.dim() != n || ns.x0.cols() != ns.r || ns.y0.dim() != n || ns.y0.cols() != ns.r))
+        throw ContractViolation("bosp: nullspace inconsistent with operators");
+    const int64_t budget = n - ns.r;
+    if (cfg.nev > budget) throw ContractViolation("bosp: nev exceeds the number of positive eigenvalues");
+
+    const int64_t nb = cfg.effective_nb();
+    const bool moving = cfg.effective_moving();
+    const int64_t wx = std::min(moving ? cfg.s * nb : cfg.nev, budget);
+    const int64_t avail = budget - wx;
+    const int64_t wp = std::min(nb, avail / 2);
+    const int64_t ww = std::min(nb, avail - wp);
+    const int64_t d = wx + wp + ww;
+    // capacity: a moving step appends P and W to the window (X width <= wx - 2nb + 2nb)
+    const int64_t cap = std::max<int64_t>(d, wx + 2 * nb);
+
+    SolverState ss;
+    DeviceState& st = ss.dev();
+    st.n = n;
+    st.wx = wx;
+    st.wp = wp;
+    st.ww = ww;
+    if (ns.r > 0) {
+        st.x0 = DBlock(n, ns.r);
+        st.y0 = DBlock(n, ns.r);
+        to_device(ns.x0.data(), n, ns.r, n, st.x0.view());
+        to_device(ns.y0.data(), n, ns.r, n, st.y0.view());
+    }
+    // Steps 1-2: the reference's RNG stream (mt19937_64, U[-1,1], fill order x,p,w,y,q,z --
+    // bosp_solver.cpp:144-150) so both solvers start from the same vectors.
+    DBlock u(n, cap), v(n, cap);
+    {
+        std::mt19937_64 rng(cfg.rng_seed);
+        std::uniform_real_distribution<double> dist(-1.0, 1.0);
+        Runtime& rt = Runtime::get();
+        const int64_t widths[6] = {wx, wp, ww, wx, wp, ww};
+        const int64_t offs[6] = {0, wx, wx + wp, 0, wx, wx + wp};
+        double* stage[2] = {nullptr, nullptr};
+        cudaEvent_t done[2];
+        for (int i = 0; i < 2; ++i) {
+            BOSP_CUDA(cudaMallocHost(&stage[i], sizeof(double) * n));
+            BOSP_CUDA(cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming));
+            BOSP_CUDA(cudaEventRecord(done[i], rt.stream()));
+        }
+        int64_t col = 0;
+        for (int b = 0; b < 6; ++b) {
+            DBlock& dst = b < 3 ? u : v;
+            for (int64_t j = 0; j < widths[b]; ++j, ++col) {
+                const int s = static_cast<int>(col & 1);
+                BOSP_CUDA(cudaEventSynchronize(done[s]));
+                for (int64_t i = 0; i < n; ++i) stage[s][i] = dist(rng);
+                BOSP_CUDA(cudaMemcpyAsync(dst.data() + (offs[b] + j) * dst.ld(), stage[s], sizeof(double) * n,
+                                          cudaMemcpyHostToDevice, rt.stream()));
+                BOSP_CUDA(cudaEventRecord(done[s], rt.stream()));
+            }
+        }
+        rt.sync();
+        for (int i = 0; i < 2; ++i) {
+            cudaFreeHost(stage[i]);
+            cudaEventDestroy(done[i]);
+        }
+    }
+    const DMat ua = u.cols(0, d), va = v.cols(0, d);
+    dev_biorth_against(deflation_bases(st), ua, va, ip);
+    st.U = DBlock(n, cap);
+    st.V = DBlock(n, cap);
+    DevBiorthOutcome out = dev_mgs_biorth(ua, va, st.U.cols(0, d), st.V.cols(0, d), ip);
+    if (out.kept < d)
+        throw InitializationFailure("bosp: column drops during seeding left fewer than the required " +
+                                    std::to_string(d) + " columns");
+    st.lambdas.assign(static_cast<size_t>(wx), std::numeric_limits<double>::infinity());
+    st.residuals.assign(static_cast<size_t>(wx), 1.0);
+    st.last_residual.assign(static_cast<size_t>(cfg.nev), 1.0);
+    return ss;
+}
+
+bool iterate_once(SolverState& ss, const LinearOperator& k, const LinearOperator& m,
+                  const InnerProduct& ip, const GeneralizedNullspace& ns, const BospConfig& cfg) {
+    DeviceState& st = ss.dev();
+    const int64_t n = st.n;
+    const int64_t nb = cfg.effective_nb();
+    const bool moving = cfg.effective_moving();
+    const int64_t budget = n - ns.r;
+    ++st.iter;
+    ++st.stats.iterations;
+
+    const int64_t wxa = st.wx - st.frozen;
+    st.stats.max_width_u = std::max(st.stats.max_width_u, wxa + st.wp + st.ww);
+    RitzOut ro;
+    try {
+        ro = ritz_step(st, k, m, wxa);
+    } catch (const NullspaceLeak&) {
+        if (st.leak_recovered) throw NumericalAbort("bosp: projected blocks lost positive definiteness twice");
+        st.leak_recovered = true;
+        rebiorthogonalize_state(st, ip);
+        ro = ritz_step(st, k, m, wxa);
+    }
+    const int64_t d = ro.d;
+    const SmallEigenSolution& sol = ro.sol;
+
+    // write the refreshed window back
+    copy_block(st.xt.view(), st.U.cols(st.frozen, wxa));
+    copy_block(st.yt.view(), st.V.cols(st.frozen, wxa));
+    for (int64_t j = 0; j < wxa; ++j) st.lambdas[st.frozen + j] = sol.lambdas[j];
+
+    // Step 4: normalized residuals of the window pairs (:246-272)
+    DMat xt_b = st.xt.view(), yt_b = st.yt.view();
+    if (ip.weighted()) {
+        ensure_block(st.xtb, n, wxa);
+        ensure_block(st.ytb, n, wxa);
+        ip.weight()->apply_device(st.xt.view(), st.xtb.view());
+        ip.weight()->apply_device(st.yt.view(), st.ytb.view());
+        xt_b = st.xtb.view();
+        yt_b = st.ytb.view();
+        st.stats.matvec_count += 2 * wxa;
+    }
+    const double* lam_dev = upload_scalars(st, sol.lambdas, 0);
+    double* num_dev = st.scal.data() + 1024;
+    double* den_dev = st.scal.data() + 2048;
+    residual_sums(st.kxt.view(), st.myt.view(), xt_b, yt_b, st.xt.view(), st.yt.view(), lam_dev,
+                  num_dev, den_dev);
+    std::vector<double> nd(static_cast<size_t>(2 * 1024));
+    BOSP_CUDA(cudaMemcpyAsync(nd.data(), num_dev, sizeof(double) * 2048, cudaMemcpyDeviceToHost, Runtime::get().stream()));
+    Runtime::get().sync();
+    for (int64_t j = 0; j < wxa; ++j) {
+        const double lam = sol.lambdas[j];
+        st.residuals[st.frozen + j] = std::sqrt(nd[j]) / ((1.0 + lam) * std::sqrt(nd[1024 + j]));
+    }
+    const int64_t base = st.locked_count() + st.frozen;
+    int64_t prefix = 0;
+    while (prefix < wxa && st.residuals[st.frozen + prefix] < cfg.tol) ++prefix;
+    st.nev_conv = std::max(st.nev_conv, base + prefix);
+    for (int64_t j = 0; j < wxa && base + j < cfg.nev; ++j) st.last_residual[base + j] = st.residuals[st.frozen + j];
+    st.residual_history.push_back(st.last_residual);
+    if (!st.nevconv_history.empty() && st.nev_conv < st.nevconv_history.back()) st.stats.nevconv_monotone = false;
+    st.nevconv_history.push_back(st.nev_conv);
+    if (st.nev_conv >= cfg.nev) return true;
+
+    // Step 5 (:288-327): host algebra on the d x nb coefficients, then P~ = U P^, Q~ = V Q^
+    const int64_t c0 = std::min(st.nev_conv - base, wxa);
+    int64_t nb_eff = std::min(nb, wxa - c0);
+    if (wxa + 2 * nb_eff > budget) nb_eff = (budget - wxa) / 2;
+    int64_t kp = 0;
+    const DMat u_act = st.U.cols(st.frozen, d), v_act = st.V.cols(st.frozen, d);
+    if (nb_eff > 0) {
+        const auto t0 = Clock::now();
+        DenseMatrix t1(d, nb_eff), t2(d, nb_eff);
+        for (int64_t j = 0; j < nb_eff; ++j) {
+            for (int64_t i = 0; i < d; ++i) {
+                t1(i, j) = sol.xhat(i, c0 + j);
+                t2(i, j) = sol.yhat(i, c0 + j);
+            }
+            t1(c0 + j, j) -= 1.0;
+            t2(c0 + j, j) -= 1.0;
+        }
+        DenseMatrix phat = t1, qhat = t2;
+        {
+            DenseMatrix corr = matmul(sol.xhat, matmul_tn(sol.yhat, t1));
+            for (int64_t j = 0; j < nb_eff; ++j)
+                for (int64_t i = 0; i < d; ++i) phat(i, j) -= corr(i, j);
+        }
+        {
+            DenseMatrix corr = matmul(sol.yhat, matmul_tn(sol.xhat, t2));
+            for (int64_t j = 0; j < nb_eff; ++j)
+                for (int64_t i = 0; i < d; ++i) qhat(i, j) -= corr(i, j);
+        }
+        HostBiorth small = host_mgs_biorth(phat, qhat);
+        st.stats.host_small_seconds += secs(t0, Clock::now());
+        kp = small.p.cols();
+        if (kp > 0) {
+            ensure_block(st.small, d, 2 * kp);
+            to_device(small.p.data(), d, kp, d, st.small.cols(0, kp));
+            to_device(small.q.data(), d, kp, d, st.small.cols(kp, kp));
+            ensure_block(st.pt, n, kp);
+            ensure_block(st.qt, n, kp);
+            ProductJob pj[2] = {{ColList(u_act), st.small.data(), st.small.ld(), static_cast<int32_t>(kp), st.pt.data(), st.pt.ld(), 1.0, 0.0},
+                                {ColList(v_act), st.small.data() + kp * st.small.ld(), st.small.ld(), static_cast<int32_t>(kp), st.qt.data(), st.qt.ld(), 1.0, 0.0}};
+            product(pj, 2, n);
+        }
+    }
+
+    // Step 6 (:329-388): block Gauss-Seidel with batched inner CG, projection, MGS-Biorth
+    int64_t kw = 0;
+    if (nb_eff > 0) {
+        std::vector<double> lam_b(sol.lambdas.begin() + c0, sol.lambdas.begin() + c0 + nb_eff);
+        const double* lamb = upload_scalars(st, lam_b, 3072);
+        ensure_block(st.rz, n, nb_eff);
+        ensure_block(st.rw, n, nb_eff);
+        ensure_block(st.zg, n, nb_eff);
+        ensure_block(st.wg, n, nb_eff);
+        ensure_block(st.tmp, n, nb_eff);
+        lam_axmy(xt_b.cols_range(c0, nb_eff), st.myt.cols(c0, nb_eff), lamb, st.rz.view());
+        lam_axmy(yt_b.cols_range(c0, nb_eff), st.kxt.cols(c0, nb_eff), lamb, st.rw.view());
+        for (int64_t sweep = 0; sweep < cfg.ngs; ++sweep) {
+            // rhs_z = rz (+ lam B W on later sweeps); Z = CG(M, rhs_z)
+            DMat rhs_z = st.rz.view();
+            if (sweep > 0) {
+                copy_block(st.rz.view(), st.tmp.view());
+                if (ip.weighted()) {
+                    DBlock bw(n, nb_eff);
+                    ip.weight()->apply_device(st.wg.view(), bw.view());
+                    lam_axpy(bw.view(), lamb, st.tmp.view());
+                    st.stats.matvec_count += nb_eff;
+                } else {
+                    lam_axpy(st.wg.view(), lamb, st.tmp.view());
+                }
+                rhs_z = st.tmp.view();
+            }
+            DevCgOutcome cz = dev_cg(m, rhs_z, st.zg.view(), cfg.inner_cg_tol, cfg.inner_cg_max_iter, st.cg);
+            st.stats.cg_iterations += cz.sweeps;
+            // rhs_w = rw + lam B Z; W = CG(K, rhs_w)
+            copy_block(st.rw.view(), st.tmp.view());
+            if (ip.weighted()) {
+                DBlock bz(n, nb_eff);
+                ip.weight()->apply_device(st.zg.view(), bz.view());
+                lam_axpy(bz.view(), lamb, st.tmp.view());
+                st.stats.matvec_count += nb_eff;
+            } else {
+                lam_axpy(st.zg.view(), lamb, st.tmp.view());
+            }
+            DevCgOutcome cw = dev_cg(k, st.tmp.view(), st.wg.view(), cfg.inner_cg_tol, cfg.inner_cg_max_iter, st.cg);
+            st.stats.cg_iterations += cw.sweeps;
+        }
+        std::vector<DevBasis> bases = deflation_bases(st);
+        bases.push_back({st.X(), st.Y()});
+        if (kp > 0) bases.push_back({st.pt.view(), st.qt.view()});
+        dev_biorth_against(bases, st.wg.view(), st.zg.view(), ip);
+        // MGS into the W/Z slots of U/V right after the new P/Q (old P/W are dead here)
+        ensure_block(st.rz, n, nb_eff);
+        ensure_block(st.rw, n, nb_eff);
+        DevBiorthOutcome wz = dev_mgs_biorth(st.wg.view(), st.zg.view(), st.rz.view(), st.rw.view(), ip);
+        kw = wz.kept;
+    }
+
+    // Step 7 (:390-427): U = [X, P~, W~], V = [Y, Q~, Z~]
+    copy_block(st.pt.cols(0, kp), st.U.cols(st.wx, kp));
+    copy_block(st.qt.cols(0, kp), st.V.cols(st.wx, kp));
+    copy_block(st.rz.cols(0, kw), st.U.cols(st.wx + kp, kw));
+    copy_block(st.rw.cols(0, kw), st.V.cols(st.wx + kp, kw));
+    st.wp = kp;
+    st.ww = kw;
+
+    if (moving) {
+        const int64_t conv_window = st.nev_conv - st.locked_count();
+        if (conv_window >= 2 * nb && st.wx >= 2 * nb) {
+            DBlock lp(n, 2 * nb), lq(n, 2 * nb);
+            copy_block(st.U.cols(0, 2 * nb), lp.view());
+            copy_block(st.V.cols(0, 2 * nb), lq.view());
+            st.locked_p.push_back(std::move(lp));
+            st.locked_q.push_back(std::move(lq));
+            for (int64_t j = 0; j < 2 * nb; ++j) st.locked_lambdas.push_back(st.lambdas[j]);
+            // X = [X_rest, P, W]: shift columns [2nb, width) left by 2nb (through a temp copy)
+            const int64_t rest = st.width() - 2 * nb;
+            DBlock su(n, std::max<int64_t>(rest, 1)), sv(n, std::max<int64_t>(rest, 1));
+            copy_block(st.U.cols(2 * nb, rest), su.cols(0, rest));
+            copy_block(st.V.cols(2 * nb, rest), sv.cols(0, rest));
+            copy_block(su.cols(0, rest), st.U.cols(0, rest));
+            copy_block(sv.cols(0, rest), st.V.cols(0, rest));
+            std::vector<double> lam_rest(st.lambdas.begin() + 2 * nb, st.lambdas.end());
+            std::vector<double> res_rest(st.residuals.begin() + 2 * nb, st.residuals.end());
+            st.wx = rest;
+            st.wp = st.ww = 0;
+            lam_rest.resize(static_cast<size_t>(st.wx), std::numeric_limits<double>::infinity());
+            res_rest.resize(static_cast<size_t>(st.wx), 1.0);
+            st.lambdas = std::move(lam_rest);
+            st.residuals = std::move(res_rest);
+        }
+    } else if (st.wx > nb) {
+        const int64_t milestone = nb * (st.nev_conv / nb);
+        st.frozen = std::max(st.frozen, std::min(milestone, st.wx - nb));
+    }
+
+    // invariant sampling doubles as the drift monitor (:429-432)
+    const double dev = sample_invariants(st, ip);
+    if (dev > 5e-11) rebiorthogonalize_state(st, ip);
+    return false;
+}
+
+namespace {
+
+EigenResult assemble_result(DeviceState& st, const LinearOperator& k, const LinearOperator& m,
+                            const InnerProduct& ip, const BospConfig& cfg, bool converged) {
+    const int64_t n = st.n;
+    const int64_t have = std::min<int64_t>(cfg.nev, st.locked_count() + st.wx);
+    std::vector<double> lambdas;
+    std::vector<std::pair<const double*, const double*>> cols;  // (x col, y col) device pointers
+    int64_t at = 0;
+    for (size_t b = 0; b < st.locked_p.size() && at < have; ++b)
+        for (int64_t j = 0; j < st.locked_p[b].ncols() && at < have; ++j, ++at) {
+            cols.push_back({st.locked_p[b].data() + j * st.locked_p[b].ld(), st.locked_q[b].data() + j * st.locked_q[b].ld()});
+            lambdas.push_back(st.locked_lambdas[at]);
+        }
+    for (int64_t j = 0; at < have && j < st.wx; ++j, ++at) {
+        cols.push_back({st.U.data() + j * st.U.ld(), st.V.data() + j * st.V.ld()});
+        lambdas.push_back(st.lambdas[j]);
+    }
+    std::vector<int64_t> order(lambdas.size());
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return lambdas[a] < lambdas[b]; });
+
+    const int64_t h = static_cast<int64_t>(order.size());
+    DBlock rx(n, std::max<int64_t>(h, 1)), ry(n, std::max<int64_t>(h, 1));
+    rx.set_cols(h);
+    ry.set_cols(h);
+    EigenResult res;
+    res.lambdas.resize(static_cast<size_t>(h));
+    for (int64_t j = 0; j < h; ++j) {
+        res.lambdas[j] = lambdas[order[j]];
+        copy_block(DMat{const_cast<double*>(cols[order[j]].first), n, n, 1}, rx.cols(j, 1));
+        copy_block(DMat{const_cast<double*>(cols[order[j]].second), n, n, 1}, ry.cols(j, 1));
+    }
+    // fresh residuals of the assembled pairs (:486-497)
+    DBlock kx(n, std::max<int64_t>(h, 1)), my(n, std::max<int64_t>(h, 1));
+    kx.set_cols(h);
+    my.set_cols(h);
+    k.apply_device(rx.view(), kx.view());
+    m.apply_device(ry.view(), my.view());
+    DMat bx = rx.view(), by = ry.view();
+    DBlock wbx, wby;
+    if (ip.weighted()) {
+        wbx = DBlock(n, std::max<int64_t>(h, 1));
+        wby = DBlock(n, std::max<int64_t>(h, 1));
+        wbx.set_cols(h);
+        wby.set_cols(h);
+        ip.weight()->apply_device(rx.view(), wbx.view());
+        ip.weight()->apply_device(ry.view(), wby.view());
+        bx = wbx.view();
+        by = wby.view();
+    }
+    DBlock sc(std::max<int64_t>(h, 1), 3);
+    to_device(res.lambdas.data(), h, 1, h, sc.cols(0, 1));
+    residual_sums(kx.view(), my.view(), bx, by, rx.view(), ry.view(), sc.data(), sc.data() + sc.ld(),
+                  sc.data() + 2 * sc.ld());
+    std::vector<double> nd(static_cast<size_t>(3 * sc.ld()));
+    to_host(sc.view(), nd.data(), sc.ld());
+    res.residuals.resize(static_cast<size_t>(h));
+    for (int64_t j = 0; j < h; ++j)
+        res.residuals[j] = std::sqrt(nd[sc.ld() + j]) / ((1.0 + res.lambdas[j]) * std::sqrt(nd[2 * sc.ld() + j]));
+
+    res.iterations = st.iter;
+    res.history = st.residual_history;
+    res.nevconv_history = st.nevconv_history;
+    res.converged = converged;
+    res.nev_converged = std::min(st.nev_conv, cfg.nev);
+    res.stats = st.stats;
+    DenseMatrix g = ip_gram_host(ip, rx.view(), ry.view());
+    for (int64_t i = 0; i < g.rows(); ++i) g(i, i) -= 1.0;
+    res.stats.final_biorth_deviation = g.max_abs();
+    res.x = BlockVectors(n, h);
+    res.y = BlockVectors(n, h);
+    to_host(rx.view(), res.x.data(), n);
+    to_host(ry.view(), res.y.data(), n);
+    return res;
+}
+
+}  // namespace
+
+EigenResult solve(const LinearOperator& k, const LinearOperator& m, const InnerProduct& ip,
+                  const BospConfig& cfg, std::optional<GeneralizedNullspace> ns) {
+    cfg.validate();
+    Runtime& rt = Runtime::get();
+    const int64_t launches0 = rt.launches();
+    cudaEvent_t ev0, ev1;
+    BOSP_CUDA(cudaEventCreate(&ev0));
+    BOSP_CUDA(cudaEventCreate(&ev1));
+    const auto t0 = Clock::now();
+    BOSP_CUDA(cudaEventRecord(ev0, rt.stream()));
+    GeneralizedNullspace nullspace =
+        ns ? std::move(*ns) : compute_nullspace(k, m, cfg.rank_hint, cfg.tol_null, ip, cfg.rng_seed + 1);
+    SolverState st = initialize(k, m, ip, nullspace, cfg);
+    bool converged = false;
+    while (st.iter() < cfg.max_outer_iter) {
+        if (iterate_once(st, k, m, ip, nullspace, cfg)) {
+            converged = true;
+            break;
+        }
+    }
+    EigenResult res = assemble_result(st.dev(), k, m, ip, cfg, converged);
+    BOSP_CUDA(cudaEventRecord(ev1, rt.stream()));
+    rt.sync();
+    res.stats.wall_seconds = secs(t0, Clock::now());
+    float ms = 0.f;
+    BOSP_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
+    res.stats.device_seconds = ms * 1e-3;
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
+    res.stats.gpu_launches = rt.launches() - launches0;
+    return res;
+}
+
+RegressionFit regression_coefficients(const std::vector<std::vector<double>>& history,
+                                      int64_t eigenindex, double tol) {
+    std::vector<double> r;
+    for (const auto& row : history)
+        if (eigenindex < static_cast<int64_t>(row.size())) r.push_back(row[eigenindex]);
+    std::vector<std::pair<double, double>> pts;
+    for (size_t j = 1; j < r.size(); ++j) {
+        if (!(r[j - 1] > 10.0 * tol) || !(r[j] > 10.0 * tol)) continue;
+        if (!(r[j - 1] > 0.0) || !(r[j] > 0.0)) continue;
+        pts.emplace_back(std::log(r[j - 1]), std::log(r[j]));
+    }
+    if (pts.size() < 2)
+        throw NotEnoughSamples("regression_coefficients: need at least 3 iterations of residuals above 10*tol");
+    double sx = 0.0, sy = 0.0;
+    for (auto& p : pts) {
+        sx += p.first;
+        sy += p.second;
+    }
+    const double mx = sx / pts.size(), my = sy / pts.size();
+    double sxx = 0.0, sxy = 0.0;
+    for (auto& p : pts) {
+        sxx += (p.first - mx) * (p.first - mx);
+        sxy += (p.first - mx) * (p.second - my);
+    }
+    RegressionFit fit;
+    if (sxx < 1e-24) {
+        fit.degenerate = true;
+        fit.alpha = std::exp(my);
+        return fit;
+    }
+    fit.beta = sxy / sxx;
+    fit.alpha = std::exp(my - fit.beta * mx);
+    return fit;
+}
+
+}  // namespace b200
+}  // namespace bosp

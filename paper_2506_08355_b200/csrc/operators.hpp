@@ -1,0 +1,26 @@
+// Operator implementation interface (device apply) behind bosp::LinearOperator.
+#pragma once
+
+#include "api.hpp"
+#include "runtime.hpp"
+#include "sparse_ops.hpp"
+
+namespace bosp {
+inline namespace b200 {
+
+class OperatorImpl {
+public:
+    OperatorImpl(int64_t n, LinearOperator::Kind k) : n_(n), kind_(k) {}
+    virtual ~OperatorImpl();
+    // y(:, j) = A x(:, j), x and y device blocks with rows == dim(), y fully overwritten.
+    virtual void apply(const DMat& x, const DMat& y) const = 0;
+    int64_t dim() const { return n_; }
+    LinearOperator::Kind kind() const { return kind_; }
+
+private:
+    int64_t n_;
+    LinearOperator::Kind kind_;
+};
+
+}  // namespace b200
+}  // namespace bosp

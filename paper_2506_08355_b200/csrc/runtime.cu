@@ -1,0 +1,212 @@
+#include "runtime.hpp"
+
+#include <cstdio>
+#include <cstring>
+
+namespace bosp {
+inline namespace b200 {
+
+void throw_cuda(cudaError_t e, const char* what, const char* file, int line) {
+    char buf[512];
+    std::snprintf(buf, sizeof(buf), "CUDA error %s (%s) at %s:%d in %s", cudaGetErrorName(e),
+                  cudaGetErrorString(e), file, line, what);
+    throw CudaError(buf);
+}
+
+Runtime& Runtime::get() {
+    static Runtime rt;
+    return rt;
+}
+
+Runtime::Runtime() {
+    BOSP_CUDA(cudaGetDevice(&device_));
+    cudaDeviceProp prop{};
+    BOSP_CUDA(cudaGetDeviceProperties(&prop, device_));
+    sm_count_ = prop.multiProcessorCount;
+    if (prop.major < 10)
+        throw CudaError("bosp_b200: this library is built for sm_100a (B200); found sm_" +
+                        std::to_string(prop.major) + std::to_string(prop.minor));
+    BOSP_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    cudaMemPool_t pool;
+    BOSP_CUDA(cudaDeviceGetDefaultMemPool(&pool, device_));
+    uint64_t thresh = UINT64_MAX;
+    BOSP_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thresh));
+}
+
+Runtime::~Runtime() {
+    // Process teardown: the driver reclaims everything; avoid CUDA calls after context death.
+}
+
+void* Runtime::alloc(size_t bytes) {
+    if (bytes == 0) return nullptr;
+    void* p = nullptr;
+    BOSP_CUDA(cudaMallocAsync(&p, bytes, stream_));
+    return p;
+}
+
+void Runtime::free(void* p) {
+    if (p) cudaFreeAsync(p, stream_);
+}
+
+void Runtime::sync() { BOSP_CUDA(cudaStreamSynchronize(stream_)); }
+
+double* Runtime::scratch(size_t doubles) {
+    if (doubles > scratch_cap_) {
+        if (scratch_) free(scratch_);
+        scratch_cap_ = doubles + doubles / 2 + 4096;
+        scratch_ = static_cast<double*>(alloc(scratch_cap_ * sizeof(double)));
+    }
+    return scratch_;
+}
+
+unsigned int* Runtime::tickets(size_t count) {
+    if (count > tickets_cap_) {
+        if (tickets_) free(tickets_);
+        tickets_cap_ = count + 1024;
+        tickets_ = static_cast<unsigned int*>(alloc(tickets_cap_ * sizeof(unsigned int)));
+        BOSP_CUDA(cudaMemsetAsync(tickets_, 0, tickets_cap_ * sizeof(unsigned int), stream_));
+    }
+    return tickets_;
+}
+
+double* Runtime::pinned(size_t doubles) {
+    if (doubles > pinned_cap_) {
+        if (pinned_) {
+            sync();
+            cudaFreeHost(pinned_);
+        }
+        pinned_cap_ = doubles + doubles / 2 + 4096;
+        BOSP_CUDA(cudaMallocHost(&pinned_, pinned_cap_ * sizeof(double)));
+    }
+    return pinned_;
+}
+
+void Runtime::count_launch(const char* family) {
+    ++launches_;
+    ++family_launches_[family];
+}
+
+void Runtime::prof_enable(const std::string& family) {
+    prof_family_ = family;
+    prof_events_.clear();
+}
+
+bool Runtime::prof_on(const char* family) const {
+    return !prof_family_.empty() && prof_family_ == family;
+}
+
+cudaEvent_t Runtime::take_event() {
+    if (!event_pool_.empty()) {
+        cudaEvent_t e = event_pool_.back();
+        event_pool_.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    BOSP_CUDA(cudaEventCreate(&e));
+    return e;
+}
+
+void Runtime::prof_begin(const char* family, double bytes, double flops) {
+    (void)family;
+    Ev ev{take_event(), take_event(), bytes, flops};
+    BOSP_CUDA(cudaEventRecord(ev.a, stream_));
+    prof_events_.push_back(ev);
+}
+
+void Runtime::prof_end(const char* family) {
+    (void)family;
+    BOSP_CUDA(cudaEventRecord(prof_events_.back().b, stream_));
+}
+
+Runtime::ProfReport Runtime::prof_collect() {
+    sync();
+    ProfReport r{0, 0.0, 0.0, 0.0};
+    for (auto& e : prof_events_) {
+        float ms = 0.f;
+        BOSP_CUDA(cudaEventElapsedTime(&ms, e.a, e.b));
+        r.ms += ms;
+        r.bytes += e.bytes;
+        r.flops += e.flops;
+        ++r.launches;
+        event_pool_.push_back(e.a);
+        event_pool_.push_back(e.b);
+    }
+    prof_events_.clear();
+    return r;
+}
+
+LaunchScope::LaunchScope(const char* fam, double bytes, double flops) : family(fam) {
+    Runtime& rt = Runtime::get();
+    rt.count_launch(fam);
+    timed = rt.prof_on(fam);
+    if (timed) rt.prof_begin(fam, bytes, flops);
+}
+
+LaunchScope::~LaunchScope() {
+    if (timed) Runtime::get().prof_end(family);
+}
+
+DBlock::DBlock(int64_t rows, int64_t cols) : rows_(rows), cols_(cols), cap_(cols), ld_(ld_for(rows)) {
+    if (rows > 0 && cols > 0)
+        p_ = static_cast<double*>(Runtime::get().alloc(sizeof(double) * ld_ * cols));
+}
+
+DBlock::~DBlock() {
+    if (p_) Runtime::get().free(p_);
+}
+
+DBlock::DBlock(DBlock&& o) noexcept
+    : p_(o.p_), rows_(o.rows_), cols_(o.cols_), cap_(o.cap_), ld_(o.ld_) {
+    o.p_ = nullptr;
+    o.rows_ = o.cols_ = o.cap_ = 0;
+}
+
+DBlock& DBlock::operator=(DBlock&& o) noexcept {
+    if (this != &o) {
+        if (p_) Runtime::get().free(p_);
+        p_ = o.p_;
+        rows_ = o.rows_;
+        cols_ = o.cols_;
+        cap_ = o.cap_;
+        ld_ = o.ld_;
+        o.p_ = nullptr;
+        o.rows_ = o.cols_ = o.cap_ = 0;
+    }
+    return *this;
+}
+
+void DBlock::set_cols(int64_t c) {
+    if (c > cap_) throw ContractViolation("DBlock::set_cols: exceeds capacity");
+    cols_ = c;
+}
+
+void DBlock::zero() {
+    if (p_) BOSP_CUDA(cudaMemsetAsync(p_, 0, sizeof(double) * ld_ * cap_, Runtime::get().stream()));
+}
+
+void to_device(const double* host, int64_t rows, int64_t cols, int64_t ld_host, const DMat& dst) {
+    if (rows == 0 || cols == 0) return;
+    BOSP_CUDA(cudaMemcpy2DAsync(dst.p, dst.ld * sizeof(double), host, ld_host * sizeof(double),
+                                rows * sizeof(double), cols, cudaMemcpyHostToDevice,
+                                Runtime::get().stream()));
+}
+
+void to_host(const DMat& src, double* host, int64_t ld_host) {
+    if (src.rows == 0 || src.cols == 0) return;
+    Runtime& rt = Runtime::get();
+    BOSP_CUDA(cudaMemcpy2DAsync(host, ld_host * sizeof(double), src.p, src.ld * sizeof(double),
+                                src.rows * sizeof(double), src.cols, cudaMemcpyDeviceToHost,
+                                rt.stream()));
+    rt.sync();
+}
+
+void copy_block(const DMat& src, const DMat& dst) {
+    if (src.rows == 0 || src.cols == 0) return;
+    if (src.p == dst.p && src.ld == dst.ld) return;
+    BOSP_CUDA(cudaMemcpy2DAsync(dst.p, dst.ld * sizeof(double), src.p, src.ld * sizeof(double),
+                                src.rows * sizeof(double), src.cols, cudaMemcpyDeviceToDevice,
+                                Runtime::get().stream()));
+}
+
+}  // namespace b200
+}  // namespace bosp

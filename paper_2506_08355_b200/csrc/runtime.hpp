@@ -1,0 +1,116 @@
+// Device runtime for the B200 BOSP core: one stream per process/device, a stream-ordered memory
+// pool (cudaMallocAsync, release threshold = unlimited so HBM stays cached across solves), a
+// grow-only scratch arena for split-K partials and reduction tickets, pinned staging for the
+// small host<->device matrices, launch counting and per-kernel-family CUDA-event timing.
+#pragma once
+
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.hpp"
+
+namespace bosp {
+inline namespace b200 {
+
+class Runtime {
+public:
+    static Runtime& get();
+
+    cudaStream_t stream() const { return stream_; }
+    int device() const { return device_; }
+    int sm_count() const { return sm_count_; }
+
+    void* alloc(size_t bytes);
+    void free(void* p);
+    void sync();
+
+    // Scratch for split-K partials (fp64) -- valid until the next call; stream-ordered reuse is
+    // safe because every consumer runs on stream().
+    double* scratch(size_t doubles);
+    // Zero-initialised uint32 tickets; each kernel that takes tickets leaves them at zero.
+    unsigned int* tickets(size_t count);
+    // Pinned host staging (grow-only).
+    double* pinned(size_t doubles);
+
+    // Kernel accounting (gpu_launches) and optional CUDA-event timing of one kernel family.
+    void count_launch(const char* family);
+    int64_t launches() const { return launches_; }
+    void reset_launches() { launches_ = 0; family_launches_.clear(); }
+    const std::map<std::string, int64_t>& family_launches() const { return family_launches_; }
+
+    void prof_enable(const std::string& family);  // "" disables
+    bool prof_on(const char* family) const;
+    void prof_begin(const char* family, double algo_bytes, double algo_flops);
+    void prof_end(const char* family);
+    struct ProfReport { int64_t launches; double ms; double bytes; double flops; };
+    ProfReport prof_collect();  // synchronises, sums elapsed times, resets
+
+private:
+    Runtime();
+    ~Runtime();
+    int device_ = 0;
+    int sm_count_ = 148;
+    cudaStream_t stream_ = nullptr;
+    double* scratch_ = nullptr;
+    size_t scratch_cap_ = 0;
+    unsigned int* tickets_ = nullptr;
+    size_t tickets_cap_ = 0;
+    double* pinned_ = nullptr;
+    size_t pinned_cap_ = 0;
+    int64_t launches_ = 0;
+    std::map<std::string, int64_t> family_launches_;
+    std::string prof_family_;
+    struct Ev { cudaEvent_t a, b; double bytes, flops; };
+    std::vector<Ev> prof_events_;
+    std::vector<cudaEvent_t> event_pool_;
+    cudaEvent_t take_event();
+};
+
+// RAII: times one launch of `family` when profiling is on for it; always counts the launch.
+struct LaunchScope {
+    const char* family;
+    bool timed;
+    LaunchScope(const char* fam, double bytes = 0.0, double flops = 0.0);
+    ~LaunchScope();
+};
+
+// Owning device block: rows x capacity columns, column stride ld = rows rounded up to 32
+// doubles (256 B) so every column starts on a 256-byte boundary.
+class DBlock {
+public:
+    DBlock() = default;
+    DBlock(int64_t rows, int64_t cols);
+    ~DBlock();
+    DBlock(const DBlock&) = delete;
+    DBlock& operator=(const DBlock&) = delete;
+    DBlock(DBlock&& o) noexcept;
+    DBlock& operator=(DBlock&& o) noexcept;
+
+    DMat view() const { return DMat{p_, ld_, rows_, cols_}; }
+    DMat cols(int64_t c0, int64_t nc) const { return view().cols_range(c0, nc); }
+    int64_t rows() const { return rows_; }
+    int64_t ncols() const { return cols_; }
+    int64_t ld() const { return ld_; }
+    double* data() const { return p_; }
+    // Reshape the logical width within capacity (no data movement).
+    void set_cols(int64_t c);
+    int64_t capacity() const { return cap_; }
+    void zero();
+
+    static int64_t ld_for(int64_t rows) { return ((rows + 31) / 32) * 32; }
+
+private:
+    double* p_ = nullptr;
+    int64_t rows_ = 0, cols_ = 0, cap_ = 0, ld_ = 0;
+};
+
+// Device copies of small host matrices (column-major) and back.
+void to_device(const double* host, int64_t rows, int64_t cols, int64_t ld_host, const DMat& dst);
+void to_host(const DMat& src, double* host, int64_t ld_host);
+// D2D copy of a column range (handles differing ld).
+void copy_block(const DMat& src, const DMat& dst);
+
+}  // namespace b200
+}  // namespace bosp

@@ -1,0 +1,539 @@
+// Host small dense algebra for the projected LREP and the coefficient-space MGS-Biorth.
+#include "small_dense.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <numeric>
+
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+namespace bosp {
+inline namespace b200 {
+
+DenseMatrix DenseMatrix::identity(int64_t n) {
+    DenseMatrix a(n, n);
+    for (int64_t i = 0; i < n; ++i) a(i, i) = 1.0;
+    return a;
+}
+
+DenseMatrix DenseMatrix::diagonal(const std::vector<double>& d) {
+    DenseMatrix a(static_cast<int64_t>(d.size()), static_cast<int64_t>(d.size()));
+    for (size_t i = 0; i < d.size(); ++i) a(i, i) = d[i];
+    return a;
+}
+
+DenseMatrix DenseMatrix::transposed() const {
+    DenseMatrix t(cols_, rows_);
+    for (int64_t j = 0; j < cols_; ++j)
+        for (int64_t i = 0; i < rows_; ++i) t(j, i) = (*this)(i, j);
+    return t;
+}
+
+DenseMatrix DenseMatrix::symmetrized() const {
+    require(rows_ == cols_, "symmetrized: matrix is not square");
+    DenseMatrix s(rows_, cols_);
+    for (int64_t j = 0; j < cols_; ++j)
+        for (int64_t i = 0; i < rows_; ++i) s(i, j) = 0.5 * ((*this)(i, j) + (*this)(j, i));
+    return s;
+}
+
+void DenseMatrix::mirror_lower() {
+    require(rows_ == cols_, "mirror_lower: matrix is not square");
+    for (int64_t j = 0; j < cols_; ++j)
+        for (int64_t i = j + 1; i < rows_; ++i) (*this)(j, i) = (*this)(i, j);
+}
+
+double DenseMatrix::max_abs() const {
+    double m = 0.0;
+    for (double v : data_) m = std::max(m, std::fabs(v));
+    return m;
+}
+
+double DenseMatrix::frobenius_norm() const {
+    double s = 0.0;
+    for (double v : data_) s += v * v;
+    return std::sqrt(s);
+}
+
+bool DenseMatrix::is_symmetric(double tol_rel) const {
+    if (rows_ != cols_) return false;
+    const double scale = max_abs();
+    for (int64_t j = 0; j < cols_; ++j)
+        for (int64_t i = j + 1; i < rows_; ++i)
+            if (std::fabs((*this)(i, j) - (*this)(j, i)) > tol_rel * scale) return false;
+    return true;
+}
+
+DenseMatrix matmul(const DenseMatrix& a, const DenseMatrix& b) {
+    require(a.cols() == b.rows(), "matmul: inner dimensions disagree");
+    DenseMatrix c(a.rows(), b.cols());
+    const int64_t m = a.rows(), k = a.cols();
+    for (int64_t j = 0; j < b.cols(); ++j) {
+        double* cj = c.col(j);
+        for (int64_t p = 0; p < k; ++p) {
+            const double bpj = b(p, j);
+            if (bpj == 0.0) continue;
+            const double* ap = a.col(p);
+            for (int64_t i = 0; i < m; ++i) cj[i] += ap[i] * bpj;
+        }
+    }
+    return c;
+}
+
+DenseMatrix matmul_tn(const DenseMatrix& a, const DenseMatrix& b) {
+    require(a.rows() == b.rows(), "matmul_tn: row dimensions disagree");
+    DenseMatrix c(a.cols(), b.cols());
+    const int64_t m = a.rows();
+    for (int64_t j = 0; j < b.cols(); ++j) {
+        const double* bj = b.col(j);
+        for (int64_t i = 0; i < a.cols(); ++i) {
+            const double* ai = a.col(i);
+            double s = 0.0;
+            for (int64_t r = 0; r < m; ++r) s += ai[r] * bj[r];
+            c(i, j) = s;
+        }
+    }
+    return c;
+}
+
+std::optional<DenseMatrix> cholesky_lower(const DenseMatrix& a) {
+    if (a.rows() != a.cols()) return std::nullopt;
+    const int64_t n = a.rows();
+    DenseMatrix l(n, n);
+    // Row-oriented dot products as in the reference (the diagonal pivot test is the contract).
+    for (int64_t j = 0; j < n; ++j) {
+        double d = a(j, j);
+        for (int64_t k = 0; k < j; ++k) d -= l(j, k) * l(j, k);
+        if (!(d > 0.0) || !std::isfinite(d)) return std::nullopt;
+        const double ljj = std::sqrt(d);
+        l(j, j) = ljj;
+        for (int64_t i = j + 1; i < n; ++i) {
+            double s = a(i, j);
+            for (int64_t k = 0; k < j; ++k) s -= l(i, k) * l(j, k);
+            l(i, j) = s / ljj;
+        }
+    }
+    return l;
+}
+
+namespace {
+
+// Rotate columns p, q of a (m rows) and v (k rows) if they are not yet orthogonal; returns
+// whether a rotation happened.  Formula of dense_kernels.cpp:47-79.
+inline bool jacobi_pair(DenseMatrix& a, DenseMatrix& v, int64_t p, int64_t q) {
+    const int64_t m = a.rows(), k = v.rows();
+    double* ap = a.col(p);
+    double* aq = a.col(q);
+    double alpha = 0.0, beta = 0.0, gamma = 0.0;
+    for (int64_t i = 0; i < m; ++i) {
+        alpha += ap[i] * ap[i];
+        beta += aq[i] * aq[i];
+        gamma += ap[i] * aq[i];
+    }
+    if (alpha == 0.0 || beta == 0.0) return false;
+    if (std::fabs(gamma) <= 1e-15 * std::sqrt(alpha * beta)) return false;
+    const double zeta = (beta - alpha) / (2.0 * gamma);
+    const double t = ((zeta >= 0.0) ? 1.0 : -1.0) / (std::fabs(zeta) + std::sqrt(1.0 + zeta * zeta));
+    const double c = 1.0 / std::sqrt(1.0 + t * t);
+    const double s = c * t;
+    for (int64_t i = 0; i < m; ++i) {
+        const double x = ap[i], y = aq[i];
+        ap[i] = c * x - s * y;
+        aq[i] = s * x + c * y;
+    }
+    double* vp = v.col(p);
+    double* vq = v.col(q);
+    for (int64_t i = 0; i < k; ++i) {
+        const double x = vp[i], y = vq[i];
+        vp[i] = c * x - s * y;
+        vq[i] = s * x + c * y;
+    }
+    return true;
+}
+
+}  // namespace
+
+JacobiSvdResult jacobi_svd(DenseMatrix a, int64_t max_sweeps) {
+    const int64_t m = a.rows(), k = a.cols();
+    require(m >= k, "jacobi_svd: requires rows >= cols");
+    JacobiSvdResult res;
+    res.v = DenseMatrix::identity(k);
+    bool rotated = true;
+    int64_t sweep = 0;
+    if (k < 96) {
+        // cyclic-by-row order, exactly the reference's sweep
+        while (rotated && sweep < max_sweeps) {
+            rotated = false;
+            ++sweep;
+            for (int64_t p = 0; p + 1 < k; ++p)
+                for (int64_t q = p + 1; q < k; ++q) rotated |= jacobi_pair(a, res.v, p, q);
+        }
+    } else {
+        // round-robin tournament: each round pairs disjoint columns, rotated in parallel
+        const int64_t kk = k + (k & 1);
+        std::vector<int64_t> pos(kk);
+        std::iota(pos.begin(), pos.end(), 0);
+        while (rotated && sweep < max_sweeps) {
+            rotated = false;
+            ++sweep;
+            for (int64_t round = 0; round < kk - 1; ++round) {
+                int any = 0;
+#pragma omp parallel for schedule(static) reduction(| : any)
+                for (int64_t i = 0; i < kk / 2; ++i) {
+                    int64_t p = pos[i], q = pos[kk - 1 - i];
+                    if (p >= k || q >= k) continue;
+                    if (p > q) std::swap(p, q);
+                    any |= jacobi_pair(a, res.v, p, q) ? 1 : 0;
+                }
+                rotated |= (any != 0);
+                const int64_t last = pos[kk - 1];
+                for (int64_t i = kk - 1; i > 1; --i) pos[i] = pos[i - 1];
+                pos[1] = last;
+            }
+        }
+    }
+    res.converged = !rotated;
+    res.sweeps = sweep;
+    std::vector<double> sig(static_cast<size_t>(k));
+    for (int64_t j = 0; j < k; ++j) {
+        double s = 0.0;
+        const double* aj = a.col(j);
+        for (int64_t i = 0; i < m; ++i) s += aj[i] * aj[i];
+        sig[j] = std::sqrt(s);
+    }
+    std::vector<int64_t> order(static_cast<size_t>(k));
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int64_t i, int64_t j) { return sig[i] < sig[j]; });
+    res.u = DenseMatrix(m, k);
+    res.sigma.resize(static_cast<size_t>(k));
+    DenseMatrix vs(k, k);
+    for (int64_t j = 0; j < k; ++j) {
+        const int64_t src = order[j];
+        res.sigma[j] = sig[src];
+        const double inv = sig[src] > 0.0 ? 1.0 / sig[src] : 0.0;
+        for (int64_t i = 0; i < m; ++i) res.u(i, j) = a(i, src) * inv;
+        for (int64_t i = 0; i < k; ++i) vs(i, j) = res.v(i, src);
+    }
+    res.v = std::move(vs);
+    return res;
+}
+
+double spectral_norm(const DenseMatrix& a) {
+    if (a.rows() == 0 || a.cols() == 0) return 0.0;
+    auto svd = a.rows() >= a.cols() ? jacobi_svd(a) : jacobi_svd(a.transposed());
+    return svd.sigma.back();
+}
+
+DenseMatrix lu_inverse(const DenseMatrix& a0) {
+    require(a0.rows() == a0.cols(), "lu_inverse: matrix not square");
+    const int64_t n = a0.rows();
+    DenseMatrix a = a0;
+    std::vector<int64_t> perm(static_cast<size_t>(n));
+    std::iota(perm.begin(), perm.end(), 0);
+    for (int64_t k = 0; k < n; ++k) {
+        int64_t piv = k;
+        for (int64_t i = k + 1; i < n; ++i)
+            if (std::fabs(a(i, k)) > std::fabs(a(piv, k))) piv = i;
+        if (a(piv, k) == 0.0) throw ContractViolation("lu_factor: singular matrix");
+        if (piv != k) {
+            for (int64_t j = 0; j < n; ++j) std::swap(a(k, j), a(piv, j));
+            std::swap(perm[k], perm[piv]);
+        }
+        for (int64_t i = k + 1; i < n; ++i) {
+            const double l = a(i, k) / a(k, k);
+            a(i, k) = l;
+            for (int64_t j = k + 1; j < n; ++j) a(i, j) -= l * a(k, j);
+        }
+    }
+    DenseMatrix inv(n, n);
+    std::vector<double> x(static_cast<size_t>(n));
+    for (int64_t c = 0; c < n; ++c) {
+        for (int64_t i = 0; i < n; ++i) x[i] = (perm[i] == c) ? 1.0 : 0.0;
+        for (int64_t i = 1; i < n; ++i)
+            for (int64_t j = 0; j < i; ++j) x[i] -= a(i, j) * x[j];
+        for (int64_t i = n - 1; i >= 0; --i) {
+            for (int64_t j = i + 1; j < n; ++j) x[i] -= a(i, j) * x[j];
+            x[i] /= a(i, i);
+        }
+        for (int64_t i = 0; i < n; ++i) inv(i, c) = x[i];
+    }
+    return inv;
+}
+
+ProjectedLrep finish_assembly(const DenseMatrix& khat, const DenseMatrix& mhat) {
+    ProjectedLrep p;
+    p.d = khat.rows();
+    p.khat = khat.symmetrized();
+    p.mhat = mhat.symmetrized();
+    auto lk = cholesky_lower(p.khat);
+    if (!lk) throw NullspaceLeak("assemble_projected: U^T K U is not SPD");
+    auto lm = cholesky_lower(p.mhat);
+    if (!lm) throw NullspaceLeak("assemble_projected: V^T M V is not SPD");
+    p.chol_k = std::move(*lk);
+    p.chol_m = std::move(*lm);
+    return p;
+}
+
+SmallEigenSolution solve_small_lrep(const ProjectedLrep& p, int64_t k) {
+    require(k <= p.d, "solve_small_lrep: k exceeds d");
+    require(p.chol_k.rows() == p.d && p.chol_m.rows() == p.d, "solve_small_lrep: missing Cholesky factors");
+    const DenseMatrix& l = p.chol_k;
+    const DenseMatrix& r = p.chol_m;
+    JacobiSvdResult svd = jacobi_svd(matmul_tn(l, r));
+    const double smax = svd.sigma.empty() ? 0.0 : svd.sigma.back();
+    for (double s : svd.sigma)
+        if (s < 1e-14 * smax)
+            throw DegenerateSpectrum("solve_small_lrep: singular value at round-off scale, "
+                                     "a near-zero eigenvalue escaped deflation");
+    SmallEigenSolution sol;
+    sol.lambdas.assign(svd.sigma.begin(), svd.sigma.begin() + k);
+    DenseMatrix phi(p.d, k), psi(p.d, k);
+    for (int64_t j = 0; j < k; ++j) {
+        const double w = 1.0 / std::sqrt(svd.sigma[j]);
+        for (int64_t i = 0; i < p.d; ++i) {
+            phi(i, j) = svd.u(i, j) * w;
+            psi(i, j) = svd.v(i, j) * w;
+        }
+    }
+    sol.yhat = matmul(l, phi);
+    sol.xhat = matmul(r, psi);
+    return sol;
+}
+
+namespace {
+
+inline double dotn(const double* a, const double* b, int64_t n) {
+    double s = 0.0;
+    for (int64_t i = 0; i < n; ++i) s += a[i] * b[i];
+    return s;
+}
+inline void axpyn(double alpha, const double* x, double* y, int64_t n) {
+    for (int64_t i = 0; i < n; ++i) y[i] += alpha * x[i];
+}
+inline double sign_or_plus(double v) { return v < 0.0 ? -1.0 : 1.0; }
+
+HostBiorth host_gs(const DenseMatrix& x, const DenseMatrix& y, double drop_tol, bool classical) {
+    require(x.rows() == y.rows() && x.cols() == y.cols(), "biorth: X and Y must have equal shape");
+    const int64_t n = x.rows(), m = x.cols();
+    DenseMatrix p(n, m), q(n, m);
+    HostBiorth out;
+    std::vector<double> pl(static_cast<size_t>(n)), ql(static_cast<size_t>(n));
+    for (int64_t l = 0; l < m; ++l) {
+        std::copy(x.col(l), x.col(l) + n, pl.begin());
+        std::copy(y.col(l), y.col(l) + n, ql.begin());
+        for (size_t t = 0; t < out.kept.size(); ++t) {
+            const double r = classical ? dotn(q.col(t), x.col(l), n) : dotn(q.col(t), pl.data(), n);
+            axpyn(-r, p.col(t), pl.data(), n);
+            const double s = classical ? dotn(p.col(t), y.col(l), n) : dotn(p.col(t), ql.data(), n);
+            axpyn(-s, q.col(t), ql.data(), n);
+        }
+        const double pn = std::sqrt(std::max(0.0, dotn(pl.data(), pl.data(), n)));
+        const double qn = std::sqrt(std::max(0.0, dotn(ql.data(), ql.data(), n)));
+        const double eta = dotn(pl.data(), ql.data(), n);
+        if (pn == 0.0 || qn == 0.0 || std::fabs(eta) < drop_tol * pn * qn) {
+            out.dropped.push_back(l);
+            continue;
+        }
+        const double sc = 1.0 / std::sqrt(std::fabs(eta)), sg = sign_or_plus(eta);
+        const int64_t kc = static_cast<int64_t>(out.kept.size());
+        for (int64_t i = 0; i < n; ++i) {
+            p(i, kc) = sg * pl[i] * sc;
+            q(i, kc) = ql[i] * sc;
+        }
+        out.kept.push_back(l);
+    }
+    const int64_t k = static_cast<int64_t>(out.kept.size());
+    out.p = DenseMatrix(n, k);
+    out.q = DenseMatrix(n, k);
+    std::copy(p.data(), p.data() + n * k, out.p.data());
+    std::copy(q.data(), q.data() + n * k, out.q.data());
+    return out;
+}
+
+}  // namespace
+
+double biorth_loss(const DenseMatrix& g) {
+    DenseMatrix d = g;
+    for (int64_t i = 0; i < d.rows(); ++i) d(i, i) -= 1.0;
+    return spectral_norm(d);
+}
+
+bool biorth_loss_exceeds(const DenseMatrix& g, double thr) {
+    DenseMatrix d = g;
+    for (int64_t i = 0; i < d.rows(); ++i) d(i, i) -= 1.0;
+    if (d.frobenius_norm() <= thr) return false;  // ||.||_2 <= ||.||_F settles it exactly
+    return spectral_norm(d) > thr;
+}
+
+HostBiorth host_mgs_biorth(const DenseMatrix& x, const DenseMatrix& y, double drop_tol) {
+    HostBiorth out = host_gs(x, y, drop_tol, false);
+    const int64_t k = out.p.cols(), n = out.p.rows();
+    if (k > 1 && biorth_loss_exceeds(matmul_tn(out.p, out.q), 1e-10)) {
+        // rebiorth_pass (biorth.cpp:72-98)
+        std::vector<double> pl(static_cast<size_t>(n)), ql(static_cast<size_t>(n));
+        for (int64_t l = 0; l < k; ++l) {
+            std::copy(out.p.col(l), out.p.col(l) + n, pl.begin());
+            std::copy(out.q.col(l), out.q.col(l) + n, ql.begin());
+            for (int64_t j = 0; j < l; ++j) {
+                const double r = dotn(out.q.col(j), pl.data(), n);
+                axpyn(-r, out.p.col(j), pl.data(), n);
+                const double s = dotn(out.p.col(j), ql.data(), n);
+                axpyn(-s, out.q.col(j), ql.data(), n);
+            }
+            const double eta = dotn(pl.data(), ql.data(), n);
+            if (eta == 0.0) continue;
+            const double sc = 1.0 / std::sqrt(std::fabs(eta)), sg = sign_or_plus(eta);
+            for (int64_t i = 0; i < n; ++i) {
+                out.p(i, l) = sg * pl[i] * sc;
+                out.q(i, l) = ql[i] * sc;
+            }
+        }
+    }
+    return out;
+}
+
+HostBiorth host_cgs_biorth(const DenseMatrix& x, const DenseMatrix& y, double drop_tol) {
+    return host_gs(x, y, drop_tol, true);
+}
+
+CoefBiorth coef_mgs(const DenseMatrix& gxx, const DenseMatrix& gxy, const DenseMatrix& gyy,
+                    double drop_tol, bool classical) {
+    const int64_t m = gxy.rows();
+    // coefficient columns of the kept pairs, plus their images ua = Gyx a, ub = Gxy b
+    std::vector<std::vector<double>> av, bv, ua, ub;
+    CoefBiorth out;
+    std::vector<double> al, be, ta, tb;
+    for (int64_t l = 0; l < m; ++l) {
+        const int64_t len = l + 1;  // supports are within [0, l]
+        al.assign(static_cast<size_t>(len), 0.0);
+        be.assign(static_cast<size_t>(len), 0.0);
+        al[l] = be[l] = 1.0;
+        // ta = Gyx e_l = row l of Gxy ;  tb = Gxy e_l = column l of Gxy  (first len entries)
+        ta.resize(static_cast<size_t>(len));
+        tb.resize(static_cast<size_t>(len));
+        for (int64_t i = 0; i < len; ++i) {
+            ta[i] = gxy(l, i);
+            tb[i] = gxy(i, l);
+        }
+        const std::vector<double> ta0 = ta, tb0 = tb;
+        for (size_t t = 0; t < av.size(); ++t) {
+            const int64_t lt = static_cast<int64_t>(av[t].size());  // support of pair t
+            // r = <q_t, p~> = b_t^T Gyx alpha  (classical: <q_t, x_l> = b_t^T Gyx e_l)
+            const double r = dotn(bv[t].data(), classical ? ta0.data() : ta.data(), lt);
+            axpyn(-r, av[t].data(), al.data(), lt);
+            axpyn(-r, ua[t].data(), ta.data(), len);
+            const double s = dotn(av[t].data(), classical ? tb0.data() : tb.data(), lt);
+            axpyn(-s, bv[t].data(), be.data(), lt);
+            axpyn(-s, ub[t].data(), tb.data(), len);
+        }
+        double pn2 = 0.0, qn2 = 0.0;
+        for (int64_t j = 0; j < len; ++j) {
+            if (al[j] != 0.0) pn2 += al[j] * dotn(gxx.col(j), al.data(), len);
+            if (be[j] != 0.0) qn2 += be[j] * dotn(gyy.col(j), be.data(), len);
+        }
+        const double pn = std::sqrt(std::max(0.0, pn2)), qn = std::sqrt(std::max(0.0, qn2));
+        const double eta = dotn(al.data(), tb.data(), len);
+        if (pn == 0.0 || qn == 0.0 || std::fabs(eta) < drop_tol * pn * qn) {
+            out.dropped.push_back(l);
+            continue;
+        }
+        const double sc = 1.0 / std::sqrt(std::fabs(eta)), sg = sign_or_plus(eta);
+        std::vector<double> a_new(al), b_new(be), ua_new(static_cast<size_t>(m)), ub_new(static_cast<size_t>(m));
+        for (auto& v : a_new) v *= sg * sc;
+        for (auto& v : b_new) v *= sc;
+        // full-length images for later columns: ua = Gyx a_new, ub = Gxy b_new
+        for (int64_t i = 0; i < m; ++i) {
+            double sa = 0.0, sb = 0.0;
+            for (int64_t j = 0; j < len; ++j) {
+                sa += gxy(j, i) * a_new[j];
+                sb += gxy(i, j) * b_new[j];
+            }
+            ua_new[i] = sa;
+            ub_new[i] = sb;
+        }
+        av.push_back(std::move(a_new));
+        bv.push_back(std::move(b_new));
+        ua.push_back(std::move(ua_new));
+        ub.push_back(std::move(ub_new));
+        out.kept.push_back(l);
+    }
+    const int64_t k = static_cast<int64_t>(out.kept.size());
+    out.a = DenseMatrix(m, k);
+    out.b = DenseMatrix(m, k);
+    for (int64_t t = 0; t < k; ++t)
+        for (size_t i = 0; i < av[t].size(); ++i) {
+            out.a(static_cast<int64_t>(i), t) = av[t][i];
+            out.b(static_cast<int64_t>(i), t) = bv[t][i];
+        }
+    return out;
+}
+
+CoefBiorth coef_rebiorth(const DenseMatrix& gpq) {
+    const int64_t k = gpq.rows();
+    std::vector<std::vector<double>> av, bv, ua, ub;
+    std::vector<double> al, be, ta, tb;
+    for (int64_t l = 0; l < k; ++l) {
+        const int64_t len = l + 1;
+        al.assign(static_cast<size_t>(len), 0.0);
+        be.assign(static_cast<size_t>(len), 0.0);
+        al[l] = be[l] = 1.0;
+        ta.resize(static_cast<size_t>(len));
+        tb.resize(static_cast<size_t>(len));
+        for (int64_t i = 0; i < len; ++i) {
+            ta[i] = gpq(l, i);
+            tb[i] = gpq(i, l);
+        }
+        for (int64_t t = 0; t < l; ++t) {
+            const int64_t lt = static_cast<int64_t>(av[t].size());
+            const double r = dotn(bv[t].data(), ta.data(), lt);
+            axpyn(-r, av[t].data(), al.data(), lt);
+            axpyn(-r, ua[t].data(), ta.data(), len);
+            const double s = dotn(av[t].data(), tb.data(), lt);
+            axpyn(-s, bv[t].data(), be.data(), lt);
+            axpyn(-s, ub[t].data(), tb.data(), len);
+        }
+        const double eta = dotn(al.data(), tb.data(), len);
+        std::vector<double> a_new, b_new;
+        if (eta == 0.0) {  // biorth.cpp:90: column left as it was
+            a_new.assign(static_cast<size_t>(len), 0.0);
+            b_new.assign(static_cast<size_t>(len), 0.0);
+            a_new[l] = b_new[l] = 1.0;
+        } else {
+            const double sc = 1.0 / std::sqrt(std::fabs(eta)), sg = sign_or_plus(eta);
+            a_new = al;
+            b_new = be;
+            for (auto& v : a_new) v *= sg * sc;
+            for (auto& v : b_new) v *= sc;
+        }
+        std::vector<double> ua_new(static_cast<size_t>(k)), ub_new(static_cast<size_t>(k));
+        for (int64_t i = 0; i < k; ++i) {
+            double sa = 0.0, sb = 0.0;
+            for (int64_t j = 0; j < len; ++j) {
+                sa += gpq(j, i) * a_new[j];
+                sb += gpq(i, j) * b_new[j];
+            }
+            ua_new[i] = sa;
+            ub_new[i] = sb;
+        }
+        av.push_back(std::move(a_new));
+        bv.push_back(std::move(b_new));
+        ua.push_back(std::move(ua_new));
+        ub.push_back(std::move(ub_new));
+    }
+    CoefBiorth out;
+    out.a = DenseMatrix(k, k);
+    out.b = DenseMatrix(k, k);
+    for (int64_t t = 0; t < k; ++t) {
+        out.kept.push_back(t);
+        for (size_t i = 0; i < av[t].size(); ++i) {
+            out.a(static_cast<int64_t>(i), t) = av[t][i];
+            out.b(static_cast<int64_t>(i), t) = bv[t][i];
+        }
+    }
+    return out;
+}
+
+}  // namespace b200
+}  // namespace bosp

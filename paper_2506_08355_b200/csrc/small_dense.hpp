@@ -1,0 +1,105 @@
+// Host-side small dense algebra of the projected problem (stays on the host per the north
+// star): Cholesky, one-sided Jacobi SVD, the small LREP solve, the Step-5 Euclidean
+// MGS-Biorth, and the coefficient-space form of MGS-Biorth that drives the device kernels.
+#pragma once
+
+#include <cstdint>
+#include <optional>
+#include <vector>
+
+#include "common.hpp"
+
+namespace bosp {
+inline namespace b200 {
+
+// Column-major host matrix (the reference's DenseMatrix, dense_matrix.hpp:9-56).
+class DenseMatrix {
+public:
+    DenseMatrix() = default;
+    DenseMatrix(int64_t rows, int64_t cols) : rows_(rows), cols_(cols), data_(static_cast<size_t>(rows * cols), 0.0) {}
+    static DenseMatrix identity(int64_t n);
+    static DenseMatrix diagonal(const std::vector<double>& d);
+
+    int64_t rows() const { return rows_; }
+    int64_t cols() const { return cols_; }
+    double& operator()(int64_t i, int64_t j) { return data_[static_cast<size_t>(i + j * rows_)]; }
+    double operator()(int64_t i, int64_t j) const { return data_[static_cast<size_t>(i + j * rows_)]; }
+    double* data() { return data_.data(); }
+    const double* data() const { return data_.data(); }
+    double* col(int64_t j) { return data_.data() + j * rows_; }
+    const double* col(int64_t j) const { return data_.data() + j * rows_; }
+
+    DenseMatrix transposed() const;
+    DenseMatrix symmetrized() const;
+    void mirror_lower();
+    double max_abs() const;
+    double frobenius_norm() const;
+    bool is_symmetric(double tol_rel) const;
+
+private:
+    int64_t rows_ = 0, cols_ = 0;
+    std::vector<double> data_;
+};
+
+DenseMatrix matmul(const DenseMatrix& a, const DenseMatrix& b);
+DenseMatrix matmul_tn(const DenseMatrix& a, const DenseMatrix& b);
+
+// A = L L^T, or nullopt when a pivot is <= 0 / non-finite (dense_kernels.cpp:11-28).
+std::optional<DenseMatrix> cholesky_lower(const DenseMatrix& a);
+
+struct JacobiSvdResult {
+    DenseMatrix u;
+    std::vector<double> sigma;  // ascending
+    DenseMatrix v;
+    bool converged = true;
+    int64_t sweeps = 0;
+};
+// One-sided Hestenes Jacobi, same rotation formula, threshold (1e-15) and sweep cap (40) as
+// dense_kernels.cpp:30-113; the sweep is executed in a parallel round-robin ordering so that
+// column pairs of one round rotate concurrently (threads when d is large).
+JacobiSvdResult jacobi_svd(DenseMatrix a, int64_t max_sweeps = 40);
+double spectral_norm(const DenseMatrix& a);
+DenseMatrix lu_inverse(const DenseMatrix& a);
+
+// Small LREP (projected_lrep.cpp:48-80): W = L^T R, SVD, Yhat = L Phi S^-1/2, Xhat = R Psi S^-1/2.
+struct SmallEigenSolution {
+    std::vector<double> lambdas;
+    DenseMatrix xhat, yhat;
+};
+struct ProjectedLrep {
+    int64_t d = 0;
+    DenseMatrix khat, mhat, chol_k, chol_m;
+};
+// symmetrize + 2 Cholesky (throws NullspaceLeak), projected_lrep.cpp:13-25
+ProjectedLrep finish_assembly(const DenseMatrix& khat, const DenseMatrix& mhat);
+SmallEigenSolution solve_small_lrep(const ProjectedLrep& p, int64_t k);
+
+// Euclidean column-space MGS-Biorth on host (Step 5 small problem, bosp_solver.cpp:322),
+// same semantics as biorth.cpp:19-109.
+struct HostBiorth {
+    DenseMatrix p, q;
+    std::vector<int64_t> kept, dropped;
+};
+HostBiorth host_mgs_biorth(const DenseMatrix& x, const DenseMatrix& y, double drop_tol = 1e-12);
+HostBiorth host_cgs_biorth(const DenseMatrix& x, const DenseMatrix& y, double drop_tol = 1e-12);
+
+// ||G - I||_2 > thr, decided exactly: Frobenius bound first, Jacobi spectral norm only when the
+// bound does not settle it (biorth_residual, biorth.cpp:135-143, compared at mgs_biorth :104).
+bool biorth_loss_exceeds(const DenseMatrix& g, double thr);
+double biorth_loss(const DenseMatrix& g);  // exact spectral ||G - I||_2
+
+// MGS-Biorth in coefficient space.  Given the Grams of the input pair (X, Y) under the inner
+// product -- Gxx = <X,X>, Gxy = <X,Y>, Gyy = <Y,Y> -- run the exact column-sequential recurrence
+// of gs_biorth (biorth.cpp:19-69: modified projections, norms, drop test, sign/sqrt|eta|
+// scaling) on coefficient vectors, so that P = X A and Q = Y B reproduce its output.
+struct CoefBiorth {
+    DenseMatrix a, b;  // m x k
+    std::vector<int64_t> kept, dropped;
+};
+CoefBiorth coef_mgs(const DenseMatrix& gxx, const DenseMatrix& gxy, const DenseMatrix& gyy,
+                    double drop_tol, bool classical = false);
+// rebiorth_pass (biorth.cpp:72-98) in coefficient space given Gpq = <P, Q> (k x k).
+CoefBiorth coef_rebiorth(const DenseMatrix& gpq);
+
+}  // namespace b200
+}  // namespace bosp

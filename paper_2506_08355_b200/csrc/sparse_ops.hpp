@@ -1,0 +1,40 @@
+// Block sparse-matrix x multi-vector on sm_100a: SELL-32 CSR and matrix-free 5/7-point stencils.
+#pragma once
+
+#include "common.hpp"
+
+namespace bosp {
+inline namespace b200 {
+
+// SELL-C-sigma with C = 32, sigma = 1 (no row sorting): rows in slices of 32; within a slice the
+// k-th entry of every row is stored contiguously (entry k of lane l at ptr[s] + 32*k + l), so a
+// warp's matrix loads are fully coalesced.  Padding entries point at the row itself with value 0.
+struct SellDev {
+    int64_t n = 0;
+    int64_t nslices = 0;
+    const int64_t* slice_ptr = nullptr;  // nslices + 1
+    const int32_t* slice_w = nullptr;    // nslices
+    const int32_t* col = nullptr;
+    const double* val = nullptr;
+    int64_t nnz = 0;                     // true nonzeros (for algorithmic byte counts)
+};
+
+// y(:, j) = A x(:, j) for all columns of x.
+void sell_spmm(const SellDev& a, const DMat& x, const DMat& y);
+
+// Structured-grid Laplacian family: y = scale * (L_bc x) + v .* x on nx*ny*nz nodes (nz = 1 ->
+// 5-point).  bc: 0 = Neumann graph Laplacian (diag = #in-grid neighbours), 1 = Dirichlet
+// (diag = 2*dims).  potential: 0 none, 1 harmonic 0.5|x|^2 with x_i = origin + (i+1)*h,
+// 2 explicit per-node array v.
+struct StencilDev {
+    int64_t nx = 0, ny = 0, nz = 1;
+    int32_t bc = 0;
+    double scale = 1.0;
+    int32_t potential = 0;
+    double origin = 0.0, h = 1.0;
+    const double* v = nullptr;
+};
+void stencil_spmm(const StencilDev& s, const DMat& x, const DMat& y);
+
+}  // namespace b200
+}  // namespace bosp

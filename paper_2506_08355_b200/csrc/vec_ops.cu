@@ -1,0 +1,375 @@
+// Column-wise reductions, the batched-CG vector kernels and element-wise helpers.
+//
+// Reductions are deterministic: grid (chunks x columns), every block writes its partial sums,
+// the last block to finish (one ticket per launch) folds the partials in fixed chunk order and
+// runs the per-column epilogue.  HBM traffic is one streaming pass over the operands.
+#include <algorithm>
+
+#include "dense_ops.hpp"
+#include "runtime.hpp"
+
+namespace bosp {
+inline namespace b200 {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+template <int K>
+__device__ __forceinline__ void block_sum(double (&v)[K], double* sh) {
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0)
+#pragma unroll
+        for (int k = 0; k < K; ++k) sh[warp * K + k] = v[k];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            double s = 0.0;
+            for (int w = 0; w < kThreads / 32; ++w) s += sh[w * K + k];
+            v[k] = s;
+        }
+    }
+}
+
+// Generic column reduction: F::row(i, j, acc) accumulates K sums over rows of column j;
+// F::skip(j) lets a block skip a masked column; F::fin(j, sums) is the epilogue (last block).
+template <int K, class F>
+__global__ void __launch_bounds__(kThreads) k_colred(int64_t n, int ncols, int nchunks,
+                                                      int64_t chunk, F f, double* partial,
+                                                      unsigned* ticket) {
+    __shared__ double sh[(kThreads / 32) * K];
+    __shared__ bool last;
+    const int j = blockIdx.y;
+    const int c = blockIdx.x;
+    double acc[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) acc[k] = 0.0;
+    if (!f.skip(j)) {
+        const int64_t r0 = c * chunk;
+        const int64_t r1 = min(n, r0 + chunk);
+        int64_t i = r0 + threadIdx.x;
+        for (; i + 3 * kThreads < r1; i += 4 * kThreads) {
+            f.row(i, j, acc);
+            f.row(i + kThreads, j, acc);
+            f.row(i + 2 * kThreads, j, acc);
+            f.row(i + 3 * kThreads, j, acc);
+        }
+        for (; i < r1; i += kThreads) f.row(i, j, acc);
+    }
+    block_sum<K>(acc, sh);
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) partial[(static_cast<int64_t>(j) * nchunks + c) * K + k] = acc[k];
+        __threadfence();
+        const unsigned total = static_cast<unsigned>(nchunks) * ncols;
+        last = (atomicAdd(ticket, 1u) == total - 1);
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    for (int jj = threadIdx.x; jj < ncols; jj += kThreads) {
+        double s[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) s[k] = 0.0;
+        for (int cc = 0; cc < nchunks; ++cc)
+#pragma unroll
+            for (int k = 0; k < K; ++k) s[k] += __ldcg(&partial[(static_cast<int64_t>(jj) * nchunks + cc) * K + k]);
+        f.fin(jj, s);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        f.fin_all(ncols);
+        *ticket = 0u;
+    }
+}
+
+struct NoFinAll {
+    __device__ void fin_all(int) const {}
+};
+
+template <int K, class F>
+void launch_colred(const char* family, int64_t n, int ncols, const F& f, double bytes) {
+    if (ncols <= 0) return;
+    Runtime& rt = Runtime::get();
+    const int64_t target = 4LL * rt.sm_count();
+    int nchunks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n + 4095) / 4096,
+                                                                            (target + ncols - 1) / ncols)));
+    const int64_t chunk = (n + nchunks - 1) / nchunks;
+    double* partial = rt.scratch(static_cast<size_t>(nchunks) * ncols * K);
+    unsigned* ticket = rt.tickets(1);
+    LaunchScope ls(family, bytes, 0.0);
+    dim3 grid(nchunks, ncols);
+    k_colred<K, F><<<grid, kThreads, 0, rt.stream()>>>(n, ncols, nchunks, chunk, f, partial, ticket);
+    BOSP_LAUNCH_CHECK();
+}
+
+// ---- functors -------------------------------------------------------------------------------
+struct DotF : NoFinAll {
+    const double* x; int64_t ldx;
+    const double* y; int64_t ldy;
+    double* out;
+    __device__ bool skip(int) const { return false; }
+    __device__ void row(int64_t i, int j, double (&a)[1]) const {
+        a[0] += x[i + j * ldx] * y[i + j * ldy];
+    }
+    __device__ void fin(int j, const double (&s)[1]) const { out[j] = s[0]; }
+};
+
+struct ResidF : NoFinAll {
+    const double *kx, *my, *xb, *yb, *x, *y;
+    int64_t lkx, lmy, lxb, lyb, lx, ly;
+    const double* lam;
+    double *num, *den;
+    __device__ bool skip(int) const { return false; }
+    __device__ void row(int64_t i, int j, double (&a)[2]) const {
+        const double l = lam[j];
+        const double r1 = kx[i + j * lkx] - l * yb[i + j * lyb];
+        const double r2 = my[i + j * lmy] - l * xb[i + j * lxb];
+        const double xv = x[i + j * lx], yv = y[i + j * ly];
+        a[0] += r1 * r1 + r2 * r2;
+        a[1] += xv * xv + yv * yv;
+    }
+    __device__ void fin(int j, const double (&s)[2]) const {
+        num[j] = s[0];
+        den[j] = s[1];
+    }
+};
+
+// CG start: x = 0, r = b, p = b and ||b||^2 in one pass.
+struct CgStartF {
+    const double* b; int64_t lb;
+    double *x, *r, *p; int64_t lx, lr, lp;
+    CgScalars s;
+    double tol; int max_iter;
+    __device__ bool skip(int) const { return false; }
+    __device__ void row(int64_t i, int j, double (&a)[1]) const {
+        const double v = b[i + j * lb];
+        x[i + j * lx] = 0.0;
+        r[i + j * lr] = v;
+        p[i + j * lp] = v;
+        a[0] += v * v;
+    }
+    __device__ void fin(int j, const double (&sm)[1]) const {
+        const double bn = sqrt(sm[0]);
+        s.rr[j] = sm[0];
+        s.bnorm[j] = bn;
+        s.iters[j] = 0;
+        s.broken[j] = 0;
+        // cg.cpp:22 (bnorm == 0 -> column skipped) and the loop test at :33
+        s.active[j] = (bn != 0.0 && sqrt(sm[0]) > tol * bn && max_iter > 0) ? 1 : 0;
+    }
+    __device__ void fin_all(int ncols) const {
+        int c = 0;
+        for (int j = 0; j < ncols; ++j) c += s.active[j];
+        *s.any_active = c;
+    }
+};
+
+struct CgStartX0F {
+    const double *b, *x0, *ax0; int64_t lb, lx0, lax0;
+    double *x, *r, *p; int64_t lx, lr, lp;
+    CgScalars s;
+    double tol; int max_iter;
+    __device__ bool skip(int) const { return false; }
+    __device__ void row(int64_t i, int j, double (&a)[2]) const {
+        const double bv = b[i + j * lb];
+        const double rv = bv - ax0[i + j * lax0];
+        x[i + j * lx] = x0[i + j * lx0];
+        r[i + j * lr] = rv;
+        p[i + j * lp] = rv;
+        a[0] += rv * rv;
+        a[1] += bv * bv;
+    }
+    __device__ void fin(int j, const double (&sm)[2]) const {
+        const double bn = sqrt(sm[1]);
+        s.rr[j] = sm[0];
+        s.bnorm[j] = bn;
+        s.iters[j] = 0;
+        s.broken[j] = 0;
+        s.active[j] = (bn != 0.0 && sqrt(sm[0]) > tol * bn && max_iter > 0) ? 1 : 0;
+    }
+    __device__ void fin_all(int ncols) const {
+        int c = 0;
+        for (int j = 0; j < ncols; ++j) c += s.active[j];
+        *s.any_active = c;
+    }
+};
+
+struct CgPapF : NoFinAll {
+    const double *p, *ap; int64_t lp, lap;
+    CgScalars s;
+    __device__ bool skip(int j) const { return s.active[j] == 0; }
+    __device__ void row(int64_t i, int j, double (&a)[1]) const { a[0] += p[i + j * lp] * ap[i + j * lap]; }
+    __device__ void fin(int j, const double (&sm)[1]) const {
+        if (s.active[j]) s.pap[j] = sm[0];
+    }
+};
+
+// x += alpha p, r -= alpha ap, accumulate r^T r (cg.cpp:37-48); epilogue decides the masks.
+struct CgXrF {
+    double *x, *r; const double *p, *ap; int64_t lx, lr, lp, lap;
+    CgScalars s;
+    double* beta;
+    double tol; int max_iter;
+    __device__ bool skip(int j) const { return s.active[j] == 0 || !(s.pap[j] > 0.0); }
+    __device__ void row(int64_t i, int j, double (&a)[1]) const {
+        const double alpha = s.rr[j] / s.pap[j];
+        const double xv = x[i + j * lx] + alpha * p[i + j * lp];
+        const double rv = r[i + j * lr] - alpha * ap[i + j * lap];
+        x[i + j * lx] = xv;
+        r[i + j * lr] = rv;
+        a[0] += rv * rv;
+    }
+    __device__ void fin(int j, const double (&sm)[1]) const {
+        if (!s.active[j]) {
+            beta[j] = 0.0;
+            return;
+        }
+        if (!(s.pap[j] > 0.0)) {  // cg.cpp:40-44: breakdown keeps the current iterate
+            s.broken[j] = 1;
+            s.active[j] = 0;
+            beta[j] = 0.0;
+            return;
+        }
+        const double rr_new = sm[0];
+        beta[j] = rr_new / s.rr[j];
+        s.rr[j] = rr_new;
+        s.iters[j] += 1;
+        s.active[j] = (sqrt(rr_new) > tol * s.bnorm[j] && s.iters[j] < max_iter) ? 1 : 0;
+    }
+    __device__ void fin_all(int ncols) const {
+        int c = 0;
+        for (int j = 0; j < ncols; ++j) c += s.active[j];
+        *s.any_active = c;
+    }
+};
+
+// ---- element-wise kernels ----------------------------------------------------------------
+template <class F>
+__global__ void __launch_bounds__(kThreads) k_cols(int64_t n, F f) {
+    const int j = blockIdx.y;
+    if (f.skip(j)) return;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(kThreads) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * kThreads)
+        f(i, j);
+}
+
+template <class F>
+void launch_cols(const char* family, int64_t n, int ncols, const F& f, double bytes) {
+    if (ncols <= 0 || n <= 0) return;
+    Runtime& rt = Runtime::get();
+    const int64_t target = 8LL * rt.sm_count();
+    const unsigned gx = static_cast<unsigned>(std::max<int64_t>(
+        1, std::min<int64_t>((n + kThreads - 1) / kThreads, (target + ncols - 1) / ncols)));
+    LaunchScope ls(family, bytes, 0.0);
+    k_cols<F><<<dim3(gx, ncols), kThreads, 0, rt.stream()>>>(n, f);
+    BOSP_LAUNCH_CHECK();
+}
+
+struct LamAxmyF {
+    const double *a, *b; double* o; int64_t la, lb, lo; const double* lam;
+    __device__ bool skip(int) const { return false; }
+    __device__ void operator()(int64_t i, int j) const { o[i + j * lo] = lam[j] * a[i + j * la] - b[i + j * lb]; }
+};
+struct LamAxpyF {
+    const double* x; double* y; int64_t lx, ly; const double* lam;
+    __device__ bool skip(int) const { return false; }
+    __device__ void operator()(int64_t i, int j) const { y[i + j * ly] += lam[j] * x[i + j * lx]; }
+};
+struct AxpbyF {
+    double a, b; const double* x; double* y; int64_t lx, ly;
+    __device__ bool skip(int) const { return false; }
+    __device__ void operator()(int64_t i, int j) const {
+        const double xv = x[i + j * lx];
+        y[i + j * ly] = (b == 0.0) ? a * xv : a * xv + b * y[i + j * ly];
+    }
+};
+struct DiagF {
+    const double* d; const double* x; double* y; int64_t lx, ly;
+    __device__ bool skip(int) const { return false; }
+    __device__ void operator()(int64_t i, int j) const { y[i + j * ly] = d[i] * x[i + j * lx]; }
+};
+struct CgDirF {  // p = r + beta p for still-active columns (cg.cpp:49)
+    const double* r; double* p; int64_t lr, lp; const double* beta; const int* active;
+    __device__ bool skip(int j) const { return active[j] == 0; }
+    __device__ void operator()(int64_t i, int j) const { p[i + j * lp] = r[i + j * lr] + beta[j] * p[i + j * lp]; }
+};
+
+}  // namespace
+
+void col_dots(const DMat& x, const DMat& y, double* out) {
+    DotF f;
+    f.x = x.p; f.ldx = x.ld; f.y = y.p; f.ldy = y.ld; f.out = out;
+    launch_colred<1>("coldot", x.rows, static_cast<int>(x.cols), f, 16.0 * x.rows * x.cols);
+}
+
+void residual_sums(const DMat& kx, const DMat& my, const DMat& xb, const DMat& yb, const DMat& x,
+                   const DMat& y, const double* lam, double* num, double* den) {
+    ResidF f;
+    f.kx = kx.p; f.my = my.p; f.xb = xb.p; f.yb = yb.p; f.x = x.p; f.y = y.p;
+    f.lkx = kx.ld; f.lmy = my.ld; f.lxb = xb.ld; f.lyb = yb.ld; f.lx = x.ld; f.ly = y.ld;
+    f.lam = lam; f.num = num; f.den = den;
+    launch_colred<2>("residual", x.rows, static_cast<int>(x.cols), f, 8.0 * 4 * x.rows * x.cols);
+}
+
+void lam_axmy(const DMat& a, const DMat& b, const double* lam, const DMat& out) {
+    LamAxmyF f{a.p, b.p, out.p, a.ld, b.ld, out.ld, lam};
+    launch_cols("elementwise", a.rows, static_cast<int>(a.cols), f, 24.0 * a.rows * a.cols);
+}
+
+void lam_axpy(const DMat& x, const double* lam, const DMat& y) {
+    LamAxpyF f{x.p, y.p, x.ld, y.ld, lam};
+    launch_cols("elementwise", x.rows, static_cast<int>(x.cols), f, 24.0 * x.rows * x.cols);
+}
+
+void axpby(double a, const DMat& x, double b, const DMat& y) {
+    AxpbyF f{a, b, x.p, y.p, x.ld, y.ld};
+    launch_cols("elementwise", x.rows, static_cast<int>(x.cols), f, 24.0 * x.rows * x.cols);
+}
+
+void diag_scale(const double* d, const DMat& x, const DMat& y) {
+    DiagF f{d, x.p, y.p, x.ld, y.ld};
+    launch_cols("elementwise", x.rows, static_cast<int>(x.cols), f, 24.0 * x.rows * x.cols);
+}
+
+void cg_start(const DMat& b, const DMat& x, const DMat& r, const DMat& p, const CgScalars& s,
+              double tol, int max_iter) {
+    CgStartF f;
+    f.b = b.p; f.lb = b.ld; f.x = x.p; f.r = r.p; f.p = p.p; f.lx = x.ld; f.lr = r.ld; f.lp = p.ld;
+    f.s = s; f.tol = tol; f.max_iter = max_iter;
+    launch_colred<1>("cg_vec", b.rows, static_cast<int>(b.cols), f, 32.0 * b.rows * b.cols);
+}
+
+void cg_start_x0(const DMat& b, const DMat& x0, const DMat& ax0, const DMat& x, const DMat& r,
+                 const DMat& p, const CgScalars& s, double tol, int max_iter) {
+    CgStartX0F f;
+    f.b = b.p; f.x0 = x0.p; f.ax0 = ax0.p; f.lb = b.ld; f.lx0 = x0.ld; f.lax0 = ax0.ld;
+    f.x = x.p; f.r = r.p; f.p = p.p; f.lx = x.ld; f.lr = r.ld; f.lp = p.ld;
+    f.s = s; f.tol = tol; f.max_iter = max_iter;
+    launch_colred<2>("cg_vec", b.rows, static_cast<int>(b.cols), f, 48.0 * b.rows * b.cols);
+}
+
+void cg_pap(const DMat& p, const DMat& ap, const CgScalars& s) {
+    CgPapF f;
+    f.p = p.p; f.ap = ap.p; f.lp = p.ld; f.lap = ap.ld; f.s = s;
+    launch_colred<1>("cg_vec", p.rows, static_cast<int>(p.cols), f, 16.0 * p.rows * p.cols);
+}
+
+void cg_update(const DMat& x, const DMat& r, const DMat& p, const DMat& ap, const CgScalars& s,
+               double tol, int max_iter) {
+    CgXrF f;
+    f.x = x.p; f.r = r.p; f.p = p.p; f.ap = ap.p; f.lx = x.ld; f.lr = r.ld; f.lp = p.ld; f.lap = ap.ld;
+    f.s = s; f.beta = s.beta;
+    f.tol = tol; f.max_iter = max_iter;
+    launch_colred<1>("cg_vec", x.rows, static_cast<int>(x.cols), f, 48.0 * x.rows * x.cols);
+    CgDirF d{r.p, p.p, r.ld, p.ld, s.beta, s.active};
+    launch_cols("cg_vec", r.rows, static_cast<int>(r.cols), d, 24.0 * r.rows * r.cols);
+}
+
+}  // namespace b200
+}  // namespace bosp

@@ -1,0 +1,211 @@
+"""GPU parity of the individual sm_100a kernels against the oracle (numpy restatement of the
+reference, pinned by tests/test_oracle.py) and the golden fixtures, through the C ABI."""
+import numpy as np
+import pytest
+
+from oracle import bosp_oracle as O
+from paper_2506_08355_b200 import bosp
+from paper_2506_08355_b200 import problems as P
+from tests.golden.make_golden import kernel_inputs
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return np.abs(a - b).max() / max(np.abs(b).max(), 1e-300)
+
+
+@pytest.mark.parametrize("n,a,b", [(1, 1, 1), (7, 3, 5), (300, 7, 7), (1000, 33, 17),
+                                   (4099, 64, 65), (100003, 20, 20), (262144, 60, 60),
+                                   (5000, 130, 97)])
+def test_gram_matches_numpy(n, a, b):
+    rng = np.random.default_rng(n + a + b)
+    x = np.asfortranarray(rng.uniform(-1, 1, (n, a)))
+    y = np.asfortranarray(rng.uniform(-1, 1, (n, b)))
+    g = bosp.block_inner(None, x, y)
+    assert rel(g, x.T @ y) < 1e-13
+
+
+def test_gram_empty_rows():
+    g = bosp.block_inner(None, np.zeros((0, 3)), np.zeros((0, 2)))
+    assert g.shape == (3, 2) and not g.any()
+
+
+def test_block_kernels_golden(golden_small):
+    x, y = kernel_inputs(1, 300, 7)
+    c = np.random.default_rng(2).uniform(-1, 1, (7, 5))
+    assert rel(bosp.block_inner(None, x, y), golden_small["inner_xy"]) < 1e-13
+    assert rel(bosp.block_product(x, c), golden_small["product_xc"]) < 1e-13
+    assert rel(bosp.block_axpy(x, c, y[:, :5]), golden_small["axpy_yxc"]) < 1e-13
+
+
+@pytest.mark.parametrize("n,k,b", [(5, 2, 1), (1000, 30, 10), (4097, 320, 192), (262144, 60, 20),
+                                   (70000, 33, 65)])
+def test_product_and_axpy(n, k, b):
+    rng = np.random.default_rng(n + k)
+    x = np.asfortranarray(rng.uniform(-1, 1, (n, k)))
+    c = np.asfortranarray(rng.uniform(-1, 1, (k, b)))
+    y = np.asfortranarray(rng.uniform(-1, 1, (n, b)))
+    assert rel(bosp.block_product(x, c), x @ c) < 1e-13
+    assert rel(bosp.block_axpy(x, c, y), y - x @ c) < 1e-13
+
+
+def test_dense_operator_apply():
+    rng = np.random.default_rng(0)
+    for n, m in ((50, 1), (2000, 10), (3001, 33)):
+        a = np.asfortranarray(rng.standard_normal((n, n)))
+        x = np.asfortranarray(rng.standard_normal((n, m)))
+        op = bosp.LinearOperator.from_dense(a)
+        assert op.kind == bosp.LinearOperator.dense
+        assert rel(op.apply(x), a @ x) < 1e-13
+
+
+def test_csr_operator_apply_and_spec_examples():
+    # T(0) size 3 on ones -> (1,0,1); T(-1) size 4 on ones -> 0
+    t0 = bosp.LinearOperator.from_csr(P.t_matrix(3, 0.0))
+    assert np.allclose(t0.apply(np.ones(3))[:, 0], [1, 0, 1])
+    tm = bosp.LinearOperator.from_csr(P.t_matrix(4, -1.0))
+    assert np.abs(tm.apply(np.ones(4))).max() == 0.0
+    p = P.config2(16)
+    for which in ("K", "M"):
+        csr = p.K if which == "K" else p.M
+        op = bosp.LinearOperator.from_csr(csr)
+        x = np.asfortranarray(np.random.default_rng(1).uniform(-1, 1, (p.n, 9)))
+        assert rel(op.apply(x), csr.scipy() @ x) < 1e-14
+
+
+@pytest.mark.parametrize("grid", [(16, 16, 16), (13, 7, 5), (32, 32, 1), (9, 11, 1)])
+@pytest.mark.parametrize("bc,pot", [("neumann", "none"), ("dirichlet", "harmonic"), ("dirichlet", "array")])
+def test_stencil_matches_csr(grid, bc, pot):
+    nx, ny, nz = grid
+    n = nx * ny * nz
+    h = 16.0 / (nx + 1)
+    v = np.random.default_rng(3).uniform(1, 2, n) if pot == "array" else None
+    s = P.Stencil(nx, ny, nz, bc, 1.0 / h ** 2, pot, -8.0, h, v)
+    op = bosp.LinearOperator.from_stencil(s)
+    x = np.asfortranarray(np.random.default_rng(4).uniform(-1, 1, (n, 6)))
+    assert rel(op.apply(x), s.to_csr().scipy() @ x) < 1e-13
+
+
+@pytest.mark.parametrize("tag,seed,n,m", [("a", 3, 200, 12), ("b", 4, 64, 30)])
+def test_mgs_biorth_golden(golden_small, tag, seed, n, m):
+    x, y = kernel_inputs(seed, n, m)
+    p, q, kept, dropped = bosp.mgs_biorth(x, y)
+    assert list(kept) == list(golden_small[f"mgs_{tag}_kept"])
+    assert np.allclose(p, golden_small[f"mgs_{tag}_p"], rtol=1e-7, atol=1e-8)
+    assert np.allclose(q, golden_small[f"mgs_{tag}_q"], rtol=1e-7, atol=1e-8)
+    assert bosp.biorth_residual(p, q) < 1e-10
+
+
+def test_mgs_biorth_spec_examples():
+    p, q, kept, _ = bosp.mgs_biorth(np.array([[1.0], [0.0]]), np.array([[2.0], [0.0]]))
+    assert np.allclose(p[:, 0], [1 / np.sqrt(2), 0]) and np.allclose(q[:, 0], [np.sqrt(2), 0])
+    e = np.array([[1.0, 1.0], [0.0, 0.0], [0.0, 0.0]])
+    _, _, kept, dropped = bosp.mgs_biorth(e, e)
+    assert kept == [0] and dropped == [1]
+    eye = np.eye(3)[:, :2]
+    p, q, kept, _ = bosp.mgs_biorth(eye, eye)
+    assert np.allclose(p, eye) and np.allclose(q, eye) and kept == [0, 1]
+    # biorth_residual SPEC.md:177-179: P = Q = [e1, e1] -> 1
+    assert np.isclose(bosp.biorth_residual(np.array([[1.0, 1], [0, 0]]), np.array([[1.0, 1], [0, 0]])), 1.0)
+
+
+def test_mgs_biorth_large_matches_oracle_properties():
+    rng = np.random.default_rng(11)
+    n, m = 100000, 64
+    x = np.asfortranarray(rng.uniform(-1, 1, (n, m)))
+    y = np.asfortranarray(rng.uniform(-1, 1, (n, m)))
+    p, q, kept, dropped = bosp.mgs_biorth(x, y)
+    assert len(kept) == m and not dropped
+    assert bosp.biorth_residual(p, q) < 1e-10
+    # span preservation: x_j in span(P), y_j in span(Q)
+    for a, b in ((x, p), (y, q)):
+        coef, *_ = np.linalg.lstsq(b, a, rcond=None)
+        assert np.abs(b @ coef - a).max() / np.abs(a).max() < 1e-10
+
+
+def test_cgs_biorth_matches_oracle():
+    x, y = kernel_inputs(21, 120, 8)
+    p, q, kept, _ = bosp.cgs_biorth(x, y)
+    po, qo, ko, _ = O.cgs_biorth(x, y)
+    assert kept == ko
+    assert np.allclose(p, po, rtol=1e-8, atol=1e-9)
+
+
+def test_biorth_against_golden(golden_small):
+    x, y = kernel_inputs(5, 150, 6)
+    bx, by = kernel_inputs(6, 150, 4)
+    cx, cy = kernel_inputs(7, 150, 3)
+    bp, bq, _, _ = O.mgs_biorth(bx, by)
+    cp, cq, _, _ = O.mgs_biorth(cx, cy)
+    w, z = bosp.biorth_against([(bp, bq), (cp, cq)], x, y)
+    assert np.allclose(w, golden_small["against_w"], rtol=1e-10, atol=1e-11)
+    assert np.allclose(z, golden_small["against_z"], rtol=1e-10, atol=1e-11)
+    # basis (e1, e1), X = Y = e1 -> 0
+    e1 = np.array([[1.0], [0.0], [0.0]])
+    w, z = bosp.biorth_against([(e1, e1)], e1, e1)
+    assert not w.any() and not z.any()
+
+
+def test_cg_golden_and_masks(golden_small):
+    t = bosp.LinearOperator.from_csr(P.t_matrix(50, 0.0))
+    rhs = np.random.default_rng(8).uniform(-1, 1, (50, 4))
+    for tol, it in ((1e-2, 20), (1e-12, 100)):
+        x, br, mi = bosp.cg_solve(t, rhs, tol=tol, max_iter=it)
+        assert mi == int(golden_small[f"cg_{it}_maxit"][0])
+        assert np.allclose(x, golden_small[f"cg_{it}"], rtol=1e-9, atol=1e-10)
+    # rhs = 0 -> 0; 2I -> b/2 in one iteration
+    x, br, mi = bosp.cg_solve(t, np.zeros((50, 2)))
+    assert not x.any() and mi == 0
+    two = bosp.LinearOperator.scaled_identity(5, 2.0)
+    b = np.arange(1.0, 6.0)[:, None]
+    x, br, mi = bosp.cg_solve(two, b, tol=1e-12, max_iter=10)
+    assert np.allclose(x, b / 2) and mi == 1
+    # mixed columns: one zero rhs column stays exactly zero
+    rhs2 = np.concatenate([rhs[:, :2], np.zeros((50, 1)), rhs[:, 2:]], axis=1)
+    x2, _, _ = bosp.cg_solve(t, rhs2, tol=1e-2, max_iter=20)
+    assert not x2[:, 2].any()
+    assert np.allclose(x2[:, [0, 1, 3, 4]], golden_small["cg_20"], rtol=1e-9, atol=1e-10)
+
+
+def test_cg_breakdown_on_spsd():
+    # K = T(-1) is singular along ones: CG on rhs = ones hits p^T A p = 0 -> breakdown, x stays 0
+    k = bosp.LinearOperator.from_csr(P.t_matrix(8, -1.0))
+    x, br, mi = bosp.cg_solve(k, np.ones((8, 1)), tol=1e-12, max_iter=10)
+    xo, bo, mo = O.cg_solve(O.op_from_spec(P.t_matrix(8, -1.0).spec()), np.ones((8, 1)),
+                            np.zeros((8, 1)), 1e-12, 10)
+    assert br == bo and mi == mo
+    assert np.allclose(x, xo)
+
+
+def test_small_lrep_host(golden_small):
+    lam, xh, yh = bosp.solve_small_lrep(golden_small["small_k"], golden_small["small_m"], 5)
+    assert np.allclose(lam, golden_small["small_lam"], rtol=1e-13)
+    assert np.allclose(xh.T @ yh, np.eye(5), atol=1e-12)
+    lam, xh, yh = bosp.solve_small_lrep(np.array([[4.0]]), np.array([[9.0]]), 1)
+    assert np.isclose(lam[0], 6.0) and np.isclose(yh[0, 0], 2 / np.sqrt(6))
+    with pytest.raises(bosp.NullspaceLeak):
+        bosp.solve_small_lrep(np.array([[-1.0]]), np.array([[1.0]]), 1)
+
+
+def test_weighted_inner_product():
+    rng = np.random.default_rng(5)
+    n = 200
+    d = rng.uniform(1, 2, n)
+    B = bosp.LinearOperator.diagonal(d)
+    ip = bosp.InnerProduct(B)
+    x = rng.uniform(-1, 1, (n, 4))
+    y = rng.uniform(-1, 1, (n, 3))
+    assert rel(bosp.block_inner(ip, x, y), x.T @ (d[:, None] * y)) < 1e-13
+    p, q, kept, _ = bosp.mgs_biorth(x[:, :3], y, ip)
+    assert np.abs(p.T @ (d[:, None] * q) - np.eye(3)).max() < 1e-12
+
+
+def test_shape_errors_map_to_contract_violation():
+    with pytest.raises(bosp.ContractViolation):
+        bosp.block_inner(None, np.ones((5, 2)), np.ones((4, 2)))
+    with pytest.raises(bosp.ContractViolation):
+        bosp.block_product(np.ones((5, 2)), np.ones((3, 2)))
+    op = bosp.LinearOperator.identity(4)
+    with pytest.raises(bosp.ContractViolation):
+        op.apply(np.ones((5, 1)))

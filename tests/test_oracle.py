@@ -1,0 +1,169 @@
+"""CPU: pin the oracle (numpy restatement + reference build) against the golden fixtures and
+the paper's published tables.  No GPU needed."""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import bosp_oracle as O
+from paper_2506_08355_b200 import problems as P
+from tests.golden.make_golden import TABLE3_ADVANPIX, kernel_inputs
+
+try:
+    from oracle import ref
+    HAVE_REF = ref.available()
+except Exception:  # pragma: no cover
+    HAVE_REF = False
+
+needs_ref = pytest.mark.skipif(not HAVE_REF, reason="oracle/_ref not built")
+
+
+def test_rng_stream_matches_reference(golden_small):
+    # mt19937_64 + uniform_real_distribution(-1,1) restated (block_vectors.cpp:27-30)
+    assert np.array_equal(O.MT19937_64(0).uniform(2000), golden_small["rng_seed0"])
+    assert np.array_equal(O.MT19937_64(12345).uniform(777), golden_small["rng_seed12345"])
+
+
+def test_block_kernels_match_golden(golden_small):
+    x, y = kernel_inputs(1, 300, 7)
+    c = np.random.default_rng(2).uniform(-1, 1, (7, 5))
+    assert np.allclose(O.block_inner(O.InnerProduct(), x, y), golden_small["inner_xy"], rtol=1e-13, atol=1e-12)
+    assert np.allclose(O.block_product(x, c), golden_small["product_xc"], rtol=1e-13, atol=1e-13)
+    assert np.allclose(O.block_axpy(x, c, y[:, :5]), golden_small["axpy_yxc"], rtol=1e-13, atol=1e-13)
+
+
+@pytest.mark.parametrize("tag,seed,n,m", [("a", 3, 200, 12), ("b", 4, 64, 30)])
+def test_mgs_biorth_matches_golden(golden_small, tag, seed, n, m):
+    x, y = kernel_inputs(seed, n, m)
+    p, q, kept, dropped = O.mgs_biorth(x, y)
+    assert list(kept) == list(golden_small[f"mgs_{tag}_kept"])
+    assert np.allclose(p, golden_small[f"mgs_{tag}_p"], rtol=1e-8, atol=1e-9)
+    assert np.allclose(q, golden_small[f"mgs_{tag}_q"], rtol=1e-8, atol=1e-9)
+    assert O.biorth_residual(p, q, O.InnerProduct()) < 1e-10
+
+
+def test_biorth_against_matches_golden(golden_small):
+    x, y = kernel_inputs(5, 150, 6)
+    bx, by = kernel_inputs(6, 150, 4)
+    cx, cy = kernel_inputs(7, 150, 3)
+    bp, bq, _, _ = O.mgs_biorth(bx, by)
+    cp, cq, _, _ = O.mgs_biorth(cx, cy)
+    w, z = O.biorth_against([(bp, bq), (cp, cq)], x, y, O.InnerProduct())
+    assert np.allclose(w, golden_small["against_w"], rtol=1e-10, atol=1e-11)
+    assert np.allclose(z, golden_small["against_z"], rtol=1e-10, atol=1e-11)
+
+
+def test_cg_matches_golden(golden_small):
+    t = P.t_matrix(50, 0.0)
+    op = O.op_from_spec(t.spec())
+    rhs = np.random.default_rng(8).uniform(-1, 1, (50, 4))
+    for tol, it in ((1e-2, 20), (1e-12, 100)):
+        x, _, mi = O.cg_solve(op, rhs, np.zeros_like(rhs), tol, it)
+        assert mi == int(golden_small[f"cg_{it}_maxit"][0])
+        assert np.allclose(x, golden_small[f"cg_{it}"], rtol=1e-9, atol=1e-10)
+
+
+def test_small_lrep_matches_golden(golden_small):
+    kh, mh = golden_small["small_k"], golden_small["small_m"]
+    _, _, lk, lm = O.finish_assembly(kh, mh)
+    lam, xh, yh = O.solve_small_lrep(lk, lm, 5)
+    assert np.allclose(lam, golden_small["small_lam"], rtol=1e-13)
+    # eigenvector signs are fixed by the SVD convention; compare directly
+    assert np.allclose(np.abs(xh), np.abs(golden_small["small_xhat"]), rtol=1e-9, atol=1e-12)
+    assert np.allclose(xh.T @ yh, np.eye(5), atol=1e-12)
+
+
+def test_spec_examples():
+    # SPEC.md:152-154  x=(1,0), y=(2,0) -> p=(1/sqrt2,0), q=(sqrt2,0)
+    p, q, kept, dropped = O.mgs_biorth(np.array([[1.0], [0.0]]), np.array([[2.0], [0.0]]))
+    assert np.allclose(p[:, 0], [1 / np.sqrt(2), 0]) and np.allclose(q[:, 0], [np.sqrt(2), 0])
+    # SPEC.md:115 X=[e1,e1] -> second column dropped
+    e = np.array([[1.0, 1.0], [0.0, 0.0]])
+    _, _, kept, dropped = O.mgs_biorth(e, e)
+    assert kept == [0] and dropped == [1]
+    # SPEC.md:239-241  d=1, K=[4], M=[9] -> lambda=6, yhat=2/sqrt6, xhat=3/sqrt6
+    _, _, lk, lm = O.finish_assembly(np.array([[4.0]]), np.array([[9.0]]))
+    lam, xh, yh = O.solve_small_lrep(lk, lm, 1)
+    assert np.isclose(lam[0], 6.0) and np.isclose(yh[0, 0], 2 / np.sqrt(6)) and np.isclose(xh[0, 0], 3 / np.sqrt(6))
+    # SPEC.md:248-250  Khat = Mhat = T(0) size 3 -> {2-sqrt2, 2, 2+sqrt2}
+    t3 = np.array([[2.0, -1, 0], [-1, 2, -1], [0, -1, 2]])
+    _, _, lk, lm = O.finish_assembly(t3, t3)
+    lam, _, _ = O.solve_small_lrep(lk, lm, 3)
+    assert np.allclose(lam, [2 - np.sqrt(2), 2, 2 + np.sqrt(2)], rtol=1e-14)
+    # SPEC.md:292-294  T(-1)/T(0) n=4 -> X0 ∝ ones, Y0 ∝ (2,3,3,2)
+    x0, y0 = P.analytic_nullspace_T(4)
+    assert np.allclose(y0[:, 0] / y0[0, 0], [1, 1.5, 1.5, 1]) and np.isclose((x0.T @ y0)[0, 0], 1.0)
+
+
+def test_oracle_solve_t0_matches_golden_and_analytic(golden_solves):
+    n = 100
+    t = P.t_matrix(n, 0.0)
+    op = O.op_from_spec(t.spec())
+    r = O.solve(op, op, O.InnerProduct(), O.BospConfig(nev=5, nb=5, tol=1e-10), None, n)
+    g = golden_solves["t0_t0_n100"]
+    assert r.converged and r.iterations == g["iterations"]
+    assert np.allclose(r.lambdas, g["lambdas"], rtol=1e-12)
+    assert np.allclose(r.lambdas, P.t_eigenvalues(n, 5), rtol=1e-12)
+
+
+def test_oracle_solve_tm1_nullspace(golden_solves):
+    n = 100
+    k, m = P.t_matrix(n, -1.0), P.t_matrix(n, 0.0)
+    r = O.solve(O.op_from_spec(k.spec()), O.op_from_spec(m.spec()), O.InnerProduct(),
+                O.BospConfig(nev=5, nb=5, tol=1e-10), P.analytic_nullspace_T(n), n)
+    g = golden_solves["tm1_t0_n100"]
+    assert r.converged
+    assert np.allclose(r.lambdas, g["lambdas"], rtol=1e-11)
+    assert r.stats["final_biorth_deviation"] < 1e-10
+
+
+def test_oracle_moving_mechanism(golden_solves):
+    n = 400
+    t = P.t_matrix(n, 0.0)
+    op = O.op_from_spec(t.spec())
+    r = O.solve(op, op, O.InnerProduct(), O.BospConfig(nev=12, nb=2, tol=1e-9), None, n)
+    g = golden_solves["t0_moving_n400"]
+    assert r.converged
+    assert np.allclose(r.lambdas, g["lambdas"], rtol=1e-10)
+    assert np.allclose(r.lambdas, P.t_eigenvalues(n, 12), rtol=1e-10)
+    assert r.stats["max_width_u"] <= (3 + 2) * 2
+
+
+def test_golden_pins_paper_tables(golden_solves):
+    # Table 2: analytic 4 sin^2; Table 3: Advanpix
+    g2 = golden_solves["t0_t0_n1000"]["lambdas"]
+    assert np.allclose(g2, P.t_eigenvalues(1000, 10), rtol=1e-12)
+    g3 = golden_solves["tm1_t0_n1000"]["lambdas"]
+    assert np.allclose(g3, TABLE3_ADVANPIX, rtol=2e-12)
+
+
+@needs_ref
+def test_restatement_vs_reference_config2_small(golden_solves):
+    p = P.config2(8)
+    K, M = O.op_from_spec(p.oracle_spec("K")), O.op_from_spec(p.oracle_spec("M"))
+    r = O.solve(K, M, O.InnerProduct(), O.BospConfig(nev=20, nb=40, tol=1e-8), (p.x0, p.y0), p.n)
+    g = golden_solves["config2_m8"]
+    assert r.converged
+    assert np.allclose(r.lambdas, g["lambdas"], rtol=1e-10)
+    assert max(r.residuals) < 1e-8
+
+
+@needs_ref
+def test_reference_build_reproduces_golden(golden_solves):
+    n = 100
+    t = P.t_matrix(n, 0.0)
+    r = ref.solve(t.spec(), t.spec(), ref.RefConfig(nev=5, nb=5, tol=1e-10))
+    assert np.allclose(r.lambdas, golden_solves["t0_t0_n100"]["lambdas"], rtol=1e-14)
+    assert r.stats["iterations"] == golden_solves["t0_t0_n100"]["iterations"]
+
+
+def test_problem_generators_shapes():
+    p = P.config2(8)
+    assert p.n == 512 and p.K.nnz == 7 * 8 ** 3 - 6 * 8 ** 2
+    k = p.K.scipy()
+    assert abs(k @ np.ones(p.n)).max() == 0.0            # N(K) = constants
+    m = p.M.scipy()
+    assert np.allclose(m @ p.y0, p.x0, atol=1e-12)        # M Y0 = X0
+    assert np.isclose((p.x0.T @ p.y0)[0, 0], 1.0)          # X0^T Y0 = I
+    p5 = P.config5(16)
+    assert p5.K.to_csr().nnz == 5 * 16 ** 2 - 4 * 16
