@@ -1,0 +1,318 @@
+#!/usr/bin/env python
+"""Benchmark: BOSP LREP solve on B200 -- converged eigenpairs/s (BASELINE.json metric).
+
+Workload (N=1): BASELINE configs[1] = config 2, the 64^3 sparse LREP (n = 262,144, fp64 CSR,
+nev = 20, nb = 40 -> 20, tol 1e-8), explicit generalized nullspace (constants).  One "step" =
+one full bosp::solve (initialize + outer iterations + assemble_result) on the device.
+
+Arms:
+  default            the B200 library (libbosp_b200.so) through its C ABI.
+  --impl reference   the UNMODIFIED reference CPU solver (oracle/_ref/libbosp_ref.so, built from
+                     /root/reference/proj/src) on the box's host cores: each step is a bounded
+                     sample (initialize + a few iterate_once) extrapolated to a full solve with the
+                     reference's own iteration count for this config.
+
+JSON line keys follow the driver contract (metric/value/unit/n_gpus/steps/warmup/ms_per_step/
+higher_is_better/scaling/vs_baseline/dtype/data/config) plus roofline, cpu_baseline, e2e,
+gpu_launches and clocks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "converged eigenpairs/s (LREP solve, config 2: 64^3 CSR, nev=20)"
+UNIT = "eigenpairs/s"
+GOLDEN = os.path.join(ROOT, "tests", "golden", "golden_solves.json")
+
+
+def load_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "_fallback": True}
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+    return world, rank, local, dist
+
+
+def barrier(dist):
+    if dist is not None:
+        dist.barrier()
+
+
+def max_over_ranks(dist, v: float) -> float:
+    if dist is None:
+        return v
+    import torch
+    t = torch.tensor([v], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def reference_iterations() -> int:
+    try:
+        return int(json.load(open(GOLDEN))["config2"]["iterations"])
+    except Exception:
+        return 78
+
+
+def cpu_reference_sample(prob, iters: int, threads: int):
+    """Reference solver (oracle/_ref) on a bounded sample: initialize + `iters` iterate_once."""
+    from oracle import ref
+    ref.set_threads(threads)
+    out = ref.time_iterations(prob.oracle_spec("K"), prob.oracle_spec("M"), ref.RefConfig(**prob.cfg),
+                              (prob.x0, prob.y0), iters)
+    full_iters = reference_iterations()
+    t_iter = out["t_iters"] / max(1, out["iters"])
+    est = out["t_init"] + full_iters * t_iter
+    return dict(est_solve_s=est, t_init=out["t_init"], t_iter=t_iter, iters=out["iters"],
+                full_iters=full_iters, threads=ref.threads())
+
+
+def run_reference(args, world, rank, dist):
+    if rank != 0:
+        return
+    from paper_2506_08355_b200 import problems as P
+    prob = P.config2(64)
+    threads = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        cpu_reference_sample(prob, 1, threads)
+    samples = [cpu_reference_sample(prob, args.ref_iters, threads) for _ in range(args.steps)]
+    est = statistics.median(s["est_solve_s"] for s in samples)
+    value = prob.cfg["nev"] / est
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": est * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generator, paper_2506_08355_b200/problems.py)",
+        "config": {"workload": prob.name, "n": prob.n, "nev": 20, "nb": 40, "tol": 1e-8,
+                   "parallelism": "host OpenMP (reference kernels), serial CSR matvec"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": samples[0]["threads"], "kind": "reference",
+                         "sample": (f"initialize + {args.ref_iters} iterate_once per step (public API), "
+                                    f"solve time = t_init + {samples[0]['full_iters']} x t_iter "
+                                    f"(the reference's own iteration count on this config); "
+                                    f"t_init={samples[0]['t_init']:.2f}s t_iter={samples[0]['t_iter']:.2f}s")},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_b200(args, world, rank, local, dist):
+    from paper_2506_08355_b200 import _lib, bosp
+    from paper_2506_08355_b200 import problems as P
+    _lib.lib().bosp_set_device(local)
+    name, sms = bosp.device_info()
+    prob = P.config2(64)
+    cfg = bosp.BospConfig(**prob.cfg)
+    ns = bosp.GeneralizedNullspace(prob.x0, prob.y0)
+    K, M = bosp.operators_for(prob)   # resident in HBM before the timed region
+    flush = 512 << 20                  # 512 MB > 126 MB L2, written between steps
+
+    def one_step(profile_family=None):
+        _lib.lib().bosp_flush_l2(flush)
+        if profile_family:
+            bosp.profile_enable(profile_family)
+        r = bosp.solve(K, M, None, cfg, ns, want_vectors=True)
+        prof = bosp.profile_collect() if profile_family else None
+        if profile_family:
+            bosp.profile_enable(None)
+        return r, prof
+
+    for _ in range(args.warmup):
+        one_step()
+    barrier(dist)
+    bosp.device_sync()
+    bosp.launch_reset()
+    dev_s, wall_s, iters, profs = [], [], [], []
+    res = None
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            res, prof = one_step(args.roofline_kernel)
+            dev_s.append(res.stats["device_seconds"])
+            wall_s.append(res.stats["wall_seconds"])
+            iters.append(res.iterations)
+            profs.append(prof)
+    bosp.device_sync()
+    barrier(dist)
+    launches = bosp.launch_count()
+    families = bosp.launch_families()
+    total = max_over_ranks(dist, float(sum(dev_s)))
+    ms_per_step = total / args.steps * 1e3
+    value = prob.cfg["nev"] * args.steps * world / total
+
+    # parity of the measured run against the reference's own eigenvalues (golden fixture)
+    parity = None
+    try:
+        g = json.load(open(GOLDEN))["config2"]["lambdas"]
+        parity = float(np.max(np.abs(res.lambdas - np.array(g)) / np.array(g)))
+    except Exception:
+        pass
+
+    # e2e: public API with host buffers -- operator construction from pinned host CSR, the solve,
+    # results back to host; all inside the timed region.
+    kc, mc = prob.K, prob.M
+    host = {}
+    for tag, c in (("k", kc), ("m", mc)):
+        host[tag] = (np.ascontiguousarray(c.rowptr), np.ascontiguousarray(c.colidx), np.ascontiguousarray(c.vals))
+    h2d = sum(a.nbytes for t in host.values() for a in t) + prob.x0.nbytes + prob.y0.nbytes
+    d2h = 2 * prob.n * prob.cfg["nev"] * 8 + 2 * prob.cfg["nev"] * 8
+    e2e_t = []
+    for _ in range(max(1, args.steps)):
+        _lib.lib().bosp_flush_l2(flush)
+        barrier(dist)
+        t0 = time.perf_counter()
+        Ke = bosp.LinearOperator.from_csr(*host["k"])
+        Me = bosp.LinearOperator.from_csr(*host["m"])
+        r2 = bosp.solve(Ke, Me, None, cfg, ns, want_vectors=True)
+        _ = float(r2.lambdas.sum())
+        e2e_t.append(time.perf_counter() - t0)
+        del Ke, Me
+    e2e_total = max_over_ranks(dist, float(sum(e2e_t)))
+    e2e_value = prob.cfg["nev"] * len(e2e_t) * world / e2e_total
+
+    # roofline of the dominant kernel family (CUDA events on the solver stream, timed region)
+    peaks = load_peaks()
+    roof = None
+    pr = [p for p in profs if p]
+    if pr:
+        launches_k = sum(p["launches"] for p in pr)
+        ms_k = sum(p["ms"] for p in pr)
+        bytes_k = sum(p["bytes"] for p in pr)
+        if launches_k and ms_k > 0:
+            achieved = bytes_k / (ms_k * 1e-3) / 1e9
+            roof = {"kernel": args.roofline_kernel, "bound": "hbm", "achieved": achieved,
+                    "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
+                    "frac": achieved / peaks.get("hbm_gbs", 6650.0), "traffic": None,
+                    "launches_per_step": launches_k / len(pr),
+                    "avg_launch_us": ms_k * 1e3 / launches_k,
+                    "algorithmic_bytes_per_launch": bytes_k / launches_k,
+                    "share_of_step": ms_k / (sum(dev_s) * 1e3),
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if "_fallback" not in peaks
+                    else "fallback 6650 GB/s (B200_PROFILING.md)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            s = cpu_reference_sample(prob, args.ref_iters, os.cpu_count() or 1)
+            cpu = {"value": prob.cfg["nev"] / s["est_solve_s"], "unit": UNIT, "cores": s["threads"],
+                   "kind": "reference",
+                   "sample": (f"oracle/_ref (unmodified reference) initialize + {s['iters']} iterate_once on "
+                              f"config 2; solve = t_init + {s['full_iters']} x t_iter "
+                              f"(t_init={s['t_init']:.2f}s, t_iter={s['t_iter']:.2f}s)")}
+        except Exception as e:  # the checker is optional on a box without oracle/_ref
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generator, paper_2506_08355_b200/problems.py; no dataset)",
+            "config": {"workload": prob.name, "n": prob.n, "nnz_K": kc.nnz, "nev": 20, "nb": 40,
+                       "tol": 1e-8, "parallelism": "replicas" if world > 1 else "single GPU",
+                       "l2": "flushed between steps (512 MB memset)", "device": name, "sms": sms},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h)},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "solve": {"iterations": iters, "device_s": dev_s, "wall_s": wall_s,
+                      "host_small_s": res.stats["host_small_seconds"], "repairs": res.stats["repairs"],
+                      "cg_iterations": res.stats["cg_iterations"],
+                      "max_rel_eig_err_vs_reference": parity,
+                      "max_residual": float(res.residuals.max()),
+                      "final_biorth_deviation": res.stats["final_biorth_deviation"],
+                      "launch_families": families},
+        }
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--roofline-kernel", default="spmm")
+    ap.add_argument("--ref-iters", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world, rank, local, dist = dist_setup()
+    if args.impl == "reference":
+        run_reference(args, world, rank, dist)
+    else:
+        run_b200(args, world, rank, local, dist)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -191,6 +191,11 @@ void bosp_launch_reset(void);
 /* Per-family launch counts as "family=count;..." into buf. */
 int bosp_launch_families(char* buf, int len);
 void bosp_device_sync(void);
+/* Select the CUDA device for this process (call before any other entry point; one process
+ * per GPU).  Returns 0 on success. */
+int bosp_set_device(int device);
+/* Evict L2 by writing `bytes` (>= 2x the 126 MB L2) on the solver stream; synchronises. */
+void bosp_flush_l2(int64_t bytes);
 /* Pinned host memory for e2e measurements. */
 void* bosp_host_alloc(int64_t bytes);
 void bosp_host_free(void* p);

@@ -77,7 +77,7 @@ EXPORTED = [
     "bosp_biorth_residual", "bosp_cg_solve", "bosp_solve_small_lrep", "bosp_jacobi_svd",
     "bosp_cholesky", "bosp_profile_enable", "bosp_profile_collect", "bosp_launch_count",
     "bosp_launch_reset", "bosp_launch_families", "bosp_device_sync", "bosp_host_alloc",
-    "bosp_host_free",
+    "bosp_host_free", "bosp_set_device", "bosp_flush_l2",
 ]
 
 
@@ -97,6 +97,7 @@ def lib():
         L.bosp_host_alloc.argtypes = [C.c_int64]
         L.bosp_host_free.argtypes = [C.c_void_p]
         L.bosp_profile_enable.argtypes = [C.c_char_p]
+        L.bosp_flush_l2.argtypes = [C.c_int64]
         _lib = L
     return _lib
 

@@ -257,6 +257,8 @@ def compute_nullspace(K, M, rank_hint=None, tol_null=1e-10, ip=None, seed=777, c
 # ---- block kernels (kernels.hpp / biorth.hpp / cg.hpp) -------------------------------------
 def block_inner(ip, x, y):
     x, y = _f(x), _f(y)
+    if x.shape[0] != y.shape[0]:
+        raise ContractViolation("block_inner: dimension mismatch")
     ip = ip or InnerProduct()
     g = np.zeros((x.shape[1], y.shape[1]), order="F")
     check(lib().bosp_block_inner(ip._h(), C.c_int64(x.shape[0]), C.c_int64(x.shape[1]),
@@ -266,6 +268,8 @@ def block_inner(ip, x, y):
 
 def block_product(x, c):
     x, c = _f(x), _f(c)
+    if x.shape[1] != c.shape[0]:
+        raise ContractViolation("block_product: shape mismatch")
     out = np.zeros((x.shape[0], c.shape[1]), order="F")
     check(lib().bosp_block_product(C.c_int64(x.shape[0]), C.c_int64(x.shape[1]),
                                    C.c_int64(c.shape[1]), _p(x), _p(c), _p(out)))
@@ -275,6 +279,10 @@ def block_product(x, c):
 def block_axpy(x, c, y):
     x, c = _f(x), _f(c)
     y = np.array(y, dtype=np.float64, order="F", copy=True)
+    if y.ndim == 1:
+        y = y[:, None].copy(order="F")
+    if x.shape[1] != c.shape[0] or c.shape[1] != y.shape[1] or x.shape[0] != y.shape[0]:
+        raise ContractViolation("block_axpy: shape mismatch")
     check(lib().bosp_block_axpy(C.c_int64(x.shape[0]), C.c_int64(x.shape[1]),
                                 C.c_int64(c.shape[1]), _p(x), _p(c), _p(y)))
     return y
@@ -282,6 +290,8 @@ def block_axpy(x, c, y):
 
 def _biorth(x, y, ip, drop_tol, classical):
     x, y = _f(x), _f(y)
+    if x.shape != y.shape:
+        raise ContractViolation("biorth: X and Y must have equal shape")
     n, m = x.shape
     ip = ip or InnerProduct()
     p = np.zeros((n, m), order="F")
@@ -309,8 +319,12 @@ def biorth_against(bases, x, y, ip=None):
     x, y = _f(x), _f(y)
     n, m = x.shape
     ip = ip or InnerProduct()
+    if x.shape[0] != y.shape[0]:
+        raise ContractViolation("biorth_against: X and Y dimension mismatch")
     ps = [_f(p) for p, _ in bases]
     qs = [_f(q) for _, q in bases]
+    if any(p.shape[0] != n or q.shape != p.shape for p, q in zip(ps, qs)):
+        raise ContractViolation("biorth_against: basis dimension mismatch")
     widths = np.array([p.shape[1] for p in ps] or [0], dtype=np.int64)
     parr = (C.c_void_p * max(1, len(ps)))(*[p.ctypes.data for p in ps])
     qarr = (C.c_void_p * max(1, len(qs)))(*[q.ctypes.data for q in qs])

@@ -444,6 +444,26 @@ void bosp_device_sync(void) {
     }
 }
 
+int bosp_set_device(int device) {
+    return cudaSetDevice(device) == cudaSuccess ? 0 : -1;
+}
+
+void bosp_flush_l2(int64_t bytes) {
+    try {
+        bosp::Runtime& rt = bosp::Runtime::get();
+        static void* buf = nullptr;
+        static int64_t cap = 0;
+        if (bytes > cap) {
+            if (buf) cudaFree(buf);
+            BOSP_CUDA(cudaMalloc(&buf, static_cast<size_t>(bytes)));
+            cap = bytes;
+        }
+        BOSP_CUDA(cudaMemsetAsync(buf, cap & 1, static_cast<size_t>(bytes), rt.stream()));
+        rt.sync();
+    } catch (...) {
+    }
+}
+
 void* bosp_host_alloc(int64_t bytes) {
     void* p = nullptr;
     if (cudaMallocHost(&p, static_cast<size_t>(bytes)) != cudaSuccess) return nullptr;

@@ -114,17 +114,68 @@ DevBiorthOutcome dev_mgs_biorth(const DMat& x, const DMat& y, const DMat& p, con
                                 const InnerProduct& ip, double drop_tol, bool classical) {
     require(x.rows == y.rows && x.cols == y.cols, "biorth: X and Y must have equal shape");
     DevBiorthOutcome out;
-    const int64_t m = x.cols;
+    const int64_t m = x.cols, n = x.rows;
     if (m == 0) return out;
-    DenseMatrix gxx, gxy, gyy;
-    pair_grams(x, y, ip, gxx, gxy, gyy);
-    CoefBiorth cb = coef_mgs(gxx, gxy, gyy, drop_tol, classical);
-    out.kept = static_cast<int64_t>(cb.kept.size());
-    out.kept_columns = cb.kept;
-    out.dropped_columns = cb.dropped;
+    // Columns are processed in order.  Runs of well-conditioned columns go through the Gram /
+    // coefficient recurrence (level-3 on the DMMA pipe); a column whose residual cancels
+    // (nearly dependent on the kept pairs) is materialised in n-space and projected
+    // explicitly, exactly as gs_biorth would, then the remaining columns are projected against
+    // the pairs kept so far and the recurrence resumes on them.
+    constexpr double kCancel = 1e-8;
+    const int passes = classical ? 1 : 2;
+    DMat cx = x, cy = y;
+    DBlock wx, wy;
+    int64_t start = 0, kept = 0;
+    for (;;) {
+        const int64_t mr = cx.cols;
+        if (mr == 0) break;
+        DenseMatrix gxx, gxy, gyy;
+        pair_grams(cx, cy, ip, gxx, gxy, gyy);
+        int64_t stop = mr;
+        CoefBiorth cb = coef_mgs(gxx, gxy, gyy, drop_tol, classical, kCancel, &stop);
+        const int64_t kb = static_cast<int64_t>(cb.kept.size());
+        if (kb > 0) apply_coefs(cx, cy, cb.a, cb.b, p.cols_range(kept, kb), q.cols_range(kept, kb));
+        for (int64_t c : cb.kept) out.kept_columns.push_back(start + c);
+        for (int64_t c : cb.dropped) out.dropped_columns.push_back(start + c);
+        kept += kb;
+        if (stop >= mr) break;
+        // materialise column `stop`: p~ = x - P_k (Q_k^T x) (twice for MGS), q~ likewise
+        DBlock tp(n, 1), tq(n, 1);
+        copy_block(cx.cols_range(stop, 1), tp.view());
+        copy_block(cy.cols_range(stop, 1), tq.view());
+        const std::vector<DevBasis> kb_basis{{p.cols_range(0, kept), q.cols_range(0, kept)}};
+        if (kept > 0)
+            for (int ps = 0; ps < passes; ++ps) dev_biorth_against(kb_basis, tp.view(), tq.view(), ip);
+        DenseMatrix sxx, sxy, syy;
+        pair_grams(tp.view(), tq.view(), ip, sxx, sxy, syy);
+        const double pn = std::sqrt(std::max(0.0, sxx(0, 0))), qn = std::sqrt(std::max(0.0, syy(0, 0)));
+        const double eta = sxy(0, 0);
+        if (pn == 0.0 || qn == 0.0 || std::fabs(eta) < drop_tol * pn * qn) {
+            out.dropped_columns.push_back(start + stop);
+        } else {
+            const double sc = 1.0 / std::sqrt(std::fabs(eta)), sg = eta < 0.0 ? -1.0 : 1.0;
+            axpby(sg * sc, tp.view(), 0.0, p.cols_range(kept, 1));
+            axpby(sc, tq.view(), 0.0, q.cols_range(kept, 1));
+            out.kept_columns.push_back(start + stop);
+            ++kept;
+        }
+        const int64_t rest = mr - stop - 1;
+        if (rest == 0) break;
+        DBlock nx(n, rest), ny(n, rest);
+        copy_block(cx.cols_range(stop + 1, rest), nx.view());
+        copy_block(cy.cols_range(stop + 1, rest), ny.view());
+        const std::vector<DevBasis> all{{p.cols_range(0, kept), q.cols_range(0, kept)}};
+        if (kept > 0)
+            for (int ps = 0; ps < passes; ++ps) dev_biorth_against(all, nx.view(), ny.view(), ip);
+        wx = std::move(nx);
+        wy = std::move(ny);
+        cx = wx.view();
+        cy = wy.view();
+        start += stop + 1;
+    }
+    out.kept = kept;
     if (out.kept == 0) return out;
     const DMat pk = p.cols_range(0, out.kept), qk = q.cols_range(0, out.kept);
-    apply_coefs(x, y, cb.a, cb.b, pk, qk);
     if (classical || out.kept <= 1) return out;
     const DenseMatrix gpq = ip_gram_host(ip, pk, qk);
     if (!biorth_loss_exceeds(gpq, 1e-10)) return out;

@@ -11,6 +11,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <limits>
 #include <numeric>
 
@@ -77,6 +79,11 @@ void BospConfig::validate() const {
 namespace {
 
 using Clock = std::chrono::steady_clock;
+
+bool debug_enabled() {
+    static const bool on = std::getenv("BOSP_DEBUG") != nullptr;
+    return on;
+}
 
 double secs(Clock::time_point a, Clock::time_point b) {
     return std::chrono::duration<double>(b - a).count();
@@ -295,9 +302,12 @@ bool iterate_once(SolverState& ss, const LinearOperator& k, const LinearOperator
     const int64_t d = ro.d;
     const SmallEigenSolution& sol = ro.sol;
 
-    // write the refreshed window back
-    copy_block(st.xt.view(), st.U.cols(st.frozen, wxa));
-    copy_block(st.yt.view(), st.V.cols(st.frozen, wxa));
+    // The refreshed window X~ = U X^ is written back into U only after Step 5 has formed
+    // P~ = U P^ from the old U (the reference's `u` is a copy taken before assign_columns).
+    auto write_back_window = [&] {
+        copy_block(st.xt.view(), st.U.cols(st.frozen, wxa));
+        copy_block(st.yt.view(), st.V.cols(st.frozen, wxa));
+    };
     for (int64_t j = 0; j < wxa; ++j) st.lambdas[st.frozen + j] = sol.lambdas[j];
 
     // Step 4: normalized residuals of the window pairs (:246-272)
@@ -331,7 +341,10 @@ bool iterate_once(SolverState& ss, const LinearOperator& k, const LinearOperator
     st.residual_history.push_back(st.last_residual);
     if (!st.nevconv_history.empty() && st.nev_conv < st.nevconv_history.back()) st.stats.nevconv_monotone = false;
     st.nevconv_history.push_back(st.nev_conv);
-    if (st.nev_conv >= cfg.nev) return true;
+    if (st.nev_conv >= cfg.nev) {
+        write_back_window();
+        return true;
+    }
 
     // Step 5 (:288-327): host algebra on the d x nb coefficients, then P~ = U P^, Q~ = V Q^
     const int64_t c0 = std::min(st.nev_conv - base, wxa);
@@ -375,6 +388,7 @@ bool iterate_once(SolverState& ss, const LinearOperator& k, const LinearOperator
             product(pj, 2, n);
         }
     }
+    write_back_window();
 
     // Step 6 (:329-388): block Gauss-Seidel with batched inner CG, projection, MGS-Biorth
     int64_t kw = 0;
@@ -469,6 +483,11 @@ bool iterate_once(SolverState& ss, const LinearOperator& k, const LinearOperator
 
     // invariant sampling doubles as the drift monitor (:429-432)
     const double dev = sample_invariants(st, ip);
+    if (debug_enabled())
+        std::fprintf(stderr, "[bosp] it=%lld wx=%lld wp=%lld ww=%lld frozen=%lld locked=%lld nev_conv=%lld "
+                     "nb_eff=%lld c0=%lld dev=%.3e\n", (long long)st.iter, (long long)st.wx, (long long)st.wp,
+                     (long long)st.ww, (long long)st.frozen, (long long)st.locked_count(),
+                     (long long)st.nev_conv, (long long)nb_eff, (long long)c0, dev);
     if (dev > 5e-11) rebiorthogonalize_state(st, ip);
     return false;
 }

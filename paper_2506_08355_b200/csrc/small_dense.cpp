@@ -3,6 +3,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <numeric>
 
 #ifdef _OPENMP
@@ -399,8 +401,9 @@ HostBiorth host_cgs_biorth(const DenseMatrix& x, const DenseMatrix& y, double dr
 }
 
 CoefBiorth coef_mgs(const DenseMatrix& gxx, const DenseMatrix& gxy, const DenseMatrix& gyy,
-                    double drop_tol, bool classical) {
+                    double drop_tol, bool classical, double cancel_tol, int64_t* stop) {
     const int64_t m = gxy.rows();
+    if (stop) *stop = m;
     // coefficient columns of the kept pairs, plus their images ua = Gyx a, ub = Gxy b
     std::vector<std::vector<double>> av, bv, ua, ub;
     CoefBiorth out;
@@ -428,14 +431,24 @@ CoefBiorth coef_mgs(const DenseMatrix& gxx, const DenseMatrix& gxy, const DenseM
             axpyn(-s, bv[t].data(), be.data(), lt);
             axpyn(-s, ub[t].data(), tb.data(), len);
         }
-        double pn2 = 0.0, qn2 = 0.0;
+        double pn2 = 0.0, qn2 = 0.0, pnaive = 0.0, qnaive = 0.0;
         for (int64_t j = 0; j < len; ++j) {
             if (al[j] != 0.0) pn2 += al[j] * dotn(gxx.col(j), al.data(), len);
             if (be[j] != 0.0) qn2 += be[j] * dotn(gyy.col(j), be.data(), len);
+            pnaive += std::fabs(al[j]) * std::sqrt(std::max(0.0, gxx(j, j)));
+            qnaive += std::fabs(be[j]) * std::sqrt(std::max(0.0, gyy(j, j)));
+        }
+        if (cancel_tol > 0.0 && ((pnaive > 0.0 && pn2 < cancel_tol * pnaive * pnaive) ||
+                                 (qnaive > 0.0 && qn2 < cancel_tol * qnaive * qnaive))) {
+            if (stop) *stop = l;  // caller materialises column l in n-space
+            break;
         }
         const double pn = std::sqrt(std::max(0.0, pn2)), qn = std::sqrt(std::max(0.0, qn2));
         const double eta = dotn(al.data(), tb.data(), len);
         if (pn == 0.0 || qn == 0.0 || std::fabs(eta) < drop_tol * pn * qn) {
+            if (std::getenv("BOSP_DEBUG"))
+                std::fprintf(stderr, "[bosp] coef_mgs drop col %lld/%lld: pn2=%.3e qn2=%.3e eta=%.3e gxx=%.3e gyy=%.3e\n",
+                             (long long)l, (long long)m, pn2, qn2, eta, gxx(l, l), gyy(l, l));
             out.dropped.push_back(l);
             continue;
         }

@@ -96,8 +96,14 @@ struct CoefBiorth {
     DenseMatrix a, b;  // m x k
     std::vector<int64_t> kept, dropped;
 };
+// The Gram route squares the conditioning of a column that is nearly dependent on the kept
+// ones (catastrophic cancellation in a^T Gxx a).  coef_mgs therefore stops at the first column
+// whose residual norm^2 falls below cancel_tol x its naive magnitude; `stop` returns that
+// column (m when all were processed) so the caller can materialise it in n-space exactly as the
+// reference does.  cancel_tol = 0 disables the check.
 CoefBiorth coef_mgs(const DenseMatrix& gxx, const DenseMatrix& gxy, const DenseMatrix& gyy,
-                    double drop_tol, bool classical = false);
+                    double drop_tol, bool classical = false, double cancel_tol = 0.0,
+                    int64_t* stop = nullptr);
 // rebiorth_pass (biorth.cpp:72-98) in coefficient space given Gpq = <P, Q> (k x k).
 CoefBiorth coef_rebiorth(const DenseMatrix& gpq);
 

@@ -101,7 +101,9 @@ void sell_spmm(const SellDev& a, const DMat& x, const DMat& y) {
     constexpr int CB = 4;
     const int ncols = static_cast<int>(x.cols);
     dim3 grid(static_cast<unsigned>((a.n + kRows - 1) / kRows), (ncols + CB - 1) / CB);
-    const double bytes = 12.0 * a.nnz * grid.y + 4.0 * (a.n + 1) + 16.0 * a.n * ncols;
+    // algorithmic (minimum) traffic: CSR once (8 B value + 4 B int32 index per nnz,
+    // 4 B per row pointer) + x read once + y written once
+    const double bytes = 12.0 * a.nnz + 4.0 * (a.n + 1) + 16.0 * a.n * ncols;
     LaunchScope ls("spmm", bytes, 2.0 * a.nnz * ncols);
     k_sell<CB><<<grid, kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols);
     BOSP_LAUNCH_CHECK();
