@@ -170,6 +170,11 @@ bosp_status bosp_biorth_residual(bosp_op B, int64_t n, int64_t m, const double* 
 bosp_status bosp_cg_solve(bosp_op A, int64_t m, const double* rhs, const double* x0, double tol,
                           int64_t max_iter, double* x, int32_t* breakdown, int64_t* max_it_used);
 
+/* The initial random blocks exactly as initialize() draws them (bosp_solver.cpp:144-150):
+ * U = [X|P|W] (n x d) then V = [Y|Q|Z] (n x d) from mt19937_64(seed), uniform [-1, 1),
+ * generated on the device. */
+bosp_status bosp_seed_blocks(uint64_t seed, int64_t n, int64_t d, double* u, double* v);
+
 /* Host small dense (projected_lrep.cpp:48-80, dense_kernels.cpp:11-123). */
 bosp_status bosp_solve_small_lrep(int64_t d, const double* khat, const double* mhat, int64_t k,
                                   double* lambdas, double* xhat, double* yhat);
@@ -185,6 +190,12 @@ bosp_status bosp_cholesky(int64_t n, const double* a, double* l, int32_t* ok);
 void bosp_profile_enable(const char* family);
 /* Synchronises; returns launches, summed device ms, algorithmic bytes and flops since enable. */
 void bosp_profile_collect(int64_t* launches, double* ms, double* bytes, double* flops);
+/* Microbenchmark: apply `op` to a device-resident random n x ncols block `reps` times (after
+ * one warm-up); returns the mean device time per apply in *ms (CUDA events). */
+bosp_status bosp_bench_apply(bosp_op op, int64_t ncols, int64_t reps, double* ms);
+/* Microbenchmark of the tall-skinny kernels on device-resident random data: kind 0 = Gram
+ * (n x a)^T (n x b), 1 = product (n x a)(a x b), 2 = axpy; mean ms per call over `reps`. */
+bosp_status bosp_bench_blas(int32_t kind, int64_t n, int64_t a, int64_t b, int64_t reps, double* ms);
 /* Kernel launches issued by this library since the last reset. */
 int64_t bosp_launch_count(void);
 void bosp_launch_reset(void);

@@ -77,7 +77,8 @@ EXPORTED = [
     "bosp_biorth_residual", "bosp_cg_solve", "bosp_solve_small_lrep", "bosp_jacobi_svd",
     "bosp_cholesky", "bosp_profile_enable", "bosp_profile_collect", "bosp_launch_count",
     "bosp_launch_reset", "bosp_launch_families", "bosp_device_sync", "bosp_host_alloc",
-    "bosp_host_free", "bosp_set_device", "bosp_flush_l2",
+    "bosp_host_free", "bosp_set_device", "bosp_flush_l2", "bosp_seed_blocks",
+    "bosp_bench_apply", "bosp_bench_blas",
 ]
 
 

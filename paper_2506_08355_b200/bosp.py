@@ -386,6 +386,14 @@ def cholesky_lower(a):
     return l if ok.value else None
 
 
+def seed_blocks(seed, n, d):
+    """(U, V) initial blocks as initialize() draws them, generated on the device."""
+    u = np.zeros((n, d), order="F")
+    v = np.zeros((n, d), order="F")
+    check(lib().bosp_seed_blocks(C.c_uint64(seed), C.c_int64(n), C.c_int64(d), _p(u), _p(v)))
+    return u, v
+
+
 # ---- measurement hooks ----------------------------------------------------------------------
 def device_info():
     buf = C.create_string_buffer(256)
@@ -426,6 +434,21 @@ def launch_families():
 
 def device_sync():
     lib().bosp_device_sync()
+
+
+def bench_apply(op, ncols, reps=20):
+    ms = C.c_double()
+    check(lib().bosp_bench_apply(op._h, C.c_int64(ncols), C.c_int64(reps), C.byref(ms)))
+    return ms.value
+
+
+def bench_blas(kind, n, a, b, reps=20):
+    """kind: 'gram' | 'product' | 'axpy' -> mean ms per call on device-resident data."""
+    k = {"gram": 0, "product": 1, "axpy": 2}[kind]
+    ms = C.c_double()
+    check(lib().bosp_bench_blas(C.c_int32(k), C.c_int64(n), C.c_int64(a), C.c_int64(b),
+                                C.c_int64(reps), C.byref(ms)))
+    return ms.value
 
 
 def operators_for(problem):

@@ -6,7 +6,9 @@
 #include <string>
 
 #include "api.hpp"
+#include "dense_ops.hpp"
 #include "operators.hpp"
+#include "rng.hpp"
 #include "runtime.hpp"
 
 struct bosp_op_s {
@@ -67,6 +69,29 @@ bosp::InnerProduct ip_of(bosp_op b) {
 }
 
 bosp_op wrap(bosp::LinearOperator op) { return new bosp_op_s{std::move(op)}; }
+
+void fill_random(const bosp::DMat& m, uint64_t seed) {
+    bosp::DBlock tmp(m.rows, m.cols);
+    bosp::mt_fill_uv(seed, m, tmp.view());
+}
+
+template <class F>
+double time_reps(int64_t reps, F&& f) {
+    bosp::Runtime& rt = bosp::Runtime::get();
+    f();
+    cudaEvent_t a, b;
+    BOSP_CUDA(cudaEventCreate(&a));
+    BOSP_CUDA(cudaEventCreate(&b));
+    BOSP_CUDA(cudaEventRecord(a, rt.stream()));
+    for (int64_t i = 0; i < reps; ++i) f();
+    BOSP_CUDA(cudaEventRecord(b, rt.stream()));
+    rt.sync();
+    float ms = 0.f;
+    BOSP_CUDA(cudaEventElapsedTime(&ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    return ms / static_cast<double>(std::max<int64_t>(reps, 1));
+}
 
 bosp::BospConfig cfg_of(const bosp_config* c) {
     bosp::BospConfig cfg;
@@ -357,6 +382,17 @@ bosp_status bosp_cg_solve(bosp_op A, int64_t m, const double* rhs, const double*
     });
 }
 
+bosp_status bosp_seed_blocks(uint64_t seed, int64_t n, int64_t d, double* u, double* v) {
+    return guarded([&] {
+        bosp::DBlock du(n, std::max<int64_t>(d, 1)), dv(n, std::max<int64_t>(d, 1));
+        du.set_cols(d);
+        dv.set_cols(d);
+        bosp::mt_fill_uv(seed, du.view(), dv.view());
+        bosp::to_host(du.view(), u, n);
+        bosp::to_host(dv.view(), v, n);
+    });
+}
+
 bosp_status bosp_solve_small_lrep(int64_t d, const double* khat, const double* mhat, int64_t k,
                                   double* lambdas, double* xhat, double* yhat) {
     return guarded([&] {
@@ -442,6 +478,31 @@ void bosp_device_sync(void) {
         bosp::Runtime::get().sync();
     } catch (...) {
     }
+}
+
+bosp_status bosp_bench_apply(bosp_op op, int64_t ncols, int64_t reps, double* ms) {
+    return guarded([&] {
+        const int64_t n = op->op.dim();
+        bosp::DBlock x(n, ncols), y(n, ncols);
+        fill_random(x.view(), 1);
+        *ms = time_reps(reps, [&] { op->op.apply_device(x.view(), y.view()); });
+    });
+}
+
+bosp_status bosp_bench_blas(int32_t kind, int64_t n, int64_t a, int64_t b, int64_t reps, double* ms) {
+    return guarded([&] {
+        bosp::DBlock x(n, a), y(n, b), c(std::max<int64_t>(a, b), std::max<int64_t>(a, b));
+        fill_random(x.view(), 1);
+        fill_random(y.view(), 2);
+        fill_random(c.view(), 3);
+        if (kind == 0)
+            *ms = time_reps(reps, [&] { bosp::gram(bosp::ColList(x.view()), bosp::ColList(y.view()), n, c.data(), c.ld()); });
+        else
+            *ms = time_reps(reps, [&] {
+                bosp::product(bosp::ColList(x.view()), c.data(), c.ld(), static_cast<int32_t>(b), y.view(),
+                              kind == 1 ? 1.0 : -1.0, kind == 1 ? 0.0 : 1.0);
+            });
+    });
 }
 
 int bosp_set_device(int device) {

@@ -57,6 +57,8 @@ void lam_axpy(const DMat& x, const double* lam_dev, const DMat& y);
 // y = x + sigma * y  (shifted operator epilogue) / y = alpha * x / y = d .* x
 void axpby(double a, const DMat& x, double b, const DMat& y);
 void diag_scale(const double* d_dev, const DMat& x, const DMat& y);
+// t = a^T (square or rectangular; t.rows == a.cols, t.cols == a.rows)
+void transpose(const DMat& a, const DMat& t);
 
 // ---- Batched multi-RHS CG kernels (reference cg_solve, cg.cpp:11-58) -------------------------
 // Per-column scalars live on the device in CgScalars; every kernel honours the column masks, so
@@ -70,6 +72,11 @@ struct CgScalars {
     int* broken;      // p^T A p <= 0 hit
     int* iters;       // iterations taken
     int* any_active;  // scalar: number of active columns (device)
+    int* loops;       // scalar: batched iterations executed (device)
+    // When the CG runs as a CUDA graph with a `while` conditional node, the start/update
+    // epilogues set the loop condition to (any column still active).
+    cudaGraphConditionalHandle cond = 0;
+    int has_cond = 0;
 };
 // x = 0, r = b, p = b, rr = ||b||^2, bnorm = ||b||, active = (bnorm != 0 && sqrt(rr) > tol*bnorm)
 void cg_start(const DMat& b, const DMat& x, const DMat& r, const DMat& p, const CgScalars& s,

@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "operators.hpp"
 
@@ -198,8 +199,19 @@ double dev_biorth_residual(const DMat& p, const DMat& q, const InnerProduct& ip)
 // ---------------------------------------------------------------------------------------------
 // Batched multi-RHS CG
 // ---------------------------------------------------------------------------------------------
+namespace {
+void drop_graphs(std::vector<CgGraph>& gs) {
+    for (CgGraph& g : gs) {
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+        if (g.graph) cudaGraphDestroy(g.graph);
+    }
+    gs.clear();
+}
+}  // namespace
+
 void CgWorkspace::ensure(int64_t n, int64_t m) {
     if (r.rows() != n || r.capacity() < m) {
+        drop_graphs(graphs);  // recorded launches point at the old buffers
         r = DBlock(n, m);
         p = DBlock(n, m);
         ap = DBlock(n, m);
@@ -208,6 +220,7 @@ void CgWorkspace::ensure(int64_t n, int64_t m) {
     p.set_cols(m);
     ap.set_cols(m);
     if (m > m_cap_) {
+        drop_graphs(graphs);
         Runtime& rt = Runtime::get();
         if (scal_) rt.free(scal_);
         m_cap_ = m;
@@ -223,6 +236,7 @@ void CgWorkspace::ensure(int64_t n, int64_t m) {
         s.broken = iv + m;
         s.iters = iv + 2 * m;
         s.any_active = iv + 3 * m;
+        s.loops = iv + 3 * m + 1;
     }
     if (!host_active) {
         BOSP_CUDA(cudaMallocHost(&host_active, 4 * sizeof(int)));
@@ -246,36 +260,106 @@ DevCgOutcome dev_cg(const LinearOperator& a, const DMat& rhs, const DMat& x, dou
     ws.ensure(rhs.rows, m);
     const DMat r = ws.r.view(), p = ws.p.view(), ap = ws.ap.view();
     const int mi = static_cast<int>(std::min<int64_t>(max_iter, 1 << 30));
-    if (x0) {
-        a.apply_device(*x0, ap);
-        cg_start_x0(rhs, *x0, ap, x, r, p, ws.s, tol, mi);
-    } else {
-        cg_start(rhs, x, r, p, ws.s, tol, mi);
-    }
-    // State s (s = 0 after start, s = it+1 after iteration it) publishes its active-column count
-    // to pinned slot s % 2.  Before issuing iteration it the host looks at state it-1, which the
-    // device has finished while it works on iteration it-1: no stall, and at most one fully
-    // masked iteration is ever issued.
-    auto publish = [&](int64_t state) {
-        const int slot = static_cast<int>(state & 1);
-        BOSP_CUDA(cudaMemcpyAsync(&ws.host_active[slot], ws.s.any_active, sizeof(int),
-                                  cudaMemcpyDeviceToHost, rt.stream()));
-        BOSP_CUDA(cudaEventRecord(ws.ev[slot], rt.stream()));
-    };
-    publish(0);
-    int64_t it = 0;
-    for (; it < max_iter; ++it) {
-        if (it >= 1) {
-            const int slot = static_cast<int>((it - 1) & 1);
-            BOSP_CUDA(cudaEventSynchronize(ws.ev[slot]));
-            if (ws.host_active[slot] == 0) break;
+    if (!x0 && a.impl()->capturable() && !std::getenv("BOSP_NO_GRAPHS")) {
+        // ---- graph path: the whole solve is one launch, the loop runs on the device ----
+        CgGraph* g = nullptr;
+        for (CgGraph& c : ws.graphs)
+            if (c.op == a.impl() && c.rhs == rhs.p && c.ldr == rhs.ld && c.x == x.p && c.ldx == x.ld &&
+                c.m == m && c.tol == tol && c.max_iter == max_iter && c.prof_family == rt.prof_family())
+                g = &c;
+        if (!g) {
+            if (ws.graphs.size() >= 8) drop_graphs(ws.graphs);
+            ws.graphs.emplace_back();
+            g = &ws.graphs.back();
+            g->op = a.impl();
+            g->rhs = rhs.p;
+            g->ldr = rhs.ld;
+            g->x = x.p;
+            g->ldx = x.ld;
+            g->m = m;
+            g->tol = tol;
+            g->max_iter = max_iter;
+            g->prof_family = rt.prof_family();
+            rt.set_capture_prof(&g->prof_pairs);
+            rt.scratch(1 << 16);  // no pool growth while recording
+            rt.tickets(64);
+            rt.sync();
+            BOSP_CUDA(cudaGraphCreate(&g->graph, 0));
+            cudaGraphConditionalHandle h;
+            BOSP_CUDA(cudaGraphConditionalHandleCreate(&h, g->graph, 0, 0));
+            CgScalars sc = ws.s;
+            sc.cond = h;
+            sc.has_cond = 1;
+            // prologue: x = 0, r = p = b, norms, loop condition
+            rt.set_capture_sink(&g->start_launches);
+            BOSP_CUDA(cudaStreamBeginCaptureToGraph(rt.stream(), g->graph, nullptr, nullptr, 0,
+                                                    cudaStreamCaptureModeRelaxed));
+            cg_start(rhs, x, r, p, sc, tol, mi);
+            BOSP_CUDA(cudaStreamEndCapture(rt.stream(), &g->graph));
+            size_t nn = 0;
+            BOSP_CUDA(cudaGraphGetNodes(g->graph, nullptr, &nn));
+            std::vector<cudaGraphNode_t> deps(nn);
+            BOSP_CUDA(cudaGraphGetNodes(g->graph, deps.data(), &nn));
+            cudaGraphNodeParams cp{};
+            cp.type = cudaGraphNodeTypeConditional;
+            cp.conditional.handle = h;
+            cp.conditional.type = cudaGraphCondTypeWhile;
+            cp.conditional.size = 1;
+            cudaGraphNode_t cnode;
+            BOSP_CUDA(cudaGraphAddNode(&cnode, g->graph, deps.data(), nn, &cp));
+            cudaGraph_t body = cp.conditional.phGraph_out[0];
+            rt.set_capture_sink(&g->body_launches);
+            BOSP_CUDA(cudaStreamBeginCaptureToGraph(rt.stream(), body, nullptr, nullptr, 0,
+                                                    cudaStreamCaptureModeRelaxed));
+            a.apply_device(p, ap);
+            cg_pap(p, ap, sc);
+            cg_update(x, r, p, ap, sc, tol, mi);
+            BOSP_CUDA(cudaStreamEndCapture(rt.stream(), &body));
+            rt.set_capture_sink(nullptr);
+            rt.set_capture_prof(nullptr);
+            BOSP_CUDA(cudaGraphInstantiate(&g->exec, g->graph, 0));
         }
-        a.apply_device(p, ap);
-        cg_pap(p, ap, ws.s);
-        cg_update(x, r, p, ap, ws.s, tol, mi);
-        publish(it + 1);
+        BOSP_CUDA(cudaGraphLaunch(g->exec, rt.stream()));
+        BOSP_CUDA(cudaMemcpyAsync(&ws.host_active[2], ws.s.loops, sizeof(int), cudaMemcpyDeviceToHost, rt.stream()));
+        rt.sync();
+        out.sweeps = ws.host_active[2];
+        // event pairs inside the body hold the last iteration's launch: one live sample each
+        if (!g->prof_pairs.empty() && out.sweeps > 0) rt.add_prof_samples(g->prof_pairs);
+        rt.add_launches(g->start_launches, 1);
+        rt.add_launches(g->body_launches, out.sweeps);
+    } else {
+        // ---- host-driven loop (host callbacks, x0 != 0, or per-kernel profiling) ----
+        if (x0) {
+            a.apply_device(*x0, ap);
+            cg_start_x0(rhs, *x0, ap, x, r, p, ws.s, tol, mi);
+        } else {
+            cg_start(rhs, x, r, p, ws.s, tol, mi);
+        }
+        // State s (s = 0 after start, s = it+1 after iteration it) publishes its active-column
+        // count to pinned slot s % 2.  Before issuing iteration it the host looks at state it-1,
+        // which the device has finished while it works on iteration it-1: no stall, and at most
+        // one fully masked iteration is ever issued.
+        auto publish = [&](int64_t state) {
+            const int slot = static_cast<int>(state & 1);
+            BOSP_CUDA(cudaMemcpyAsync(&ws.host_active[slot], ws.s.any_active, sizeof(int),
+                                      cudaMemcpyDeviceToHost, rt.stream()));
+            BOSP_CUDA(cudaEventRecord(ws.ev[slot], rt.stream()));
+        };
+        publish(0);
+        int64_t it = 0;
+        for (; it < max_iter; ++it) {
+            if (it >= 1) {
+                const int slot = static_cast<int>((it - 1) & 1);
+                BOSP_CUDA(cudaEventSynchronize(ws.ev[slot]));
+                if (ws.host_active[slot] == 0) break;
+            }
+            a.apply_device(p, ap);
+            cg_pap(p, ap, ws.s);
+            cg_update(x, r, p, ap, ws.s, tol, mi);
+            publish(it + 1);
+        }
+        out.sweeps = it;
     }
-    out.sweeps = it;
     if (want_stats) {
         std::vector<int> broken(static_cast<size_t>(m)), iters(static_cast<size_t>(m));
         BOSP_CUDA(cudaMemcpyAsync(broken.data(), ws.s.broken, sizeof(int) * m, cudaMemcpyDeviceToHost, rt.stream()));

@@ -3,6 +3,8 @@
 // batched multi-RHS CG.
 #pragma once
 
+#include <map>
+#include <string>
 #include <vector>
 
 #include "api.hpp"
@@ -39,6 +41,20 @@ DevBiorthOutcome dev_mgs_biorth(const DMat& x, const DMat& y, const DMat& p, con
 // ||P^T Q - I||_2 (biorth.cpp:135-143).
 double dev_biorth_residual(const DMat& p, const DMat& q, const InnerProduct& ip);
 
+// One instantiated CUDA graph of a whole batched CG solve: [start] -> while(any active)
+// { A p; p^T A p; x, r update; p update }.  Keyed by everything the recorded launches capture.
+struct CgGraph {
+    const void* op = nullptr;
+    const double *rhs = nullptr, *x = nullptr;
+    int64_t ldr = 0, ldx = 0, m = 0, max_iter = 0;
+    double tol = 0.0;
+    std::string prof_family;  // kernel family timed inside the graph ("" = none)
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    std::map<std::string, int64_t> start_launches, body_launches;
+    std::vector<Runtime::ProfPair> prof_pairs;
+};
+
 // Batched CG workspace (per operator size / width).
 class CgWorkspace {
 public:
@@ -47,6 +63,7 @@ public:
     CgScalars s{};
     int* host_active = nullptr;  // pinned ring
     cudaEvent_t ev[2] = {nullptr, nullptr};
+    std::vector<CgGraph> graphs;
     ~CgWorkspace();
 
 private:

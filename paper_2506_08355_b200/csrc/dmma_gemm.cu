@@ -176,6 +176,20 @@ k_gram(GramParams prm) {
     }
     cp_async_wait<0>();
 
+    if (prm.splits == 1) {  // whole K range in this CTA: write G directly
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+#pragma unroll
+            for (int j = 0; j < NTL; ++j) {
+                const int m = m0 + wm0 + i * 8 + gid;
+                const int nn = n0 + wn0 + j * 8 + 2 * tig;
+                if (m < acols) {
+                    if (nn < bcols) job.g[m + static_cast<int64_t>(nn) * job.ldg] = acc[i][j][0];
+                    if (nn + 1 < bcols) job.g[m + static_cast<int64_t>(nn + 1) * job.ldg] = acc[i][j][1];
+                }
+            }
+        return;
+    }
     // partial tile -> scratch (element (m, n) of the tile at m + n*BM)
     double* part = prm.partial + jb * prm.job_stride +
                    (static_cast<int64_t>(blockIdx.y) * prm.tiles[jb] + tile) * (BM * BN);
@@ -190,32 +204,42 @@ k_gram(GramParams prm) {
         }
 }
 
-// Sum split partials in fixed order: out tile element e of job jb.
-// grid.x over (tile, element block), grid.z = job.
+// Sum split partials in a fixed order.  A block owns 32 consecutive output elements; its 8
+// warps each fold a strided eighth of the splits (two accumulators, loads independent across
+// the unrolled loop), then warp 0 folds the 8 group sums in order.  grid.z = job.
+constexpr int kRedElems = 32, kRedGroups = 8;
+
 template <int BM, int BN>
-__global__ void k_gram_reduce(GramParams prm) {
+__global__ void __launch_bounds__(kRedElems * kRedGroups) k_gram_reduce(GramParams prm) {
+    __shared__ double part_sum[kRedGroups][kRedElems];
     const int jb = blockIdx.z;
     const GramJob& job = prm.job[jb];
-    const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int el = threadIdx.x % kRedElems, grp = threadIdx.x / kRedElems;
+    const int64_t e = static_cast<int64_t>(blockIdx.x) * kRedElems + el;
     const int64_t total = static_cast<int64_t>(prm.tiles[jb]) * BM * BN;
-    if (e >= total) return;
+    double s0 = 0.0, s1 = 0.0;
+    if (e < total) {
+        const double* part = prm.partial + jb * prm.job_stride + e;
+        int sp = grp;
+#pragma unroll 4
+        for (; sp + kRedGroups < prm.splits; sp += 2 * kRedGroups) {
+            s0 += __ldcg(part + sp * total);
+            s1 += __ldcg(part + (sp + kRedGroups) * total);
+        }
+        if (sp < prm.splits) s0 += __ldcg(part + sp * total);
+    }
+    part_sum[grp][el] = s0 + s1;
+    __syncthreads();
+    if (grp != 0 || e >= total) return;
+    double s = 0.0;
+#pragma unroll
+    for (int g = 0; g < kRedGroups; ++g) s += part_sum[g][el];
     const int tile = static_cast<int>(e / (BM * BN));
     const int r = static_cast<int>(e % (BM * BN));
     const int m = (tile / prm.tiles_n[jb]) * BM + r % BM;
     const int nn = (tile % prm.tiles_n[jb]) * BN + r / BM;
     if (m >= job.a.cols() || nn >= job.b.cols()) return;
-    const double* part = prm.partial + jb * prm.job_stride + e;
-    const int64_t stride = total;
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-    int sp = 0;
-    for (; sp + 4 <= prm.splits; sp += 4) {
-        s0 += part[(sp + 0) * stride];
-        s1 += part[(sp + 1) * stride];
-        s2 += part[(sp + 2) * stride];
-        s3 += part[(sp + 3) * stride];
-    }
-    for (; sp < prm.splits; ++sp) s0 += part[sp * stride];
-    job.g[m + nn * job.ldg] = (s0 + s1) + (s2 + s3);
+    job.g[m + nn * job.ldg] = s;
 }
 
 template <int BM, int BN, int WM, int WN>
@@ -257,11 +281,11 @@ void launch_gram(const GramJob* jobs, int njobs, int64_t n) {
         k_gram<BM, BN, WM, WN><<<grid, NT, smem, rt.stream()>>>(prm);
         BOSP_LAUNCH_CHECK();
     }
-    {
+    if (prm.splits > 1) {
         LaunchScope ls("gram_reduce");
         const int64_t total = static_cast<int64_t>(max_tiles) * BM * BN;
-        dim3 grid(static_cast<unsigned>((total + 255) / 256), 1, njobs);
-        k_gram_reduce<BM, BN><<<grid, 256, 0, rt.stream()>>>(prm);
+        dim3 grid(static_cast<unsigned>((total + kRedElems - 1) / kRedElems), 1, njobs);
+        k_gram_reduce<BM, BN><<<grid, kRedElems * kRedGroups, 0, rt.stream()>>>(prm);
         BOSP_LAUNCH_CHECK();
     }
 }
@@ -411,6 +435,169 @@ void launch_product(const ProductJob* jobs, int njobs, int64_t n) {
     BOSP_LAUNCH_CHECK();
 }
 
+// ------------------------------------------------------------------------------------------
+// Skinny product: k <= 64 and b <= 64 (the Ritz pullbacks, Step-5 P~/Q~, biorth_against and
+// MGS applications at the configs' widths).  HBM-bound: A streams once.  Each CTA keeps the
+// whole C (k x BN) in shared memory and walks row tiles of 128 rows (grid-stride, persistent),
+// double-buffering the next A tile with cp.async while the DMMA pipe works on the current one.
+// BN is b rounded up to 8 so no tensor work is spent on padding columns.
+// ------------------------------------------------------------------------------------------
+constexpr int kSkBM = 128;
+constexpr int kSkLdM = kSkBM + 4;
+
+struct SkinnyParams {
+    ProductJob job[4];
+    int64_t n;
+    int64_t tiles;
+    int kp;     // k rounded up to 4 (max over jobs)
+    int ldc;    // smem ld of C (== 4 mod 16)
+};
+
+template <int BN>
+__global__ void __launch_bounds__(256) k_product_skinny(SkinnyParams prm) {
+    constexpr int NT = BN / 8;
+    extern __shared__ __align__(16) double smem[];
+    const int kp = prm.kp, ldc = prm.ldc;
+    double* sc = smem;                                // [BN][ldc]
+    double* sa = smem + BN * ldc;                     // [2][kp][kSkLdM]
+    const ProductJob& job = prm.job[blockIdx.z];
+    const int kcols = job.a.cols();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int gid = lane >> 2, tig = lane & 3;
+
+    // C -> shared (zero-padded to kp x BN)
+    {
+        ColList cl;
+        cl.p[0] = job.c;
+        cl.ld[0] = job.ldc;
+        cl.start[1] = job.ncols;
+        cl.nseg = 1;
+        for (int i = 2; i <= kMaxSeg; ++i) cl.start[i] = job.ncols;
+        const int chunks = BN * (kp / 2);
+        for (int ch = threadIdx.x; ch < chunks; ch += 256) {
+            const int c = ch / (kp / 2), k2 = 2 * (ch % (kp / 2));
+            int bytes = 0;
+            const double* src = job.c;
+            if (c < job.ncols && k2 < kcols) {
+                bytes = (kcols - k2) >= 2 ? 16 : 8;
+                src = colptr(cl, c) + k2;
+            }
+            cp_async16(sc + c * ldc + k2, src, bytes);
+        }
+    }
+    auto load_a = [&](int buf, int64_t tile) {
+        double* dst = sa + buf * kp * kSkLdM;
+        const int64_t m0 = tile * kSkBM;
+        const int chunks = kp * (kSkBM / 2);
+        for (int ch = threadIdx.x; ch < chunks; ch += 256) {
+            const int kk = ch / (kSkBM / 2), m2 = 2 * (ch % (kSkBM / 2));
+            const int64_t m = m0 + m2;
+            int bytes = 0;
+            const double* src = job.c;
+            if (kk < kcols && m < prm.n) {
+                bytes = (prm.n - m) >= 2 ? 16 : 8;
+                src = colptr(job.a, kk) + m;
+            }
+            cp_async16(dst + kk * kSkLdM + m2, src, bytes);
+        }
+    };
+    int64_t tile = blockIdx.x;
+    if (tile < prm.tiles) load_a(0, tile);
+    cp_async_commit();
+    int buf = 0;
+    for (; tile < prm.tiles; tile += gridDim.x, buf ^= 1) {
+        const int64_t next = tile + gridDim.x;
+        if (next < prm.tiles) load_a(buf ^ 1, next);
+        cp_async_commit();
+        cp_async_wait<1>();
+        __syncthreads();
+        const double* a = sa + buf * kp * kSkLdM;
+        const int wm0 = warp * 16;
+        const double alpha = job.alpha, beta = job.beta;
+        const int64_t r0 = tile * kSkBM + wm0 + gid;
+        // beta != 0: issue the loads of Out now so their latency hides under the DMMA loop
+        double old[2][NT][2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < NT; ++j)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int64_t row = r0 + i * 8;
+                    const int col = j * 8 + 2 * tig + h;
+                    old[i][j][h] = (beta != 0.0 && row < prm.n && col < job.ncols)
+                                       ? __ldcs(job.out + static_cast<int64_t>(col) * job.ldo + row)
+                                       : 0.0;
+                }
+        double acc[2][NT][2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        for (int kk = 0; kk < kp; kk += 4) {
+            double af[2], bf[NT];
+#pragma unroll
+            for (int i = 0; i < 2; ++i) af[i] = a[(kk + tig) * kSkLdM + wm0 + i * 8 + gid];
+#pragma unroll
+            for (int j = 0; j < NT; ++j) bf[j] = sc[(j * 8 + gid) * ldc + kk + tig];
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+                for (int j = 0; j < NT; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const int64_t row = r0 + i * 8;
+            if (row >= prm.n) continue;
+#pragma unroll
+            for (int j = 0; j < NT; ++j)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int col = j * 8 + 2 * tig + h;
+                    if (col < job.ncols) {
+                        const double v = alpha * acc[i][j][h];
+                        __stcs(job.out + static_cast<int64_t>(col) * job.ldo + row,
+                               beta == 0.0 ? v : v + beta * old[i][j][h]);
+                    }
+                }
+        }
+        __syncthreads();  // everyone is done with `buf` before it is refilled
+    }
+    cp_async_wait<0>();
+}
+
+template <int BN>
+void launch_skinny(const ProductJob* jobs, int njobs, int64_t n) {
+    Runtime& rt = Runtime::get();
+    SkinnyParams prm{};
+    int kmax = 0;
+    double flops = 0, bytes = 0;
+    for (int j = 0; j < njobs; ++j) {
+        prm.job[j] = jobs[j];
+        kmax = std::max(kmax, jobs[j].a.cols());
+        const double k = jobs[j].a.cols(), b = jobs[j].ncols;
+        flops += 2.0 * n * k * b;
+        bytes += 8.0 * n * (k + b * (jobs[j].beta != 0.0 ? 2.0 : 1.0));
+    }
+    prm.n = n;
+    prm.tiles = (n + kSkBM - 1) / kSkBM;
+    prm.kp = std::max(4, (kmax + 3) / 4 * 4);
+    prm.ldc = (prm.kp + 15) / 16 * 16 + 4;
+    const size_t smem = sizeof(double) * (static_cast<size_t>(BN) * prm.ldc + 2ull * prm.kp * kSkLdM);
+    static int attr_set = 0;
+    if (attr_set < static_cast<int>(smem)) {
+        BOSP_CUDA(cudaFuncSetAttribute(k_product_skinny<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr_set = 200 * 1024;
+    }
+    int per_sm = 1;
+    BOSP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_product_skinny<BN>, 256, smem));
+    const int64_t ctas = std::max<int64_t>(1, std::min<int64_t>(prm.tiles, int64_t(std::max(per_sm, 1)) * rt.sm_count()));
+    LaunchScope ls("product", bytes, flops);
+    dim3 grid(static_cast<unsigned>(ctas), 1, njobs);
+    k_product_skinny<BN><<<grid, 256, smem, rt.stream()>>>(prm);
+    BOSP_LAUNCH_CHECK();
+}
+
 void check_aligned(const ColList& cl) {
     for (int s = 0; s < cl.nseg; ++s)
         if ((reinterpret_cast<uintptr_t>(cl.p[s]) & 15) || (cl.ld[s] & 1))
@@ -452,6 +639,20 @@ void product(const ProductJob* jobs, int njobs, int64_t n) {
         bmax = std::max(bmax, jobs[j].ncols);
     }
     if (n == 0 || bmax == 0) return;
+    int kmax = 0;
+    for (int j = 0; j < njobs; ++j) kmax = std::max(kmax, jobs[j].a.cols());
+    if (kmax <= 64 && bmax <= 64 && kmax > 0) {
+        switch ((bmax + 7) / 8) {
+            case 1: return launch_skinny<8>(jobs, njobs, n);
+            case 2: return launch_skinny<16>(jobs, njobs, n);
+            case 3: return launch_skinny<24>(jobs, njobs, n);
+            case 4: return launch_skinny<32>(jobs, njobs, n);
+            case 5: return launch_skinny<40>(jobs, njobs, n);
+            case 6: return launch_skinny<48>(jobs, njobs, n);
+            case 7: return launch_skinny<56>(jobs, njobs, n);
+            default: return launch_skinny<64>(jobs, njobs, n);
+        }
+    }
     // k == 0: Out = beta * Out (handled by the kernel with an empty K loop)
     if (bmax <= 32)
         launch_product<64, 32, 2, 2>(jobs, njobs, n);

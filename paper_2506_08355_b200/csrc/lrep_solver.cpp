@@ -19,11 +19,41 @@
 #include "api.hpp"
 #include "dev_algos.hpp"
 #include "operators.hpp"
+#include "rng.hpp"
 
 namespace bosp {
 inline namespace b200 {
 
+// Wall-time attribution per solver phase (BOSP_PHASES=1 synchronises at each phase end so GPU
+// time lands in the phase that issued it; printed at the end of solve()).
+enum Phase { PH_INIT, PH_RITZ, PH_SMALL, PH_RESID, PH_STEP5, PH_CG, PH_AGAINST, PH_MGS, PH_STEP7,
+             PH_SAMPLE, PH_REPAIR, PH_ASSEMBLE, PH_COUNT };
+static const char* kPhaseNames[PH_COUNT] = {"init", "ritz(apply+gram+pullback)", "host small solve",
+                                            "residuals", "step5", "cg", "biorth_against", "mgs_biorth",
+                                            "step7", "sample_invariants", "repair", "assemble"};
+
+bool phases_enabled() {
+    static const bool on = std::getenv("BOSP_PHASES") != nullptr;
+    return on;
+}
+
+struct PhaseClock {
+    double acc[PH_COUNT] = {};
+    struct Scope {
+        PhaseClock* pc;
+        Phase ph;
+        std::chrono::steady_clock::time_point t0;
+        Scope(PhaseClock* p, Phase h) : pc(p), ph(h), t0(std::chrono::steady_clock::now()) {}
+        ~Scope() {
+            if (phases_enabled()) Runtime::get().sync();
+            pc->acc[ph] += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        }
+    };
+    Scope scope(Phase p) { return Scope(this, p); }
+};
+
 struct DeviceState {
+    PhaseClock phases;
     int64_t n = 0;
     DBlock U, V;                  // [X | P | W], [Y | Q | Z]
     int64_t wx = 0, wp = 0, ww = 0;
@@ -173,8 +203,11 @@ RitzOut ritz_step(DeviceState& st, const LinearOperator& k, const LinearOperator
     std::copy(both.data() + d * d, both.data() + 2 * d * d, mhat.data());
 
     const auto t0 = Clock::now();
-    ProjectedLrep proj = finish_assembly(khat, mhat);  // NullspaceLeak propagates
-    ro.sol = solve_small_lrep(proj, wxa);
+    {
+        auto ph = st.phases.scope(PH_SMALL);
+        ProjectedLrep proj = finish_assembly(khat, mhat);  // NullspaceLeak propagates
+        ro.sol = solve_small_lrep(proj, wxa);
+    }
     st.stats.host_small_seconds += secs(t0, Clock::now());
 
     ensure_block(st.small, d, 2 * wxa);
@@ -233,38 +266,8 @@ SolverState initialize(const LinearOperator& k, const LinearOperator& m, const I
     // Steps 1-2: the reference's RNG stream (mt19937_64, U[-1,1], fill order x,p,w,y,q,z --
     // bosp_solver.cpp:144-150) so both solvers start from the same vectors.
     DBlock u(n, cap), v(n, cap);
-    {
-        std::mt19937_64 rng(cfg.rng_seed);
-        std::uniform_real_distribution<double> dist(-1.0, 1.0);
-        Runtime& rt = Runtime::get();
-        const int64_t widths[6] = {wx, wp, ww, wx, wp, ww};
-        const int64_t offs[6] = {0, wx, wx + wp, 0, wx, wx + wp};
-        double* stage[2] = {nullptr, nullptr};
-        cudaEvent_t done[2];
-        for (int i = 0; i < 2; ++i) {
-            BOSP_CUDA(cudaMallocHost(&stage[i], sizeof(double) * n));
-            BOSP_CUDA(cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming));
-            BOSP_CUDA(cudaEventRecord(done[i], rt.stream()));
-        }
-        int64_t col = 0;
-        for (int b = 0; b < 6; ++b) {
-            DBlock& dst = b < 3 ? u : v;
-            for (int64_t j = 0; j < widths[b]; ++j, ++col) {
-                const int s = static_cast<int>(col & 1);
-                BOSP_CUDA(cudaEventSynchronize(done[s]));
-                for (int64_t i = 0; i < n; ++i) stage[s][i] = dist(rng);
-                BOSP_CUDA(cudaMemcpyAsync(dst.data() + (offs[b] + j) * dst.ld(), stage[s], sizeof(double) * n,
-                                          cudaMemcpyHostToDevice, rt.stream()));
-                BOSP_CUDA(cudaEventRecord(done[s], rt.stream()));
-            }
-        }
-        rt.sync();
-        for (int i = 0; i < 2; ++i) {
-            cudaFreeHost(stage[i]);
-            cudaEventDestroy(done[i]);
-        }
-    }
     const DMat ua = u.cols(0, d), va = v.cols(0, d);
+    mt_fill_uv(cfg.rng_seed, ua, va);  // the exact x,p,w,y,q,z stream, generated in HBM
     dev_biorth_against(deflation_bases(st), ua, va, ip);
     st.U = DBlock(n, cap);
     st.V = DBlock(n, cap);
@@ -292,6 +295,7 @@ bool iterate_once(SolverState& ss, const LinearOperator& k, const LinearOperator
     st.stats.max_width_u = std::max(st.stats.max_width_u, wxa + st.wp + st.ww);
     RitzOut ro;
     try {
+        auto ph = st.phases.scope(PH_RITZ);
         ro = ritz_step(st, k, m, wxa);
     } catch (const NullspaceLeak&) {
         if (st.leak_recovered) throw NumericalAbort("bosp: projected blocks lost positive definiteness twice");
@@ -417,6 +421,7 @@ bool iterate_once(SolverState& ss, const LinearOperator& k, const LinearOperator
                 }
                 rhs_z = st.tmp.view();
             }
+            auto phz = st.phases.scope(PH_CG);
             DevCgOutcome cz = dev_cg(m, rhs_z, st.zg.view(), cfg.inner_cg_tol, cfg.inner_cg_max_iter, st.cg);
             st.stats.cg_iterations += cz.sweeps;
             // rhs_w = rw + lam B Z; W = CG(K, rhs_w)
@@ -429,16 +434,21 @@ bool iterate_once(SolverState& ss, const LinearOperator& k, const LinearOperator
             } else {
                 lam_axpy(st.zg.view(), lamb, st.tmp.view());
             }
+            auto phw = st.phases.scope(PH_CG);
             DevCgOutcome cw = dev_cg(k, st.tmp.view(), st.wg.view(), cfg.inner_cg_tol, cfg.inner_cg_max_iter, st.cg);
             st.stats.cg_iterations += cw.sweeps;
         }
         std::vector<DevBasis> bases = deflation_bases(st);
         bases.push_back({st.X(), st.Y()});
         if (kp > 0) bases.push_back({st.pt.view(), st.qt.view()});
-        dev_biorth_against(bases, st.wg.view(), st.zg.view(), ip);
+        {
+            auto ph = st.phases.scope(PH_AGAINST);
+            dev_biorth_against(bases, st.wg.view(), st.zg.view(), ip);
+        }
         // MGS into the W/Z slots of U/V right after the new P/Q (old P/W are dead here)
         ensure_block(st.rz, n, nb_eff);
         ensure_block(st.rw, n, nb_eff);
+        auto phm = st.phases.scope(PH_MGS);
         DevBiorthOutcome wz = dev_mgs_biorth(st.wg.view(), st.zg.view(), st.rz.view(), st.rw.view(), ip);
         kw = wz.kept;
     }
@@ -482,13 +492,20 @@ bool iterate_once(SolverState& ss, const LinearOperator& k, const LinearOperator
     }
 
     // invariant sampling doubles as the drift monitor (:429-432)
-    const double dev = sample_invariants(st, ip);
+    double dev;
+    {
+        auto ph = st.phases.scope(PH_SAMPLE);
+        dev = sample_invariants(st, ip);
+    }
     if (debug_enabled())
         std::fprintf(stderr, "[bosp] it=%lld wx=%lld wp=%lld ww=%lld frozen=%lld locked=%lld nev_conv=%lld "
                      "nb_eff=%lld c0=%lld dev=%.3e\n", (long long)st.iter, (long long)st.wx, (long long)st.wp,
                      (long long)st.ww, (long long)st.frozen, (long long)st.locked_count(),
                      (long long)st.nev_conv, (long long)nb_eff, (long long)c0, dev);
-    if (dev > 5e-11) rebiorthogonalize_state(st, ip);
+    if (dev > 5e-11) {
+        auto ph = st.phases.scope(PH_REPAIR);
+        rebiorthogonalize_state(st, ip);
+    }
     return false;
 }
 
@@ -583,7 +600,10 @@ EigenResult solve(const LinearOperator& k, const LinearOperator& m, const InnerP
     BOSP_CUDA(cudaEventRecord(ev0, rt.stream()));
     GeneralizedNullspace nullspace =
         ns ? std::move(*ns) : compute_nullspace(k, m, cfg.rank_hint, cfg.tol_null, ip, cfg.rng_seed + 1);
+    const auto ti = Clock::now();
     SolverState st = initialize(k, m, ip, nullspace, cfg);
+    if (phases_enabled()) rt.sync();
+    st.dev().phases.acc[PH_INIT] += secs(ti, Clock::now());
     bool converged = false;
     while (st.iter() < cfg.max_outer_iter) {
         if (iterate_once(st, k, m, ip, nullspace, cfg)) {
@@ -591,7 +611,14 @@ EigenResult solve(const LinearOperator& k, const LinearOperator& m, const InnerP
             break;
         }
     }
+    const auto ta = Clock::now();
     EigenResult res = assemble_result(st.dev(), k, m, ip, cfg, converged);
+    st.dev().phases.acc[PH_ASSEMBLE] += secs(ta, Clock::now());
+    if (phases_enabled()) {
+        std::fprintf(stderr, "[bosp] phase wall times (s), %lld iterations:\n", (long long)st.iter());
+        for (int i = 0; i < PH_COUNT; ++i)
+            std::fprintf(stderr, "[bosp]   %-28s %9.4f\n", kPhaseNames[i], st.dev().phases.acc[i]);
+    }
     BOSP_CUDA(cudaEventRecord(ev1, rt.stream()));
     rt.sync();
     res.stats.wall_seconds = secs(t0, Clock::now());

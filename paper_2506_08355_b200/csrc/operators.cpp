@@ -81,19 +81,23 @@ struct DevFree {
     ~DevFree() { Runtime::get().free(p); }
 };
 
+// Dense operator.  A^T is stored (transposed once on the device at construction), so
+// y = A x = (A^T)^T x is a tall-skinny Gram over the long dimension: split-K DMMA tiles keep
+// every SM streaming A even when n is small (config 1) and A is read once per apply.
 class DenseOp final : public OperatorImpl {
 public:
-    DenseOp(const double* a, int64_t n) : OperatorImpl(n, LinearOperator::Kind::dense), m_(n, n) {
-        to_device(a, n, n, n, m_.view());
+    DenseOp(const double* a, int64_t n) : OperatorImpl(n, LinearOperator::Kind::dense), t_(n, n) {
+        DBlock staged(n, n);
+        to_device(a, n, n, n, staged.view());
+        transpose(staged.view(), t_.view());
+        Runtime::get().sync();
     }
     void apply(const DMat& x, const DMat& y) const override {
-        // y = A x as a DMMA product with A streamed once per column tile
-        product(ColList(m_.view()), x.p, x.ld, static_cast<int32_t>(x.cols), y, 1.0, 0.0);
+        gram(ColList(t_.view()), ColList(x), x.rows, y.p, y.ld);
     }
-    const DBlock& matrix() const { return m_; }
 
 private:
-    DBlock m_;
+    DBlock t_;
 };
 
 class CsrOp final : public OperatorImpl {
@@ -208,6 +212,7 @@ public:
         base_->apply(x, y);
         axpby(sigma_, x, 1.0, y);  // y += sigma x (linear_operator.cpp:81-92)
     }
+    bool capturable() const override { return base_->capturable(); }
 
 private:
     std::shared_ptr<const OperatorImpl> base_;
@@ -225,6 +230,7 @@ public:
         to_device(hy.data(), x.rows, x.cols, x.rows, y);
         Runtime::get().sync();
     }
+    bool capturable() const override { return false; }
 
 private:
     LinearOperator::ApplyFn fn_;
@@ -237,6 +243,7 @@ public:
     void apply(const DMat& x, const DMat& y) const override {
         fn_(x.p, x.ld, y.p, y.ld, x.cols, Runtime::get().stream());
     }
+    bool capturable() const override { return false; }
 
 private:
     LinearOperator::DeviceApplyFn fn_;

@@ -16,6 +16,9 @@ public:
     virtual void apply(const DMat& x, const DMat& y) const = 0;
     int64_t dim() const { return n_; }
     LinearOperator::Kind kind() const { return kind_; }
+    // Whether apply() only enqueues device work on the solver stream (so it can be recorded
+    // into a CUDA graph); host callbacks cannot.
+    virtual bool capturable() const { return true; }
 
 private:
     int64_t n_;

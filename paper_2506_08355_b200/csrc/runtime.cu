@@ -82,13 +82,26 @@ double* Runtime::pinned(size_t doubles) {
 }
 
 void Runtime::count_launch(const char* family) {
+    if (capture_sink_) {
+        ++(*capture_sink_)[family];
+        return;
+    }
     ++launches_;
     ++family_launches_[family];
+}
+
+void Runtime::add_launches(const std::map<std::string, int64_t>& fam, int64_t times) {
+    for (const auto& kv : fam) {
+        launches_ += kv.second * times;
+        family_launches_[kv.first] += kv.second * times;
+    }
 }
 
 void Runtime::prof_enable(const std::string& family) {
     prof_family_ = family;
     prof_events_.clear();
+    timer_pending_.clear();
+    graph_samples_ = ProfReport{0, 0.0, 0.0, 0.0};
 }
 
 bool Runtime::prof_on(const char* family) const {
@@ -108,6 +121,7 @@ cudaEvent_t Runtime::take_event() {
 
 void Runtime::prof_begin(const char* family, double bytes, double flops) {
     (void)family;
+    if (capture_prof_) return;  // inside a graph only device-clock timers are possible
     Ev ev{take_event(), take_event(), bytes, flops};
     BOSP_CUDA(cudaEventRecord(ev.a, stream_));
     prof_events_.push_back(ev);
@@ -115,12 +129,50 @@ void Runtime::prof_begin(const char* family, double bytes, double flops) {
 
 void Runtime::prof_end(const char* family) {
     (void)family;
+    if (capture_prof_) return;
     BOSP_CUDA(cudaEventRecord(prof_events_.back().b, stream_));
+}
+
+unsigned long long* Runtime::timer_begin(const char* family, double bytes, double flops) {
+    if (!prof_on(family)) return nullptr;
+    if (!timer_slots_) {
+        BOSP_CUDA(cudaMalloc(&timer_slots_, sizeof(unsigned long long) * 2 * kTimerSlots));
+    }
+    const int64_t slot = timer_next_++ % kTimerSlots;
+    unsigned long long* p = timer_slots_ + 2 * slot;
+    BOSP_CUDA(cudaMemsetAsync(p, 0, 2 * sizeof(unsigned long long), stream_));
+    ProfPair pp{slot, bytes, flops};
+    if (capture_prof_) capture_prof_->push_back(pp);
+    else timer_pending_.push_back(pp);
+    return p;
+}
+
+void Runtime::read_timer_samples(const std::vector<ProfPair>& pairs) {
+    if (pairs.empty()) return;
+    std::vector<unsigned long long> host(2 * kTimerSlots);
+    BOSP_CUDA(cudaMemcpy(host.data(), timer_slots_, sizeof(unsigned long long) * 2 * kTimerSlots,
+                         cudaMemcpyDeviceToHost));
+    for (const ProfPair& p : pairs) {
+        const unsigned long long s = ~host[2 * p.slot], e = host[2 * p.slot + 1];
+        if (host[2 * p.slot] == 0 || e == 0 || e < s) continue;
+        graph_samples_.launches += 1;
+        graph_samples_.ms += (e - s) * 1e-6;
+        graph_samples_.bytes += p.bytes;
+        graph_samples_.flops += p.flops;
+    }
+}
+
+void Runtime::add_prof_samples(const std::vector<ProfPair>& pairs) {
+    sync();
+    read_timer_samples(pairs);
 }
 
 Runtime::ProfReport Runtime::prof_collect() {
     sync();
-    ProfReport r{0, 0.0, 0.0, 0.0};
+    read_timer_samples(timer_pending_);
+    timer_pending_.clear();
+    ProfReport r = graph_samples_;
+    graph_samples_ = ProfReport{0, 0.0, 0.0, 0.0};
     for (auto& e : prof_events_) {
         float ms = 0.f;
         BOSP_CUDA(cudaEventElapsedTime(&ms, e.a, e.b));
@@ -135,10 +187,10 @@ Runtime::ProfReport Runtime::prof_collect() {
     return r;
 }
 
-LaunchScope::LaunchScope(const char* fam, double bytes, double flops) : family(fam) {
+LaunchScope::LaunchScope(const char* fam, double bytes, double flops, bool events) : family(fam) {
     Runtime& rt = Runtime::get();
     rt.count_launch(fam);
-    timed = rt.prof_on(fam);
+    timed = events && rt.prof_on(fam);
     if (timed) rt.prof_begin(fam, bytes, flops);
 }
 

@@ -40,12 +40,27 @@ public:
     void reset_launches() { launches_ = 0; family_launches_.clear(); }
     const std::map<std::string, int64_t>& family_launches() const { return family_launches_; }
 
+    // Launches issued while a stream capture is recorded are tallied into `sink` (per family)
+    // instead of the live counters; graph replays add them back per execution.
+    void set_capture_sink(std::map<std::string, int64_t>* sink) { capture_sink_ = sink; }
+    void add_launches(const std::map<std::string, int64_t>& fam, int64_t times);
+
     void prof_enable(const std::string& family);  // "" disables
     bool prof_on(const char* family) const;
+    bool prof_active() const { return !prof_family_.empty(); }
     void prof_begin(const char* family, double algo_bytes, double algo_flops);
     void prof_end(const char* family);
     struct ProfReport { int64_t launches; double ms; double bytes; double flops; };
     ProfReport prof_collect();  // synchronises, sums elapsed times, resets
+    // Device-clock timing for kernels that may run inside CUDA graphs (event nodes are not
+    // allowed in conditional bodies): the kernel writes (max of ~start, max of end) %globaltimer
+    // into a 2-word slot that a memset resets before each launch.  A launch recorded into a
+    // graph keeps its slot; after each replay the slot holds that launch's last execution.
+    struct ProfPair { int64_t slot; double bytes, flops; };
+    unsigned long long* timer_begin(const char* family, double bytes, double flops);
+    void set_capture_prof(std::vector<ProfPair>* sink) { capture_prof_ = sink; }
+    void add_prof_samples(const std::vector<ProfPair>& pairs);  // after the replay finished
+    const std::string& prof_family() const { return prof_family_; }
 
 private:
     Runtime();
@@ -61,9 +76,17 @@ private:
     size_t pinned_cap_ = 0;
     int64_t launches_ = 0;
     std::map<std::string, int64_t> family_launches_;
+    std::map<std::string, int64_t>* capture_sink_ = nullptr;
     std::string prof_family_;
     struct Ev { cudaEvent_t a, b; double bytes, flops; };
     std::vector<Ev> prof_events_;
+    std::vector<ProfPair>* capture_prof_ = nullptr;
+    std::vector<ProfPair> timer_pending_;
+    unsigned long long* timer_slots_ = nullptr;
+    int64_t timer_next_ = 0;
+    static constexpr int64_t kTimerSlots = 1 << 15;
+    ProfReport graph_samples_{0, 0.0, 0.0, 0.0};
+    void read_timer_samples(const std::vector<ProfPair>& pairs);
     std::vector<cudaEvent_t> event_pool_;
     cudaEvent_t take_event();
 };
@@ -72,7 +95,8 @@ private:
 struct LaunchScope {
     const char* family;
     bool timed;
-    LaunchScope(const char* fam, double bytes = 0.0, double flops = 0.0);
+    // events = false: the kernel times itself with a device-clock slot (Runtime::timer_begin)
+    LaunchScope(const char* fam, double bytes = 0.0, double flops = 0.0, bool events = true);
     ~LaunchScope();
 };
 

@@ -167,6 +167,8 @@ struct CgStartF {
         int c = 0;
         for (int j = 0; j < ncols; ++j) c += s.active[j];
         *s.any_active = c;
+        *s.loops = 0;
+        if (s.has_cond) cudaGraphSetConditional(s.cond, c > 0 ? 1u : 0u);
     }
 };
 
@@ -197,6 +199,8 @@ struct CgStartX0F {
         int c = 0;
         for (int j = 0; j < ncols; ++j) c += s.active[j];
         *s.any_active = c;
+        *s.loops = 0;
+        if (s.has_cond) cudaGraphSetConditional(s.cond, c > 0 ? 1u : 0u);
     }
 };
 
@@ -246,6 +250,8 @@ struct CgXrF {
         int c = 0;
         for (int j = 0; j < ncols; ++j) c += s.active[j];
         *s.any_active = c;
+        *s.loops += 1;
+        if (s.has_cond) cudaGraphSetConditional(s.cond, c > 0 ? 1u : 0u);
     }
 };
 
@@ -300,7 +306,31 @@ struct CgDirF {  // p = r + beta p for still-active columns (cg.cpp:49)
     __device__ void operator()(int64_t i, int j) const { p[i + j * lp] = r[i + j * lr] + beta[j] * p[i + j * lp]; }
 };
 
+__global__ void k_transpose(const double* __restrict__ a, int64_t lda, int64_t rows, int64_t cols,
+                            double* __restrict__ t, int64_t ldt) {
+    __shared__ double tile[32][33];
+    const int64_t r0 = static_cast<int64_t>(blockIdx.x) * 32, c0 = static_cast<int64_t>(blockIdx.y) * 32;
+    for (int j = threadIdx.y; j < 32; j += 8) {
+        const int64_t r = r0 + threadIdx.x, c = c0 + j;
+        if (r < rows && c < cols) tile[j][threadIdx.x] = a[c * lda + r];
+    }
+    __syncthreads();
+    for (int j = threadIdx.y; j < 32; j += 8) {
+        const int64_t c = c0 + threadIdx.x, r = r0 + j;  // t(c, r) = a(r, c)
+        if (r < rows && c < cols) t[r * ldt + c] = tile[threadIdx.x][j];
+    }
+}
+
 }  // namespace
+
+void transpose(const DMat& a, const DMat& t) {
+    if (a.rows == 0 || a.cols == 0) return;
+    Runtime& rt = Runtime::get();
+    LaunchScope ls("transpose", 16.0 * a.rows * a.cols, 0.0);
+    dim3 grid(static_cast<unsigned>((a.rows + 31) / 32), static_cast<unsigned>((a.cols + 31) / 32));
+    k_transpose<<<grid, dim3(32, 8), 0, rt.stream()>>>(a.p, a.ld, a.rows, a.cols, t.p, t.ld);
+    BOSP_LAUNCH_CHECK();
+}
 
 void col_dots(const DMat& x, const DMat& y, double* out) {
     DotF f;

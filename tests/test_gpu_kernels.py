@@ -201,6 +201,18 @@ def test_weighted_inner_product():
     assert np.abs(p.T @ (d[:, None] * q) - np.eye(3)).max() < 1e-12
 
 
+def test_seed_blocks_bit_exact_reference_stream(golden_small):
+    """Device MT19937-64 fill == the reference's fill_uniform stream (x,p,w,y,q,z order)."""
+    n, d = 100, 10  # 2 * 100 * 10 = 2000 draws = golden rng_seed0
+    u, v = bosp.seed_blocks(0, n, d)
+    stream = np.concatenate([u.T.reshape(-1), v.T.reshape(-1)])
+    assert np.array_equal(stream, golden_small["rng_seed0"])
+    # longer stream against the oracle restatement (crosses many 312-word twists)
+    u, v = bosp.seed_blocks(12345, 4099, 3)
+    ref = O.MT19937_64(12345).uniform(2 * 4099 * 3)
+    assert np.array_equal(np.concatenate([u.T.reshape(-1), v.T.reshape(-1)]), ref)
+
+
 def test_shape_errors_map_to_contract_violation():
     with pytest.raises(bosp.ContractViolation):
         bosp.block_inner(None, np.ones((5, 2)), np.ones((4, 2)))
