@@ -196,6 +196,9 @@ bosp_status bosp_bench_apply(bosp_op op, int64_t ncols, int64_t reps, double* ms
 /* Microbenchmark of the tall-skinny kernels on device-resident random data: kind 0 = Gram
  * (n x a)^T (n x b), 1 = product (n x a)(a x b), 2 = axpy; mean ms per call over `reps`. */
 bosp_status bosp_bench_blas(int32_t kind, int64_t n, int64_t a, int64_t b, int64_t reps, double* ms);
+/* Microbenchmark of the batched CG: `iters` iterations (tol 0, so every column runs all of
+ * them) on a random n x ncols right-hand side; mean ms per CG iteration over `reps` solves. */
+bosp_status bosp_bench_cg(bosp_op op, int64_t ncols, int64_t iters, int64_t reps, double* ms);
 /* Kernel launches issued by this library since the last reset. */
 int64_t bosp_launch_count(void);
 void bosp_launch_reset(void);

@@ -78,7 +78,7 @@ EXPORTED = [
     "bosp_cholesky", "bosp_profile_enable", "bosp_profile_collect", "bosp_launch_count",
     "bosp_launch_reset", "bosp_launch_families", "bosp_device_sync", "bosp_host_alloc",
     "bosp_host_free", "bosp_set_device", "bosp_flush_l2", "bosp_seed_blocks",
-    "bosp_bench_apply", "bosp_bench_blas",
+    "bosp_bench_apply", "bosp_bench_blas", "bosp_bench_cg",
 ]
 
 

@@ -442,6 +442,13 @@ def bench_apply(op, ncols, reps=20):
     return ms.value
 
 
+def bench_cg(op, ncols, iters=20, reps=5):
+    """Mean ms per batched-CG iteration (all columns active)."""
+    ms = C.c_double()
+    check(lib().bosp_bench_cg(op._h, C.c_int64(ncols), C.c_int64(iters), C.c_int64(reps), C.byref(ms)))
+    return ms.value
+
+
 def bench_blas(kind, n, a, b, reps=20):
     """kind: 'gram' | 'product' | 'axpy' -> mean ms per call on device-resident data."""
     k = {"gram": 0, "product": 1, "axpy": 2}[kind]

@@ -7,6 +7,7 @@
 
 #include "api.hpp"
 #include "dense_ops.hpp"
+#include "dev_algos.hpp"
 #include "operators.hpp"
 #include "rng.hpp"
 #include "runtime.hpp"
@@ -486,6 +487,17 @@ bosp_status bosp_bench_apply(bosp_op op, int64_t ncols, int64_t reps, double* ms
         bosp::DBlock x(n, ncols), y(n, ncols);
         fill_random(x.view(), 1);
         *ms = time_reps(reps, [&] { op->op.apply_device(x.view(), y.view()); });
+    });
+}
+
+bosp_status bosp_bench_cg(bosp_op op, int64_t ncols, int64_t iters, int64_t reps, double* ms) {
+    return guarded([&] {
+        const int64_t n = op->op.dim();
+        bosp::DBlock b(n, ncols), x(n, ncols);
+        fill_random(b.view(), 7);
+        bosp::CgWorkspace ws;
+        *ms = time_reps(reps, [&] { bosp::dev_cg(op->op, b.view(), x.view(), 0.0, iters, ws); }) /
+              static_cast<double>(std::max<int64_t>(iters, 1));
     });
 }
 

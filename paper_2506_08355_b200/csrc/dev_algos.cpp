@@ -238,6 +238,13 @@ void CgWorkspace::ensure(int64_t n, int64_t m) {
         s.any_active = iv + 3 * m;
         s.loops = iv + 3 * m + 1;
     }
+    if (!parts_) {  // [pap partials | r^T r partials], 160 columns x 512 blocks each
+        parts_ = static_cast<double*>(Runtime::get().alloc(sizeof(double) * 2 * kPartsPerRegion));
+        ticket_ = static_cast<unsigned*>(Runtime::get().alloc(sizeof(unsigned) * 4));
+        BOSP_CUDA(cudaMemsetAsync(ticket_, 0, sizeof(unsigned) * 4, Runtime::get().stream()));
+    }
+    s.parts = parts_ + kPartsPerRegion;
+    s.parts_cap = static_cast<int>(kPartsPerRegion);
     if (!host_active) {
         BOSP_CUDA(cudaMallocHost(&host_active, 4 * sizeof(int)));
         BOSP_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
@@ -249,6 +256,31 @@ CgWorkspace::~CgWorkspace() {
     // owned device memory is returned with the pool at teardown; pinned/event handles leak
     // intentionally when the workspace outlives the CUDA context at process exit.
 }
+
+namespace {
+// One batched CG iteration: ap = A p with p^T A p fused into the operator when it can
+// (SELL / stencil), then the cooperative fused update; unfused kernels otherwise.
+void cg_iteration(const LinearOperator& a, const DMat& x, const DMat& r, const DMat& p, const DMat& ap,
+                  const CgScalars& sc, CgWorkspace& ws, double tol, int mi) {
+    // BOSP_CG_MODE: 0 = SpMM with fused p^T A p + update + direction (default),
+    //               1 = separate p^T A p kernel, 2 = cooperative single-kernel update
+    static const int mode = std::getenv("BOSP_CG_MODE") ? std::atoi(std::getenv("BOSP_CG_MODE")) : 0;
+    if (mode == 2 && p.cols <= 160) {
+        a.apply_device(p, ap);
+        cg_pap(p, ap, sc);
+        cg_update_fused(x, r, p, ap, sc, sc.pap, 1, tol, mi);
+        return;
+    }
+    const SpmmDot dot{ws.pap_parts(), ws.ticket(), sc.pap};
+    if (mode != 1 && a.impl()->apply_dot(p, ap, dot)) {
+        cg_update(x, r, p, ap, sc, tol, mi);
+        return;
+    }
+    a.apply_device(p, ap);
+    cg_pap(p, ap, sc);
+    cg_update(x, r, p, ap, sc, tol, mi);
+}
+}  // namespace
 
 DevCgOutcome dev_cg(const LinearOperator& a, const DMat& rhs, const DMat& x, double tol,
                     int64_t max_iter, CgWorkspace& ws, const DMat* x0, bool want_stats) {
@@ -311,9 +343,7 @@ DevCgOutcome dev_cg(const LinearOperator& a, const DMat& rhs, const DMat& x, dou
             rt.set_capture_sink(&g->body_launches);
             BOSP_CUDA(cudaStreamBeginCaptureToGraph(rt.stream(), body, nullptr, nullptr, 0,
                                                     cudaStreamCaptureModeRelaxed));
-            a.apply_device(p, ap);
-            cg_pap(p, ap, sc);
-            cg_update(x, r, p, ap, sc, tol, mi);
+            cg_iteration(a, x, r, p, ap, sc, ws, tol, mi);
             BOSP_CUDA(cudaStreamEndCapture(rt.stream(), &body));
             rt.set_capture_sink(nullptr);
             rt.set_capture_prof(nullptr);
@@ -353,9 +383,7 @@ DevCgOutcome dev_cg(const LinearOperator& a, const DMat& rhs, const DMat& x, dou
                 BOSP_CUDA(cudaEventSynchronize(ws.ev[slot]));
                 if (ws.host_active[slot] == 0) break;
             }
-            a.apply_device(p, ap);
-            cg_pap(p, ap, ws.s);
-            cg_update(x, r, p, ap, ws.s, tol, mi);
+            cg_iteration(a, x, r, p, ap, ws.s, ws, tol, mi);
             publish(it + 1);
         }
         out.sweeps = it;

@@ -64,10 +64,15 @@ public:
     int* host_active = nullptr;  // pinned ring
     cudaEvent_t ev[2] = {nullptr, nullptr};
     std::vector<CgGraph> graphs;
+    double* pap_parts() const { return parts_; }
+    unsigned* ticket() const { return ticket_; }
     ~CgWorkspace();
 
 private:
+    static constexpr int64_t kPartsPerRegion = 160 * 512;
     void* scal_ = nullptr;
+    double* parts_ = nullptr;
+    unsigned* ticket_ = nullptr;
     int64_t m_cap_ = 0;
 };
 struct DevCgOutcome {

@@ -145,6 +145,10 @@ public:
         Runtime::get().sync();  // host staging vectors die at scope exit
     }
     void apply(const DMat& x, const DMat& y) const override { sell_spmm(dev_, x, y); }
+    bool apply_dot(const DMat& x, const DMat& y, const SpmmDot& dot) const override {
+        sell_spmm(dev_, x, y, &dot);
+        return true;
+    }
 
 private:
     DevFree sp_{nullptr}, sw_{nullptr}, col_{nullptr}, val_{nullptr};
@@ -171,6 +175,10 @@ public:
         }
     }
     void apply(const DMat& x, const DMat& y) const override { stencil_spmm(dev_, x, y); }
+    bool apply_dot(const DMat& x, const DMat& y, const SpmmDot& dot) const override {
+        stencil_spmm(dev_, x, y, &dot);
+        return true;
+    }
 
 private:
     DevFree v_{nullptr};

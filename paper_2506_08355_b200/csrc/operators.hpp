@@ -19,6 +19,12 @@ public:
     // Whether apply() only enqueues device work on the solver stream (so it can be recorded
     // into a CUDA graph); host callbacks cannot.
     virtual bool capturable() const { return true; }
+    // y = A x with x(:,j)^T y(:,j) (the CG's p^T A p) fused into the apply and folded into
+    // dot.out; returns false when unsupported (nothing done).
+    virtual bool apply_dot(const DMat& x, const DMat& y, const SpmmDot& dot) const {
+        (void)x; (void)y; (void)dot;
+        return false;
+    }
 
 private:
     int64_t n_;

@@ -19,8 +19,17 @@ struct SellDev {
     int64_t nnz = 0;                     // true nonzeros (for algorithmic byte counts)
 };
 
-// y(:, j) = A x(:, j) for all columns of x.
-void sell_spmm(const SellDev& a, const DMat& x, const DMat& y);
+// Fused x(:,j)^T y(:,j) (the CG's p^T A p): per-block partials in `parts` (<= 256 x ncols),
+// folded in fixed order by the last block into out[j]; `ticket` must be zero and stays zero.
+struct SpmmDot {
+    double* parts;
+    unsigned* ticket;
+    double* out;
+};
+
+// y(:, j) = A x(:, j) for all columns of x (optionally with the fused dots); returns the number
+// of row blocks.
+int sell_spmm(const SellDev& a, const DMat& x, const DMat& y, const SpmmDot* dot = nullptr);
 
 // Structured-grid Laplacian family: y = scale * (L_bc x) + v .* x on nx*ny*nz nodes (nz = 1 ->
 // 5-point).  bc: 0 = Neumann graph Laplacian (diag = #in-grid neighbours), 1 = Dirichlet
@@ -34,7 +43,7 @@ struct StencilDev {
     double origin = 0.0, h = 1.0;
     const double* v = nullptr;
 };
-void stencil_spmm(const StencilDev& s, const DMat& x, const DMat& y);
+int stencil_spmm(const StencilDev& s, const DMat& x, const DMat& y, const SpmmDot* dot = nullptr);
 
 }  // namespace b200
 }  // namespace bosp

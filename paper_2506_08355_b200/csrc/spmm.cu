@@ -104,16 +104,74 @@ __global__ void __launch_bounds__(kRows) k_sell(SellDev a, const double* __restr
     tm.stop();
 }
 
-// Column-group variant: grid.y walks groups of CB columns, the row's entries are re-read per
-// group (from L2).  More independent blocks; kept for shapes where it wins.
+// Per-block partial sums of x(:,j)^T y(:,j) for the CB columns of this block, written to
+// dots[j * gridDim.x + blockIdx.x] (fixed order; folded by cg_update_fused).
 template <int CB>
+__device__ __forceinline__ void block_dots_out(double (&d)[CB], double* dots, int j0, int ncols) {
+    __shared__ double red[kRows / 32][CB];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+    for (int c = 0; c < CB; ++c)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) d[c] += __shfl_xor_sync(0xffffffffu, d[c], o);
+    if (lane == 0)
+#pragma unroll
+        for (int c = 0; c < CB; ++c) red[warp][c] = d[c];
+    __syncthreads();
+    if (threadIdx.x < CB && j0 + static_cast<int>(threadIdx.x) < ncols) {
+        double t = 0.0;
+        for (int w = 0; w < kRows / 32; ++w) t += red[w][threadIdx.x];
+        dots[static_cast<int64_t>(j0 + threadIdx.x) * gridDim.x + blockIdx.x] = t;
+    }
+}
+
+// Last block of the grid (ticket) folds the per-block partials of every column in a fixed order
+// (one warp per column, lanes strided) into out[j]; leaves the ticket at zero.
+__device__ __forceinline__ void fold_dots_last_block(const double* dots, int ncols, unsigned* ticket,
+                                                     double* out) {
+    __shared__ bool last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(ticket, 1u) == gridDim.x * gridDim.y - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int j = warp; j < ncols; j += kRows / 32) {
+        double t = 0.0;
+        for (int q = lane; q < static_cast<int>(gridDim.x); q += 32)
+            t += __ldcg(dots + static_cast<int64_t>(j) * gridDim.x + q);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (lane == 0) out[j] = t;
+    }
+    if (threadIdx.x == 0) *ticket = 0u;
+}
+
+struct DotOut {
+    double* parts;     // [ncols][gridDim.x] per-block partials
+    unsigned* ticket;  // zero on entry, left at zero
+    double* out;       // folded x^T y per column
+};
+
+// Column-group variant: grid.y walks groups of CB columns, grid.x strides over 256-row tiles;
+// the row's entries are re-read per column group (L2).  Optionally accumulates x^T y per
+// column (the CG's p^T A p) while y is produced.
+template <int CB, bool DOT>
 __global__ void __launch_bounds__(kRows) k_sell_cb(SellDev a, const double* __restrict__ x, int64_t ldx,
                                                     double* __restrict__ y, int64_t ldy, int ncols,
-                                                    KTimer tm) {
+                                                    KTimer tm, DotOut dots) {
     tm.start();
-    const int64_t row = static_cast<int64_t>(blockIdx.x) * kRows + threadIdx.x;
-    if (row < a.n) {
-        const int j0 = blockIdx.y * CB;
+    const int j0 = blockIdx.y * CB;
+    double d[CB];
+#pragma unroll
+    for (int c = 0; c < CB; ++c) d[c] = 0.0;
+    const int64_t ntiles = (a.n + kRows - 1) / kRows;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t row = tile * kRows + threadIdx.x;
+        if (row >= a.n) continue;
         const int64_t s = row >> 5;
         const int64_t base = a.slice_ptr[s] + (row & 31);
         const int w = a.slice_w[s];
@@ -130,20 +188,32 @@ __global__ void __launch_bounds__(kRows) k_sell_cb(SellDev a, const double* __re
         }
 #pragma unroll
         for (int c = 0; c < CB; ++c)
-            if (j0 + c < ncols) y[(j0 + c) * ldy + row] = acc[c];
+            if (j0 + c < ncols) {
+                y[(j0 + c) * ldy + row] = acc[c];
+                if (DOT) d[c] += __ldg(xb + c * ldx + row) * acc[c];
+            }
+    }
+    if (DOT) {
+        block_dots_out<CB>(d, dots.parts, j0, ncols);
+        fold_dots_last_block(dots.parts, ncols, dots.ticket, dots.out);
     }
     tm.stop();
 }
 
-template <int CB>
+template <int CB, bool DOT>
 __global__ void __launch_bounds__(kRows) k_stencil(StencilDev st, const double* __restrict__ x,
                                                     int64_t ldx, double* __restrict__ y,
-                                                    int64_t ldy, int ncols, KTimer tm) {
+                                                    int64_t ldy, int ncols, KTimer tm, DotOut dots) {
     tm.start();
     const int64_t n = st.nx * st.ny * st.nz;
-    const int64_t idx = static_cast<int64_t>(blockIdx.x) * kRows + threadIdx.x;
-    if (idx < n) {
-        const int j0 = blockIdx.y * CB;
+    const int j0 = blockIdx.y * CB;
+    double d[CB];
+#pragma unroll
+    for (int c = 0; c < CB; ++c) d[c] = 0.0;
+    const int64_t ntiles = (n + kRows - 1) / kRows;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t idx = tile * kRows + threadIdx.x;
+        if (idx >= n) continue;
         const int64_t nxy = st.nx * st.ny;
         const int64_t i = idx % st.nx;
         const int64_t jy = (idx / st.nx) % st.ny;
@@ -181,16 +251,30 @@ __global__ void __launch_bounds__(kRows) k_stencil(StencilDev st, const double* 
                 if (zm) nb += __ldg(xc - nxy);
                 if (zp) nb += __ldg(xc + nxy);
             }
-            y[(j0 + c) * ldy + idx] = dg * __ldg(xc) - st.scale * nb;
+            const double xs = __ldg(xc);
+            const double yv = dg * xs - st.scale * nb;
+            y[(j0 + c) * ldy + idx] = yv;
+            if (DOT) d[c] += xs * yv;
         }
+    }
+    if (DOT) {
+        block_dots_out<CB>(d, dots.parts, j0, ncols);
+        fold_dots_last_block(dots.parts, ncols, dots.ticket, dots.out);
     }
     tm.stop();
 }
 
+// Row-tile blocks per column group: all tiles when no dots are wanted, else at most 256 so the
+// consumer folds <= 256 partials per column.
+unsigned row_blocks(int64_t n, bool dots) {
+    const int64_t tiles = (n + kRows - 1) / kRows;
+    return static_cast<unsigned>(dots ? std::min<int64_t>(tiles, 256) : tiles);
+}
+
 }  // namespace
 
-void sell_spmm(const SellDev& a, const DMat& x, const DMat& y) {
-    if (a.n == 0 || x.cols == 0) return;
+int sell_spmm(const SellDev& a, const DMat& x, const DMat& y, const SpmmDot* dot) {
+    if (a.n == 0 || x.cols == 0) return 0;
     Runtime& rt = Runtime::get();
     const int ncols = static_cast<int>(x.cols);
     // algorithmic (minimum) traffic: CSR once (8 B value + 4 B int32 index per nnz,
@@ -202,30 +286,41 @@ void sell_spmm(const SellDev& a, const DMat& x, const DMat& y) {
     // Column groups of CB (grid.y) keep many independent blocks in flight; measured 2x the
     // bandwidth of the all-columns-per-thread variant (k_sell) on config 2 (B200).
     static const int variant = std::getenv("BOSP_SPMM_CB") ? std::atoi(std::getenv("BOSP_SPMM_CB")) : 4;
-    const unsigned gx = static_cast<unsigned>((a.n + kRows - 1) / kRows);
-    switch (variant) {
-        case 0: k_sell<<<gx, kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm); break;
-        case 1: k_sell_cb<1><<<dim3(gx, ncols), kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm); break;
-        case 2: k_sell_cb<2><<<dim3(gx, (ncols + 1) / 2), kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm); break;
-        case 8: k_sell_cb<8><<<dim3(gx, (ncols + 7) / 8), kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm); break;
-        default: k_sell_cb<4><<<dim3(gx, (ncols + 3) / 4), kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm); break;
+    const unsigned gx = row_blocks(a.n, dot != nullptr);
+    if (dot) {
+        k_sell_cb<4, true><<<dim3(gx, (ncols + 3) / 4), kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm,
+                                                                                DotOut{dot->parts, dot->ticket, dot->out});
+    } else {
+        switch (variant) {
+            case 0: k_sell<<<gx, kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm); break;
+            case 2: k_sell_cb<2, false><<<dim3(gx, (ncols + 1) / 2), kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm, DotOut{}); break;
+            case 8: k_sell_cb<8, false><<<dim3(gx, (ncols + 7) / 8), kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm, DotOut{}); break;
+            default: k_sell_cb<4, false><<<dim3(gx, (ncols + 3) / 4), kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm, DotOut{}); break;
+        }
     }
     BOSP_LAUNCH_CHECK();
+    return static_cast<int>(gx);
 }
 
-void stencil_spmm(const StencilDev& s, const DMat& x, const DMat& y) {
+int stencil_spmm(const StencilDev& s, const DMat& x, const DMat& y, const SpmmDot* dot) {
     const int64_t n = s.nx * s.ny * s.nz;
-    if (n == 0 || x.cols == 0) return;
+    if (n == 0 || x.cols == 0) return 0;
     Runtime& rt = Runtime::get();
     constexpr int CB = 4;
     const int ncols = static_cast<int>(x.cols);
-    dim3 grid(static_cast<unsigned>((n + kRows - 1) / kRows), (ncols + CB - 1) / CB);
+    const unsigned gx = row_blocks(n, dot != nullptr);
+    dim3 grid(gx, (ncols + CB - 1) / CB);
     const double pts = s.nz > 1 ? 7.0 : 5.0;
     const double bytes = 16.0 * n * ncols, flops = 2.0 * pts * n * ncols;
     KTimer tm{rt.timer_begin("spmm", bytes, flops)};
     LaunchScope ls("spmm", bytes, flops, false);
-    k_stencil<CB><<<grid, kRows, 0, rt.stream()>>>(s, x.p, x.ld, y.p, y.ld, ncols, tm);
+    if (dot)
+        k_stencil<CB, true><<<grid, kRows, 0, rt.stream()>>>(s, x.p, x.ld, y.p, y.ld, ncols, tm,
+                                                              DotOut{dot->parts, dot->ticket, dot->out});
+    else
+        k_stencil<CB, false><<<grid, kRows, 0, rt.stream()>>>(s, x.p, x.ld, y.p, y.ld, ncols, tm, DotOut{});
     BOSP_LAUNCH_CHECK();
+    return static_cast<int>(gx);
 }
 
 }  // namespace b200

@@ -3,6 +3,8 @@
 // Reductions are deterministic: grid (chunks x columns), every block writes its partial sums,
 // the last block to finish (one ticket per launch) folds the partials in fixed chunk order and
 // runs the per-column epilogue.  HBM traffic is one streaming pass over the operands.
+#include <cooperative_groups.h>
+
 #include <algorithm>
 
 #include "dense_ops.hpp"
@@ -49,17 +51,19 @@ __global__ void __launch_bounds__(kThreads) k_colred(int64_t n, int ncols, int n
     double acc[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) acc[k] = 0.0;
+    f.prologue(j);
     if (!f.skip(j)) {
+        // 16-byte accesses: rows in pairs (chunk is even, columns are 256-byte aligned)
         const int64_t r0 = c * chunk;
         const int64_t r1 = min(n, r0 + chunk);
-        int64_t i = r0 + threadIdx.x;
-        for (; i + 3 * kThreads < r1; i += 4 * kThreads) {
-            f.row(i, j, acc);
-            f.row(i + kThreads, j, acc);
-            f.row(i + 2 * kThreads, j, acc);
-            f.row(i + 3 * kThreads, j, acc);
+        const int64_t pend = r0 + ((r1 - r0) & ~int64_t(1));
+        int64_t i = r0 + 2 * threadIdx.x;
+        for (; i + 2 * kThreads < pend; i += 4 * kThreads) {
+            f.row2(i, j, acc);
+            f.row2(i + 2 * kThreads, j, acc);
         }
-        for (; i < r1; i += kThreads) f.row(i, j, acc);
+        for (; i < pend; i += 2 * kThreads) f.row2(i, j, acc);
+        if (pend < r1 && threadIdx.x == 0) f.row(pend, j, acc);
     }
     block_sum<K>(acc, sh);
     if (threadIdx.x == 0) {
@@ -90,7 +94,14 @@ __global__ void __launch_bounds__(kThreads) k_colred(int64_t n, int ncols, int n
 
 struct NoFinAll {
     __device__ void fin_all(int) const {}
+    __device__ void prologue(int) const {}
 };
+
+__device__ __forceinline__ double2 ldg2(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
+__device__ __forceinline__ double2 ld2(const double* p) { return *reinterpret_cast<const double2*>(p); }
+__device__ __forceinline__ void st2(double* p, double a, double b) {
+    *reinterpret_cast<double2*>(p) = make_double2(a, b);
+}
 
 template <int K, class F>
 void launch_colred(const char* family, int64_t n, int ncols, const F& f, double bytes) {
@@ -99,7 +110,7 @@ void launch_colred(const char* family, int64_t n, int ncols, const F& f, double 
     const int64_t target = 4LL * rt.sm_count();
     int nchunks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n + 4095) / 4096,
                                                                             (target + ncols - 1) / ncols)));
-    const int64_t chunk = (n + nchunks - 1) / nchunks;
+    const int64_t chunk = ((n + nchunks - 1) / nchunks + 1) & ~int64_t(1);  // even: pairs stay aligned
     double* partial = rt.scratch(static_cast<size_t>(nchunks) * ncols * K);
     unsigned* ticket = rt.tickets(1);
     LaunchScope ls(family, bytes, 0.0);
@@ -109,6 +120,7 @@ void launch_colred(const char* family, int64_t n, int ncols, const F& f, double 
 }
 
 // ---- functors -------------------------------------------------------------------------------
+// row(i, j, acc) handles one row; row2(i, j, acc) rows i, i+1 (i even) with 16-byte accesses.
 struct DotF : NoFinAll {
     const double* x; int64_t ldx;
     const double* y; int64_t ldy;
@@ -116,6 +128,10 @@ struct DotF : NoFinAll {
     __device__ bool skip(int) const { return false; }
     __device__ void row(int64_t i, int j, double (&a)[1]) const {
         a[0] += x[i + j * ldx] * y[i + j * ldy];
+    }
+    __device__ void row2(int64_t i, int j, double (&a)[1]) const {
+        const double2 u = ldg2(x + i + j * ldx), v = ldg2(y + i + j * ldy);
+        a[0] += u.x * v.x + u.y * v.y;
     }
     __device__ void fin(int j, const double (&s)[1]) const { out[j] = s[0]; }
 };
@@ -134,11 +150,30 @@ struct ResidF : NoFinAll {
         a[0] += r1 * r1 + r2 * r2;
         a[1] += xv * xv + yv * yv;
     }
+    __device__ void row2(int64_t i, int j, double (&a)[2]) const {
+        const double l = lam[j];
+        const double2 k2 = ldg2(kx + i + j * lkx), y2 = ldg2(yb + i + j * lyb);
+        const double2 m2 = ldg2(my + i + j * lmy), x2 = ldg2(xb + i + j * lxb);
+        const double2 xv = ldg2(x + i + j * lx), yv = ldg2(y + i + j * ly);
+        const double r1a = k2.x - l * y2.x, r1b = k2.y - l * y2.y;
+        const double r2a = m2.x - l * x2.x, r2b = m2.y - l * x2.y;
+        a[0] += (r1a * r1a + r2a * r2a) + (r1b * r1b + r2b * r2b);
+        a[1] += (xv.x * xv.x + yv.x * yv.x) + (xv.y * xv.y + yv.y * yv.y);
+    }
     __device__ void fin(int j, const double (&s)[2]) const {
         num[j] = s[0];
         den[j] = s[1];
     }
 };
+
+__device__ __forceinline__ void cg_publish(const CgScalars& s, int ncols, bool reset_loops) {
+    int c = 0;
+    for (int j = 0; j < ncols; ++j) c += s.active[j];
+    *s.any_active = c;
+    if (reset_loops) *s.loops = 0;
+    else *s.loops += 1;
+    if (s.has_cond) cudaGraphSetConditional(s.cond, c > 0 ? 1u : 0u);
+}
 
 // CG start: x = 0, r = b, p = b and ||b||^2 in one pass.
 struct CgStartF {
@@ -146,6 +181,7 @@ struct CgStartF {
     double *x, *r, *p; int64_t lx, lr, lp;
     CgScalars s;
     double tol; int max_iter;
+    __device__ void prologue(int) const {}
     __device__ bool skip(int) const { return false; }
     __device__ void row(int64_t i, int j, double (&a)[1]) const {
         const double v = b[i + j * lb];
@@ -153,6 +189,13 @@ struct CgStartF {
         r[i + j * lr] = v;
         p[i + j * lp] = v;
         a[0] += v * v;
+    }
+    __device__ void row2(int64_t i, int j, double (&a)[1]) const {
+        const double2 v = ldg2(b + i + j * lb);
+        st2(x + i + j * lx, 0.0, 0.0);
+        st2(r + i + j * lr, v.x, v.y);
+        st2(p + i + j * lp, v.x, v.y);
+        a[0] += v.x * v.x + v.y * v.y;
     }
     __device__ void fin(int j, const double (&sm)[1]) const {
         const double bn = sqrt(sm[0]);
@@ -163,13 +206,7 @@ struct CgStartF {
         // cg.cpp:22 (bnorm == 0 -> column skipped) and the loop test at :33
         s.active[j] = (bn != 0.0 && sqrt(sm[0]) > tol * bn && max_iter > 0) ? 1 : 0;
     }
-    __device__ void fin_all(int ncols) const {
-        int c = 0;
-        for (int j = 0; j < ncols; ++j) c += s.active[j];
-        *s.any_active = c;
-        *s.loops = 0;
-        if (s.has_cond) cudaGraphSetConditional(s.cond, c > 0 ? 1u : 0u);
-    }
+    __device__ void fin_all(int ncols) const { cg_publish(s, ncols, true); }
 };
 
 struct CgStartX0F {
@@ -177,6 +214,7 @@ struct CgStartX0F {
     double *x, *r, *p; int64_t lx, lr, lp;
     CgScalars s;
     double tol; int max_iter;
+    __device__ void prologue(int) const {}
     __device__ bool skip(int) const { return false; }
     __device__ void row(int64_t i, int j, double (&a)[2]) const {
         const double bv = b[i + j * lb];
@@ -187,6 +225,10 @@ struct CgStartX0F {
         a[0] += rv * rv;
         a[1] += bv * bv;
     }
+    __device__ void row2(int64_t i, int j, double (&a)[2]) const {
+        row(i, j, a);
+        row(i + 1, j, a);
+    }
     __device__ void fin(int j, const double (&sm)[2]) const {
         const double bn = sqrt(sm[1]);
         s.rr[j] = sm[0];
@@ -195,13 +237,7 @@ struct CgStartX0F {
         s.broken[j] = 0;
         s.active[j] = (bn != 0.0 && sqrt(sm[0]) > tol * bn && max_iter > 0) ? 1 : 0;
     }
-    __device__ void fin_all(int ncols) const {
-        int c = 0;
-        for (int j = 0; j < ncols; ++j) c += s.active[j];
-        *s.any_active = c;
-        *s.loops = 0;
-        if (s.has_cond) cudaGraphSetConditional(s.cond, c > 0 ? 1u : 0u);
-    }
+    __device__ void fin_all(int ncols) const { cg_publish(s, ncols, true); }
 };
 
 struct CgPapF : NoFinAll {
@@ -209,6 +245,10 @@ struct CgPapF : NoFinAll {
     CgScalars s;
     __device__ bool skip(int j) const { return s.active[j] == 0; }
     __device__ void row(int64_t i, int j, double (&a)[1]) const { a[0] += p[i + j * lp] * ap[i + j * lap]; }
+    __device__ void row2(int64_t i, int j, double (&a)[1]) const {
+        const double2 u = ldg2(p + i + j * lp), v = ldg2(ap + i + j * lap);
+        a[0] += u.x * v.x + u.y * v.y;
+    }
     __device__ void fin(int j, const double (&sm)[1]) const {
         if (s.active[j]) s.pap[j] = sm[0];
     }
@@ -220,6 +260,7 @@ struct CgXrF {
     CgScalars s;
     double* beta;
     double tol; int max_iter;
+    __device__ void prologue(int) const {}
     __device__ bool skip(int j) const { return s.active[j] == 0 || !(s.pap[j] > 0.0); }
     __device__ void row(int64_t i, int j, double (&a)[1]) const {
         const double alpha = s.rr[j] / s.pap[j];
@@ -228,6 +269,16 @@ struct CgXrF {
         x[i + j * lx] = xv;
         r[i + j * lr] = rv;
         a[0] += rv * rv;
+    }
+    __device__ void row2(int64_t i, int j, double (&a)[1]) const {
+        const double alpha = s.rr[j] / s.pap[j];
+        const double2 xv = ld2(x + i + j * lx), pv = ldg2(p + i + j * lp);
+        const double2 rv = ld2(r + i + j * lr), av = ldg2(ap + i + j * lap);
+        const double x0 = xv.x + alpha * pv.x, x1 = xv.y + alpha * pv.y;
+        const double r0 = rv.x - alpha * av.x, r1 = rv.y - alpha * av.y;
+        st2(x + i + j * lx, x0, x1);
+        st2(r + i + j * lr, r0, r1);
+        a[0] += r0 * r0 + r1 * r1;
     }
     __device__ void fin(int j, const double (&sm)[1]) const {
         if (!s.active[j]) {
@@ -246,23 +297,20 @@ struct CgXrF {
         s.iters[j] += 1;
         s.active[j] = (sqrt(rr_new) > tol * s.bnorm[j] && s.iters[j] < max_iter) ? 1 : 0;
     }
-    __device__ void fin_all(int ncols) const {
-        int c = 0;
-        for (int j = 0; j < ncols; ++j) c += s.active[j];
-        *s.any_active = c;
-        *s.loops += 1;
-        if (s.has_cond) cudaGraphSetConditional(s.cond, c > 0 ? 1u : 0u);
-    }
+    __device__ void fin_all(int ncols) const { cg_publish(s, ncols, false); }
 };
 
 // ---- element-wise kernels ----------------------------------------------------------------
+// f(i, j) one row, f.pair(i, j) rows i, i+1 (i even, 16-byte accesses).
 template <class F>
 __global__ void __launch_bounds__(kThreads) k_cols(int64_t n, F f) {
     const int j = blockIdx.y;
     if (f.skip(j)) return;
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(kThreads) + threadIdx.x; i < n;
-         i += static_cast<int64_t>(gridDim.x) * kThreads)
-        f(i, j);
+    const int64_t npair = n >> 1;
+    for (int64_t q = blockIdx.x * static_cast<int64_t>(kThreads) + threadIdx.x; q < npair;
+         q += static_cast<int64_t>(gridDim.x) * kThreads)
+        f.pair(2 * q, j);
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) f(n - 1, j);
 }
 
 template <class F>
@@ -271,7 +319,7 @@ void launch_cols(const char* family, int64_t n, int ncols, const F& f, double by
     Runtime& rt = Runtime::get();
     const int64_t target = 8LL * rt.sm_count();
     const unsigned gx = static_cast<unsigned>(std::max<int64_t>(
-        1, std::min<int64_t>((n + kThreads - 1) / kThreads, (target + ncols - 1) / ncols)));
+        1, std::min<int64_t>((n / 2 + kThreads - 1) / kThreads, (target + ncols - 1) / ncols)));
     LaunchScope ls(family, bytes, 0.0);
     k_cols<F><<<dim3(gx, ncols), kThreads, 0, rt.stream()>>>(n, f);
     BOSP_LAUNCH_CHECK();
@@ -281,11 +329,21 @@ struct LamAxmyF {
     const double *a, *b; double* o; int64_t la, lb, lo; const double* lam;
     __device__ bool skip(int) const { return false; }
     __device__ void operator()(int64_t i, int j) const { o[i + j * lo] = lam[j] * a[i + j * la] - b[i + j * lb]; }
+    __device__ void pair(int64_t i, int j) const {
+        const double l = lam[j];
+        const double2 u = ldg2(a + i + j * la), v = ldg2(b + i + j * lb);
+        st2(o + i + j * lo, l * u.x - v.x, l * u.y - v.y);
+    }
 };
 struct LamAxpyF {
     const double* x; double* y; int64_t lx, ly; const double* lam;
     __device__ bool skip(int) const { return false; }
     __device__ void operator()(int64_t i, int j) const { y[i + j * ly] += lam[j] * x[i + j * lx]; }
+    __device__ void pair(int64_t i, int j) const {
+        const double l = lam[j];
+        const double2 u = ldg2(x + i + j * lx), v = ld2(y + i + j * ly);
+        st2(y + i + j * ly, v.x + l * u.x, v.y + l * u.y);
+    }
 };
 struct AxpbyF {
     double a, b; const double* x; double* y; int64_t lx, ly;
@@ -294,17 +352,151 @@ struct AxpbyF {
         const double xv = x[i + j * lx];
         y[i + j * ly] = (b == 0.0) ? a * xv : a * xv + b * y[i + j * ly];
     }
+    __device__ void pair(int64_t i, int j) const {
+        const double2 u = ld2(x + i + j * lx);
+        if (b == 0.0) {
+            st2(y + i + j * ly, a * u.x, a * u.y);
+        } else {
+            const double2 v = ld2(y + i + j * ly);
+            st2(y + i + j * ly, a * u.x + b * v.x, a * u.y + b * v.y);
+        }
+    }
 };
 struct DiagF {
     const double* d; const double* x; double* y; int64_t lx, ly;
     __device__ bool skip(int) const { return false; }
     __device__ void operator()(int64_t i, int j) const { y[i + j * ly] = d[i] * x[i + j * lx]; }
+    __device__ void pair(int64_t i, int j) const {
+        (*this)(i, j);
+        (*this)(i + 1, j);
+    }
 };
 struct CgDirF {  // p = r + beta p for still-active columns (cg.cpp:49)
     const double* r; double* p; int64_t lr, lp; const double* beta; const int* active;
     __device__ bool skip(int j) const { return active[j] == 0; }
     __device__ void operator()(int64_t i, int j) const { p[i + j * lp] = r[i + j * lr] + beta[j] * p[i + j * lp]; }
+    __device__ void pair(int64_t i, int j) const {
+        const double bj = beta[j];
+        const double2 u = ldg2(r + i + j * lr), v = ld2(p + i + j * lp);
+        st2(p + i + j * lp, u.x + bj * v.x, u.y + bj * v.y);
+    }
 };
+
+// ---- fused CG update (cooperative) ----------------------------------------------------------
+constexpr int kUpdMaxCols = 160;  // the reference's nb rule caps nb at 150
+constexpr int kUpdChunk = 8;      // columns reduced together
+
+__global__ void __launch_bounds__(kThreads) k_cg_update_fused(
+    int64_t n, int ncols, double* __restrict__ x, int64_t lx, double* __restrict__ r, int64_t lr,
+    double* __restrict__ p, int64_t lp, const double* __restrict__ ap, int64_t lap, CgScalars s,
+    const double* __restrict__ pap_parts, int nparts, double tol, int max_iter) {
+    __shared__ double s_alpha[kUpdMaxCols], s_beta[kUpdMaxCols], s_rr[kUpdMaxCols];
+    __shared__ int s_upd[kUpdMaxCols], s_act[kUpdMaxCols], s_new[kUpdMaxCols], s_it[kUpdMaxCols];
+    __shared__ double red[kThreads / 32][kUpdChunk];
+    const int nb = gridDim.x, b = blockIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int kWarps = kThreads / 32;
+    // phase 0: fold the p^T A p partials (one warp per column, lanes strided, fixed order) and
+    // snapshot the per-column state (block 0 rewrites it after the grid barrier)
+    for (int j = warp; j < ncols; j += kWarps) {
+        double t = 0.0;
+        for (int q = lane; q < nparts; q += 32) t += __ldcg(&pap_parts[static_cast<int64_t>(j) * nparts + q]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (lane == 0) {
+            const double pap = t;
+            const int act = s.active[j];
+            const int upd = act && pap > 0.0;
+            s_act[j] = act;
+            s_upd[j] = upd;
+            s_rr[j] = s.rr[j];
+            s_it[j] = s.iters[j];
+            s_alpha[j] = upd ? s.rr[j] / pap : 0.0;
+            if (b == 0 && act) s.pap[j] = pap;
+        }
+    }
+    __syncthreads();
+    const int64_t chunk = (n + nb - 1) / nb;
+    const int64_t r0 = b * chunk, r1 = min(n, r0 + chunk);
+    // phase 1: x += a p, r -= a ap, per-block partial r^T r
+    for (int c0 = 0; c0 < ncols; c0 += kUpdChunk) {
+        double acc[kUpdChunk];
+#pragma unroll
+        for (int jj = 0; jj < kUpdChunk; ++jj) acc[jj] = 0.0;
+        for (int64_t i = r0 + threadIdx.x; i < r1; i += kThreads) {
+#pragma unroll
+            for (int jj = 0; jj < kUpdChunk; ++jj) {
+                const int j = c0 + jj;
+                if (j < ncols && s_upd[j]) {
+                    const double a = s_alpha[j];
+                    const double xv = x[i + j * lx] + a * p[i + j * lp];
+                    const double rv = r[i + j * lr] - a * ap[i + j * lap];
+                    x[i + j * lx] = xv;
+                    r[i + j * lr] = rv;
+                    acc[jj] += rv * rv;
+                }
+            }
+        }
+#pragma unroll
+        for (int jj = 0; jj < kUpdChunk; ++jj)
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc[jj] += __shfl_xor_sync(0xffffffffu, acc[jj], o);
+        if (lane == 0)
+#pragma unroll
+            for (int jj = 0; jj < kUpdChunk; ++jj) red[warp][jj] = acc[jj];
+        __syncthreads();
+        if (threadIdx.x < kUpdChunk && c0 + threadIdx.x < ncols) {
+            double t = 0.0;
+            for (int w = 0; w < kThreads / 32; ++w) t += red[w][threadIdx.x];
+            s.parts[static_cast<int64_t>(c0 + threadIdx.x) * nb + b] = t;
+        }
+        __syncthreads();
+    }
+    __threadfence();
+    cooperative_groups::this_grid().sync();
+    // phase 2: every block folds the partials in the same order -> identical beta everywhere
+    for (int j = warp; j < ncols; j += kWarps) {
+        double rr = 0.0;
+        if (s_upd[j]) {
+            for (int q = lane; q < nb; q += 32) rr += __ldcg(&s.parts[static_cast<int64_t>(j) * nb + q]);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) rr += __shfl_xor_sync(0xffffffffu, rr, o);
+        }
+        if (lane != 0) continue;
+        if (s_upd[j]) {
+            const double beta = rr / s_rr[j];
+            const int nit = s_it[j] + 1;
+            const int na = (sqrt(rr) > tol * s.bnorm[j] && nit < max_iter) ? 1 : 0;
+            s_beta[j] = beta;
+            s_new[j] = na;
+            if (b == 0) {
+                s.rr[j] = rr;
+                s.iters[j] = nit;
+                s.active[j] = na;
+                s.beta[j] = beta;
+            }
+        } else {
+            s_beta[j] = 0.0;
+            s_new[j] = 0;
+            if (b == 0 && s_act[j]) {  // p^T A p <= 0: breakdown keeps the iterate (cg.cpp:40-44)
+                s.broken[j] = 1;
+                s.active[j] = 0;
+            }
+        }
+    }
+    __syncthreads();
+    // p = r + beta p for the columns that continue
+    for (int64_t i = r0 + threadIdx.x; i < r1; i += kThreads)
+        for (int j = 0; j < ncols; ++j)
+            if (s_new[j]) p[i + j * lp] = r[i + j * lr] + s_beta[j] * p[i + j * lp];
+    if (b == 0 && threadIdx.x == 0) {
+        int c = 0;
+        for (int j = 0; j < ncols; ++j) c += s_new[j];
+        *s.any_active = c;
+        *s.loops += 1;
+        if (s.has_cond) cudaGraphSetConditional(s.cond, c > 0 ? 1u : 0u);
+    }
+}
 
 __global__ void k_transpose(const double* __restrict__ a, int64_t lda, int64_t rows, int64_t cols,
                             double* __restrict__ t, int64_t ldt) {
@@ -322,6 +514,37 @@ __global__ void k_transpose(const double* __restrict__ a, int64_t lda, int64_t r
 }
 
 }  // namespace
+
+void cg_update_fused(const DMat& x, const DMat& r, const DMat& p, const DMat& ap, const CgScalars& s,
+                     const double* pap_parts, int nparts, double tol, int max_iter) {
+    const int ncols = static_cast<int>(x.cols);
+    if (ncols <= 0) return;
+    require(ncols <= kUpdMaxCols, "cg_update_fused: too many columns");
+    Runtime& rt = Runtime::get();
+    static int max_blocks = 0;
+    if (max_blocks == 0) {
+        int per_sm = 0;
+        BOSP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cg_update_fused, kThreads, 0));
+        max_blocks = std::max(1, per_sm) * rt.sm_count();
+    }
+    // two blocks per SM: enough to stream HBM, few enough that the redundant fold of the
+    // partials (ncols x blocks loads per block) stays cheap
+    const int nb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(
+        {static_cast<int64_t>(max_blocks), 2LL * rt.sm_count(), (x.rows + kThreads - 1) / kThreads})));
+    require(static_cast<int64_t>(nb) * ncols <= s.parts_cap, "cg_update_fused: partial buffer too small");
+    LaunchScope ls("cg_vec", 8.0 * x.rows * ncols * 8.0, 0.0);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(nb);
+    cfg.blockDim = dim3(kThreads);
+    cfg.stream = rt.stream();
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    BOSP_CUDA(cudaLaunchKernelEx(&cfg, k_cg_update_fused, x.rows, ncols, x.p, x.ld, r.p, r.ld, p.p, p.ld,
+                                 static_cast<const double*>(ap.p), ap.ld, s, pap_parts, nparts, tol, max_iter));
+}
 
 void transpose(const DMat& a, const DMat& t) {
     if (a.rows == 0 || a.cols == 0) return;
