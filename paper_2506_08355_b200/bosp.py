@@ -458,6 +458,25 @@ def bench_blas(kind, n, a, b, reps=20):
     return ms.value
 
 
+def device_solver(op_or_problem_op, tol=1e-13, max_iter=20000):
+    """b -> M^-1 b by the batched device CG (setup helper for the nullspace pair Y0 = M^-1 X0;
+    M SPD).  Accepts a LinearOperator or a problems.{Csr,Stencil} / dense ndarray."""
+    from . import problems as P
+    op = op_or_problem_op
+    if not isinstance(op, LinearOperator):
+        if isinstance(op, np.ndarray):
+            op = LinearOperator.from_dense(op)
+        elif isinstance(op, P.Stencil):
+            op = LinearOperator.from_stencil(op)
+        else:
+            op = LinearOperator.from_csr(op)
+
+    def solve(b):
+        x, _, _ = cg_solve(op, b, tol=tol, max_iter=max_iter)
+        return x
+    return solve
+
+
 def operators_for(problem):
     """problems.Problem -> (K, M) device operators (dense / CSR / matrix-free stencil)."""
     from . import problems as P

@@ -104,18 +104,23 @@ std::optional<DenseMatrix> cholesky_lower(const DenseMatrix& a) {
     if (a.rows() != a.cols()) return std::nullopt;
     const int64_t n = a.rows();
     DenseMatrix l(n, n);
-    // Row-oriented dot products as in the reference (the diagonal pivot test is the contract).
+    // Left-looking, column-oriented: column j = (a(:, j) - sum_k l(j,k) l(:, k)) / l_jj with the
+    // k-sum accumulated in the reference's order (dense_kernels.cpp:11-28) but as unit-stride
+    // axpys; the diagonal pivot test (d > 0, finite) is the contract.
+    std::vector<double> s(static_cast<size_t>(n));
     for (int64_t j = 0; j < n; ++j) {
-        double d = a(j, j);
-        for (int64_t k = 0; k < j; ++k) d -= l(j, k) * l(j, k);
+        for (int64_t i = j; i < n; ++i) s[i] = a(i, j);
+        for (int64_t k = 0; k < j; ++k) {
+            const double ljk = l(j, k);
+            const double* lk = l.col(k);
+            for (int64_t i = j; i < n; ++i) s[i] -= lk[i] * ljk;
+        }
+        const double d = s[j];
         if (!(d > 0.0) || !std::isfinite(d)) return std::nullopt;
         const double ljj = std::sqrt(d);
-        l(j, j) = ljj;
-        for (int64_t i = j + 1; i < n; ++i) {
-            double s = a(i, j);
-            for (int64_t k = 0; k < j; ++k) s -= l(i, k) * l(j, k);
-            l(i, j) = s / ljj;
-        }
+        double* lj = l.col(j);
+        lj[j] = ljj;
+        for (int64_t i = j + 1; i < n; ++i) lj[i] = s[i] / ljj;
     }
     return l;
 }
@@ -177,23 +182,30 @@ JacobiSvdResult jacobi_svd(DenseMatrix a, int64_t max_sweeps) {
         const int64_t kk = k + (k & 1);
         std::vector<int64_t> pos(kk);
         std::iota(pos.begin(), pos.end(), 0);
+        // one parallel region per sweep; rounds are separated by barriers (the pair schedule
+        // of round r+1 depends only on r, so every thread can advance its own copy of `pos`)
         while (rotated && sweep < max_sweeps) {
-            rotated = false;
             ++sweep;
-            for (int64_t round = 0; round < kk - 1; ++round) {
-                int any = 0;
-#pragma omp parallel for schedule(static) reduction(| : any)
-                for (int64_t i = 0; i < kk / 2; ++i) {
-                    int64_t p = pos[i], q = pos[kk - 1 - i];
-                    if (p >= k || q >= k) continue;
-                    if (p > q) std::swap(p, q);
-                    any |= jacobi_pair(a, res.v, p, q) ? 1 : 0;
+            int any = 0;
+#pragma omp parallel reduction(| : any)
+            {
+                std::vector<int64_t> lp(pos);
+                for (int64_t round = 0; round < kk - 1; ++round) {
+#pragma omp for schedule(static)
+                    for (int64_t i = 0; i < kk / 2; ++i) {
+                        int64_t p = lp[i], q = lp[kk - 1 - i];
+                        if (p >= k || q >= k) continue;
+                        if (p > q) std::swap(p, q);
+                        any |= jacobi_pair(a, res.v, p, q) ? 1 : 0;
+                    }  // implicit barrier
+                    const int64_t last = lp[kk - 1];
+                    for (int64_t i = kk - 1; i > 1; --i) lp[i] = lp[i - 1];
+                    lp[1] = last;
                 }
-                rotated |= (any != 0);
-                const int64_t last = pos[kk - 1];
-                for (int64_t i = kk - 1; i > 1; --i) pos[i] = pos[i - 1];
-                pos[1] = last;
+#pragma omp single
+                pos = lp;
             }
+            rotated = (any != 0);
         }
     }
     res.converged = !rotated;
@@ -400,10 +412,109 @@ HostBiorth host_cgs_biorth(const DenseMatrix& x, const DenseMatrix& y, double dr
     return host_gs(x, y, drop_tol, true);
 }
 
+namespace {
+
+// Fast path of the coefficient recurrence for m >= 64: in exact arithmetic MGS-Biorth of (X, Y)
+// is the unpivoted LDU factorisation Gxy = L D U with P = X L^-T, Q = Y U^-1 (then the
+// sign/sqrt|eta| split of D).  Computed with vectorised/threaded loops; returns false -- and the
+// caller runs the column-sequential recurrence instead -- whenever a pivot would be dropped or a
+// column cancels (the rare cases where the order of operations matters).
+bool coef_mgs_ldu(const DenseMatrix& gxx, const DenseMatrix& gxy, const DenseMatrix& gyy,
+                  double drop_tol, double cancel_tol, CoefBiorth& out) {
+    const int64_t m = gxy.rows();
+    DenseMatrix g = gxy;
+    std::vector<double> dpiv(static_cast<size_t>(m));
+    for (int64_t l = 0; l < m; ++l) {
+        const double d = g(l, l);
+        if (!(std::fabs(d) > 0.0) || !std::isfinite(d)) return false;
+        dpiv[l] = d;
+        const double inv = 1.0 / d;
+        for (int64_t i = l + 1; i < m; ++i) g(i, l) *= inv;  // L below the diagonal
+        // trailing update G_ij -= L_il * G_lj (G_lj still unscaled = D_l U_lj)
+#pragma omp parallel for schedule(static) if (m - l > 96)
+        for (int64_t j = l + 1; j < m; ++j) {
+            const double glj = g(l, j);
+            if (glj == 0.0) continue;
+            double* gj = g.col(j);
+            const double* gl = g.col(l);
+            for (int64_t i = l + 1; i < m; ++i) gj[i] -= gl[i] * glj;
+        }
+        for (int64_t j = l + 1; j < m; ++j) g(l, j) *= inv;  // U right of the diagonal
+    }
+    // Ahat = L^-T (unit upper): column c of L^-T = row c of L^-1.  Solve L^T Ahat = I.
+    DenseMatrix ah(m, m), bh(m, m);
+#pragma omp parallel for schedule(dynamic, 8)
+    for (int64_t c = 0; c < m; ++c) {
+        // L^T a = e_c, L^T upper unit: back substitution; a supported on [0, c]
+        double* a = ah.col(c);
+        a[c] = 1.0;
+        for (int64_t i = c - 1; i >= 0; --i) {
+            double s = 0.0;
+            for (int64_t k = i + 1; k <= c; ++k) s += g(k, i) * a[k];
+            a[i] = -s;
+        }
+        // U b = e_c, U upper unit: back substitution
+        double* b = bh.col(c);
+        b[c] = 1.0;
+        for (int64_t i = c - 1; i >= 0; --i) {
+            double s = 0.0;
+            for (int64_t k = i + 1; k <= c; ++k) s += g(i, k) * b[k];
+            b[i] = -s;
+        }
+    }
+    // norms of the unscaled residuals: diag(Ah^T Gxx Ah), diag(Bh^T Gyy Bh); naive magnitudes
+    std::vector<double> pn2(static_cast<size_t>(m)), qn2(static_cast<size_t>(m));
+    bool ok = true;
+#pragma omp parallel for schedule(dynamic, 8) reduction(&& : ok)
+    for (int64_t c = 0; c < m; ++c) {
+        const double* a = ah.col(c);
+        const double* b = bh.col(c);
+        double sp = 0.0, sq = 0.0, pnaive = 0.0, qnaive = 0.0;
+        for (int64_t j = 0; j <= c; ++j) {
+            const double* gx = gxx.col(j);
+            const double* gy = gyy.col(j);
+            double tx = 0.0, ty = 0.0;
+            for (int64_t i = 0; i <= c; ++i) {
+                tx += gx[i] * a[i];
+                ty += gy[i] * b[i];
+            }
+            sp += a[j] * tx;
+            sq += b[j] * ty;
+            pnaive += std::fabs(a[j]) * std::sqrt(std::max(0.0, gxx(j, j)));
+            qnaive += std::fabs(b[j]) * std::sqrt(std::max(0.0, gyy(j, j)));
+        }
+        pn2[c] = sp;
+        qn2[c] = sq;
+        const double pn = std::sqrt(std::max(0.0, sp)), qn = std::sqrt(std::max(0.0, sq));
+        if (cancel_tol > 0.0 && ((pnaive > 0.0 && sp < cancel_tol * pnaive * pnaive) ||
+                                 (qnaive > 0.0 && sq < cancel_tol * qnaive * qnaive)))
+            ok = false;
+        if (pn == 0.0 || qn == 0.0 || std::fabs(dpiv[c]) < drop_tol * pn * qn) ok = false;
+    }
+    if (!ok) return false;
+    out.a = DenseMatrix(m, m);
+    out.b = DenseMatrix(m, m);
+    for (int64_t c = 0; c < m; ++c) {
+        const double sc = 1.0 / std::sqrt(std::fabs(dpiv[c])), sg = sign_or_plus(dpiv[c]);
+        for (int64_t i = 0; i <= c; ++i) {
+            out.a(i, c) = sg * sc * ah(i, c);
+            out.b(i, c) = sc * bh(i, c);
+        }
+        out.kept.push_back(c);
+    }
+    return true;
+}
+
+}  // namespace
+
 CoefBiorth coef_mgs(const DenseMatrix& gxx, const DenseMatrix& gxy, const DenseMatrix& gyy,
                     double drop_tol, bool classical, double cancel_tol, int64_t* stop) {
     const int64_t m = gxy.rows();
     if (stop) *stop = m;
+    if (!classical && m >= 64) {
+        CoefBiorth fast;
+        if (coef_mgs_ldu(gxx, gxy, gyy, drop_tol, cancel_tol, fast)) return fast;
+    }
     // coefficient columns of the kept pairs, plus their images ua = Gyx a, ub = Gxy b
     std::vector<std::vector<double>> av, bv, ua, ub;
     CoefBiorth out;

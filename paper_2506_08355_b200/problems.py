@@ -217,38 +217,46 @@ def _grid3_ops(m: int):
     return kop, mop
 
 
-def _constant_nullspace(mcsr: Csr, n: int):
+def _constant_nullspace(mop, n: int, solve=None):
+    """X0 ∝ constants (N of the Neumann graph Laplacian); Y0 = M^-1 X0 by `solve(M)` (a factory
+    M -> (b -> M^-1 b), e.g. bosp.device_solver on a GPU box) or scipy CG on the CSR form."""
     x_raw = np.full((n, 1), 1.0 / np.sqrt(n))
-    y_raw = _cg_solve_sparse(mcsr.scipy(), x_raw)
+    if solve is not None:
+        y_raw = solve(mop)(x_raw)
+    else:
+        mcsr = mop.to_csr() if isinstance(mop, Stencil) else mop
+        y_raw = _cg_solve_sparse(mcsr.scipy(), x_raw)
     return normalize_nullspace(x_raw, y_raw)
 
 
-def config2(m: int = 64) -> Problem:
+def config2(m: int = 64, solve=None) -> Problem:
     kop, mop = _grid3_ops(m)
     kc, mc = kop.to_csr(), mop.to_csr()
-    x0, y0 = _constant_nullspace(mc, kc.n)
+    x0, y0 = _constant_nullspace(mc, kc.n, solve)
     cfg = dict(nev=20, nb=40, tol=1e-8)
     return Problem(f"config2-csr-{m}^3", kc.n, kc, mc, x0, y0, cfg, dict(grid=m))
 
 
-def config3(m: int = 128) -> Problem:
+def config3(m: int = 128, solve=None, nev: int = 100) -> Problem:
     kop, mop = _grid3_ops(m)
-    x0, y0 = _constant_nullspace(mop.to_csr(), kop.n)
-    cfg = dict(nev=100, nb=64, tol=1e-8, moving=True)
+    x0, y0 = _constant_nullspace(mop, kop.n, solve)
+    cfg = dict(nev=nev, nb=64, tol=1e-8, moving=True)
     return Problem(f"config3-stencil7-{m}^3", kop.n, kop, mop, x0, y0, cfg, dict(grid=m))
 
 
-def config5(m: int = 1024, seed: int = DEFAULT_SEED) -> Problem:
+def config5(m: int = 1024, seed: int = DEFAULT_SEED, solve=None, nev: int = 500) -> Problem:
     rng = np.random.default_rng(seed)
     u = rng.uniform(0.0, 1.0, m * m)
     kop = Stencil(m, m, 1, "neumann", 1.0)
     mop = Stencil(m, m, 1, "dirichlet", 1.0, "array", v=1.0 + u)
-    x0, y0 = _constant_nullspace(mop.to_csr(), kop.n)
-    cfg = dict(nev=500, nb=64, tol=1e-8)
+    x0, y0 = _constant_nullspace(mop, kop.n, solve)
+    cfg = dict(nev=nev, nb=64, tol=1e-8)
     return Problem(f"config5-stencil5-{m}^2", kop.n, kop, mop, x0, y0, cfg, dict(grid=m, seed=seed))
 
 
-def config4(seed: int = DEFAULT_SEED, n: int = 16384, rank: int = 512, nnull: int = 64) -> Problem:
+def config4(seed: int = DEFAULT_SEED, n: int = 16384, rank: int = 512, nnull: int = 64,
+            solve_factory=None) -> Problem:
+    """solve_factory(M dense) -> callable b -> M^-1 b (GPU CG on a box); default LAPACK."""
     rng = np.random.default_rng(seed)
     eps = rng.uniform(1.0, 20.0, n)
     v = rng.standard_normal((n, rank)) * np.sqrt(1.0 / n)
@@ -261,14 +269,14 @@ def config4(seed: int = DEFAULT_SEED, n: int = 16384, rank: int = 512, nnull: in
     # K = Pi (A - B) Pi with Pi = I - N N^T
     t = amb - nbasis @ (nbasis.T @ amb)
     k = t - (t @ nbasis) @ nbasis.T
+    del t, amb
     mm = a + b
-    for x in (k, mm):
-        il = np.tril_indices(n, -1)
-        x.T[il] = x[il]
-    k = np.asfortranarray(k)
-    mm = np.asfortranarray(mm)
+    del a, b
+    # (A + A^T)/2 is exactly symmetric in floating point (x + y == y + x)
+    k = np.asfortranarray(0.5 * (k + k.T))
+    mm = np.asfortranarray(0.5 * (mm + mm.T))
     x_raw = np.asfortranarray(nbasis)
-    y_raw = np.linalg.solve(mm, x_raw)
+    y_raw = solve_factory(mm)(x_raw) if solve_factory else np.linalg.solve(mm, x_raw)
     x0, y0 = normalize_nullspace(x_raw, y_raw)
     cfg = dict(nev=32, nb=64, tol=1e-8)
     return Problem(f"config4-dense-n{n}", n, k, mm, x0, y0, cfg, dict(seed=seed))
