@@ -166,14 +166,26 @@ def run_reference(args, world, rank, dist):
 
 def run_b200(args, world, rank, local, dist):
     from paper_2506_08355_b200 import _lib, bosp
+    from paper_2506_08355_b200 import dist as D
     from paper_2506_08355_b200 import problems as P
     _lib.lib().bosp_set_device(local)
     name, sms = bosp.device_info()
     prob = P.config2(64)
     cfg = bosp.BospConfig(**prob.cfg)
-    ns = bosp.GeneralizedNullspace(prob.x0, prob.y0)
-    K, M = bosp.operators_for(prob)   # resident in HBM before the timed region
+    partitioned = world > 1 and args.partition == "rows"
+    if partitioned:
+        # one process per GPU, rows of every n-length block on this rank; NCCL communicator
+        # inside libbosp_b200.so (torch.distributed only carries the unique id + timings)
+        uid = D.broadcast_uid()
+        row0, nl = D.attach(prob.K, uid, world, rank)
+        ns = D.local_nullspace(prob.x0, prob.y0, row0, nl)
+        K, M = bosp.local_operator(prob.K, world, rank), bosp.local_operator(prob.M, world, rank)
+    else:
+        row0, nl = 0, prob.n
+        ns = bosp.GeneralizedNullspace(prob.x0, prob.y0)
+        K, M = bosp.operators_for(prob)   # resident in HBM before the timed region
     flush = 512 << 20                  # 512 MB > 126 MB L2, written between steps
+    units = 1 if partitioned else world  # one shared problem vs. one replica per rank
 
     def one_step(profile_family=None):
         _lib.lib().bosp_flush_l2(flush)
@@ -205,7 +217,7 @@ def run_b200(args, world, rank, local, dist):
     families = bosp.launch_families()
     total = max_over_ranks(dist, float(sum(dev_s)))
     ms_per_step = total / args.steps * 1e3
-    value = prob.cfg["nev"] * args.steps * world / total
+    value = prob.cfg["nev"] * args.steps * units / total
 
     # parity of the measured run against the reference's own eigenvalues (golden fixture)
     parity = None
@@ -220,22 +232,30 @@ def run_b200(args, world, rank, local, dist):
     kc, mc = prob.K, prob.M
     host = {}
     for tag, c in (("k", kc), ("m", mc)):
-        host[tag] = (np.ascontiguousarray(c.rowptr), np.ascontiguousarray(c.colidx), np.ascontiguousarray(c.vals))
-    h2d = sum(a.nbytes for t in host.values() for a in t) + prob.x0.nbytes + prob.y0.nbytes
-    d2h = 2 * prob.n * prob.cfg["nev"] * 8 + 2 * prob.cfg["nev"] * 8
+        rp = c.rowptr[row0:row0 + nl + 1]
+        host[tag] = (np.ascontiguousarray(rp), np.ascontiguousarray(c.colidx[rp[0]:rp[-1]]),
+                     np.ascontiguousarray(c.vals[rp[0]:rp[-1]]))
+    h2d = sum(a.nbytes for t in host.values() for a in t) + ns.x0.nbytes + ns.y0.nbytes
+    d2h = 2 * nl * prob.cfg["nev"] * 8 + 2 * prob.cfg["nev"] * 8
     e2e_t = []
     for _ in range(max(1, args.steps)):
         _lib.lib().bosp_flush_l2(flush)
         barrier(dist)
         t0 = time.perf_counter()
-        Ke = bosp.LinearOperator.from_csr(*host["k"])
-        Me = bosp.LinearOperator.from_csr(*host["m"])
+        if partitioned:
+            Ke = bosp.LinearOperator.from_csr_rows(prob.n, row0, *host["k"])
+            Me = bosp.LinearOperator.from_csr_rows(prob.n, row0, *host["m"])
+        else:
+            Ke = bosp.LinearOperator.from_csr(*host["k"])
+            Me = bosp.LinearOperator.from_csr(*host["m"])
         r2 = bosp.solve(Ke, Me, None, cfg, ns, want_vectors=True)
         _ = float(r2.lambdas.sum())
         e2e_t.append(time.perf_counter() - t0)
         del Ke, Me
     e2e_total = max_over_ranks(dist, float(sum(e2e_t)))
-    e2e_value = prob.cfg["nev"] * len(e2e_t) * world / e2e_total
+    e2e_value = prob.cfg["nev"] * len(e2e_t) * units / e2e_total
+    if partitioned:
+        bosp.comm_free()
 
     # roofline of the dominant kernel family (CUDA events on the solver stream, timed region)
     peaks = load_peaks()
@@ -273,10 +293,12 @@ def run_b200(args, world, rank, local, dist):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong" if partitioned else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generator, paper_2506_08355_b200/problems.py; no dataset)",
             "config": {"workload": prob.name, "n": prob.n, "nnz_K": kc.nnz, "nev": 20, "nb": 40,
-                       "tol": 1e-8, "parallelism": "replicas" if world > 1 else "single GPU",
+                       "tol": 1e-8,
+                       "parallelism": (f"row partition x{world} (NCCL allreduce + halo)" if partitioned
+                                       else "replicas" if world > 1 else "single GPU"),
                        "l2": "flushed between steps (512 MB memset)", "device": name, "sms": sms},
             "roofline": roof,
             "cpu_baseline": cpu,
@@ -304,6 +326,8 @@ def main():
     ap.add_argument("--roofline-kernel", default="spmm")
     ap.add_argument("--ref-iters", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--partition", default="rows", choices=["rows", "replicas"],
+                    help="N>1: row-partition one solve over the ranks (NCCL) or run N replicas")
     args = ap.parse_args()
     world, rank, local, dist = dist_setup()
     if args.impl == "reference":

@@ -72,8 +72,20 @@ typedef struct {
     int32_t potential;
     double origin, h;
     const double* v;
+    /* row partition along the slowest axis (z in 3-D, y in 2-D): local planes [s0, s0 + nz|ny)
+     * of s_global, global z extent nz_global; s_global = 0 -> unpartitioned */
+    int64_t s0, s_global, nz_global;
 } bosp_stencil;
 bosp_status bosp_op_stencil(const bosp_stencil* spec, bosp_op* out);
+
+/* Row-partitioned operators: this rank's rows [row0, row0 + n_local) of an
+ * n_global operator; requires a communicator on the calling thread (bosp_comm_init_nccl or
+ * bosp_solve_multi).  CSR: rowptr has n_local + 1 entries (any base), colidx are global. */
+bosp_status bosp_op_csr_rows(int64_t n_global, int64_t row0, int64_t n_local, const int64_t* rowptr,
+                             const int64_t* colidx, const double* values, bosp_op* out);
+/* a_rows: n_local x n_global column-major (ld n_local) */
+bosp_status bosp_op_dense_rows(int64_t n_global, int64_t row0, int64_t n_local, const double* a_rows,
+                               bosp_op* out);
 
 /* identity / scaled_identity / diagonal / shifted (linear_operator.cpp:49-92). */
 bosp_status bosp_op_identity(int64_t n, bosp_op* out);
@@ -130,6 +142,38 @@ bosp_status bosp_solve(bosp_op K, bosp_op M, bosp_op B, const bosp_config* cfg, 
                        const double* x0, const double* y0, int64_t cap, double* lambdas,
                        double* x, double* y, double* residuals, int64_t* nout, bosp_stats* stats,
                        double* history, int64_t history_cap, int64_t* history_rows);
+
+/* ---------------------------------------------------------------------------------------
+ * Multi-GPU row partition (new; the reference is single address space).
+ * --------------------------------------------------------------------------------------- */
+/* One process per GPU: rank 0 creates an id (128 bytes), all ranks call init with it; the
+ * communicator (NCCL) and this rank's row window attach to the calling thread.  After that,
+ * bosp_solve on row-partitioned operators and local X0/Y0 rows returns local rows of x, y. */
+bosp_status bosp_comm_nccl_unique_id(unsigned char* id128);
+bosp_status bosp_comm_init_nccl(const unsigned char* id128, int32_t nranks, int32_t rank,
+                                int64_t n_global, int64_t row0);
+bosp_status bosp_comm_free(void);
+
+/* A global operator for the in-process driver (each rank slices it). kind: 0 dense, 1 csr,
+ * 2 stencil (the stencil's s0/s_global must be 0). */
+typedef struct {
+    int32_t kind;
+    int64_t n;
+    const double* dense;
+    const int64_t* rowptr;
+    const int64_t* colidx;
+    const double* vals;
+    bosp_stencil stencil;
+} bosp_global_op;
+
+/* nranks row-partitioned ranks as threads of this process over ngpus devices (round-robin;
+ * <= 0: all visible).  Several ranks may share a GPU.  Outputs as bosp_solve, eigenvectors in
+ * global row order; stats: max wall/device time over ranks. */
+bosp_status bosp_solve_multi(int32_t nranks, int32_t ngpus, const bosp_global_op* K,
+                             const bosp_global_op* M, const bosp_config* cfg, int64_t r,
+                             const double* x0, const double* y0, int64_t cap, double* lambdas,
+                             double* x, double* y, double* residuals, int64_t* nout,
+                             bosp_stats* stats);
 
 /* regression_coefficients (bosp_solver.cpp:538-580); history rows x cols row-major. */
 bosp_status bosp_regression(const double* history, int64_t rows, int64_t cols, int64_t idx,

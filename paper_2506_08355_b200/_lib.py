@@ -63,7 +63,13 @@ class Stats(C.Structure):
 class Stencil(C.Structure):
     _fields_ = [("nx", C.c_int64), ("ny", C.c_int64), ("nz", C.c_int64), ("bc", C.c_int32),
                 ("scale", C.c_double), ("potential", C.c_int32), ("origin", C.c_double),
-                ("h", C.c_double), ("v", C.c_void_p)]
+                ("h", C.c_double), ("v", C.c_void_p), ("s0", C.c_int64), ("s_global", C.c_int64),
+                ("nz_global", C.c_int64)]
+
+
+class GlobalOp(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("n", C.c_int64), ("dense", C.c_void_p), ("rowptr", C.c_void_p),
+                ("colidx", C.c_void_p), ("vals", C.c_void_p), ("stencil", Stencil)]
 
 
 # C-ABI symbols declared in include/bosp_b200.h (tests check every one is exported).
@@ -78,7 +84,8 @@ EXPORTED = [
     "bosp_cholesky", "bosp_profile_enable", "bosp_profile_collect", "bosp_launch_count",
     "bosp_launch_reset", "bosp_launch_families", "bosp_device_sync", "bosp_host_alloc",
     "bosp_host_free", "bosp_set_device", "bosp_flush_l2", "bosp_seed_blocks",
-    "bosp_bench_apply", "bosp_bench_blas", "bosp_bench_cg",
+    "bosp_bench_apply", "bosp_bench_blas", "bosp_bench_cg", "bosp_op_csr_rows", "bosp_op_dense_rows",
+    "bosp_comm_nccl_unique_id", "bosp_comm_init_nccl", "bosp_comm_free", "bosp_solve_multi",
 ]
 
 

@@ -33,6 +33,16 @@ def _p(a):
     return None if a is None else C.c_void_p(a.ctypes.data)
 
 
+def _stencil_spec(nx, ny, nz, bc, scale, potential="none", origin=0.0, h=1.0, v=None, s0=0, s_global=0,
+                  nz_global=0):
+    bcs = {"neumann": 0, "dirichlet": 1}[bc]
+    pot = {"none": 0, "harmonic": 1, "array": 2}[potential]
+    vv = None if v is None else np.ascontiguousarray(v, dtype=np.float64)
+    spec = L.Stencil(nx, ny, nz, bcs, scale, pot, origin, h, None if vv is None else vv.ctypes.data,
+                     s0, s_global, nz_global)
+    return spec, vv
+
+
 class LinearOperator:
     """Apply-only operator (linear_operator.hpp:15-48); data lives in HBM."""
     dense, sparse_csr, matrix_free_callback = 0, 1, 2
@@ -81,12 +91,31 @@ class LinearOperator:
         return cls._make(lib().bosp_op_callback, C.c_int64(dim), cb, None, keep=cb)
 
     @classmethod
-    def stencil(cls, nx, ny, nz, bc, scale, potential="none", origin=0.0, h=1.0, v=None):
-        bcs = {"neumann": 0, "dirichlet": 1}[bc]
-        pot = {"none": 0, "harmonic": 1, "array": 2}[potential]
-        vv = None if v is None else np.ascontiguousarray(v, dtype=np.float64)
-        spec = L.Stencil(nx, ny, nz, bcs, scale, pot, origin, h, None if vv is None else vv.ctypes.data)
+    def stencil(cls, nx, ny, nz, bc, scale, potential="none", origin=0.0, h=1.0, v=None,
+                s0=0, s_global=0, nz_global=0):
+        """Matrix-free stencil.  s_global > 0: this rank's slab of slow-axis planes
+        [s0, s0 + nz) (3-D; grid rows for 2-D) out of s_global, under an attached communicator."""
+        spec, vv = _stencil_spec(nx, ny, nz, bc, scale, potential, origin, h, v, s0, s_global, nz_global)
         return cls._make(lib().bosp_op_stencil, C.byref(spec), keep=vv)
+
+    @classmethod
+    def from_csr_rows(cls, n_global, row0, rowptr, colidx, vals):
+        """Rows [row0, row0 + n_local) of a global CSR operator (global column indices); rowptr
+        may keep the global offsets.  Needs an attached communicator (comm_init_nccl)."""
+        rp = np.ascontiguousarray(rowptr, dtype=np.int64)
+        ci = np.ascontiguousarray(colidx, dtype=np.int64)
+        vv = np.ascontiguousarray(vals, dtype=np.float64)
+        return cls._make(lib().bosp_op_csr_rows, C.c_int64(n_global), C.c_int64(row0),
+                         C.c_int64(rp.shape[0] - 1), _p(rp), _p(ci), _p(vv))
+
+    @classmethod
+    def from_dense_rows(cls, n_global, row0, a_rows):
+        """Rows [row0, row0 + n_local) of a dense n_global x n_global operator (n_local x n_global)."""
+        a = _f(a_rows)
+        if a.shape[1] != n_global:
+            raise ContractViolation("from_dense_rows: a_rows must have n_global columns")
+        return cls._make(lib().bosp_op_dense_rows, C.c_int64(n_global), C.c_int64(row0),
+                         C.c_int64(a.shape[0]), _p(a))
 
     @classmethod
     def from_stencil(cls, s):
@@ -224,6 +253,106 @@ def solve(K: LinearOperator, M: LinearOperator, ip: InnerProduct | None, cfg: Bo
     stats = {f[0]: getattr(st, f[0]) for f in L.Stats._fields_}
     return EigenResult(lam[:k], None if x is None else x[:, :k], None if y is None else y[:, :k],
                        int(st.iterations), res[:k], hist[:min(hrows.value, history_cap)],
+                       bool(st.converged), int(st.nev_converged), stats)
+
+
+# ---- row-partitioned ranks ---------------------------------------------------------------
+def comm_nccl_unique_id() -> bytes:
+    """ncclGetUniqueId: rank 0 creates it and broadcasts the 128 bytes (e.g. torch.distributed)."""
+    buf = (C.c_ubyte * 128)()
+    check(lib().bosp_comm_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def comm_init_nccl(uid: bytes, nranks: int, rank: int, n_global: int, row0: int):
+    """Attach an NCCL communicator and this rank's row window [row0, ...) to the calling thread;
+    afterwards solve() on partitioned operators returns this rank's rows of x, y."""
+    buf = (C.c_ubyte * 128).from_buffer_copy(uid)
+    check(lib().bosp_comm_init_nccl(buf, C.c_int32(nranks), C.c_int32(rank), C.c_int64(n_global),
+                                    C.c_int64(row0)))
+
+
+def comm_free():
+    check(lib().bosp_comm_free())
+
+
+def row_slice(op, nranks, rank):
+    """Rows (row0, n_local) and slow-axis planes (s0, count) of one rank; the rule the native
+    driver uses (multi.cpp row_slice): balanced rows, or balanced z-planes / grid rows."""
+    from .problems import Stencil
+    if isinstance(op, Stencil):
+        three = op.nz > 1
+        sg = op.nz if three else op.ny
+        plane = op.nx * op.ny if three else op.nx
+        s0 = sg * rank // nranks
+        cnt = sg * (rank + 1) // nranks - s0
+        return s0 * plane, cnt * plane, s0, cnt
+    n = op.n if hasattr(op, "n") and not isinstance(op, np.ndarray) else np.asarray(op).shape[0]
+    r0 = n * rank // nranks
+    return r0, n * (rank + 1) // nranks - r0, 0, 0
+
+
+def local_operator(op, nranks, rank):
+    """This rank's LinearOperator slice of a global problems.Csr / problems.Stencil / dense array."""
+    from .problems import Csr, Stencil
+    row0, nl, s0, cnt = row_slice(op, nranks, rank)
+    if isinstance(op, Stencil):
+        three = op.nz > 1
+        v = None if op.v is None else np.asarray(op.v)[row0:row0 + nl]
+        return LinearOperator.stencil(op.nx, op.ny if three else cnt, cnt if three else 1, op.bc, op.scale,
+                                      op.potential, op.origin, op.h, v, s0=s0,
+                                      s_global=op.nz if three else op.ny, nz_global=op.nz)
+    if isinstance(op, Csr):
+        rp = op.rowptr[row0:row0 + nl + 1]
+        return LinearOperator.from_csr_rows(op.n, row0, rp, op.colidx[rp[0]:rp[-1]], op.vals[rp[0]:rp[-1]])
+    a = np.asarray(op, dtype=np.float64)
+    return LinearOperator.from_dense_rows(a.shape[0], row0, a[row0:row0 + nl])
+
+
+def _global_op(op):
+    from .problems import Csr, Stencil
+    g = L.GlobalOp()
+    keep = []
+    if isinstance(op, Stencil):
+        spec, vv = _stencil_spec(op.nx, op.ny, op.nz, op.bc, op.scale, op.potential, op.origin, op.h, op.v)
+        g.kind, g.n, g.stencil = 2, op.n, spec
+        keep.append(vv)
+    elif isinstance(op, Csr):
+        rp = np.ascontiguousarray(op.rowptr, dtype=np.int64)
+        ci = np.ascontiguousarray(op.colidx, dtype=np.int64)
+        vv = np.ascontiguousarray(op.vals, dtype=np.float64)
+        g.kind, g.n, g.rowptr, g.colidx, g.vals = 1, op.n, rp.ctypes.data, ci.ctypes.data, vv.ctypes.data
+        keep += [rp, ci, vv]
+    else:
+        a = _f(op)
+        g.kind, g.n, g.dense = 0, a.shape[0], a.ctypes.data
+        keep.append(a)
+    return g, keep
+
+
+def solve_multi(nranks, K, M, cfg: BospConfig, ns: GeneralizedNullspace | None = None, ngpus=0) -> EigenResult:
+    """Row-partitioned solve: nranks ranks as threads of this process over ngpus devices
+    (several may share one GPU).  K, M: global problems.Csr / problems.Stencil / dense arrays."""
+    gk, kk = _global_op(K)
+    gm, km = _global_op(M)
+    n = gk.n
+    cap = cfg.nev
+    lam, res = np.zeros(cap), np.zeros(cap)
+    x = np.zeros((n, cap), order="F")
+    y = np.zeros((n, cap), order="F")
+    nout, st, cc = C.c_int64(), L.Stats(), cfg.c()
+    if ns is None:
+        r, x0, y0 = -1, None, None
+    else:
+        x0, y0 = _f(ns.x0), _f(ns.y0)
+        r = x0.shape[1]
+    check(lib().bosp_solve_multi(C.c_int32(nranks), C.c_int32(ngpus), C.byref(gk), C.byref(gm), C.byref(cc),
+                                 C.c_int64(r), _p(x0), _p(y0), C.c_int64(cap), _p(lam), _p(x), _p(y), _p(res),
+                                 C.byref(nout), C.byref(st)))
+    del kk, km
+    k = nout.value
+    stats = {f[0]: getattr(st, f[0]) for f in L.Stats._fields_}
+    return EigenResult(lam[:k], x[:, :k], y[:, :k], int(st.iterations), res[:k], np.zeros((0, cfg.nev)),
                        bool(st.converged), int(st.nev_converged), stats)
 
 

@@ -60,7 +60,11 @@ struct StencilSpec {
     double scale = 1.0;
     enum class Potential { none = 0, harmonic = 1, array = 2 } potential = Potential::none;
     double origin = 0.0, h = 1.0;
-    std::vector<double> v;  // potential == array
+    std::vector<double> v;  // potential == array (local rows)
+    // Row partition along the slowest axis (z for 3-D, y for 2-D): this rank holds slow planes
+    // [s0, s0 + nz) (3-D) or [s0, s0 + ny) (2-D) of s_global; nz_global = global z extent.
+    // s_global = 0: unpartitioned.
+    int64_t s0 = 0, s_global = 0, nz_global = 0;
 };
 
 class OperatorImpl;
@@ -86,6 +90,14 @@ public:
     static LinearOperator scaled_identity(int64_t dim, double alpha);
     static LinearOperator diagonal(std::vector<double> d);
     static LinearOperator shifted(const LinearOperator& a, double sigma);
+    // Row-partitioned operators (one rank = one thread/process with a communicator, see
+    // comm.hpp): this rank's rows [row0, row0 + n_local) of an n_global operator.
+    static LinearOperator from_csr_rows(int64_t n_global, int64_t row0, int64_t n_local,
+                                        const int64_t* rowptr, const int64_t* colidx_global,
+                                        const double* vals);
+    // a_rows: n_local x n_global column-major (ld n_local)
+    static LinearOperator from_dense_rows(int64_t n_global, int64_t row0, int64_t n_local,
+                                          const double* a_rows);
 
     int64_t dim() const;
     Kind kind() const;

@@ -6,8 +6,10 @@
 #include <string>
 
 #include "api.hpp"
+#include "comm.hpp"
 #include "dense_ops.hpp"
 #include "dev_algos.hpp"
+#include "multi.hpp"
 #include "operators.hpp"
 #include "rng.hpp"
 #include "runtime.hpp"
@@ -70,6 +72,71 @@ bosp::InnerProduct ip_of(bosp_op b) {
 }
 
 bosp_op wrap(bosp::LinearOperator op) { return new bosp_op_s{std::move(op)}; }
+
+void write_result(const bosp::EigenResult& res, const bosp::BospConfig& cfg, int64_t cap, double* lambdas,
+                  double* x, double* y, double* residuals, int64_t* nout, bosp_stats* stats, double* history,
+                  int64_t history_cap, int64_t* history_rows) {
+    const int64_t h = static_cast<int64_t>(res.lambdas.size());
+    bosp::require(h <= cap, "bosp_solve: output capacity too small");
+    *nout = h;
+    for (int64_t j = 0; j < h; ++j) {
+        lambdas[j] = res.lambdas[j];
+        residuals[j] = res.residuals[j];
+    }
+    copy_out(res.x, x);
+    copy_out(res.y, y);
+    if (stats) {
+        const bosp::SolverStats& s = res.stats;
+        stats->iterations = s.iterations;
+        stats->matvec_count = s.matvec_count;
+        stats->step3_matvecs = s.step3_matvecs;
+        stats->step3_vecprods = s.step3_vecprods;
+        stats->max_width_u = s.max_width_u;
+        stats->max_biorth_deviation = s.max_biorth_deviation;
+        stats->max_deflation_crossgram = s.max_deflation_crossgram;
+        stats->final_biorth_deviation = s.final_biorth_deviation;
+        stats->nevconv_monotone = s.nevconv_monotone ? 1 : 0;
+        stats->wall_seconds = s.wall_seconds;
+        stats->nev_converged = res.nev_converged;
+        stats->converged = res.converged ? 1 : 0;
+        stats->device_seconds = s.device_seconds;
+        stats->host_small_seconds = s.host_small_seconds;
+        stats->repairs = s.repairs;
+        stats->cg_iterations = s.cg_iterations;
+        stats->gpu_launches = s.gpu_launches;
+    }
+    if (history_rows) *history_rows = static_cast<int64_t>(res.history.size());
+    if (history) {
+        const int64_t rows = std::min<int64_t>(static_cast<int64_t>(res.history.size()), history_cap);
+        for (int64_t i = 0; i < rows; ++i)
+            for (int64_t j = 0; j < cfg.nev; ++j)
+                history[i * cfg.nev + j] = j < static_cast<int64_t>(res.history[i].size()) ? res.history[i][j] : 0.0;
+    }
+}
+
+bosp::GlobalOp global_of(const bosp_global_op* g) {
+    bosp::GlobalOp o;
+    o.kind = static_cast<bosp::GlobalOp::Kind>(g->kind);
+    o.n = g->n;
+    o.dense = g->dense;
+    o.rowptr = g->rowptr;
+    o.colidx = g->colidx;
+    o.vals = g->vals;
+    if (g->kind == 2) {
+        const bosp_stencil* s = &g->stencil;
+        o.stencil.nx = s->nx;
+        o.stencil.ny = s->ny;
+        o.stencil.nz = s->nz;
+        o.stencil.bc = static_cast<bosp::StencilSpec::Boundary>(s->bc);
+        o.stencil.scale = s->scale;
+        o.stencil.potential = static_cast<bosp::StencilSpec::Potential>(s->potential);
+        o.stencil.origin = s->origin;
+        o.stencil.h = s->h;
+        if (s->potential == 2) o.stencil.v.assign(s->v, s->v + s->nx * s->ny * s->nz);
+        o.n = s->nx * s->ny * s->nz;
+    }
+    return o;
+}
 
 void fill_random(const bosp::DMat& m, uint64_t seed) {
     bosp::DBlock tmp(m.rows, m.cols);
@@ -177,6 +244,9 @@ bosp_status bosp_op_stencil(const bosp_stencil* s, bosp_op* out) {
         sp.origin = s->origin;
         sp.h = s->h;
         if (s->potential == 2) sp.v.assign(s->v, s->v + s->nx * s->ny * s->nz);
+        sp.s0 = s->s0;
+        sp.s_global = s->s_global;
+        sp.nz_global = s->nz_global;
         *out = wrap(bosp::LinearOperator::stencil(sp));
     });
 }
@@ -243,42 +313,57 @@ bosp_status bosp_solve(bosp_op K, bosp_op M, bosp_op B, const bosp_config* c, in
             ns = std::move(g);
         }
         bosp::EigenResult res = bosp::solve(K->op, M->op, ip_of(B), cfg, std::move(ns));
-        const int64_t h = static_cast<int64_t>(res.lambdas.size());
-        bosp::require(h <= cap, "bosp_solve: output capacity too small");
-        *nout = h;
-        for (int64_t j = 0; j < h; ++j) {
-            lambdas[j] = res.lambdas[j];
-            residuals[j] = res.residuals[j];
+        write_result(res, cfg, cap, lambdas, x, y, residuals, nout, stats, history, history_cap, history_rows);
+    });
+}
+
+bosp_status bosp_op_csr_rows(int64_t n_global, int64_t row0, int64_t n_local, const int64_t* rp, const int64_t* ci,
+                             const double* vv, bosp_op* out) {
+    return guarded([&] { *out = wrap(bosp::LinearOperator::from_csr_rows(n_global, row0, n_local, rp, ci, vv)); });
+}
+
+bosp_status bosp_op_dense_rows(int64_t n_global, int64_t row0, int64_t n_local, const double* a, bosp_op* out) {
+    return guarded([&] { *out = wrap(bosp::LinearOperator::from_dense_rows(n_global, row0, n_local, a)); });
+}
+
+bosp_status bosp_comm_nccl_unique_id(unsigned char* id128) {
+    return guarded([&] { bosp::NcclComm::unique_id(id128); });
+}
+
+bosp_status bosp_comm_init_nccl(const unsigned char* id128, int32_t nranks, int32_t rank, int64_t n_global,
+                                int64_t row0) {
+    return guarded([&] {
+        bosp::Runtime& rt = bosp::Runtime::get();
+        rt.set_comm(std::make_shared<bosp::NcclComm>(id128, nranks, rank));
+        rt.set_rows(n_global, row0);
+    });
+}
+
+bosp_status bosp_comm_free(void) {
+    return guarded([&] {
+        bosp::Runtime& rt = bosp::Runtime::get();
+        rt.sync();
+        rt.set_comm(nullptr);
+        rt.set_rows(0, 0);
+    });
+}
+
+bosp_status bosp_solve_multi(int32_t nranks, int32_t ngpus, const bosp_global_op* K, const bosp_global_op* M,
+                             const bosp_config* c, int64_t r, const double* x0, const double* y0, int64_t cap,
+                             double* lambdas, double* x, double* y, double* residuals, int64_t* nout,
+                             bosp_stats* stats) {
+    return guarded([&] {
+        const bosp::BospConfig cfg = cfg_of(c);
+        bosp::GlobalOp k = global_of(K), m = global_of(M);
+        std::optional<bosp::GeneralizedNullspace> ns;
+        if (r >= 0) {
+            ns.emplace();
+            ns->r = r;
+            ns->x0 = host_block(x0, k.n, r);
+            ns->y0 = host_block(y0, k.n, r);
         }
-        copy_out(res.x, x);
-        copy_out(res.y, y);
-        if (stats) {
-            const bosp::SolverStats& s = res.stats;
-            stats->iterations = s.iterations;
-            stats->matvec_count = s.matvec_count;
-            stats->step3_matvecs = s.step3_matvecs;
-            stats->step3_vecprods = s.step3_vecprods;
-            stats->max_width_u = s.max_width_u;
-            stats->max_biorth_deviation = s.max_biorth_deviation;
-            stats->max_deflation_crossgram = s.max_deflation_crossgram;
-            stats->final_biorth_deviation = s.final_biorth_deviation;
-            stats->nevconv_monotone = s.nevconv_monotone ? 1 : 0;
-            stats->wall_seconds = s.wall_seconds;
-            stats->nev_converged = res.nev_converged;
-            stats->converged = res.converged ? 1 : 0;
-            stats->device_seconds = s.device_seconds;
-            stats->host_small_seconds = s.host_small_seconds;
-            stats->repairs = s.repairs;
-            stats->cg_iterations = s.cg_iterations;
-            stats->gpu_launches = s.gpu_launches;
-        }
-        if (history_rows) *history_rows = static_cast<int64_t>(res.history.size());
-        if (history) {
-            const int64_t rows = std::min<int64_t>(static_cast<int64_t>(res.history.size()), history_cap);
-            for (int64_t i = 0; i < rows; ++i)
-                for (int64_t j = 0; j < cfg.nev; ++j)
-                    history[i * cfg.nev + j] = j < static_cast<int64_t>(res.history[i].size()) ? res.history[i][j] : 0.0;
-        }
+        bosp::EigenResult res = bosp::solve_multi(nranks, ngpus, k, m, bosp::InnerProduct{}, cfg, ns);
+        write_result(res, cfg, cap, lambdas, x, y, residuals, nout, stats, nullptr, 0, nullptr);
     });
 }
 

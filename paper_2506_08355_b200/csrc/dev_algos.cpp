@@ -19,13 +19,15 @@ void apply_weight(const InnerProduct& ip, const DMat& b, const DMat& out) {
 }
 
 void ip_gram_dev(const InnerProduct& ip, const DMat& a, const DMat& b, const DMat& g) {
+    Runtime& rt = Runtime::get();
     if (!ip.weighted()) {
         gram(ColList(a), ColList(b), a.rows, g.p, g.ld);
-        return;
+    } else {
+        DBlock wb(b.rows, b.cols);
+        ip.weight()->apply_device(b, wb.view());
+        gram(ColList(a), ColList(wb.view()), a.rows, g.p, g.ld);
     }
-    DBlock wb(b.rows, b.cols);
-    ip.weight()->apply_device(b, wb.view());
-    gram(ColList(a), ColList(wb.view()), a.rows, g.p, g.ld);
+    rt.allreduce(g.p, g.ld * g.cols);  // row-partitioned: sum the per-rank partial Grams
 }
 
 DenseMatrix ip_gram_host(const InnerProduct& ip, const DMat& a, const DMat& b) {
@@ -53,6 +55,7 @@ void dev_biorth_against(const std::vector<DevBasis>& bases, const DMat& w, const
             GramJob jobs[2] = {{ColList(b.q), ColList(w), cw.p, cw.ld},
                                {ColList(b.p), ColList(z), cz.p, cz.ld}};
             gram(jobs, 2, w.rows);
+            Runtime::get().allreduce(c.data(), c.ld() * 2 * m);
         } else {
             ip_gram_dev(ip, b.q, w, cw);
             ip_gram_dev(ip, b.p, z, cz);
@@ -99,6 +102,7 @@ void pair_grams(const DMat& x, const DMat& y, const InnerProduct& ip, DenseMatri
                            {ColList(y), ColList(wy.view()), g.data() + 2 * m * g.ld(), g.ld()}};
         gram(jobs, 3, x.rows);
     }
+    Runtime::get().allreduce(g.data(), g.ld() * 3 * m);
     DenseMatrix all(m, 3 * m);
     to_host(g.view().cols_range(0, 3 * m), all.data(), m);
     gxx = DenseMatrix(m, m);
@@ -265,7 +269,7 @@ void cg_iteration(const LinearOperator& a, const DMat& x, const DMat& r, const D
     // BOSP_CG_MODE: 0 = SpMM with fused p^T A p + update + direction (default),
     //               1 = separate p^T A p kernel, 2 = cooperative single-kernel update
     static const int mode = std::getenv("BOSP_CG_MODE") ? std::atoi(std::getenv("BOSP_CG_MODE")) : 0;
-    if (mode == 2 && p.cols <= 160) {
+    if (mode == 2 && p.cols <= 160 && Runtime::get().nranks() == 1) {
         a.apply_device(p, ap);
         cg_pap(p, ap, sc);
         cg_update_fused(x, r, p, ap, sc, sc.pap, 1, tol, mi);
@@ -273,6 +277,7 @@ void cg_iteration(const LinearOperator& a, const DMat& x, const DMat& r, const D
     }
     const SpmmDot dot{ws.pap_parts(), ws.ticket(), sc.pap};
     if (mode != 1 && a.impl()->apply_dot(p, ap, dot)) {
+        Runtime::get().allreduce(sc.pap, p.cols);  // per-rank p^T A p -> global
         cg_update(x, r, p, ap, sc, tol, mi);
         return;
     }
@@ -292,7 +297,9 @@ DevCgOutcome dev_cg(const LinearOperator& a, const DMat& rhs, const DMat& x, dou
     ws.ensure(rhs.rows, m);
     const DMat r = ws.r.view(), p = ws.p.view(), ap = ws.ap.view();
     const int mi = static_cast<int>(std::min<int64_t>(max_iter, 1 << 30));
-    if (!x0 && a.impl()->capturable() && !std::getenv("BOSP_NO_GRAPHS")) {
+    // one rank: the whole solve is a CUDA graph; several ranks exchange through the
+    // communicator between kernels (host-synchronised for ThreadComm), so the loop is host-driven
+    if (!x0 && rt.nranks() == 1 && a.impl()->capturable() && !std::getenv("BOSP_NO_GRAPHS")) {
         // ---- graph path: the whole solve is one launch, the loop runs on the device ----
         CgGraph* g = nullptr;
         for (CgGraph& c : ws.graphs)

@@ -267,12 +267,10 @@ void launch_gram(const GramJob* jobs, int njobs, int64_t n) {
 
     constexpr int NT = WM * WN * 32;
     constexpr size_t smem = sizeof(double) * kStages * (BM + BN) * kLdK;
-    static bool attr = false;
-    if (!attr) {
+    static unsigned attr_mask = 0;
+    if (rt.first_use(attr_mask))
         BOSP_CUDA(cudaFuncSetAttribute(k_gram<BM, BN, WM, WN>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
     const double flops = 2.0 * n * (double)jobs[0].a.cols() * jobs[0].b.cols() * njobs;
     const double bytes = 8.0 * n * (double)(jobs[0].a.cols() + jobs[0].b.cols()) * njobs;
     {
@@ -421,12 +419,10 @@ void launch_product(const ProductJob* jobs, int njobs, int64_t n) {
     constexpr size_t smem_pipe = sizeof(double) * kStages * (kBK * (BM + 4) + BN * kLdK);
     constexpr size_t smem_epi = sizeof(double) * BN * (BM + 4);
     constexpr size_t smem = smem_pipe > smem_epi ? smem_pipe : smem_epi;
-    static bool attr = false;
-    if (!attr) {
+    static unsigned attr_mask = 0;
+    if (rt.first_use(attr_mask))
         BOSP_CUDA(cudaFuncSetAttribute(k_product<BM, BN, WM, WN>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
     LaunchScope ls("product", bytes, flops);
     const unsigned gx = static_cast<unsigned>(std::min<int64_t>(max_tiles, 65535));
     const unsigned gy = static_cast<unsigned>((max_tiles + gx - 1) / gx);
@@ -584,11 +580,9 @@ void launch_skinny(const ProductJob* jobs, int njobs, int64_t n) {
     prm.kp = std::max(4, (kmax + 3) / 4 * 4);
     prm.ldc = (prm.kp + 15) / 16 * 16 + 4;
     const size_t smem = sizeof(double) * (static_cast<size_t>(BN) * prm.ldc + 2ull * prm.kp * kSkLdM);
-    static int attr_set = 0;
-    if (attr_set < static_cast<int>(smem)) {
+    static unsigned attr_mask = 0;
+    if (rt.first_use(attr_mask))
         BOSP_CUDA(cudaFuncSetAttribute(k_product_skinny<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        attr_set = 200 * 1024;
-    }
     int per_sm = 1;
     BOSP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_product_skinny<BN>, 256, smem));
     const int64_t ctas = std::max<int64_t>(1, std::min<int64_t>(prm.tiles, int64_t(std::max(per_sm, 1)) * rt.sm_count()));

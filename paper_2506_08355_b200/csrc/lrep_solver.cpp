@@ -196,6 +196,7 @@ RitzOut ritz_step(DeviceState& st, const LinearOperator& k, const LinearOperator
     GramJob jobs[2] = {{ColList(u), ColList(st.ku.view()), g.data(), g.ld()},
                        {ColList(v), ColList(st.mv.view()), g.data() + d * g.ld(), g.ld()}};
     gram(jobs, 2, st.n);
+    Runtime::get().allreduce(g.data(), g.ld() * 2 * d);
     DenseMatrix both(d, 2 * d);
     to_host(g.view().cols_range(0, 2 * d), both.data(), d);
     DenseMatrix khat(d, d), mhat(d, d);
@@ -238,7 +239,11 @@ SolverState initialize(const LinearOperator& k, const LinearOperator& m, const I
     if (m.dim() != n) throw ContractViolation("bosp: K and M dimension mismatch");
     if (ns.r > 0 && (ns.x0.dim() != n || ns.x0.cols() != ns.r || ns.y0.dim() != n || ns.y0.cols() != ns.r))
         throw ContractViolation("bosp: nullspace inconsistent with operators");
-    const int64_t budget = n - ns.r;
+    // row-partitioned solves see their local rows; widths follow the global dimension
+    Runtime& rt = Runtime::get();
+    const int64_t n_global = rt.nranks() > 1 ? rt.n_global() : n;
+    const int64_t row0 = rt.nranks() > 1 ? rt.row0() : 0;
+    const int64_t budget = n_global - ns.r;
     if (cfg.nev > budget) throw ContractViolation("bosp: nev exceeds the number of positive eigenvalues");
 
     const int64_t nb = cfg.effective_nb();
@@ -267,7 +272,7 @@ SolverState initialize(const LinearOperator& k, const LinearOperator& m, const I
     // bosp_solver.cpp:144-150) so both solvers start from the same vectors.
     DBlock u(n, cap), v(n, cap);
     const DMat ua = u.cols(0, d), va = v.cols(0, d);
-    mt_fill_uv(cfg.rng_seed, ua, va);  // the exact x,p,w,y,q,z stream, generated in HBM
+    mt_fill_uv(cfg.rng_seed, ua, va, n_global, row0);  // the exact x,p,w,y,q,z stream, in HBM
     dev_biorth_against(deflation_bases(st), ua, va, ip);
     st.U = DBlock(n, cap);
     st.V = DBlock(n, cap);
@@ -287,7 +292,7 @@ bool iterate_once(SolverState& ss, const LinearOperator& k, const LinearOperator
     const int64_t n = st.n;
     const int64_t nb = cfg.effective_nb();
     const bool moving = cfg.effective_moving();
-    const int64_t budget = n - ns.r;
+    const int64_t budget = (Runtime::get().nranks() > 1 ? Runtime::get().n_global() : n) - ns.r;
     ++st.iter;
     ++st.stats.iterations;
 

@@ -31,6 +31,7 @@ void orthonormalize(const DMat& v) {
             DBlock c(j, 1);
             for (int pass = 0; pass < 2; ++pass) {
                 gram(ColList(prev), ColList(vj), v.rows, c.data(), c.ld());
+                Runtime::get().allreduce(c.data(), c.ld());
                 product(ColList(prev), c.data(), c.ld(), 1, vj, -1.0, 1.0);
             }
         }
@@ -39,10 +40,21 @@ void orthonormalize(const DMat& v) {
     }
 }
 
+// Global row count (row-partitioned ranks) or the local one.
+int64_t global_dim(int64_t n) {
+    const Runtime& rt = Runtime::get();
+    return rt.nranks() > 1 ? rt.n_global() : n;
+}
+
+// The full n_global x cols random block is drawn on every rank and each keeps its own rows, so
+// a partitioned run starts from exactly the serial run's vectors.
 void fill_host_uniform(DBlock& b, std::mt19937_64& rng) {
-    BlockVectors h(b.rows(), b.ncols());
+    const Runtime& rt = Runtime::get();
+    const int64_t ng = global_dim(b.rows());
+    BlockVectors h(ng, b.ncols());
     h.fill_uniform(rng);
-    to_device(h.data(), b.rows(), b.ncols(), b.rows(), b.view());
+    const int64_t r0 = rt.nranks() > 1 ? rt.row0() : 0;
+    to_device(h.data() + r0, b.rows(), b.ncols(), ng, b.view());
 }
 
 }  // namespace
@@ -72,7 +84,8 @@ GeneralizedNullspace compute_nullspace(const LinearOperator& k, const LinearOper
     if (m.dim() != n) throw ContractViolation("compute_nullspace: K and M dimension mismatch");
     const double knorm = std::max(estimate_operator_norm(k, 50, 12345), 1e-300);
     const double zero_thresh = tol_null * knorm;
-    int64_t block = std::min<int64_t>(r_hint ? *r_hint + 1 : 3, n);
+    const int64_t ng = global_dim(n);
+    int64_t block = std::min<int64_t>(r_hint ? *r_hint + 1 : 3, ng);
     std::mt19937_64 rng(seed);
     CgWorkspace ws;
     for (;;) {
@@ -85,7 +98,7 @@ GeneralizedNullspace compute_nullspace(const LinearOperator& k, const LinearOper
         std::vector<double> rayleigh(static_cast<size_t>(block), knorm), resid(static_cast<size_t>(block), knorm);
         double prev_min = std::numeric_limits<double>::infinity();
         for (int outer = 0; outer < 300; ++outer) {
-            dev_cg(shifted, v.view(), tmp.view(), 1e-10, 10 * n, ws);
+            dev_cg(shifted, v.view(), tmp.view(), 1e-10, 10 * ng, ws);
             copy_block(tmp.view(), v.view());
             orthonormalize(v.view());
             k.apply_device(v.view(), kv.view());
@@ -133,8 +146,8 @@ GeneralizedNullspace compute_nullspace(const LinearOperator& k, const LinearOper
         int64_t r = 0;
         for (int64_t j = 0; j < block; ++j)
             if (std::fabs(rayleigh[j]) < zero_thresh) ++r;
-        if (r == block && block < n) {
-            block = std::min(n, block * 2);
+        if (r == block && block < ng) {
+            block = std::min(ng, block * 2);
             continue;
         }
         if (r_hint && r != *r_hint)
@@ -150,7 +163,7 @@ GeneralizedNullspace compute_nullspace(const LinearOperator& k, const LinearOper
         for (int64_t j = 0; j < block; ++j)
             if (std::fabs(rayleigh[j]) < zero_thresh) copy_block(v.cols(j, 1), xr.cols(at++, 1));
         apply_weight(ip, xr.view(), rhs.view());
-        dev_cg(m, rhs.view(), yr.view(), 1e-12, 10 * n, ws);
+        dev_cg(m, rhs.view(), yr.view(), 1e-12, 10 * ng, ws);
         DenseMatrix gram_h = ip_gram_host(ip, xr.view(), yr.view()).symmetrized();
         auto chol = cholesky_lower(gram_h);
         if (!chol) throw InvalidNullspace("compute_nullspace: nullspace Gram matrix is not SPD");

@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cstring>
 
+#include "comm.hpp"
 #include "dense_ops.hpp"
 #include "runtime.hpp"
 
@@ -77,8 +78,18 @@ T* upload(const T* host, size_t count) {
 }
 
 struct DevFree {
-    void* p;
-    ~DevFree() { Runtime::get().free(p); }
+    void* p = nullptr;
+    DevFree(void* q = nullptr) : p(q) {}
+    DevFree(DevFree&& o) noexcept : p(o.p) { o.p = nullptr; }
+    DevFree& operator=(DevFree&& o) noexcept {
+        std::swap(p, o.p);
+        return *this;
+    }
+    DevFree(const DevFree&) = delete;
+    DevFree& operator=(const DevFree&) = delete;
+    ~DevFree() {
+        if (p) Runtime::get().free(p);
+    }
 };
 
 // Dense operator.  A^T is stored (transposed once on the device at construction), so
@@ -100,59 +111,281 @@ private:
     DBlock t_;
 };
 
-class CsrOp final : public OperatorImpl {
-public:
-    CsrOp(int64_t n, const int64_t* rp, const int64_t* ci, const double* vv)
-        : OperatorImpl(n, LinearOperator::Kind::sparse_csr) {
+// CSR (rows rp[0..n], entries from rp[0]) -> SELL-32 in HBM.  Column indices are taken as given
+// (a row-partitioned operator passes them already remapped to [local | halo]).
+struct SellStore {
+    DevFree sp{nullptr}, sw{nullptr}, col{nullptr}, val{nullptr};
+    SellDev dev;
+    SellStore(int64_t n, const int64_t* rp, const int64_t* ci, const double* vv) {
         require(n < (int64_t(1) << 31), "from_csr: dimension exceeds int32 device indices");
+        const int64_t base = rp[0];
         const int64_t nsl = (n + 31) / 32;
-        std::vector<int64_t> sp(static_cast<size_t>(nsl + 1), 0);
-        std::vector<int32_t> sw(static_cast<size_t>(nsl), 0);
+        std::vector<int64_t> spv(static_cast<size_t>(nsl + 1), 0);
+        std::vector<int32_t> swv(static_cast<size_t>(nsl), 0);
         for (int64_t s = 0; s < nsl; ++s) {
             int64_t w = 0;
             for (int64_t r = s * 32; r < std::min(n, s * 32 + 32); ++r) w = std::max(w, rp[r + 1] - rp[r]);
-            sw[s] = static_cast<int32_t>(w);
-            sp[s + 1] = sp[s] + 32 * w;
+            swv[s] = static_cast<int32_t>(w);
+            spv[s + 1] = spv[s] + 32 * w;
         }
-        std::vector<int32_t> col(static_cast<size_t>(sp[nsl]));
-        std::vector<double> val(static_cast<size_t>(sp[nsl]), 0.0);
+        std::vector<int32_t> colv(static_cast<size_t>(spv[nsl]));
+        std::vector<double> valv(static_cast<size_t>(spv[nsl]), 0.0);
         for (int64_t s = 0; s < nsl; ++s)
             for (int64_t l = 0; l < 32; ++l) {
                 const int64_t r = s * 32 + l;
                 const int64_t len = r < n ? rp[r + 1] - rp[r] : 0;
-                for (int64_t k = 0; k < sw[s]; ++k) {
-                    const int64_t at = sp[s] + 32 * k + l;
+                for (int64_t k = 0; k < swv[s]; ++k) {
+                    const int64_t at = spv[s] + 32 * k + l;
                     if (k < len) {
-                        col[at] = static_cast<int32_t>(ci[rp[r] + k]);
-                        val[at] = vv[rp[r] + k];
+                        colv[at] = static_cast<int32_t>(ci[rp[r] - base + k]);
+                        valv[at] = vv[rp[r] - base + k];
                     } else {
-                        col[at] = static_cast<int32_t>(r < n ? r : 0);
-                        val[at] = 0.0;
+                        colv[at] = static_cast<int32_t>(r < n ? r : 0);
+                        valv[at] = 0.0;
                     }
                 }
             }
-        sp_.p = upload(sp.data(), sp.size());
-        sw_.p = upload(sw.data(), sw.size());
-        col_.p = upload(col.data(), col.size());
-        val_.p = upload(val.data(), val.size());
-        dev_.n = n;
-        dev_.nslices = nsl;
-        dev_.slice_ptr = static_cast<const int64_t*>(sp_.p);
-        dev_.slice_w = static_cast<const int32_t*>(sw_.p);
-        dev_.col = static_cast<const int32_t*>(col_.p);
-        dev_.val = static_cast<const double*>(val_.p);
-        dev_.nnz = rp[n];
+        sp.p = upload(spv.data(), spv.size());
+        sw.p = upload(swv.data(), swv.size());
+        col.p = upload(colv.data(), colv.size());
+        val.p = upload(valv.data(), valv.size());
+        dev.n = n;
+        dev.nslices = nsl;
+        dev.slice_ptr = static_cast<const int64_t*>(sp.p);
+        dev.slice_w = static_cast<const int32_t*>(sw.p);
+        dev.col = static_cast<const int32_t*>(col.p);
+        dev.val = static_cast<const double*>(val.p);
+        dev.nnz = rp[n] - base;
         Runtime::get().sync();  // host staging vectors die at scope exit
     }
-    void apply(const DMat& x, const DMat& y) const override { sell_spmm(dev_, x, y); }
+};
+
+class CsrOp final : public OperatorImpl {
+public:
+    CsrOp(int64_t n, const int64_t* rp, const int64_t* ci, const double* vv)
+        : OperatorImpl(n, LinearOperator::Kind::sparse_csr), s_(n, rp, ci, vv) {}
+    void apply(const DMat& x, const DMat& y) const override { sell_spmm(s_.dev, x, y); }
     bool apply_dot(const DMat& x, const DMat& y, const SpmmDot& dot) const override {
-        sell_spmm(dev_, x, y, &dot);
+        sell_spmm(s_.dev, x, y, &dot);
         return true;
     }
 
 private:
-    DevFree sp_{nullptr}, sw_{nullptr}, col_{nullptr}, val_{nullptr};
-    SellDev dev_;
+    SellStore s_;
+};
+
+// ---- row-partitioned operators ---------------------------------------------------------------
+struct RankRange {
+    int64_t row0, n;
+};
+
+// (row0, n) of every rank through the communicator (collective).
+std::vector<RankRange> gather_ranges(int64_t row0, int64_t n) {
+    Runtime& rt = Runtime::get();
+    Comm* c = rt.comm();
+    const int P = c->size();
+    DBlock buf(2, P + 1);
+    const double mine[2] = {static_cast<double>(row0), static_cast<double>(n)};
+    BOSP_CUDA(cudaMemcpyAsync(buf.data() + P * buf.ld(), mine, sizeof(mine), cudaMemcpyHostToDevice, rt.stream()));
+    // contiguous send (2 doubles) -> contiguous receive (2*P doubles)
+    DBlock flat(2 * P, 1);
+    c->allgather(buf.data() + P * buf.ld(), 2, flat.data(), rt.stream());
+    std::vector<double> h(static_cast<size_t>(2 * P));
+    BOSP_CUDA(cudaMemcpyAsync(h.data(), flat.data(), sizeof(double) * 2 * P, cudaMemcpyDeviceToHost, rt.stream()));
+    rt.sync();
+    std::vector<RankRange> out(static_cast<size_t>(P));
+    for (int r = 0; r < P; ++r) out[r] = {static_cast<int64_t>(h[2 * r]), static_cast<int64_t>(h[2 * r + 1])};
+    return out;
+}
+
+// Local rows [row0, row0 + n) of a global CSR.  Columns owned by other ranks are fetched into a
+// halo block before every apply (grouped point-to-point exchange; only the rows actually
+// referenced, planned once at construction) and read by the SpMM kernel from there.
+class CsrRowsOp final : public OperatorImpl {
+public:
+    CsrRowsOp(int64_t n_global, int64_t row0, int64_t n, const int64_t* rp, const int64_t* ci, const double* vv)
+        : OperatorImpl(n, LinearOperator::Kind::sparse_csr) {
+        Runtime& rt = Runtime::get();
+        Comm* comm = rt.comm();
+        require(comm != nullptr, "from_csr_rows: no communicator on this thread");
+        const int P = comm->size(), me = comm->rank();
+        const std::vector<RankRange> rg = gather_ranges(row0, n);
+        auto owner = [&](int64_t c) {
+            for (int r = 0; r < P; ++r)
+                if (c >= rg[r].row0 && c < rg[r].row0 + rg[r].n) return r;
+            throw ContractViolation("from_csr_rows: column outside every rank's rows");
+        };
+        const int64_t base = rp[0], nnz = rp[n] - base;
+        std::vector<std::vector<int64_t>> need(static_cast<size_t>(P));
+        for (int64_t k = 0; k < nnz; ++k) {
+            const int64_t c = ci[k];
+            require(c >= 0 && c < n_global, "from_csr_rows: column index out of range");
+            if (c < row0 || c >= row0 + n) need[owner(c)].push_back(c);
+        }
+        for (auto& v : need) {
+            std::sort(v.begin(), v.end());
+            v.erase(std::unique(v.begin(), v.end()), v.end());
+        }
+        // how many rows every rank needs from every other: P x P counts, allgathered
+        DBlock cnt(P, 1), allc(P * P, 1);
+        std::vector<double> mycnt(static_cast<size_t>(P));
+        for (int r = 0; r < P; ++r) mycnt[r] = static_cast<double>(need[r].size());
+        BOSP_CUDA(cudaMemcpyAsync(cnt.data(), mycnt.data(), sizeof(double) * P, cudaMemcpyHostToDevice, rt.stream()));
+        comm->allgather(cnt.data(), P, allc.data(), rt.stream());
+        std::vector<double> hc(static_cast<size_t>(P * P));
+        BOSP_CUDA(cudaMemcpyAsync(hc.data(), allc.data(), sizeof(double) * P * P, cudaMemcpyDeviceToHost, rt.stream()));
+        rt.sync();
+        // exchange the index lists (as doubles: exact below 2^53)
+        std::vector<DBlock> req_out, req_in;
+        std::vector<HaloMsg> sends, recvs;
+        for (int r = 0; r < P; ++r) {
+            if (r == me) continue;
+            const int64_t out_n = static_cast<int64_t>(need[r].size());
+            const int64_t in_n = static_cast<int64_t>(hc[static_cast<size_t>(r) * P + me]);
+            if (out_n > 0) {
+                std::vector<double> tmp(need[r].begin(), need[r].end());
+                req_out.emplace_back(out_n, 1);
+                BOSP_CUDA(cudaMemcpyAsync(req_out.back().data(), tmp.data(), sizeof(double) * out_n, cudaMemcpyHostToDevice, rt.stream()));
+                rt.sync();
+                sends.push_back({r, req_out.back().data(), out_n});
+            }
+            if (in_n > 0) {
+                req_in.emplace_back(in_n, 1);
+                recvs.push_back({r, req_in.back().data(), in_n});
+            }
+        }
+        comm->exchange(sends, recvs, rt.stream());
+        // send plan: the local rows each peer asked for
+        for (const HaloMsg& m : recvs) {
+            std::vector<double> g(static_cast<size_t>(m.count));
+            BOSP_CUDA(cudaMemcpyAsync(g.data(), m.ptr, sizeof(double) * m.count, cudaMemcpyDeviceToHost, rt.stream()));
+            rt.sync();
+            std::vector<int32_t> loc(static_cast<size_t>(m.count));
+            for (size_t i = 0; i < g.size(); ++i) loc[i] = static_cast<int32_t>(static_cast<int64_t>(g[i]) - row0);
+            SendPlan sp;
+            sp.peer = m.peer;
+            sp.cnt = m.count;
+            sp.idx.p = upload(loc.data(), loc.size());
+            send_.push_back(std::move(sp));
+        }
+        // receive plan + remapped columns: local -> c - row0, halo -> n + offset(owner) + position
+        std::vector<int64_t> off(static_cast<size_t>(P), 0);
+        n_halo_ = 0;
+        for (int r = 0; r < P; ++r) {
+            off[r] = n_halo_;
+            if (r != me && !need[r].empty()) {
+                recv_.push_back({r, static_cast<int64_t>(need[r].size()), n_halo_});
+                n_halo_ += static_cast<int64_t>(need[r].size());
+            }
+        }
+        std::vector<int64_t> cir(static_cast<size_t>(nnz));
+        for (int64_t k = 0; k < nnz; ++k) {
+            const int64_t c = ci[k];
+            if (c >= row0 && c < row0 + n) {
+                cir[k] = c - row0;
+            } else {
+                const int o = owner(c);
+                const auto it = std::lower_bound(need[o].begin(), need[o].end(), c);
+                cir[k] = n + off[o] + (it - need[o].begin());
+            }
+        }
+        std::vector<int64_t> rpl(rp, rp + n + 1);
+        store_ = std::make_unique<SellStore>(n, rpl.data(), cir.data(), vv);
+        Runtime::get().sync();
+    }
+    void apply(const DMat& x, const DMat& y) const override { sell_spmm(with_halo(x), x, y); }
+    bool apply_dot(const DMat& x, const DMat& y, const SpmmDot& dot) const override {
+        sell_spmm(with_halo(x), x, y, &dot);
+        return true;
+    }
+    bool capturable() const override { return false; }
+
+private:
+    struct SendPlan {
+        int peer = 0;
+        int64_t cnt = 0;
+        DevFree idx{nullptr};
+    };
+    struct RecvPlan {
+        int peer;
+        int64_t cnt, off;
+    };
+    SellDev with_halo(const DMat& x) const {
+        Runtime& rt = Runtime::get();
+        const int64_t m = x.cols;
+        if (!halo_ || halo_->capacity() < m) {
+            halo_ = std::make_unique<DBlock>(std::max<int64_t>(n_halo_, 1), m);
+            sbuf_.clear();
+            rbuf_.clear();
+            for (const SendPlan& s : send_) sbuf_.emplace_back(s.cnt, m);
+            for (const RecvPlan& r : recv_) rbuf_.emplace_back(r.cnt, m);
+        }
+        std::vector<HaloMsg> sends, recvs;
+        for (size_t i = 0; i < send_.size(); ++i) {
+            gather_rows(x.p, x.ld, static_cast<const int32_t*>(send_[i].idx.p), send_[i].cnt, m, sbuf_[i].data(),
+                        send_[i].cnt, rt.stream());
+            sends.push_back({send_[i].peer, sbuf_[i].data(), send_[i].cnt * m});
+        }
+        for (size_t i = 0; i < recv_.size(); ++i) recvs.push_back({recv_[i].peer, rbuf_[i].data(), recv_[i].cnt * m});
+        rt.comm()->exchange(sends, recvs, rt.stream());
+        const int64_t ldh = halo_->ld();
+        for (size_t i = 0; i < recv_.size(); ++i)
+            BOSP_CUDA(cudaMemcpy2DAsync(halo_->data() + recv_[i].off, ldh * sizeof(double), rbuf_[i].data(),
+                                        recv_[i].cnt * sizeof(double), recv_[i].cnt * sizeof(double), m,
+                                        cudaMemcpyDeviceToDevice, rt.stream()));
+        SellDev d = store_->dev;
+        d.halo = halo_->data();
+        d.ldh = ldh;
+        return d;
+    }
+    std::unique_ptr<SellStore> store_;
+    std::vector<SendPlan> send_;
+    std::vector<RecvPlan> recv_;
+    int64_t n_halo_ = 0;
+    mutable std::unique_ptr<DBlock> halo_;
+    mutable std::vector<DBlock> sbuf_, rbuf_;
+};
+
+// Rows [row0, row0 + n) of a dense operator: stores (A_rows)^T (n_global x n); every apply
+// allgathers x and runs the split-K Gram over the full dimension.
+class DenseRowsOp final : public OperatorImpl {
+public:
+    DenseRowsOp(int64_t n_global, int64_t row0, int64_t n, const double* a_rows)
+        : OperatorImpl(n, LinearOperator::Kind::dense), t_(n_global, n), ng_(n_global) {
+        (void)row0;
+        DBlock staged(n, n_global);
+        to_device(a_rows, n, n_global, n, staged.view());
+        transpose(staged.view(), t_.view());
+        rg_ = gather_ranges(row0, n);
+        for (const RankRange& r : rg_) nmax_ = std::max(nmax_, r.n);
+        Runtime::get().sync();
+    }
+    void apply(const DMat& x, const DMat& y) const override {
+        Runtime& rt = Runtime::get();
+        const int64_t m = x.cols, P = static_cast<int64_t>(rg_.size());
+        if (!full_ || full_->capacity() < m) {
+            full_ = std::make_unique<DBlock>(ng_, m);
+            send_ = std::make_unique<DBlock>(nmax_ * m, 1);
+            recv_ = std::make_unique<DBlock>(P * nmax_ * m, 1);
+        }
+        BOSP_CUDA(cudaMemcpy2DAsync(send_->data(), nmax_ * sizeof(double), x.p, x.ld * sizeof(double),
+                                    x.rows * sizeof(double), m, cudaMemcpyDeviceToDevice, rt.stream()));
+        rt.comm()->allgather(send_->data(), nmax_ * m, recv_->data(), rt.stream());
+        for (int64_t r = 0; r < P; ++r)
+            if (rg_[r].n > 0)
+                BOSP_CUDA(cudaMemcpy2DAsync(full_->data() + rg_[r].row0, full_->ld() * sizeof(double),
+                                            recv_->data() + r * nmax_ * m, nmax_ * sizeof(double),
+                                            rg_[r].n * sizeof(double), m, cudaMemcpyDeviceToDevice, rt.stream()));
+        gram(ColList(t_.view()), ColList(full_->cols(0, m)), ng_, y.p, y.ld);
+    }
+    bool capturable() const override { return false; }
+
+private:
+    DBlock t_;
+    int64_t ng_;
+    std::vector<RankRange> rg_;
+    int64_t nmax_ = 0;
+    mutable std::unique_ptr<DBlock> full_, send_, recv_;
 };
 
 class StencilOp final : public OperatorImpl {
@@ -162,27 +395,72 @@ public:
         dev_.nx = s.nx;
         dev_.ny = s.ny;
         dev_.nz = s.nz;
+        // 3-D when the *global* grid has several z planes (a slab may hold a single plane)
+        dev_.dims = (s.s_global > 0 ? s.nz_global : s.nz) > 1 ? 3 : 2;
         dev_.bc = static_cast<int32_t>(s.bc);
         dev_.scale = s.scale;
         dev_.potential = static_cast<int32_t>(s.potential);
         dev_.origin = s.origin;
         dev_.h = s.h;
+        dev_.s0 = s.s0;
+        dev_.s_global = s.s_global;
         if (s.potential == StencilSpec::Potential::array) {
             require(static_cast<int64_t>(s.v.size()) == dim(), "stencil: potential array size mismatch");
             v_.p = upload(s.v.data(), s.v.size());
             dev_.v = static_cast<const double*>(v_.p);
             Runtime::get().sync();
         }
+        const int64_t snl = dev_.dims == 3 ? s.nz : s.ny;
+        partitioned_ = s.s_global > 0 && (s.s0 > 0 || s.s0 + snl < s.s_global);
     }
-    void apply(const DMat& x, const DMat& y) const override { stencil_spmm(dev_, x, y); }
+    void apply(const DMat& x, const DMat& y) const override { stencil_spmm(with_halo(x), x, y); }
     bool apply_dot(const DMat& x, const DMat& y, const SpmmDot& dot) const override {
-        stencil_spmm(dev_, x, y, &dot);
+        stencil_spmm(with_halo(x), x, y, &dot);
         return true;
     }
+    bool capturable() const override { return !partitioned_; }
 
 private:
+    // Slab partition along the slowest axis: exchange the first / last local plane of every
+    // column with the ranks holding the neighbouring slabs (rank - 1 below, rank + 1 above).
+    StencilDev with_halo(const DMat& x) const {
+        if (!partitioned_) return dev_;
+        Runtime& rt = Runtime::get();
+        const int me = rt.comm()->rank();
+        const int64_t plane = dev_.dims == 3 ? dev_.nx * dev_.ny : dev_.nx;
+        const int64_t snl = dev_.dims == 3 ? dev_.nz : dev_.ny;
+        const int64_t m = x.cols;
+        if (!lo_ || lo_->capacity() < m) {
+            lo_ = std::make_unique<DBlock>(plane, m);
+            hi_ = std::make_unique<DBlock>(plane, m);
+            slo_ = std::make_unique<DBlock>(plane, m);
+            shi_ = std::make_unique<DBlock>(plane, m);
+        }
+        const bool has_lo = dev_.s0 > 0, has_hi = dev_.s0 + snl < dev_.s_global;
+        std::vector<HaloMsg> sends, recvs;
+        const size_t pb = plane * sizeof(double);
+        if (has_lo) {
+            BOSP_CUDA(cudaMemcpy2DAsync(slo_->data(), pb, x.p, x.ld * sizeof(double), pb, m,
+                                        cudaMemcpyDeviceToDevice, rt.stream()));
+            sends.push_back({me - 1, slo_->data(), plane * m});
+            recvs.push_back({me - 1, lo_->data(), plane * m});
+        }
+        if (has_hi) {
+            BOSP_CUDA(cudaMemcpy2DAsync(shi_->data(), pb, x.p + (snl - 1) * plane, x.ld * sizeof(double), pb, m,
+                                        cudaMemcpyDeviceToDevice, rt.stream()));
+            sends.push_back({me + 1, shi_->data(), plane * m});
+            recvs.push_back({me + 1, hi_->data(), plane * m});
+        }
+        rt.comm()->exchange(sends, recvs, rt.stream());
+        StencilDev d = dev_;
+        d.halo_lo = has_lo ? lo_->data() : nullptr;
+        d.halo_hi = has_hi ? hi_->data() : nullptr;
+        return d;
+    }
     DevFree v_{nullptr};
     StencilDev dev_;
+    bool partitioned_ = false;
+    mutable std::unique_ptr<DBlock> lo_, hi_, slo_, shi_;
 };
 
 class ScaledIdentityOp final : public OperatorImpl {
@@ -275,6 +553,21 @@ LinearOperator LinearOperator::from_csr(const SparseMatrixCSR& a) {
 }
 LinearOperator LinearOperator::from_csr(int64_t n, const int64_t* rp, const int64_t* ci, const double* vv) {
     return LinearOperator(std::make_shared<CsrOp>(n, rp, ci, vv));
+}
+LinearOperator LinearOperator::from_csr_rows(int64_t n_global, int64_t row0, int64_t n_local, const int64_t* rp,
+                                             const int64_t* ci, const double* vv) {
+    if (Runtime::get().nranks() == 1) {  // one rank: plain local CSR
+        require(row0 == 0 && n_local == n_global, "from_csr_rows: partial rows without a communicator");
+        return from_csr(n_local, rp, ci, vv);
+    }
+    return LinearOperator(std::make_shared<CsrRowsOp>(n_global, row0, n_local, rp, ci, vv));
+}
+LinearOperator LinearOperator::from_dense_rows(int64_t n_global, int64_t row0, int64_t n_local, const double* a) {
+    if (Runtime::get().nranks() == 1) {
+        require(row0 == 0 && n_local == n_global, "from_dense_rows: partial rows without a communicator");
+        return from_dense(a, n_local);
+    }
+    return LinearOperator(std::make_shared<DenseRowsOp>(n_global, row0, n_local, a));
 }
 LinearOperator LinearOperator::from_callback(int64_t dim, ApplyFn fn) {
     return LinearOperator(std::make_shared<HostCallbackOp>(dim, std::move(fn)));

@@ -27,7 +27,8 @@ __device__ __forceinline__ unsigned long long mt_mag(unsigned long long x) {
 }
 
 __global__ void __launch_bounds__(320) k_mt_fill(MtSeed seed, double* u, int64_t ldu, double* v,
-                                                  int64_t ldv, int64_t n, int64_t d) {
+                                                  int64_t ldv, int64_t n, int64_t d, int64_t row0,
+                                                  int64_t nloc) {
     __shared__ unsigned long long mt[kN];
     const int t = threadIdx.x;
     if (t < kN) mt[t] = seed.mt[t];
@@ -67,9 +68,12 @@ __global__ void __launch_bounds__(320) k_mt_fill(MtSeed seed, double* u, int64_t
                 double r = __ull2double_rn(y) * 0x1p-64;
                 if (r >= 1.0) r = 0x1.fffffffffffffp-1;
                 r = __dadd_rn(__dmul_rn(r, 2.0), -1.0);
-                const int64_t c = k / n, row = k - c * n;
-                if (c < d) u[c * ldu + row] = r;
-                else v[(c - d) * ldv + row] = r;
+                const int64_t c = k / n, grow = k - c * n;   // global row of this draw
+                const int64_t row = grow - row0;            // this rank keeps its window
+                if (row >= 0 && row < nloc) {
+                    if (c < d) u[c * ldu + row] = r;
+                    else v[(c - d) * ldv + row] = r;
+                }
             }
         }
         // no barrier needed here: the next step only reads mt[] before its first barrier
@@ -78,7 +82,8 @@ __global__ void __launch_bounds__(320) k_mt_fill(MtSeed seed, double* u, int64_t
 
 }  // namespace
 
-void mt_fill_uv(uint64_t seed, const DMat& u, const DMat& v) {
+void mt_fill_uv(uint64_t seed, const DMat& u, const DMat& v, int64_t n_global, int64_t row0) {
+    if (n_global <= 0) n_global = u.rows;
     require(u.rows == v.rows && u.cols == v.cols, "mt_fill_uv: U and V must have equal shape");
     if (u.rows == 0 || u.cols == 0) return;
     MtSeed s;
@@ -86,7 +91,7 @@ void mt_fill_uv(uint64_t seed, const DMat& u, const DMat& v) {
     for (int i = 1; i < kN; ++i) s.mt[i] = 6364136223846793005ULL * (s.mt[i - 1] ^ (s.mt[i - 1] >> 62)) + i;
     Runtime& rt = Runtime::get();
     LaunchScope ls("rng", 16.0 * u.rows * u.cols, 0.0);
-    k_mt_fill<<<1, 320, 0, rt.stream()>>>(s, u.p, u.ld, v.p, v.ld, u.rows, u.cols);
+    k_mt_fill<<<1, 320, 0, rt.stream()>>>(s, u.p, u.ld, v.p, v.ld, n_global, u.cols, row0, u.rows);
     BOSP_LAUNCH_CHECK();
 }
 

@@ -13,8 +13,10 @@ void throw_cuda(cudaError_t e, const char* what, const char* file, int line) {
     throw CudaError(buf);
 }
 
+Comm::~Comm() = default;
+
 Runtime& Runtime::get() {
-    static Runtime rt;
+    thread_local Runtime rt;
     return rt;
 }
 

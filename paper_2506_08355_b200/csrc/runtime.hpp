@@ -14,9 +14,56 @@
 namespace bosp {
 inline namespace b200 {
 
+// Row-partition communicator: every n-length block of the solve is split by rows across ranks;
+// Grams, dots and residual sums are partial per rank and summed by allreduce_sum (which must give
+// bit-identical results on every rank so all ranks take the same host decisions).  Halo rows of
+// the sparse operators move with sendrecv, dense operators allgather x.
+struct HaloMsg {
+    int peer;
+    double* ptr;    // device buffer (read for sends, written for receives)
+    int64_t count;  // doubles
+};
+
+class Comm {
+public:
+    virtual ~Comm();
+    virtual int rank() const = 0;
+    virtual int size() const = 0;
+    // in place over `count` doubles in device memory, ordered on `stream`; identical result on
+    // every rank
+    virtual void allreduce_sum(double* dev, int64_t count, cudaStream_t stream) = 0;
+    // point-to-point halo exchange: every send must be matched by the peer's receive
+    virtual void exchange(const std::vector<HaloMsg>& sends, const std::vector<HaloMsg>& recvs,
+                          cudaStream_t stream) = 0;
+    // every rank contributes `count` doubles; recv holds size()*count, rank-major
+    virtual void allgather(const double* sdev, int64_t count, double* rdev, cudaStream_t stream) = 0;
+};
+
 class Runtime {
 public:
+    // One runtime per host thread: its own stream, pool, scratch and communicator, so that
+    // several ranks (one thread per GPU, or several virtual ranks on one GPU) never share state.
     static Runtime& get();
+    void set_comm(std::shared_ptr<Comm> c) { comm_ = std::move(c); }
+    Comm* comm() const { return comm_.get(); }
+    int nranks() const { return comm_ ? comm_->size() : 1; }
+    int rank() const { return comm_ ? comm_->rank() : 0; }
+    // Global row window of this rank (row-partitioned solve): rows [row0, row0 + local) of
+    // n_global.  Defaults describe an unpartitioned solve (set by solve()).
+    void set_rows(int64_t n_global, int64_t row0) { n_global_ = n_global; row0_ = row0; }
+    int64_t n_global() const { return n_global_; }
+    int64_t row0() const { return row0_; }
+    // Sum a per-rank partial result across ranks (no-op on one rank).
+    void allreduce(double* dev, int64_t count) {
+        if (comm_ && comm_->size() > 1) comm_->allreduce_sum(dev, count, stream_);
+    }
+    // Per-device one-time kernel attribute setup (bit per device id).
+    bool first_use(unsigned& mask) {
+        const unsigned bit = 1u << (device_ & 31);
+        if (mask & bit) return false;
+        mask |= bit;
+        return true;
+    }
 
     cudaStream_t stream() const { return stream_; }
     int device() const { return device_; }
@@ -68,6 +115,8 @@ private:
     int device_ = 0;
     int sm_count_ = 148;
     cudaStream_t stream_ = nullptr;
+    std::shared_ptr<Comm> comm_;
+    int64_t n_global_ = 0, row0_ = 0;
     double* scratch_ = nullptr;
     size_t scratch_cap_ = 0;
     unsigned int* tickets_ = nullptr;

@@ -17,6 +17,9 @@ struct SellDev {
     const int32_t* col = nullptr;
     const double* val = nullptr;
     int64_t nnz = 0;                     // true nonzeros (for algorithmic byte counts)
+    // row-partitioned: column indices >= n refer to halo row (c - n) of `halo` (ld `ldh`)
+    const double* halo = nullptr;
+    int64_t ldh = 0;
 };
 
 // Fused x(:,j)^T y(:,j) (the CG's p^T A p): per-block partials in `parts` (<= 256 x ncols),
@@ -36,12 +39,19 @@ int sell_spmm(const SellDev& a, const DMat& x, const DMat& y, const SpmmDot* dot
 // (diag = 2*dims).  potential: 0 none, 1 harmonic 0.5|x|^2 with x_i = origin + (i+1)*h,
 // 2 explicit per-node array v.
 struct StencilDev {
-    int64_t nx = 0, ny = 0, nz = 1;
+    int64_t nx = 0, ny = 0, nz = 1;  // local grid (partitioned along the slowest axis)
+    int32_t dims = 3;                // 3 = 7-point (global nz > 1), 2 = 5-point
     int32_t bc = 0;
     double scale = 1.0;
     int32_t potential = 0;
     double origin = 0.0, h = 1.0;
-    const double* v = nullptr;
+    const double* v = nullptr;       // local rows of the explicit potential
+    // row partition along the slowest axis (z for 3-D, y for 2-D): this rank holds slow-axis
+    // planes [s0, s0 + local) of s_global; halo_lo/halo_hi hold the neighbouring planes
+    // (plane = nx*ny (3-D) or nx (2-D) values per column, ld = plane) or are null.
+    int64_t s0 = 0, s_global = 0;
+    const double* halo_lo = nullptr;
+    const double* halo_hi = nullptr;
 };
 int stencil_spmm(const StencilDev& s, const DMat& x, const DMat& y, const SpmmDot* dot = nullptr);
 

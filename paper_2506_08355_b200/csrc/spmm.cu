@@ -159,7 +159,7 @@ struct DotOut {
 // Column-group variant: grid.y walks groups of CB columns, grid.x strides over 256-row tiles;
 // the row's entries are re-read per column group (L2).  Optionally accumulates x^T y per
 // column (the CG's p^T A p) while y is produced.
-template <int CB, bool DOT>
+template <int CB, bool DOT, bool HALO = false>
 __global__ void __launch_bounds__(kRows) k_sell_cb(SellDev a, const double* __restrict__ x, int64_t ldx,
                                                     double* __restrict__ y, int64_t ldy, int ncols,
                                                     KTimer tm, DotOut dots) {
@@ -182,6 +182,13 @@ __global__ void __launch_bounds__(kRows) k_sell_cb(SellDev a, const double* __re
         for (int k = 0; k < w; ++k) {
             const int col = __ldg(a.col + base + 32 * k);
             const double v = __ldg(a.val + base + 32 * k);
+            if (HALO && col >= a.n) {  // row owned by a neighbour rank: read the halo copy
+                const double* hb = a.halo + static_cast<int64_t>(j0) * a.ldh + (col - a.n);
+#pragma unroll
+                for (int c = 0; c < CB; ++c)
+                    if (j0 + c < ncols) acc[c] += v * __ldg(hb + c * a.ldh);
+                continue;
+            }
 #pragma unroll
             for (int c = 0; c < CB; ++c)
                 if (j0 + c < ncols) acc[c] += v * __ldg(xb + c * ldx + col);
@@ -218,10 +225,17 @@ __global__ void __launch_bounds__(kRows) k_stencil(StencilDev st, const double* 
         const int64_t i = idx % st.nx;
         const int64_t jy = (idx / st.nx) % st.ny;
         const int64_t kz = idx / nxy;
+        const int dims = st.dims;
+        // global coordinate along the (partitioned) slowest axis
+        const int64_t sl = dims == 3 ? kz : jy;                   // local slow index
+        const int64_t snl = dims == 3 ? st.nz : st.ny;            // local slow extent
+        const int64_t sg = st.s0 + sl;
+        const int64_t sgn = st.s_global > 0 ? st.s_global : snl;  // global slow extent
+        const int64_t plane = dims == 3 ? nxy : st.nx;            // values per slow plane
         const bool xm = i > 0, xp = i + 1 < st.nx;
-        const bool ym = jy > 0, yp = jy + 1 < st.ny;
-        const bool zm = kz > 0, zp = kz + 1 < st.nz;
-        const int dims = st.nz > 1 ? 3 : 2;
+        const bool ym = dims == 3 ? jy > 0 : sg > 0;
+        const bool yp = dims == 3 ? jy + 1 < st.ny : sg + 1 < sgn;
+        const bool zm = dims == 3 && sg > 0, zp = dims == 3 && sg + 1 < sgn;
         double diag;
         if (st.bc == 0)
             diag = static_cast<double>(xm + xp + ym + yp + (dims == 3 ? (zm + zp) : 0));
@@ -231,13 +245,17 @@ __global__ void __launch_bounds__(kRows) k_stencil(StencilDev st, const double* 
         double pot = 0.0;
         if (st.potential == 1) {
             const double cx = st.origin + (i + 1) * st.h;
-            const double cy = st.origin + (jy + 1) * st.h;
-            const double cz = dims == 3 ? st.origin + (kz + 1) * st.h : 0.0;
+            const double cy = st.origin + ((dims == 3 ? jy : sg) + 1) * st.h;
+            const double cz = dims == 3 ? st.origin + (sg + 1) * st.h : 0.0;
             pot = 0.5 * (cx * cx + cy * cy + cz * cz);
         } else if (st.potential == 2) {
             pot = __ldg(st.v + idx);
         }
         const double dg = diag + pot;
+        const int64_t in_plane = idx - sl * plane;
+        // neighbours across the slow axis: local row, or the neighbour rank's halo plane
+        const bool lo_local = sl > 0, hi_local = sl + 1 < snl;
+        const bool lo = dims == 3 ? zm : ym, hi = dims == 3 ? zp : yp;
 #pragma unroll
         for (int c = 0; c < CB; ++c) {
             if (j0 + c >= ncols) break;
@@ -245,12 +263,12 @@ __global__ void __launch_bounds__(kRows) k_stencil(StencilDev st, const double* 
             double nb = 0.0;
             if (xm) nb += __ldg(xc - 1);
             if (xp) nb += __ldg(xc + 1);
-            if (ym) nb += __ldg(xc - st.nx);
-            if (yp) nb += __ldg(xc + st.nx);
             if (dims == 3) {
-                if (zm) nb += __ldg(xc - nxy);
-                if (zp) nb += __ldg(xc + nxy);
+                if (ym) nb += __ldg(xc - st.nx);
+                if (yp) nb += __ldg(xc + st.nx);
             }
+            if (lo) nb += lo_local ? __ldg(xc - plane) : __ldg(st.halo_lo + static_cast<int64_t>(j0 + c) * plane + in_plane);
+            if (hi) nb += hi_local ? __ldg(xc + plane) : __ldg(st.halo_hi + static_cast<int64_t>(j0 + c) * plane + in_plane);
             const double xs = __ldg(xc);
             const double yv = dg * xs - st.scale * nb;
             y[(j0 + c) * ldy + idx] = yv;
@@ -287,9 +305,16 @@ int sell_spmm(const SellDev& a, const DMat& x, const DMat& y, const SpmmDot* dot
     // bandwidth of the all-columns-per-thread variant (k_sell) on config 2 (B200).
     static const int variant = std::getenv("BOSP_SPMM_CB") ? std::atoi(std::getenv("BOSP_SPMM_CB")) : 4;
     const unsigned gx = row_blocks(a.n, dot != nullptr);
-    if (dot) {
-        k_sell_cb<4, true><<<dim3(gx, (ncols + 3) / 4), kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm,
-                                                                                DotOut{dot->parts, dot->ticket, dot->out});
+    const dim3 grid4(gx, (ncols + 3) / 4);
+    if (a.halo) {  // row-partitioned: columns >= n read the halo copy of neighbour rows
+        if (dot)
+            k_sell_cb<4, true, true><<<grid4, kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm,
+                                                                        DotOut{dot->parts, dot->ticket, dot->out});
+        else
+            k_sell_cb<4, false, true><<<grid4, kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm, DotOut{});
+    } else if (dot) {
+        k_sell_cb<4, true><<<grid4, kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm,
+                                                             DotOut{dot->parts, dot->ticket, dot->out});
     } else {
         switch (variant) {
             case 0: k_sell<<<gx, kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm); break;

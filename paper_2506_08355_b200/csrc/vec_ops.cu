@@ -43,7 +43,7 @@ __device__ __forceinline__ void block_sum(double (&v)[K], double* sh) {
 template <int K, class F>
 __global__ void __launch_bounds__(kThreads) k_colred(int64_t n, int ncols, int nchunks,
                                                       int64_t chunk, F f, double* partial,
-                                                      unsigned* ticket) {
+                                                      unsigned* ticket, double* defer) {
     __shared__ double sh[(kThreads / 32) * K];
     __shared__ bool last;
     const int j = blockIdx.y;
@@ -83,13 +83,31 @@ __global__ void __launch_bounds__(kThreads) k_colred(int64_t n, int ncols, int n
         for (int cc = 0; cc < nchunks; ++cc)
 #pragma unroll
             for (int k = 0; k < K; ++k) s[k] += __ldcg(&partial[(static_cast<int64_t>(jj) * nchunks + cc) * K + k]);
-        f.fin(jj, s);
+        if (defer) {  // row-partitioned: the epilogue runs after the cross-rank allreduce
+#pragma unroll
+            for (int k = 0; k < K; ++k) defer[k * ncols + jj] = s[k];
+        } else {
+            f.fin(jj, s);
+        }
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        f.fin_all(ncols);
+        if (!defer) f.fin_all(ncols);
         *ticket = 0u;
     }
+}
+
+// Epilogue of k_colred on cross-rank sums (one block).
+template <int K, class F>
+__global__ void k_colred_finish(F f, const double* sums, int ncols) {
+    for (int jj = threadIdx.x; jj < ncols; jj += blockDim.x) {
+        double s[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) s[k] = sums[k * ncols + jj];
+        f.fin(jj, s);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) f.fin_all(ncols);
 }
 
 struct NoFinAll {
@@ -111,12 +129,23 @@ void launch_colred(const char* family, int64_t n, int ncols, const F& f, double 
     int nchunks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n + 4095) / 4096,
                                                                             (target + ncols - 1) / ncols)));
     const int64_t chunk = ((n + nchunks - 1) / nchunks + 1) & ~int64_t(1);  // even: pairs stay aligned
-    double* partial = rt.scratch(static_cast<size_t>(nchunks) * ncols * K);
+    double* partial = rt.scratch(static_cast<size_t>(nchunks) * ncols * K + static_cast<size_t>(K) * ncols);
     unsigned* ticket = rt.tickets(1);
-    LaunchScope ls(family, bytes, 0.0);
-    dim3 grid(nchunks, ncols);
-    k_colred<K, F><<<grid, kThreads, 0, rt.stream()>>>(n, ncols, nchunks, chunk, f, partial, ticket);
-    BOSP_LAUNCH_CHECK();
+    // several ranks: park the column sums after the partials, allreduce them, then run the
+    // epilogue on the global sums so every rank sets identical scalars
+    double* defer = rt.nranks() > 1 ? partial + static_cast<size_t>(nchunks) * ncols * K : nullptr;
+    {
+        LaunchScope ls(family, bytes, 0.0);
+        dim3 grid(nchunks, ncols);
+        k_colred<K, F><<<grid, kThreads, 0, rt.stream()>>>(n, ncols, nchunks, chunk, f, partial, ticket, defer);
+        BOSP_LAUNCH_CHECK();
+    }
+    if (defer) {
+        rt.allreduce(defer, static_cast<int64_t>(K) * ncols);
+        LaunchScope ls(family, 0.0, 0.0);
+        k_colred_finish<K, F><<<1, kThreads, 0, rt.stream()>>>(f, defer, ncols);
+        BOSP_LAUNCH_CHECK();
+    }
 }
 
 // ---- functors -------------------------------------------------------------------------------

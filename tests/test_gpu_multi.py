@@ -1,0 +1,109 @@
+"""Row-partitioned solves against the unpartitioned solve and the reference.
+
+Every n-length block is split by rows over `nranks` ranks; Grams/dots are allreduced, sparse
+applies exchange halo rows, dense applies allgather X.  Here the ranks are threads of one
+process sharing the single B200 of the test box (ThreadComm over device memory), which runs
+exactly the partitioned code path a multi-GPU NCCL run takes, minus the transport.  The bar is
+the solver's: eigenvalues within 1e-10 relative of the reference, residuals below tol,
+max |X^T Y - I| below 1e-10 -- and agreement with the one-rank solve.
+"""
+import numpy as np
+import pytest
+
+from paper_2506_08355_b200 import bosp
+from paper_2506_08355_b200 import problems as P
+from tests.test_gpu_solver import check_result
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("nranks", [2, 3, 4])
+def test_partitioned_csr_config2(golden_solves, nranks):
+    p = P.config2(16)
+    cfg = bosp.BospConfig(**p.cfg)
+    res = bosp.solve_multi(nranks, p.K, p.M, cfg, bosp.GeneralizedNullspace(p.x0, p.y0))
+    check_result(res, golden_solves["config2_m16"]["lambdas"], 1e-8, 20)
+
+
+@pytest.mark.parametrize("nranks", [2, 4])
+def test_partitioned_stencil3d_matches_serial(golden_solves, nranks):
+    p = P.config2(16)
+    kop, mop = P._grid3_ops(16)
+    cfg = bosp.BospConfig(**p.cfg)
+    ns = bosp.GeneralizedNullspace(p.x0, p.y0)
+    serial = bosp.solve(bosp.LinearOperator.from_stencil(kop), bosp.LinearOperator.from_stencil(mop), None,
+                        cfg, ns)
+    res = bosp.solve_multi(nranks, kop, mop, cfg, ns)
+    check_result(res, golden_solves["config2_m16"]["lambdas"], 1e-8, 20)
+    assert np.abs(res.lambdas - serial.lambdas).max() / serial.lambdas.max() < 1e-11
+    # the partitioned run starts from the serial run's random vectors: same trajectory
+    assert abs(res.iterations - serial.iterations) <= 1
+
+
+def test_partitioned_stencil2d_moving(golden_solves):
+    """Config-5 family (5-point, array potential) with moving/locking over 2 ranks."""
+    p = P.config5(32)
+    cfg = bosp.BospConfig(nev=40, nb=8, tol=1e-8)
+    assert cfg.effective_moving()
+    res = bosp.solve_multi(2, p.K, p.M, cfg, bosp.GeneralizedNullspace(p.x0, p.y0))
+    check_result(res, golden_solves["config5_m32"]["lambdas"], 1e-8, 40)
+
+
+def test_partitioned_dense_config1(golden_solves):
+    p = P.config1()
+    res = bosp.solve_multi(2, p.K, p.M, bosp.BospConfig(**p.cfg), bosp.GeneralizedNullspace(p.x0, p.y0))
+    check_result(res, golden_solves["config1"]["lambdas"], 1e-8, 10)
+
+
+def test_partitioned_table3(golden_solves):
+    n = 1000
+    res = bosp.solve_multi(3, P.t_matrix(n, -1.0), P.t_matrix(n, 0.0), bosp.BospConfig(nev=10, nb=10, tol=1e-10),
+                           bosp.GeneralizedNullspace(*P.analytic_nullspace_T(n)))
+    check_result(res, golden_solves["tm1_t0_n1000"]["lambdas"], 1e-10, 10)
+
+
+def test_partitioned_computes_nullspace():
+    """No nullspace given: every rank runs the partitioned compute_nullspace first."""
+    n = 200
+    t = P.t_matrix(n, 0.0)
+    res = bosp.solve_multi(2, t, t, bosp.BospConfig(nev=4, nb=4, tol=1e-10))
+    assert res.converged
+    assert np.allclose(res.lambdas, P.t_eigenvalues(n, 4), rtol=1e-11)
+
+
+def test_partitioned_ragged_rows():
+    """n not divisible by nranks (ragged slices) and more ranks than z-planes would allow evenly."""
+    n = 401
+    t = P.t_matrix(n, 0.0)
+    serial = bosp.solve(bosp.LinearOperator.from_csr(t), bosp.LinearOperator.from_csr(t), None,
+                        bosp.BospConfig(nev=5, nb=5, tol=1e-10), bosp.GeneralizedNullspace(*P.analytic_nullspace_T(n)))
+    res = bosp.solve_multi(4, t, t, bosp.BospConfig(nev=5, nb=5, tol=1e-10),
+                           bosp.GeneralizedNullspace(*P.analytic_nullspace_T(n)))
+    assert res.converged
+    assert np.allclose(res.lambdas, serial.lambdas, rtol=1e-11)
+    assert np.allclose(res.lambdas, P.t_eigenvalues(n, 5), rtol=1e-11)
+
+
+def test_partitioned_errors():
+    t = P.t_matrix(50, 0.0)
+    with pytest.raises(bosp.ContractViolation):
+        bosp.solve_multi(17, t, t, bosp.BospConfig(nev=2, nb=2))
+    with pytest.raises(bosp.ContractViolation):
+        bosp.solve_multi(2, t, P.t_matrix(60, 0.0), bosp.BospConfig(nev=2, nb=2))
+
+
+def test_nccl_single_rank_comm():
+    """NCCL bootstrap on one GPU: unique id, a 1-rank communicator attached to this thread,
+    then a solve through it (the multi-GPU bench path with N = 1)."""
+    uid = bosp.comm_nccl_unique_id()
+    assert len(uid) == 128
+    n = 300
+    t = P.t_matrix(n, 0.0)
+    bosp.comm_init_nccl(uid, 1, 0, n, 0)
+    try:
+        op = bosp.local_operator(t, 1, 0)
+        res = bosp.solve(op, op, None, bosp.BospConfig(nev=4, nb=4, tol=1e-10),
+                         bosp.GeneralizedNullspace(*P.analytic_nullspace_T(n)))
+    finally:
+        bosp.comm_free()
+    assert np.allclose(res.lambdas, P.t_eigenvalues(n, 4), rtol=1e-11)
