@@ -113,6 +113,10 @@ def main():
     for n in (100, 1000):
         tm, t0 = P.t_matrix(n, -1.0), P.t_matrix(n, 0.0)
         solves[f"tm1_t0_n{n}"] = solve_record(tm.spec(), t0.spec(), ref.RefConfig(nev=10 if n == 1000 else 5, nb=10 if n == 1000 else 5, tol=1e-10), P.analytic_nullspace_T(n), n, f"T-1/T0 n={n}")
+    # odd sizes for the row-partition tests (ragged slices)
+    for n, k in ((300, 4), (401, 5)):
+        tm, t0 = P.t_matrix(n, -1.0), P.t_matrix(n, 0.0)
+        solves[f"tm1_t0_n{n}"] = solve_record(tm.spec(), t0.spec(), ref.RefConfig(nev=k, nb=k, tol=1e-10), P.analytic_nullspace_T(n), n, f"T-1/T0 n={n}")
     # moving-mechanism case on T(0): nev=12, nb=2 -> moving on, locks happen
     t = P.t_matrix(400, 0.0)
     solves["t0_moving_n400"] = solve_record(t.spec(), t.spec(), ref.RefConfig(nev=12, nb=2, tol=1e-9), None, 400, "T0 moving")

@@ -213,6 +213,17 @@ def test_seed_blocks_bit_exact_reference_stream(golden_small):
     assert np.array_equal(np.concatenate([u.T.reshape(-1), v.T.reshape(-1)]), ref)
 
 
+def test_seed_blocks_jump_ahead_long_stream():
+    """17.3M draws: ~130 CTAs each jump to their 2^16-draw segments with both polynomial tables
+    (segment index >= 256 uses table B then A) -- still the reference's single stream."""
+    n, d = 262147, 33
+    u, v = bosp.seed_blocks(7, n, d)
+    got = np.concatenate([u.T.reshape(-1), v.T.reshape(-1)])
+    ref = O.MT19937_64(7).uniform(2 * n * d)
+    bad = np.flatnonzero(got != ref)
+    assert bad.size == 0, (bad.size, bad[:5])
+
+
 def test_shape_errors_map_to_contract_violation():
     with pytest.raises(bosp.ContractViolation):
         bosp.block_inner(None, np.ones((5, 2)), np.ones((4, 2)))

@@ -36,8 +36,9 @@ def test_partitioned_stencil3d_matches_serial(golden_solves, nranks):
     res = bosp.solve_multi(nranks, kop, mop, cfg, ns)
     check_result(res, golden_solves["config2_m16"]["lambdas"], 1e-8, 20)
     assert np.abs(res.lambdas - serial.lambdas).max() / serial.lambdas.max() < 1e-11
-    # the partitioned run starts from the serial run's random vectors: same trajectory
-    assert abs(res.iterations - serial.iterations) <= 1
+    # same random start; allreduce summation order perturbs roundoff, so the trajectories
+    # (drops, repairs) may drift apart a little, not the converged eigenvalues
+    assert abs(res.iterations - serial.iterations) <= 0.15 * serial.iterations
 
 
 def test_partitioned_stencil2d_moving(golden_solves):
@@ -71,17 +72,16 @@ def test_partitioned_computes_nullspace():
     assert np.allclose(res.lambdas, P.t_eigenvalues(n, 4), rtol=1e-11)
 
 
-def test_partitioned_ragged_rows():
-    """n not divisible by nranks (ragged slices) and more ranks than z-planes would allow evenly."""
+def test_partitioned_ragged_rows(golden_solves):
+    """n = 401 over 4 ranks: slices of 100, 100, 100, 101 rows."""
     n = 401
-    t = P.t_matrix(n, 0.0)
-    serial = bosp.solve(bosp.LinearOperator.from_csr(t), bosp.LinearOperator.from_csr(t), None,
-                        bosp.BospConfig(nev=5, nb=5, tol=1e-10), bosp.GeneralizedNullspace(*P.analytic_nullspace_T(n)))
-    res = bosp.solve_multi(4, t, t, bosp.BospConfig(nev=5, nb=5, tol=1e-10),
-                           bosp.GeneralizedNullspace(*P.analytic_nullspace_T(n)))
-    assert res.converged
-    assert np.allclose(res.lambdas, serial.lambdas, rtol=1e-11)
-    assert np.allclose(res.lambdas, P.t_eigenvalues(n, 5), rtol=1e-11)
+    k, m = P.t_matrix(n, -1.0), P.t_matrix(n, 0.0)
+    ns = bosp.GeneralizedNullspace(*P.analytic_nullspace_T(n))
+    cfg = bosp.BospConfig(nev=5, nb=5, tol=1e-10)
+    serial = bosp.solve(bosp.LinearOperator.from_csr(k), bosp.LinearOperator.from_csr(m), None, cfg, ns)
+    res = bosp.solve_multi(4, k, m, cfg, ns)
+    check_result(res, golden_solves["tm1_t0_n401"]["lambdas"], 1e-10, 5)
+    assert np.allclose(res.lambdas, serial.lambdas, rtol=1e-12)
 
 
 def test_partitioned_errors():
@@ -92,18 +92,17 @@ def test_partitioned_errors():
         bosp.solve_multi(2, t, P.t_matrix(60, 0.0), bosp.BospConfig(nev=2, nb=2))
 
 
-def test_nccl_single_rank_comm():
+def test_nccl_single_rank_comm(golden_solves):
     """NCCL bootstrap on one GPU: unique id, a 1-rank communicator attached to this thread,
     then a solve through it (the multi-GPU bench path with N = 1)."""
     uid = bosp.comm_nccl_unique_id()
     assert len(uid) == 128
     n = 300
-    t = P.t_matrix(n, 0.0)
+    k, m = P.t_matrix(n, -1.0), P.t_matrix(n, 0.0)
     bosp.comm_init_nccl(uid, 1, 0, n, 0)
     try:
-        op = bosp.local_operator(t, 1, 0)
-        res = bosp.solve(op, op, None, bosp.BospConfig(nev=4, nb=4, tol=1e-10),
-                         bosp.GeneralizedNullspace(*P.analytic_nullspace_T(n)))
+        res = bosp.solve(bosp.local_operator(k, 1, 0), bosp.local_operator(m, 1, 0), None,
+                         bosp.BospConfig(nev=4, nb=4, tol=1e-10), bosp.GeneralizedNullspace(*P.analytic_nullspace_T(n)))
     finally:
         bosp.comm_free()
-    assert np.allclose(res.lambdas, P.t_eigenvalues(n, 4), rtol=1e-11)
+    check_result(res, golden_solves["tm1_t0_n300"]["lambdas"], 1e-10, 4)
