@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbosp_b200.so")
+LIB_PATH = os.environ.get("BOSP_LIB_PATH") or os.path.join(_HERE, "libbosp_b200.so")  # override: experiments only
 
 _lib = None
 

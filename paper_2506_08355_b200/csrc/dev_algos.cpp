@@ -264,18 +264,24 @@ CgWorkspace::~CgWorkspace() {
 namespace {
 // One batched CG iteration: ap = A p with p^T A p fused into the operator when it can
 // (SELL / stencil), then the cooperative fused update; unfused kernels otherwise.
+// BOSP_CG_MODE: 0 = SpMM with fused p^T A p (masked) + update + direction (default);
+//               1 = separate p^T A p kernel; 2 = cooperative single-kernel update.
+// (A row-major "interleaved" CG layout was measured 15-20% slower on config 2 and dropped.)
+int cg_mode() {
+    static const int mode = std::getenv("BOSP_CG_MODE") ? std::atoi(std::getenv("BOSP_CG_MODE")) : 0;
+    return mode;
+}
+
 void cg_iteration(const LinearOperator& a, const DMat& x, const DMat& r, const DMat& p, const DMat& ap,
                   const CgScalars& sc, CgWorkspace& ws, double tol, int mi) {
-    // BOSP_CG_MODE: 0 = SpMM with fused p^T A p + update + direction (default),
-    //               1 = separate p^T A p kernel, 2 = cooperative single-kernel update
-    static const int mode = std::getenv("BOSP_CG_MODE") ? std::atoi(std::getenv("BOSP_CG_MODE")) : 0;
+    const int mode = cg_mode();
     if (mode == 2 && p.cols <= 160 && Runtime::get().nranks() == 1) {
         a.apply_device(p, ap);
         cg_pap(p, ap, sc);
         cg_update_fused(x, r, p, ap, sc, sc.pap, 1, tol, mi);
         return;
     }
-    const SpmmDot dot{ws.pap_parts(), ws.ticket(), sc.pap};
+    const SpmmDot dot{ws.pap_parts(), ws.ticket(), sc.pap, sc.active, CgWorkspace::kPartsPerRegion};
     if (mode != 1 && a.impl()->apply_dot(p, ap, dot)) {
         Runtime::get().allreduce(sc.pap, p.cols);  // per-rank p^T A p -> global
         cg_update(x, r, p, ap, sc, tol, mi);

@@ -67,9 +67,9 @@ public:
     double* pap_parts() const { return parts_; }
     unsigned* ticket() const { return ticket_; }
     ~CgWorkspace();
+    static constexpr int64_t kPartsPerRegion = 160 * 512;
 
 private:
-    static constexpr int64_t kPartsPerRegion = 160 * 512;
     void* scal_ = nullptr;
     double* parts_ = nullptr;
     unsigned* ticket_ = nullptr;

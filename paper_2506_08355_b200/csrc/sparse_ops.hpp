@@ -25,9 +25,11 @@ struct SellDev {
 // Fused x(:,j)^T y(:,j) (the CG's p^T A p): per-block partials in `parts` (<= 256 x ncols),
 // folded in fixed order by the last block into out[j]; `ticket` must be zero and stays zero.
 struct SpmmDot {
-    double* parts;
+    double* parts;              // per-block partials, parts_cap doubles
     unsigned* ticket;
     double* out;
+    const int* active = nullptr;  // optional column mask: inactive columns are neither applied nor dotted
+    int64_t parts_cap = 0;
 };
 
 // y(:, j) = A x(:, j) for all columns of x (optionally with the fused dots); returns the number

@@ -45,6 +45,11 @@ struct KTimer {
 
 // Rows whose slice is wider than kWMax fall back to the streaming loop below.
 constexpr int kWMax = 16;
+// Occupancy floor of the masked/halo SELL kernel (the CG's SpMM): it is memory-latency bound
+// and 4 resident blocks (64 registers) measured best for the batched CG on config 2.
+#ifndef BOSP_SELL_MINB
+#define BOSP_SELL_MINB 4
+#endif
 
 __global__ void __launch_bounds__(kRows) k_sell(SellDev a, const double* __restrict__ x, int64_t ldx,
                                                  double* __restrict__ y, int64_t ldy, int ncols,
@@ -151,16 +156,63 @@ __device__ __forceinline__ void fold_dots_last_block(const double* dots, int nco
 }
 
 struct DotOut {
-    double* parts;     // [ncols][gridDim.x] per-block partials
-    unsigned* ticket;  // zero on entry, left at zero
-    double* out;       // folded x^T y per column
+    double* parts;       // [ncols][gridDim.x] per-block partials
+    unsigned* ticket;    // zero on entry, left at zero
+    double* out;         // folded x^T y per column
+    const int* active;   // optional mask: skip inactive columns entirely
 };
+
+// Columns this block applies: in range and (with a mask) still active.
+template <int CB, bool DOT>
+__device__ __forceinline__ bool group_columns(const DotOut& dots, int j0, int ncols, bool (&on)[CB]) {
+    bool any = false;
+#pragma unroll
+    for (int c = 0; c < CB; ++c) {
+        on[c] = j0 + c < ncols;
+        if (DOT && dots.active) on[c] = on[c] && dots.active[j0 + c] != 0;
+        any |= on[c];
+    }
+    return any;
+}
+
+// Plain column-group SpMM (no dots, no halo): the simplest loop, which the compiler schedules
+// best (40 registers, measured ~10% faster than the masked/halo template at m = 20..60).
+template <int CB>
+__global__ void __launch_bounds__(kRows) k_sell_plain(SellDev a, const double* __restrict__ x, int64_t ldx,
+                                                       double* __restrict__ y, int64_t ldy, int ncols,
+                                                       KTimer tm) {
+    tm.start();
+    const int j0 = blockIdx.y * CB;
+    const int64_t ntiles = (a.n + kRows - 1) / kRows;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t row = tile * kRows + threadIdx.x;
+        if (row >= a.n) continue;
+        const int64_t s = row >> 5;
+        const int64_t base = a.slice_ptr[s] + (row & 31);
+        const int w = a.slice_w[s];
+        double acc[CB];
+#pragma unroll
+        for (int c = 0; c < CB; ++c) acc[c] = 0.0;
+        const double* xb = x + static_cast<int64_t>(j0) * ldx;
+        for (int k = 0; k < w; ++k) {
+            const int col = __ldg(a.col + base + 32 * k);
+            const double v = __ldg(a.val + base + 32 * k);
+#pragma unroll
+            for (int c = 0; c < CB; ++c)
+                if (j0 + c < ncols) acc[c] += v * __ldg(xb + c * ldx + col);
+        }
+#pragma unroll
+        for (int c = 0; c < CB; ++c)
+            if (j0 + c < ncols) y[(j0 + c) * ldy + row] = acc[c];
+    }
+    tm.stop();
+}
 
 // Column-group variant: grid.y walks groups of CB columns, grid.x strides over 256-row tiles;
 // the row's entries are re-read per column group (L2).  Optionally accumulates x^T y per
 // column (the CG's p^T A p) while y is produced.
 template <int CB, bool DOT, bool HALO = false>
-__global__ void __launch_bounds__(kRows) k_sell_cb(SellDev a, const double* __restrict__ x, int64_t ldx,
+__global__ void __launch_bounds__(kRows, BOSP_SELL_MINB) k_sell_cb(SellDev a, const double* __restrict__ x, int64_t ldx,
                                                     double* __restrict__ y, int64_t ldy, int ncols,
                                                     KTimer tm, DotOut dots) {
     tm.start();
@@ -168,7 +220,9 @@ __global__ void __launch_bounds__(kRows) k_sell_cb(SellDev a, const double* __re
     double d[CB];
 #pragma unroll
     for (int c = 0; c < CB; ++c) d[c] = 0.0;
-    const int64_t ntiles = (a.n + kRows - 1) / kRows;
+    bool on[CB];
+    const bool any = group_columns<CB, DOT>(dots, j0, ncols, on);
+    const int64_t ntiles = any ? (a.n + kRows - 1) / kRows : 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int64_t row = tile * kRows + threadIdx.x;
         if (row >= a.n) continue;
@@ -186,16 +240,16 @@ __global__ void __launch_bounds__(kRows) k_sell_cb(SellDev a, const double* __re
                 const double* hb = a.halo + static_cast<int64_t>(j0) * a.ldh + (col - a.n);
 #pragma unroll
                 for (int c = 0; c < CB; ++c)
-                    if (j0 + c < ncols) acc[c] += v * __ldg(hb + c * a.ldh);
+                    if (on[c]) acc[c] += v * __ldg(hb + c * a.ldh);
                 continue;
             }
 #pragma unroll
             for (int c = 0; c < CB; ++c)
-                if (j0 + c < ncols) acc[c] += v * __ldg(xb + c * ldx + col);
+                if (on[c]) acc[c] += v * __ldg(xb + c * ldx + col);
         }
 #pragma unroll
         for (int c = 0; c < CB; ++c)
-            if (j0 + c < ncols) {
+            if (on[c]) {
                 y[(j0 + c) * ldy + row] = acc[c];
                 if (DOT) d[c] += __ldg(xb + c * ldx + row) * acc[c];
             }
@@ -207,7 +261,7 @@ __global__ void __launch_bounds__(kRows) k_sell_cb(SellDev a, const double* __re
     tm.stop();
 }
 
-template <int CB, bool DOT>
+template <int CB, bool DOT, bool PART>
 __global__ void __launch_bounds__(kRows) k_stencil(StencilDev st, const double* __restrict__ x,
                                                     int64_t ldx, double* __restrict__ y,
                                                     int64_t ldy, int ncols, KTimer tm, DotOut dots) {
@@ -217,7 +271,9 @@ __global__ void __launch_bounds__(kRows) k_stencil(StencilDev st, const double* 
     double d[CB];
 #pragma unroll
     for (int c = 0; c < CB; ++c) d[c] = 0.0;
-    const int64_t ntiles = (n + kRows - 1) / kRows;
+    bool on[CB];
+    const bool any = group_columns<CB, DOT>(dots, j0, ncols, on);
+    const int64_t ntiles = any ? (n + kRows - 1) / kRows : 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int64_t idx = tile * kRows + threadIdx.x;
         if (idx >= n) continue;
@@ -225,6 +281,44 @@ __global__ void __launch_bounds__(kRows) k_stencil(StencilDev st, const double* 
         const int64_t i = idx % st.nx;
         const int64_t jy = (idx / st.nx) % st.ny;
         const int64_t kz = idx / nxy;
+        if (!PART) {  // whole grid on this rank: plain index arithmetic (register-light)
+            const bool three = st.dims == 3;
+            const bool xm = i > 0, xp = i + 1 < st.nx;
+            const bool ym = jy > 0, yp = jy + 1 < st.ny;
+            const bool zm = kz > 0, zp = kz + 1 < st.nz;
+            double diag = st.bc == 0 ? static_cast<double>(xm + xp + ym + yp + (three ? (zm + zp) : 0))
+                                     : 2.0 * st.dims;
+            diag *= st.scale;
+            double pot = 0.0;
+            if (st.potential == 1) {
+                const double cx = st.origin + (i + 1) * st.h;
+                const double cy = st.origin + (jy + 1) * st.h;
+                const double cz = three ? st.origin + (kz + 1) * st.h : 0.0;
+                pot = 0.5 * (cx * cx + cy * cy + cz * cz);
+            } else if (st.potential == 2) {
+                pot = __ldg(st.v + idx);
+            }
+            const double dg = diag + pot;
+#pragma unroll
+            for (int c = 0; c < CB; ++c) {
+                if (!on[c]) continue;
+                const double* xc = x + static_cast<int64_t>(j0 + c) * ldx + idx;
+                double nb = 0.0;
+                if (xm) nb += __ldg(xc - 1);
+                if (xp) nb += __ldg(xc + 1);
+                if (ym) nb += __ldg(xc - st.nx);
+                if (yp) nb += __ldg(xc + st.nx);
+                if (three) {
+                    if (zm) nb += __ldg(xc - nxy);
+                    if (zp) nb += __ldg(xc + nxy);
+                }
+                const double xs = __ldg(xc);
+                const double yv = dg * xs - st.scale * nb;
+                y[(j0 + c) * ldy + idx] = yv;
+                if (DOT) d[c] += xs * yv;
+            }
+            continue;
+        }
         const int dims = st.dims;
         // global coordinate along the (partitioned) slowest axis
         const int64_t sl = dims == 3 ? kz : jy;                   // local slow index
@@ -258,7 +352,7 @@ __global__ void __launch_bounds__(kRows) k_stencil(StencilDev st, const double* 
         const bool lo = dims == 3 ? zm : ym, hi = dims == 3 ? zp : yp;
 #pragma unroll
         for (int c = 0; c < CB; ++c) {
-            if (j0 + c >= ncols) break;
+            if (!on[c]) continue;
             const double* xc = x + static_cast<int64_t>(j0 + c) * ldx + idx;
             double nb = 0.0;
             if (xm) nb += __ldg(xc - 1);
@@ -282,11 +376,13 @@ __global__ void __launch_bounds__(kRows) k_stencil(StencilDev st, const double* 
     tm.stop();
 }
 
-// Row-tile blocks per column group: all tiles when no dots are wanted, else at most 256 so the
-// consumer folds <= 256 partials per column.
-unsigned row_blocks(int64_t n, bool dots) {
+// Row-tile blocks per column group: one per tile, bounded with dots by the partials buffer
+// (ncols x blocks doubles); the last block folds them.
+unsigned row_blocks(int64_t n, const SpmmDot* dot, int ncols) {
     const int64_t tiles = (n + kRows - 1) / kRows;
-    return static_cast<unsigned>(dots ? std::min<int64_t>(tiles, 256) : tiles);
+    if (!dot) return static_cast<unsigned>(tiles);
+    const int64_t cap = std::max<int64_t>(1, dot->parts_cap / std::max(ncols, 1));
+    return static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(tiles, cap)));
 }
 
 }  // namespace
@@ -299,28 +395,31 @@ int sell_spmm(const SellDev& a, const DMat& x, const DMat& y, const SpmmDot* dot
     // 4 B per row pointer) + x read once + y written once
     const double bytes = 12.0 * a.nnz + 4.0 * (a.n + 1) + 16.0 * a.n * ncols;
     const double flops = 2.0 * a.nnz * ncols;
-    KTimer tm{rt.timer_begin("spmm", bytes, flops)};
-    LaunchScope ls("spmm", bytes, flops, false);
+    // the CG's masked applies (family spmm_cg) touch only the active columns, so their bytes
+    // are not known on the host; the roofline family "spmm" is the unmasked applies
+    const char* fam = dot ? "spmm_cg" : "spmm";
+    KTimer tm{rt.timer_begin(fam, bytes, flops)};
+    LaunchScope ls(fam, bytes, flops, false);
     // Column groups of CB (grid.y) keep many independent blocks in flight; measured 2x the
     // bandwidth of the all-columns-per-thread variant (k_sell) on config 2 (B200).
     static const int variant = std::getenv("BOSP_SPMM_CB") ? std::atoi(std::getenv("BOSP_SPMM_CB")) : 4;
-    const unsigned gx = row_blocks(a.n, dot != nullptr);
+    const unsigned gx = row_blocks(a.n, dot, ncols);
     const dim3 grid4(gx, (ncols + 3) / 4);
     if (a.halo) {  // row-partitioned: columns >= n read the halo copy of neighbour rows
         if (dot)
             k_sell_cb<4, true, true><<<grid4, kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm,
-                                                                        DotOut{dot->parts, dot->ticket, dot->out});
+                                                                        DotOut{dot->parts, dot->ticket, dot->out, dot->active});
         else
             k_sell_cb<4, false, true><<<grid4, kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm, DotOut{});
     } else if (dot) {
         k_sell_cb<4, true><<<grid4, kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm,
-                                                             DotOut{dot->parts, dot->ticket, dot->out});
+                                                             DotOut{dot->parts, dot->ticket, dot->out, dot->active});
     } else {
         switch (variant) {
             case 0: k_sell<<<gx, kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm); break;
             case 2: k_sell_cb<2, false><<<dim3(gx, (ncols + 1) / 2), kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm, DotOut{}); break;
             case 8: k_sell_cb<8, false><<<dim3(gx, (ncols + 7) / 8), kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm, DotOut{}); break;
-            default: k_sell_cb<4, false><<<dim3(gx, (ncols + 3) / 4), kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm, DotOut{}); break;
+            default: k_sell_plain<4><<<dim3(gx, (ncols + 3) / 4), kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm); break;
         }
     }
     BOSP_LAUNCH_CHECK();
@@ -333,17 +432,25 @@ int stencil_spmm(const StencilDev& s, const DMat& x, const DMat& y, const SpmmDo
     Runtime& rt = Runtime::get();
     constexpr int CB = 4;
     const int ncols = static_cast<int>(x.cols);
-    const unsigned gx = row_blocks(n, dot != nullptr);
+    const unsigned gx = row_blocks(n, dot, ncols);
     dim3 grid(gx, (ncols + CB - 1) / CB);
     const double pts = s.nz > 1 ? 7.0 : 5.0;
     const double bytes = 16.0 * n * ncols, flops = 2.0 * pts * n * ncols;
-    KTimer tm{rt.timer_begin("spmm", bytes, flops)};
-    LaunchScope ls("spmm", bytes, flops, false);
-    if (dot)
-        k_stencil<CB, true><<<grid, kRows, 0, rt.stream()>>>(s, x.p, x.ld, y.p, y.ld, ncols, tm,
-                                                              DotOut{dot->parts, dot->ticket, dot->out});
-    else
-        k_stencil<CB, false><<<grid, kRows, 0, rt.stream()>>>(s, x.p, x.ld, y.p, y.ld, ncols, tm, DotOut{});
+    // the CG's masked applies (family spmm_cg) touch only the active columns, so their bytes
+    // are not known on the host; the roofline family "spmm" is the unmasked applies
+    const char* fam = dot ? "spmm_cg" : "spmm";
+    KTimer tm{rt.timer_begin(fam, bytes, flops)};
+    LaunchScope ls(fam, bytes, flops, false);
+    const int64_t snl = s.dims == 3 ? s.nz : s.ny;
+    const bool part = s.s_global > 0 && (s.s0 > 0 || s.s0 + snl < s.s_global);
+    const DotOut dd = dot ? DotOut{dot->parts, dot->ticket, dot->out, dot->active} : DotOut{};
+    if (part) {
+        if (dot) k_stencil<CB, true, true><<<grid, kRows, 0, rt.stream()>>>(s, x.p, x.ld, y.p, y.ld, ncols, tm, dd);
+        else k_stencil<CB, false, true><<<grid, kRows, 0, rt.stream()>>>(s, x.p, x.ld, y.p, y.ld, ncols, tm, dd);
+    } else {
+        if (dot) k_stencil<CB, true, false><<<grid, kRows, 0, rt.stream()>>>(s, x.p, x.ld, y.p, y.ld, ncols, tm, dd);
+        else k_stencil<CB, false, false><<<grid, kRows, 0, rt.stream()>>>(s, x.p, x.ld, y.p, y.ld, ncols, tm, dd);
+    }
     BOSP_LAUNCH_CHECK();
     return static_cast<int>(gx);
 }
