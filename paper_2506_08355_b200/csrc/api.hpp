@@ -6,6 +6,7 @@
 // boundary (operator construction, callbacks, results).
 #pragma once
 
+#include <cstdlib>
 #include <functional>
 #include <memory>
 #include <optional>
@@ -18,11 +19,40 @@
 namespace bosp {
 inline namespace b200 {
 
+// Host storage for large blocks: 2 MB-aligned with transparent huge pages requested (n x nev
+// eigenvector blocks are tens of MB; 4 KB first-touch faults cost more than the copy), and
+// default-initialisation left to the owner (BlockVectors zero-fills in parallel).
+template <class T>
+struct BigAlloc {
+    using value_type = T;
+    BigAlloc() = default;
+    template <class U>
+    BigAlloc(const BigAlloc<U>&) noexcept {}
+    T* allocate(size_t n);
+    void deallocate(T* p, size_t) noexcept { std::free(p); }
+    template <class U>
+    void construct(U* p) noexcept { (void)p; }  // no value-initialisation
+    template <class U, class... A>
+    void construct(U* p, A&&... a) { ::new (static_cast<void*>(p)) U(std::forward<A>(a)...); }
+    template <class U>
+    bool operator==(const BigAlloc<U>&) const noexcept { return true; }
+    template <class U>
+    bool operator!=(const BigAlloc<U>&) const noexcept { return false; }
+};
+void* big_alloc_bytes(size_t bytes);
+template <class T>
+T* BigAlloc<T>::allocate(size_t n) {
+    return static_cast<T*>(big_alloc_bytes(n * sizeof(T)));
+}
+void parallel_zero(double* p, size_t n);
+
 // Host column-major n x m block (block_vectors.hpp:10-50).
 class BlockVectors {
 public:
     BlockVectors() = default;
-    BlockVectors(int64_t dim, int64_t ncols) : dim_(dim), ncols_(ncols), data_(static_cast<size_t>(dim * ncols), 0.0) {}
+    BlockVectors(int64_t dim, int64_t ncols) : dim_(dim), ncols_(ncols), data_(static_cast<size_t>(dim * ncols)) {
+        parallel_zero(data_.data(), data_.size());
+    }
     int64_t dim() const { return dim_; }
     int64_t cols() const { return ncols_; }
     bool empty() const { return ncols_ == 0; }
@@ -40,7 +70,7 @@ public:
 
 private:
     int64_t dim_ = 0, ncols_ = 0;
-    std::vector<double> data_;
+    std::vector<double, BigAlloc<double>> data_;
 };
 
 // CSR (sparse_csr.hpp:12-28); indices are int64 at the boundary, int32 on the device.
@@ -206,8 +236,17 @@ SolverState initialize(const LinearOperator& k, const LinearOperator& m, const I
                         const GeneralizedNullspace& ns, const BospConfig& cfg);
 bool iterate_once(SolverState& st, const LinearOperator& k, const LinearOperator& m,
                   const InnerProduct& ip, const GeneralizedNullspace& ns, const BospConfig& cfg);
+// Caller-owned host buffers for the eigenvectors (n x cap each, column-major): when given, the
+// result's x / y are written there straight from HBM (through the pinned ring) and
+// EigenResult::x / y stay empty -- no intermediate host copy.
+struct HostVectorsOut {
+    double* x = nullptr;
+    double* y = nullptr;
+    int64_t cap = 0;
+};
 EigenResult solve(const LinearOperator& k, const LinearOperator& m, const InnerProduct& ip,
-                  const BospConfig& cfg, std::optional<GeneralizedNullspace> ns = std::nullopt);
+                  const BospConfig& cfg, std::optional<GeneralizedNullspace> ns = std::nullopt,
+                  const HostVectorsOut* out = nullptr);
 
 struct RegressionFit {
     double alpha = 0.0, beta = 0.0;

@@ -312,7 +312,8 @@ bosp_status bosp_solve(bosp_op K, bosp_op M, bosp_op B, const bosp_config* c, in
             g.y0 = host_block(y0, n, r);
             ns = std::move(g);
         }
-        bosp::EigenResult res = bosp::solve(K->op, M->op, ip_of(B), cfg, std::move(ns));
+        const bosp::HostVectorsOut hv{x, y, cap};
+        bosp::EigenResult res = bosp::solve(K->op, M->op, ip_of(B), cfg, std::move(ns), (x && y) ? &hv : nullptr);
         write_result(res, cfg, cap, lambdas, x, y, residuals, nout, stats, history, history_cap, history_rows);
     });
 }

@@ -517,7 +517,8 @@ bool iterate_once(SolverState& ss, const LinearOperator& k, const LinearOperator
 namespace {
 
 EigenResult assemble_result(DeviceState& st, const LinearOperator& k, const LinearOperator& m,
-                            const InnerProduct& ip, const BospConfig& cfg, bool converged) {
+                            const InnerProduct& ip, const BospConfig& cfg, bool converged,
+                            const HostVectorsOut* out = nullptr) {
     const int64_t n = st.n;
     const int64_t have = std::min<int64_t>(cfg.nev, st.locked_count() + st.wx);
     std::vector<double> lambdas;
@@ -584,6 +585,14 @@ EigenResult assemble_result(DeviceState& st, const LinearOperator& k, const Line
     DenseMatrix g = ip_gram_host(ip, rx.view(), ry.view());
     for (int64_t i = 0; i < g.rows(); ++i) g(i, i) -= 1.0;
     res.stats.final_biorth_deviation = g.max_abs();
+    if (out && out->x && out->y) {
+        require(h <= out->cap, "solve: output capacity too small");
+        to_host(rx.view(), out->x, n);
+        to_host(ry.view(), out->y, n);
+        res.x = BlockVectors(n, 0);
+        res.y = BlockVectors(n, 0);
+        return res;
+    }
     res.x = BlockVectors(n, h);
     res.y = BlockVectors(n, h);
     to_host(rx.view(), res.x.data(), n);
@@ -594,7 +603,7 @@ EigenResult assemble_result(DeviceState& st, const LinearOperator& k, const Line
 }  // namespace
 
 EigenResult solve(const LinearOperator& k, const LinearOperator& m, const InnerProduct& ip,
-                  const BospConfig& cfg, std::optional<GeneralizedNullspace> ns) {
+                  const BospConfig& cfg, std::optional<GeneralizedNullspace> ns, const HostVectorsOut* out) {
     cfg.validate();
     Runtime& rt = Runtime::get();
     const int64_t launches0 = rt.launches();
@@ -617,7 +626,7 @@ EigenResult solve(const LinearOperator& k, const LinearOperator& m, const InnerP
         }
     }
     const auto ta = Clock::now();
-    EigenResult res = assemble_result(st.dev(), k, m, ip, cfg, converged);
+    EigenResult res = assemble_result(st.dev(), k, m, ip, cfg, converged, out);
     st.dev().phases.acc[PH_ASSEMBLE] += secs(ta, Clock::now());
     if (phases_enabled()) {
         std::fprintf(stderr, "[bosp] phase wall times (s), %lld iterations:\n", (long long)st.iter());

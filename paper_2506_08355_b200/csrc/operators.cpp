@@ -2,6 +2,8 @@
 // dense / CSR / stencil-potential operators is uploaded once at construction (HBM-resident for
 // the whole solve); host ApplyFn callbacks are supported by staging through the host, exactly
 // once per call, for API compatibility with from_callback (linear_operator.cpp:45-47).
+#include <sys/mman.h>
+
 #include "operators.hpp"
 
 #include <algorithm>
@@ -15,6 +17,32 @@ namespace bosp {
 inline namespace b200 {
 
 // ---- host blocks ----------------------------------------------------------------------------
+void* big_alloc_bytes(size_t bytes) {
+    constexpr size_t kHuge = size_t(2) << 20;
+    void* p = nullptr;
+    if (bytes >= kHuge) {
+        if (posix_memalign(&p, kHuge, (bytes + kHuge - 1) / kHuge * kHuge) != 0) throw std::bad_alloc();
+        madvise(p, (bytes + kHuge - 1) / kHuge * kHuge, MADV_HUGEPAGE);
+    } else {
+        p = std::malloc(bytes ? bytes : 1);
+        if (!p) throw std::bad_alloc();
+    }
+    return p;
+}
+
+void parallel_zero(double* p, size_t n) {
+    if (n < (size_t(1) << 18)) {
+        std::memset(p, 0, n * sizeof(double));
+        return;
+    }
+    const int64_t chunks = 64;
+#pragma omp parallel for schedule(static)
+    for (int64_t c = 0; c < chunks; ++c) {
+        const size_t a = n * c / chunks, b = n * (c + 1) / chunks;
+        std::memset(p + a, 0, (b - a) * sizeof(double));
+    }
+}
+
 BlockVectors BlockVectors::columns(int64_t first, int64_t count) const {
     require(first + count <= ncols_, "columns: range exceeds block width");
     BlockVectors out(dim_, count);
@@ -116,47 +144,37 @@ private:
 struct SellStore {
     DevFree sp{nullptr}, sw{nullptr}, col{nullptr}, val{nullptr};
     SellDev dev;
+    // The CSR arrays are copied to the device once (pinned-ring staging) and converted to
+    // SELL-32 there; nothing of size nnz is built on the host.
     SellStore(int64_t n, const int64_t* rp, const int64_t* ci, const double* vv) {
         require(n < (int64_t(1) << 31), "from_csr: dimension exceeds int32 device indices");
+        Runtime& rt = Runtime::get();
         const int64_t base = rp[0];
+        const int64_t nnz = rp[n] - base;
         const int64_t nsl = (n + 31) / 32;
-        std::vector<int64_t> spv(static_cast<size_t>(nsl + 1), 0);
-        std::vector<int32_t> swv(static_cast<size_t>(nsl), 0);
-        for (int64_t s = 0; s < nsl; ++s) {
-            int64_t w = 0;
-            for (int64_t r = s * 32; r < std::min(n, s * 32 + 32); ++r) w = std::max(w, rp[r + 1] - rp[r]);
-            swv[s] = static_cast<int32_t>(w);
-            spv[s + 1] = spv[s] + 32 * w;
-        }
-        std::vector<int32_t> colv(static_cast<size_t>(spv[nsl]));
-        std::vector<double> valv(static_cast<size_t>(spv[nsl]), 0.0);
-        for (int64_t s = 0; s < nsl; ++s)
-            for (int64_t l = 0; l < 32; ++l) {
-                const int64_t r = s * 32 + l;
-                const int64_t len = r < n ? rp[r + 1] - rp[r] : 0;
-                for (int64_t k = 0; k < swv[s]; ++k) {
-                    const int64_t at = spv[s] + 32 * k + l;
-                    if (k < len) {
-                        colv[at] = static_cast<int32_t>(ci[rp[r] - base + k]);
-                        valv[at] = vv[rp[r] - base + k];
-                    } else {
-                        colv[at] = static_cast<int32_t>(r < n ? r : 0);
-                        valv[at] = 0.0;
-                    }
-                }
-            }
-        sp.p = upload(spv.data(), spv.size());
-        sw.p = upload(swv.data(), swv.size());
-        col.p = upload(colv.data(), colv.size());
-        val.p = upload(valv.data(), valv.size());
+        DevFree drp(rt.alloc(sizeof(int64_t) * (n + 1)));
+        DevFree dci(rt.alloc(sizeof(int64_t) * std::max<int64_t>(nnz, 1)));
+        DevFree dvv(rt.alloc(sizeof(double) * std::max<int64_t>(nnz, 1)));
+        h2d_bytes(drp.p, rp, sizeof(int64_t) * (n + 1));
+        h2d_bytes(dci.p, ci, sizeof(int64_t) * nnz);
+        h2d_bytes(dvv.p, vv, sizeof(double) * nnz);
+        sp.p = rt.alloc(sizeof(int64_t) * (nsl + 1));
+        sw.p = rt.alloc(sizeof(int32_t) * std::max<int64_t>(nsl, 1));
+        const int64_t total = sell_layout(n, static_cast<const int64_t*>(drp.p), static_cast<int64_t*>(sp.p),
+                                          static_cast<int32_t*>(sw.p));
+        col.p = rt.alloc(sizeof(int32_t) * std::max<int64_t>(total, 1));
+        val.p = rt.alloc(sizeof(double) * std::max<int64_t>(total, 1));
+        sell_fill(n, static_cast<const int64_t*>(drp.p), static_cast<const int64_t*>(dci.p),
+                  static_cast<const double*>(dvv.p), static_cast<const int64_t*>(sp.p),
+                  static_cast<const int32_t*>(sw.p), static_cast<int32_t*>(col.p), static_cast<double*>(val.p));
         dev.n = n;
         dev.nslices = nsl;
         dev.slice_ptr = static_cast<const int64_t*>(sp.p);
         dev.slice_w = static_cast<const int32_t*>(sw.p);
         dev.col = static_cast<const int32_t*>(col.p);
         dev.val = static_cast<const double*>(val.p);
-        dev.nnz = rp[n] - base;
-        Runtime::get().sync();  // host staging vectors die at scope exit
+        dev.nnz = nnz;
+        rt.sync();  // the CSR copies are released at scope exit
     }
 };
 

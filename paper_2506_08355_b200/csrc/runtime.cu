@@ -83,6 +83,19 @@ double* Runtime::pinned(size_t doubles) {
     return pinned_;
 }
 
+double* Runtime::stage(int i) {
+    if (!stage_[i]) {
+        BOSP_CUDA(cudaMallocHost(&stage_[i], kStageDoubles * sizeof(double)));
+        BOSP_CUDA(cudaEventCreateWithFlags(&stage_ev_[i], cudaEventDisableTiming));
+    }
+    return stage_[i];
+}
+
+cudaEvent_t Runtime::stage_event(int i) {
+    stage(i);
+    return stage_ev_[i];
+}
+
 void Runtime::count_launch(const char* family) {
     if (capture_sink_) {
         ++(*capture_sink_)[family];
@@ -238,20 +251,112 @@ void DBlock::zero() {
     if (p_) BOSP_CUDA(cudaMemsetAsync(p_, 0, sizeof(double) * ld_ * cap_, Runtime::get().stream()));
 }
 
+namespace {
+
+// Large pageable transfers go through the pinned ring in chunks: the DMA of chunk i+1 overlaps
+// the (OpenMP-parallel) host copy of chunk i, instead of the driver's serial pageable path.
+constexpr size_t kStagedMin = size_t(4) << 20;  // bytes; smaller copies go direct
+
+struct Chunk {
+    int64_t c0, nc, r0, nr;  // columns [c0, c0+nc), rows [r0, r0+nr)
+};
+
+std::vector<Chunk> chunks_of(int64_t rows, int64_t cols) {
+    std::vector<Chunk> out;
+    const int64_t cap = static_cast<int64_t>(Runtime::kStageDoubles);
+    if (rows >= cap / 2) {  // tall: split every column into row pieces
+        for (int64_t c = 0; c < cols; ++c)
+            for (int64_t r = 0; r < rows; r += cap) out.push_back({c, 1, r, std::min(cap, rows - r)});
+    } else {
+        const int64_t per = std::max<int64_t>(1, cap / rows);
+        for (int64_t c = 0; c < cols; c += per) out.push_back({c, std::min(per, cols - c), 0, rows});
+    }
+    return out;
+}
+
+void host_scatter(const double* stage, const Chunk& ch, double* host, int64_t ld_host, bool to_host_dir) {
+    // stage holds the chunk as nr x nc, ld = nr
+#pragma omp parallel for schedule(static) if (ch.nr * ch.nc > (1 << 16))
+    for (int64_t q = 0; q < ch.nc * 8; ++q) {
+        const int64_t c = q / 8, part = q % 8;
+        const int64_t lo = ch.nr * part / 8, hi = ch.nr * (part + 1) / 8;
+        if (hi <= lo) continue;
+        double* h = host + (ch.c0 + c) * ld_host + ch.r0 + lo;
+        double* st = const_cast<double*>(stage) + c * ch.nr + lo;
+        if (to_host_dir) std::memcpy(h, st, sizeof(double) * (hi - lo));
+        else std::memcpy(st, h, sizeof(double) * (hi - lo));
+    }
+}
+
+bool is_pinned(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+}  // namespace
+
 void to_device(const double* host, int64_t rows, int64_t cols, int64_t ld_host, const DMat& dst) {
     if (rows == 0 || cols == 0) return;
-    BOSP_CUDA(cudaMemcpy2DAsync(dst.p, dst.ld * sizeof(double), host, ld_host * sizeof(double),
-                                rows * sizeof(double), cols, cudaMemcpyHostToDevice,
-                                Runtime::get().stream()));
+    Runtime& rt = Runtime::get();
+    if (static_cast<size_t>(rows * cols) * sizeof(double) < kStagedMin || is_pinned(host)) {
+        BOSP_CUDA(cudaMemcpy2DAsync(dst.p, dst.ld * sizeof(double), host, ld_host * sizeof(double),
+                                    rows * sizeof(double), cols, cudaMemcpyHostToDevice, rt.stream()));
+        return;
+    }
+    const std::vector<Chunk> ch = chunks_of(rows, cols);
+    for (size_t i = 0; i < ch.size(); ++i) {
+        const int b = static_cast<int>(i & 1);
+        double* st = rt.stage(b);
+        if (i >= 2) BOSP_CUDA(cudaEventSynchronize(rt.stage_event(b)));  // buffer's previous DMA done
+        host_scatter(st, ch[i], const_cast<double*>(host), ld_host, false);
+        BOSP_CUDA(cudaMemcpy2DAsync(dst.p + ch[i].c0 * dst.ld + ch[i].r0, dst.ld * sizeof(double), st,
+                                    ch[i].nr * sizeof(double), ch[i].nr * sizeof(double), ch[i].nc,
+                                    cudaMemcpyHostToDevice, rt.stream()));
+        BOSP_CUDA(cudaEventRecord(rt.stage_event(b), rt.stream()));
+    }
+    // the ring is reused by the next transfer only after these events
+    BOSP_CUDA(cudaEventSynchronize(rt.stage_event(static_cast<int>((ch.size() - 1) & 1))));
+}
+
+void h2d_bytes(void* dst, const void* src, size_t bytes) {
+    if (bytes == 0) return;
+    if (bytes >= kStagedMin && bytes % sizeof(double) == 0 && !is_pinned(src)) {
+        const int64_t nd = static_cast<int64_t>(bytes / sizeof(double));
+        to_device(static_cast<const double*>(src), nd, 1, nd, DMat{static_cast<double*>(dst), nd, nd, 1});
+        return;
+    }
+    BOSP_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, Runtime::get().stream()));
 }
 
 void to_host(const DMat& src, double* host, int64_t ld_host) {
     if (src.rows == 0 || src.cols == 0) return;
     Runtime& rt = Runtime::get();
-    BOSP_CUDA(cudaMemcpy2DAsync(host, ld_host * sizeof(double), src.p, src.ld * sizeof(double),
-                                src.rows * sizeof(double), src.cols, cudaMemcpyDeviceToHost,
-                                rt.stream()));
-    rt.sync();
+    if (static_cast<size_t>(src.rows * src.cols) * sizeof(double) < kStagedMin || is_pinned(host)) {
+        BOSP_CUDA(cudaMemcpy2DAsync(host, ld_host * sizeof(double), src.p, src.ld * sizeof(double),
+                                    src.rows * sizeof(double), src.cols, cudaMemcpyDeviceToHost,
+                                    rt.stream()));
+        rt.sync();
+        return;
+    }
+    const std::vector<Chunk> ch = chunks_of(src.rows, src.cols);
+    auto issue = [&](size_t i) {
+        const int b = static_cast<int>(i & 1);
+        BOSP_CUDA(cudaMemcpy2DAsync(rt.stage(b), ch[i].nr * sizeof(double), src.p + ch[i].c0 * src.ld + ch[i].r0,
+                                    src.ld * sizeof(double), ch[i].nr * sizeof(double), ch[i].nc,
+                                    cudaMemcpyDeviceToHost, rt.stream()));
+        BOSP_CUDA(cudaEventRecord(rt.stage_event(b), rt.stream()));
+    };
+    issue(0);
+    for (size_t i = 0; i < ch.size(); ++i) {
+        const int b = static_cast<int>(i & 1);
+        BOSP_CUDA(cudaEventSynchronize(rt.stage_event(b)));
+        if (i + 1 < ch.size()) issue(i + 1);  // DMA of the next chunk overlaps this host copy
+        host_scatter(rt.stage(b), ch[i], host, ld_host, true);
+    }
 }
 
 void copy_block(const DMat& src, const DMat& dst) {

@@ -80,6 +80,11 @@ public:
     unsigned int* tickets(size_t count);
     // Pinned host staging (grow-only).
     double* pinned(size_t doubles);
+    // Double-buffered pinned ring for large pageable host<->device copies (to_host/to_device):
+    // buffer i of kStageDoubles doubles and its completion event.
+    static constexpr size_t kStageDoubles = size_t(1) << 20;  // 8 MB
+    double* stage(int i);
+    cudaEvent_t stage_event(int i);
 
     // Kernel accounting (gpu_launches) and optional CUDA-event timing of one kernel family.
     void count_launch(const char* family);
@@ -123,6 +128,8 @@ private:
     size_t tickets_cap_ = 0;
     double* pinned_ = nullptr;
     size_t pinned_cap_ = 0;
+    double* stage_[2] = {nullptr, nullptr};
+    cudaEvent_t stage_ev_[2] = {nullptr, nullptr};
     int64_t launches_ = 0;
     std::map<std::string, int64_t> family_launches_;
     std::map<std::string, int64_t>* capture_sink_ = nullptr;
@@ -182,6 +189,8 @@ private:
 // Device copies of small host matrices (column-major) and back.
 void to_device(const double* host, int64_t rows, int64_t cols, int64_t ld_host, const DMat& dst);
 void to_host(const DMat& src, double* host, int64_t ld_host);
+// Flat host -> device copy (stream-ordered; large 8-byte-multiple copies use the pinned ring).
+void h2d_bytes(void* dst, const void* src, size_t bytes);
 // D2D copy of a column range (handles differing ld).
 void copy_block(const DMat& src, const DMat& dst);
 

@@ -32,6 +32,13 @@ struct SpmmDot {
     int64_t parts_cap = 0;
 };
 
+// Device CSR -> SELL-32 conversion (rp/ci/vv device copies of the CSR arrays; rp may carry a
+// base offset rp[0]).  sell_layout writes the slice widths and offsets (nslices + 1) and returns
+// the padded entry count; sell_fill scatters columns/values (padding -> the row itself, 0.0).
+int64_t sell_layout(int64_t n, const int64_t* rp, int64_t* slice_ptr, int32_t* slice_w);
+void sell_fill(int64_t n, const int64_t* rp, const int64_t* ci, const double* vv, const int64_t* slice_ptr,
+               const int32_t* slice_w, int32_t* col, double* val);
+
 // y(:, j) = A x(:, j) for all columns of x (optionally with the fused dots); returns the number
 // of row blocks.
 int sell_spmm(const SellDev& a, const DMat& x, const DMat& y, const SpmmDot* dot = nullptr);

@@ -208,6 +208,97 @@ __global__ void __launch_bounds__(kRows) k_sell_plain(SellDev a, const double* _
     tm.stop();
 }
 
+// Wide variant: one thread per row loads the row's (<= kWide) entries once and sweeps all
+// columns in groups of 4 (not unrolled), so the matrix is read once per apply and each row
+// pays one index-load latency instead of one per column group.  With DOT the per-column
+// x^T y partials are warp-reduced per group (fixed order) into shared memory and folded per
+// block, then across blocks by the last block.
+constexpr int kWide = 8;
+constexpr int kWideMaxCols = 160;
+
+template <bool DOT>
+__global__ void __launch_bounds__(kRows, 3) k_sell_wide(SellDev a, const double* __restrict__ x, int64_t ldx,
+                                                         double* __restrict__ y, int64_t ldy, int ncols,
+                                                         KTimer tm, DotOut dots) {
+    __shared__ double red[DOT ? kRows / 32 : 1][DOT ? kWideMaxCols : 1];
+    tm.start();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (DOT)
+        for (int i = threadIdx.x; i < (kRows / 32) * ncols; i += kRows) red[i / ncols][i % ncols] = 0.0;
+    const int64_t ntiles = (a.n + kRows - 1) / kRows;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t row = tile * kRows + threadIdx.x;
+        const bool valid = row < a.n;
+        int w = 0;
+        int64_t base = 0;
+        if (valid) {
+            const int64_t s = row >> 5;
+            base = a.slice_ptr[s] + (row & 31);
+            w = a.slice_w[s];
+        }
+        const bool fast = w <= kWide;
+        int col[kWide];
+        double val[kWide];
+#pragma unroll
+        for (int k = 0; k < kWide; ++k) {
+            const bool in = fast && k < w;
+            col[k] = in ? __ldg(a.col + base + 32 * k) : 0;
+            val[k] = in ? __ldg(a.val + base + 32 * k) : 0.0;
+        }
+#pragma unroll 1
+        for (int j0 = 0; j0 < ncols; j0 += 4) {
+            bool on[4];
+            bool any = false;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                on[c] = j0 + c < ncols && (!DOT || !dots.active || dots.active[j0 + c] != 0);
+                any |= on[c];
+            }
+            if (!any) continue;  // uniform across the block
+            const double* xb = x + static_cast<int64_t>(j0) * ldx;
+            double acc[4] = {0.0, 0.0, 0.0, 0.0};
+            if (fast) {
+#pragma unroll
+                for (int k = 0; k < kWide; ++k)
+                    if (k < w)
+#pragma unroll
+                        for (int c = 0; c < 4; ++c)
+                            if (on[c]) acc[c] += val[k] * __ldg(xb + c * ldx + col[k]);
+            } else if (valid) {
+                for (int k = 0; k < w; ++k) {
+                    const int cc = __ldg(a.col + base + 32 * k);
+                    const double v = __ldg(a.val + base + 32 * k);
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+                        if (on[c]) acc[c] += v * __ldg(xb + c * ldx + cc);
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                if (!on[c]) continue;
+                if (valid) y[(j0 + c) * ldy + row] = acc[c];
+                if (DOT) {
+                    double t = valid ? __ldg(xb + c * ldx + row) * acc[c] : 0.0;
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+                    if (lane == 0) red[warp][j0 + c] += t;
+                }
+            }
+        }
+    }
+    if (DOT) {
+        __syncthreads();
+        for (int j = threadIdx.x; j < ncols; j += kRows) {
+            double t = 0.0;
+#pragma unroll
+            for (int q = 0; q < kRows / 32; ++q) t += red[q][j];
+            dots.parts[static_cast<int64_t>(j) * gridDim.x + blockIdx.x] = t;
+        }
+        fold_dots_last_block(dots.parts, ncols, dots.ticket, dots.out);
+    }
+    tm.stop();
+}
+
 // Column-group variant: grid.y walks groups of CB columns, grid.x strides over 256-row tiles;
 // the row's entries are re-read per column group (L2).  Optionally accumulates x^T y per
 // column (the CG's p^T A p) while y is produced.
@@ -387,6 +478,99 @@ unsigned row_blocks(int64_t n, const SpmmDot* dot, int ncols) {
 
 }  // namespace
 
+namespace {
+
+__global__ void k_slice_width(int64_t n, const int64_t* __restrict__ rp, int32_t* __restrict__ sw, int64_t nsl) {
+    const int64_t s = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (s >= nsl) return;
+    const int64_t r = s * 32 + lane;
+    int64_t len = r < n ? rp[r + 1] - rp[r] : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) len = max(len, __shfl_xor_sync(0xffffffffu, len, o));
+    if (lane == 0) sw[s] = static_cast<int32_t>(len);
+}
+
+// exclusive scan of 32 * width over the slices (one block; slices split into per-thread runs)
+__global__ void __launch_bounds__(1024) k_slice_scan(const int32_t* __restrict__ sw, int64_t nsl,
+                                                     int64_t* __restrict__ sp) {
+    __shared__ int64_t part[1024];
+    const int t = threadIdx.x;
+    const int64_t per = (nsl + 1023) / 1024;
+    const int64_t a = min(nsl, t * per), b = min(nsl, a + per);
+    int64_t sum = 0;
+    for (int64_t i = a; i < b; ++i) sum += 32 * static_cast<int64_t>(sw[i]);
+    part[t] = sum;
+    __syncthreads();
+    if (t == 0) {
+        int64_t acc = 0;
+        for (int i = 0; i < 1024; ++i) {
+            const int64_t v = part[i];
+            part[i] = acc;
+            acc += v;
+        }
+        sp[nsl] = acc;
+    }
+    __syncthreads();
+    int64_t acc = part[t];
+    for (int64_t i = a; i < b; ++i) {
+        sp[i] = acc;
+        acc += 32 * static_cast<int64_t>(sw[i]);
+    }
+}
+
+__global__ void k_sell_fill(int64_t n, const int64_t* __restrict__ rp, const int64_t* __restrict__ ci,
+                            const double* __restrict__ vv, const int64_t* __restrict__ sp,
+                            const int32_t* __restrict__ sw, int32_t* __restrict__ col, double* __restrict__ val,
+                            int64_t nsl) {
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t s = t >> 5;
+    const int lane = static_cast<int>(t & 31);
+    if (s >= nsl) return;
+    const int64_t r = s * 32 + lane;
+    const int64_t base = rp[0];
+    const int64_t beg = r < n ? rp[r] - base : 0;
+    const int64_t len = r < n ? rp[r + 1] - rp[r] : 0;
+    const int w = sw[s];
+    const int64_t o = sp[s] + lane;
+    for (int k = 0; k < w; ++k) {
+        const bool in = k < len;
+        col[o + 32 * k] = in ? static_cast<int32_t>(ci[beg + k]) : static_cast<int32_t>(r < n ? r : 0);
+        val[o + 32 * k] = in ? vv[beg + k] : 0.0;
+    }
+}
+
+}  // namespace
+
+int64_t sell_layout(int64_t n, const int64_t* rp, int64_t* slice_ptr, int32_t* slice_w) {
+    const int64_t nsl = (n + 31) / 32;
+    Runtime& rt = Runtime::get();
+    {
+        LaunchScope ls("setup");
+        k_slice_width<<<static_cast<unsigned>((nsl * 32 + 255) / 256), 256, 0, rt.stream()>>>(n, rp, slice_w, nsl);
+        BOSP_LAUNCH_CHECK();
+    }
+    {
+        LaunchScope ls("setup");
+        k_slice_scan<<<1, 1024, 0, rt.stream()>>>(slice_w, nsl, slice_ptr);
+        BOSP_LAUNCH_CHECK();
+    }
+    int64_t total = 0;
+    BOSP_CUDA(cudaMemcpyAsync(&total, slice_ptr + nsl, sizeof(int64_t), cudaMemcpyDeviceToHost, rt.stream()));
+    rt.sync();
+    return total;
+}
+
+void sell_fill(int64_t n, const int64_t* rp, const int64_t* ci, const double* vv, const int64_t* slice_ptr,
+               const int32_t* slice_w, int32_t* col, double* val) {
+    const int64_t nsl = (n + 31) / 32;
+    Runtime& rt = Runtime::get();
+    LaunchScope ls("setup");
+    k_sell_fill<<<static_cast<unsigned>((nsl * 32 + 255) / 256), 256, 0, rt.stream()>>>(n, rp, ci, vv, slice_ptr,
+                                                                                      slice_w, col, val, nsl);
+    BOSP_LAUNCH_CHECK();
+}
+
 int sell_spmm(const SellDev& a, const DMat& x, const DMat& y, const SpmmDot* dot) {
     if (a.n == 0 || x.cols == 0) return 0;
     Runtime& rt = Runtime::get();
@@ -412,10 +596,15 @@ int sell_spmm(const SellDev& a, const DMat& x, const DMat& y, const SpmmDot* dot
         else
             k_sell_cb<4, false, true><<<grid4, kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm, DotOut{});
     } else if (dot) {
-        k_sell_cb<4, true><<<grid4, kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm,
+        if (variant == 1 && ncols <= kWideMaxCols)
+            k_sell_wide<true><<<gx, kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm,
                                                              DotOut{dot->parts, dot->ticket, dot->out, dot->active});
+        else
+            k_sell_cb<4, true><<<grid4, kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm,
+                                                                 DotOut{dot->parts, dot->ticket, dot->out, dot->active});
     } else {
         switch (variant) {
+            case 1: k_sell_wide<false><<<gx, kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm, DotOut{}); break;
             case 0: k_sell<<<gx, kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm); break;
             case 2: k_sell_cb<2, false><<<dim3(gx, (ncols + 1) / 2), kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm, DotOut{}); break;
             case 8: k_sell_cb<8, false><<<dim3(gx, (ncols + 7) / 8), kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm, DotOut{}); break;
