@@ -97,8 +97,10 @@ void cg_update_fused(const DMat& x, const DMat& r, const DMat& p, const DMat& ap
                      int max_iter);
 // active & pap>0: x += a p, r -= a ap, rr_new; pap<=0 -> broken, inactive.  Then
 // p = r + beta p, rr = rr_new, active = sqrt(rr) > tol*bnorm && iters < max_iter.
+// pap_parts != nullptr: p^T A p is still in per-block partials (pap_parts[j * nparts + b], the
+// SpMM's unfolded dots) and every update block folds its column itself.
 void cg_update(const DMat& x, const DMat& r, const DMat& p, const DMat& ap, const CgScalars& s,
-               double tol, int max_iter);
+               double tol, int max_iter, const double* pap_parts = nullptr, int nparts = 0);
 
 }  // namespace b200
 }  // namespace bosp

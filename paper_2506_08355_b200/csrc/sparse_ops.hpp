@@ -26,7 +26,7 @@ struct SellDev {
 // folded in fixed order by the last block into out[j]; `ticket` must be zero and stays zero.
 struct SpmmDot {
     double* parts;              // per-block partials, parts_cap doubles
-    unsigned* ticket;
+    unsigned* ticket;           // nullptr: leave the partials unfolded (the consumer folds them)
     double* out;
     const int* active = nullptr;  // optional column mask: inactive columns are neither applied nor dotted
     int64_t parts_cap = 0;
@@ -42,6 +42,8 @@ void sell_fill(int64_t n, const int64_t* rp, const int64_t* ci, const double* vv
 // y(:, j) = A x(:, j) for all columns of x (optionally with the fused dots); returns the number
 // of row blocks.
 int sell_spmm(const SellDev& a, const DMat& x, const DMat& y, const SpmmDot* dot = nullptr);
+// Blocks a dot-fused apply of n rows x ncols uses (partials per column).
+unsigned spmm_dot_blocks(int64_t n, const SpmmDot& dot, int ncols);
 
 // Structured-grid Laplacian family: y = scale * (L_bc x) + v .* x on nx*ny*nz nodes (nz = 1 ->
 // 5-point).  bc: 0 = Neumann graph Laplacian (diag = #in-grid neighbours), 1 = Dirichlet

@@ -134,6 +134,7 @@ __device__ __forceinline__ void block_dots_out(double (&d)[CB], double* dots, in
 // (one warp per column, lanes strided) into out[j]; leaves the ticket at zero.
 __device__ __forceinline__ void fold_dots_last_block(const double* dots, int ncols, unsigned* ticket,
                                                      double* out) {
+    if (!ticket) return;  // partials left for the consumer
     __shared__ bool last;
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -144,10 +145,20 @@ __device__ __forceinline__ void fold_dots_last_block(const double* dots, int nco
     if (!last) return;
     __threadfence();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nb = static_cast<int>(gridDim.x);
     for (int j = warp; j < ncols; j += kRows / 32) {
-        double t = 0.0;
-        for (int q = lane; q < static_cast<int>(gridDim.x); q += 32)
-            t += __ldcg(dots + static_cast<int64_t>(j) * gridDim.x + q);
+        // four independent accumulators keep several L2 loads in flight per lane
+        const double* pj = dots + static_cast<int64_t>(j) * nb;
+        double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
+        int q = lane;
+        for (; q + 96 < nb; q += 128) {
+            t0 += __ldcg(pj + q);
+            t1 += __ldcg(pj + q + 32);
+            t2 += __ldcg(pj + q + 64);
+            t3 += __ldcg(pj + q + 96);
+        }
+        for (; q < nb; q += 32) t0 += __ldcg(pj + q);
+        double t = (t0 + t1) + (t2 + t3);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
         if (lane == 0) out[j] = t;
@@ -472,8 +483,11 @@ __global__ void __launch_bounds__(kRows) k_stencil(StencilDev st, const double* 
 unsigned row_blocks(int64_t n, const SpmmDot* dot, int ncols) {
     const int64_t tiles = (n + kRows - 1) / kRows;
     if (!dot) return static_cast<unsigned>(tiles);
+    // with dots: bounded by the partials buffer; when this launch folds them itself (ticket),
+    // also by a few waves so the last block's fold stays short
     const int64_t cap = std::max<int64_t>(1, dot->parts_cap / std::max(ncols, 1));
-    return static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(tiles, cap)));
+    const int64_t waves = dot->ticket ? 4LL * Runtime::get().sm_count() : tiles;
+    return static_cast<unsigned>(std::max<int64_t>(1, std::min({tiles, cap, waves})));
 }
 
 }  // namespace
@@ -570,6 +584,8 @@ void sell_fill(int64_t n, const int64_t* rp, const int64_t* ci, const double* vv
                                                                                       slice_w, col, val, nsl);
     BOSP_LAUNCH_CHECK();
 }
+
+unsigned spmm_dot_blocks(int64_t n, const SpmmDot& dot, int ncols) { return row_blocks(n, &dot, ncols); }
 
 int sell_spmm(const SellDev& a, const DMat& x, const DMat& y, const SpmmDot* dot) {
     if (a.n == 0 || x.cols == 0) return 0;

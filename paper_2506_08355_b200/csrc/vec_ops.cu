@@ -76,18 +76,28 @@ __global__ void __launch_bounds__(kThreads) k_colred(int64_t n, int ncols, int n
     __syncthreads();
     if (!last) return;
     __threadfence();
-    for (int jj = threadIdx.x; jj < ncols; jj += kThreads) {
-        double s[K];
+    // fold: one warp per column, lanes strided over the chunks (all loads independent), then a
+    // fixed shuffle tree -- the tail block finishes in a few L2 round trips, not nchunks
+    {
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        for (int jj = warp; jj < ncols; jj += kThreads / 32) {
+            double s[K];
 #pragma unroll
-        for (int k = 0; k < K; ++k) s[k] = 0.0;
-        for (int cc = 0; cc < nchunks; ++cc)
+            for (int k = 0; k < K; ++k) s[k] = 0.0;
+            for (int cc = lane; cc < nchunks; cc += 32)
 #pragma unroll
-            for (int k = 0; k < K; ++k) s[k] += __ldcg(&partial[(static_cast<int64_t>(jj) * nchunks + cc) * K + k]);
-        if (defer) {  // row-partitioned: the epilogue runs after the cross-rank allreduce
+                for (int k = 0; k < K; ++k) s[k] += __ldcg(&partial[(static_cast<int64_t>(jj) * nchunks + cc) * K + k]);
 #pragma unroll
-            for (int k = 0; k < K; ++k) defer[k * ncols + jj] = s[k];
-        } else {
-            f.fin(jj, s);
+            for (int k = 0; k < K; ++k)
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) s[k] += __shfl_xor_sync(0xffffffffu, s[k], o);
+            if (lane != 0) continue;
+            if (defer) {  // row-partitioned: the epilogue runs after the cross-rank allreduce
+#pragma unroll
+                for (int k = 0; k < K; ++k) defer[k * ncols + jj] = s[k];
+            } else {
+                f.fin(jj, s);
+            }
         }
     }
     __syncthreads();
@@ -284,15 +294,43 @@ struct CgPapF : NoFinAll {
 };
 
 // x += alpha p, r -= alpha ap, accumulate r^T r (cg.cpp:37-48); epilogue decides the masks.
+// With pap_parts set, every block first folds the SpMM's per-block p^T A p partials of its own
+// column (fixed order, all blocks in parallel) instead of the SpMM's last block doing it
+// serially; block 0 of the column publishes the value to s.pap for the epilogue.
+__device__ __forceinline__ double& xr_pap_slot() {
+    __shared__ double v;
+    return v;
+}
+
 struct CgXrF {
     double *x, *r; const double *p, *ap; int64_t lx, lr, lp, lap;
     CgScalars s;
     double* beta;
     double tol; int max_iter;
-    __device__ void prologue(int) const {}
-    __device__ bool skip(int j) const { return s.active[j] == 0 || !(s.pap[j] > 0.0); }
+    const double* pap_parts = nullptr;
+    int nparts = 0;
+    __device__ void prologue(int j) const {
+        if (!pap_parts) return;
+        __shared__ double red[kThreads / 32];
+        double t = 0.0;
+        for (int q = threadIdx.x; q < nparts; q += kThreads)
+            t += __ldcg(pap_parts + static_cast<int64_t>(j) * nparts + q);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = t;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double v = 0.0;
+            for (int w = 0; w < kThreads / 32; ++w) v += red[w];
+            xr_pap_slot() = v;
+            if (blockIdx.x == 0) s.pap[j] = v;
+        }
+        __syncthreads();
+    }
+    __device__ double pap(int j) const { return pap_parts ? xr_pap_slot() : s.pap[j]; }
+    __device__ bool skip(int j) const { return s.active[j] == 0 || !(pap(j) > 0.0); }
     __device__ void row(int64_t i, int j, double (&a)[1]) const {
-        const double alpha = s.rr[j] / s.pap[j];
+        const double alpha = s.rr[j] / pap(j);
         const double xv = x[i + j * lx] + alpha * p[i + j * lp];
         const double rv = r[i + j * lr] - alpha * ap[i + j * lap];
         x[i + j * lx] = xv;
@@ -300,7 +338,7 @@ struct CgXrF {
         a[0] += rv * rv;
     }
     __device__ void row2(int64_t i, int j, double (&a)[1]) const {
-        const double alpha = s.rr[j] / s.pap[j];
+        const double alpha = s.rr[j] / pap(j);
         const double2 xv = ld2(x + i + j * lx), pv = ldg2(p + i + j * lp);
         const double2 rv = ld2(r + i + j * lr), av = ldg2(ap + i + j * lap);
         const double x0 = xv.x + alpha * pv.x, x1 = xv.y + alpha * pv.y;
@@ -643,11 +681,13 @@ void cg_pap(const DMat& p, const DMat& ap, const CgScalars& s) {
 }
 
 void cg_update(const DMat& x, const DMat& r, const DMat& p, const DMat& ap, const CgScalars& s,
-               double tol, int max_iter) {
+               double tol, int max_iter, const double* pap_parts, int nparts) {
     CgXrF f;
     f.x = x.p; f.r = r.p; f.p = p.p; f.ap = ap.p; f.lx = x.ld; f.lr = r.ld; f.lp = p.ld; f.lap = ap.ld;
     f.s = s; f.beta = s.beta;
     f.tol = tol; f.max_iter = max_iter;
+    f.pap_parts = pap_parts;
+    f.nparts = nparts;
     launch_colred<1>("cg_vec", x.rows, static_cast<int>(x.cols), f, 48.0 * x.rows * x.cols);
     CgDirF d{r.p, p.p, r.ld, p.ld, s.beta, s.active};
     launch_cols("cg_vec", r.rows, static_cast<int>(r.cols), d, 24.0 * r.rows * r.cols);
