@@ -188,6 +188,7 @@ def run_b200(args, world, rank, local, dist):
     units = 1 if partitioned else world  # one shared problem vs. one replica per rank
 
     def one_step(profile_family=None):
+        profile_family = profile_family or None
         _lib.lib().bosp_flush_l2(flush)
         if profile_family:
             bosp.profile_enable(profile_family)
@@ -323,7 +324,8 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--roofline-kernel", default="spmm")
+    ap.add_argument("--roofline-kernel", default="spmm_cg",
+                    help="kernel family timed for the roofline (default: the dominant one, the CG SpMM)")
     ap.add_argument("--ref-iters", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--partition", default="rows", choices=["rows", "replicas"],

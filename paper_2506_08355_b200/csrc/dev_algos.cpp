@@ -204,6 +204,8 @@ double dev_biorth_residual(const DMat& p, const DMat& q, const InnerProduct& ip)
 // Batched multi-RHS CG
 // ---------------------------------------------------------------------------------------------
 namespace {
+constexpr int64_t kCgUnrollMax = 32;
+
 void drop_graphs(std::vector<CgGraph>& gs) {
     for (CgGraph& g : gs) {
         if (g.exec) cudaGraphExecDestroy(g.exec);
@@ -339,6 +341,22 @@ DevCgOutcome dev_cg(const LinearOperator& a, const DMat& rhs, const DMat& x, dou
             rt.tickets(64);
             rt.sync();
             BOSP_CUDA(cudaGraphCreate(&g->graph, 0));
+            // Short solves (the solver's inner CG: max_iter 20) are unrolled into a straight
+            // graph -- every kernel early-outs once its columns are done, no conditional node,
+            // and every launch keeps its own profiling slot.  Long solves use a device while loop.
+            static const bool force_while = std::getenv("BOSP_CG_WHILE") != nullptr;
+            if (max_iter <= kCgUnrollMax && !force_while) {
+                CgScalars sc = ws.s;
+                sc.has_cond = 0;
+                rt.set_capture_sink(&g->start_launches);
+                BOSP_CUDA(cudaStreamBeginCaptureToGraph(rt.stream(), g->graph, nullptr, nullptr, 0,
+                                                        cudaStreamCaptureModeRelaxed));
+                rt.timer_reserve(max_iter);  // one memset node for every timed launch below
+                cg_start(rhs, x, r, p, sc, tol, mi);
+                for (int64_t it = 0; it < max_iter; ++it) cg_iteration(a, x, r, p, ap, sc, ws, tol, mi);
+                rt.timer_reserve(0);
+                BOSP_CUDA(cudaStreamEndCapture(rt.stream(), &g->graph));
+            } else {
             cudaGraphConditionalHandle h;
             BOSP_CUDA(cudaGraphConditionalHandleCreate(&h, g->graph, 0, 0));
             CgScalars sc = ws.s;
@@ -367,6 +385,7 @@ DevCgOutcome dev_cg(const LinearOperator& a, const DMat& rhs, const DMat& x, dou
                                                     cudaStreamCaptureModeRelaxed));
             cg_iteration(a, x, r, p, ap, sc, ws, tol, mi);
             BOSP_CUDA(cudaStreamEndCapture(rt.stream(), &body));
+            }
             rt.set_capture_sink(nullptr);
             rt.set_capture_prof(nullptr);
             BOSP_CUDA(cudaGraphInstantiate(&g->exec, g->graph, 0));
@@ -375,7 +394,8 @@ DevCgOutcome dev_cg(const LinearOperator& a, const DMat& rhs, const DMat& x, dou
         BOSP_CUDA(cudaMemcpyAsync(&ws.host_active[2], ws.s.loops, sizeof(int), cudaMemcpyDeviceToHost, rt.stream()));
         rt.sync();
         out.sweeps = ws.host_active[2];
-        // event pairs inside the body hold the last iteration's launch: one live sample each
+        // timer slots recorded in the graph: every launch of an unrolled graph, the last
+        // iteration of a while body
         if (!g->prof_pairs.empty() && out.sweeps > 0) rt.add_prof_samples(g->prof_pairs);
         rt.add_launches(g->start_launches, 1);
         rt.add_launches(g->body_launches, out.sweeps);

@@ -1,5 +1,6 @@
 #include "runtime.hpp"
 
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 
@@ -148,32 +149,62 @@ void Runtime::prof_end(const char* family) {
     BOSP_CUDA(cudaEventRecord(prof_events_.back().b, stream_));
 }
 
-unsigned long long* Runtime::timer_begin(const char* family, double bytes, double flops) {
+unsigned long long* Runtime::timer_begin(const char* family, double bytes, double flops, double fixed_bytes,
+                                         int64_t ncols) {
     if (!prof_on(family)) return nullptr;
     if (!timer_slots_) {
-        BOSP_CUDA(cudaMalloc(&timer_slots_, sizeof(unsigned long long) * 2 * kTimerSlots));
+        BOSP_CUDA(cudaMalloc(&timer_slots_, sizeof(unsigned long long) * kSlotWords * kTimerSlots));
     }
     const int64_t slot = timer_next_++ % kTimerSlots;
-    unsigned long long* p = timer_slots_ + 2 * slot;
-    BOSP_CUDA(cudaMemsetAsync(p, 0, 2 * sizeof(unsigned long long), stream_));
-    ProfPair pp{slot, bytes, flops};
+    unsigned long long* p = timer_slots_ + kSlotWords * slot;
+    if (timer_reserved_ > 0) --timer_reserved_;
+    else BOSP_CUDA(cudaMemsetAsync(p, 0, kSlotWords * sizeof(unsigned long long), stream_));
+    ProfPair pp{slot, bytes, flops, fixed_bytes, ncols};
     if (capture_prof_) capture_prof_->push_back(pp);
     else timer_pending_.push_back(pp);
     return p;
 }
 
+void Runtime::timer_reserve(int64_t count) {
+    if (count <= 0) {
+        timer_reserved_ = 0;  // end of a reserved section
+        return;
+    }
+    if (prof_family_.empty()) return;
+    if (!timer_slots_) BOSP_CUDA(cudaMalloc(&timer_slots_, sizeof(unsigned long long) * kSlotWords * kTimerSlots));
+    count = std::min<int64_t>(count, kTimerSlots / 2);
+    if (timer_next_ % kTimerSlots + count > kTimerSlots) timer_next_ += kTimerSlots - timer_next_ % kTimerSlots;
+    BOSP_CUDA(cudaMemsetAsync(timer_slots_ + kSlotWords * (timer_next_ % kTimerSlots), 0,
+                              sizeof(unsigned long long) * kSlotWords * count, stream_));
+    timer_reserved_ = count;
+}
+
 void Runtime::read_timer_samples(const std::vector<ProfPair>& pairs) {
     if (pairs.empty()) return;
-    std::vector<unsigned long long> host(2 * kTimerSlots);
-    BOSP_CUDA(cudaMemcpy(host.data(), timer_slots_, sizeof(unsigned long long) * 2 * kTimerSlots,
-                         cudaMemcpyDeviceToHost));
+    // copy only the slot range these pairs use (they are allocated consecutively)
+    int64_t lo = kTimerSlots, hi = -1;
     for (const ProfPair& p : pairs) {
-        const unsigned long long s = ~host[2 * p.slot], e = host[2 * p.slot + 1];
-        if (host[2 * p.slot] == 0 || e == 0 || e < s) continue;
+        lo = std::min(lo, p.slot);
+        hi = std::max(hi, p.slot);
+    }
+    const int64_t cnt = hi - lo + 1;
+    if (static_cast<int64_t>(timer_host_.size()) < kSlotWords * cnt) timer_host_.resize(kSlotWords * cnt);
+    BOSP_CUDA(cudaMemcpy(timer_host_.data(), timer_slots_ + kSlotWords * lo,
+                         sizeof(unsigned long long) * kSlotWords * cnt, cudaMemcpyDeviceToHost));
+    for (const ProfPair& p : pairs) {
+        const unsigned long long* w = timer_host_.data() + kSlotWords * (p.slot - lo);
+        const unsigned long long s = ~w[0], e = w[1];
+        if (w[0] == 0 || e == 0 || e < s) continue;
+        double frac = 1.0;
+        if (p.ncols > 0) {  // the kernel reports how many columns it applied
+            const int64_t act = static_cast<int64_t>(w[2]);
+            if (act == 0) continue;  // nothing to do (converged columns): not a real apply
+            frac = static_cast<double>(act) / static_cast<double>(p.ncols);
+        }
         graph_samples_.launches += 1;
         graph_samples_.ms += (e - s) * 1e-6;
-        graph_samples_.bytes += p.bytes;
-        graph_samples_.flops += p.flops;
+        graph_samples_.bytes += p.fixed_bytes + (p.bytes - p.fixed_bytes) * frac;
+        graph_samples_.flops += p.flops * frac;
     }
 }
 

@@ -108,8 +108,17 @@ public:
     // allowed in conditional bodies): the kernel writes (max of ~start, max of end) %globaltimer
     // into a 2-word slot that a memset resets before each launch.  A launch recorded into a
     // graph keeps its slot; after each replay the slot holds that launch's last execution.
-    struct ProfPair { int64_t slot; double bytes, flops; };
-    unsigned long long* timer_begin(const char* family, double bytes, double flops);
+    // Slot words: [~earliest start, latest end, columns the launch actually applied (0 = none
+    // reported)].  bytes/flops are the launch's algorithmic totals for all `ncols` columns; a
+    // launch that reports fewer active columns is credited proportionally (fixed part kept).
+    struct ProfPair { int64_t slot; double bytes, flops, fixed_bytes; int64_t ncols; };
+    static constexpr int kSlotWords = 4;
+    unsigned long long* timer_begin(const char* family, double bytes, double flops, double fixed_bytes = 0.0,
+                                    int64_t ncols = 0);
+    // Zero `count` consecutive slots with one memset; the next `count` timer_begin calls take
+    // them without their own memset (one memset node per recorded graph instead of one per
+    // timed launch).  No-op unless a family is being profiled.
+    void timer_reserve(int64_t count);
     void set_capture_prof(std::vector<ProfPair>* sink) { capture_prof_ = sink; }
     void add_prof_samples(const std::vector<ProfPair>& pairs);  // after the replay finished
     const std::string& prof_family() const { return prof_family_; }
@@ -139,6 +148,8 @@ private:
     std::vector<ProfPair>* capture_prof_ = nullptr;
     std::vector<ProfPair> timer_pending_;
     unsigned long long* timer_slots_ = nullptr;
+    std::vector<unsigned long long> timer_host_;
+    int64_t timer_reserved_ = 0;
     int64_t timer_next_ = 0;
     static constexpr int64_t kTimerSlots = 1 << 15;
     ProfReport graph_samples_{0, 0.0, 0.0, 0.0};

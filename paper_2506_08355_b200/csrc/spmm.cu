@@ -26,11 +26,23 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 
 // Device-clock timing of one launch (Runtime::timer_begin): slot[0] = max(~start) -> earliest
-// start, slot[1] = max(end) -> latest end.
+// start, slot[1] = max(end) -> latest end, slot[2] = columns applied (reported by block 0).
 struct KTimer {
     unsigned long long* slot;
     __device__ __forceinline__ void start() const {
         if (slot && threadIdx.x == 0) atomicMax(&slot[0], ~gtimer());
+    }
+    __device__ __forceinline__ void columns(const int* active, int j0, int n, int ncols_total) const {
+        // one block reports the applied column count of the whole launch
+        if (!slot || threadIdx.x != 0 || blockIdx.x != 0 || blockIdx.y != 0) return;
+        (void)j0;
+        (void)n;
+        int c = ncols_total;
+        if (active) {
+            c = 0;
+            for (int j = 0; j < ncols_total; ++j) c += active[j] != 0;
+        }
+        slot[2] = static_cast<unsigned long long>(c);
     }
     __device__ __forceinline__ void stop() const {
         if (slot) {
@@ -55,6 +67,7 @@ __global__ void __launch_bounds__(kRows) k_sell(SellDev a, const double* __restr
                                                  double* __restrict__ y, int64_t ldy, int ncols,
                                                  KTimer tm) {
     tm.start();
+    tm.columns(nullptr, 0, 0, ncols);
     const int64_t row = static_cast<int64_t>(blockIdx.x) * kRows + threadIdx.x;
     if (row < a.n) {
         const int64_t s = row >> 5;
@@ -193,6 +206,7 @@ __global__ void __launch_bounds__(kRows) k_sell_plain(SellDev a, const double* _
                                                        double* __restrict__ y, int64_t ldy, int ncols,
                                                        KTimer tm) {
     tm.start();
+    tm.columns(nullptr, 0, 0, ncols);
     const int j0 = blockIdx.y * CB;
     const int64_t ntiles = (a.n + kRows - 1) / kRows;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -233,6 +247,7 @@ __global__ void __launch_bounds__(kRows, 3) k_sell_wide(SellDev a, const double*
                                                          KTimer tm, DotOut dots) {
     __shared__ double red[DOT ? kRows / 32 : 1][DOT ? kWideMaxCols : 1];
     tm.start();
+    tm.columns(DOT ? dots.active : nullptr, 0, 0, ncols);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (DOT)
         for (int i = threadIdx.x; i < (kRows / 32) * ncols; i += kRows) red[i / ncols][i % ncols] = 0.0;
@@ -318,6 +333,7 @@ __global__ void __launch_bounds__(kRows, BOSP_SELL_MINB) k_sell_cb(SellDev a, co
                                                     double* __restrict__ y, int64_t ldy, int ncols,
                                                     KTimer tm, DotOut dots) {
     tm.start();
+    tm.columns(DOT ? dots.active : nullptr, 0, 0, ncols);
     const int j0 = blockIdx.y * CB;
     double d[CB];
 #pragma unroll
@@ -368,6 +384,7 @@ __global__ void __launch_bounds__(kRows) k_stencil(StencilDev st, const double* 
                                                     int64_t ldx, double* __restrict__ y,
                                                     int64_t ldy, int ncols, KTimer tm, DotOut dots) {
     tm.start();
+    tm.columns(DOT ? dots.active : nullptr, 0, 0, ncols);
     const int64_t n = st.nx * st.ny * st.nz;
     const int j0 = blockIdx.y * CB;
     double d[CB];
@@ -595,10 +612,11 @@ int sell_spmm(const SellDev& a, const DMat& x, const DMat& y, const SpmmDot* dot
     // 4 B per row pointer) + x read once + y written once
     const double bytes = 12.0 * a.nnz + 4.0 * (a.n + 1) + 16.0 * a.n * ncols;
     const double flops = 2.0 * a.nnz * ncols;
-    // the CG's masked applies (family spmm_cg) touch only the active columns, so their bytes
-    // are not known on the host; the roofline family "spmm" is the unmasked applies
+    // the CG's masked applies (family spmm_cg) touch only the active columns: the kernel
+    // reports how many, and the profiler credits the bytes accordingly
     const char* fam = dot ? "spmm_cg" : "spmm";
-    KTimer tm{rt.timer_begin(fam, bytes, flops)};
+    // per-column share of the bytes scales with the columns the launch reports as applied
+    KTimer tm{rt.timer_begin(fam, bytes, flops, 12.0 * a.nnz + 4.0 * (a.n + 1), ncols)};
     LaunchScope ls(fam, bytes, flops, false);
     // Column groups of CB (grid.y) keep many independent blocks in flight; measured 2x the
     // bandwidth of the all-columns-per-thread variant (k_sell) on config 2 (B200).
@@ -641,10 +659,11 @@ int stencil_spmm(const StencilDev& s, const DMat& x, const DMat& y, const SpmmDo
     dim3 grid(gx, (ncols + CB - 1) / CB);
     const double pts = s.nz > 1 ? 7.0 : 5.0;
     const double bytes = 16.0 * n * ncols, flops = 2.0 * pts * n * ncols;
-    // the CG's masked applies (family spmm_cg) touch only the active columns, so their bytes
-    // are not known on the host; the roofline family "spmm" is the unmasked applies
+    // the CG's masked applies (family spmm_cg) touch only the active columns: the kernel
+    // reports how many, and the profiler credits the bytes accordingly
     const char* fam = dot ? "spmm_cg" : "spmm";
-    KTimer tm{rt.timer_begin(fam, bytes, flops)};
+    // per-column share of the bytes scales with the columns the launch reports as applied
+    KTimer tm{rt.timer_begin(fam, bytes, flops, 0.0, ncols)};
     LaunchScope ls(fam, bytes, flops, false);
     const int64_t snl = s.dims == 3 ? s.nz : s.ny;
     const bool part = s.s_global > 0 && (s.s0 > 0 || s.s0 + snl < s.s_global);

@@ -208,9 +208,10 @@ struct ResidF : NoFinAll {
 __device__ __forceinline__ void cg_publish(const CgScalars& s, int ncols, bool reset_loops) {
     int c = 0;
     for (int j = 0; j < ncols; ++j) c += s.active[j];
-    *s.any_active = c;
+    // an iteration counts when some column entered it active (unrolled graphs launch idle ones)
     if (reset_loops) *s.loops = 0;
-    else *s.loops += 1;
+    else if (*s.any_active > 0) *s.loops += 1;
+    *s.any_active = c;
     if (s.has_cond) cudaGraphSetConditional(s.cond, c > 0 ? 1u : 0u);
 }
 
@@ -559,8 +560,8 @@ __global__ void __launch_bounds__(kThreads) k_cg_update_fused(
     if (b == 0 && threadIdx.x == 0) {
         int c = 0;
         for (int j = 0; j < ncols; ++j) c += s_new[j];
+        if (*s.any_active > 0) *s.loops += 1;
         *s.any_active = c;
-        *s.loops += 1;
         if (s.has_cond) cudaGraphSetConditional(s.cond, c > 0 ? 1u : 0u);
     }
 }
