@@ -268,9 +268,19 @@ def run_b200(args, world, rank, local, dist):
         bytes_k = sum(p["bytes"] for p in pr)
         if launches_k and ms_k > 0:
             achieved = bytes_k / (ms_k * 1e-3) / 1e9
+            traffic, traffic_note = None, None
+            try:  # DRAM bytes per launch of the same kernel from the committed ncu --set full capture
+                tr = json.load(open(os.path.join(ROOT, "profiles", "roofline_traffic.json")))
+                if args.roofline_kernel in tr.get("kernel", ""):
+                    traffic = tr["dram_bytes_per_launch"]
+                    traffic_note = {"algorithmic_bytes_per_launch_in_capture": tr["algorithmic_bytes_per_launch"],
+                                    "source": tr["capture"]}
+            except Exception:
+                pass
             roof = {"kernel": args.roofline_kernel, "bound": "hbm", "achieved": achieved,
                     "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
-                    "frac": achieved / peaks.get("hbm_gbs", 6650.0), "traffic": None,
+                    "frac": achieved / peaks.get("hbm_gbs", 6650.0), "traffic": traffic,
+                    "traffic_capture": traffic_note,
                     "launches_per_step": launches_k / len(pr),
                     "avg_launch_us": ms_k * 1e3 / launches_k,
                     "algorithmic_bytes_per_launch": bytes_k / launches_k,
