@@ -73,6 +73,7 @@ struct CgScalars {
     int* iters;       // iterations taken
     int* any_active;  // scalar: number of active columns (device)
     int* loops;       // scalar: batched iterations executed (device)
+    unsigned long long* total = nullptr;  // running count of batched iterations over all solves
     double* parts;    // scratch for per-block partial sums (cg_update_fused / fused SpMM dots)
     int parts_cap;    // doubles available at `parts`
     // When the CG runs as a CUDA graph with a `while` conditional node, the start/update

@@ -39,6 +39,42 @@ DenseMatrix ip_gram_host(const InnerProduct& ip, const DMat& a, const DMat& b) {
     return h;
 }
 
+std::vector<DenseMatrix> ip_grams_host(const InnerProduct& ip, const std::vector<std::pair<DMat, DMat>>& pairs) {
+    std::vector<DenseMatrix> out;
+    std::vector<int64_t> off;
+    int64_t total = 0;
+    for (const auto& pr : pairs) {
+        out.emplace_back(pr.first.cols, pr.second.cols);
+        off.push_back(total);
+        total += pr.first.cols * pr.second.cols;
+    }
+    if (total == 0) return out;
+    Runtime& rt = Runtime::get();
+    DBlock g(total, 1);
+    std::vector<DBlock> weighted;
+    std::vector<GramJob> jobs;
+    for (size_t i = 0; i < pairs.size(); ++i) {
+        const DMat& a = pairs[i].first;
+        DMat b = pairs[i].second;
+        if (a.cols == 0 || b.cols == 0) continue;
+        if (ip.weighted()) {
+            weighted.emplace_back(b.rows, b.cols);
+            ip.weight()->apply_device(b, weighted.back().view());
+            b = weighted.back().view();
+        }
+        jobs.push_back({ColList(a), ColList(b), g.data() + off[i], a.cols});
+    }
+    for (size_t i = 0; i < jobs.size(); i += 4)
+        gram(jobs.data() + i, static_cast<int>(std::min<size_t>(4, jobs.size() - i)), pairs[0].first.rows);
+    rt.allreduce(g.data(), total);
+    std::vector<double> h(static_cast<size_t>(total));
+    BOSP_CUDA(cudaMemcpyAsync(h.data(), g.data(), sizeof(double) * total, cudaMemcpyDeviceToHost, rt.stream()));
+    rt.sync();
+    for (size_t i = 0; i < pairs.size(); ++i)
+        std::copy(h.begin() + off[i], h.begin() + off[i] + out[i].rows() * out[i].cols(), out[i].data());
+    return out;
+}
+
 // ---------------------------------------------------------------------------------------------
 // biorth_against: per basis two Grams (one launch) and two in-place axpy products (one launch)
 // ---------------------------------------------------------------------------------------------
@@ -246,9 +282,10 @@ void CgWorkspace::ensure(int64_t n, int64_t m) {
     }
     if (!parts_) {  // [pap partials | r^T r partials], 160 columns x 512 blocks each
         parts_ = static_cast<double*>(Runtime::get().alloc(sizeof(double) * 2 * kPartsPerRegion));
-        ticket_ = static_cast<unsigned*>(Runtime::get().alloc(sizeof(unsigned) * 4));
-        BOSP_CUDA(cudaMemsetAsync(ticket_, 0, sizeof(unsigned) * 4, Runtime::get().stream()));
+        ticket_ = static_cast<unsigned*>(Runtime::get().alloc(sizeof(unsigned) * 4 + sizeof(unsigned long long)));
+        BOSP_CUDA(cudaMemsetAsync(ticket_, 0, sizeof(unsigned) * 4 + sizeof(unsigned long long), Runtime::get().stream()));
     }
+    s.total = reinterpret_cast<unsigned long long*>(ticket_ + 4);
     s.parts = parts_ + kPartsPerRegion;
     s.parts_cap = static_cast<int>(kPartsPerRegion);
     if (!host_active) {
@@ -256,6 +293,14 @@ void CgWorkspace::ensure(int64_t n, int64_t m) {
         BOSP_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
         BOSP_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
     }
+}
+
+int64_t CgWorkspace::total_sweeps() {
+    if (!s.total) return 0;
+    unsigned long long t = 0;
+    BOSP_CUDA(cudaMemcpyAsync(&t, s.total, sizeof(t), cudaMemcpyDeviceToHost, Runtime::get().stream()));
+    Runtime::get().sync();
+    return static_cast<int64_t>(t);
 }
 
 CgWorkspace::~CgWorkspace() {
@@ -305,7 +350,7 @@ void cg_iteration(const LinearOperator& a, const DMat& x, const DMat& r, const D
 }  // namespace
 
 DevCgOutcome dev_cg(const LinearOperator& a, const DMat& rhs, const DMat& x, double tol,
-                    int64_t max_iter, CgWorkspace& ws, const DMat* x0, bool want_stats) {
+                    int64_t max_iter, CgWorkspace& ws, const DMat* x0, bool want_stats, bool defer_sweeps) {
     require(rhs.rows == a.dim() && x.rows == a.dim() && rhs.cols == x.cols, "cg_solve: shape mismatch");
     DevCgOutcome out;
     const int64_t m = rhs.cols;
@@ -391,6 +436,12 @@ DevCgOutcome dev_cg(const LinearOperator& a, const DMat& rhs, const DMat& x, dou
             BOSP_CUDA(cudaGraphInstantiate(&g->exec, g->graph, 0));
         }
         BOSP_CUDA(cudaGraphLaunch(g->exec, rt.stream()));
+        if (defer_sweeps && g->body_launches.empty() && g->prof_pairs.empty() && !want_stats) {
+            // unrolled graph: every launch is known, the sweep count lands in ws.s.total
+            rt.add_launches(g->start_launches, 1);
+            out.sweeps = -1;
+            return out;
+        }
         BOSP_CUDA(cudaMemcpyAsync(&ws.host_active[2], ws.s.loops, sizeof(int), cudaMemcpyDeviceToHost, rt.stream()));
         rt.sync();
         out.sweeps = ws.host_active[2];

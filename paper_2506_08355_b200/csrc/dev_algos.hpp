@@ -16,6 +16,8 @@ inline namespace b200 {
 
 // G = A^T (W B) for the inner product's weight W (identity when unweighted); a x b.
 DenseMatrix ip_gram_host(const InnerProduct& ip, const DMat& a, const DMat& b);
+// Several Grams in as few launches as possible (<= 4 jobs each) and one device->host copy.
+std::vector<DenseMatrix> ip_grams_host(const InnerProduct& ip, const std::vector<std::pair<DMat, DMat>>& pairs);
 void ip_gram_dev(const InnerProduct& ip, const DMat& a, const DMat& b, const DMat& g);
 // W B into `out` (copy when unweighted).
 void apply_weight(const InnerProduct& ip, const DMat& b, const DMat& out);
@@ -65,6 +67,8 @@ public:
     cudaEvent_t ev[2] = {nullptr, nullptr};
     std::vector<CgGraph> graphs;
     double* pap_parts() const { return parts_; }
+    // batched CG iterations of every solve run on this workspace (synchronises)
+    int64_t total_sweeps();
     unsigned* ticket() const { return ticket_; }
     ~CgWorkspace();
     static constexpr int64_t kPartsPerRegion = 160 * 512;
@@ -81,9 +85,11 @@ struct DevCgOutcome {
     int64_t sweeps = 0;  // batched iterations executed
 };
 // x = CG(A, rhs) column by column with masks (cg.cpp:11-58); x0 = 0 when x0 == nullptr.
+// defer_sweeps: the unrolled-graph path returns without waiting for the solve (sweeps = -1;
+// the count accumulates on the device, CgWorkspace::total_sweeps()).
 DevCgOutcome dev_cg(const LinearOperator& a, const DMat& rhs, const DMat& x, double tol,
                     int64_t max_iter, CgWorkspace& ws, const DMat* x0 = nullptr,
-                    bool want_stats = false);
+                    bool want_stats = false, bool defer_sweeps = false);
 
 }  // namespace b200
 }  // namespace bosp

@@ -74,6 +74,7 @@ struct DeviceState {
     DBlock small;                 // device copies of small coefficient matrices
     DBlock scal;                  // per-column scalars (lambdas, residual sums)
     CgWorkspace cg;
+    bool cg_deferred = false;  // some CG sweep counts are still on the device (cg.total_sweeps)
 
     int64_t width() const { return wx + wp + ww; }
     DMat X() const { return U.cols(0, wx); }
@@ -160,15 +161,19 @@ void rebiorthogonalize_state(DeviceState& st, const InnerProduct& ip) {
 double sample_invariants(DeviceState& st, const InnerProduct& ip) {
     const int64_t d = st.width();
     const DMat u = st.U.cols(0, d), v = st.V.cols(0, d);
-    DenseMatrix g = ip_gram_host(ip, u, v);
+    // U^T V and every deflation cross-Gram in one batch, one device->host copy
+    std::vector<std::pair<DMat, DMat>> pairs{{u, v}};
+    for (const DevBasis& b : deflation_bases(st)) {
+        pairs.push_back({b.q, u});
+        pairs.push_back({b.p, v});
+    }
+    std::vector<DenseMatrix> gs = ip_grams_host(ip, pairs);
+    DenseMatrix& g = gs[0];
     for (int64_t i = 0; i < g.rows(); ++i) g(i, i) -= 1.0;
     const double dev = g.max_abs();
     st.stats.max_biorth_deviation = std::max(st.stats.max_biorth_deviation, dev);
     double cg = 0.0;
-    for (const DevBasis& b : deflation_bases(st)) {
-        cg = std::max(cg, ip_gram_host(ip, b.q, u).max_abs());
-        cg = std::max(cg, ip_gram_host(ip, b.p, v).max_abs());
-    }
+    for (size_t i = 1; i < gs.size(); ++i) cg = std::max(cg, gs[i].max_abs());
     st.stats.max_deflation_crossgram = std::max(st.stats.max_deflation_crossgram, cg);
     return dev;
 }
@@ -427,8 +432,10 @@ bool iterate_once(SolverState& ss, const LinearOperator& k, const LinearOperator
                 rhs_z = st.tmp.view();
             }
             auto phz = st.phases.scope(PH_CG);
-            DevCgOutcome cz = dev_cg(m, rhs_z, st.zg.view(), cfg.inner_cg_tol, cfg.inner_cg_max_iter, st.cg);
-            st.stats.cg_iterations += cz.sweeps;
+            DevCgOutcome cz = dev_cg(m, rhs_z, st.zg.view(), cfg.inner_cg_tol, cfg.inner_cg_max_iter, st.cg,
+                                     nullptr, false, true);
+            if (cz.sweeps >= 0) st.stats.cg_iterations += cz.sweeps;
+            else st.cg_deferred = true;
             // rhs_w = rw + lam B Z; W = CG(K, rhs_w)
             copy_block(st.rw.view(), st.tmp.view());
             if (ip.weighted()) {
@@ -440,8 +447,10 @@ bool iterate_once(SolverState& ss, const LinearOperator& k, const LinearOperator
                 lam_axpy(st.zg.view(), lamb, st.tmp.view());
             }
             auto phw = st.phases.scope(PH_CG);
-            DevCgOutcome cw = dev_cg(k, st.tmp.view(), st.wg.view(), cfg.inner_cg_tol, cfg.inner_cg_max_iter, st.cg);
-            st.stats.cg_iterations += cw.sweeps;
+            DevCgOutcome cw = dev_cg(k, st.tmp.view(), st.wg.view(), cfg.inner_cg_tol, cfg.inner_cg_max_iter, st.cg,
+                                     nullptr, false, true);
+            if (cw.sweeps >= 0) st.stats.cg_iterations += cw.sweeps;
+            else st.cg_deferred = true;
         }
         std::vector<DevBasis> bases = deflation_bases(st);
         bases.push_back({st.X(), st.Y()});
@@ -581,6 +590,7 @@ EigenResult assemble_result(DeviceState& st, const LinearOperator& k, const Line
     res.nevconv_history = st.nevconv_history;
     res.converged = converged;
     res.nev_converged = std::min(st.nev_conv, cfg.nev);
+    if (st.cg_deferred) st.stats.cg_iterations = st.cg.total_sweeps();
     res.stats = st.stats;
     DenseMatrix g = ip_gram_host(ip, rx.view(), ry.view());
     for (int64_t i = 0; i < g.rows(); ++i) g(i, i) -= 1.0;

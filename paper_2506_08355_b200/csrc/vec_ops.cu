@@ -209,8 +209,12 @@ __device__ __forceinline__ void cg_publish(const CgScalars& s, int ncols, bool r
     int c = 0;
     for (int j = 0; j < ncols; ++j) c += s.active[j];
     // an iteration counts when some column entered it active (unrolled graphs launch idle ones)
-    if (reset_loops) *s.loops = 0;
-    else if (*s.any_active > 0) *s.loops += 1;
+    if (reset_loops) {
+        *s.loops = 0;
+    } else if (*s.any_active > 0) {
+        *s.loops += 1;
+        if (s.total) *s.total += 1;
+    }
     *s.any_active = c;
     if (s.has_cond) cudaGraphSetConditional(s.cond, c > 0 ? 1u : 0u);
 }
@@ -560,7 +564,10 @@ __global__ void __launch_bounds__(kThreads) k_cg_update_fused(
     if (b == 0 && threadIdx.x == 0) {
         int c = 0;
         for (int j = 0; j < ncols; ++j) c += s_new[j];
-        if (*s.any_active > 0) *s.loops += 1;
+        if (*s.any_active > 0) {
+            *s.loops += 1;
+            if (s.total) *s.total += 1;
+        }
         *s.any_active = c;
         if (s.has_cond) cudaGraphSetConditional(s.cond, c > 0 ? 1u : 0u);
     }
