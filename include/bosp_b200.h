@@ -57,6 +57,14 @@ bosp_status bosp_op_dense(int64_t n, const double* a, bosp_op* out);
 /* from_csr (linear_operator.cpp:33-43; SparseMatrixCSR sparse_csr.hpp:12-28). */
 bosp_status bosp_op_csr(int64_t n, const int64_t* row_offsets, const int64_t* col_indices,
                         const double* values, bosp_op* out);
+/* read_matrix_market (matrix_market.hpp:10-13, matrix_market.cpp:26-91): coordinate real
+ * general|symmetric -> CSR (symmetric expanded, duplicates summed).  Call once with null
+ * arrays for rows/cols/nnz, then with rowptr (rows+1), colidx and vals (nnz) to copy them out.
+ * Malformed input -> BOSP_INGESTION_ERROR, message "<path>:<line>: <what>". */
+bosp_status bosp_read_matrix_market(const char* path, int64_t* rows, int64_t* cols, int64_t* nnz,
+                                    int64_t* rowptr, int64_t* colidx, double* vals);
+/* File -> device CSR operator (square matrices). */
+bosp_status bosp_op_matrix_market(const char* path, bosp_op* out);
 /* from_callback (linear_operator.cpp:45-47). */
 bosp_status bosp_op_callback(int64_t n, bosp_host_apply_fn fn, void* ctx, bosp_op* out);
 bosp_status bosp_op_device_callback(int64_t n, bosp_device_apply_fn fn, void* ctx, bosp_op* out);

@@ -217,6 +217,19 @@ def time_iterations(K, M, cfg: RefConfig, ns, k_iters: int, B=None):
                 converged=bool(conv.value), nev_conv=nevc.value)
 
 
+def read_matrix_market(path: str):
+    """The reference's read_matrix_market (matrix_market.cpp:26-91) -> (rows, cols, rowptr,
+    colidx, vals) as int64 / float64 arrays."""
+    rows, cols, nnz = C.c_int64(), C.c_int64(), C.c_int64()
+    bp = str(path).encode()
+    _check(lib().ref_read_matrix_market(bp, C.byref(rows), C.byref(cols), C.byref(nnz), None, None, None))
+    rp = np.zeros(rows.value + 1, dtype=np.int64)
+    ci = np.zeros(nnz.value, dtype=np.int64)
+    vv = np.zeros(nnz.value)
+    _check(lib().ref_read_matrix_market(bp, C.byref(rows), C.byref(cols), C.byref(nnz), _p(rp), _p(ci), _p(vv)))
+    return rows.value, cols.value, rp, ci, vv
+
+
 def fill_uniform(seed: int, count: int) -> np.ndarray:
     out = np.zeros(count)
     _check(lib().ref_fill_uniform(C.c_uint64(seed), C.c_int64(count), _p(out)))

@@ -27,6 +27,7 @@
 #include "bosp/core/errors.hpp"
 #include "bosp/core/kernels.hpp"
 #include "bosp/core/linear_operator.hpp"
+#include "bosp/core/matrix_market.hpp"
 #include "bosp/nullspace/nullspace.hpp"
 #include "bosp/projected/dense_kernels.hpp"
 #include "bosp/projected/projected_lrep.hpp"
@@ -129,6 +130,29 @@ const char* ref_last_error() { return g_err.c_str(); }
 
 void ref_set_threads(int t) { bosp::set_kernel_threads(t); }
 int ref_threads() { return bosp::kernel_threads(); }
+
+// read_matrix_market (matrix_market.cpp:26-91).  Two calls: sizes first (arrays null), then
+// the arrays; the parse of the first call is kept for the second.
+int ref_read_matrix_market(const char* path, int64_t* rows, int64_t* cols, int64_t* nnz, int64_t* rowptr,
+                           int64_t* colidx, double* vals) {
+    static std::string last_path;
+    static bosp::SparseMatrixCSR last;
+    return guarded([&] {
+        if (last_path != path || !rowptr) {
+            last = bosp::read_matrix_market(path);
+            last_path = path;
+        }
+        *rows = static_cast<int64_t>(last.rows);
+        *cols = static_cast<int64_t>(last.cols);
+        *nnz = static_cast<int64_t>(last.values.size());
+        if (rowptr)
+            for (size_t i = 0; i < last.row_offsets.size(); ++i) rowptr[i] = static_cast<int64_t>(last.row_offsets[i]);
+        if (colidx)
+            for (size_t i = 0; i < last.col_indices.size(); ++i) colidx[i] = static_cast<int64_t>(last.col_indices[i]);
+        if (vals) std::memcpy(vals, last.values.data(), sizeof(double) * last.values.size());
+        if (rowptr) last_path.clear();
+    });
+}
 
 }  // extern "C"
 

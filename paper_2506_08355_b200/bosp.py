@@ -81,6 +81,11 @@ class LinearOperator:
         return cls._make(lib().bosp_op_csr, C.c_int64(rp.shape[0] - 1), _p(rp), _p(ci), _p(vv))
 
     @classmethod
+    def from_matrix_market(cls, path):
+        """Matrix Market file (coordinate real general|symmetric) -> device CSR operator."""
+        return cls._make(lib().bosp_op_matrix_market, str(path).encode())
+
+    @classmethod
     def from_callback(cls, dim, fn):
         """fn(x) -> y on (n, m) float64 arrays (host ApplyFn, linear_operator.cpp:45-47)."""
         def tramp(ctx, xp, yp, n, m):
@@ -254,6 +259,22 @@ def solve(K: LinearOperator, M: LinearOperator, ip: InnerProduct | None, cfg: Bo
     return EigenResult(lam[:k], None if x is None else x[:, :k], None if y is None else y[:, :k],
                        int(st.iterations), res[:k], hist[:min(hrows.value, history_cap)],
                        bool(st.converged), int(st.nev_converged), stats)
+
+
+def read_matrix_market(path):
+    """read_matrix_market (matrix_market.cpp:26-91) -> problems.Csr (square) or the raw
+    (rows, cols, rowptr, colidx, vals) tuple for rectangular files."""
+    from .problems import Csr
+    rows, cols, nnz = C.c_int64(), C.c_int64(), C.c_int64()
+    bp = str(path).encode()
+    check(lib().bosp_read_matrix_market(bp, C.byref(rows), C.byref(cols), C.byref(nnz), None, None, None))
+    rp = np.zeros(rows.value + 1, dtype=np.int64)
+    ci = np.zeros(nnz.value, dtype=np.int64)
+    vv = np.zeros(nnz.value)
+    check(lib().bosp_read_matrix_market(bp, C.byref(rows), C.byref(cols), C.byref(nnz), _p(rp), _p(ci), _p(vv)))
+    if rows.value == cols.value:
+        return Csr(rows.value, rp, ci, vv)
+    return rows.value, cols.value, rp, ci, vv
 
 
 # ---- row-partitioned ranks ---------------------------------------------------------------

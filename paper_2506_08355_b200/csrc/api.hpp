@@ -11,6 +11,7 @@
 #include <memory>
 #include <optional>
 #include <random>
+#include <string>
 #include <vector>
 
 #include "common.hpp"
@@ -96,6 +97,9 @@ struct StencilSpec {
     // s_global = 0: unpartitioned.
     int64_t s0 = 0, s_global = 0, nz_global = 0;
 };
+
+// read_matrix_market (matrix_market.hpp:10-13): coordinate real general|symmetric.
+SparseMatrixCSR read_matrix_market(const std::string& path);
 
 class OperatorImpl;
 

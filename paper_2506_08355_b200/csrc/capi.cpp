@@ -318,6 +318,34 @@ bosp_status bosp_solve(bosp_op K, bosp_op M, bosp_op B, const bosp_config* c, in
     });
 }
 
+bosp_status bosp_read_matrix_market(const char* path, int64_t* rows, int64_t* cols, int64_t* nnz, int64_t* rowptr,
+                                    int64_t* colidx, double* vals) {
+    thread_local std::string last_path;
+    thread_local bosp::SparseMatrixCSR last;
+    return guarded([&] {
+        bosp::require(path != nullptr, "read_matrix_market: null path");
+        if (last_path != path || !rowptr) {  // the size call parses; the copy call reuses it
+            last = bosp::read_matrix_market(path);
+            last_path = path;
+        }
+        *rows = last.rows;
+        *cols = last.cols;
+        *nnz = last.nnz();
+        if (rowptr) std::memcpy(rowptr, last.row_offsets.data(), sizeof(int64_t) * last.row_offsets.size());
+        if (colidx) std::memcpy(colidx, last.col_indices.data(), sizeof(int64_t) * last.col_indices.size());
+        if (vals) std::memcpy(vals, last.values.data(), sizeof(double) * last.values.size());
+        if (rowptr) last_path.clear();
+    });
+}
+
+bosp_status bosp_op_matrix_market(const char* path, bosp_op* out) {
+    return guarded([&] {
+        bosp::require(path != nullptr, "op_matrix_market: null path");
+        const bosp::SparseMatrixCSR a = bosp::read_matrix_market(path);
+        *out = wrap(bosp::LinearOperator::from_csr(a));
+    });
+}
+
 bosp_status bosp_op_csr_rows(int64_t n_global, int64_t row0, int64_t n_local, const int64_t* rp, const int64_t* ci,
                              const double* vv, bosp_op* out) {
     return guarded([&] { *out = wrap(bosp::LinearOperator::from_csr_rows(n_global, row0, n_local, rp, ci, vv)); });
