@@ -14,6 +14,7 @@
 // mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4).  Shared layouts are padded (+4 doubles) so the
 // fragment loads of a half-warp hit 16 distinct 8-byte bank pairs.
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 
 #include "dense_ops.hpp"
@@ -284,6 +285,133 @@ void launch_gram(const GramJob* jobs, int njobs, int64_t n) {
         const int64_t total = static_cast<int64_t>(max_tiles) * BM * BN;
         dim3 grid(static_cast<unsigned>((total + kRedElems - 1) / kRedElems), 1, njobs);
         k_gram_reduce<BM, BN><<<grid, kRedElems * kRedGroups, 0, rt.stream()>>>(prm);
+        BOSP_LAUNCH_CHECK();
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// Skinny Gram (a, b <= 32): DMMA fragments straight from global memory
+// ------------------------------------------------------------------------------------------
+// For G = A^T B the n rows are the MMA's k dimension: the A fragment of m8n8k4 (8 x 4, row i =
+// column m0+i of A, entry kk = row k0+kk) is one double per lane, A[k0 + (lane&3), m0 + lane/4]
+// -- a warp reads 8 columns x 4 consecutive rows, eight full 32-byte sectors.  No shared-memory
+// staging and tiles padded to 8 (not 32) columns: a 20 x 20 Gram issues 9 DMMAs per 4 rows
+// instead of 16.  Each warp walks its own 4-row steps; warps fold through shared memory in a
+// fixed order, blocks through the split-K partial buffer (k_gram_reduce, 32 x 32 layout).
+constexpr int kRegWarps = 8;
+#ifndef BOSP_GRAM_UNROLL
+#define BOSP_GRAM_UNROLL 4
+#endif
+constexpr int kGramUnroll = BOSP_GRAM_UNROLL;
+
+template <int MT, int NTL>
+__global__ void __launch_bounds__(kRegWarps * 32) k_gram_regs(GramParams prm) {
+    extern __shared__ __align__(16) double red[];  // [warp][MT*8 x NTL*8]
+    constexpr int TM = MT * 8, TN = NTL * 8;
+    const int jb = blockIdx.y;
+    const GramJob& job = prm.job[jb];
+    const int acols = job.a.cols(), bcols = job.b.cols();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int gid = lane >> 2, tig = lane & 3;
+    const double* pa[MT];
+    const double* pb[NTL];
+#pragma unroll
+    for (int i = 0; i < MT; ++i) {
+        const int c = i * 8 + gid;
+        pa[i] = c < acols ? colptr(job.a, c) : nullptr;
+    }
+#pragma unroll
+    for (int j = 0; j < NTL; ++j) {
+        const int c = j * 8 + gid;
+        pb[j] = c < bcols ? colptr(job.b, c) : nullptr;
+    }
+    double acc[MT][NTL][2];
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NTL; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    const int64_t kb = static_cast<int64_t>(blockIdx.x) * prm.chunk;
+    const int64_t ke = min(prm.n, kb + prm.chunk);
+#pragma unroll (kGramUnroll)
+    for (int64_t k0 = kb + 4 * warp; k0 < ke; k0 += 4 * kRegWarps) {
+        const int64_t r = k0 + tig;
+        const bool vr = r < ke;
+        double af[MT], bf[NTL];
+#pragma unroll
+        for (int i = 0; i < MT; ++i) af[i] = (pa[i] && vr) ? __ldg(pa[i] + r) : 0.0;
+#pragma unroll
+        for (int j = 0; j < NTL; ++j) bf[j] = (pb[j] && vr) ? __ldg(pb[j] + r) : 0.0;
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+#pragma unroll
+            for (int j = 0; j < NTL; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    double* mine = red + warp * (TM * TN);
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NTL; ++j) {
+            const int m = i * 8 + gid, nn = j * 8 + 2 * tig;
+            mine[m + nn * TM] = acc[i][j][0];
+            mine[m + (nn + 1) * TM] = acc[i][j][1];
+        }
+    __syncthreads();
+    double* part = prm.partial + jb * prm.job_stride + static_cast<int64_t>(blockIdx.x) * 1024;
+    for (int e = threadIdx.x; e < TM * TN; e += kRegWarps * 32) {
+        double v = 0.0;
+#pragma unroll
+        for (int w = 0; w < kRegWarps; ++w) v += red[w * (TM * TN) + e];
+        const int m = e % TM, nn = e / TM;
+        if (prm.splits == 1) {
+            if (m < acols && nn < bcols) job.g[m + static_cast<int64_t>(nn) * job.ldg] = v;
+        } else {
+            part[m + nn * 32] = v;  // k_gram_reduce<32, 32> layout (one tile)
+        }
+    }
+}
+
+template <int MT, int NTL>
+void launch_gram_regs(const GramJob* jobs, int njobs, int64_t n) {
+    Runtime& rt = Runtime::get();
+    GramParams prm{};
+    for (int j = 0; j < njobs; ++j) {
+        prm.job[j] = jobs[j];
+        prm.tiles_n[j] = 1;
+        prm.tiles[j] = 1;
+    }
+    prm.n = n;
+    constexpr int64_t kStep = 4 * kRegWarps;  // rows per block step
+    const int64_t steps = (n + kStep - 1) / kStep;
+    // one full wave (2 resident blocks per SM at ~100 registers); 3-8 waves measured 30-100 %
+    // slower on config 2's 20-column Grams (more partials, tail)
+    static const int64_t waves = std::getenv("BOSP_GRAM_WAVES") ? std::atoi(std::getenv("BOSP_GRAM_WAVES")) : 2;
+    int splits = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(
+        (waves * rt.sm_count() + njobs - 1) / njobs, steps / 8)));  // >= 8 steps of work per block
+    const int64_t per = (steps + splits - 1) / splits;
+    prm.chunk = per * kStep;
+    splits = static_cast<int>((n + prm.chunk - 1) / prm.chunk);
+    prm.splits = std::max(1, splits);
+    prm.job_stride = static_cast<int64_t>(prm.splits) * 1024;
+    prm.partial = rt.scratch(static_cast<size_t>(prm.job_stride) * njobs);
+    constexpr size_t smem = sizeof(double) * kRegWarps * MT * 8 * NTL * 8;
+    static unsigned attr_mask = 0;
+    if (rt.first_use(attr_mask))
+        BOSP_CUDA(cudaFuncSetAttribute(k_gram_regs<MT, NTL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem)));
+    double flops = 0.0, bytes = 0.0;
+    for (int j = 0; j < njobs; ++j) {
+        flops += 2.0 * n * jobs[j].a.cols() * jobs[j].b.cols();
+        bytes += 8.0 * n * (jobs[j].a.cols() + jobs[j].b.cols());
+    }
+    {
+        LaunchScope ls("gram", bytes, flops);
+        k_gram_regs<MT, NTL><<<dim3(prm.splits, njobs), kRegWarps * 32, smem, rt.stream()>>>(prm);
+        BOSP_LAUNCH_CHECK();
+    }
+    if (prm.splits > 1) {
+        LaunchScope ls("gram_reduce");
+        dim3 grid(static_cast<unsigned>(1024 / kRedElems), 1, njobs);
+        k_gram_reduce<32, 32><<<grid, kRedElems * kRedGroups, 0, rt.stream()>>>(prm);
         BOSP_LAUNCH_CHECK();
     }
 }
@@ -616,6 +744,19 @@ void gram(const GramJob* jobs, int njobs, int64_t n) {
                 BOSP_CUDA(cudaMemsetAsync(jobs[j].g + c * jobs[j].ldg, 0,
                                           sizeof(double) * jobs[j].a.cols(), Runtime::get().stream()));
         return;
+    }
+    static const bool regs = !std::getenv("BOSP_GRAM_SMEM");
+    if (amax <= 32 && bmax <= 32 && regs) {
+        const int mt = (amax + 7) / 8, nt = (bmax + 7) / 8;
+        switch (mt * 4 + nt) {
+#define BOSP_G(M, N) case M * 4 + N: return launch_gram_regs<M, N>(jobs, njobs, n);
+            BOSP_G(1, 1) BOSP_G(1, 2) BOSP_G(1, 3) BOSP_G(1, 4)
+            BOSP_G(2, 1) BOSP_G(2, 2) BOSP_G(2, 3) BOSP_G(2, 4)
+            BOSP_G(3, 1) BOSP_G(3, 2) BOSP_G(3, 3) BOSP_G(3, 4)
+            BOSP_G(4, 1) BOSP_G(4, 2) BOSP_G(4, 3) BOSP_G(4, 4)
+#undef BOSP_G
+            default: break;
+        }
     }
     if (amax <= 32 && bmax <= 32)
         launch_gram<32, 32, 2, 2>(jobs, njobs, n);
