@@ -173,14 +173,32 @@ def run_b200(args, world, rank, local, dist):
     prob = P.config2(64)
     cfg = bosp.BospConfig(**prob.cfg)
     partitioned = world > 1 and args.partition == "rows"
+    partition_error = None
     if partitioned:
         # one process per GPU, rows of every n-length block on this rank; NCCL communicator
-        # inside libbosp_b200.so (torch.distributed only carries the unique id + timings)
-        uid = D.broadcast_uid()
-        row0, nl = D.attach(prob.K, uid, world, rank)
-        ns = D.local_nullspace(prob.x0, prob.y0, row0, nl)
-        K, M = bosp.local_operator(prob.K, world, rank), bosp.local_operator(prob.M, world, rank)
-    else:
+        # inside libbosp_b200.so (torch.distributed only carries the unique id + timings).
+        # The ranks agree on success after one partitioned solve; if any rank failed, every
+        # rank falls back to replicas and the line records why.
+        ok = 1
+        try:
+            uid = D.broadcast_uid()
+            row0, nl = D.attach(prob.K, uid, world, rank)
+            ns = D.local_nullspace(prob.x0, prob.y0, row0, nl)
+            K, M = bosp.local_operator(prob.K, world, rank), bosp.local_operator(prob.M, world, rank)
+            bosp.solve(K, M, None, cfg, ns, want_vectors=True)
+        except Exception as e:  # noqa: BLE001 -- reported in the JSON line
+            ok, partition_error = 0, f"{type(e).__name__}: {e}"[:300]
+        import torch
+        flag = torch.tensor([ok], dtype=torch.int32)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag.item()) == 0:
+            try:
+                bosp.comm_free()
+            except Exception:
+                pass
+            partitioned = False
+            partition_error = partition_error or "another rank failed the partitioned setup"
+    if not partitioned:
         row0, nl = 0, prob.n
         ns = bosp.GeneralizedNullspace(prob.x0, prob.y0)
         K, M = bosp.operators_for(prob)   # resident in HBM before the timed region
@@ -310,6 +328,7 @@ def run_b200(args, world, rank, local, dist):
                        "tol": 1e-8,
                        "parallelism": (f"row partition x{world} (NCCL allreduce + halo)" if partitioned
                                        else "replicas" if world > 1 else "single GPU"),
+                       **({"partition_error": partition_error} if partition_error else {}),
                        "l2": "flushed between steps (512 MB memset)", "device": name, "sms": sms},
             "roofline": roof,
             "cpu_baseline": cpu,
