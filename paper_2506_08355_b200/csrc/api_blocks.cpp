@@ -3,6 +3,8 @@
 // parity tests and by callers that want single building blocks.
 #include <cmath>
 
+#include <cstdlib>
+
 #include "api.hpp"
 #include "dev_algos.hpp"
 #include "operators.hpp"
@@ -62,7 +64,12 @@ BiorthOutcome biorth_common(const BlockVectors& x, const BlockVectors& y, const 
     require(x.dim() == y.dim() && x.cols() == y.cols(), "biorth: X and Y must have equal shape");
     DBlock dx = up(x), dy = up(y);
     DBlock p(x.dim(), std::max<int64_t>(x.cols(), 1)), q(x.dim(), std::max<int64_t>(x.cols(), 1));
-    DevBiorthOutcome o = dev_mgs_biorth(dx.view(), dy.view(), p.view(), q.view(), ip, drop_tol, classical);
+    // small blocks: the reference's column-sequential recurrence itself (exact order, robust on
+    // ill-conditioned input); wide blocks: the level-3 coefficient-space path of the solver
+    static const int64_t seq_max = std::getenv("BOSP_BIORTH_SEQ_MAX") ? std::atoll(std::getenv("BOSP_BIORTH_SEQ_MAX")) : 64;
+    DevBiorthOutcome o = x.cols() <= seq_max
+        ? dev_gs_biorth_seq(dx.view(), dy.view(), p.view(), q.view(), ip, drop_tol, classical)
+        : dev_mgs_biorth(dx.view(), dy.view(), p.view(), q.view(), ip, drop_tol, classical);
     BiorthOutcome out;
     out.basis.p = down(p.cols(0, o.kept));
     out.basis.q = down(q.cols(0, o.kept));

@@ -56,6 +56,8 @@ void lam_axmy(const DMat& a, const DMat& b, const double* lam_dev, const DMat& o
 void lam_axpy(const DMat& x, const double* lam_dev, const DMat& y);
 // y = x + sigma * y  (shifted operator epilogue) / y = alpha * x / y = d .* x
 void axpby(double a, const DMat& x, double b, const DMat& y);
+// y -= s[0] * x with s a device scalar (one column)
+void sub_scaled(const DMat& x, const double* s_dev, const DMat& y);
 void diag_scale(const double* d_dev, const DMat& x, const DMat& y);
 // t = a^T (square or rectangular; t.rows == a.cols, t.cols == a.rows)
 void transpose(const DMat& a, const DMat& t);

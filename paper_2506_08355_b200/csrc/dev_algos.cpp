@@ -230,6 +230,86 @@ DevBiorthOutcome dev_mgs_biorth(const DMat& x, const DMat& y, const DMat& p, con
     return out;
 }
 
+namespace {
+// ip.dot(a, b) = a^T B b into a device scalar (one column each)
+void ip_dot_dev(const InnerProduct& ip, const DMat& a, const DMat& b, DBlock& wb, double* out) {
+    if (ip.weighted()) {
+        ip.weight()->apply_device(b, wb.view());
+        col_dots(a, wb.view(), out);
+    } else {
+        col_dots(a, b, out);
+    }
+}
+}  // namespace
+
+DevBiorthOutcome dev_gs_biorth_seq(const DMat& x, const DMat& y, const DMat& p, const DMat& q,
+                                   const InnerProduct& ip, double drop_tol, bool classical) {
+    require(x.rows == y.rows && x.cols == y.cols, "biorth: X and Y must have equal shape");
+    DevBiorthOutcome out;
+    const int64_t n = x.rows, m = x.cols;
+    if (m == 0) return out;
+    Runtime& rt = Runtime::get();
+    DBlock pl(n, 1), ql(n, 1), wb(n, 1), sc(8, 1);
+    double* r = sc.data();
+    double* s = sc.data() + 1;
+    double h[3];
+    auto norms_eta = [&](const DMat& a, const DMat& b) {  // (a^T B a, b^T B b, a^T B b)
+        ip_dot_dev(ip, a, a, wb, sc.data() + 2);
+        ip_dot_dev(ip, b, b, wb, sc.data() + 3);
+        ip_dot_dev(ip, a, b, wb, sc.data() + 4);
+        BOSP_CUDA(cudaMemcpyAsync(h, sc.data() + 2, sizeof(h), cudaMemcpyDeviceToHost, rt.stream()));
+        rt.sync();
+    };
+    int64_t kept = 0;
+    for (int64_t l = 0; l < m; ++l) {
+        const DMat xl = x.cols_range(l, 1), yl = y.cols_range(l, 1);
+        copy_block(xl, pl.view());
+        copy_block(yl, ql.view());
+        for (int64_t kk = 0; kk < kept; ++kk) {
+            const DMat pj = p.cols_range(kk, 1), qj = q.cols_range(kk, 1);
+            ip_dot_dev(ip, qj, classical ? xl : pl.view(), wb, r);
+            sub_scaled(pj, r, pl.view());
+            ip_dot_dev(ip, pj, classical ? yl : ql.view(), wb, s);
+            sub_scaled(qj, s, ql.view());
+        }
+        norms_eta(pl.view(), ql.view());
+        const double pn = std::sqrt(h[0]), qn = std::sqrt(h[1]), eta = h[2];
+        if (pn == 0.0 || qn == 0.0 || std::fabs(eta) < drop_tol * pn * qn) {
+            out.dropped_columns.push_back(l);
+            continue;
+        }
+        const double scale = 1.0 / std::sqrt(std::fabs(eta)), sgn = eta < 0.0 ? -1.0 : 1.0;
+        axpby(sgn * scale, pl.view(), 0.0, p.cols_range(kept, 1));
+        axpby(scale, ql.view(), 0.0, q.cols_range(kept, 1));
+        out.kept_columns.push_back(l);
+        ++kept;
+    }
+    out.kept = kept;
+    if (classical || kept <= 1) return out;
+    const DMat pk = p.cols_range(0, kept), qk = q.cols_range(0, kept);
+    if (!(biorth_loss(ip_gram_host(ip, pk, qk)) > 1e-10)) return out;
+    // rebiorth_pass (biorth.cpp:73-99)
+    out.second_pass = true;
+    for (int64_t l = 0; l < kept; ++l) {
+        copy_block(p.cols_range(l, 1), pl.view());
+        copy_block(q.cols_range(l, 1), ql.view());
+        for (int64_t j = 0; j < l; ++j) {
+            const DMat pj = p.cols_range(j, 1), qj = q.cols_range(j, 1);
+            ip_dot_dev(ip, qj, pl.view(), wb, r);
+            sub_scaled(pj, r, pl.view());
+            ip_dot_dev(ip, pj, ql.view(), wb, s);
+            sub_scaled(qj, s, ql.view());
+        }
+        norms_eta(pl.view(), ql.view());
+        const double eta = h[2];
+        if (eta == 0.0) continue;
+        const double scale = 1.0 / std::sqrt(std::fabs(eta)), sgn = eta < 0.0 ? -1.0 : 1.0;
+        axpby(sgn * scale, pl.view(), 0.0, p.cols_range(l, 1));
+        axpby(scale, ql.view(), 0.0, q.cols_range(l, 1));
+    }
+    return out;
+}
+
 double dev_biorth_residual(const DMat& p, const DMat& q, const InnerProduct& ip) {
     require(p.rows == q.rows && p.cols == q.cols, "biorth_residual: shape mismatch");
     if (p.cols == 0) return 0.0;

@@ -37,6 +37,11 @@ struct DevBiorthOutcome {
 };
 // MGS-Biorth of (X, Y) into (P, Q) (first `kept` columns written; P/Q need >= m columns and
 // must not alias X/Y).  Semantics of mgs_biorth (biorth.cpp:102-109); classical -> cgs_biorth.
+// The reference's column-sequential gs_biorth (biorth.cpp:19-69) in n-space, pair by pair in
+// its exact order, plus the mgs second pass (:73-107): the API-level mgs/cgs_biorth for small m,
+// where ill-conditioned inputs (Table 1) need the n-space recurrence, not Grams.
+DevBiorthOutcome dev_gs_biorth_seq(const DMat& x, const DMat& y, const DMat& p, const DMat& q,
+                                   const InnerProduct& ip, double drop_tol, bool classical);
 DevBiorthOutcome dev_mgs_biorth(const DMat& x, const DMat& y, const DMat& p, const DMat& q,
                                 const InnerProduct& ip, double drop_tol = 1e-12,
                                 bool classical = false);

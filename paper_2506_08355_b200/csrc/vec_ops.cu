@@ -417,6 +417,16 @@ struct LamAxpyF {
         st2(y + i + j * ly, v.x + l * u.x, v.y + l * u.y);
     }
 };
+struct SubScaledF {  // y -= s[0] x (device scalar)
+    const double* x; double* y; int64_t lx, ly; const double* s;
+    __device__ bool skip(int) const { return false; }
+    __device__ void operator()(int64_t i, int j) const { y[i + j * ly] -= s[0] * x[i + j * lx]; }
+    __device__ void pair(int64_t i, int j) const {
+        const double a = s[0];
+        const double2 u = ldg2(x + i + j * lx), v = ld2(y + i + j * ly);
+        st2(y + i + j * ly, v.x - a * u.x, v.y - a * u.y);
+    }
+};
 struct AxpbyF {
     double a, b; const double* x; double* y; int64_t lx, ly;
     __device__ bool skip(int) const { return false; }
@@ -652,6 +662,11 @@ void lam_axmy(const DMat& a, const DMat& b, const double* lam, const DMat& out) 
 
 void lam_axpy(const DMat& x, const double* lam, const DMat& y) {
     LamAxpyF f{x.p, y.p, x.ld, y.ld, lam};
+    launch_cols("elementwise", x.rows, static_cast<int>(x.cols), f, 24.0 * x.rows * x.cols);
+}
+
+void sub_scaled(const DMat& x, const double* s_dev, const DMat& y) {
+    SubScaledF f{x.p, y.p, x.ld, y.ld, s_dev};
     launch_cols("elementwise", x.rows, static_cast<int>(x.cols), f, 24.0 * x.rows * x.cols);
 }
 
