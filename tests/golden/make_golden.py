@@ -99,7 +99,16 @@ def solve_record(prob_k, prob_m, cfg, ns, n, label):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true", help="also run config 2 at 64^3 (~6 min)")
+    ap.add_argument("--c3", action="store_true", help="also run the config-3 family at 20^3, nev 100 (~90 s)")
+    ap.add_argument("--only-c3", action="store_true", help="only (re)run the config-3 family entry")
     args = ap.parse_args()
+    if args.only_c3:
+        path = os.path.join(OUT, "golden_solves.json")
+        solves = json.load(open(path))
+        p = P.config3(20)
+        solves["config3_m20"] = solve_record(p.oracle_spec("K"), p.oracle_spec("M"), ref.RefConfig(**p.cfg), (p.x0, p.y0), p.n, "config3 m=20 nev=100")
+        json.dump(solves, open(path, "w"), indent=1)
+        return
     ref.set_threads(0)
     np.savez_compressed(os.path.join(OUT, "golden_small.npz"), **small_fixtures())
 
@@ -128,6 +137,9 @@ def main():
     solves["config5_m32"] = solve_record(p.oracle_spec("K"), p.oracle_spec("M"), ref.RefConfig(nev=40, nb=8, tol=1e-8), (p.x0, p.y0), p.n, "config5 m=32 nev=40 nb=8")
     p = P.config1()
     solves["config1"] = solve_record(p.oracle_spec("K"), p.oracle_spec("M"), ref.RefConfig(**p.cfg), (p.x0, p.y0), p.n, "config1")
+    if args.c3:
+        p = P.config3(20)
+        solves["config3_m20"] = solve_record(p.oracle_spec("K"), p.oracle_spec("M"), ref.RefConfig(**p.cfg), (p.x0, p.y0), p.n, "config3 m=20 nev=100")
     if args.big:
         p = P.config2(64)
         solves["config2"] = solve_record(p.oracle_spec("K"), p.oracle_spec("M"), ref.RefConfig(**p.cfg), (p.x0, p.y0), p.n, "config2 64^3")
