@@ -174,3 +174,13 @@ def test_config_errors():
         bosp.solve(t, t, None, bosp.BospConfig(nev=3, s=1))
     with pytest.raises(bosp.ContractViolation):
         bosp.solve(t, t, None, bosp.BospConfig(nev=30))  # nev > n
+
+
+def test_config3_family_small(golden_solves):
+    """Config-3 family (7-point stencils, nev 100, nb 64, moving, d = 320) at 20^3 against the
+    reference's own run (tests/golden: 23 iterations, 88 s on the CPU)."""
+    p = P.config3(20)
+    K, M = bosp.operators_for(p)
+    res = bosp.solve(K, M, None, bosp.BospConfig(**p.cfg), bosp.GeneralizedNullspace(p.x0, p.y0))
+    check_result(res, golden_solves["config3_m20"]["lambdas"], 1e-8, 100)
+    assert res.stats["max_width_u"] <= (3 + 2) * 64
