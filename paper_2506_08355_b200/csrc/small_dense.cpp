@@ -1,6 +1,8 @@
 // Host small dense algebra for the projected LREP and the coefficient-space MGS-Biorth.
 #include "small_dense.hpp"
 
+#include <immintrin.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -127,37 +129,64 @@ std::optional<DenseMatrix> cholesky_lower(const DenseMatrix& a) {
 
 namespace {
 
+// AVX2 helpers for the rotation kernels (x86-64-v3 build).
+inline double dot_avx(const double* a, const double* b, int64_t m) {
+    __m256d s0 = _mm256_setzero_pd(), s1 = _mm256_setzero_pd();
+    int64_t i = 0;
+    for (; i + 8 <= m; i += 8) {
+        s0 = _mm256_fmadd_pd(_mm256_loadu_pd(a + i), _mm256_loadu_pd(b + i), s0);
+        s1 = _mm256_fmadd_pd(_mm256_loadu_pd(a + i + 4), _mm256_loadu_pd(b + i + 4), s1);
+    }
+    for (; i + 4 <= m; i += 4) s0 = _mm256_fmadd_pd(_mm256_loadu_pd(a + i), _mm256_loadu_pd(b + i), s0);
+    s0 = _mm256_add_pd(s0, s1);
+    alignas(32) double t[4];
+    _mm256_store_pd(t, s0);
+    double r = (t[0] + t[1]) + (t[2] + t[3]);
+    for (; i < m; ++i) r += a[i] * b[i];
+    return r;
+}
+
+inline void rotate_avx(double* x, double* y, int64_t m, double c, double s) {
+    const __m256d vc = _mm256_set1_pd(c), vs = _mm256_set1_pd(s);
+    int64_t i = 0;
+    for (; i + 4 <= m; i += 4) {
+        const __m256d a = _mm256_loadu_pd(x + i), b = _mm256_loadu_pd(y + i);
+        _mm256_storeu_pd(x + i, _mm256_fmsub_pd(vc, a, _mm256_mul_pd(vs, b)));
+        _mm256_storeu_pd(y + i, _mm256_fmadd_pd(vs, a, _mm256_mul_pd(vc, b)));
+    }
+    for (; i < m; ++i) {
+        const double a = x[i], b = y[i];
+        x[i] = c * a - s * b;
+        y[i] = s * a + c * b;
+    }
+}
+
 // Rotate columns p, q of a (m rows) and v (k rows) if they are not yet orthogonal; returns
-// whether a rotation happened.  Formula of dense_kernels.cpp:47-79.
-inline bool jacobi_pair(DenseMatrix& a, DenseMatrix& v, int64_t p, int64_t q) {
+// whether a rotation happened.  Rotation formula and test of dense_kernels.cpp:47-79.  The
+// squared column norms are carried in `nrm` (recomputed at every sweep start): after the
+// rotation that annihilates gamma they are exactly alpha - t*gamma and beta + t*gamma, so a pair
+// costs one dot product instead of three.
+inline bool jacobi_pair(DenseMatrix& a, DenseMatrix& v, double* nrm, int64_t p, int64_t q) {
     const int64_t m = a.rows(), k = v.rows();
     double* ap = a.col(p);
     double* aq = a.col(q);
-    double alpha = 0.0, beta = 0.0, gamma = 0.0;
-    for (int64_t i = 0; i < m; ++i) {
-        alpha += ap[i] * ap[i];
-        beta += aq[i] * aq[i];
-        gamma += ap[i] * aq[i];
-    }
+    const double alpha = nrm[p], beta = nrm[q];
     if (alpha == 0.0 || beta == 0.0) return false;
+    const double gamma = dot_avx(ap, aq, m);
     if (std::fabs(gamma) <= 1e-15 * std::sqrt(alpha * beta)) return false;
     const double zeta = (beta - alpha) / (2.0 * gamma);
     const double t = ((zeta >= 0.0) ? 1.0 : -1.0) / (std::fabs(zeta) + std::sqrt(1.0 + zeta * zeta));
     const double c = 1.0 / std::sqrt(1.0 + t * t);
     const double s = c * t;
-    for (int64_t i = 0; i < m; ++i) {
-        const double x = ap[i], y = aq[i];
-        ap[i] = c * x - s * y;
-        aq[i] = s * x + c * y;
-    }
-    double* vp = v.col(p);
-    double* vq = v.col(q);
-    for (int64_t i = 0; i < k; ++i) {
-        const double x = vp[i], y = vq[i];
-        vp[i] = c * x - s * y;
-        vq[i] = s * x + c * y;
-    }
+    rotate_avx(ap, aq, m, c, s);
+    rotate_avx(v.col(p), v.col(q), k, c, s);
+    nrm[p] = alpha - t * gamma;
+    nrm[q] = beta + t * gamma;
     return true;
+}
+
+void column_norms(const DenseMatrix& a, double* nrm) {
+    for (int64_t j = 0; j < a.cols(); ++j) nrm[j] = dot_avx(a.col(j), a.col(j), a.rows());
 }
 
 }  // namespace
@@ -171,11 +200,13 @@ JacobiSvdResult jacobi_svd(DenseMatrix a, int64_t max_sweeps) {
     int64_t sweep = 0;
     if (k < 96) {
         // cyclic-by-row order, exactly the reference's sweep
+        std::vector<double> nrm(static_cast<size_t>(k));
         while (rotated && sweep < max_sweeps) {
             rotated = false;
             ++sweep;
+            column_norms(a, nrm.data());
             for (int64_t p = 0; p + 1 < k; ++p)
-                for (int64_t q = p + 1; q < k; ++q) rotated |= jacobi_pair(a, res.v, p, q);
+                for (int64_t q = p + 1; q < k; ++q) rotated |= jacobi_pair(a, res.v, nrm.data(), p, q);
         }
     } else {
         // round-robin tournament: each round pairs disjoint columns, rotated in parallel
@@ -184,9 +215,11 @@ JacobiSvdResult jacobi_svd(DenseMatrix a, int64_t max_sweeps) {
         std::iota(pos.begin(), pos.end(), 0);
         // one parallel region per sweep; rounds are separated by barriers (the pair schedule
         // of round r+1 depends only on r, so every thread can advance its own copy of `pos`)
+        std::vector<double> nrm(static_cast<size_t>(k));
         while (rotated && sweep < max_sweeps) {
             ++sweep;
             int any = 0;
+            column_norms(a, nrm.data());
 #pragma omp parallel reduction(| : any)
             {
                 std::vector<int64_t> lp(pos);
@@ -196,7 +229,7 @@ JacobiSvdResult jacobi_svd(DenseMatrix a, int64_t max_sweeps) {
                         int64_t p = lp[i], q = lp[kk - 1 - i];
                         if (p >= k || q >= k) continue;
                         if (p > q) std::swap(p, q);
-                        any |= jacobi_pair(a, res.v, p, q) ? 1 : 0;
+                        any |= jacobi_pair(a, res.v, nrm.data(), p, q) ? 1 : 0;
                     }  // implicit barrier
                     const int64_t last = lp[kk - 1];
                     for (int64_t i = kk - 1; i > 1; --i) lp[i] = lp[i - 1];
