@@ -70,65 +70,7 @@ bool DenseMatrix::is_symmetric(double tol_rel) const {
     return true;
 }
 
-DenseMatrix matmul(const DenseMatrix& a, const DenseMatrix& b) {
-    require(a.cols() == b.rows(), "matmul: inner dimensions disagree");
-    DenseMatrix c(a.rows(), b.cols());
-    const int64_t m = a.rows(), k = a.cols();
-    for (int64_t j = 0; j < b.cols(); ++j) {
-        double* cj = c.col(j);
-        for (int64_t p = 0; p < k; ++p) {
-            const double bpj = b(p, j);
-            if (bpj == 0.0) continue;
-            const double* ap = a.col(p);
-            for (int64_t i = 0; i < m; ++i) cj[i] += ap[i] * bpj;
-        }
-    }
-    return c;
-}
-
-DenseMatrix matmul_tn(const DenseMatrix& a, const DenseMatrix& b) {
-    require(a.rows() == b.rows(), "matmul_tn: row dimensions disagree");
-    DenseMatrix c(a.cols(), b.cols());
-    const int64_t m = a.rows();
-    for (int64_t j = 0; j < b.cols(); ++j) {
-        const double* bj = b.col(j);
-        for (int64_t i = 0; i < a.cols(); ++i) {
-            const double* ai = a.col(i);
-            double s = 0.0;
-            for (int64_t r = 0; r < m; ++r) s += ai[r] * bj[r];
-            c(i, j) = s;
-        }
-    }
-    return c;
-}
-
-std::optional<DenseMatrix> cholesky_lower(const DenseMatrix& a) {
-    if (a.rows() != a.cols()) return std::nullopt;
-    const int64_t n = a.rows();
-    DenseMatrix l(n, n);
-    // Left-looking, column-oriented: column j = (a(:, j) - sum_k l(j,k) l(:, k)) / l_jj with the
-    // k-sum accumulated in the reference's order (dense_kernels.cpp:11-28) but as unit-stride
-    // axpys; the diagonal pivot test (d > 0, finite) is the contract.
-    std::vector<double> s(static_cast<size_t>(n));
-    for (int64_t j = 0; j < n; ++j) {
-        for (int64_t i = j; i < n; ++i) s[i] = a(i, j);
-        for (int64_t k = 0; k < j; ++k) {
-            const double ljk = l(j, k);
-            const double* lk = l.col(k);
-            for (int64_t i = j; i < n; ++i) s[i] -= lk[i] * ljk;
-        }
-        const double d = s[j];
-        if (!(d > 0.0) || !std::isfinite(d)) return std::nullopt;
-        const double ljj = std::sqrt(d);
-        double* lj = l.col(j);
-        lj[j] = ljj;
-        for (int64_t i = j + 1; i < n; ++i) lj[i] = s[i] / ljj;
-    }
-    return l;
-}
-
 namespace {
-
 // AVX2 helpers for the rotation kernels (x86-64-v3 build).
 inline double dot_avx(const double* a, const double* b, int64_t m) {
     __m256d s0 = _mm256_setzero_pd(), s1 = _mm256_setzero_pd();
@@ -160,6 +102,64 @@ inline void rotate_avx(double* x, double* y, int64_t m, double c, double s) {
         y[i] = s * a + c * b;
     }
 }
+
+}  // namespace
+
+DenseMatrix matmul(const DenseMatrix& a, const DenseMatrix& b) {
+    require(a.cols() == b.rows(), "matmul: inner dimensions disagree");
+    DenseMatrix c(a.rows(), b.cols());
+    const int64_t m = a.rows(), k = a.cols();
+#pragma omp parallel for schedule(static) if (m * k * b.cols() > (int64_t(1) << 21))
+    for (int64_t j = 0; j < b.cols(); ++j) {
+        double* cj = c.col(j);
+        for (int64_t p = 0; p < k; ++p) {
+            const double bpj = b(p, j);
+            if (bpj == 0.0) continue;
+            const double* ap = a.col(p);
+            for (int64_t i = 0; i < m; ++i) cj[i] += ap[i] * bpj;
+        }
+    }
+    return c;
+}
+
+DenseMatrix matmul_tn(const DenseMatrix& a, const DenseMatrix& b) {
+    require(a.rows() == b.rows(), "matmul_tn: row dimensions disagree");
+    DenseMatrix c(a.cols(), b.cols());
+    const int64_t m = a.rows();
+#pragma omp parallel for schedule(static) if (m * a.cols() * b.cols() > (int64_t(1) << 21))
+    for (int64_t j = 0; j < b.cols(); ++j) {
+        const double* bj = b.col(j);
+        for (int64_t i = 0; i < a.cols(); ++i) c(i, j) = dot_avx(a.col(i), bj, m);
+    }
+    return c;
+}
+
+std::optional<DenseMatrix> cholesky_lower(const DenseMatrix& a) {
+    if (a.rows() != a.cols()) return std::nullopt;
+    const int64_t n = a.rows();
+    DenseMatrix l(n, n);
+    // Left-looking, column-oriented: column j = (a(:, j) - sum_k l(j,k) l(:, k)) / l_jj with the
+    // k-sum accumulated in the reference's order (dense_kernels.cpp:11-28) but as unit-stride
+    // axpys; the diagonal pivot test (d > 0, finite) is the contract.
+    std::vector<double> s(static_cast<size_t>(n));
+    for (int64_t j = 0; j < n; ++j) {
+        for (int64_t i = j; i < n; ++i) s[i] = a(i, j);
+        for (int64_t k = 0; k < j; ++k) {
+            const double ljk = l(j, k);
+            const double* lk = l.col(k);
+            for (int64_t i = j; i < n; ++i) s[i] -= lk[i] * ljk;
+        }
+        const double d = s[j];
+        if (!(d > 0.0) || !std::isfinite(d)) return std::nullopt;
+        const double ljj = std::sqrt(d);
+        double* lj = l.col(j);
+        lj[j] = ljj;
+        for (int64_t i = j + 1; i < n; ++i) lj[i] = s[i] / ljj;
+    }
+    return l;
+}
+
+namespace {
 
 // Rotate columns p, q of a (m rows) and v (k rows) if they are not yet orthogonal; returns
 // whether a rotation happened.  Rotation formula and test of dense_kernels.cpp:47-79.  The
