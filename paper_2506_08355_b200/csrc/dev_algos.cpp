@@ -411,14 +411,13 @@ void cg_iteration(const LinearOperator& a, const DMat& x, const DMat& r, const D
     if (mode != 1 && Runtime::get().nranks() == 1) {
         // the SpMM leaves p^T A p as per-block partials; each update block folds its column
         const SpmmDot dot{ws.pap_parts(), nullptr, sc.pap, sc.active, CgWorkspace::kPartsPerRegion};
-        if (a.impl()->apply_dot(p, ap, dot)) {
-            const int nparts = static_cast<int>(spmm_dot_blocks(p.rows, dot, static_cast<int>(p.cols)));
+        if (const int nparts = a.impl()->apply_dot(p, ap, dot)) {
             cg_update(x, r, p, ap, sc, tol, mi, ws.pap_parts(), nparts);
             return;
         }
     }
     const SpmmDot dot{ws.pap_parts(), ws.ticket(), sc.pap, sc.active, CgWorkspace::kPartsPerRegion};
-    if (mode != 1 && a.impl()->apply_dot(p, ap, dot)) {
+    if (mode != 1 && a.impl()->apply_dot(p, ap, dot) > 0) {
         Runtime::get().allreduce(sc.pap, p.cols);  // per-rank p^T A p -> global
         cg_update(x, r, p, ap, sc, tol, mi);
         return;

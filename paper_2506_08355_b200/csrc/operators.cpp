@@ -183,9 +183,8 @@ public:
     CsrOp(int64_t n, const int64_t* rp, const int64_t* ci, const double* vv)
         : OperatorImpl(n, LinearOperator::Kind::sparse_csr), s_(n, rp, ci, vv) {}
     void apply(const DMat& x, const DMat& y) const override { sell_spmm(s_.dev, x, y); }
-    bool apply_dot(const DMat& x, const DMat& y, const SpmmDot& dot) const override {
-        sell_spmm(s_.dev, x, y, &dot);
-        return true;
+    int apply_dot(const DMat& x, const DMat& y, const SpmmDot& dot) const override {
+        return sell_spmm(s_.dev, x, y, &dot);
     }
 
 private:
@@ -312,9 +311,8 @@ public:
         Runtime::get().sync();
     }
     void apply(const DMat& x, const DMat& y) const override { sell_spmm(with_halo(x), x, y); }
-    bool apply_dot(const DMat& x, const DMat& y, const SpmmDot& dot) const override {
-        sell_spmm(with_halo(x), x, y, &dot);
-        return true;
+    int apply_dot(const DMat& x, const DMat& y, const SpmmDot& dot) const override {
+        return sell_spmm(with_halo(x), x, y, &dot);
     }
     bool capturable() const override { return false; }
 
@@ -432,9 +430,8 @@ public:
         partitioned_ = s.s_global > 0 && (s.s0 > 0 || s.s0 + snl < s.s_global);
     }
     void apply(const DMat& x, const DMat& y) const override { stencil_spmm(with_halo(x), x, y); }
-    bool apply_dot(const DMat& x, const DMat& y, const SpmmDot& dot) const override {
-        stencil_spmm(with_halo(x), x, y, &dot);
-        return true;
+    int apply_dot(const DMat& x, const DMat& y, const SpmmDot& dot) const override {
+        return stencil_spmm(with_halo(x), x, y, &dot);
     }
     bool capturable() const override { return !partitioned_; }
 

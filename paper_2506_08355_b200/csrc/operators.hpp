@@ -19,11 +19,12 @@ public:
     // Whether apply() only enqueues device work on the solver stream (so it can be recorded
     // into a CUDA graph); host callbacks cannot.
     virtual bool capturable() const { return true; }
-    // y = A x with x(:,j)^T y(:,j) (the CG's p^T A p) fused into the apply and folded into
-    // dot.out; returns false when unsupported (nothing done).
-    virtual bool apply_dot(const DMat& x, const DMat& y, const SpmmDot& dot) const {
+    // y = A x with x(:,j)^T y(:,j) (the CG's p^T A p) fused into the apply: per-block partials
+    // (dot.parts[j * blocks + b]) and, with a ticket, folded into dot.out.  Returns the number of
+    // partial blocks per column, 0 when unsupported (nothing done).
+    virtual int apply_dot(const DMat& x, const DMat& y, const SpmmDot& dot) const {
         (void)x; (void)y; (void)dot;
-        return false;
+        return 0;
     }
 
 private:

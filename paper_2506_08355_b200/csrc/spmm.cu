@@ -495,6 +495,91 @@ __global__ void __launch_bounds__(kRows) k_stencil(StencilDev st, const double* 
     tm.stop();
 }
 
+// Whole-grid stencil with nx even: one thread per pair of x-adjacent rows (i, i+1), i even --
+// half the index arithmetic (two 32-bit divisions per pair), 16-byte loads for the centre and the
+// y/z neighbours, 8-byte loads for the outer x neighbours, one 16-byte store.
+template <int CB, bool DOT>
+__global__ void __launch_bounds__(kRows) k_stencil2(StencilDev st, const double* __restrict__ x,
+                                                     int64_t ldx, double* __restrict__ y, int64_t ldy,
+                                                     int ncols, KTimer tm, DotOut dots) {
+    tm.start();
+    tm.columns(DOT ? dots.active : nullptr, 0, 0, ncols);
+    const int j0 = blockIdx.y * CB;
+    double d[CB];
+#pragma unroll
+    for (int c = 0; c < CB; ++c) d[c] = 0.0;
+    bool on[CB];
+    const bool any = group_columns<CB, DOT>(dots, j0, ncols, on);
+    const unsigned nx = static_cast<unsigned>(st.nx), ny = static_cast<unsigned>(st.ny),
+                   nz = static_cast<unsigned>(st.nz);
+    const int64_t npairs = static_cast<int64_t>(nx / 2) * ny * nz;
+    const int64_t nxy = static_cast<int64_t>(nx) * ny;
+    const bool three = st.dims == 3;
+    const int64_t ntiles = any ? (npairs + kRows - 1) / kRows : 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t pr = tile * kRows + threadIdx.x;
+        if (pr >= npairs) continue;
+        const unsigned q = static_cast<unsigned>(pr);
+        const unsigned hx = nx / 2;
+        const unsigned i = 2 * (q % hx);
+        const unsigned t = q / hx;
+        const unsigned jy = t % ny, kz = t / ny;
+        const int64_t idx = static_cast<int64_t>(t) * nx + i;
+        const bool xm = i > 0, xp = i + 2 < nx;
+        const bool ym = jy > 0, yp = jy + 1 < ny;
+        const bool zm = three && kz > 0, zp = three && kz + 1 < nz;
+        // diagonals of the two rows (they differ only in the x boundary terms)
+        double dg0, dg1;
+        if (st.bc == 0) {
+            const double rest = static_cast<double>(ym + yp + zm + zp);
+            dg0 = (rest + (xm ? 1.0 : 0.0) + 1.0) * st.scale;  // row i: neighbour i+1 always exists
+            dg1 = (rest + 1.0 + (xp ? 1.0 : 0.0)) * st.scale;  // row i+1: neighbour i always exists
+        } else {
+            dg0 = dg1 = 2.0 * st.dims * st.scale;
+        }
+        if (st.potential == 1) {
+            const double cy = st.origin + (jy + 1) * st.h;
+            const double cz = three ? st.origin + (kz + 1) * st.h : 0.0;
+            const double cx0 = st.origin + (i + 1) * st.h, cx1 = st.origin + (i + 2) * st.h;
+            const double yz = cy * cy + cz * cz;
+            dg0 += 0.5 * (cx0 * cx0 + yz);
+            dg1 += 0.5 * (cx1 * cx1 + yz);
+        } else if (st.potential == 2) {
+            const double2 v = __ldg(reinterpret_cast<const double2*>(st.v + idx));
+            dg0 += v.x;
+            dg1 += v.y;
+        }
+#pragma unroll
+        for (int c = 0; c < CB; ++c) {
+            if (!on[c]) continue;
+            const double* xc = x + static_cast<int64_t>(j0 + c) * ldx + idx;
+            const double2 ctr = __ldg(reinterpret_cast<const double2*>(xc));
+            // row i: i-1 (outer), i+1 (= ctr.y); row i+1: i (= ctr.x), i+2 (outer)
+            double nb0 = ctr.y, nb1 = ctr.x;
+            if (xm) nb0 += __ldg(xc - 1);
+            if (xp) nb1 += __ldg(xc + 2);
+            auto add2 = [&](int64_t off) {
+                const double2 v = __ldg(reinterpret_cast<const double2*>(xc + off));
+                nb0 += v.x;
+                nb1 += v.y;
+            };
+            if (ym) add2(-static_cast<int64_t>(nx));
+            if (yp) add2(nx);
+            if (zm) add2(-nxy);
+            if (zp) add2(nxy);
+            const double y0 = dg0 * ctr.x - st.scale * nb0;
+            const double y1 = dg1 * ctr.y - st.scale * nb1;
+            *reinterpret_cast<double2*>(y + static_cast<int64_t>(j0 + c) * ldy + idx) = make_double2(y0, y1);
+            if (DOT) d[c] += ctr.x * y0 + ctr.y * y1;
+        }
+    }
+    if (DOT) {
+        block_dots_out<CB>(d, dots.parts, j0, ncols);
+        fold_dots_last_block(dots.parts, ncols, dots.ticket, dots.out);
+    }
+    tm.stop();
+}
+
 // Row-tile blocks per column group: one per tile, bounded with dots by the partials buffer
 // (ncols x blocks doubles); the last block folds them.
 unsigned row_blocks(int64_t n, const SpmmDot* dot, int ncols) {
@@ -671,6 +756,15 @@ int stencil_spmm(const StencilDev& s, const DMat& x, const DMat& y, const SpmmDo
     if (part) {
         if (dot) k_stencil<CB, true, true><<<grid, kRows, 0, rt.stream()>>>(s, x.p, x.ld, y.p, y.ld, ncols, tm, dd);
         else k_stencil<CB, false, true><<<grid, kRows, 0, rt.stream()>>>(s, x.p, x.ld, y.p, y.ld, ncols, tm, dd);
+    } else if ((s.nx & 1) == 0 && (x.ld & 1) == 0 && (y.ld & 1) == 0 && n < (int64_t(1) << 32) &&
+               !std::getenv("BOSP_STENCIL_ROWS")) {
+        // row pairs: half the tiles
+        const unsigned gx2 = row_blocks(n / 2, dot, ncols);
+        const dim3 grid2(gx2, (ncols + CB - 1) / CB);
+        if (dot) k_stencil2<CB, true><<<grid2, kRows, 0, rt.stream()>>>(s, x.p, x.ld, y.p, y.ld, ncols, tm, dd);
+        else k_stencil2<CB, false><<<grid2, kRows, 0, rt.stream()>>>(s, x.p, x.ld, y.p, y.ld, ncols, tm, dd);
+        BOSP_LAUNCH_CHECK();
+        return static_cast<int>(gx2);
     } else {
         if (dot) k_stencil<CB, true, false><<<grid, kRows, 0, rt.stream()>>>(s, x.p, x.ld, y.p, y.ld, ncols, tm, dd);
         else k_stencil<CB, false, false><<<grid, kRows, 0, rt.stream()>>>(s, x.p, x.ld, y.p, y.ld, ncols, tm, dd);
