@@ -141,31 +141,42 @@ private:
 
 // CSR (rows rp[0..n], entries from rp[0]) -> SELL-32 in HBM.  Column indices are taken as given
 // (a row-partitioned operator passes them already remapped to [local | halo]).
+// CSR arrays copied to the device once (pinned-ring staging); SELL-32 and DIA are built from
+// them there, nothing of size nnz is built on the host.
+struct DevCsr {
+    DevFree rp{nullptr}, ci{nullptr}, vv{nullptr};
+    int64_t n = 0, nnz = 0;
+    DevCsr(int64_t n_, const int64_t* hrp, const int64_t* hci, const double* hvv) : n(n_) {
+        Runtime& rt = Runtime::get();
+        nnz = hrp[n] - hrp[0];
+        rp.p = rt.alloc(sizeof(int64_t) * (n + 1));
+        ci.p = rt.alloc(sizeof(int64_t) * std::max<int64_t>(nnz, 1));
+        vv.p = rt.alloc(sizeof(double) * std::max<int64_t>(nnz, 1));
+        h2d_bytes(rp.p, hrp, sizeof(int64_t) * (n + 1));
+        h2d_bytes(ci.p, hci, sizeof(int64_t) * nnz);
+        h2d_bytes(vv.p, hvv, sizeof(double) * nnz);
+    }
+    const int64_t* rowptr() const { return static_cast<const int64_t*>(rp.p); }
+    const int64_t* colidx() const { return static_cast<const int64_t*>(ci.p); }
+    const double* vals() const { return static_cast<const double*>(vv.p); }
+};
+
 struct SellStore {
     DevFree sp{nullptr}, sw{nullptr}, col{nullptr}, val{nullptr};
     SellDev dev;
-    // The CSR arrays are copied to the device once (pinned-ring staging) and converted to
-    // SELL-32 there; nothing of size nnz is built on the host.
-    SellStore(int64_t n, const int64_t* rp, const int64_t* ci, const double* vv) {
+    SellStore(int64_t n, const int64_t* rp, const int64_t* ci, const double* vv) { build(DevCsr(n, rp, ci, vv)); }
+    explicit SellStore(const DevCsr& c) { build(c); }
+    void build(const DevCsr& c) {
+        const int64_t n = c.n;
         require(n < (int64_t(1) << 31), "from_csr: dimension exceeds int32 device indices");
         Runtime& rt = Runtime::get();
-        const int64_t base = rp[0];
-        const int64_t nnz = rp[n] - base;
         const int64_t nsl = (n + 31) / 32;
-        DevFree drp(rt.alloc(sizeof(int64_t) * (n + 1)));
-        DevFree dci(rt.alloc(sizeof(int64_t) * std::max<int64_t>(nnz, 1)));
-        DevFree dvv(rt.alloc(sizeof(double) * std::max<int64_t>(nnz, 1)));
-        h2d_bytes(drp.p, rp, sizeof(int64_t) * (n + 1));
-        h2d_bytes(dci.p, ci, sizeof(int64_t) * nnz);
-        h2d_bytes(dvv.p, vv, sizeof(double) * nnz);
         sp.p = rt.alloc(sizeof(int64_t) * (nsl + 1));
         sw.p = rt.alloc(sizeof(int32_t) * std::max<int64_t>(nsl, 1));
-        const int64_t total = sell_layout(n, static_cast<const int64_t*>(drp.p), static_cast<int64_t*>(sp.p),
-                                          static_cast<int32_t*>(sw.p));
+        const int64_t total = sell_layout(n, c.rowptr(), static_cast<int64_t*>(sp.p), static_cast<int32_t*>(sw.p));
         col.p = rt.alloc(sizeof(int32_t) * std::max<int64_t>(total, 1));
         val.p = rt.alloc(sizeof(double) * std::max<int64_t>(total, 1));
-        sell_fill(n, static_cast<const int64_t*>(drp.p), static_cast<const int64_t*>(dci.p),
-                  static_cast<const double*>(dvv.p), static_cast<const int64_t*>(sp.p),
+        sell_fill(n, c.rowptr(), c.colidx(), c.vals(), static_cast<const int64_t*>(sp.p),
                   static_cast<const int32_t*>(sw.p), static_cast<int32_t*>(col.p), static_cast<double*>(val.p));
         dev.n = n;
         dev.nslices = nsl;
@@ -173,21 +184,88 @@ struct SellStore {
         dev.slice_w = static_cast<const int32_t*>(sw.p);
         dev.col = static_cast<const int32_t*>(col.p);
         dev.val = static_cast<const double*>(val.p);
-        dev.nnz = nnz;
-        rt.sync();  // the CSR copies are released at scope exit
+        dev.nnz = c.nnz;
+        rt.sync();  // the CSR copies may be released after this
+    }
+};
+
+// Banded / stencil-structured CSR (at most kDiaMax distinct column offsets, padding below 2x,
+// n even) is stored by diagonals: gather-free, vectorised applies (the CSR row sums in the same
+// order).  Everything else is SELL-32.
+struct DiaStore {
+    DevFree val{nullptr}, mask{nullptr};
+    DiaDev dev;
+    bool ok = false;
+    explicit DiaStore(const DevCsr& c) {
+        static const bool off_switch = std::getenv("BOSP_NO_DIA") != nullptr;
+        const int64_t n = c.n;
+        if (off_switch || n < 64 || (n & 1) || n >= (int64_t(1) << 31)) return;
+        int64_t offs[kDiaMax];
+        const int nd = dia_offsets(n, c.rowptr(), c.colidx(), offs);
+        if (nd <= 0 || static_cast<int64_t>(nd) * n > 2 * c.nnz) return;
+        std::sort(offs, offs + nd);
+        dev.n = n;
+        dev.ndiag = nd;
+        for (int d = 0; d < nd; ++d) dev.off[d] = offs[d];
+        Runtime& rt = Runtime::get();
+        mask.p = rt.alloc(sizeof(uint16_t) * n);
+        DBlock mm(2 * kDiaMax, 1);
+        auto* vmin = reinterpret_cast<unsigned long long*>(mm.data());
+        auto* vmax = vmin + kDiaMax;
+        std::vector<unsigned long long> init(2 * kDiaMax);
+        for (int d = 0; d < kDiaMax; ++d) {
+            init[d] = ~0ULL;
+            init[kDiaMax + d] = 0ULL;
+        }
+        BOSP_CUDA(cudaMemcpyAsync(vmin, init.data(), sizeof(unsigned long long) * 2 * kDiaMax,
+                                  cudaMemcpyHostToDevice, rt.stream()));
+        dia_scan(n, c.rowptr(), c.colidx(), c.vals(), dev, static_cast<uint16_t*>(mask.p), vmin, vmax);
+        std::vector<unsigned long long> mm_h(2 * kDiaMax);
+        BOSP_CUDA(cudaMemcpyAsync(mm_h.data(), vmin, sizeof(unsigned long long) * 2 * kDiaMax,
+                                  cudaMemcpyDeviceToHost, rt.stream()));
+        rt.sync();
+        int nvar = 0;
+        for (int d = 0; d < nd; ++d) {
+            const bool constant = mm_h[d] == mm_h[kDiaMax + d];  // identical bit patterns
+            double cv;
+            std::memcpy(&cv, &mm_h[d], sizeof(double));
+            dev.cval[d] = constant ? cv : 0.0;
+            dev.vidx[d] = constant ? -1 : nvar++;
+        }
+        val.p = rt.alloc(sizeof(double) * std::max(nvar, 1) * n);
+        if (nvar > 0) {
+            BOSP_CUDA(cudaMemsetAsync(val.p, 0, sizeof(double) * nvar * n, rt.stream()));
+            dia_fill(n, c.rowptr(), c.colidx(), c.vals(), dev, static_cast<double*>(val.p));
+        }
+        dev.val = static_cast<const double*>(val.p);
+        dev.mask = static_cast<const uint16_t*>(mask.p);
+        const uint32_t all = (1u << nd) - 1u;
+        dev.full_pair = all | (all << 16);
+        for (int d = 0; d < nd; ++d)
+            if ((offs[d] & 1) == 0) dev.even |= 1u << d;
+        dev.nnz = c.nnz;
+        ok = true;
     }
 };
 
 class CsrOp final : public OperatorImpl {
 public:
     CsrOp(int64_t n, const int64_t* rp, const int64_t* ci, const double* vv)
-        : OperatorImpl(n, LinearOperator::Kind::sparse_csr), s_(n, rp, ci, vv) {}
-    void apply(const DMat& x, const DMat& y) const override { sell_spmm(s_.dev, x, y); }
+        : CsrOp(n, DevCsr(n, rp, ci, vv)) {}
+    CsrOp(int64_t n, const DevCsr& c) : OperatorImpl(n, LinearOperator::Kind::sparse_csr), d_(c), s_(c) {}
+    void apply(const DMat& x, const DMat& y) const override {
+        if (d_.ok && dia_fits(x, y)) dia_spmm(d_.dev, x, y);
+        else sell_spmm(s_.dev, x, y);
+    }
     int apply_dot(const DMat& x, const DMat& y, const SpmmDot& dot) const override {
+        if (d_.ok && dia_fits(x, y)) return dia_spmm(d_.dev, x, y, &dot);
         return sell_spmm(s_.dev, x, y, &dot);
     }
 
 private:
+    // DIA needs 16-byte aligned row pairs; odd leading dimensions take the SELL copy
+    static bool dia_fits(const DMat& x, const DMat& y) { return (x.ld & 1) == 0 && (y.ld & 1) == 0; }
+    DiaStore d_;
     SellStore s_;
 };
 

@@ -22,6 +22,25 @@ struct SellDev {
     int64_t ldh = 0;
 };
 
+// DIA (diagonal) storage for banded / stencil-structured CSR matrices: ndiag offsets (ascending,
+// the CSR column order within a row), a per-row presence mask (bit d: A(i, i+off[d]) stored in
+// the CSR) and, per diagonal, either one constant value (every stored entry equal -- the
+// off-diagonals of a constant-coefficient stencil) or an n-vector of values.  Row i's products
+// are summed over the present entries in CSR order, so the sums equal the CSR row sums.
+constexpr int kDiaMax = 16;
+struct DiaDev {
+    int64_t n = 0;
+    int32_t ndiag = 0;
+    int64_t off[kDiaMax] = {};
+    double cval[kDiaMax] = {};   // constant diagonals
+    int32_t vidx[kDiaMax] = {};  // -1: constant, else row of `val`
+    const double* val = nullptr; // nvar x n
+    const uint16_t* mask = nullptr;
+    uint32_t full_pair = 0;  // mask word of a row pair with every diagonal present
+    uint32_t even = 0;       // bit d: off[d] even (16-byte x pairs)
+    int64_t nnz = 0;  // CSR nonzeros (algorithmic byte counts)
+};
+
 // Fused x(:,j)^T y(:,j) (the CG's p^T A p): per-block partials in `parts` (<= 256 x ncols),
 // folded in fixed order by the last block into out[j]; `ticket` must be zero and stays zero.
 struct SpmmDot {
@@ -42,6 +61,17 @@ void sell_fill(int64_t n, const int64_t* rp, const int64_t* ci, const double* vv
 // y(:, j) = A x(:, j) for all columns of x (optionally with the fused dots); returns the number
 // of row blocks.
 int sell_spmm(const SellDev& a, const DMat& x, const DMat& y, const SpmmDot* dot = nullptr);
+// Device DIA construction from device CSR arrays (rp may carry a base offset):
+//   dia_offsets: distinct column offsets into table[kDiaMax] (unsorted, INT64_MIN = empty);
+//                returns the count, or -1 when there are more than kDiaMax;
+//   dia_scan:    presence masks + per-diagonal min/max of the raw value bits (constant test);
+//   dia_fill:    values of the non-constant diagonals.
+int dia_offsets(int64_t n, const int64_t* rp, const int64_t* ci, int64_t* table);
+void dia_scan(int64_t n, const int64_t* rp, const int64_t* ci, const double* vv, const DiaDev& layout,
+              uint16_t* mask, unsigned long long* vmin, unsigned long long* vmax);
+void dia_fill(int64_t n, const int64_t* rp, const int64_t* ci, const double* vv, const DiaDev& layout, double* val);
+// y = A x for a DIA matrix (n even), optionally with the fused dots; returns the row blocks.
+int dia_spmm(const DiaDev& a, const DMat& x, const DMat& y, const SpmmDot* dot = nullptr);
 // Blocks a dot-fused apply of n rows x ncols uses (partials per column).
 unsigned spmm_dot_blocks(int64_t n, const SpmmDot& dot, int ncols);
 

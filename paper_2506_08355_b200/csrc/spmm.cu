@@ -8,6 +8,7 @@
 // the matrix-free from_callback path (linear_operator.cpp:45-47) for the stencils.
 #include <algorithm>
 #include <cstdlib>
+#include <vector>
 
 #include "runtime.hpp"
 #include "sparse_ops.hpp"
@@ -580,6 +581,71 @@ __global__ void __launch_bounds__(kRows) k_stencil2(StencilDev st, const double*
     tm.stop();
 }
 
+// DIA SpMM on row pairs (i, i+1), i even: one 4-byte load brings both rows' presence masks,
+// constant diagonals cost no memory traffic, varying ones one 16-byte load per pair (all loaded
+// once and reused for the CB columns); x(i+off) pairs are 16-byte loads for even offsets, two
+// 8-byte loads for odd ones.  Present entries are summed in CSR column order.
+template <int CB, bool DOT, int ND>
+__global__ void __launch_bounds__(kRows) k_dia(DiaDev a, const double* __restrict__ x, int64_t ldx,
+                                                double* __restrict__ y, int64_t ldy, int ncols, KTimer tm,
+                                                DotOut dots) {
+    tm.start();
+    tm.columns(DOT ? dots.active : nullptr, 0, 0, ncols);
+    const int j0 = blockIdx.y * CB;
+    double d[CB];
+#pragma unroll
+    for (int c = 0; c < CB; ++c) d[c] = 0.0;
+    bool on[CB];
+    const bool any = group_columns<CB, DOT>(dots, j0, ncols, on);
+    const int64_t n = a.n, npairs = n / 2;
+    const int nd = a.ndiag;
+    const int64_t ntiles = any ? (npairs + kRows - 1) / kRows : 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t pr = tile * kRows + threadIdx.x;
+        if (pr >= npairs) continue;
+        const int64_t i = 2 * pr;
+        const unsigned mk = __ldg(reinterpret_cast<const unsigned*>(a.mask + i));  // row i low, i+1 high
+        double2 v[ND];
+#pragma unroll
+        for (int k = 0; k < ND; ++k) {
+            if (k >= nd) break;
+            const int vi = a.vidx[k];
+            v[k] = vi < 0 ? make_double2(a.cval[k], a.cval[k])
+                          : __ldg(reinterpret_cast<const double2*>(a.val + vi * n + i));
+        }
+#pragma unroll
+        for (int c = 0; c < CB; ++c) {
+            if (!on[c]) continue;
+            const double* xc = x + static_cast<int64_t>(j0 + c) * ldx;
+            double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+            for (int k = 0; k < ND; ++k) {
+                if (k >= nd) break;
+                const bool p0 = (mk >> k) & 1u, p1 = (mk >> (16 + k)) & 1u;
+                const int64_t j = i + a.off[k];
+                if (((a.even >> k) & 1u) && p0 && p1) {
+                    const double2 t = __ldg(reinterpret_cast<const double2*>(xc + j));
+                    acc0 += v[k].x * t.x;
+                    acc1 += v[k].y * t.y;
+                } else {
+                    if (p0) acc0 += v[k].x * __ldg(xc + j);
+                    if (p1) acc1 += v[k].y * __ldg(xc + j + 1);
+                }
+            }
+            *reinterpret_cast<double2*>(y + static_cast<int64_t>(j0 + c) * ldy + i) = make_double2(acc0, acc1);
+            if (DOT) {
+                const double2 xs = __ldg(reinterpret_cast<const double2*>(xc + i));
+                d[c] += xs.x * acc0 + xs.y * acc1;
+            }
+        }
+    }
+    if (DOT) {
+        block_dots_out<CB>(d, dots.parts, j0, ncols);
+        fold_dots_last_block(dots.parts, ncols, dots.ticket, dots.out);
+    }
+    tm.stop();
+}
+
 // Row-tile blocks per column group: one per tile, bounded with dots by the partials buffer
 // (ncols x blocks doubles); the last block folds them.
 unsigned row_blocks(int64_t n, const SpmmDot* dot, int ncols) {
@@ -658,6 +724,108 @@ __global__ void k_sell_fill(int64_t n, const int64_t* __restrict__ rp, const int
 
 }  // namespace
 
+namespace {
+
+__global__ void k_dia_offsets(int64_t n, const int64_t* __restrict__ rp, const int64_t* __restrict__ ci,
+                              unsigned long long* table, int* overflow) {
+    const int64_t base = rp[0];
+    for (int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < n;
+         r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        for (int64_t k = rp[r] - base; k < rp[r + 1] - base; ++k) {
+            const unsigned long long o = static_cast<unsigned long long>(ci[k] - r);
+            bool found = false;
+            for (int q = 0; q < kDiaMax && !found; ++q) found = (*(volatile unsigned long long*)&table[q]) == o;
+            if (found) continue;
+            bool placed = false;
+            for (int q = 0; q < kDiaMax && !placed; ++q) {
+                const unsigned long long prev = atomicCAS(&table[q], 0x8000000000000000ULL, o);
+                placed = prev == 0x8000000000000000ULL || prev == o;
+            }
+            if (!placed) atomicExch(overflow, 1);
+        }
+    }
+}
+
+__device__ __forceinline__ int dia_index(const DiaDev& a, int64_t o) {
+    int d = 0;
+    for (int q = 0; q < a.ndiag; ++q) d += a.off[q] < o;  // offsets sorted ascending
+    return d;
+}
+
+__global__ void k_dia_scan(int64_t n, const int64_t* __restrict__ rp, const int64_t* __restrict__ ci,
+                           const double* __restrict__ vv, DiaDev a, uint16_t* mask, unsigned long long* vmin,
+                           unsigned long long* vmax) {
+    const int64_t base = rp[0];
+    for (int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < n;
+         r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        unsigned m = 0;
+        for (int64_t k = rp[r] - base; k < rp[r + 1] - base; ++k) {
+            const int d = dia_index(a, ci[k] - r);
+            m |= 1u << d;
+            const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(vv[k]));
+            atomicMin(&vmin[d], bits);
+            atomicMax(&vmax[d], bits);
+        }
+        mask[r] = static_cast<uint16_t>(m);
+    }
+}
+
+__global__ void k_dia_fill(int64_t n, const int64_t* __restrict__ rp, const int64_t* __restrict__ ci,
+                           const double* __restrict__ vv, DiaDev a, double* val) {
+    const int64_t base = rp[0];
+    for (int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < n;
+         r += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        for (int64_t k = rp[r] - base; k < rp[r + 1] - base; ++k) {
+            const int d = dia_index(a, ci[k] - r);
+            if (a.vidx[d] >= 0) val[a.vidx[d] * n + r] = vv[k];
+        }
+}
+
+}  // namespace
+
+int dia_offsets(int64_t n, const int64_t* rp, const int64_t* ci, int64_t* table) {
+    Runtime& rt = Runtime::get();
+    DBlock scratch(kDiaMax + 1, 1);
+    auto* t = reinterpret_cast<unsigned long long*>(scratch.data());
+    auto* ovf = reinterpret_cast<int*>(t + kDiaMax);
+    std::vector<unsigned long long> init(kDiaMax + 1, 0x8000000000000000ULL);
+    init[kDiaMax] = 0;
+    BOSP_CUDA(cudaMemcpyAsync(t, init.data(), sizeof(unsigned long long) * (kDiaMax + 1), cudaMemcpyHostToDevice,
+                              rt.stream()));
+    {
+        LaunchScope ls("setup");
+        k_dia_offsets<<<static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 4LL * rt.sm_count())), 256, 0,
+                        rt.stream()>>>(n, rp, ci, t, ovf);
+        BOSP_LAUNCH_CHECK();
+    }
+    std::vector<unsigned long long> h(kDiaMax + 1);
+    BOSP_CUDA(cudaMemcpyAsync(h.data(), t, sizeof(unsigned long long) * (kDiaMax + 1), cudaMemcpyDeviceToHost,
+                              rt.stream()));
+    rt.sync();
+    if (static_cast<int>(h[kDiaMax] & 0xffffffffULL) != 0) return -1;
+    int cnt = 0;
+    for (int q = 0; q < kDiaMax; ++q)
+        if (h[q] != 0x8000000000000000ULL) table[cnt++] = static_cast<int64_t>(h[q]);
+    return cnt;
+}
+
+void dia_scan(int64_t n, const int64_t* rp, const int64_t* ci, const double* vv, const DiaDev& layout,
+              uint16_t* mask, unsigned long long* vmin, unsigned long long* vmax) {
+    Runtime& rt = Runtime::get();
+    LaunchScope ls("setup");
+    k_dia_scan<<<static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 8LL * rt.sm_count())), 256, 0,
+                 rt.stream()>>>(n, rp, ci, vv, layout, mask, vmin, vmax);
+    BOSP_LAUNCH_CHECK();
+}
+
+void dia_fill(int64_t n, const int64_t* rp, const int64_t* ci, const double* vv, const DiaDev& layout, double* val) {
+    Runtime& rt = Runtime::get();
+    LaunchScope ls("setup");
+    k_dia_fill<<<static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 8LL * rt.sm_count())), 256, 0,
+                 rt.stream()>>>(n, rp, ci, vv, layout, val);
+    BOSP_LAUNCH_CHECK();
+}
+
 int64_t sell_layout(int64_t n, const int64_t* rp, int64_t* slice_ptr, int32_t* slice_w) {
     const int64_t nsl = (n + 31) / 32;
     Runtime& rt = Runtime::get();
@@ -731,6 +899,41 @@ int sell_spmm(const SellDev& a, const DMat& x, const DMat& y, const SpmmDot* dot
         }
     }
     BOSP_LAUNCH_CHECK();
+    return static_cast<int>(gx);
+}
+
+template <int CB>
+unsigned launch_dia(const DiaDev& a, const DMat& x, const DMat& y, const SpmmDot* dot, KTimer tm) {
+    Runtime& rt = Runtime::get();
+    const int ncols = static_cast<int>(x.cols);
+    const unsigned gx = row_blocks(a.n / 2, dot, ncols);
+    const dim3 grid(gx, (ncols + CB - 1) / CB);
+    const DotOut dd = dot ? DotOut{dot->parts, dot->ticket, dot->out, dot->active} : DotOut{};
+    if (a.ndiag <= 8) {  // stencils: 5 / 7 diagonals, half the value registers
+        if (dot) k_dia<CB, true, 8><<<grid, kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm, dd);
+        else k_dia<CB, false, 8><<<grid, kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm, dd);
+    } else {
+        if (dot) k_dia<CB, true, kDiaMax><<<grid, kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm, dd);
+        else k_dia<CB, false, kDiaMax><<<grid, kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm, dd);
+    }
+    BOSP_LAUNCH_CHECK();
+    return gx;
+}
+
+int dia_spmm(const DiaDev& a, const DMat& x, const DMat& y, const SpmmDot* dot) {
+    if (a.n == 0 || x.cols == 0) return 0;
+    require((a.n & 1) == 0 && (x.ld & 1) == 0 && (y.ld & 1) == 0, "dia_spmm: even rows and leading dims");
+    Runtime& rt = Runtime::get();
+    const int ncols = static_cast<int>(x.cols);
+    // algorithmic bytes as for CSR so the roofline is format-independent
+    const double bytes = 12.0 * a.nnz + 4.0 * (a.n + 1) + 16.0 * a.n * ncols;
+    const double flops = 2.0 * a.nnz * ncols;
+    const char* fam = dot ? "spmm_cg" : "spmm";
+    KTimer tm{rt.timer_begin(fam, bytes, flops, 12.0 * a.nnz + 4.0 * (a.n + 1), ncols)};
+    LaunchScope ls(fam, bytes, flops, false);
+    static const int cb = std::getenv("BOSP_DIA_CB") ? std::atoi(std::getenv("BOSP_DIA_CB")) : 4;
+    const unsigned gx = cb == 8 ? launch_dia<8>(a, x, y, dot, tm) : cb == 2 ? launch_dia<2>(a, x, y, dot, tm)
+                                                                            : launch_dia<4>(a, x, y, dot, tm);
     return static_cast<int>(gx);
 }
 
