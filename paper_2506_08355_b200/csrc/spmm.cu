@@ -726,23 +726,44 @@ __global__ void k_sell_fill(int64_t n, const int64_t* __restrict__ rp, const int
 
 namespace {
 
+// Distinct column offsets: each block builds its own set in shared memory (CAS on shared slots),
+// then merges it into the global table -- at most kDiaMax global CAS per block.
 __global__ void k_dia_offsets(int64_t n, const int64_t* __restrict__ rp, const int64_t* __restrict__ ci,
                               unsigned long long* table, int* overflow) {
+    constexpr unsigned long long kEmpty = 0x8000000000000000ULL;
+    __shared__ unsigned long long local[kDiaMax];
+    __shared__ int ovf;
+    if (threadIdx.x < kDiaMax) local[threadIdx.x] = kEmpty;
+    if (threadIdx.x == 0) ovf = 0;
+    __syncthreads();
     const int64_t base = rp[0];
     for (int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < n;
          r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         for (int64_t k = rp[r] - base; k < rp[r + 1] - base; ++k) {
             const unsigned long long o = static_cast<unsigned long long>(ci[k] - r);
-            bool found = false;
-            for (int q = 0; q < kDiaMax && !found; ++q) found = (*(volatile unsigned long long*)&table[q]) == o;
-            if (found) continue;
             bool placed = false;
             for (int q = 0; q < kDiaMax && !placed; ++q) {
-                const unsigned long long prev = atomicCAS(&table[q], 0x8000000000000000ULL, o);
-                placed = prev == 0x8000000000000000ULL || prev == o;
+                const unsigned long long cur = *(volatile unsigned long long*)&local[q];
+                if (cur == o) {
+                    placed = true;
+                } else if (cur == kEmpty) {
+                    const unsigned long long prev = atomicCAS(&local[q], kEmpty, o);
+                    placed = prev == kEmpty || prev == o;
+                }
             }
-            if (!placed) atomicExch(overflow, 1);
+            if (!placed) ovf = 1;
         }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && ovf) atomicExch(overflow, 1);
+    if (threadIdx.x < kDiaMax && local[threadIdx.x] != kEmpty) {
+        const unsigned long long o = local[threadIdx.x];
+        bool placed = false;
+        for (int q = 0; q < kDiaMax && !placed; ++q) {
+            const unsigned long long prev = atomicCAS(&table[q], kEmpty, o);
+            placed = prev == kEmpty || prev == o;
+        }
+        if (!placed) atomicExch(overflow, 1);
     }
 }
 
@@ -755,6 +776,12 @@ __device__ __forceinline__ int dia_index(const DiaDev& a, int64_t o) {
 __global__ void k_dia_scan(int64_t n, const int64_t* __restrict__ rp, const int64_t* __restrict__ ci,
                            const double* __restrict__ vv, DiaDev a, uint16_t* mask, unsigned long long* vmin,
                            unsigned long long* vmax) {
+    __shared__ unsigned long long smin[kDiaMax], smax[kDiaMax];
+    if (threadIdx.x < kDiaMax) {
+        smin[threadIdx.x] = ~0ULL;
+        smax[threadIdx.x] = 0ULL;
+    }
+    __syncthreads();
     const int64_t base = rp[0];
     for (int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < n;
          r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -763,10 +790,15 @@ __global__ void k_dia_scan(int64_t n, const int64_t* __restrict__ rp, const int6
             const int d = dia_index(a, ci[k] - r);
             m |= 1u << d;
             const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(vv[k]));
-            atomicMin(&vmin[d], bits);
-            atomicMax(&vmax[d], bits);
+            if (bits < smin[d]) atomicMin(&smin[d], bits);
+            if (bits > smax[d]) atomicMax(&smax[d], bits);
         }
         mask[r] = static_cast<uint16_t>(m);
+    }
+    __syncthreads();
+    if (threadIdx.x < kDiaMax && threadIdx.x < a.ndiag) {
+        atomicMin(&vmin[threadIdx.x], smin[threadIdx.x]);
+        atomicMax(&vmax[threadIdx.x], smax[threadIdx.x]);
     }
 }
 
