@@ -585,7 +585,7 @@ __global__ void __launch_bounds__(kRows) k_stencil2(StencilDev st, const double*
 // constant diagonals cost no memory traffic, varying ones one 16-byte load per pair (all loaded
 // once and reused for the CB columns); x(i+off) pairs are 16-byte loads for even offsets, two
 // 8-byte loads for odd ones.  Present entries are summed in CSR column order.
-template <int CB, bool DOT, int ND>
+template <int CB, bool DOT, int ND, bool EXACT>
 __global__ void __launch_bounds__(kRows) k_dia(DiaDev a, const double* __restrict__ x, int64_t ldx,
                                                 double* __restrict__ y, int64_t ldy, int ncols, KTimer tm,
                                                 DotOut dots) {
@@ -598,7 +598,7 @@ __global__ void __launch_bounds__(kRows) k_dia(DiaDev a, const double* __restric
     bool on[CB];
     const bool any = group_columns<CB, DOT>(dots, j0, ncols, on);
     const int64_t n = a.n, npairs = n / 2;
-    const int nd = a.ndiag;
+    const int nd = EXACT ? ND : a.ndiag;
     const int64_t ntiles = any ? (npairs + kRows - 1) / kRows : 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int64_t pr = tile * kRows + threadIdx.x;
@@ -934,19 +934,29 @@ int sell_spmm(const SellDev& a, const DMat& x, const DMat& y, const SpmmDot* dot
     return static_cast<int>(gx);
 }
 
+template <int CB, int ND, bool EXACT>
+void launch_dia_nd(const DiaDev& a, const DMat& x, const DMat& y, const DotOut& dd, bool dot, dim3 grid, KTimer tm) {
+    Runtime& rt = Runtime::get();
+    const int ncols = static_cast<int>(x.cols);
+    if (dot) k_dia<CB, true, ND, EXACT><<<grid, kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm, dd);
+    else k_dia<CB, false, ND, EXACT><<<grid, kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm, dd);
+}
+
 template <int CB>
 unsigned launch_dia(const DiaDev& a, const DMat& x, const DMat& y, const SpmmDot* dot, KTimer tm) {
-    Runtime& rt = Runtime::get();
     const int ncols = static_cast<int>(x.cols);
     const unsigned gx = row_blocks(a.n / 2, dot, ncols);
     const dim3 grid(gx, (ncols + CB - 1) / CB);
     const DotOut dd = dot ? DotOut{dot->parts, dot->ticket, dot->out, dot->active} : DotOut{};
-    if (a.ndiag <= 8) {  // stencils: 5 / 7 diagonals, half the value registers
-        if (dot) k_dia<CB, true, 8><<<grid, kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm, dd);
-        else k_dia<CB, false, 8><<<grid, kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm, dd);
-    } else {
-        if (dot) k_dia<CB, true, kDiaMax><<<grid, kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm, dd);
-        else k_dia<CB, false, kDiaMax><<<grid, kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm, dd);
+    const bool d = dot != nullptr;
+    switch (a.ndiag) {  // the common stencil widths get fully unrolled loops
+        case 3: launch_dia_nd<CB, 3, true>(a, x, y, dd, d, grid, tm); break;
+        case 5: launch_dia_nd<CB, 5, true>(a, x, y, dd, d, grid, tm); break;
+        case 7: launch_dia_nd<CB, 7, true>(a, x, y, dd, d, grid, tm); break;
+        case 9: launch_dia_nd<CB, 9, true>(a, x, y, dd, d, grid, tm); break;
+        default:
+            if (a.ndiag <= 8) launch_dia_nd<CB, 8, false>(a, x, y, dd, d, grid, tm);
+            else launch_dia_nd<CB, kDiaMax, false>(a, x, y, dd, d, grid, tm);
     }
     BOSP_LAUNCH_CHECK();
     return gx;
