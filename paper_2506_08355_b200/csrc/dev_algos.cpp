@@ -469,7 +469,7 @@ DevCgOutcome dev_cg(const LinearOperator& a, const DMat& rhs, const DMat& x, dou
             // graph -- every kernel early-outs once its columns are done, no conditional node,
             // and every launch keeps its own profiling slot.  Long solves use a device while loop.
             static const bool force_while = std::getenv("BOSP_CG_WHILE") != nullptr;
-            if (max_iter <= kCgUnrollMax && !force_while) {
+            if (max_iter <= kCgUnrollMax && !force_while && a.impl()->has_masked_dot() && cg_mode() != 2) {
                 CgScalars sc = ws.s;
                 sc.has_cond = 0;
                 rt.set_capture_sink(&g->start_launches);

@@ -261,6 +261,7 @@ public:
         if (d_.ok && dia_fits(x, y)) return dia_spmm(d_.dev, x, y, &dot);
         return sell_spmm(s_.dev, x, y, &dot);
     }
+    bool has_masked_dot() const override { return true; }
 
 private:
     // DIA needs 16-byte aligned row pairs; odd leading dimensions take the SELL copy
@@ -392,6 +393,7 @@ public:
     int apply_dot(const DMat& x, const DMat& y, const SpmmDot& dot) const override {
         return sell_spmm(with_halo(x), x, y, &dot);
     }
+    bool has_masked_dot() const override { return true; }
     bool capturable() const override { return false; }
 
 private:
@@ -511,6 +513,7 @@ public:
     int apply_dot(const DMat& x, const DMat& y, const SpmmDot& dot) const override {
         return stencil_spmm(with_halo(x), x, y, &dot);
     }
+    bool has_masked_dot() const override { return true; }
     bool capturable() const override { return !partitioned_; }
 
 private:

@@ -26,6 +26,9 @@ public:
         (void)x; (void)y; (void)dot;
         return 0;
     }
+    // apply_dot honours the column mask (converged CG columns cost nothing): unrolled CG graphs
+    // are only worth it then -- otherwise every idle iteration would still pay a full apply.
+    virtual bool has_masked_dot() const { return false; }
 
 private:
     int64_t n_;
