@@ -646,6 +646,446 @@ __global__ void __launch_bounds__(kRows) k_dia(DiaDev a, const double* __restric
     tm.stop();
 }
 
+// DIA SpMM, one row per thread and no branches in the column loop: an absent entry reads x(i)
+// (always in range, an L1 hit) with a zero coefficient, so every load is issued up front and
+// warps never diverge.  32-bit row indices (n < 2^31); the column base stays 64-bit.
+// Present entries are summed in CSR column order; absent ones add an exact +0.
+template <int CB, bool DOT, int ND, bool TWO_PHASE, bool VAR>
+__global__ void __launch_bounds__(kRows) k_dia_row(DiaDev a, const double* __restrict__ x, int64_t ldx,
+                                                    double* __restrict__ y, int64_t ldy, int ncols, KTimer tm,
+                                                    DotOut dots) {
+    tm.start();
+    tm.columns(DOT ? dots.active : nullptr, 0, 0, ncols);
+    const int j0 = blockIdx.y * CB;
+    double d[CB];
+#pragma unroll
+    for (int c = 0; c < CB; ++c) d[c] = 0.0;
+    bool on[CB];
+    const bool any = group_columns<CB, DOT>(dots, j0, ncols, on);
+    const int n = static_cast<int>(a.n);
+    const int stride = static_cast<int>(gridDim.x) * kRows;
+    // column bases hoisted out of the row loop: each x load is then one 32-bit-index IMAD.WIDE
+    const double* xcol[CB];
+    double* ycol[CB];
+#pragma unroll
+    for (int c = 0; c < CB; ++c) {
+        xcol[c] = x + static_cast<int64_t>(j0 + c) * ldx;
+        ycol[c] = y + static_cast<int64_t>(j0 + c) * ldy;
+        // opaque to the optimiser, which otherwise re-derives (j0 + c) * ld + jj in 64 bits per load
+        asm volatile("mov.b64 %0, %0;" : "+l"(xcol[c]));
+        asm volatile("mov.b64 %0, %0;" : "+l"(ycol[c]));
+    }
+    for (int i = any ? static_cast<int>(blockIdx.x) * kRows + threadIdx.x : n; i < n; i += stride) {
+        const unsigned mk = __ldg(a.mask + i);
+        int jj[ND];
+        double v[ND];
+#pragma unroll
+        for (int k = 0; k < ND; ++k) {
+            const bool p = (mk >> k) & 1u;
+            jj[k] = p ? i + static_cast<int>(a.off[k]) : i;
+            // VAR = false: every diagonal constant (no per-row coefficient loads at all)
+            const int vi = VAR ? a.vidx[k] : -1;
+            const double w = vi < 0 ? a.cval[k] : __ldg(a.val + static_cast<int64_t>(vi) * n + i);
+            v[k] = p ? w : 0.0;
+        }
+        if (TWO_PHASE) {
+            // every column's loads issued before any is consumed: CB x ND loads in flight per thread
+            double xv[CB][ND], xs[CB];
+#pragma unroll
+            for (int c = 0; c < CB; ++c) {
+                if (!on[c]) continue;
+#pragma unroll
+                for (int k = 0; k < ND; ++k) xv[c][k] = __ldg(xcol[c] + jj[k]);
+                if (DOT) xs[c] = __ldg(xcol[c] + i);
+            }
+#pragma unroll
+            for (int c = 0; c < CB; ++c) {
+                if (!on[c]) continue;
+                double acc = 0.0;
+#pragma unroll
+                for (int k = 0; k < ND; ++k) acc = fma(v[k], xv[c][k], acc);
+                __stcg(ycol[c] + i, acc);
+                if (DOT) d[c] = fma(xs[c], acc, d[c]);
+            }
+        } else {
+#pragma unroll
+            for (int c = 0; c < CB; ++c) {
+                if (!on[c]) continue;
+                const double* xc = xcol[c];
+                double acc = 0.0;
+#pragma unroll
+                for (int k = 0; k < ND; ++k) acc = fma(v[k], __ldg(xc + jj[k]), acc);
+                __stcg(ycol[c] + i, acc);
+                if (DOT) d[c] = fma(__ldg(xc + i), acc, d[c]);
+            }
+        }
+    }
+    if (DOT) {
+        block_dots_out<CB>(d, dots.parts, j0, ncols);
+        fold_dots_last_block(dots.parts, ncols, dots.ticket, dots.out);
+    }
+    tm.stop();
+}
+
+// DIA SpMM on row pairs (i, i+1), i even, with 16-byte x loads: an even offset o reads the
+// aligned pair x(i+o), x(i+o+1) once for both rows; an odd one reads the pair at i+o-1 (row i
+// takes .y) and one 8-byte x(i+o+1) for row i+1.  Absent entries get a zero coefficient and
+// an in-range address (the row pair itself), so there are no divergent branches; the offset
+// parity tests are warp-uniform.  TWO_PHASE issues every column's loads before the FMAs.
+template <int CB, bool DOT, int ND, bool TWO_PHASE, bool VAR>
+__global__ void __launch_bounds__(kRows) k_dia_pair(DiaDev a, const double* __restrict__ x, int64_t ldx,
+                                                     double* __restrict__ y, int64_t ldy, int ncols, KTimer tm,
+                                                     DotOut dots) {
+    tm.start();
+    tm.columns(DOT ? dots.active : nullptr, 0, 0, ncols);
+    const int j0 = blockIdx.y * CB;
+    double d[CB];
+#pragma unroll
+    for (int c = 0; c < CB; ++c) d[c] = 0.0;
+    bool on[CB];
+    const bool any = group_columns<CB, DOT>(dots, j0, ncols, on);
+    const int n = static_cast<int>(a.n), npairs = n >> 1;
+    const int stride = static_cast<int>(gridDim.x) * kRows;
+    const double* xcol[CB];
+    double* ycol[CB];
+#pragma unroll
+    for (int c = 0; c < CB; ++c) {
+        xcol[c] = x + static_cast<int64_t>(j0 + c) * ldx;
+        ycol[c] = y + static_cast<int64_t>(j0 + c) * ldy;
+        asm volatile("mov.b64 %0, %0;" : "+l"(xcol[c]));
+        asm volatile("mov.b64 %0, %0;" : "+l"(ycol[c]));
+    }
+    for (int pr = any ? static_cast<int>(blockIdx.x) * kRows + threadIdx.x : npairs; pr < npairs; pr += stride) {
+        const int i = 2 * pr;
+        const unsigned mk = __ldg(reinterpret_cast<const unsigned*>(a.mask + i));  // row i low, i+1 high
+        int ja[ND], jb[ND];
+        double v0[ND], v1[ND];
+#pragma unroll
+        for (int k = 0; k < ND; ++k) {
+            const bool p0 = (mk >> k) & 1u, p1 = (mk >> (16 + k)) & 1u;
+            const int o = static_cast<int>(a.off[k]);
+            double c0 = a.cval[k], c1 = a.cval[k];
+            if (VAR && a.vidx[k] >= 0) {
+                const double2 t = __ldg(reinterpret_cast<const double2*>(a.val + static_cast<int64_t>(a.vidx[k]) * n + i));
+                c0 = t.x;
+                c1 = t.y;
+            }
+            v0[k] = p0 ? c0 : 0.0;
+            v1[k] = p1 ? c1 : 0.0;
+            if ((o & 1) == 0) {
+                ja[k] = (p0 || p1) ? i + o : i;
+                jb[k] = 0;
+            } else {
+                ja[k] = p0 ? i + o - 1 : i;
+                jb[k] = p1 ? i + o + 1 : i;
+            }
+        }
+        auto column = [&](int c, const double2 (&t)[ND], const double (&u)[ND]) {
+            double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+            for (int k = 0; k < ND; ++k) {
+                const bool odd = a.off[k] & 1;
+                acc0 = fma(v0[k], odd ? t[k].y : t[k].x, acc0);
+                acc1 = fma(v1[k], odd ? u[k] : t[k].y, acc1);
+            }
+            __stcg(reinterpret_cast<double2*>(ycol[c] + i), make_double2(acc0, acc1));
+            return make_double2(acc0, acc1);
+        };
+        auto load = [&](int c, double2 (&t)[ND], double (&u)[ND]) {
+            const double* xc = xcol[c];
+#pragma unroll
+            for (int k = 0; k < ND; ++k) {
+                t[k] = __ldg(reinterpret_cast<const double2*>(xc + ja[k]));
+                u[k] = (a.off[k] & 1) ? __ldg(xc + jb[k]) : 0.0;
+            }
+        };
+        if (TWO_PHASE) {
+            double2 t[CB][ND], xs[CB];
+            double u[CB][ND];
+#pragma unroll
+            for (int c = 0; c < CB; ++c) {
+                if (!on[c]) continue;
+                load(c, t[c], u[c]);
+                if (DOT) xs[c] = __ldg(reinterpret_cast<const double2*>(xcol[c] + i));
+            }
+#pragma unroll
+            for (int c = 0; c < CB; ++c) {
+                if (!on[c]) continue;
+                const double2 r = column(c, t[c], u[c]);
+                if (DOT) d[c] = fma(xs[c].x, r.x, fma(xs[c].y, r.y, d[c]));
+            }
+        } else {
+#pragma unroll
+            for (int c = 0; c < CB; ++c) {
+                if (!on[c]) continue;
+                double2 t[ND];
+                double u[ND];
+                load(c, t, u);
+                const double2 r = column(c, t, u);
+                if (DOT) {
+                    const double2 xs = __ldg(reinterpret_cast<const double2*>(xcol[c] + i));
+                    d[c] = fma(xs.x, r.x, fma(xs.y, r.y, d[c]));
+                }
+            }
+        }
+    }
+    if (DOT) {
+        block_dots_out<CB>(d, dots.parts, j0, ncols);
+        fold_dots_last_block(dots.parts, ncols, dots.ticket, dots.out);
+    }
+    tm.stop();
+}
+
+// DIA SpMM for the banded "stencil-like" layout: ND odd, offsets [.., -1, 0, 1, ..] with every
+// other offset even.  A row pair (i, i+1) then needs exactly ND aligned 16-byte x loads:
+// P(i + o) for each even o != 0, and P(i - 2), P(i), P(i + 2) for the -1/0/+1 triple (row i
+// takes x(i-1) = P(i-2).y, row i+1 takes x(i+2) = P(i+2).x).  Pair addresses are clamped into
+// the vector, absent entries get a zero coefficient (presence mask), so the loop is free of
+// divergent branches.  Entries are summed in ascending offset order (CSR column order).
+template <int CB, bool DOT, int ND, bool VAR>
+__global__ void __launch_bounds__(kRows) k_dia_sym(DiaDev a, const double* __restrict__ x, int64_t ldx,
+                                                    double* __restrict__ y, int64_t ldy, int ncols, KTimer tm,
+                                                    DotOut dots) {
+    constexpr int kC = ND / 2;  // index of the zero offset
+    tm.start();
+    tm.columns(DOT ? dots.active : nullptr, 0, 0, ncols);
+    const int j0 = blockIdx.y * CB;
+    double d[CB];
+#pragma unroll
+    for (int c = 0; c < CB; ++c) d[c] = 0.0;
+    bool on[CB];
+    const bool any = group_columns<CB, DOT>(dots, j0, ncols, on);
+    const int n = static_cast<int>(a.n), npairs = n >> 1;
+    const int stride = static_cast<int>(gridDim.x) * kRows;
+    const double* xcol[CB];
+    double* ycol[CB];
+#pragma unroll
+    for (int c = 0; c < CB; ++c) {
+        xcol[c] = x + static_cast<int64_t>(j0 + c) * ldx;
+        ycol[c] = y + static_cast<int64_t>(j0 + c) * ldy;
+        asm volatile("mov.b64 %0, %0;" : "+l"(xcol[c]));
+        asm volatile("mov.b64 %0, %0;" : "+l"(ycol[c]));
+    }
+    for (int pr = any ? static_cast<int>(blockIdx.x) * kRows + threadIdx.x : npairs; pr < npairs; pr += stride) {
+        const int i = 2 * pr;
+        const unsigned mk = __ldg(reinterpret_cast<const unsigned*>(a.mask + i));  // row i low, i+1 high
+        int e[ND];  // pair start of slot k (slot kC-1: P(i-2), kC: P(i), kC+1: P(i+2))
+        double v0[ND], v1[ND];
+#pragma unroll
+        for (int k = 0; k < ND; ++k) {
+            const int o = k == kC - 1 ? -2 : k == kC + 1 ? 2 : static_cast<int>(a.off[k]);
+            e[k] = min(max(i + o, 0), n - 2);
+            double c0 = a.cval[k], c1 = a.cval[k];
+            if (VAR && a.vidx[k] >= 0) {
+                const double2 t = __ldg(reinterpret_cast<const double2*>(a.val + static_cast<int64_t>(a.vidx[k]) * n + i));
+                c0 = t.x;
+                c1 = t.y;
+            }
+            v0[k] = ((mk >> k) & 1u) ? c0 : 0.0;
+            v1[k] = ((mk >> (16 + k)) & 1u) ? c1 : 0.0;
+        }
+#pragma unroll
+        for (int c = 0; c < CB; ++c) {
+            if (!on[c]) continue;
+            const double* xc = xcol[c];
+            double2 t[ND];
+#pragma unroll
+            for (int k = 0; k < ND; ++k) t[k] = __ldg(reinterpret_cast<const double2*>(xc + e[k]));
+            double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+            for (int k = 0; k < ND; ++k) {
+                // row i: x(i + o_k); row i+1: x(i + 1 + o_k)
+                const double a0 = k == kC - 1 ? t[k].y : k == kC + 1 ? t[kC].y : t[k].x;
+                const double a1 = k == kC - 1 ? t[kC].x : k == kC + 1 ? t[k].x : t[k].y;
+                acc0 = fma(v0[k], a0, acc0);
+                acc1 = fma(v1[k], a1, acc1);
+            }
+            __stcg(reinterpret_cast<double2*>(ycol[c] + i), make_double2(acc0, acc1));
+            if (DOT) d[c] = fma(t[kC].x, acc0, fma(t[kC].y, acc1, d[c]));
+        }
+    }
+    if (DOT) {
+        block_dots_out<CB>(d, dots.parts, j0, ncols);
+        fold_dots_last_block(dots.parts, ncols, dots.ticket, dots.out);
+    }
+    tm.stop();
+}
+
+// ---- DIA SpMM with bulk-async (TMA 1-D) staging of x -------------------------------------
+// Offsets are grouped into windows (runs of diagonals closer than kWinGap).  For a tile of kRows
+// rows starting at i0 (even), window w needs x rows [i0 + lo_w, i0 + kRows - 1 + hi_w]; one
+// cp.async.bulk per (column, window) lands them in shared memory, double-buffered against the
+// compute of the previous tile, so a thread's loads are shared-memory reads and the DRAM
+// stream is kept busy by the copy engine instead of by registers.
+struct DiaWin {
+    int nwin = 0;
+    int s = 0;                // doubles per column per stage
+    int lo[kDiaMax] = {};     // window start offset rounded down to even
+    int len[kDiaMax] = {};    // doubles staged per window (even)
+    int base[kDiaMax] = {};   // window start in the column's stage slice
+    int sidx[kDiaMax] = {};   // per diagonal: smem index of x(i0 + off_k) minus 0 (add t)
+    int sctr = -1;            // smem index of x(i0) when a window covers offset 0, else -1
+};
+
+constexpr int kWinGap = 512;
+
+bool dia_windows(const DiaDev& a, DiaWin& w) {
+    w = DiaWin{};
+    int k = 0;
+    while (k < a.ndiag) {
+        int e = k;
+        while (e + 1 < a.ndiag && a.off[e + 1] - a.off[e] <= kWinGap) ++e;
+        if (a.off[e] - a.off[k] > (int64_t(1) << 20)) return false;
+        const int lo = static_cast<int>(a.off[k]), hi = static_cast<int>(a.off[e]);
+        const int lo2 = lo & ~1;
+        int len = kRows + (hi - lo2) + 2;
+        len += len & 1;
+        const int wi = w.nwin++;
+        w.lo[wi] = lo2;
+        w.len[wi] = len;
+        w.base[wi] = w.s;
+        for (int q = k; q <= e; ++q) w.sidx[q] = w.s + static_cast<int>(a.off[q]) - lo2;
+        if (lo <= 0 && 0 <= hi) w.sctr = w.s - lo2;
+        w.s += len;
+        k = e + 1;
+    }
+    return true;
+}
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned cnt) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(cnt));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* b) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(b))
+        : "memory");
+}
+
+template <int CB>
+__device__ __forceinline__ void dia_stage_issue(const DiaWin& w, const double* const (&xcol)[CB], const bool (&on)[CB],
+                                                int64_t n, int64_t i0, double* stage, unsigned long long* bar) {
+    unsigned tx = 0;
+    int64_t g0s[kDiaMax], cnts[kDiaMax];
+    for (int q = 0; q < w.nwin; ++q) {
+        const int64_t b = i0 + w.lo[q];
+        const int64_t g0 = b < 0 ? 0 : b;
+        const int64_t g1 = min(b + w.len[q], n);  // exclusive; even
+        g0s[q] = g0;
+        cnts[q] = g1 > g0 ? g1 - g0 : 0;
+    }
+    int act = 0;
+#pragma unroll
+    for (int c = 0; c < CB; ++c) act += on[c];
+    for (int q = 0; q < w.nwin; ++q) tx += static_cast<unsigned>(cnts[q] * 8) * act;
+    mbar_expect_tx(bar, tx);
+#pragma unroll
+    for (int c = 0; c < CB; ++c) {
+        if (!on[c]) continue;
+        for (int q = 0; q < w.nwin; ++q) {
+            if (cnts[q] == 0) continue;
+            const int64_t b = i0 + w.lo[q];
+            bulk_g2s(stage + c * w.s + w.base[q] + (g0s[q] - b), xcol[c] + g0s[q], static_cast<unsigned>(cnts[q] * 8), bar);
+        }
+    }
+}
+
+template <int CB, bool DOT, int ND>
+__global__ void __launch_bounds__(kRows) k_dia_tma(DiaDev a, DiaWin w, const double* __restrict__ x, int64_t ldx,
+                                                    double* __restrict__ y, int64_t ldy, int ncols, KTimer tm,
+                                                    DotOut dots) {
+    extern __shared__ __align__(128) double sm_dia[];
+    __shared__ __align__(8) unsigned long long bar[2];
+    tm.start();
+    tm.columns(DOT ? dots.active : nullptr, 0, 0, ncols);
+    const int j0 = blockIdx.y * CB;
+    double d[CB];
+#pragma unroll
+    for (int c = 0; c < CB; ++c) d[c] = 0.0;
+    bool on[CB];
+    const bool any = group_columns<CB, DOT>(dots, j0, ncols, on);
+    const int64_t n = a.n;
+    const int64_t ntiles = (n + kRows - 1) / kRows;
+    const int64_t mine = any && blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const double* xcol[CB];
+    double* ycol[CB];
+#pragma unroll
+    for (int c = 0; c < CB; ++c) {
+        xcol[c] = x + static_cast<int64_t>(j0 + c) * ldx;
+        ycol[c] = y + static_cast<int64_t>(j0 + c) * ldy;
+    }
+    const int stage_len = CB * w.s;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (int64_t k = 0; k < 2 && k < mine; ++k)
+            dia_stage_issue<CB>(w, xcol, on, n, (blockIdx.x + k * gridDim.x) * kRows, sm_dia + k * stage_len, &bar[k]);
+    double v[ND];
+    int sx[ND];
+#pragma unroll
+    for (int k = 0; k < ND; ++k) sx[k] = w.sidx[k] + threadIdx.x;
+    for (int64_t k = 0; k < mine; ++k) {
+        const int64_t i = (blockIdx.x + k * gridDim.x) * kRows + threadIdx.x;
+        const int st = static_cast<int>(k & 1);
+        unsigned mk = 0;
+        if (i < n) {
+            mk = __ldg(a.mask + i);
+#pragma unroll
+            for (int q = 0; q < ND; ++q) {
+                const int vi = a.vidx[q];
+                v[q] = vi < 0 ? a.cval[q] : __ldg(a.val + static_cast<int64_t>(vi) * n + i);
+            }
+        }
+        mbar_wait(&bar[st], static_cast<unsigned>((k >> 1) & 1));
+        if (i < n) {
+            const double* sb = sm_dia + st * stage_len;
+#pragma unroll
+            for (int c = 0; c < CB; ++c) {
+                if (!on[c]) continue;
+                const double* xs = sb + c * w.s;
+                double acc = 0.0;
+#pragma unroll
+                for (int q = 0; q < ND; ++q) {
+                    const double t = xs[sx[q]];
+                    acc = ((mk >> q) & 1u) ? fma(v[q], t, acc) : acc;
+                }
+                __stcg(ycol[c] + i, acc);
+                if (DOT) d[c] = fma(w.sctr >= 0 ? xs[w.sctr + threadIdx.x] : __ldg(xcol[c] + i), acc, d[c]);
+            }
+        }
+        __syncthreads();  // every thread is done with this stage before it is refilled
+        if (threadIdx.x == 0 && k + 2 < mine) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            dia_stage_issue<CB>(w, xcol, on, n, (blockIdx.x + (k + 2) * gridDim.x) * kRows, sm_dia + st * stage_len,
+                                &bar[st]);
+        }
+    }
+    if (DOT) {
+        block_dots_out<CB>(d, dots.parts, j0, ncols);
+        fold_dots_last_block(dots.parts, ncols, dots.ticket, dots.out);
+    }
+    tm.stop();
+}
+
 // Row-tile blocks per column group: one per tile, bounded with dots by the partials buffer
 // (ncols x blocks doubles); the last block folds them.
 unsigned row_blocks(int64_t n, const SpmmDot* dot, int ncols) {
@@ -942,9 +1382,109 @@ void launch_dia_nd(const DiaDev& a, const DMat& x, const DMat& y, const DotOut& 
     else k_dia<CB, false, ND, EXACT><<<grid, kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm, dd);
 }
 
+template <int CB, int ND>
+unsigned launch_dia_row(const DiaDev& a, const DMat& x, const DMat& y, const DotOut& dd, bool dot, dim3 grid, KTimer tm) {
+    Runtime& rt = Runtime::get();
+    const int ncols = static_cast<int>(x.cols);
+    static const bool two = std::getenv("BOSP_DIA_1PHASE") == nullptr;
+    static const bool rows = std::getenv("BOSP_DIA_PAIR") == nullptr;
+    bool var = false;
+    for (int k = 0; k < a.ndiag; ++k) var = var || a.vidx[k] >= 0;
+    auto go = [&](auto kern) { kern<<<grid, kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm, dd); };
+    bool sym = (ND & 1) && a.off[ND / 2] == 0 && a.off[ND / 2 - 1] == -1 && a.off[ND / 2 + 1] == 1;
+    for (int k = 0; k < ND; ++k)
+        if (k < ND / 2 - 1 || k > ND / 2 + 1) sym = sym && (a.off[k] & 1) == 0;
+    static const bool nosym = std::getenv("BOSP_DIA_NOSYM") != nullptr;
+    if (sym && !nosym) {
+        const dim3 g2(std::min<unsigned>(grid.x, row_blocks(a.n / 2, nullptr, ncols)), grid.y);
+        auto go2 = [&](auto kern) { kern<<<g2, kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm, dd); };
+        if (var) dot ? go2(k_dia_sym<CB, true, ND, true>) : go2(k_dia_sym<CB, false, ND, true>);
+        else dot ? go2(k_dia_sym<CB, true, ND, false>) : go2(k_dia_sym<CB, false, ND, false>);
+        return g2.x;
+    }
+    if (!rows) {
+        const dim3 g2(std::min<unsigned>(grid.x, row_blocks(a.n / 2, nullptr, ncols)), grid.y);
+        auto go2 = [&](auto kern) { kern<<<g2, kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm, dd); };
+        if (two) {
+            if (var) dot ? go2(k_dia_pair<CB, true, ND, true, true>) : go2(k_dia_pair<CB, false, ND, true, true>);
+            else dot ? go2(k_dia_pair<CB, true, ND, true, false>) : go2(k_dia_pair<CB, false, ND, true, false>);
+        } else {
+            if (var) dot ? go2(k_dia_pair<CB, true, ND, false, true>) : go2(k_dia_pair<CB, false, ND, false, true>);
+            else dot ? go2(k_dia_pair<CB, true, ND, false, false>) : go2(k_dia_pair<CB, false, ND, false, false>);
+        }
+        return g2.x;
+    }
+    if (two) {
+        if (var) dot ? go(k_dia_row<CB, true, ND, true, true>) : go(k_dia_row<CB, false, ND, true, true>);
+        else dot ? go(k_dia_row<CB, true, ND, true, false>) : go(k_dia_row<CB, false, ND, true, false>);
+    } else {
+        if (var) dot ? go(k_dia_row<CB, true, ND, false, true>) : go(k_dia_row<CB, false, ND, false, true>);
+        else dot ? go(k_dia_row<CB, true, ND, false, false>) : go(k_dia_row<CB, false, ND, false, false>);
+    }
+    return grid.x;
+}
+
+template <int CB, int ND>
+unsigned launch_dia_tma(const DiaDev& a, const DiaWin& w, const DMat& x, const DMat& y, const SpmmDot* dot, KTimer tm) {
+    Runtime& rt = Runtime::get();
+    const int ncols = static_cast<int>(x.cols);
+    const size_t smem = sizeof(double) * 2 * CB * static_cast<size_t>(w.s);
+    auto kern = dot ? k_dia_tma<CB, true, ND> : k_dia_tma<CB, false, ND>;
+    static int configured[2] = {0, 0};
+    static int resident[2] = {0, 0};
+    const int di = dot ? 1 : 0;
+    if (configured[di] < static_cast<int>(smem)) {
+        BOSP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        BOSP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident[di], kern, kRows, smem));
+        configured[di] = static_cast<int>(smem);
+    }
+    const int groups = (ncols + CB - 1) / CB;
+    const int64_t slots = static_cast<int64_t>(std::max(resident[di], 1)) * rt.sm_count();
+    const unsigned gx = std::min<unsigned>(row_blocks(a.n, dot, ncols),
+                                           static_cast<unsigned>(std::max<int64_t>(1, slots / groups)));
+    const DotOut dd = dot ? DotOut{dot->parts, dot->ticket, dot->out, dot->active} : DotOut{};
+    kern<<<dim3(gx, groups), kRows, smem, rt.stream()>>>(a, w, x.p, x.ld, y.p, y.ld, ncols, tm, dd);
+    BOSP_LAUNCH_CHECK();
+    return gx;
+}
+
 template <int CB>
 unsigned launch_dia(const DiaDev& a, const DMat& x, const DMat& y, const SpmmDot* dot, KTimer tm) {
     const int ncols = static_cast<int>(x.cols);
+    static const int tma = std::getenv("BOSP_DIA_TMA") ? std::atoi(std::getenv("BOSP_DIA_TMA")) : 0;
+    DiaWin w;
+    if (tma && (reinterpret_cast<uintptr_t>(x.p) & 15) == 0 && a.n >= kRows && dia_windows(a, w) &&
+        sizeof(double) * 2 * CB * static_cast<size_t>(w.s) <= 110 * 1024) {
+        switch (a.ndiag) {
+            case 3: return launch_dia_tma<CB, 3>(a, w, x, y, dot, tm);
+            case 5: return launch_dia_tma<CB, 5>(a, w, x, y, dot, tm);
+            case 7: return launch_dia_tma<CB, 7>(a, w, x, y, dot, tm);
+            case 9: return launch_dia_tma<CB, 9>(a, w, x, y, dot, tm);
+            default: break;
+        }
+    }
+    static const bool pairs = std::getenv("BOSP_DIA_PAIRS") != nullptr;
+    if (!pairs && a.n < (int64_t(1) << 31) && (a.ndiag == 3 || a.ndiag == 5 || a.ndiag == 7 || a.ndiag == 9)) {
+        // a few rows per thread: the per-block prologue/epilogue (column mask, timer, dot
+        // reduction) is then amortised; ~kDiaWaves resident waves over all column groups
+        static const int waves = std::getenv("BOSP_DIA_WAVES") ? std::atoi(std::getenv("BOSP_DIA_WAVES")) : 8;
+        const int groups = (ncols + CB - 1) / CB;
+        const unsigned cap = static_cast<unsigned>(
+            std::max<int64_t>(1, (static_cast<int64_t>(waves) * Runtime::get().sm_count() + groups - 1) / groups));
+        const unsigned gx = waves > 0 ? std::min(row_blocks(a.n, dot, ncols), cap) : row_blocks(a.n, dot, ncols);
+        const dim3 grid(gx, (ncols + CB - 1) / CB);
+        const DotOut dd = dot ? DotOut{dot->parts, dot->ticket, dot->out, dot->active} : DotOut{};
+        const bool d = dot != nullptr;
+        unsigned used = gx;
+        switch (a.ndiag) {
+            case 3: used = launch_dia_row<CB, 3>(a, x, y, dd, d, grid, tm); break;
+            case 5: used = launch_dia_row<CB, 5>(a, x, y, dd, d, grid, tm); break;
+            case 7: used = launch_dia_row<CB, 7>(a, x, y, dd, d, grid, tm); break;
+            default: used = launch_dia_row<CB, 9>(a, x, y, dd, d, grid, tm); break;
+        }
+        BOSP_LAUNCH_CHECK();
+        return used;
+    }
     const unsigned gx = row_blocks(a.n / 2, dot, ncols);
     const dim3 grid(gx, (ncols + CB - 1) / CB);
     const DotOut dd = dot ? DotOut{dot->parts, dot->ticket, dot->out, dot->active} : DotOut{};
