@@ -870,19 +870,24 @@ __global__ void __launch_bounds__(kRows) k_dia_sym(DiaDev a, const double* __res
         const int i = 2 * pr;
         const unsigned mk = __ldg(reinterpret_cast<const unsigned*>(a.mask + i));  // row i low, i+1 high
         int e[ND];  // pair start of slot k (slot kC-1: P(i-2), kC: P(i), kC+1: P(i+2))
-        double v0[ND], v1[ND];
+        // VAR: per-row coefficients (zeroed where absent); constant diagonals instead keep the
+        // coefficient in the constant bank and predicate the FMA on the presence bit
+        double v0[VAR ? ND : 1], v1[VAR ? ND : 1];
 #pragma unroll
         for (int k = 0; k < ND; ++k) {
             const int o = k == kC - 1 ? -2 : k == kC + 1 ? 2 : static_cast<int>(a.off[k]);
             e[k] = min(max(i + o, 0), n - 2);
-            double c0 = a.cval[k], c1 = a.cval[k];
-            if (VAR && a.vidx[k] >= 0) {
-                const double2 t = __ldg(reinterpret_cast<const double2*>(a.val + static_cast<int64_t>(a.vidx[k]) * n + i));
-                c0 = t.x;
-                c1 = t.y;
+            if (VAR) {
+                double c0 = a.cval[k], c1 = a.cval[k];
+                if (a.vidx[k] >= 0) {
+                    const double2 t =
+                        __ldg(reinterpret_cast<const double2*>(a.val + static_cast<int64_t>(a.vidx[k]) * n + i));
+                    c0 = t.x;
+                    c1 = t.y;
+                }
+                v0[VAR ? k : 0] = ((mk >> k) & 1u) ? c0 : 0.0;
+                v1[VAR ? k : 0] = ((mk >> (16 + k)) & 1u) ? c1 : 0.0;
             }
-            v0[k] = ((mk >> k) & 1u) ? c0 : 0.0;
-            v1[k] = ((mk >> (16 + k)) & 1u) ? c1 : 0.0;
         }
 #pragma unroll
         for (int c = 0; c < CB; ++c) {
@@ -897,8 +902,13 @@ __global__ void __launch_bounds__(kRows) k_dia_sym(DiaDev a, const double* __res
                 // row i: x(i + o_k); row i+1: x(i + 1 + o_k)
                 const double a0 = k == kC - 1 ? t[k].y : k == kC + 1 ? t[kC].y : t[k].x;
                 const double a1 = k == kC - 1 ? t[kC].x : k == kC + 1 ? t[k].x : t[k].y;
-                acc0 = fma(v0[k], a0, acc0);
-                acc1 = fma(v1[k], a1, acc1);
+                if (VAR) {
+                    acc0 = fma(v0[VAR ? k : 0], a0, acc0);
+                    acc1 = fma(v1[VAR ? k : 0], a1, acc1);
+                } else {
+                    acc0 = ((mk >> k) & 1u) ? fma(a.cval[k], a0, acc0) : acc0;
+                    acc1 = ((mk >> (16 + k)) & 1u) ? fma(a.cval[k], a1, acc1) : acc1;
+                }
             }
             __stcg(reinterpret_cast<double2*>(ycol[c] + i), make_double2(acc0, acc1));
             if (DOT) d[c] = fma(t[kC].x, acc0, fma(t[kC].y, acc1, d[c]));

@@ -6,6 +6,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "dense_ops.hpp"
 #include "runtime.hpp"
@@ -135,7 +136,8 @@ template <int K, class F>
 void launch_colred(const char* family, int64_t n, int ncols, const F& f, double bytes) {
     if (ncols <= 0) return;
     Runtime& rt = Runtime::get();
-    const int64_t target = 4LL * rt.sm_count();  // 2..16 waves measured within 3% on config 2
+    static const int64_t waves = std::getenv("BOSP_COLRED_WAVES") ? std::atoll(std::getenv("BOSP_COLRED_WAVES")) : 4;
+    const int64_t target = waves * rt.sm_count();  // 2..16 waves measured within 3% on config 2
     int nchunks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n + 4095) / 4096,
                                                                             (target + ncols - 1) / ncols)));
     const int64_t chunk = ((n + nchunks - 1) / nchunks + 1) & ~int64_t(1);  // even: pairs stay aligned
