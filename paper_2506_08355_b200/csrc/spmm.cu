@@ -842,7 +842,8 @@ __global__ void __launch_bounds__(kRows) k_dia_pair(DiaDev a, const double* __re
 // takes x(i-1) = P(i-2).y, row i+1 takes x(i+2) = P(i+2).x).  Pair addresses are clamped into
 // the vector, absent entries get a zero coefficient (presence mask), so the loop is free of
 // divergent branches.  Entries are summed in ascending offset order (CSR column order).
-template <int CB, bool DOT, int ND, bool VAR>
+// VAR: 0 every diagonal constant, 1 only the zero-offset diagonal varies, 2 any may vary
+template <int CB, bool DOT, int ND, int VAR>
 __global__ void __launch_bounds__(kRows) k_dia_sym(DiaDev a, const double* __restrict__ x, int64_t ldx,
                                                     double* __restrict__ y, int64_t ldy, int ncols, KTimer tm,
                                                     DotOut dots) {
@@ -870,14 +871,21 @@ __global__ void __launch_bounds__(kRows) k_dia_sym(DiaDev a, const double* __res
         const int i = 2 * pr;
         const unsigned mk = __ldg(reinterpret_cast<const unsigned*>(a.mask + i));  // row i low, i+1 high
         int e[ND];  // pair start of slot k (slot kC-1: P(i-2), kC: P(i), kC+1: P(i+2))
-        // VAR: per-row coefficients (zeroed where absent); constant diagonals instead keep the
-        // coefficient in the constant bank and predicate the FMA on the presence bit
-        double v0[VAR ? ND : 1], v1[VAR ? ND : 1];
+        // VAR == 2: per-row coefficients (zeroed where absent).  Otherwise constant diagonals
+        // keep their coefficient in the constant bank and predicate the FMA on the presence bit;
+        // with VAR == 1 the zero-offset diagonal is one 16-byte load per pair.
+        double v0[VAR == 2 ? ND : 1], v1[VAR == 2 ? ND : 1];
+        double2 vc = make_double2(0.0, 0.0);
+        if (VAR == 1) {
+            vc = __ldg(reinterpret_cast<const double2*>(a.val + static_cast<int64_t>(a.vidx[kC]) * n + i));
+            vc.x = ((mk >> kC) & 1u) ? vc.x : 0.0;
+            vc.y = ((mk >> (16 + kC)) & 1u) ? vc.y : 0.0;
+        }
 #pragma unroll
         for (int k = 0; k < ND; ++k) {
             const int o = k == kC - 1 ? -2 : k == kC + 1 ? 2 : static_cast<int>(a.off[k]);
             e[k] = min(max(i + o, 0), n - 2);
-            if (VAR) {
+            if (VAR == 2) {
                 double c0 = a.cval[k], c1 = a.cval[k];
                 if (a.vidx[k] >= 0) {
                     const double2 t =
@@ -885,8 +893,8 @@ __global__ void __launch_bounds__(kRows) k_dia_sym(DiaDev a, const double* __res
                     c0 = t.x;
                     c1 = t.y;
                 }
-                v0[VAR ? k : 0] = ((mk >> k) & 1u) ? c0 : 0.0;
-                v1[VAR ? k : 0] = ((mk >> (16 + k)) & 1u) ? c1 : 0.0;
+                v0[VAR == 2 ? k : 0] = ((mk >> k) & 1u) ? c0 : 0.0;
+                v1[VAR == 2 ? k : 0] = ((mk >> (16 + k)) & 1u) ? c1 : 0.0;
             }
         }
 #pragma unroll
@@ -902,9 +910,12 @@ __global__ void __launch_bounds__(kRows) k_dia_sym(DiaDev a, const double* __res
                 // row i: x(i + o_k); row i+1: x(i + 1 + o_k)
                 const double a0 = k == kC - 1 ? t[k].y : k == kC + 1 ? t[kC].y : t[k].x;
                 const double a1 = k == kC - 1 ? t[kC].x : k == kC + 1 ? t[k].x : t[k].y;
-                if (VAR) {
-                    acc0 = fma(v0[VAR ? k : 0], a0, acc0);
-                    acc1 = fma(v1[VAR ? k : 0], a1, acc1);
+                if (VAR == 2) {
+                    acc0 = fma(v0[VAR == 2 ? k : 0], a0, acc0);
+                    acc1 = fma(v1[VAR == 2 ? k : 0], a1, acc1);
+                } else if (VAR == 1 && k == kC) {
+                    acc0 = fma(vc.x, a0, acc0);
+                    acc1 = fma(vc.y, a1, acc1);
                 } else {
                     acc0 = ((mk >> k) & 1u) ? fma(a.cval[k], a0, acc0) : acc0;
                     acc1 = ((mk >> (16 + k)) & 1u) ? fma(a.cval[k], a1, acc1) : acc1;
@@ -1408,8 +1419,11 @@ unsigned launch_dia_row(const DiaDev& a, const DMat& x, const DMat& y, const Dot
     if (sym && !nosym) {
         const dim3 g2(std::min<unsigned>(grid.x, row_blocks(a.n / 2, nullptr, ncols)), grid.y);
         auto go2 = [&](auto kern) { kern<<<g2, kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm, dd); };
-        if (var) dot ? go2(k_dia_sym<CB, true, ND, true>) : go2(k_dia_sym<CB, false, ND, true>);
-        else dot ? go2(k_dia_sym<CB, true, ND, false>) : go2(k_dia_sym<CB, false, ND, false>);
+        int nvar = 0;
+        for (int k = 0; k < ND; ++k) nvar += a.vidx[k] >= 0;
+        if (nvar == 0) dot ? go2(k_dia_sym<CB, true, ND, 0>) : go2(k_dia_sym<CB, false, ND, 0>);
+        else if (nvar == 1 && a.vidx[ND / 2] >= 0) dot ? go2(k_dia_sym<CB, true, ND, 1>) : go2(k_dia_sym<CB, false, ND, 1>);
+        else dot ? go2(k_dia_sym<CB, true, ND, 2>) : go2(k_dia_sym<CB, false, ND, 2>);
         return g2.x;
     }
     if (!rows) {

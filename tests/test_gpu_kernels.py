@@ -234,7 +234,7 @@ def test_shape_errors_map_to_contract_violation():
         op.apply(np.ones((5, 1)))
 
 
-@pytest.mark.parametrize("case", ["stencil_csr", "banded_varying", "holes", "sym_holes", "tridiag_holes", "wide_band"])
+@pytest.mark.parametrize("case", ["stencil_csr", "banded_varying", "holes", "sym_holes", "tridiag_holes", "sym_const", "wide_band"])
 def test_csr_storage_formats_apply(case):
     """Banded CSR goes to DIA (constant diagonals + presence mask), everything else to SELL-32;
     both must reproduce the CSR products (scipy) to rounding."""
@@ -254,11 +254,14 @@ def test_csr_storage_formats_apply(case):
             a[i, i + 1] = 0.0
         a = a.tocsr()
         a.eliminate_zeros()
-    elif case in ("sym_holes", "tridiag_holes"):
-        # the banded pair kernel's layout: offsets (.., -1, 0, 1, ..) with the others even
+    elif case in ("sym_holes", "tridiag_holes", "sym_const"):
+        # the banded pair kernel's layout: offsets (.., -1, 0, 1, ..) with the others even;
+        # sym_const: every diagonal constant (coefficients from the constant bank)
         n = 4096
         offs = [-1, 0, 1] if case == "tridiag_holes" else [-512, -10, -1, 0, 1, 10, 512]
-        a = sp.diags([rng.standard_normal(n - abs(o)) for o in offs], offs, shape=(n, n), format="lil")
+        vals = ([np.full(n - abs(o), 0.5 + k) for k, o in enumerate(offs)] if case == "sym_const"
+                else [rng.standard_normal(n - abs(o)) for o in offs])
+        a = sp.diags(vals, offs, shape=(n, n), format="lil")
         for i in rng.integers(0, n - 12, 300):
             a[i, i + 1] = 0.0
             a[i + 11, i + 1] = 0.0
