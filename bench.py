@@ -305,6 +305,8 @@ def run_b200(args, world, rank, local, dist):
                     "avg_launch_us": ms_k * 1e3 / launches_k,
                     "algorithmic_bytes_per_launch": bytes_k / launches_k,
                     "share_of_step": ms_k / (sum(dev_s) * 1e3),
+                    "bytes_note": "CSR-equivalent algorithmic bytes (SURVEY 8d: 12 nnz + 4(n+1) + 16 n m_active); "
+                                  "the DIA form stored for config 2 moves 16 n m + 10 n, see DESIGN.md section 6",
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if "_fallback" not in peaks
                     else "fallback 6650 GB/s (B200_PROFILING.md)"}
 
