@@ -727,8 +727,6 @@ void launch_product(const ProductJob* jobs, int njobs, int64_t n) {
 // double-buffering the next A tile with cp.async while the DMMA pipe works on the current one.
 // BN is b rounded up to 8 so no tensor work is spent on padding columns.
 // ------------------------------------------------------------------------------------------
-constexpr int kSkBM = 128;
-constexpr int kSkLdM = kSkBM + 4;
 
 struct SkinnyParams {
     ProductJob job[4];
@@ -738,9 +736,10 @@ struct SkinnyParams {
     int ldc;    // smem ld of C (== 4 mod 16)
 };
 
-template <int BN>
+template <int BN, int RT>
 __global__ void __launch_bounds__(256) k_product_skinny(SkinnyParams prm) {
     constexpr int NT = BN / 8;
+    constexpr int kSkBM = 64 * RT, kSkLdM = kSkBM + 4;  // rows per tile: 8 warps x RT m-tiles
     extern __shared__ __align__(16) double smem[];
     const int kp = prm.kp, ldc = prm.ldc;
     double* sc = smem;                                // [BN][ldc]
@@ -797,13 +796,13 @@ __global__ void __launch_bounds__(256) k_product_skinny(SkinnyParams prm) {
         cp_async_wait<1>();
         __syncthreads();
         const double* a = sa + buf * kp * kSkLdM;
-        const int wm0 = warp * 16;
+        const int wm0 = warp * 8 * RT;
         const double alpha = job.alpha, beta = job.beta;
         const int64_t r0 = tile * kSkBM + wm0 + gid;
         // beta != 0: issue the loads of Out now so their latency hides under the DMMA loop
-        double old[2][NT][2];
+        double old[RT][NT][2];
 #pragma unroll
-        for (int i = 0; i < 2; ++i)
+        for (int i = 0; i < RT; ++i)
 #pragma unroll
             for (int j = 0; j < NT; ++j)
 #pragma unroll
@@ -814,24 +813,24 @@ __global__ void __launch_bounds__(256) k_product_skinny(SkinnyParams prm) {
                                        ? __ldcs(job.out + static_cast<int64_t>(col) * job.ldo + row)
                                        : 0.0;
                 }
-        double acc[2][NT][2];
+        double acc[RT][NT][2];
 #pragma unroll
-        for (int i = 0; i < 2; ++i)
+        for (int i = 0; i < RT; ++i)
 #pragma unroll
             for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
         for (int kk = 0; kk < kp; kk += 4) {
-            double af[2], bf[NT];
+            double af[RT], bf[NT];
 #pragma unroll
-            for (int i = 0; i < 2; ++i) af[i] = a[(kk + tig) * kSkLdM + wm0 + i * 8 + gid];
+            for (int i = 0; i < RT; ++i) af[i] = a[(kk + tig) * kSkLdM + wm0 + i * 8 + gid];
 #pragma unroll
             for (int j = 0; j < NT; ++j) bf[j] = sc[(j * 8 + gid) * ldc + kk + tig];
 #pragma unroll
-            for (int i = 0; i < 2; ++i)
+            for (int i = 0; i < RT; ++i)
 #pragma unroll
                 for (int j = 0; j < NT; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
         }
 #pragma unroll
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < RT; ++i) {
             const int64_t row = r0 + i * 8;
             if (row >= prm.n) continue;
 #pragma unroll
@@ -851,8 +850,22 @@ __global__ void __launch_bounds__(256) k_product_skinny(SkinnyParams prm) {
     cp_async_wait<0>();
 }
 
+template <int BN, int RT>
+void launch_skinny_rt(const ProductJob* jobs, int njobs, int64_t n);
+
 template <int BN>
 void launch_skinny(const ProductJob* jobs, int njobs, int64_t n) {
+    // one m-tile per warp (64-row tiles, ~half the shared memory, 2+ blocks per SM) measured
+    // 20-30 % faster than two for C widths >= 16 on config 2's shapes; width 8 keeps two
+    static const int rt_env = std::getenv("BOSP_SKINNY_RT") ? std::atoi(std::getenv("BOSP_SKINNY_RT")) : 0;
+    const int rt = rt_env ? rt_env : (BN <= 8 ? 2 : 1);
+    if (rt == 1) return launch_skinny_rt<BN, 1>(jobs, njobs, n);
+    return launch_skinny_rt<BN, 2>(jobs, njobs, n);
+}
+
+template <int BN, int RT>
+void launch_skinny_rt(const ProductJob* jobs, int njobs, int64_t n) {
+    constexpr int kSkBM = 64 * RT, kSkLdM = kSkBM + 4;
     Runtime& rt = Runtime::get();
     SkinnyParams prm{};
     int kmax = 0;
@@ -871,13 +884,133 @@ void launch_skinny(const ProductJob* jobs, int njobs, int64_t n) {
     const size_t smem = sizeof(double) * (static_cast<size_t>(BN) * prm.ldc + 2ull * prm.kp * kSkLdM);
     static unsigned attr_mask = 0;
     if (rt.first_use(attr_mask))
-        BOSP_CUDA(cudaFuncSetAttribute(k_product_skinny<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        BOSP_CUDA(cudaFuncSetAttribute(k_product_skinny<BN, RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     int per_sm = 1;
-    BOSP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_product_skinny<BN>, 256, smem));
+    BOSP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_product_skinny<BN, RT>, 256, smem));
     const int64_t ctas = std::max<int64_t>(1, std::min<int64_t>(prm.tiles, int64_t(std::max(per_sm, 1)) * rt.sm_count()));
     LaunchScope ls("product", bytes, flops);
     dim3 grid(static_cast<unsigned>(ctas), 1, njobs);
-    k_product_skinny<BN><<<grid, 256, smem, rt.stream()>>>(prm);
+    k_product_skinny<BN, RT><<<grid, 256, smem, rt.stream()>>>(prm);
+    BOSP_LAUNCH_CHECK();
+}
+
+// Skinny product without staging A: for Out = A*C the n rows are the MMA's M dimension, so the
+// A fragment of m8n8k4 (row gid, k tig) is one double per lane, A[m0 + gid, k0 + tig] -- a warp
+// reads 4 columns x 8 consecutive rows (eight full sectors).  Each warp owns RT x 8 rows and all
+// of C's column tiles; C sits in shared memory (<= 64 x 64).  No A staging means no block-wide
+// barrier and no 130 KB buffer, so several blocks per SM keep the loads in flight.
+template <int NT, int RT>
+__global__ void __launch_bounds__(256) k_product_regs(SkinnyParams prm) {
+    extern __shared__ __align__(16) double smem[];
+    const int kp = prm.kp, ldc = prm.ldc;
+    double* sc = smem;  // [NT * 8][ldc], zero-padded to kp
+    const ProductJob& job = prm.job[blockIdx.z];
+    const int kcols = job.a.cols();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int gid = lane >> 2, tig = lane & 3;
+    for (int idx = threadIdx.x; idx < NT * 8 * kp; idx += 256) {
+        const int c = idx / kp, k = idx - c * kp;
+        sc[c * ldc + k] = (c < job.ncols && k < kcols) ? job.c[static_cast<int64_t>(c) * job.ldc + k] : 0.0;
+    }
+    __syncthreads();
+    constexpr int kRowsW = 8 * RT;
+    const int64_t n = prm.n;
+    const int64_t wtiles = (n + kRowsW - 1) / kRowsW;
+    const double alpha = job.alpha, beta = job.beta;
+    for (int64_t wt = static_cast<int64_t>(blockIdx.x) * 8 + warp; wt < wtiles; wt += static_cast<int64_t>(gridDim.x) * 8) {
+        const int64_t m0 = wt * kRowsW;
+        double acc[RT][NT][2];
+#pragma unroll
+        for (int i = 0; i < RT; ++i)
+#pragma unroll
+            for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll 4
+        for (int kk = 0; kk < kp; kk += 4) {
+            const int kc = kk + tig;
+            const double* col = kc < kcols ? colptr(job.a, kc) + m0 + gid : nullptr;
+            double af[RT], bf[NT];
+#pragma unroll
+            for (int i = 0; i < RT; ++i) af[i] = (col && m0 + i * 8 + gid < n) ? __ldcs(col + i * 8) : 0.0;
+#pragma unroll
+            for (int j = 0; j < NT; ++j) bf[j] = sc[(j * 8 + gid) * ldc + kc];
+#pragma unroll
+            for (int i = 0; i < RT; ++i)
+#pragma unroll
+                for (int j = 0; j < NT; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        }
+        if (beta != 0.0) {  // Out = alpha A C + beta Out: every old value loaded before the first use
+#pragma unroll
+            for (int i = 0; i < RT; ++i)
+#pragma unroll
+                for (int j = 0; j < NT; ++j)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int64_t row = m0 + i * 8 + gid;
+                        const int col = j * 8 + 2 * tig + h;
+                        const double o = (row < n && col < job.ncols)
+                                             ? __ldcs(job.out + static_cast<int64_t>(col) * job.ldo + row)
+                                             : 0.0;
+                        acc[i][j][h] = alpha * acc[i][j][h] + beta * o;
+                    }
+        } else {
+#pragma unroll
+            for (int i = 0; i < RT; ++i)
+#pragma unroll
+                for (int j = 0; j < NT; ++j) {
+                    acc[i][j][0] *= alpha;
+                    acc[i][j][1] *= alpha;
+                }
+        }
+#pragma unroll
+        for (int i = 0; i < RT; ++i) {
+            const int64_t row = m0 + i * 8 + gid;
+            if (row >= n) continue;
+#pragma unroll
+            for (int j = 0; j < NT; ++j)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int col = j * 8 + 2 * tig + h;
+                    if (col < job.ncols) __stcs(job.out + static_cast<int64_t>(col) * job.ldo + row, acc[i][j][h]);
+                }
+        }
+    }
+}
+
+template <int BN>
+void launch_product_regs(const ProductJob* jobs, int njobs, int64_t n) {
+    constexpr int NT = BN / 8;
+#ifndef BOSP_PRODUCT_RT
+    constexpr int RT = NT <= 2 ? 4 : NT <= 4 ? 2 : 1;
+#else
+    constexpr int RT = BOSP_PRODUCT_RT;
+#endif
+    Runtime& rt = Runtime::get();
+    SkinnyParams prm{};
+    int kmax = 0;
+    double flops = 0, bytes = 0;
+    for (int j = 0; j < njobs; ++j) {
+        prm.job[j] = jobs[j];
+        kmax = std::max(kmax, jobs[j].a.cols());
+        const double k = jobs[j].a.cols(), b = jobs[j].ncols;
+        flops += 2.0 * n * k * b;
+        bytes += 8.0 * n * (k + b * (jobs[j].beta != 0.0 ? 2.0 : 1.0));
+    }
+    prm.n = n;
+    prm.kp = std::max(4, (kmax + 3) / 4 * 4);
+    prm.ldc = (prm.kp + 15) / 16 * 16 + 4;
+    const size_t smem = sizeof(double) * static_cast<size_t>(BN) * prm.ldc;
+    static int per_sm = 0;
+    if (per_sm == 0) {
+        BOSP_CUDA(cudaFuncSetAttribute(k_product_regs<NT, RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+        BOSP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_product_regs<NT, RT>, 256, 64 * 1024));
+        per_sm = std::max(per_sm, 1);
+    }
+    const int64_t wtiles = (n + 8 * RT - 1) / (8 * RT);
+    static const int waves = std::getenv("BOSP_PRODUCT_WAVES") ? std::atoi(std::getenv("BOSP_PRODUCT_WAVES")) : 1;
+    const int64_t ctas = std::max<int64_t>(
+        1, std::min<int64_t>((wtiles + 7) / 8, static_cast<int64_t>(per_sm) * waves * rt.sm_count() / njobs));
+    LaunchScope ls("product", bytes, flops);
+    k_product_regs<NT, RT><<<dim3(static_cast<unsigned>(ctas), 1, njobs), 256, smem, rt.stream()>>>(prm);
     BOSP_LAUNCH_CHECK();
 }
 
@@ -940,6 +1073,19 @@ void product(const ProductJob* jobs, int njobs, int64_t n) {
     if (n == 0 || bmax == 0) return;
     int kmax = 0;
     for (int j = 0; j < njobs; ++j) kmax = std::max(kmax, jobs[j].a.cols());
+    static const bool regs = std::getenv("BOSP_PRODUCT_REGS") != nullptr;
+    if (kmax <= 64 && bmax <= 64 && kmax > 0 && regs) {
+        switch ((bmax + 7) / 8) {
+            case 1: return launch_product_regs<8>(jobs, njobs, n);
+            case 2: return launch_product_regs<16>(jobs, njobs, n);
+            case 3: return launch_product_regs<24>(jobs, njobs, n);
+            case 4: return launch_product_regs<32>(jobs, njobs, n);
+            case 5: return launch_product_regs<40>(jobs, njobs, n);
+            case 6: return launch_product_regs<48>(jobs, njobs, n);
+            case 7: return launch_product_regs<56>(jobs, njobs, n);
+            default: return launch_product_regs<64>(jobs, njobs, n);
+        }
+    }
     if (kmax <= 64 && bmax <= 64 && kmax > 0) {
         switch ((bmax + 7) / 8) {
             case 1: return launch_skinny<8>(jobs, njobs, n);
