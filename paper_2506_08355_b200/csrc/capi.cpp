@@ -623,6 +623,13 @@ bosp_status bosp_bench_blas(int32_t kind, int64_t n, int64_t a, int64_t b, int64
         fill_random(c.view(), 3);
         if (kind == 0)
             *ms = time_reps(reps, [&] { bosp::gram(bosp::ColList(x.view()), bosp::ColList(y.view()), n, c.data(), c.ld()); });
+        else if (kind == 3) {  // the MGS triple XᵀX, XᵀY, YᵀY in one launch
+            bosp::DBlock c2(std::max<int64_t>(a, b), std::max<int64_t>(a, b)), c3(std::max<int64_t>(a, b), std::max<int64_t>(a, b));
+            const bosp::GramJob jobs[3] = {{bosp::ColList(x.view()), bosp::ColList(x.view()), c.data(), c.ld()},
+                                           {bosp::ColList(x.view()), bosp::ColList(y.view()), c2.data(), c2.ld()},
+                                           {bosp::ColList(y.view()), bosp::ColList(y.view()), c3.data(), c3.ld()}};
+            *ms = time_reps(reps, [&] { bosp::gram(jobs, 3, n); });
+        }
         else
             *ms = time_reps(reps, [&] {
                 bosp::product(bosp::ColList(x.view()), c.data(), c.ld(), static_cast<int32_t>(b), y.view(),

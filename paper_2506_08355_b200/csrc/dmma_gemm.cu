@@ -214,7 +214,7 @@ k_gram(GramParams prm) {
 // Sum split partials in a fixed order.  A block owns 32 consecutive output elements; its 8
 // warps each fold a strided eighth of the splits (two accumulators, loads independent across
 // the unrolled loop), then warp 0 folds the 8 group sums in order.  grid.z = job.
-constexpr int kRedElems = 32, kRedGroups = 8;
+constexpr int kRedElems = 8, kRedGroups = 32;  // 8 outputs x 32 split groups per block: ~4x the blocks of 32 x 8
 
 template <int BM, int BN>
 __global__ void __launch_bounds__(kRedElems * kRedGroups) k_gram_reduce(GramParams prm) {
@@ -324,74 +324,95 @@ constexpr int kRegWarps = 8;
 #endif
 constexpr int kGramUnroll = BOSP_GRAM_UNROLL;
 
-template <int MT, int NTL>
+template <int MT, int NTL, int GM, int GN>
 __global__ void __launch_bounds__(kRegWarps * 32) k_gram_regs(GramParams prm) {
-    extern __shared__ __align__(16) double red[];  // [warp][MT*8 x NTL*8]
-    constexpr int TM = MT * 8, TN = NTL * 8;
+    // GM x GN warp groups split the MT x NTL fragment tiles (each warp holds MS x NS of them);
+    // the warps of a group walk alternate 4-row steps.  GM = GN = 1: every warp the whole tile.
+    constexpr int G = GM * GN, WPG = kRegWarps / G;
+    constexpr int MS = (MT + GM - 1) / GM, NS = (NTL + GN - 1) / GN;
+    constexpr int TM = MT * 8, TN = NTL * 8, SM = MS * 8, SN = NS * 8;
+    constexpr int LDP = (TM <= 32 && TN <= 32) ? 32 : 64;  // k_gram_reduce<LDP, LDP> layout
+    extern __shared__ __align__(16) double red[];  // [warp][SM x SN]
     const int jb = blockIdx.y;
     const GramJob& job = prm.job[jb];
     const int acols = job.a.cols(), bcols = job.b.cols();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int gid = lane >> 2, tig = lane & 3;
-    const double* pa[MT];
-    const double* pb[NTL];
+    const int grp = warp / WPG, wig = warp - grp * WPG;
+    const int gm = grp / GN, gn = grp - gm * GN;
+    const double* pa[MS];
+    const double* pb[NS];
 #pragma unroll
-    for (int i = 0; i < MT; ++i) {
-        const int c = i * 8 + gid;
+    for (int i = 0; i < MS; ++i) {
+        const int c = (gm * MS + i) * 8 + gid;
         pa[i] = c < acols ? colptr(job.a, c) : nullptr;
     }
 #pragma unroll
-    for (int j = 0; j < NTL; ++j) {
-        const int c = j * 8 + gid;
+    for (int j = 0; j < NS; ++j) {
+        const int c = (gn * NS + j) * 8 + gid;
         pb[j] = c < bcols ? colptr(job.b, c) : nullptr;
     }
-    double acc[MT][NTL][2];
+    double acc[MS][NS][2];
 #pragma unroll
-    for (int i = 0; i < MT; ++i)
+    for (int i = 0; i < MS; ++i)
 #pragma unroll
-        for (int j = 0; j < NTL; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        for (int j = 0; j < NS; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     const int64_t kb = static_cast<int64_t>(blockIdx.x) * prm.chunk;
     const int64_t ke = min(prm.n, kb + prm.chunk);
-#pragma unroll (kGramUnroll)
-    for (int64_t k0 = kb + 4 * warp; k0 < ke; k0 += 4 * kRegWarps) {
-        const int64_t r = k0 + tig;
-        const bool vr = r < ke;
-        double af[MT], bf[NTL];
+    // U consecutive 4-row steps per iteration, every load issued before the first DMMA: ~16
+    // independent loads in flight per lane whatever the tile size
+    constexpr int U = (16 / (MS + NS)) < 1 ? 1 : (16 / (MS + NS)) > 8 ? 8 : 16 / (MS + NS);
+    for (int64_t k0 = kb + 4 * U * wig; k0 < ke; k0 += 4 * U * WPG) {
+        double af[U][MS], bf[U][NS];
 #pragma unroll
-        for (int i = 0; i < MT; ++i) af[i] = (pa[i] && vr) ? __ldg(pa[i] + r) : 0.0;
+        for (int u = 0; u < U; ++u) {
+            const int64_t r = k0 + 4 * u + tig;
+            const bool vr = r < ke;
 #pragma unroll
-        for (int j = 0; j < NTL; ++j) bf[j] = (pb[j] && vr) ? __ldg(pb[j] + r) : 0.0;
+            for (int i = 0; i < MS; ++i) af[u][i] = (pa[i] && vr) ? __ldg(pa[i] + r) : 0.0;
 #pragma unroll
-        for (int i = 0; i < MT; ++i)
+            for (int j = 0; j < NS; ++j) bf[u][j] = (pb[j] && vr) ? __ldg(pb[j] + r) : 0.0;
+        }
 #pragma unroll
-            for (int j = 0; j < NTL; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int i = 0; i < MS; ++i)
+#pragma unroll
+                for (int j = 0; j < NS; ++j) dmma(acc[i][j][0], acc[i][j][1], af[u][i], bf[u][j]);
     }
-    double* mine = red + warp * (TM * TN);
+    double* mine = red + warp * (SM * SN);
 #pragma unroll
-    for (int i = 0; i < MT; ++i)
+    for (int i = 0; i < MS; ++i)
 #pragma unroll
-        for (int j = 0; j < NTL; ++j) {
+        for (int j = 0; j < NS; ++j) {
             const int m = i * 8 + gid, nn = j * 8 + 2 * tig;
-            mine[m + nn * TM] = acc[i][j][0];
-            mine[m + (nn + 1) * TM] = acc[i][j][1];
+            mine[m + nn * SM] = acc[i][j][0];
+            mine[m + (nn + 1) * SM] = acc[i][j][1];
         }
     __syncthreads();
-    double* part = prm.partial + jb * prm.job_stride + static_cast<int64_t>(blockIdx.x) * 1024;
+    double* part = prm.partial + jb * prm.job_stride + static_cast<int64_t>(blockIdx.x) * (LDP * LDP);
     for (int e = threadIdx.x; e < TM * TN; e += kRegWarps * 32) {
-        double v = 0.0;
-#pragma unroll
-        for (int w = 0; w < kRegWarps; ++w) v += red[w * (TM * TN) + e];
         const int m = e % TM, nn = e / TM;
+        const int om = m / SM, on = nn / SN;  // owning group
+        double v = 0.0;
+        if (om < GM && on < GN) {
+            const int g = om * GN + on, loc = (m - om * SM) + (nn - on * SN) * SM;
+#pragma unroll
+            for (int w = 0; w < WPG; ++w) v += red[(g * WPG + w) * (SM * SN) + loc];
+        }
         if (prm.splits == 1) {
             if (m < acols && nn < bcols) job.g[m + static_cast<int64_t>(nn) * job.ldg] = v;
         } else {
-            part[m + nn * 32] = v;  // k_gram_reduce<32, 32> layout (one tile)
+            part[m + nn * LDP] = v;
         }
     }
 }
 
-template <int MT, int NTL>
+template <int MT, int NTL, int GM = 1, int GN = 1>
 void launch_gram_regs(const GramJob* jobs, int njobs, int64_t n) {
+    constexpr int LDP = (MT * 8 <= 32 && NTL * 8 <= 32) ? 32 : 64;
+    constexpr int MS = (MT + GM - 1) / GM, NS = (NTL + GN - 1) / GN;
+    constexpr int WPG = kRegWarps / (GM * GN);
     Runtime& rt = Runtime::get();
     GramParams prm{};
     for (int j = 0; j < njobs; ++j) {
@@ -400,23 +421,24 @@ void launch_gram_regs(const GramJob* jobs, int njobs, int64_t n) {
         prm.tiles[j] = 1;
     }
     prm.n = n;
-    constexpr int64_t kStep = 4 * kRegWarps;  // rows per block step
-    const int64_t steps = (n + kStep - 1) / kStep;
+    constexpr int U = (16 / (MS + NS)) < 1 ? 1 : (16 / (MS + NS)) > 8 ? 8 : 16 / (MS + NS);
+    constexpr int64_t kStep = 4 * U * WPG;  // rows per warp-group iteration
+    const int64_t steps = (n + 4 * kRegWarps - 1) / (4 * kRegWarps);
     // one full wave (2 resident blocks per SM at ~100 registers); 3-8 waves measured 30-100 %
     // slower on config 2's 20-column Grams (more partials, tail)
     static const int64_t waves = std::getenv("BOSP_GRAM_WAVES") ? std::atoi(std::getenv("BOSP_GRAM_WAVES")) : 2;
     int splits = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(
         (waves * rt.sm_count() + njobs - 1) / njobs, steps / 8)));  // >= 8 steps of work per block
-    const int64_t per = (steps + splits - 1) / splits;
+    const int64_t per = ((n + splits - 1) / splits + kStep - 1) / kStep;
     prm.chunk = per * kStep;
     splits = static_cast<int>((n + prm.chunk - 1) / prm.chunk);
     prm.splits = std::max(1, splits);
-    prm.job_stride = static_cast<int64_t>(prm.splits) * 1024;
+    prm.job_stride = static_cast<int64_t>(prm.splits) * LDP * LDP;
     prm.partial = rt.scratch(static_cast<size_t>(prm.job_stride) * njobs);
-    constexpr size_t smem = sizeof(double) * kRegWarps * MT * 8 * NTL * 8;
+    constexpr size_t smem = sizeof(double) * kRegWarps * MS * 8 * NS * 8;
     static unsigned attr_mask = 0;
     if (rt.first_use(attr_mask))
-        BOSP_CUDA(cudaFuncSetAttribute(k_gram_regs<MT, NTL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        BOSP_CUDA(cudaFuncSetAttribute(k_gram_regs<MT, NTL, GM, GN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem)));
     double flops = 0.0, bytes = 0.0;
     for (int j = 0; j < njobs; ++j) {
@@ -425,16 +447,17 @@ void launch_gram_regs(const GramJob* jobs, int njobs, int64_t n) {
     }
     {
         LaunchScope ls("gram", bytes, flops);
-        k_gram_regs<MT, NTL><<<dim3(prm.splits, njobs), kRegWarps * 32, smem, rt.stream()>>>(prm);
+        k_gram_regs<MT, NTL, GM, GN><<<dim3(prm.splits, njobs), kRegWarps * 32, smem, rt.stream()>>>(prm);
         BOSP_LAUNCH_CHECK();
     }
     if (prm.splits > 1) {
         LaunchScope ls("gram_reduce");
-        dim3 grid(static_cast<unsigned>(1024 / kRedElems), 1, njobs);
-        k_gram_reduce<32, 32><<<grid, kRedElems * kRedGroups, 0, rt.stream()>>>(prm);
+        dim3 grid(static_cast<unsigned>(LDP * LDP / kRedElems), 1, njobs);
+        k_gram_reduce<LDP, LDP><<<grid, kRedElems * kRedGroups, 0, rt.stream()>>>(prm);
         BOSP_LAUNCH_CHECK();
     }
 }
+
 
 // ------------------------------------------------------------------------------------------
 // Product kernel
@@ -1040,15 +1063,37 @@ void gram(const GramJob* jobs, int njobs, int64_t n) {
         return;
     }
     static const bool regs = !std::getenv("BOSP_GRAM_SMEM");
-    if (amax <= 32 && bmax <= 32 && regs) {
+    // register-fragment Grams (n rows = the MMA k dimension, operands straight from global):
+    // up to 4 x 4 fragment tiles (32 columns) every warp holds the whole tile; a side wider
+    // than 32 is split over two warp groups (a 2 x 1, 1 x 2 or 2 x 2 group layout, each warp
+    // <= 4 x 4 tiles); beyond wide_max columns the shared-memory tiled DMMA kernel
+    static const int wide_max = std::getenv("BOSP_GRAM_WIDE_MAX") ? std::atoi(std::getenv("BOSP_GRAM_WIDE_MAX")) : 64;
+    // several jobs wider than 48 (the MGS triple at width 60): the tiled kernel measured faster
+    const int lim = njobs > 1 ? std::min(wide_max, 48) : wide_max;
+    if (amax <= lim && bmax <= lim && regs) {
         const int mt = (amax + 7) / 8, nt = (bmax + 7) / 8;
-        switch (mt * 4 + nt) {
+        if (mt <= 4 && nt <= 4) {
+            switch (mt * 4 + nt) {
 #define BOSP_G(M, N) case M * 4 + N: return launch_gram_regs<M, N>(jobs, njobs, n);
-            BOSP_G(1, 1) BOSP_G(1, 2) BOSP_G(1, 3) BOSP_G(1, 4)
-            BOSP_G(2, 1) BOSP_G(2, 2) BOSP_G(2, 3) BOSP_G(2, 4)
-            BOSP_G(3, 1) BOSP_G(3, 2) BOSP_G(3, 3) BOSP_G(3, 4)
-            BOSP_G(4, 1) BOSP_G(4, 2) BOSP_G(4, 3) BOSP_G(4, 4)
+                BOSP_G(1, 1) BOSP_G(1, 2) BOSP_G(1, 3) BOSP_G(1, 4)
+                BOSP_G(2, 1) BOSP_G(2, 2) BOSP_G(2, 3) BOSP_G(2, 4)
+                BOSP_G(3, 1) BOSP_G(3, 2) BOSP_G(3, 3) BOSP_G(3, 4)
+                BOSP_G(4, 1) BOSP_G(4, 2) BOSP_G(4, 3) BOSP_G(4, 4)
 #undef BOSP_G
+                default: break;
+            }
+        }
+        const int mp = mt <= 4 ? mt : (mt <= 6 ? 6 : 8), np = nt <= 4 ? nt : (nt <= 6 ? 6 : 8);
+        switch (mp * 16 + np) {
+#define BOSP_A(M, N) case M * 16 + N: return launch_gram_regs<M, N, 2, 1>(jobs, njobs, n);
+#define BOSP_B(M, N) case M * 16 + N: return launch_gram_regs<M, N, 1, 2>(jobs, njobs, n);
+#define BOSP_C(M, N) case M * 16 + N: return launch_gram_regs<M, N, 2, 2>(jobs, njobs, n);
+            BOSP_A(6, 1) BOSP_A(6, 2) BOSP_A(6, 3) BOSP_A(6, 4) BOSP_A(8, 1) BOSP_A(8, 2) BOSP_A(8, 3) BOSP_A(8, 4)
+            BOSP_B(1, 6) BOSP_B(2, 6) BOSP_B(3, 6) BOSP_B(4, 6) BOSP_B(1, 8) BOSP_B(2, 8) BOSP_B(3, 8) BOSP_B(4, 8)
+            BOSP_C(6, 6) BOSP_C(6, 8) BOSP_C(8, 6) BOSP_C(8, 8)
+#undef BOSP_A
+#undef BOSP_B
+#undef BOSP_C
             default: break;
         }
     }
