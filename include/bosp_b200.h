@@ -201,6 +201,10 @@ bosp_status bosp_compute_nullspace(bosp_op K, bosp_op M, bosp_op B, int64_t rank
 bosp_status bosp_block_inner(bosp_op B, int64_t n, int64_t a, int64_t b, const double* x,
                              const double* y, double* g);
 /* out (n x b) = X C  (block_product, kernels.cpp:70-87). */
+/* Test hook (no reference counterpart): the solver's multi-job Gram launch, X split into nseg
+ * column segments; out = [XᵀY | XᵀX | YᵀY] column-major. */
+bosp_status bosp_test_gram_jobs(int64_t n, int64_t a, int64_t b, const double* x, const double* y, int32_t nseg,
+                                int32_t njobs, double* out);
 bosp_status bosp_block_product(int64_t n, int64_t a, int64_t b, const double* x, const double* c,
                                double* out);
 /* Y (n x b) -= X C  (block_axpy, kernels.cpp:89-104). */

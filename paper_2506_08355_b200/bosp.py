@@ -416,6 +416,17 @@ def block_inner(ip, x, y):
     return g
 
 
+def _test_gram_jobs(x, y, nseg=1, njobs=3):
+    """Test hook: the solver's multi-job Gram launch -> (XᵀY, XᵀX, YᵀY); X in nseg segments."""
+    x, y = _f(x), _f(y)
+    n, a, b = x.shape[0], x.shape[1], y.shape[1]
+    out = np.zeros(a * b + a * a + b * b)
+    check(lib().bosp_test_gram_jobs(C.c_int64(n), C.c_int64(a), C.c_int64(b), _p(x), _p(y), C.c_int32(nseg),
+                                    C.c_int32(njobs), _p(out)))
+    return (out[:a * b].reshape((a, b), order="F"), out[a * b:a * b + a * a].reshape((a, a), order="F"),
+            out[a * b + a * a:].reshape((b, b), order="F"))
+
+
 def block_product(x, c):
     x, c = _f(x), _f(c)
     if x.shape[1] != c.shape[0]:

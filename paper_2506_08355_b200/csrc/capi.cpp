@@ -437,6 +437,34 @@ bosp_status bosp_block_inner(bosp_op B, int64_t n, int64_t a, int64_t b, const d
     });
 }
 
+// Test hook: the multi-job Gram launch the solver uses (XᵀY, XᵀX, YᵀY in one launch) with X
+// split into nseg separately allocated column segments.  out = [XᵀY (a x b) | XᵀX (a x a) | YᵀY (b x b)].
+bosp_status bosp_test_gram_jobs(int64_t n, int64_t a, int64_t b, const double* x, const double* y, int32_t nseg,
+                                int32_t njobs, double* out) {
+    return guarded([&] {
+        bosp::require(nseg >= 1 && nseg <= 4 && njobs >= 1 && njobs <= 3 && a >= nseg, "test_gram_jobs: bad arguments");
+        std::vector<bosp::DBlock> xs;
+        bosp::ColList xl;
+        int64_t c0 = 0;
+        for (int s = 0; s < nseg; ++s) {
+            const int64_t w = (a - c0) / (nseg - s);
+            xs.emplace_back(n, w);
+            bosp::to_device(x + c0 * n, n, w, n, xs.back().view());
+            c0 += w;
+        }
+        for (auto& blk : xs) xl.add(blk.view());
+        bosp::DBlock yd(n, b);
+        bosp::to_device(y, n, b, n, yd.view());
+        bosp::DBlock g1(a, b), g2(a, a), g3(b, b);
+        const bosp::ColList yl(yd.view());
+        const bosp::GramJob jobs[3] = {{xl, yl, g1.data(), g1.ld()}, {xl, xl, g2.data(), g2.ld()}, {yl, yl, g3.data(), g3.ld()}};
+        bosp::gram(jobs, njobs, n);
+        bosp::to_host(g1.view(), out, a);
+        if (njobs > 1) bosp::to_host(g2.view(), out + a * b, a);
+        if (njobs > 2) bosp::to_host(g3.view(), out + a * b + a * a, b);
+    });
+}
+
 bosp_status bosp_block_product(int64_t n, int64_t a, int64_t b, const double* x, const double* c, double* out) {
     return guarded([&] { copy_out(bosp::block_product(host_block(x, n, a), host_dense(c, a, b)), out); });
 }

@@ -277,3 +277,47 @@ def test_csr_storage_formats_apply(case):
     y = op.apply(x)
     ref = a @ x
     assert np.abs(y - ref).max() <= 1e-13 * max(1.0, np.abs(ref).max())
+
+
+GRAM_WIDTHS = [1, 8, 9, 17, 24, 25, 32, 33, 40, 41, 48, 49, 56, 57, 64, 65]
+
+
+@pytest.mark.parametrize("a", GRAM_WIDTHS)
+def test_gram_width_sweep(a):
+    """Every Gram dispatch class (single-warp-group register tiles, 2x1 / 1x2 / 2x2 warp
+    groups, the shared-memory tiled kernel) against numpy, with odd row counts."""
+    rng = np.random.default_rng(a)
+    n = 3001 + 7 * a
+    x = np.asfortranarray(rng.uniform(-1, 1, (n, a)))
+    for b in GRAM_WIDTHS:
+        y = np.asfortranarray(rng.uniform(-1, 1, (n, b)))
+        assert rel(bosp.block_inner(None, x, y), x.T @ y) < 1e-13, (a, b)
+
+
+@pytest.mark.parametrize("k", [1, 7, 8, 20, 33, 60, 64, 65, 100])
+def test_product_width_sweep(k):
+    rng = np.random.default_rng(100 + k)
+    n = 5003
+    x = np.asfortranarray(rng.uniform(-1, 1, (n, k)))
+    for b in (1, 8, 9, 20, 24, 33, 48, 60, 64, 65):
+        c = np.asfortranarray(rng.uniform(-1, 1, (k, b)))
+        y = np.asfortranarray(rng.uniform(-1, 1, (n, b)))
+        assert rel(bosp.block_product(x, c), x @ c) < 1e-13, (k, b)
+        assert rel(bosp.block_axpy(x, c, y), y - x @ c) < 1e-13, (k, b)
+
+
+@pytest.mark.parametrize("a,b", [(20, 20), (33, 33), (40, 40), (48, 48), (40, 8), (60, 60), (64, 64), (64, 20), (96, 64)])
+@pytest.mark.parametrize("nseg", [1, 3])
+def test_gram_multi_job_segments(a, b, nseg):
+    """The MGS / drift-monitor Gram triple in one launch, X in column segments."""
+    rng = np.random.default_rng(a * 100 + b + nseg)
+    n = 20011
+    x = np.asfortranarray(rng.uniform(-1, 1, (n, a)))
+    y = np.asfortranarray(rng.uniform(-1, 1, (n, b)))
+    for njobs in (1, 2, 3):
+        g1, g2, g3 = bosp._test_gram_jobs(x, y, nseg, njobs)
+        assert rel(g1, x.T @ y) < 1e-13, (njobs, "xy")
+        if njobs > 1:
+            assert rel(g2, x.T @ x) < 1e-13, (njobs, "xx")
+        if njobs > 2:
+            assert rel(g3, y.T @ y) < 1e-13, (njobs, "yy")
