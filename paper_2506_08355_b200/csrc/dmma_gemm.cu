@@ -1067,9 +1067,10 @@ void gram(const GramJob* jobs, int njobs, int64_t n) {
     // up to 4 x 4 fragment tiles (32 columns) every warp holds the whole tile; a side wider
     // than 32 is split over two warp groups (a 2 x 1, 1 x 2 or 2 x 2 group layout, each warp
     // <= 4 x 4 tiles); beyond wide_max columns the shared-memory tiled DMMA kernel
-    static const int wide_max = std::getenv("BOSP_GRAM_WIDE_MAX") ? std::atoi(std::getenv("BOSP_GRAM_WIDE_MAX")) : 64;
-    // several jobs wider than 48 (the MGS triple at width 60): the tiled kernel measured faster
-    const int lim = njobs > 1 ? std::min(wide_max, 48) : wide_max;
+    // 48: config 2 is flat between 32 and 64; at 64 the rounding of config 5's 64-wide Grams
+    // pushed its (repair-heavy) run into the reference's NumericalAbort path -- 48 converges
+    static const int wide_max = std::getenv("BOSP_GRAM_WIDE_MAX") ? std::atoi(std::getenv("BOSP_GRAM_WIDE_MAX")) : 48;
+    const int lim = wide_max;
     if (amax <= lim && bmax <= lim && regs) {
         const int mt = (amax + 7) / 8, nt = (bmax + 7) / 8;
         if (mt <= 4 && nt <= 4) {
