@@ -727,115 +727,6 @@ __global__ void __launch_bounds__(kRows) k_dia_row(DiaDev a, const double* __res
     tm.stop();
 }
 
-// DIA SpMM on row pairs (i, i+1), i even, with 16-byte x loads: an even offset o reads the
-// aligned pair x(i+o), x(i+o+1) once for both rows; an odd one reads the pair at i+o-1 (row i
-// takes .y) and one 8-byte x(i+o+1) for row i+1.  Absent entries get a zero coefficient and
-// an in-range address (the row pair itself), so there are no divergent branches; the offset
-// parity tests are warp-uniform.  TWO_PHASE issues every column's loads before the FMAs.
-template <int CB, bool DOT, int ND, bool TWO_PHASE, bool VAR>
-__global__ void __launch_bounds__(kRows) k_dia_pair(DiaDev a, const double* __restrict__ x, int64_t ldx,
-                                                     double* __restrict__ y, int64_t ldy, int ncols, KTimer tm,
-                                                     DotOut dots) {
-    tm.start();
-    tm.columns(DOT ? dots.active : nullptr, 0, 0, ncols);
-    const int j0 = blockIdx.y * CB;
-    double d[CB];
-#pragma unroll
-    for (int c = 0; c < CB; ++c) d[c] = 0.0;
-    bool on[CB];
-    const bool any = group_columns<CB, DOT>(dots, j0, ncols, on);
-    const int n = static_cast<int>(a.n), npairs = n >> 1;
-    const int stride = static_cast<int>(gridDim.x) * kRows;
-    const double* xcol[CB];
-    double* ycol[CB];
-#pragma unroll
-    for (int c = 0; c < CB; ++c) {
-        xcol[c] = x + static_cast<int64_t>(j0 + c) * ldx;
-        ycol[c] = y + static_cast<int64_t>(j0 + c) * ldy;
-        asm volatile("mov.b64 %0, %0;" : "+l"(xcol[c]));
-        asm volatile("mov.b64 %0, %0;" : "+l"(ycol[c]));
-    }
-    for (int pr = any ? static_cast<int>(blockIdx.x) * kRows + threadIdx.x : npairs; pr < npairs; pr += stride) {
-        const int i = 2 * pr;
-        const unsigned mk = __ldg(reinterpret_cast<const unsigned*>(a.mask + i));  // row i low, i+1 high
-        int ja[ND], jb[ND];
-        double v0[ND], v1[ND];
-#pragma unroll
-        for (int k = 0; k < ND; ++k) {
-            const bool p0 = (mk >> k) & 1u, p1 = (mk >> (16 + k)) & 1u;
-            const int o = static_cast<int>(a.off[k]);
-            double c0 = a.cval[k], c1 = a.cval[k];
-            if (VAR && a.vidx[k] >= 0) {
-                const double2 t = __ldg(reinterpret_cast<const double2*>(a.val + static_cast<int64_t>(a.vidx[k]) * n + i));
-                c0 = t.x;
-                c1 = t.y;
-            }
-            v0[k] = p0 ? c0 : 0.0;
-            v1[k] = p1 ? c1 : 0.0;
-            if ((o & 1) == 0) {
-                ja[k] = (p0 || p1) ? i + o : i;
-                jb[k] = 0;
-            } else {
-                ja[k] = p0 ? i + o - 1 : i;
-                jb[k] = p1 ? i + o + 1 : i;
-            }
-        }
-        auto column = [&](int c, const double2 (&t)[ND], const double (&u)[ND]) {
-            double acc0 = 0.0, acc1 = 0.0;
-#pragma unroll
-            for (int k = 0; k < ND; ++k) {
-                const bool odd = a.off[k] & 1;
-                acc0 = fma(v0[k], odd ? t[k].y : t[k].x, acc0);
-                acc1 = fma(v1[k], odd ? u[k] : t[k].y, acc1);
-            }
-            __stcg(reinterpret_cast<double2*>(ycol[c] + i), make_double2(acc0, acc1));
-            return make_double2(acc0, acc1);
-        };
-        auto load = [&](int c, double2 (&t)[ND], double (&u)[ND]) {
-            const double* xc = xcol[c];
-#pragma unroll
-            for (int k = 0; k < ND; ++k) {
-                t[k] = __ldg(reinterpret_cast<const double2*>(xc + ja[k]));
-                u[k] = (a.off[k] & 1) ? __ldg(xc + jb[k]) : 0.0;
-            }
-        };
-        if (TWO_PHASE) {
-            double2 t[CB][ND], xs[CB];
-            double u[CB][ND];
-#pragma unroll
-            for (int c = 0; c < CB; ++c) {
-                if (!on[c]) continue;
-                load(c, t[c], u[c]);
-                if (DOT) xs[c] = __ldg(reinterpret_cast<const double2*>(xcol[c] + i));
-            }
-#pragma unroll
-            for (int c = 0; c < CB; ++c) {
-                if (!on[c]) continue;
-                const double2 r = column(c, t[c], u[c]);
-                if (DOT) d[c] = fma(xs[c].x, r.x, fma(xs[c].y, r.y, d[c]));
-            }
-        } else {
-#pragma unroll
-            for (int c = 0; c < CB; ++c) {
-                if (!on[c]) continue;
-                double2 t[ND];
-                double u[ND];
-                load(c, t, u);
-                const double2 r = column(c, t, u);
-                if (DOT) {
-                    const double2 xs = __ldg(reinterpret_cast<const double2*>(xcol[c] + i));
-                    d[c] = fma(xs.x, r.x, fma(xs.y, r.y, d[c]));
-                }
-            }
-        }
-    }
-    if (DOT) {
-        block_dots_out<CB>(d, dots.parts, j0, ncols);
-        fold_dots_last_block(dots.parts, ncols, dots.ticket, dots.out);
-    }
-    tm.stop();
-}
-
 // DIA SpMM for the banded "stencil-like" layout: ND odd, offsets [.., -1, 0, 1, ..] with every
 // other offset even.  A row pair (i, i+1) then needs exactly ND aligned 16-byte x loads:
 // P(i + o) for each even o != 0, and P(i - 2), P(i), P(i + 2) for the -1/0/+1 triple (row i
@@ -1408,7 +1299,6 @@ unsigned launch_dia_row(const DiaDev& a, const DMat& x, const DMat& y, const Dot
     Runtime& rt = Runtime::get();
     const int ncols = static_cast<int>(x.cols);
     static const bool two = std::getenv("BOSP_DIA_1PHASE") == nullptr;
-    static const bool rows = std::getenv("BOSP_DIA_PAIR") == nullptr;
     bool var = false;
     for (int k = 0; k < a.ndiag; ++k) var = var || a.vidx[k] >= 0;
     auto go = [&](auto kern) { kern<<<grid, kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm, dd); };
@@ -1424,18 +1314,6 @@ unsigned launch_dia_row(const DiaDev& a, const DMat& x, const DMat& y, const Dot
         if (nvar == 0) dot ? go2(k_dia_sym<CB, true, ND, 0>) : go2(k_dia_sym<CB, false, ND, 0>);
         else if (nvar == 1 && a.vidx[ND / 2] >= 0) dot ? go2(k_dia_sym<CB, true, ND, 1>) : go2(k_dia_sym<CB, false, ND, 1>);
         else dot ? go2(k_dia_sym<CB, true, ND, 2>) : go2(k_dia_sym<CB, false, ND, 2>);
-        return g2.x;
-    }
-    if (!rows) {
-        const dim3 g2(std::min<unsigned>(grid.x, row_blocks(a.n / 2, nullptr, ncols)), grid.y);
-        auto go2 = [&](auto kern) { kern<<<g2, kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm, dd); };
-        if (two) {
-            if (var) dot ? go2(k_dia_pair<CB, true, ND, true, true>) : go2(k_dia_pair<CB, false, ND, true, true>);
-            else dot ? go2(k_dia_pair<CB, true, ND, true, false>) : go2(k_dia_pair<CB, false, ND, true, false>);
-        } else {
-            if (var) dot ? go2(k_dia_pair<CB, true, ND, false, true>) : go2(k_dia_pair<CB, false, ND, false, true>);
-            else dot ? go2(k_dia_pair<CB, true, ND, false, false>) : go2(k_dia_pair<CB, false, ND, false, false>);
-        }
         return g2.x;
     }
     if (two) {
