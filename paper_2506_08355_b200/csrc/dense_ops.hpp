@@ -82,7 +82,12 @@ struct CgScalars {
     // epilogues set the loop condition to (any column still active).
     cudaGraphConditionalHandle cond = 0;
     int has_cond = 0;
+    // Optional device scalar: columns >= *m_live are not part of this solve (never read or
+    // written, inactive from the start).  Lets one recorded graph serve every narrower call.
+    const int* m_live = nullptr;
 };
+// *p = v on the stream (sets a graph's live width before its launch)
+void set_device_int(int* p, int v);
 // x = 0, r = b, p = b, rr = ||b||^2, bnorm = ||b||, active = (bnorm != 0 && sqrt(rr) > tol*bnorm)
 void cg_start(const DMat& b, const DMat& x, const DMat& r, const DMat& p, const CgScalars& s,
               double tol, int max_iter);

@@ -1,3 +1,4 @@
+#include <cstdio>
 // Device orchestration of the biorthogonalization and inner-CG building blocks.
 #include "dev_algos.hpp"
 
@@ -359,6 +360,7 @@ void CgWorkspace::ensure(int64_t n, int64_t m) {
         s.iters = iv + 2 * m;
         s.any_active = iv + 3 * m;
         s.loops = iv + 3 * m + 1;
+        m_live = iv + 3 * m + 2;
     }
     if (!parts_) {  // [pap partials | r^T r partials], 160 columns x 512 blocks each
         parts_ = static_cast<double*>(Runtime::get().alloc(sizeof(double) * 2 * kPartsPerRegion));
@@ -442,13 +444,28 @@ DevCgOutcome dev_cg(const LinearOperator& a, const DMat& rhs, const DMat& x, dou
     // communicator between kernels (host-synchronised for ThreadComm), so the loop is host-driven
     if (!x0 && rt.nranks() == 1 && a.impl()->capturable() && !std::getenv("BOSP_NO_GRAPHS")) {
         // ---- graph path: the whole solve is one launch, the loop runs on the device ----
+        // Operators whose apply honours the column mask record the unrolled graph once at the
+        // workspace width and serve every narrower call through the live-width scalar (the
+        // solver's GS sweeps shrink 20 -> 19 -> 16 -> ... -> 1 as columns converge).
+        static const bool force_while = std::getenv("BOSP_CG_WHILE") != nullptr;
+        const bool unrolled = max_iter <= kCgUnrollMax && !force_while && a.impl()->has_masked_dot() && cg_mode() != 2;
+        // Recorded width: the next power of two (capped at the workspace width), so a graph
+        // serves widths within 2x of its own and the kernels' grids stay sized for them
+        // (recording at the full width for every call measured 8 % slower: narrow solves then
+        // run on grids split for 20 columns).
+        int64_t mg = m;
+        if (unrolled) {
+            mg = 1;
+            while (mg < m) mg *= 2;
+            mg = std::max<int64_t>(m, std::min<int64_t>(mg, ws.r.capacity()));
+        }
         CgGraph* g = nullptr;
         for (CgGraph& c : ws.graphs)
             if (c.op == a.impl() && c.rhs == rhs.p && c.ldr == rhs.ld && c.x == x.p && c.ldx == x.ld &&
-                c.m == m && c.tol == tol && c.max_iter == max_iter && c.prof_family == rt.prof_family())
+                c.m == mg && c.tol == tol && c.max_iter == max_iter && c.prof_family == rt.prof_family())
                 g = &c;
         if (!g) {
-            if (ws.graphs.size() >= 8) drop_graphs(ws.graphs);
+            if (ws.graphs.size() >= 16) drop_graphs(ws.graphs);
             ws.graphs.emplace_back();
             g = &ws.graphs.back();
             g->op = a.impl();
@@ -456,7 +473,7 @@ DevCgOutcome dev_cg(const LinearOperator& a, const DMat& rhs, const DMat& x, dou
             g->ldr = rhs.ld;
             g->x = x.p;
             g->ldx = x.ld;
-            g->m = m;
+            g->m = mg;
             g->tol = tol;
             g->max_iter = max_iter;
             g->prof_family = rt.prof_family();
@@ -468,16 +485,19 @@ DevCgOutcome dev_cg(const LinearOperator& a, const DMat& rhs, const DMat& x, dou
             // Short solves (the solver's inner CG: max_iter 20) are unrolled into a straight
             // graph -- every kernel early-outs once its columns are done, no conditional node,
             // and every launch keeps its own profiling slot.  Long solves use a device while loop.
-            static const bool force_while = std::getenv("BOSP_CG_WHILE") != nullptr;
-            if (max_iter <= kCgUnrollMax && !force_while && a.impl()->has_masked_dot() && cg_mode() != 2) {
+            if (unrolled) {
                 CgScalars sc = ws.s;
                 sc.has_cond = 0;
+                sc.m_live = ws.m_live;
+                const DMat rg = ws.r.cols(0, mg), pg = ws.p.cols(0, mg), apg = ws.ap.cols(0, mg);
+                DMat rhsg = rhs, xg = x;
+                rhsg.cols = xg.cols = mg;  // columns >= the live width are never touched
                 rt.set_capture_sink(&g->start_launches);
                 BOSP_CUDA(cudaStreamBeginCaptureToGraph(rt.stream(), g->graph, nullptr, nullptr, 0,
                                                         cudaStreamCaptureModeRelaxed));
                 rt.timer_reserve(max_iter);  // one memset node for every timed launch below
-                cg_start(rhs, x, r, p, sc, tol, mi);
-                for (int64_t it = 0; it < max_iter; ++it) cg_iteration(a, x, r, p, ap, sc, ws, tol, mi);
+                cg_start(rhsg, xg, rg, pg, sc, tol, mi);
+                for (int64_t it = 0; it < max_iter; ++it) cg_iteration(a, xg, rg, pg, apg, sc, ws, tol, mi);
                 rt.timer_reserve(0);
                 BOSP_CUDA(cudaStreamEndCapture(rt.stream(), &g->graph));
             } else {
@@ -513,7 +533,13 @@ DevCgOutcome dev_cg(const LinearOperator& a, const DMat& rhs, const DMat& x, dou
             rt.set_capture_sink(nullptr);
             rt.set_capture_prof(nullptr);
             BOSP_CUDA(cudaGraphInstantiate(&g->exec, g->graph, 0));
+            rt.graph_builds_ += 1;
+            if (std::getenv("BOSP_SYNC_STATS"))
+                std::fprintf(stderr, "[bosp] cg graph: op %p rhs %p x %p m %lld tol %g max_iter %lld (cache %zu)\n",
+                             (const void*)a.impl(), (const void*)rhs.p, (const void*)x.p, (long long)m, tol,
+                             (long long)max_iter, ws.graphs.size());
         }
+        if (unrolled) set_device_int(ws.m_live, static_cast<int>(m));
         BOSP_CUDA(cudaGraphLaunch(g->exec, rt.stream()));
         if (defer_sweeps && g->body_launches.empty() && g->prof_pairs.empty() && !want_stats) {
             // unrolled graph: every launch is known, the sweep count lands in ws.s.total

@@ -68,6 +68,7 @@ public:
     void ensure(int64_t n, int64_t m);
     DBlock r, p, ap;
     CgScalars s{};
+    int* m_live = nullptr;       // device: live width of a graph recorded wider (see dev_cg)
     int* host_active = nullptr;  // pinned ring
     cudaEvent_t ev[2] = {nullptr, nullptr};
     std::vector<CgGraph> graphs;

@@ -32,10 +32,13 @@ static const char* kPhaseNames[PH_COUNT] = {"init", "ritz(apply+gram+pullback)",
                                             "residuals", "step5", "cg", "biorth_against", "mgs_biorth",
                                             "step7", "sample_invariants", "repair", "assemble"};
 
-bool phases_enabled() {
-    static const bool on = std::getenv("BOSP_PHASES") != nullptr;
-    return on;
+// BOSP_PHASES=1: synchronise at each phase end (GPU time lands in its phase); BOSP_PHASES=2:
+// no synchronisation -- host time only (what the host spends issuing each phase)
+int phases_mode() {
+    static const int m = std::getenv("BOSP_PHASES") ? std::atoi(std::getenv("BOSP_PHASES")) : 0;
+    return m;
 }
+bool phases_enabled() { return phases_mode() == 1; }
 
 struct PhaseClock {
     double acc[PH_COUNT] = {};
@@ -638,8 +641,12 @@ EigenResult solve(const LinearOperator& k, const LinearOperator& m, const InnerP
     const auto ta = Clock::now();
     EigenResult res = assemble_result(st.dev(), k, m, ip, cfg, converged, out);
     st.dev().phases.acc[PH_ASSEMBLE] += secs(ta, Clock::now());
-    if (phases_enabled()) {
-        std::fprintf(stderr, "[bosp] phase wall times (s), %lld iterations:\n", (long long)st.iter());
+    if (std::getenv("BOSP_SYNC_STATS"))
+        std::fprintf(stderr, "[bosp] %lld host syncs, %.4f s waiting in them, %lld CG graphs built\n",
+                     (long long)rt.sync_count_, rt.sync_wait_s_, (long long)rt.graph_builds_);
+    if (phases_mode() != 0) {
+        std::fprintf(stderr, "[bosp] phase %s times (s), %lld iterations:\n", phases_enabled() ? "wall" : "host",
+                     (long long)st.iter());
         for (int i = 0; i < PH_COUNT; ++i)
             std::fprintf(stderr, "[bosp]   %-28s %9.4f\n", kPhaseNames[i], st.dev().phases.acc[i]);
     }

@@ -1,3 +1,4 @@
+#include <chrono>
 #include "runtime.hpp"
 
 #include <algorithm>
@@ -51,7 +52,17 @@ void Runtime::free(void* p) {
     if (p) cudaFreeAsync(p, stream_);
 }
 
-void Runtime::sync() { BOSP_CUDA(cudaStreamSynchronize(stream_)); }
+void Runtime::sync() {
+    static const bool stats = std::getenv("BOSP_SYNC_STATS") != nullptr;
+    if (!stats) {
+        BOSP_CUDA(cudaStreamSynchronize(stream_));
+        return;
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    BOSP_CUDA(cudaStreamSynchronize(stream_));
+    sync_count_ += 1;
+    sync_wait_s_ += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
 
 double* Runtime::scratch(size_t doubles) {
     if (doubles > scratch_cap_) {

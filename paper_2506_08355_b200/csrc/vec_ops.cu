@@ -228,7 +228,8 @@ struct CgStartF {
     CgScalars s;
     double tol; int max_iter;
     __device__ void prologue(int) const {}
-    __device__ bool skip(int) const { return false; }
+    __device__ bool dead(int j) const { return s.m_live && j >= *s.m_live; }
+    __device__ bool skip(int j) const { return dead(j); }
     __device__ void row(int64_t i, int j, double (&a)[1]) const {
         const double v = b[i + j * lb];
         x[i + j * lx] = 0.0;
@@ -244,6 +245,11 @@ struct CgStartF {
         a[0] += v.x * v.x + v.y * v.y;
     }
     __device__ void fin(int j, const double (&sm)[1]) const {
+        if (dead(j)) {
+            s.rr[j] = s.bnorm[j] = 0.0;
+            s.iters[j] = s.broken[j] = s.active[j] = 0;
+            return;
+        }
         const double bn = sqrt(sm[0]);
         s.rr[j] = sm[0];
         s.bnorm[j] = bn;
@@ -680,6 +686,16 @@ void axpby(double a, const DMat& x, double b, const DMat& y) {
 void diag_scale(const double* d, const DMat& x, const DMat& y) {
     DiagF f{d, x.p, y.p, x.ld, y.ld};
     launch_cols("elementwise", x.rows, static_cast<int>(x.cols), f, 24.0 * x.rows * x.cols);
+}
+
+namespace {
+__global__ void k_set_int(int* p, int v) { *p = v; }
+}  // namespace
+
+void set_device_int(int* p, int v) {
+    LaunchScope ls("cg_vec");
+    k_set_int<<<1, 1, 0, Runtime::get().stream()>>>(p, v);
+    BOSP_LAUNCH_CHECK();
 }
 
 void cg_start(const DMat& b, const DMat& x, const DMat& r, const DMat& p, const CgScalars& s,
