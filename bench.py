@@ -218,8 +218,8 @@ def run_b200(args, world, rank, local, dist):
             bosp.profile_enable(None)
         return r, prof
 
-    for _ in range(args.warmup):
-        one_step()
+    for _ in range(args.warmup):  # same configuration as the timed steps (graphs recorded here)
+        one_step(args.roofline_kernel)
     barrier(dist)
     bosp.device_sync()
     bosp.launch_reset()

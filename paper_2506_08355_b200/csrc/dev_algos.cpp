@@ -1,3 +1,4 @@
+#include <chrono>
 #include <cstdio>
 // Device orchestration of the biorthogonalization and inner-CG building blocks.
 #include "dev_algos.hpp"
@@ -465,6 +466,7 @@ DevCgOutcome dev_cg(const LinearOperator& a, const DMat& rhs, const DMat& x, dou
                 c.m == mg && c.tol == tol && c.max_iter == max_iter && c.prof_family == rt.prof_family())
                 g = &c;
         if (!g) {
+            const auto tb = std::chrono::steady_clock::now();
             if (ws.graphs.size() >= 16) drop_graphs(ws.graphs);
             ws.graphs.emplace_back();
             g = &ws.graphs.back();
@@ -534,6 +536,7 @@ DevCgOutcome dev_cg(const LinearOperator& a, const DMat& rhs, const DMat& x, dou
             rt.set_capture_prof(nullptr);
             BOSP_CUDA(cudaGraphInstantiate(&g->exec, g->graph, 0));
             rt.graph_builds_ += 1;
+            rt.graph_build_s_ += std::chrono::duration<double>(std::chrono::steady_clock::now() - tb).count();
             if (std::getenv("BOSP_SYNC_STATS"))
                 std::fprintf(stderr, "[bosp] cg graph: op %p rhs %p x %p m %lld tol %g max_iter %lld (cache %zu)\n",
                              (const void*)a.impl(), (const void*)rhs.p, (const void*)x.p, (long long)m, tol,

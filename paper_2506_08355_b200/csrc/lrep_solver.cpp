@@ -642,8 +642,8 @@ EigenResult solve(const LinearOperator& k, const LinearOperator& m, const InnerP
     EigenResult res = assemble_result(st.dev(), k, m, ip, cfg, converged, out);
     st.dev().phases.acc[PH_ASSEMBLE] += secs(ta, Clock::now());
     if (std::getenv("BOSP_SYNC_STATS"))
-        std::fprintf(stderr, "[bosp] %lld host syncs, %.4f s waiting in them, %lld CG graphs built\n",
-                     (long long)rt.sync_count_, rt.sync_wait_s_, (long long)rt.graph_builds_);
+        std::fprintf(stderr, "[bosp] %lld host syncs, %.4f s waiting in them, %lld CG graphs built in %.4f s\n",
+                     (long long)rt.sync_count_, rt.sync_wait_s_, (long long)rt.graph_builds_, rt.graph_build_s_);
     if (phases_mode() != 0) {
         std::fprintf(stderr, "[bosp] phase %s times (s), %lld iterations:\n", phases_enabled() ? "wall" : "host",
                      (long long)st.iter());

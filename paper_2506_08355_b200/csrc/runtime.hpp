@@ -75,6 +75,7 @@ public:
     // BOSP_SYNC_STATS=1: host synchronisations and the host time spent waiting in them
     int64_t sync_count_ = 0;
     int64_t graph_builds_ = 0;
+    double graph_build_s_ = 0.0;
     double sync_wait_s_ = 0.0;
 
     // Scratch for split-K partials (fp64) -- valid until the next call; stream-ordered reuse is
