@@ -138,7 +138,8 @@ void launch_colred(const char* family, int64_t n, int ncols, const F& f, double 
     Runtime& rt = Runtime::get();
     static const int64_t waves = std::getenv("BOSP_COLRED_WAVES") ? std::atoll(std::getenv("BOSP_COLRED_WAVES")) : 4;
     const int64_t target = waves * rt.sm_count();  // 2..16 waves measured within 3% on config 2
-    int nchunks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n + 4095) / 4096,
+    // >= 1024 rows per chunk: narrow solves (1-8 live columns) still fill the machine
+    int nchunks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n + 1023) / 1024,
                                                                             (target + ncols - 1) / ncols)));
     const int64_t chunk = ((n + nchunks - 1) / nchunks + 1) & ~int64_t(1);  // even: pairs stay aligned
     double* partial = rt.scratch(static_cast<size_t>(nchunks) * ncols * K + static_cast<size_t>(K) * ncols);
