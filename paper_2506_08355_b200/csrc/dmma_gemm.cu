@@ -60,13 +60,13 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 
 // Load a "k-contiguous" tile: R columns (from ColList starting at col0, total ncols), rows
 // [k0, k0+kBK) clipped to kmax, into smem[c * kLdK + k].  Missing data is zero-filled.
-template <int R, int NT>
+template <int R, int NT, int BK = kBK>
 __device__ __forceinline__ void load_kcontig(double* smem, const ColList& cl, int col0, int ncols,
                                              int64_t k0, int64_t kmax) {
-    constexpr int kChunks = R * (kBK / 2);
+    constexpr int kChunks = R * (BK / 2);
     for (int ch = threadIdx.x; ch < kChunks; ch += NT) {
-        const int c = ch / (kBK / 2);
-        const int kp = ch % (kBK / 2);
+        const int c = ch / (BK / 2);
+        const int kp = ch % (BK / 2);
         const int64_t k = k0 + 2 * kp;
         const int gc = col0 + c;
         int bytes = 0;
@@ -76,16 +76,16 @@ __device__ __forceinline__ void load_kcontig(double* smem, const ColList& cl, in
             bytes = rem >= 2 ? 16 : 8;
             src = colptr(cl, gc) + k;
         }
-        cp_async16(smem + c * kLdK + 2 * kp, src, bytes);
+        cp_async16(smem + c * (BK + 4) + 2 * kp, src, bytes);
     }
 }
 
 // Load an "m-contiguous" tile for the NN product: kBK columns (k0..k0+kBK of A, clipped to
 // kcols) x BM rows (m0.., clipped to mmax) into smem[k * (BM+4) + m].
-template <int BM, int NT>
+template <int BM, int NT, int BK = kBK>
 __device__ __forceinline__ void load_mcontig(double* smem, const ColList& cl, int k0, int kcols,
                                              int64_t m0, int64_t mmax) {
-    constexpr int kChunks = kBK * (BM / 2);
+    constexpr int kChunks = BK * (BM / 2);
     for (int ch = threadIdx.x; ch < kChunks; ch += NT) {
         const int kk = ch / (BM / 2);
         const int mp = ch % (BM / 2);
@@ -319,10 +319,6 @@ void launch_gram(const GramJob* jobs, int njobs, int64_t n) {
 // instead of 16.  Each warp walks its own 4-row steps; warps fold through shared memory in a
 // fixed order, blocks through the split-K partial buffer (k_gram_reduce, 32 x 32 layout).
 constexpr int kRegWarps = 8;
-#ifndef BOSP_GRAM_UNROLL
-#define BOSP_GRAM_UNROLL 4
-#endif
-constexpr int kGramUnroll = BOSP_GRAM_UNROLL;
 
 template <int MT, int NTL, int GM, int GN>
 __global__ void __launch_bounds__(kRegWarps * 32) k_gram_regs(GramParams prm) {
@@ -462,6 +458,19 @@ void launch_gram_regs(const GramJob* jobs, int njobs, int64_t n) {
 // ------------------------------------------------------------------------------------------
 // Product kernel
 // ------------------------------------------------------------------------------------------
+// The product streams A from L2 (every column tile of Out re-reads the same row tile), so a
+// shallower stage (16 k) with 3 stages keeps 3 blocks per SM instead of 2: measured 24.6 ->
+// 29.0 TF/s at n = 2^21, k = b = 320 (the Gram, streaming fresh rows from HBM, keeps 3 x 32).
+#ifndef BOSP_PSTAGES
+#define BOSP_PSTAGES 3
+#endif
+#ifndef BOSP_PBK
+#define BOSP_PBK 16
+#endif
+constexpr int kPStages = BOSP_PSTAGES;
+constexpr int kPBK = BOSP_PBK;
+constexpr int kPLdK = kPBK + 4;
+
 struct ProductParams {
     ProductJob job[4];
     int64_t n;
@@ -477,8 +486,8 @@ k_product(ProductParams prm) {
     constexpr int MT = WTM / 8, NTL = WTN / 8;
     constexpr int LdM = BM + 4;
     extern __shared__ __align__(16) double smem[];
-    double* sa = smem;                        // [kStages][kBK][LdM]
-    double* sb = smem + kStages * kBK * LdM;  // [kStages][BN][kLdK]
+    double* sa = smem;                        // [kPStages][kPBK][LdM]
+    double* sb = smem + kPStages * kPBK * LdM;  // [kPStages][BN][kPLdK]
 
     const int jb = blockIdx.z;
     const ProductJob& job = prm.job[jb];
@@ -506,38 +515,38 @@ k_product(ProductParams prm) {
 #pragma unroll
         for (int j = 0; j < NTL; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-    const int nk = (kcols + kBK - 1) / kBK;
+    const int nk = (kcols + kPBK - 1) / kPBK;
 #pragma unroll
-    for (int s = 0; s < kStages - 1; ++s) {
+    for (int s = 0; s < kPStages - 1; ++s) {
         if (s < nk) {
-            load_mcontig<BM, NT>(sa + s * kBK * LdM, job.a, s * kBK, kcols, m0, prm.n);
-            load_kcontig<BN, NT>(sb + s * BN * kLdK, cl, n0, job.ncols, s * kBK, kcols);
+            load_mcontig<BM, NT, kPBK>(sa + s * kPBK * LdM, job.a, s * kPBK, kcols, m0, prm.n);
+            load_kcontig<BN, NT, kPBK>(sb + s * BN * kPLdK, cl, n0, job.ncols, s * kPBK, kcols);
         }
         cp_async_commit();
     }
     for (int it = 0; it < nk; ++it) {
-        cp_async_wait<kStages - 2>();
+        cp_async_wait<kPStages - 2>();
         __syncthreads();
-        const int st = it % kStages;
-        const double* a = sa + st * kBK * LdM;
-        const double* b = sb + st * BN * kLdK;
+        const int st = it % kPStages;
+        const double* a = sa + st * kPBK * LdM;
+        const double* b = sb + st * BN * kPLdK;
 #pragma unroll
-        for (int kk = 0; kk < kBK; kk += 4) {
+        for (int kk = 0; kk < kPBK; kk += 4) {
             double af[MT], bf[NTL];
 #pragma unroll
             for (int i = 0; i < MT; ++i) af[i] = a[(kk + tig) * LdM + wm0 + i * 8 + gid];
 #pragma unroll
-            for (int j = 0; j < NTL; ++j) bf[j] = b[(wn0 + j * 8 + gid) * kLdK + kk + tig];
+            for (int j = 0; j < NTL; ++j) bf[j] = b[(wn0 + j * 8 + gid) * kPLdK + kk + tig];
 #pragma unroll
             for (int i = 0; i < MT; ++i)
 #pragma unroll
                 for (int j = 0; j < NTL; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
         }
-        const int nxt = it + kStages - 1;
+        const int nxt = it + kPStages - 1;
         if (nxt < nk) {
-            const int sn = nxt % kStages;
-            load_mcontig<BM, NT>(sa + sn * kBK * LdM, job.a, nxt * kBK, kcols, m0, prm.n);
-            load_kcontig<BN, NT>(sb + sn * BN * kLdK, cl, n0, job.ncols, nxt * kBK, kcols);
+            const int sn = nxt % kPStages;
+            load_mcontig<BM, NT, kPBK>(sa + sn * kPBK * LdM, job.a, nxt * kPBK, kcols, m0, prm.n);
+            load_kcontig<BN, NT, kPBK>(sb + sn * BN * kPLdK, cl, n0, job.ncols, nxt * kPBK, kcols);
         }
         cp_async_commit();
     }
@@ -583,8 +592,8 @@ k_product_persist(ProductParams prm, int64_t total_tiles) {
     constexpr int MT = WTM / 8, NTL = WTN / 8;
     constexpr int LdM = BM + 4;
     extern __shared__ __align__(16) double smem[];
-    double* sa = smem;                        // [kStages][kBK][LdM]
-    double* sb = smem + kStages * kBK * LdM;  // [kStages][BN][kLdK]
+    double* sa = smem;                        // [kPStages][kPBK][LdM]
+    double* sb = smem + kPStages * kPBK * LdM;  // [kPStages][BN][kPLdK]
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int gid = lane >> 2, tig = lane & 3;
     const int wm0 = (warp / WN) * WTM, wn0 = (warp % WN) * WTN;
@@ -615,7 +624,7 @@ k_product_persist(ProductParams prm, int64_t total_tiles) {
     int64_t m00;
     int n00;
     decode(blockIdx.x, jb0, m00, n00);
-    const int nk = (prm.job[jb0].a.cols() + kBK - 1) / kBK;  // all jobs share k (asserted on the host)
+    const int nk = (prm.job[jb0].a.cols() + kPBK - 1) / kPBK;  // all jobs share k (asserted on the host)
     const int64_t total_steps = my_tiles * nk;
     auto issue = [&](int64_t step) {
         if (step < total_steps) {
@@ -626,9 +635,9 @@ k_product_persist(ProductParams prm, int64_t total_tiles) {
             int n0;
             decode(t, jb, m0, n0);
             const ProductJob& job = prm.job[jb];
-            const int st = static_cast<int>(step % kStages);
-            load_mcontig<BM, NT>(sa + st * kBK * LdM, job.a, ks * kBK, job.a.cols(), m0, prm.n);
-            load_kcontig<BN, NT>(sb + st * BN * kLdK, c_list(jb), n0, job.ncols, ks * kBK, job.a.cols());
+            const int st = static_cast<int>(step % kPStages);
+            load_mcontig<BM, NT, kPBK>(sa + st * kPBK * LdM, job.a, ks * kPBK, job.a.cols(), m0, prm.n);
+            load_kcontig<BN, NT, kPBK>(sb + st * BN * kPLdK, c_list(jb), n0, job.ncols, ks * kPBK, job.a.cols());
         }
         cp_async_commit();
     };
@@ -638,26 +647,26 @@ k_product_persist(ProductParams prm, int64_t total_tiles) {
 #pragma unroll
         for (int j = 0; j < NTL; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 #pragma unroll
-    for (int s = 0; s < kStages - 1; ++s) issue(s);
+    for (int s = 0; s < kPStages - 1; ++s) issue(s);
     for (int64_t step = 0; step < total_steps; ++step) {
-        cp_async_wait<kStages - 2>();
+        cp_async_wait<kPStages - 2>();
         __syncthreads();
-        const int st = static_cast<int>(step % kStages);
-        const double* a = sa + st * kBK * LdM;
-        const double* b = sb + st * BN * kLdK;
+        const int st = static_cast<int>(step % kPStages);
+        const double* a = sa + st * kPBK * LdM;
+        const double* b = sb + st * BN * kPLdK;
 #pragma unroll
-        for (int kk = 0; kk < kBK; kk += 4) {
+        for (int kk = 0; kk < kPBK; kk += 4) {
             double af[MT], bf[NTL];
 #pragma unroll
             for (int i = 0; i < MT; ++i) af[i] = a[(kk + tig) * LdM + wm0 + i * 8 + gid];
 #pragma unroll
-            for (int j = 0; j < NTL; ++j) bf[j] = b[(wn0 + j * 8 + gid) * kLdK + kk + tig];
+            for (int j = 0; j < NTL; ++j) bf[j] = b[(wn0 + j * 8 + gid) * kPLdK + kk + tig];
 #pragma unroll
             for (int i = 0; i < MT; ++i)
 #pragma unroll
                 for (int j = 0; j < NTL; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
         }
-        issue(step + kStages - 1);
+        issue(step + kPStages - 1);
         if (step % nk == nk - 1) {  // tile complete: registers -> Out, then start the next tile
             const int64_t t = blockIdx.x + (step / nk) * gridDim.x;
             int jb;
@@ -705,7 +714,7 @@ void launch_product(const ProductJob* jobs, int njobs, int64_t n) {
     }
     prm.n = n;
     constexpr int NT = WM * WN * 32;
-    constexpr size_t smem_pipe = sizeof(double) * kStages * (kBK * (BM + 4) + BN * kLdK);
+    constexpr size_t smem_pipe = sizeof(double) * kPStages * (kPBK * (BM + 4) + BN * kPLdK);
     constexpr size_t smem_epi = sizeof(double) * BN * (BM + 4);
     constexpr size_t smem = smem_pipe > smem_epi ? smem_pipe : smem_epi;
     static unsigned attr_mask = 0;
