@@ -166,6 +166,38 @@ def run_reference(args, world, rank, dist):
     print(json.dumps(line), flush=True)
 
 
+def dmma_roofline():
+    """The dense contractions of configs 3/5 (d = 320) on the fp64 tensor pipe: Rayleigh-Ritz
+    Gram U^T (K U) (n x 320)^T (n x 320) and Ritz pullback (n x 320)(320 x 192) at n = 128^3,
+    device-resident random data, against cuBLAS DGEMM 8192^3 measured in the same process."""
+    import torch
+    from paper_2506_08355_b200 import bosp
+    n, d, w = 128 ** 3, 320, 192
+    out = {"bound": "tensor (fp64 DMMA)", "unit": "TFLOP/s", "n": n}
+    g_ms = bosp.bench_blas("gram", n, d, d, reps=10)
+    p_ms = bosp.bench_blas("product", n, d, w, reps=10)
+    a = torch.randn(8192, 8192, dtype=torch.float64, device="cuda")
+    b = torch.randn(8192, 8192, dtype=torch.float64, device="cuda")
+    for _ in range(2):
+        torch.matmul(a, b)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(5):
+        torch.matmul(a, b)
+    e1.record()
+    torch.cuda.synchronize()
+    peak = 2 * 8192 ** 3 * 5 / (e0.elapsed_time(e1) * 1e-3) / 1e12
+    del a, b
+    torch.cuda.empty_cache()
+    gt = 2 * n * d * d / (g_ms * 1e-3) / 1e12
+    pt = 2 * n * d * w / (p_ms * 1e-3) / 1e12
+    out.update({"kernel": "k_gram<64,64> (G = A^T B, 320 x 320)", "achieved": gt, "peak": peak, "frac": gt / peak,
+                "gram_ms": g_ms, "product_kernel": "k_product<64,64> (A C, 320 -> 192)", "product_achieved": pt,
+                "product_frac": pt / peak, "product_ms": p_ms,
+                "peak_source": "cuBLAS DGEMM 8192^3 (torch.matmul fp64), best-effort same-process measurement"})
+    return out
+
+
 def run_b200(args, world, rank, local, dist):
     from paper_2506_08355_b200 import _lib, bosp
     from paper_2506_08355_b200 import dist as D
@@ -310,6 +342,29 @@ def run_b200(args, world, rank, local, dist):
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if "_fallback" not in peaks
                     else "fallback 6650 GB/s (B200_PROFILING.md)"}
 
+    # MGS-Biorth as a unit (biorth.cpp:102-109): one extra profiled solve (outside the timed
+    # region) in which every launch issued inside an MGS-Biorth call is timed on the device.
+    roof_mgs = None
+    if not args.no_kernel_rooflines:
+        _lib.lib().bosp_flush_l2(flush)
+        _, pm = one_step("mgs")
+        if pm and pm["launches"] and pm["ms"] > 0:
+            hbm = peaks.get("hbm_gbs", 6650.0)
+            ach = pm["region_bytes"] / (pm["ms"] * 1e-3) / 1e9
+            roof_mgs = {"kernel": "mgs_biorth (Gram + coefficient product + P^T Q check kernels)",
+                        "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                        "calls_per_solve": pm["region_calls"], "launches_per_solve": pm["launches"],
+                        "avg_call_us": pm["ms"] * 1e3 / max(1, pm["region_calls"]),
+                        "algorithmic_bytes_per_call": pm["region_bytes"] / max(1, pm["region_calls"]),
+                        "kernel_operand_gbs": pm["bytes"] / (pm["ms"] * 1e-3) / 1e9,
+                        "share_of_step": pm["ms"] / (ms_per_step),
+                        "bytes_note": "48 n m per call (SURVEY 8d: X, Y read + P, Q written = 32 n m, + 16 n m "
+                                      "for the P^T Q Gram of the second-pass test); kernel_operand_gbs counts "
+                                      "every operand each kernel reads/writes (the Gram re-reads X, Y)"}
+    roof_dmma = None
+    if rank == 0 and not args.no_kernel_rooflines:
+        roof_dmma = dmma_roofline()
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -335,6 +390,8 @@ def run_b200(args, world, rank, local, dist):
                        **({"partition_error": partition_error} if partition_error else {}),
                        "l2": "flushed between steps (512 MB memset)", "device": name, "sms": sms},
             "roofline": roof,
+            "roofline_mgs": roof_mgs,
+            "roofline_dmma": roof_dmma,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h)},
@@ -361,6 +418,8 @@ def main():
                     help="kernel family timed for the roofline (default: the dominant one, the CG SpMM)")
     ap.add_argument("--ref-iters", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-kernel-rooflines", action="store_true",
+                    help="skip the MGS-Biorth and fp64-DMMA kernel rooflines (extra, untimed work)")
     ap.add_argument("--partition", default="rows", choices=["rows", "replicas"],
                     help="N>1: row-partition one solve over the ranks (NCCL) or run N replicas")
     args = ap.parse_args()

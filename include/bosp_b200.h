@@ -242,10 +242,16 @@ bosp_status bosp_cholesky(int64_t n, const double* a, double* l, int32_t* ok);
  * Measurement hooks (bench.py): kernel-family CUDA-event timing and launch counting.
  * --------------------------------------------------------------------------------------- */
 /* Time every launch of one kernel family ("spmm", "gram", "product", "cg_vec", ...); NULL or
- * "" disables. */
+ * "" disables.  A composite-operation name ("mgs" = one MGS-Biorth call, biorth.cpp:102-109)
+ * times every launch issued inside that operation. */
 void bosp_profile_enable(const char* family);
 /* Synchronises; returns launches, summed device ms, algorithmic bytes and flops since enable. */
 void bosp_profile_collect(int64_t* launches, double* ms, double* bytes, double* flops);
+/* As bosp_profile_collect, plus the number of composite operations profiled and their summed
+ * algorithmic bytes (MGS-Biorth of n x m: 32 n m for X, Y in and P, Q out, + 16 n m for the
+ * P^T Q check of the second-pass test).  Either extra pointer may be NULL. */
+void bosp_profile_collect_regions(int64_t* launches, double* ms, double* bytes, double* flops,
+                                  int64_t* region_calls, double* region_bytes);
 /* Microbenchmark: apply `op` to a device-resident random n x ncols block `reps` times (after
  * one warm-up); returns the mean device time per apply in *ms (CUDA events). */
 bosp_status bosp_bench_apply(bosp_op op, int64_t ncols, int64_t reps, double* ms);

@@ -570,8 +570,11 @@ def profile_enable(family: str | None):
 
 def profile_collect():
     n, ms, b, f = C.c_int64(), C.c_double(), C.c_double(), C.c_double()
-    lib().bosp_profile_collect(C.byref(n), C.byref(ms), C.byref(b), C.byref(f))
-    return dict(launches=n.value, ms=ms.value, bytes=b.value, flops=f.value)
+    rc, rb = C.c_int64(), C.c_double()
+    lib().bosp_profile_collect_regions(C.byref(n), C.byref(ms), C.byref(b), C.byref(f),
+                                       C.byref(rc), C.byref(rb))
+    return dict(launches=n.value, ms=ms.value, bytes=b.value, flops=f.value,
+                region_calls=rc.value, region_bytes=rb.value)
 
 
 def launch_count():

@@ -575,15 +575,24 @@ void bosp_profile_enable(const char* family) {
 }
 
 void bosp_profile_collect(int64_t* launches, double* ms, double* bytes, double* flops) {
+    bosp_profile_collect_regions(launches, ms, bytes, flops, nullptr, nullptr);
+}
+
+void bosp_profile_collect_regions(int64_t* launches, double* ms, double* bytes, double* flops,
+                                  int64_t* region_calls, double* region_bytes) {
     try {
         auto r = bosp::Runtime::get().prof_collect();
         *launches = r.launches;
         *ms = r.ms;
         *bytes = r.bytes;
         *flops = r.flops;
+        if (region_calls) *region_calls = r.region_calls;
+        if (region_bytes) *region_bytes = r.region_bytes;
     } catch (...) {
         *launches = 0;
         *ms = *bytes = *flops = 0.0;
+        if (region_calls) *region_calls = 0;
+        if (region_bytes) *region_bytes = 0.0;
     }
 }
 

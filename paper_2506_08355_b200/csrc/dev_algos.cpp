@@ -159,6 +159,8 @@ DevBiorthOutcome dev_mgs_biorth(const DMat& x, const DMat& y, const DMat& p, con
     DevBiorthOutcome out;
     const int64_t m = x.cols, n = x.rows;
     if (m == 0) return out;
+    // profiled as one unit ("mgs"): X, Y in and P, Q out (32 n m) + the P^T Q check (16 n m)
+    ProfRegion region("mgs", classical ? 32.0 * n * m : 48.0 * n * m);
     // Columns are processed in order.  Runs of well-conditioned columns go through the Gram /
     // coefficient recurrence (level-3 on the DMMA pipe); a column whose residual cancels
     // (nearly dependent on the kept pairs) is materialised in n-space and projected

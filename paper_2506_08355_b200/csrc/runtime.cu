@@ -129,10 +129,25 @@ void Runtime::prof_enable(const std::string& family) {
     prof_events_.clear();
     timer_pending_.clear();
     graph_samples_ = ProfReport{0, 0.0, 0.0, 0.0};
+    region_depth_ = 0;
 }
 
 bool Runtime::prof_on(const char* family) const {
-    return !prof_family_.empty() && prof_family_ == family;
+    return !prof_family_.empty() && (region_depth_ > 0 || prof_family_ == family);
+}
+
+bool Runtime::region_open(const char* name) {
+    if (prof_family_.empty() || prof_family_ != name) return false;
+    ++region_depth_;
+    return true;
+}
+
+void Runtime::region_close(double algo_bytes) {
+    if (region_depth_ > 0) --region_depth_;
+    if (region_depth_ == 0) {
+        graph_samples_.region_calls += 1;
+        graph_samples_.region_bytes += algo_bytes;
+    }
 }
 
 cudaEvent_t Runtime::take_event() {

@@ -107,8 +107,18 @@ public:
     bool prof_active() const { return !prof_family_.empty(); }
     void prof_begin(const char* family, double algo_bytes, double algo_flops);
     void prof_end(const char* family);
-    struct ProfReport { int64_t launches; double ms; double bytes; double flops; };
+    // launches/ms/bytes/flops: the timed kernels (each with its own operand bytes);
+    // region_calls/region_bytes: composite operations (ProfRegion) and their algorithmic bytes.
+    struct ProfReport {
+        int64_t launches; double ms; double bytes; double flops;
+        int64_t region_calls = 0; double region_bytes = 0.0;
+    };
     ProfReport prof_collect();  // synchronises, sums elapsed times, resets
+    // Composite-operation profiling: while a region named like the profiled family is open,
+    // every launch inside it is timed (whatever its own family); at close the region credits
+    // its algorithmic bytes once.  Nested regions of the same name count once (outermost).
+    bool region_open(const char* name);
+    void region_close(double algo_bytes);
     // Device-clock timing for kernels that may run inside CUDA graphs (event nodes are not
     // allowed in conditional bodies): the kernel writes (max of ~start, max of end) %globaltimer
     // into a 2-word slot that a memset resets before each launch.  A launch recorded into a
@@ -158,6 +168,7 @@ private:
     int64_t timer_next_ = 0;
     static constexpr int64_t kTimerSlots = 1 << 15;
     ProfReport graph_samples_{0, 0.0, 0.0, 0.0};
+    int region_depth_ = 0;
     void read_timer_samples(const std::vector<ProfPair>& pairs);
     std::vector<cudaEvent_t> event_pool_;
     cudaEvent_t take_event();
@@ -170,6 +181,17 @@ struct LaunchScope {
     // events = false: the kernel times itself with a device-clock slot (Runtime::timer_begin)
     LaunchScope(const char* fam, double bytes = 0.0, double flops = 0.0, bool events = true);
     ~LaunchScope();
+};
+
+// RAII: a composite operation (e.g. one MGS-Biorth call) profiled as a unit when its name is the
+// profiled family; `algo_bytes` is the operation's algorithmic traffic.
+struct ProfRegion {
+    bool open;
+    double algo_bytes;
+    ProfRegion(const char* name, double bytes) : open(Runtime::get().region_open(name)), algo_bytes(bytes) {}
+    ~ProfRegion() {
+        if (open) Runtime::get().region_close(algo_bytes);
+    }
 };
 
 // Owning device block: rows x capacity columns, column stride ld = rows rounded up to 32
