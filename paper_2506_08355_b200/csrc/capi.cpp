@@ -666,6 +666,12 @@ bosp_status bosp_bench_blas(int32_t kind, int64_t n, int64_t a, int64_t b, int64
                                            {bosp::ColList(x.view()), bosp::ColList(y.view()), c2.data(), c2.ld()},
                                            {bosp::ColList(y.view()), bosp::ColList(y.view()), c3.data(), c3.ld()}};
             *ms = time_reps(reps, [&] { bosp::gram(jobs, 3, n); });
+        } else if (kind == 4) {  // the same three blocks as one symmetric Gram of Z = [X | Y]
+            bosp::DBlock z(a + b, a + b);
+            bosp::GramJob job{bosp::ColList(x.view()).add(y.view()), bosp::ColList(x.view()).add(y.view()),
+                              z.data(), z.ld()};
+            job.sym = true;
+            *ms = time_reps(reps, [&] { bosp::gram(&job, 1, n); });
         }
         else
             *ms = time_reps(reps, [&] {

@@ -14,6 +14,9 @@ struct GramJob {
     ColList a, b;
     double* g;
     int64_t ldg;
+    // a and b are the same columns (G = A^T A): only the upper-triangular tiles are computed and
+    // G(i, j), i <= j, is mirrored to G(j, i) -- G exactly symmetric, ~half the DMMA work.
+    bool sym = false;
 };
 void gram(const GramJob* jobs, int njobs, int64_t n);
 inline void gram(const ColList& a, const ColList& b, int64_t n, double* g, int64_t ldg) {

@@ -125,6 +125,27 @@ void apply_coefs(const DMat& x, const DMat& y, const DenseMatrix& a, const Dense
 void pair_grams(const DMat& x, const DMat& y, const InnerProduct& ip, DenseMatrix& gxx,
                 DenseMatrix& gxy, DenseMatrix& gyy) {
     const int64_t m = x.cols;
+    if (!ip.weighted() && !std::getenv("BOSP_PAIR_GRAM3")) {
+        // one symmetric Gram of Z = [X | Y]: X and Y streamed once, upper tiles only;
+        // Z^T Z = [[X^T X, X^T Y], [., Y^T Y]]
+        DBlock g(2 * m, 2 * m);
+        GramJob job{ColList(x).add(y), ColList(x).add(y), g.data(), g.ld()};
+        job.sym = true;
+        gram(&job, 1, x.rows);
+        Runtime::get().allreduce(g.data(), g.ld() * 2 * m);
+        DenseMatrix z(2 * m, 2 * m);
+        to_host(g.view(), z.data(), 2 * m);
+        gxx = DenseMatrix(m, m);
+        gxy = DenseMatrix(m, m);
+        gyy = DenseMatrix(m, m);
+        for (int64_t j = 0; j < m; ++j)
+            for (int64_t i = 0; i < m; ++i) {
+                gxx(i, j) = z(i, j);
+                gxy(i, j) = z(i, m + j);
+                gyy(i, j) = z(m + i, m + j);
+            }
+        return;
+    }
     DBlock g(m, 3 * m);
     if (!ip.weighted()) {
         GramJob jobs[3] = {{ColList(x), ColList(x), g.data(), g.ld()},

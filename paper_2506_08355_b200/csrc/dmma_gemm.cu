@@ -109,12 +109,41 @@ struct GramParams {
     GramJob job[4];
     int64_t n;
     int tiles_n[4];      // column tiles per job
-    int tiles[4];        // tiles per job
+    int tiles[4];        // tiles per job (sym: upper-triangular tiles only)
+    int sym[4];          // job is G = A^T A: tile t -> upper pair, mirrored stores
     int splits;
     int64_t chunk;       // rows per split (multiple of kBK)
     double* partial;     // [job][split][tile][BM*BN]
     int64_t job_stride;  // doubles per job in partial
 };
+
+// Tile index -> (tm, tn).  Symmetric jobs enumerate the upper triangle row by row
+// (tm <= tn, T tiles per side).
+__device__ __forceinline__ void gram_tile(const GramParams& prm, int jb, int tile, int& tm, int& tn) {
+    const int T = prm.tiles_n[jb];
+    if (!prm.sym[jb]) {
+        tm = tile / T;
+        tn = tile % T;
+        return;
+    }
+    int r = 0, t = tile;
+    while (t >= T - r) {
+        t -= T - r;
+        ++r;
+    }
+    tm = r;
+    tn = r + t;
+}
+
+// Store one reduced Gram element; symmetric jobs store (m, n) for m <= n and mirror it.
+__device__ __forceinline__ void gram_store(const GramJob& job, bool sym, int m, int nn, double v) {
+    if (!sym) {
+        job.g[m + static_cast<int64_t>(nn) * job.ldg] = v;
+    } else if (m <= nn) {
+        job.g[m + static_cast<int64_t>(nn) * job.ldg] = v;
+        job.g[nn + static_cast<int64_t>(m) * job.ldg] = v;
+    }
+}
 
 template <int BM, int BN, int WM, int WN>
 __global__ void __launch_bounds__(WM * WN * 32)
@@ -130,7 +159,8 @@ k_gram(GramParams prm) {
     const GramJob& job = prm.job[jb];
     const int tile = blockIdx.x;
     if (tile >= prm.tiles[jb]) return;
-    const int tm = tile / prm.tiles_n[jb], tn = tile % prm.tiles_n[jb];
+    int tm, tn;
+    gram_tile(prm, jb, tile, tm, tn);
     const int m0 = tm * BM, n0 = tn * BN;
     const int acols = job.a.cols(), bcols = job.b.cols();
     const int64_t kb = static_cast<int64_t>(blockIdx.y) * prm.chunk;
@@ -191,8 +221,8 @@ k_gram(GramParams prm) {
                 const int m = m0 + wm0 + i * 8 + gid;
                 const int nn = n0 + wn0 + j * 8 + 2 * tig;
                 if (m < acols) {
-                    if (nn < bcols) job.g[m + static_cast<int64_t>(nn) * job.ldg] = acc[i][j][0];
-                    if (nn + 1 < bcols) job.g[m + static_cast<int64_t>(nn + 1) * job.ldg] = acc[i][j][1];
+                    if (nn < bcols) gram_store(job, prm.sym[jb], m, nn, acc[i][j][0]);
+                    if (nn + 1 < bcols) gram_store(job, prm.sym[jb], m, nn + 1, acc[i][j][1]);
                 }
             }
         return;
@@ -243,10 +273,12 @@ __global__ void __launch_bounds__(kRedElems * kRedGroups) k_gram_reduce(GramPara
     for (int g = 0; g < kRedGroups; ++g) s += part_sum[g][el];
     const int tile = static_cast<int>(e / (BM * BN));
     const int r = static_cast<int>(e % (BM * BN));
-    const int m = (tile / prm.tiles_n[jb]) * BM + r % BM;
-    const int nn = (tile % prm.tiles_n[jb]) * BN + r / BM;
+    int tm, tn;
+    gram_tile(prm, jb, tile, tm, tn);
+    const int m = tm * BM + r % BM;
+    const int nn = tn * BN + r / BM;
     if (m >= job.a.cols() || nn >= job.b.cols()) return;
-    job.g[m + nn * job.ldg] = s;
+    gram_store(job, prm.sym[jb], m, nn, s);
 }
 
 template <int BM, int BN, int WM, int WN>
@@ -257,7 +289,9 @@ void launch_gram(const GramJob* jobs, int njobs, int64_t n) {
     for (int j = 0; j < njobs; ++j) {
         prm.job[j] = jobs[j];
         prm.tiles_n[j] = (jobs[j].b.cols() + BN - 1) / BN;
-        prm.tiles[j] = ((jobs[j].a.cols() + BM - 1) / BM) * prm.tiles_n[j];
+        prm.sym[j] = jobs[j].sym && BM == BN;
+        const int tm = (jobs[j].a.cols() + BM - 1) / BM;
+        prm.tiles[j] = prm.sym[j] ? tm * (tm + 1) / 2 : tm * prm.tiles_n[j];
         max_tiles = std::max(max_tiles, prm.tiles[j]);
     }
     prm.n = n;
@@ -292,8 +326,11 @@ void launch_gram(const GramJob* jobs, int njobs, int64_t n) {
     if (rt.first_use(attr_mask))
         BOSP_CUDA(cudaFuncSetAttribute(k_gram<BM, BN, WM, WN>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const double flops = 2.0 * n * (double)jobs[0].a.cols() * jobs[0].b.cols() * njobs;
-    const double bytes = 8.0 * n * (double)(jobs[0].a.cols() + jobs[0].b.cols()) * njobs;
+    double flops = 0.0, bytes = 0.0;
+    for (int j = 0; j < njobs; ++j) {
+        flops += 2.0 * n * (double)jobs[j].a.cols() * jobs[j].b.cols() * (prm.sym[j] ? 0.5 : 1.0);
+        bytes += 8.0 * n * (double)(jobs[j].sym ? jobs[j].a.cols() : jobs[j].a.cols() + jobs[j].b.cols());
+    }
     {
         LaunchScope ls("gram", bytes, flops);
         dim3 grid(max_tiles, prm.splits, njobs);
@@ -354,7 +391,9 @@ __global__ void __launch_bounds__(kRegWarps * 32) k_gram_regs(GramParams prm) {
 #pragma unroll
         for (int j = 0; j < NS; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     const int64_t kb = static_cast<int64_t>(blockIdx.x) * prm.chunk;
-    const int64_t ke = min(prm.n, kb + prm.chunk);
+    const bool sym = prm.sym[jb] != 0;
+    // symmetric job: a warp group wholly below the diagonal has nothing to compute
+    const int64_t ke = (sym && gm > gn) ? kb : min(prm.n, kb + prm.chunk);
     // U consecutive 4-row steps per iteration, every load issued before the first DMMA: ~16
     // independent loads in flight per lane whatever the tile size
     constexpr int U = (16 / (MS + NS)) < 1 ? 1 : (16 / (MS + NS)) > 8 ? 8 : 16 / (MS + NS);
@@ -374,7 +413,8 @@ __global__ void __launch_bounds__(kRegWarps * 32) k_gram_regs(GramParams prm) {
 #pragma unroll
             for (int i = 0; i < MS; ++i)
 #pragma unroll
-                for (int j = 0; j < NS; ++j) dmma(acc[i][j][0], acc[i][j][1], af[u][i], bf[u][j]);
+                for (int j = 0; j < NS; ++j)
+                    if (!sym || gm * MS + i <= gn * NS + j) dmma(acc[i][j][0], acc[i][j][1], af[u][i], bf[u][j]);
     }
     double* mine = red + warp * (SM * SN);
 #pragma unroll
@@ -397,7 +437,7 @@ __global__ void __launch_bounds__(kRegWarps * 32) k_gram_regs(GramParams prm) {
             for (int w = 0; w < WPG; ++w) v += red[(g * WPG + w) * (SM * SN) + loc];
         }
         if (prm.splits == 1) {
-            if (m < acols && nn < bcols) job.g[m + static_cast<int64_t>(nn) * job.ldg] = v;
+            if (m < acols && nn < bcols) gram_store(job, sym, m, nn, v);
         } else {
             part[m + nn * LDP] = v;
         }
@@ -415,6 +455,7 @@ void launch_gram_regs(const GramJob* jobs, int njobs, int64_t n) {
         prm.job[j] = jobs[j];
         prm.tiles_n[j] = 1;
         prm.tiles[j] = 1;
+        prm.sym[j] = jobs[j].sym && MT == NTL && GM == GN;
     }
     prm.n = n;
     constexpr int U = (16 / (MS + NS)) < 1 ? 1 : (16 / (MS + NS)) > 8 ? 8 : 16 / (MS + NS);
@@ -438,8 +479,8 @@ void launch_gram_regs(const GramJob* jobs, int njobs, int64_t n) {
                                        static_cast<int>(smem)));
     double flops = 0.0, bytes = 0.0;
     for (int j = 0; j < njobs; ++j) {
-        flops += 2.0 * n * jobs[j].a.cols() * jobs[j].b.cols();
-        bytes += 8.0 * n * (jobs[j].a.cols() + jobs[j].b.cols());
+        flops += 2.0 * n * jobs[j].a.cols() * jobs[j].b.cols() * (prm.sym[j] ? 0.5 : 1.0);
+        bytes += 8.0 * n * (jobs[j].sym ? jobs[j].a.cols() : jobs[j].a.cols() + jobs[j].b.cols());
     }
     {
         LaunchScope ls("gram", bytes, flops);
