@@ -356,6 +356,13 @@ void launch_gram(const GramJob* jobs, int njobs, int64_t n) {
 // instead of 16.  Each warp walks its own 4-row steps; warps fold through shared memory in a
 // fixed order, blocks through the split-K partial buffer (k_gram_reduce, 32 x 32 layout).
 constexpr int kRegWarps = 8;
+// k-steps per iteration of the register Gram: ~16 independent fragments in flight per lane,
+// even (k-steps come in pairs from one 16-byte load)
+// single-group layouts wider than 4 x 4 fragment tiles fold the warps sequentially
+template <int G, int MS, int NS>
+constexpr bool kGramSeqFold = G == 1 && MS * NS > 16;
+template <int F>
+constexpr int kGramU = (16 / F) < 2 ? 2 : (16 / F) > 8 ? 8 : ((16 / F) & ~1);
 
 template <int MT, int NTL, int GM, int GN>
 __global__ void __launch_bounds__(kRegWarps * 32) k_gram_regs(GramParams prm) {
@@ -394,19 +401,45 @@ __global__ void __launch_bounds__(kRegWarps * 32) k_gram_regs(GramParams prm) {
     const bool sym = prm.sym[jb] != 0;
     // symmetric job: a warp group wholly below the diagonal has nothing to compute
     const int64_t ke = (sym && gm > gn) ? kb : min(prm.n, kb + prm.chunk);
-    // U consecutive 4-row steps per iteration, every load issued before the first DMMA: ~16
-    // independent loads in flight per lane whatever the tile size
-    constexpr int U = (16 / (MS + NS)) < 1 ? 1 : (16 / (MS + NS)) > 8 ? 8 : 16 / (MS + NS);
+    const bool same_ab = sym && gm == gn;
+    // U 4-row k-steps per iteration (U even), every load issued before the first DMMA.  The
+    // Gram sums over rows in any order, so a k-step need not be 4 consecutive rows: lane tig
+    // loads rows (2 tig, 2 tig + 1) of each 8-row block as one 16-byte load and feeds .x to
+    // k-step u, .y to k-step u + 1 (A and B paired identically) -- half the load instructions,
+    // and each warp load covers 64 contiguous bytes of 8 columns.
+    constexpr int U = kGramU<MS + NS>;
     for (int64_t k0 = kb + 4 * U * wig; k0 < ke; k0 += 4 * U * WPG) {
         double af[U][MS], bf[U][NS];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int64_t r = k0 + 4 * u + tig;
-            const bool vr = r < ke;
+        for (int u = 0; u < U; u += 2) {
+            const int64_t r = k0 + 4 * u + 2 * tig;
+            const bool v2 = r + 1 < ke, v1 = r < ke;
 #pragma unroll
-            for (int i = 0; i < MS; ++i) af[u][i] = (pa[i] && vr) ? __ldg(pa[i] + r) : 0.0;
+            for (int i = 0; i < MS; ++i) {
+                double2 t = make_double2(0.0, 0.0);
+                if (pa[i] && v2) t = __ldg(reinterpret_cast<const double2*>(pa[i] + r));
+                else if (pa[i] && v1) t.x = __ldg(pa[i] + r);
+                af[u][i] = t.x;
+                af[u + 1][i] = t.y;
+            }
+            if constexpr (MS == NS) {
+                if (same_ab) {  // G = A^T A on the diagonal group: B fragments are the A fragments
 #pragma unroll
-            for (int j = 0; j < NS; ++j) bf[u][j] = (pb[j] && vr) ? __ldg(pb[j] + r) : 0.0;
+                    for (int j = 0; j < NS; ++j) {
+                        bf[u][j] = af[u][j];
+                        bf[u + 1][j] = af[u + 1][j];
+                    }
+                    continue;
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < NS; ++j) {
+                double2 t = make_double2(0.0, 0.0);
+                if (pb[j] && v2) t = __ldg(reinterpret_cast<const double2*>(pb[j] + r));
+                else if (pb[j] && v1) t.x = __ldg(pb[j] + r);
+                bf[u][j] = t.x;
+                bf[u + 1][j] = t.y;
+            }
         }
 #pragma unroll
         for (int u = 0; u < U; ++u)
@@ -414,24 +447,46 @@ __global__ void __launch_bounds__(kRegWarps * 32) k_gram_regs(GramParams prm) {
             for (int i = 0; i < MS; ++i)
 #pragma unroll
                 for (int j = 0; j < NS; ++j)
-                    if (!sym || gm * MS + i <= gn * NS + j) dmma(acc[i][j][0], acc[i][j][1], af[u][i], bf[u][j]);
+                    if ((!sym || gm * MS + i <= gn * NS + j) && (gm * MS + i) * 8 < acols &&
+                        (gn * NS + j) * 8 < bcols)  // skip pairs of all-padding fragment tiles
+                        dmma(acc[i][j][0], acc[i][j][1], af[u][i], bf[u][j]);
     }
-    double* mine = red + warp * (SM * SN);
+    if constexpr (kGramSeqFold<G, MS, NS>) {
+        // wide single-group tiles: warps add into one tile in warp order (same fixed order as
+        // the per-warp buffers, 1/8 of the shared memory)
+        for (int w = 0; w < kRegWarps; ++w) {
+            if (warp == w) {
 #pragma unroll
-    for (int i = 0; i < MS; ++i)
+                for (int i = 0; i < MS; ++i)
 #pragma unroll
-        for (int j = 0; j < NS; ++j) {
-            const int m = i * 8 + gid, nn = j * 8 + 2 * tig;
-            mine[m + nn * SM] = acc[i][j][0];
-            mine[m + (nn + 1) * SM] = acc[i][j][1];
+                    for (int j = 0; j < NS; ++j) {
+                        const int m = i * 8 + gid, nn = j * 8 + 2 * tig;
+                        red[m + nn * SM] = (w == 0 ? 0.0 : red[m + nn * SM]) + acc[i][j][0];
+                        red[m + (nn + 1) * SM] = (w == 0 ? 0.0 : red[m + (nn + 1) * SM]) + acc[i][j][1];
+                    }
+            }
+            __syncthreads();
         }
-    __syncthreads();
+    } else {
+        double* mine = red + warp * (SM * SN);
+#pragma unroll
+        for (int i = 0; i < MS; ++i)
+#pragma unroll
+            for (int j = 0; j < NS; ++j) {
+                const int m = i * 8 + gid, nn = j * 8 + 2 * tig;
+                mine[m + nn * SM] = acc[i][j][0];
+                mine[m + (nn + 1) * SM] = acc[i][j][1];
+            }
+        __syncthreads();
+    }
     double* part = prm.partial + jb * prm.job_stride + static_cast<int64_t>(blockIdx.x) * (LDP * LDP);
     for (int e = threadIdx.x; e < TM * TN; e += kRegWarps * 32) {
         const int m = e % TM, nn = e / TM;
         const int om = m / SM, on = nn / SN;  // owning group
         double v = 0.0;
-        if (om < GM && on < GN) {
+        if constexpr (kGramSeqFold<G, MS, NS>) {
+            v = red[m + nn * SM];
+        } else if (om < GM && on < GN) {
             const int g = om * GN + on, loc = (m - om * SM) + (nn - on * SN) * SM;
 #pragma unroll
             for (int w = 0; w < WPG; ++w) v += red[(g * WPG + w) * (SM * SN) + loc];
@@ -458,12 +513,24 @@ void launch_gram_regs(const GramJob* jobs, int njobs, int64_t n) {
         prm.sym[j] = jobs[j].sym && MT == NTL && GM == GN;
     }
     prm.n = n;
-    constexpr int U = (16 / (MS + NS)) < 1 ? 1 : (16 / (MS + NS)) > 8 ? 8 : 16 / (MS + NS);
+    constexpr int U = kGramU<MS + NS>;
     constexpr int64_t kStep = 4 * U * WPG;  // rows per warp-group iteration
     const int64_t steps = (n + 4 * kRegWarps - 1) / (4 * kRegWarps);
-    // one full wave (2 resident blocks per SM at ~100 registers); 3-8 waves measured 30-100 %
-    // slower on config 2's 20-column Grams (more partials, tail)
-    static const int64_t waves = std::getenv("BOSP_GRAM_WAVES") ? std::atoi(std::getenv("BOSP_GRAM_WAVES")) : 2;
+    // one full wave of resident blocks (2 per SM at ~100 registers, 1 for the wide symmetric
+    // layouts); 3-8 waves measured 30-100 % slower on config 2's 20-column Grams (more partials,
+    // tail).  BOSP_GRAM_WAVES overrides the blocks per SM.
+    constexpr size_t smem_need = sizeof(double) * (kGramSeqFold<GM * GN, MS, NS> ? 1 : kRegWarps) * MS * 8 * NS * 8;
+    static int resident[64] = {0};
+    if (resident[rt.device() & 63] == 0) {
+        int r = 0;
+        BOSP_CUDA(cudaFuncSetAttribute(k_gram_regs<MT, NTL, GM, GN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem_need)));
+        BOSP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, k_gram_regs<MT, NTL, GM, GN>, kRegWarps * 32,
+                                                                smem_need));
+        resident[rt.device() & 63] = std::max(1, std::min(r, 2));
+    }
+    static const int64_t waves_env = std::getenv("BOSP_GRAM_WAVES") ? std::atoi(std::getenv("BOSP_GRAM_WAVES")) : 0;
+    const int64_t waves = waves_env > 0 ? waves_env : resident[rt.device() & 63];
     int splits = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(
         (waves * rt.sm_count() + njobs - 1) / njobs, steps / 8)));  // >= 8 steps of work per block
     const int64_t per = ((n + splits - 1) / splits + kStep - 1) / kStep;
@@ -472,7 +539,7 @@ void launch_gram_regs(const GramJob* jobs, int njobs, int64_t n) {
     prm.splits = std::max(1, splits);
     prm.job_stride = static_cast<int64_t>(prm.splits) * LDP * LDP;
     prm.partial = rt.scratch(static_cast<size_t>(prm.job_stride) * njobs);
-    constexpr size_t smem = sizeof(double) * kRegWarps * MS * 8 * NS * 8;
+    constexpr size_t smem = sizeof(double) * (kGramSeqFold<GM * GN, MS, NS> ? 1 : kRegWarps) * MS * 8 * NS * 8;
     static unsigned attr_mask = 0;
     if (rt.first_use(attr_mask))
         BOSP_CUDA(cudaFuncSetAttribute(k_gram_regs<MT, NTL, GM, GN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1123,6 +1190,11 @@ void gram(const GramJob* jobs, int njobs, int64_t n) {
     const int lim = wide_max;
     if (amax <= lim && bmax <= lim && regs) {
         const int mt = (amax + 7) / 8, nt = (bmax + 7) / 8;
+        // a symmetric Gram up to 48 columns ([X | Y] of MGS-Biorth, m <= 24): every warp holds
+        // all upper fragment pairs and loads each column fragment once (the 2 x 2 group layout
+        // re-loads every fragment per group)
+        if (njobs == 1 && jobs[0].sym && mt == nt && (mt == 5 || mt == 6) && !std::getenv("BOSP_GRAM_SYM_GROUPS"))
+            return mt == 5 ? launch_gram_regs<5, 5>(jobs, njobs, n) : launch_gram_regs<6, 6>(jobs, njobs, n);
         if (mt <= 4 && nt <= 4) {
             switch (mt * 4 + nt) {
 #define BOSP_G(M, N) case M * 4 + N: return launch_gram_regs<M, N>(jobs, njobs, n);

@@ -1,0 +1,51 @@
+#!/usr/bin/env python
+"""Summarise an ncu --set full report (one or more kernels) into the metrics DESIGN.md cites.
+
+  python tools/ncu_summary.py report.ncu-rep [more.ncu-rep ...] > profiles/<name>.txt
+"""
+import csv
+import io
+import subprocess
+import sys
+
+WANT = [
+    ("gpu__time_duration.sum", "duration"),
+    ("sm__cycles_elapsed.avg.per_second", "SM clock"),
+    ("dram__bytes_read.sum", "DRAM read"),
+    ("dram__bytes_write.sum", "DRAM write"),
+    ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput % of peak"),
+    ("sm__ops_path_tensor_src_fp64.sum.per_second", "fp64 tensor ops/s (DMMA flops)"),
+    ("sm__ops_path_tensor_src_fp64.avg.pct_of_peak_sustained_elapsed", "fp64 tensor path % of peak"),
+    ("sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active", "DMMA pipe active %"),
+    ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "FP64 (non-tensor) pipe active %"),
+    ("sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active", "shared pipe active %"),
+    ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "shared bank conflicts"),
+    ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM throughput %"),
+    ("sm__warps_active.avg.pct_of_peak_sustained_active", "achieved occupancy %"),
+    ("launch__registers_per_thread", "registers/thread"),
+    ("launch__grid_size", "grid"),
+    ("launch__block_size", "block"),
+    ("lts__t_sector_hit_rate.pct", "L2 hit rate %"),
+]
+
+
+def main():
+    for rep in sys.argv[1:]:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+        rows = list(csv.reader(io.StringIO(out)))
+        if len(rows) < 3:
+            print(f"# {rep}: no data")
+            continue
+        head, units = rows[0], rows[1]
+        idx = {h: i for i, h in enumerate(head)}
+        for r in rows[2:]:
+            print(f"# {rep}")
+            print(f"kernel: {r[idx['Kernel Name']]}")
+            for key, label in WANT:
+                if key in idx:
+                    print(f"  {label:34s} {r[idx[key]]:>18s} {units[idx[key]]}   ({key})")
+            print()
+
+
+if __name__ == "__main__":
+    main()
