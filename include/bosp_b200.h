@@ -205,6 +205,10 @@ bosp_status bosp_block_inner(bosp_op B, int64_t n, int64_t a, int64_t b, const d
  * column segments; out = [XᵀY | XᵀX | YᵀY] column-major. */
 bosp_status bosp_test_gram_jobs(int64_t n, int64_t a, int64_t b, const double* x, const double* y, int32_t nseg,
                                 int32_t njobs, double* out);
+/* Test hook (no reference counterpart): the solver's fused MGS-Biorth application -- P = X A,
+ * Q = Y B (X, Y n x k; A, B k x kb; k, kb <= 32) and g = P^T Q (kb x kb) from the same kernel. */
+bosp_status bosp_test_biorth_apply(int64_t n, int64_t k, int64_t kb, const double* x, const double* y,
+                                   const double* a, const double* b, double* p, double* q, double* g);
 bosp_status bosp_block_product(int64_t n, int64_t a, int64_t b, const double* x, const double* c,
                                double* out);
 /* Y (n x b) -= X C  (block_axpy, kernels.cpp:89-104). */

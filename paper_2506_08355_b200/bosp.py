@@ -427,6 +427,18 @@ def _test_gram_jobs(x, y, nseg=1, njobs=3):
             out[a * b + a * a:].reshape((b, b), order="F"))
 
 
+def _test_biorth_apply(x, y, a, b):
+    """Test hook: the fused MGS-Biorth application -> (P = X A, Q = Y B, P^T Q)."""
+    x, y, a, b = _f(x), _f(y), _f(a), _f(b)
+    n, k, kb = x.shape[0], x.shape[1], a.shape[1]
+    p = np.zeros((n, kb), order="F")
+    q = np.zeros((n, kb), order="F")
+    g = np.zeros((kb, kb), order="F")
+    check(lib().bosp_test_biorth_apply(C.c_int64(n), C.c_int64(k), C.c_int64(kb), _p(x), _p(y), _p(a), _p(b),
+                                       _p(p), _p(q), _p(g)))
+    return p, q, g
+
+
 def block_product(x, c):
     x, c = _f(x), _f(c)
     if x.shape[1] != c.shape[0]:

@@ -465,6 +465,22 @@ bosp_status bosp_test_gram_jobs(int64_t n, int64_t a, int64_t b, const double* x
     });
 }
 
+bosp_status bosp_test_biorth_apply(int64_t n, int64_t k, int64_t kb, const double* x, const double* y,
+                                   const double* a, const double* b, double* p, double* q, double* g) {
+    return guarded([&] {
+        bosp::DBlock xd(n, k), yd(n, k), pd(n, kb), qd(n, kb), cd(k, 2 * kb), gd(kb, kb);
+        bosp::to_device(x, n, k, n, xd.view());
+        bosp::to_device(y, n, k, n, yd.view());
+        bosp::to_device(a, k, kb, k, cd.cols(0, kb));
+        bosp::to_device(b, k, kb, k, cd.cols(kb, kb));
+        bosp::biorth_apply(xd.view(), yd.view(), cd.data(), cd.data() + kb * cd.ld(), cd.ld(), static_cast<int>(kb),
+                           pd.view(), qd.view(), gd.data(), gd.ld());
+        bosp::to_host(pd.view(), p, n);
+        bosp::to_host(qd.view(), q, n);
+        bosp::to_host(gd.view(), g, kb);
+    });
+}
+
 bosp_status bosp_block_product(int64_t n, int64_t a, int64_t b, const double* x, const double* c, double* out) {
     return guarded([&] { copy_out(bosp::block_product(host_block(x, n, a), host_dense(c, a, b)), out); });
 }

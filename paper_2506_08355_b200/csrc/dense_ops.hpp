@@ -37,6 +37,11 @@ struct ProductJob {
     double alpha, beta;
 };
 void product(const ProductJob* jobs, int njobs, int64_t n);
+// MGS-Biorth application fused with its check Gram (x, y widths and kb <= 32): P = X A,
+// Q = Y B for the k x kb coefficient matrices A (ca) and B (cb) with leading dimension ldc, and
+// G = P^T Q (kb x kb, ldg) from the same pass -- one launch + the split reduction.
+void biorth_apply(const DMat& x, const DMat& y, const double* ca, const double* cb, int64_t ldc, int kb,
+                  const DMat& p, const DMat& q, double* g, int64_t ldg);
 inline void product(const ColList& a, const double* c, int64_t ldc, int32_t b, const DMat& out,
                     double alpha, double beta) {
     ProductJob j{a, c, ldc, b, out.p, out.ld, alpha, beta};

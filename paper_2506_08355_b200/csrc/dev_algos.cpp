@@ -121,6 +121,21 @@ void apply_coefs(const DMat& x, const DMat& y, const DenseMatrix& a, const Dense
     product(pj, 2, x.rows);
 }
 
+// apply_coefs fused with the P^T Q Gram of the written columns (widths <= 32, unweighted):
+// returns P^T Q on the host (allreduced across ranks).
+DenseMatrix apply_coefs_gram(const DMat& x, const DMat& y, const DenseMatrix& a, const DenseMatrix& b,
+                             const DMat& p, const DMat& q) {
+    const int64_t m = a.rows(), k = a.cols();
+    DBlock c(m, 2 * k), g(k, k);
+    to_device(a.data(), m, k, m, c.cols(0, k));
+    to_device(b.data(), m, k, m, c.cols(k, k));
+    biorth_apply(x, y, c.data(), c.data() + k * c.ld(), c.ld(), static_cast<int>(k), p, q, g.data(), g.ld());
+    Runtime::get().allreduce(g.data(), g.ld() * k);
+    DenseMatrix h(k, k);
+    to_host(g.view(), h.data(), k);
+    return h;
+}
+
 // Gxx, Gxy, Gyy of the pair under ip.
 void pair_grams(const DMat& x, const DMat& y, const InnerProduct& ip, DenseMatrix& gxx,
                 DenseMatrix& gxy, DenseMatrix& gyy) {
@@ -192,6 +207,9 @@ DevBiorthOutcome dev_mgs_biorth(const DMat& x, const DMat& y, const DMat& p, con
     DMat cx = x, cy = y;
     DBlock wx, wy;
     int64_t start = 0, kept = 0;
+    static const bool fused_off = std::getenv("BOSP_MGS_UNFUSED") != nullptr;
+    DenseMatrix gpq_fused;
+    bool have_fused = false;
     for (;;) {
         const int64_t mr = cx.cols;
         if (mr == 0) break;
@@ -200,7 +218,15 @@ DevBiorthOutcome dev_mgs_biorth(const DMat& x, const DMat& y, const DMat& p, con
         int64_t stop = mr;
         CoefBiorth cb = coef_mgs(gxx, gxy, gyy, drop_tol, classical, kCancel, &stop);
         const int64_t kb = static_cast<int64_t>(cb.kept.size());
-        if (kb > 0) apply_coefs(cx, cy, cb.a, cb.b, p.cols_range(kept, kb), q.cols_range(kept, kb));
+        // whole block in one recurrence pass: the check Gram P^T Q comes out of the same kernel
+        const bool fuse = !classical && !ip.weighted() && start == 0 && stop >= mr && mr <= 32 && kb >= 2 &&
+                          !fused_off;
+        if (fuse) {
+            gpq_fused = apply_coefs_gram(cx, cy, cb.a, cb.b, p.cols_range(0, kb), q.cols_range(0, kb));
+            have_fused = true;
+        } else if (kb > 0) {
+            apply_coefs(cx, cy, cb.a, cb.b, p.cols_range(kept, kb), q.cols_range(kept, kb));
+        }
         for (int64_t c : cb.kept) out.kept_columns.push_back(start + c);
         for (int64_t c : cb.dropped) out.dropped_columns.push_back(start + c);
         kept += kb;
@@ -243,7 +269,7 @@ DevBiorthOutcome dev_mgs_biorth(const DMat& x, const DMat& y, const DMat& p, con
     if (out.kept == 0) return out;
     const DMat pk = p.cols_range(0, out.kept), qk = q.cols_range(0, out.kept);
     if (classical || out.kept <= 1) return out;
-    const DenseMatrix gpq = ip_gram_host(ip, pk, qk);
+    const DenseMatrix gpq = have_fused ? std::move(gpq_fused) : ip_gram_host(ip, pk, qk);
     if (!biorth_loss_exceeds(gpq, 1e-10)) return out;
     // second subtraction pass (biorth.cpp:104-107)
     out.second_pass = true;

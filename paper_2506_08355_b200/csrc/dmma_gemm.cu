@@ -1229,6 +1229,225 @@ void gram(const GramJob* jobs, int njobs, int64_t n) {
         launch_gram<64, 64, 2, 4>(jobs, njobs, n);
 }
 
+namespace {
+// ------------------------------------------------------------------------------------------
+// Fused MGS-Biorth application: P = X A, Q = Y B and the check Gram P^T Q in one pass
+// ------------------------------------------------------------------------------------------
+// (biorth.cpp:19-69 projections/normalisation applied through the coefficient matrices, then
+// the second-pass test of mgs_biorth, biorth.cpp:104-107, on the P^T Q of the written P, Q.)
+// Persistent CTAs walk 64-row tiles; X and Y tiles are double-buffered in shared memory by
+// cp.async, A and B stay resident.  Warp w computes rows 8w..8w+7 of P and Q on the DMMA pipe,
+// streams them out and parks them (column-major, stride 68) in a warp-private shared strip,
+// from which the same warp feeds its rows into the running P^T Q fragments -- no CTA barrier
+// between product and Gram, and P, Q are never re-read from memory.  Warps fold in order,
+// CTAs through k_gram_reduce: deterministic.
+constexpr int kBaLd = 68;  // smem stride of the 64-row tiles
+
+struct BiorthApplyParams {
+    ColList x, y;
+    const double *ca, *cb;
+    int64_t ldc;
+    int k, kb, kp, ldcs;
+    double *p, *q;
+    int64_t ldp, ldq, n, tiles;
+    double* partial;
+};
+
+template <int BN>
+__global__ void __launch_bounds__(256) k_biorth_apply(BiorthApplyParams prm) {
+    constexpr int NT = BN / 8;
+    extern __shared__ __align__(16) double smem[];
+    const int kp = prm.kp, ldcs = prm.ldcs;
+    double* sca = smem;                        // [BN][ldcs]
+    double* scb = sca + BN * ldcs;             // [BN][ldcs]
+    double* sx = scb + BN * ldcs;              // [2][kp][kBaLd]
+    double* sy = sx + 2 * kp * kBaLd;          // [2][kp][kBaLd]
+    double* sp = sy + 2 * kp * kBaLd;          // [BN][kBaLd]
+    double* sq = sp + BN * kBaLd;              // [BN][kBaLd]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int gid = lane >> 2, tig = lane & 3;
+    const int k = prm.k, kb = prm.kb;
+    // A, B -> shared, zero-padded to kp x BN
+    for (int e = threadIdx.x; e < BN * (kp / 2); e += 256) {
+        const int c = e / (kp / 2), k2 = 2 * (e % (kp / 2));
+        int bytes = 0;
+        const double *srca = prm.ca, *srcb = prm.cb;
+        if (c < kb && k2 < k) {
+            bytes = (k - k2) >= 2 ? 16 : 8;
+            srca = prm.ca + c * prm.ldc + k2;
+            srcb = prm.cb + c * prm.ldc + k2;
+        }
+        cp_async16(sca + c * ldcs + k2, srca, bytes);
+        cp_async16(scb + c * ldcs + k2, srcb, bytes);
+    }
+    auto load = [&](int buf, int64_t tile) {
+        const int64_t m0 = tile * 64;
+        for (int e = threadIdx.x; e < kp * 32; e += 256) {
+            const int kk = e / 32, m2 = 2 * (e % 32);
+            const int64_t m = m0 + m2;
+            int bytes = 0;
+            const double *srcx = prm.ca, *srcy = prm.ca;
+            if (kk < k && m < prm.n) {
+                bytes = (prm.n - m) >= 2 ? 16 : 8;
+                srcx = colptr(prm.x, kk) + m;
+                srcy = colptr(prm.y, kk) + m;
+            }
+            cp_async16(sx + (buf * kp + kk) * kBaLd + m2, srcx, bytes);
+            cp_async16(sy + (buf * kp + kk) * kBaLd + m2, srcy, bytes);
+        }
+    };
+    double g[NT][NT][2];
+#pragma unroll
+    for (int i = 0; i < NT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) g[i][j][0] = g[i][j][1] = 0.0;
+    int64_t tile = blockIdx.x;
+    if (tile < prm.tiles) load(0, tile);
+    cp_async_commit();
+    int buf = 0;
+    const int wr = warp * 8;  // this warp's rows within the tile
+    for (; tile < prm.tiles; tile += gridDim.x, buf ^= 1) {
+        const int64_t next = tile + gridDim.x;
+        if (next < prm.tiles) load(buf ^ 1, next);
+        cp_async_commit();
+        cp_async_wait<1>();
+        __syncthreads();
+        const double* ax = sx + buf * kp * kBaLd;
+        const double* ay = sy + buf * kp * kBaLd;
+        double accp[NT][2], accq[NT][2];
+#pragma unroll
+        for (int j = 0; j < NT; ++j) accp[j][0] = accp[j][1] = accq[j][0] = accq[j][1] = 0.0;
+        for (int kk = 0; kk < kp; kk += 4) {
+            const double fx = ax[(kk + tig) * kBaLd + wr + gid];
+            const double fy = ay[(kk + tig) * kBaLd + wr + gid];
+#pragma unroll
+            for (int j = 0; j < NT; ++j) {
+                dmma(accp[j][0], accp[j][1], fx, sca[(j * 8 + gid) * ldcs + kk + tig]);
+                dmma(accq[j][0], accq[j][1], fy, scb[(j * 8 + gid) * ldcs + kk + tig]);
+            }
+        }
+        const int64_t row = tile * 64 + wr + gid;
+#pragma unroll
+        for (int j = 0; j < NT; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int col = j * 8 + 2 * tig + h;
+                sp[col * kBaLd + wr + gid] = accp[j][h];
+                sq[col * kBaLd + wr + gid] = accq[j][h];
+                if (row < prm.n && col < kb) {
+                    __stcs(prm.p + static_cast<int64_t>(col) * prm.ldp + row, accp[j][h]);
+                    __stcs(prm.q + static_cast<int64_t>(col) * prm.ldq + row, accq[j][h]);
+                }
+            }
+        __syncwarp();
+        // P^T Q over this warp's 8 rows (two 4-row k-steps); rows past n are zero
+#pragma unroll
+        for (int s2 = 0; s2 < 8; s2 += 4) {
+            double fp[NT], fq[NT];
+#pragma unroll
+            for (int i = 0; i < NT; ++i) {
+                fp[i] = sp[(i * 8 + gid) * kBaLd + wr + s2 + tig];
+                fq[i] = sq[(i * 8 + gid) * kBaLd + wr + s2 + tig];
+            }
+#pragma unroll
+            for (int i = 0; i < NT; ++i)
+#pragma unroll
+                for (int j = 0; j < NT; ++j) dmma(g[i][j][0], g[i][j][1], fp[i], fq[j]);
+        }
+        __syncthreads();  // everyone is done with `buf` (and its strip) before refills
+    }
+    cp_async_wait<0>();
+    // fold the warps in order (reusing the A/B area), then the CTA partial (32 x 32 layout)
+    __syncthreads();
+    double* red = smem;
+    for (int w = 0; w < 8; ++w) {
+        if (warp == w) {
+#pragma unroll
+            for (int i = 0; i < NT; ++i)
+#pragma unroll
+                for (int j = 0; j < NT; ++j) {
+                    const int m = i * 8 + gid, nn = j * 8 + 2 * tig;
+                    red[m + nn * BN] = (w == 0 ? 0.0 : red[m + nn * BN]) + g[i][j][0];
+                    red[m + (nn + 1) * BN] = (w == 0 ? 0.0 : red[m + (nn + 1) * BN]) + g[i][j][1];
+                }
+        }
+        __syncthreads();
+    }
+    double* part = prm.partial + static_cast<int64_t>(blockIdx.x) * (32 * 32);
+    for (int e = threadIdx.x; e < BN * BN; e += 256) {
+        const int m = e % BN, nn = e / BN;
+        part[m + nn * 32] = red[e];
+    }
+}
+
+template <int BN>
+void launch_biorth_apply(BiorthApplyParams prm, int64_t n, double* g, int64_t ldg, const DMat& pv, const DMat& qv) {
+    Runtime& rt = Runtime::get();
+    const size_t smem = sizeof(double) * (2ull * BN * prm.ldcs + 4ull * prm.kp * kBaLd + 2ull * BN * kBaLd);
+    static int per_sm[64] = {0};
+    if (per_sm[rt.device() & 63] == 0) {
+        BOSP_CUDA(cudaFuncSetAttribute(k_biorth_apply<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(232448)));
+        int r = 0;
+        BOSP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, k_biorth_apply<BN>, 256, smem));
+        per_sm[rt.device() & 63] = std::max(1, r);
+    }
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(prm.tiles, per_sm[rt.device() & 63] * rt.sm_count())));
+    prm.partial = rt.scratch(static_cast<size_t>(grid) * 32 * 32);
+    const double flops = 2.0 * n * prm.k * prm.kb * 2 + 2.0 * n * prm.kb * prm.kb;
+    const double bytes = 8.0 * n * (2.0 * prm.k + 2.0 * prm.kb);
+    {
+        LaunchScope ls("product", bytes, flops);
+        k_biorth_apply<BN><<<grid, 256, smem, rt.stream()>>>(prm);
+        BOSP_LAUNCH_CHECK();
+    }
+    GramParams gp{};
+    gp.job[0] = GramJob{ColList(pv), ColList(qv), g, ldg};
+    gp.tiles_n[0] = 1;
+    gp.tiles[0] = 1;
+    gp.splits = grid;
+    gp.partial = prm.partial;
+    gp.job_stride = static_cast<int64_t>(grid) * 32 * 32;
+    {
+        LaunchScope ls("gram_reduce");
+        k_gram_reduce<32, 32><<<dim3(32 * 32 / kRedElems, 1, 1), kRedElems * kRedGroups, 0, rt.stream()>>>(gp);
+        BOSP_LAUNCH_CHECK();
+    }
+}
+}  // namespace
+
+void biorth_apply(const DMat& x, const DMat& y, const double* ca, const double* cb, int64_t ldc, int kb,
+                  const DMat& p, const DMat& q, double* g, int64_t ldg) {
+    require(x.cols == y.cols && x.rows == y.rows && p.rows == x.rows && q.rows == x.rows, "biorth_apply: shapes");
+    require(x.cols <= 32 && kb <= 32 && kb >= 1 && p.cols >= kb && q.cols >= kb, "biorth_apply: widths <= 32");
+    check_aligned(ColList(x));
+    check_aligned(ColList(y));
+    const int64_t n = x.rows;
+    BiorthApplyParams prm{};
+    prm.x = ColList(x);
+    prm.y = ColList(y);
+    prm.ca = ca;
+    prm.cb = cb;
+    prm.ldc = ldc;
+    prm.k = static_cast<int>(x.cols);
+    prm.kb = kb;
+    prm.kp = std::max(4, (prm.k + 3) / 4 * 4);
+    prm.ldcs = (prm.kp + 15) / 16 * 16 + 4;
+    prm.p = p.p;
+    prm.q = q.p;
+    prm.ldp = p.ld;
+    prm.ldq = q.ld;
+    prm.n = n;
+    prm.tiles = (n + 63) / 64;
+    const DMat pv = p.cols_range(0, kb), qv = q.cols_range(0, kb);
+    switch ((kb + 7) / 8) {
+        case 1: return launch_biorth_apply<8>(prm, n, g, ldg, pv, qv);
+        case 2: return launch_biorth_apply<16>(prm, n, g, ldg, pv, qv);
+        case 3: return launch_biorth_apply<24>(prm, n, g, ldg, pv, qv);
+        default: return launch_biorth_apply<32>(prm, n, g, ldg, pv, qv);
+    }
+}
+
 void product(const ProductJob* jobs, int njobs, int64_t n) {
     require(njobs >= 1 && njobs <= 4, "product: 1..4 jobs per launch");
     int bmax = 0;
