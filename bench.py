@@ -394,7 +394,7 @@ def run_b200(args, world, rank, local, dist):
             "roofline_dmma": roof_dmma,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-                    "d2h_bytes_per_step": int(d2h)},
+                    "d2h_bytes_per_step": int(d2h), "steps_s": [round(t, 4) for t in e2e_t]},
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "solve": {"iterations": iters, "device_s": dev_s, "wall_s": wall_s,
