@@ -14,8 +14,9 @@ struct GramJob {
     ColList a, b;
     double* g;
     int64_t ldg;
-    // a and b are the same columns (G = A^T A): only the upper-triangular tiles are computed and
-    // G(i, j), i <= j, is mirrored to G(j, i) -- G exactly symmetric, ~half the DMMA work.
+    // G is symmetric (A^T A, or U^T (K U) with K symmetric): only the upper-triangular tiles
+    // are computed and G(i, j), i <= j, is mirrored to G(j, i) -- G exactly symmetric, ~half
+    // the DMMA work.  Requires a.cols() == b.cols().
     bool sym = false;
 };
 void gram(const GramJob* jobs, int njobs, int64_t n);
@@ -35,6 +36,10 @@ struct ProductJob {
     double* out;
     int64_t ldo;
     double alpha, beta;
+    // optional (host array of ncols): rows of C that can be nonzero in each column (e.g. the
+    // upper-triangular coefficient matrices of MGS-Biorth) -- the K loop of a column tile stops
+    // there.  Read at launch time only.
+    const int32_t* col_kend = nullptr;
 };
 void product(const ProductJob* jobs, int njobs, int64_t n);
 // MGS-Biorth application fused with its check Gram (x, y widths and kb <= 32): P = X A,

@@ -110,14 +110,31 @@ void dev_biorth_against(const std::vector<DevBasis>& bases, const DMat& w, const
 // ---------------------------------------------------------------------------------------------
 namespace {
 
+// rows of each column of a (m x k) up to its last nonzero: the K bound of a triangular product
+std::vector<int32_t> last_nonzero_rows(const DenseMatrix& a) {
+    std::vector<int32_t> ke(static_cast<size_t>(a.cols()), 0);
+    for (int64_t c = 0; c < a.cols(); ++c)
+        for (int64_t r = a.rows() - 1; r >= 0; --r)
+            if (a(r, c) != 0.0) {
+                ke[c] = static_cast<int32_t>(r + 1);
+                break;
+            }
+    return ke;
+}
+
 void apply_coefs(const DMat& x, const DMat& y, const DenseMatrix& a, const DenseMatrix& b,
                  const DMat& p, const DMat& q) {
     const int64_t m = a.rows(), k = a.cols();
     DBlock c(m, 2 * k);
     to_device(a.data(), m, k, m, c.cols(0, k));
     to_device(b.data(), m, k, m, c.cols(k, k));
+    // the recurrence's coefficients are upper triangular (column j of P combines x_0..x_j):
+    // wide products skip the zero K blocks (about half the DMMA work at d = 320)
+    const std::vector<int32_t> ka = last_nonzero_rows(a), kb = last_nonzero_rows(b);
     ProductJob pj[2] = {{ColList(x), c.data(), c.ld(), static_cast<int32_t>(k), p.p, p.ld, 1.0, 0.0},
                         {ColList(y), c.data() + k * c.ld(), c.ld(), static_cast<int32_t>(k), q.p, q.ld, 1.0, 0.0}};
+    pj[0].col_kend = ka.data();
+    pj[1].col_kend = kb.data();
     product(pj, 2, x.rows);
 }
 

@@ -110,12 +110,20 @@ struct GramParams {
     int64_t n;
     int tiles_n[4];      // column tiles per job
     int tiles[4];        // tiles per job (sym: upper-triangular tiles only)
-    int sym[4];          // job is G = A^T A: tile t -> upper pair, mirrored stores
+    int sym[4];          // G symmetric: tile t -> upper pair, mirrored stores
+    int same[4];         // and A, B are the same columns (B fragments = A fragments)
     int splits;
     int64_t chunk;       // rows per split (multiple of kBK)
     double* partial;     // [job][split][tile][BM*BN]
     int64_t job_stride;  // doubles per job in partial
 };
+
+bool same_columns(const ColList& a, const ColList& b) {
+    if (a.nseg != b.nseg) return false;
+    for (int s = 0; s < a.nseg; ++s)
+        if (a.p[s] != b.p[s] || a.ld[s] != b.ld[s] || a.start[s + 1] != b.start[s + 1]) return false;
+    return true;
+}
 
 // Tile index -> (tm, tn).  Symmetric jobs enumerate the upper triangle row by row
 // (tm <= tn, T tiles per side).
@@ -329,7 +337,7 @@ void launch_gram(const GramJob* jobs, int njobs, int64_t n) {
     double flops = 0.0, bytes = 0.0;
     for (int j = 0; j < njobs; ++j) {
         flops += 2.0 * n * (double)jobs[j].a.cols() * jobs[j].b.cols() * (prm.sym[j] ? 0.5 : 1.0);
-        bytes += 8.0 * n * (double)(jobs[j].sym ? jobs[j].a.cols() : jobs[j].a.cols() + jobs[j].b.cols());
+        bytes += 8.0 * n * (double)(same_columns(jobs[j].a, jobs[j].b) ? jobs[j].a.cols() : jobs[j].a.cols() + jobs[j].b.cols());
     }
     {
         LaunchScope ls("gram", bytes, flops);
@@ -401,7 +409,7 @@ __global__ void __launch_bounds__(kRegWarps * 32) k_gram_regs(GramParams prm) {
     const bool sym = prm.sym[jb] != 0;
     // symmetric job: a warp group wholly below the diagonal has nothing to compute
     const int64_t ke = (sym && gm > gn) ? kb : min(prm.n, kb + prm.chunk);
-    const bool same_ab = sym && gm == gn;
+    const bool same_ab = sym && prm.same[jb] && gm == gn;
     // U 4-row k-steps per iteration (U even), every load issued before the first DMMA.  The
     // Gram sums over rows in any order, so a k-step need not be 4 consecutive rows: lane tig
     // loads rows (2 tig, 2 tig + 1) of each 8-row block as one 16-byte load and feeds .x to
@@ -511,6 +519,7 @@ void launch_gram_regs(const GramJob* jobs, int njobs, int64_t n) {
         prm.tiles_n[j] = 1;
         prm.tiles[j] = 1;
         prm.sym[j] = jobs[j].sym && MT == NTL && GM == GN;
+        prm.same[j] = prm.sym[j] && same_columns(jobs[j].a, jobs[j].b);
     }
     prm.n = n;
     constexpr int U = kGramU<MS + NS>;
@@ -547,7 +556,7 @@ void launch_gram_regs(const GramJob* jobs, int njobs, int64_t n) {
     double flops = 0.0, bytes = 0.0;
     for (int j = 0; j < njobs; ++j) {
         flops += 2.0 * n * jobs[j].a.cols() * jobs[j].b.cols() * (prm.sym[j] ? 0.5 : 1.0);
-        bytes += 8.0 * n * (jobs[j].sym ? jobs[j].a.cols() : jobs[j].a.cols() + jobs[j].b.cols());
+        bytes += 8.0 * n * (same_columns(jobs[j].a, jobs[j].b) ? jobs[j].a.cols() : jobs[j].a.cols() + jobs[j].b.cols());
     }
     {
         LaunchScope ls("gram", bytes, flops);
@@ -584,6 +593,7 @@ struct ProductParams {
     int64_t n;
     int tiles_n[4];
     int64_t tiles[4];
+    int16_t kend[4][16];  // per column tile: K rows of C that can be nonzero (0 = all)
 };
 
 template <int BM, int BN, int WM, int WN>
@@ -605,7 +615,9 @@ k_product(ProductParams prm) {
     const int64_t tm = tile / prm.tiles_n[jb];
     const int64_t m0 = tm * BM;
     const int n0 = tn * BN;
-    const int kcols = job.a.cols();
+    // structured C (triangular coefficients): the K loop stops at the tile's last nonzero row
+    const int kend = tn < 16 ? prm.kend[jb][tn] : 0;
+    const int kcols = kend > 0 ? min(job.a.cols(), kend) : job.a.cols();
     ColList cl;  // C as a one-segment list (k-contiguous columns)
     cl.p[0] = job.c;
     cl.ld[0] = job.ldc;
@@ -816,6 +828,13 @@ void launch_product(const ProductJob* jobs, int njobs, int64_t n) {
         prm.tiles_n[j] = (jobs[j].ncols + BN - 1) / BN;
         prm.tiles[j] = ((n + BM - 1) / BM) * prm.tiles_n[j];
         max_tiles = std::max(max_tiles, prm.tiles[j]);
+        if (jobs[j].col_kend && prm.tiles_n[j] <= 16) {
+            for (int t = 0; t < prm.tiles_n[j]; ++t) {
+                int ke = 1;
+                for (int c = t * BN; c < std::min(jobs[j].ncols, (t + 1) * BN); ++c) ke = std::max(ke, jobs[j].col_kend[c]);
+                prm.kend[j][t] = static_cast<int16_t>(std::min(ke, 32767));
+            }
+        }
         const double k = jobs[j].a.cols(), b = jobs[j].ncols;
         flops += 2.0 * n * k * b;
         bytes += 8.0 * n * (k + b * (jobs[j].beta != 0.0 ? 2.0 : 1.0));
