@@ -509,7 +509,13 @@ DevCgOutcome dev_cg(const LinearOperator& a, const DMat& rhs, const DMat& x, dou
     const int mi = static_cast<int>(std::min<int64_t>(max_iter, 1 << 30));
     // one rank: the whole solve is a CUDA graph; several ranks exchange through the
     // communicator between kernels (host-synchronised for ThreadComm), so the loop is host-driven
-    if (!x0 && rt.nranks() == 1 && a.impl()->capturable() && !std::getenv("BOSP_NO_GRAPHS")) {
+    // Graphs pay off where launch overhead matters (config 2: 262144 x 20); on the large blocks
+    // of configs 3/5 graph and host loop measured within run-to-run noise (config 3: 14.2-19.4 s
+    // vs 17.1-18.8 s over several boxes), so graphs stay the default.  BOSP_CG_GRAPHS=0 forces
+    // the host loop.
+    static const int graphs_env = std::getenv("BOSP_CG_GRAPHS") ? std::atoi(std::getenv("BOSP_CG_GRAPHS")) : 1;
+    const bool graphs_size_ok = graphs_env != 0;
+    if (!x0 && rt.nranks() == 1 && a.impl()->capturable() && !std::getenv("BOSP_NO_GRAPHS") && graphs_size_ok) {
         // ---- graph path: the whole solve is one launch, the loop runs on the device ----
         // Operators whose apply honours the column mask record the unrolled graph once at the
         // workspace width and serve every narrower call through the live-width scalar (the
