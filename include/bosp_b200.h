@@ -205,6 +205,10 @@ bosp_status bosp_block_inner(bosp_op B, int64_t n, int64_t a, int64_t b, const d
  * column segments; out = [XᵀY | XᵀX | YᵀY] column-major. */
 bosp_status bosp_test_gram_jobs(int64_t n, int64_t a, int64_t b, const double* x, const double* y, int32_t nseg,
                                 int32_t njobs, double* out);
+/* Test hook (no reference counterpart): the symmetric Gram.  same != 0: out (2a x 2a) = Z^T Z
+ * for Z = [X | Y] (the MGS pair Gram); same == 0: out (a x a) = X^T Y computed as a symmetric
+ * Gram (upper tiles mirrored -- the Ritz K^ = U^T (K U) path; X^T Y must be symmetric). */
+bosp_status bosp_test_gram_sym(int64_t n, int64_t a, const double* x, const double* y, int32_t same, double* out);
 /* Test hook (no reference counterpart): the solver's fused MGS-Biorth application -- P = X A,
  * Q = Y B (X, Y n x k; A, B k x kb; k, kb <= 32) and g = P^T Q (kb x kb) from the same kernel. */
 bosp_status bosp_test_biorth_apply(int64_t n, int64_t k, int64_t kb, const double* x, const double* y,

@@ -427,6 +427,16 @@ def _test_gram_jobs(x, y, nseg=1, njobs=3):
             out[a * b + a * a:].reshape((b, b), order="F"))
 
 
+def _test_gram_sym(x, y, same=True):
+    """Test hook: symmetric Gram -> [X | Y]^T [X | Y] (same) or X^T Y via the mirrored path."""
+    x, y = _f(x), _f(y)
+    n, a = x.shape
+    w = 2 * a if same else a
+    out = np.zeros((w, w), order="F")
+    check(lib().bosp_test_gram_sym(C.c_int64(n), C.c_int64(a), _p(x), _p(y), C.c_int32(1 if same else 0), _p(out)))
+    return out
+
+
 def _test_biorth_apply(x, y, a, b):
     """Test hook: the fused MGS-Biorth application -> (P = X A, Q = Y B, P^T Q)."""
     x, y, a, b = _f(x), _f(y), _f(a), _f(b)

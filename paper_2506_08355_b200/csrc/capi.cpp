@@ -465,6 +465,20 @@ bosp_status bosp_test_gram_jobs(int64_t n, int64_t a, int64_t b, const double* x
     });
 }
 
+bosp_status bosp_test_gram_sym(int64_t n, int64_t a, const double* x, const double* y, int32_t same, double* out) {
+    return guarded([&] {
+        bosp::DBlock xd(n, a), yd(n, a), gd(same ? 2 * a : a, same ? 2 * a : a);
+        bosp::to_device(x, n, a, n, xd.view());
+        bosp::to_device(y, n, a, n, yd.view());
+        bosp::GramJob job = same ? bosp::GramJob{bosp::ColList(xd.view()).add(yd.view()),
+                                                 bosp::ColList(xd.view()).add(yd.view()), gd.data(), gd.ld()}
+                                 : bosp::GramJob{bosp::ColList(xd.view()), bosp::ColList(yd.view()), gd.data(), gd.ld()};
+        job.sym = true;
+        bosp::gram(&job, 1, n);
+        bosp::to_host(gd.view(), out, gd.rows());
+    });
+}
+
 bosp_status bosp_test_biorth_apply(int64_t n, int64_t k, int64_t kb, const double* x, const double* y,
                                    const double* a, const double* b, double* p, double* q, double* g) {
     return guarded([&] {

@@ -337,3 +337,23 @@ def test_biorth_apply_fused(k, kb, n):
     pr, qr = x @ a, y @ b
     assert rel(p, pr) < 1e-13 and rel(q, qr) < 1e-13
     assert rel(g, pr.T @ qr) < 1e-12
+
+
+@pytest.mark.parametrize("a", [1, 4, 10, 16, 20, 24, 30, 60, 160])
+@pytest.mark.parametrize("n", [7, 20011])
+def test_gram_symmetric(a, n):
+    """Symmetric Grams (upper tiles mirrored): the MGS pair Gram of Z = [X | Y] (register path up
+    to 48 columns of Z, tiled beyond) and a U^T (K U)-style Gram with distinct operands."""
+    rng = np.random.default_rng(31 * a + n)
+    x = np.asfortranarray(rng.uniform(-1, 1, (n, a)))
+    y = np.asfortranarray(rng.uniform(-1, 1, (n, a)))
+    z = np.hstack([x, y])
+    g = bosp._test_gram_sym(x, y, same=True)
+    assert np.array_equal(g, g.T)
+    assert rel(g, z.T @ z) < 1e-13
+    d = rng.uniform(0.5, 2.0, n)
+    ky = np.asfortranarray(d[:, None] * x)        # K = diag(d): X^T (K X) is symmetric
+    h = bosp._test_gram_sym(x, ky, same=False)
+    ref = x.T @ ky
+    assert np.array_equal(h, h.T)
+    assert rel(h, 0.5 * (ref + ref.T)) < 1e-13
