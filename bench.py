@@ -189,6 +189,16 @@ def dmma_roofline():
     peak = 2 * 8192 ** 3 * 5 / (e0.elapsed_time(e1) * 1e-3) / 1e12
     del a, b
     torch.cuda.empty_cache()
+    # MGS-Biorth at HBM scale (m = 20 at n = 2^21, X, Y, P, Q far beyond L2): the pair Gram of
+    # [X | Y] + the fused apply/check kernel, against 48 n m algorithmic bytes
+    m = 20
+    mg_ms = bosp.bench_blas("gramsym", n, m, m, reps=10)
+    ma_ms = bosp.bench_blas("mgsapply", n, m, m, reps=10)
+    hbm = load_peaks().get("hbm_gbs", 6650.0)
+    mgs_gbs = 48.0 * n * m / ((mg_ms + ma_ms) * 1e-3) / 1e9
+    out["mgs_at_hbm_scale"] = {"n": n, "m": m, "pair_gram_ms": mg_ms, "apply_check_ms": ma_ms,
+                               "achieved_gbs": mgs_gbs, "frac_hbm": mgs_gbs / hbm,
+                               "note": "kernel time only (no host recurrence between the two launches)"}
     gt = 2 * n * d * d / (g_ms * 1e-3) / 1e12
     pt = 2 * n * d * w / (p_ms * 1e-3) / 1e12
     out.update({"kernel": "k_gram<64,64> (G = A^T B, 320 x 320)", "achieved": gt, "peak": peak, "frac": gt / peak,

@@ -265,7 +265,8 @@ void bosp_profile_collect_regions(int64_t* launches, double* ms, double* bytes, 
 bosp_status bosp_bench_apply(bosp_op op, int64_t ncols, int64_t reps, double* ms);
 /* Microbenchmark of the tall-skinny kernels on device-resident random data: kind 0 = Gram
  * (n x a)^T (n x b), 1 = product (n x a)(a x b), 2 = axpy, 3 = the three Grams X^T X, X^T Y,
- * Y^T Y as three jobs, 4 = the same as one symmetric Gram of [X | Y]; mean ms per call. */
+ * Y^T Y as three jobs, 4 = the same as one symmetric Gram of [X | Y], 5 = the fused MGS-Biorth
+ * apply (P = X A, Q = Y B, P^T Q; a = b <= 32); mean ms per call. */
 bosp_status bosp_bench_blas(int32_t kind, int64_t n, int64_t a, int64_t b, int64_t reps, double* ms);
 /* Microbenchmark of the batched CG: `iters` iterations (tol 0, so every column runs all of
  * them) on a random n x ncols right-hand side; mean ms per CG iteration over `reps` solves. */

@@ -637,7 +637,7 @@ def bench_cg(op, ncols, iters=20, reps=5):
 
 def bench_blas(kind, n, a, b, reps=20):
     """kind: 'gram' | 'product' | 'axpy' -> mean ms per call on device-resident data."""
-    k = {"gram": 0, "product": 1, "axpy": 2, "gram3": 3, "gramsym": 4}[kind]
+    k = {"gram": 0, "product": 1, "axpy": 2, "gram3": 3, "gramsym": 4, "mgsapply": 5}[kind]
     ms = C.c_double()
     check(lib().bosp_bench_blas(C.c_int32(k), C.c_int64(n), C.c_int64(a), C.c_int64(b),
                                 C.c_int64(reps), C.byref(ms)))

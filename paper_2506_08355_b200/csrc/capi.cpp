@@ -696,6 +696,13 @@ bosp_status bosp_bench_blas(int32_t kind, int64_t n, int64_t a, int64_t b, int64
                                            {bosp::ColList(x.view()), bosp::ColList(y.view()), c2.data(), c2.ld()},
                                            {bosp::ColList(y.view()), bosp::ColList(y.view()), c3.data(), c3.ld()}};
             *ms = time_reps(reps, [&] { bosp::gram(jobs, 3, n); });
+        } else if (kind == 5) {  // fused MGS-Biorth apply (a = b <= 32): P = X A, Q = Y B, P^T Q
+            bosp::DBlock p(n, a), q(n, a), z(a, 2 * a), g(a, a);
+            fill_random(z.view(), 4);
+            *ms = time_reps(reps, [&] {
+                bosp::biorth_apply(x.view(), y.view().cols_range(0, a), z.data(), z.data() + a * z.ld(), z.ld(),
+                                   static_cast<int>(a), p.view(), q.view(), g.data(), g.ld());
+            });
         } else if (kind == 4) {  // the same three blocks as one symmetric Gram of Z = [X | Y]
             bosp::DBlock z(a + b, a + b);
             bosp::GramJob job{bosp::ColList(x.view()).add(y.view()), bosp::ColList(x.view()).add(y.view()),
