@@ -1240,8 +1240,13 @@ void gram(const GramJob* jobs, int njobs, int64_t n) {
         }
     }
     static const int gw = std::getenv("BOSP_GEMM_WARPS") ? std::atoi(std::getenv("BOSP_GEMM_WARPS")) : 8;
+    static const bool narrow_b = std::getenv("BOSP_GRAM_NO_NARROW") == nullptr;
     if (amax <= 32 && bmax <= 32)
         launch_gram<32, 32, 2, 2>(jobs, njobs, n);
+    else if (narrow_b && bmax <= 32 && amax >= 128)
+        // many output rows, <= 32 columns (the dense operator's A x = (A^T)^T x at the CG's
+        // widths): 128 x 32 tiles, the same 32 x 16 warp tiles, no padding of b to 64
+        launch_gram<128, 32, 4, 2>(jobs, njobs, n);
     else if (gw == 4)
         launch_gram<64, 64, 2, 2>(jobs, njobs, n);
     else
