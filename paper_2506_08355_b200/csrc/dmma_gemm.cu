@@ -153,9 +153,10 @@ __device__ __forceinline__ void gram_store(const GramJob& job, bool sym, int m, 
     }
 }
 
-template <int BM, int BN, int WM, int WN>
+template <int BM, int BN, int WM, int WN, int GBK = kBK, int GST = kStages>
 __global__ void __launch_bounds__(WM * WN * 32)
 k_gram(GramParams prm) {
+    constexpr int kBK = GBK, kStages = GST, kLdK = GBK + 4;
     constexpr int NT = WM * WN * 32;
     constexpr int WTM = BM / WM, WTN = BN / WN;
     constexpr int MT = WTM / 8, NTL = WTN / 8;
@@ -188,8 +189,8 @@ k_gram(GramParams prm) {
 #pragma unroll
     for (int s = 0; s < kStages - 1; ++s) {
         if (s < nk) {
-            load_kcontig<BM, NT>(sa + s * BM * kLdK, job.a, m0, acols, kb + s * kBK, ke);
-            load_kcontig<BN, NT>(sb + s * BN * kLdK, job.b, n0, bcols, kb + s * kBK, ke);
+            load_kcontig<BM, NT, kBK>(sa + s * BM * kLdK, job.a, m0, acols, kb + s * kBK, ke);
+            load_kcontig<BN, NT, kBK>(sb + s * BN * kLdK, job.b, n0, bcols, kb + s * kBK, ke);
         }
         cp_async_commit();
     }
@@ -214,8 +215,8 @@ k_gram(GramParams prm) {
         const int nxt = it + kStages - 1;
         if (nxt < nk) {
             const int sn = nxt % kStages;
-            load_kcontig<BM, NT>(sa + sn * BM * kLdK, job.a, m0, acols, kb + nxt * kBK, ke);
-            load_kcontig<BN, NT>(sb + sn * BN * kLdK, job.b, n0, bcols, kb + nxt * kBK, ke);
+            load_kcontig<BM, NT, kBK>(sa + sn * BM * kLdK, job.a, m0, acols, kb + nxt * kBK, ke);
+            load_kcontig<BN, NT, kBK>(sb + sn * BN * kLdK, job.b, n0, bcols, kb + nxt * kBK, ke);
         }
         cp_async_commit();
     }
@@ -289,8 +290,9 @@ __global__ void __launch_bounds__(kRedElems * kRedGroups) k_gram_reduce(GramPara
     gram_store(job, prm.sym[jb], m, nn, s);
 }
 
-template <int BM, int BN, int WM, int WN>
+template <int BM, int BN, int WM, int WN, int GBK = kBK, int GST = kStages>
 void launch_gram(const GramJob* jobs, int njobs, int64_t n) {
+    constexpr int kBK = GBK, kStages = GST, kLdK = GBK + 4;
     Runtime& rt = Runtime::get();
     GramParams prm{};
     int max_tiles = 0;
@@ -308,9 +310,9 @@ void launch_gram(const GramJob* jobs, int njobs, int64_t n) {
     static int resident[64] = {0};  // CTAs per SM, per device
     if (resident[rt.device() & 63] == 0) {
         int r = 0;
-        BOSP_CUDA(cudaFuncSetAttribute(k_gram<BM, BN, WM, WN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        BOSP_CUDA(cudaFuncSetAttribute(k_gram<BM, BN, WM, WN, GBK, GST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem_b)));
-        BOSP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, k_gram<BM, BN, WM, WN>, NTh, smem_b));
+        BOSP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, k_gram<BM, BN, WM, WN, GBK, GST>, NTh, smem_b));
         resident[rt.device() & 63] = std::max(1, r);
     }
     const int kblocks = static_cast<int>((n + kBK - 1) / kBK);
@@ -332,7 +334,7 @@ void launch_gram(const GramJob* jobs, int njobs, int64_t n) {
     constexpr size_t smem = sizeof(double) * kStages * (BM + BN) * kLdK;
     static unsigned attr_mask = 0;
     if (rt.first_use(attr_mask))
-        BOSP_CUDA(cudaFuncSetAttribute(k_gram<BM, BN, WM, WN>,
+        BOSP_CUDA(cudaFuncSetAttribute(k_gram<BM, BN, WM, WN, GBK, GST>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     double flops = 0.0, bytes = 0.0;
     for (int j = 0; j < njobs; ++j) {
@@ -342,7 +344,7 @@ void launch_gram(const GramJob* jobs, int njobs, int64_t n) {
     {
         LaunchScope ls("gram", bytes, flops);
         dim3 grid(max_tiles, prm.splits, njobs);
-        k_gram<BM, BN, WM, WN><<<grid, NT, smem, rt.stream()>>>(prm);
+        k_gram<BM, BN, WM, WN, GBK, GST><<<grid, NT, smem, rt.stream()>>>(prm);
         BOSP_LAUNCH_CHECK();
     }
     if (prm.splits > 1) {
@@ -1246,7 +1248,13 @@ void gram(const GramJob* jobs, int njobs, int64_t n) {
     else if (narrow_b && bmax <= 32 && amax >= 128)
         // many output rows, <= 32 columns (the dense operator's A x = (A^T)^T x at the CG's
         // widths): 128 x 32 tiles, the same 32 x 16 warp tiles, no padding of b to 64
-        launch_gram<128, 32, 4, 2>(jobs, njobs, n);
+    {
+        // 16-row stages keep two 8-warp CTAs per SM (the 32-row ring fits one): the tile is
+        // DMMA-latency bound, not byte bound -- n = 16384, 32 columns: 1.47 -> 0.93 ms
+        static const bool deep = std::getenv("BOSP_GRAM_NARROW_BK32") != nullptr;
+        if (deep) launch_gram<128, 32, 4, 2>(jobs, njobs, n);
+        else launch_gram<128, 32, 4, 2, 16, 3>(jobs, njobs, n);
+    }
     else if (gw == 4)
         launch_gram<64, 64, 2, 2>(jobs, njobs, n);
     else
