@@ -48,9 +48,14 @@ typedef struct bosp_op_s* bosp_op;
 /* Host callback: y(:, j) = A x(:, j), x and y host n x ncols column-major (ld = n).
  * Replaces LinearOperator::ApplyFn / from_callback (linear_operator.hpp:19,25). */
 typedef void (*bosp_host_apply_fn)(void* ctx, const double* x, double* y, int64_t n, int64_t ncols);
-/* Device callback (new): x, y in HBM with leading dims ldx, ldy; stream is a cudaStream_t. */
-typedef void (*bosp_device_apply_fn)(void* ctx, const double* x, int64_t ldx, double* y,
-                                     int64_t ldy, int64_t n, int64_t ncols, void* stream);
+/* Device callback -- the device analog of ApplyFn / from_callback (linear_operator.hpp:19,25):
+ * y(:, j) = A x(:, j) for j < ncols, x and y in HBM of `device` (column-major, leading dims
+ * ldx, ldy, n rows each), work enqueued on `stream` (a cudaStream_t).  Same contract as ApplyFn:
+ * overwrite all of y, accept any ncols >= 1.  Return 0 on success; any other value aborts the
+ * solve with BOSP_ERROR ("device callback returned <status>"), the C analog of an exception
+ * thrown from an ApplyFn. */
+typedef int (*bosp_device_apply_fn)(void* ctx, int device, const double* x, int64_t ldx, double* y,
+                                    int64_t ldy, int64_t n, int64_t ncols, void* stream);
 
 /* from_dense (linear_operator.cpp:12-31): a is n x n column-major, copied to HBM. */
 bosp_status bosp_op_dense(int64_t n, const double* a, bosp_op* out);

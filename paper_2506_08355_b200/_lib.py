@@ -41,6 +41,9 @@ class OpaqueOp(C.Structure):
 
 OpPtr = C.POINTER(OpaqueOp)
 HOST_APPLY = C.CFUNCTYPE(None, C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int64, C.c_int64)
+# bosp_device_apply_fn: (ctx, device, x, ldx, y, ldy, n, ncols, stream) -> status
+DEVICE_APPLY = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
+                           C.c_int64, C.c_int64, C.c_void_p)
 
 
 class Config(C.Structure):

@@ -96,6 +96,21 @@ class LinearOperator:
         return cls._make(lib().bosp_op_callback, C.c_int64(dim), cb, None, keep=cb)
 
     @classmethod
+    def from_device_callback(cls, dim, fn):
+        """Device matrix-free plugin (bosp_op_device_callback): fn(device, x_ptr, ldx, y_ptr, ldy,
+        n, ncols, stream_ptr) -> int status, called with HBM pointers of column-major blocks
+        and the solver's cudaStream_t; it must enqueue y(:, j) = A x(:, j) on that stream and
+        return 0 (nonzero aborts the solve).  The device analog of from_callback
+        (linear_operator.hpp:19,25)."""
+        def tramp(ctx, dev, xp, ldx, yp, ldy, n, m, stream):
+            try:
+                return int(fn(dev, xp or 0, ldx, yp or 0, ldy, n, m, stream or 0))
+            except Exception:  # an exception must not unwind through C frames
+                return -1
+        cb = L.DEVICE_APPLY(tramp)
+        return cls._make(lib().bosp_op_device_callback, C.c_int64(dim), cb, None, keep=cb)
+
+    @classmethod
     def stencil(cls, nx, ny, nz, bc, scale, potential="none", origin=0.0, h=1.0, v=None,
                 s0=0, s_global=0, nz_global=0):
         """Matrix-free stencil.  s_global > 0: this rank's slab of slow-axis planes
@@ -351,7 +366,8 @@ def _global_op(op):
     return g, keep
 
 
-def solve_multi(nranks, K, M, cfg: BospConfig, ns: GeneralizedNullspace | None = None, ngpus=0) -> EigenResult:
+def solve_multi(nranks, K, M, cfg: BospConfig, ns: GeneralizedNullspace | None = None, ngpus=0,
+                want_vectors=True) -> EigenResult:
     """Row-partitioned solve: nranks ranks as threads of this process over ngpus devices
     (several may share one GPU).  K, M: global problems.Csr / problems.Stencil / dense arrays."""
     gk, kk = _global_op(K)
@@ -359,8 +375,8 @@ def solve_multi(nranks, K, M, cfg: BospConfig, ns: GeneralizedNullspace | None =
     n = gk.n
     cap = cfg.nev
     lam, res = np.zeros(cap), np.zeros(cap)
-    x = np.zeros((n, cap), order="F")
-    y = np.zeros((n, cap), order="F")
+    x = np.zeros((n, cap), order="F") if want_vectors else None
+    y = np.zeros((n, cap), order="F") if want_vectors else None
     nout, st, cc = C.c_int64(), L.Stats(), cfg.c()
     if ns is None:
         r, x0, y0 = -1, None, None
@@ -373,7 +389,8 @@ def solve_multi(nranks, K, M, cfg: BospConfig, ns: GeneralizedNullspace | None =
     del kk, km
     k = nout.value
     stats = {f[0]: getattr(st, f[0]) for f in L.Stats._fields_}
-    return EigenResult(lam[:k], x[:, :k], y[:, :k], int(st.iterations), res[:k], np.zeros((0, cfg.nev)),
+    return EigenResult(lam[:k], None if x is None else x[:, :k], None if y is None else y[:, :k],
+                       int(st.iterations), res[:k], np.zeros((0, cfg.nev)),
                        bool(st.converged), int(st.nev_converged), stats)
 
 

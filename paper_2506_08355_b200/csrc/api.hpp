@@ -107,9 +107,11 @@ class LinearOperator {
 public:
     enum class Kind { dense, sparse_csr, matrix_free_callback };
     using ApplyFn = std::function<void(const BlockVectors&, BlockVectors&)>;
-    // Device matrix-free hook: y(:, j) = A x(:, j) for j < ncols, both column-major in HBM.
-    using DeviceApplyFn = std::function<void(const double* x, int64_t ldx, double* y, int64_t ldy,
-                                             int64_t ncols, cudaStream_t stream)>;
+    // Device matrix-free hook (the device analog of ApplyFn): y(:, j) = A x(:, j) for
+    // j < ncols, both column-major in HBM of `device`, enqueued on `stream`; returns 0 on
+    // success, anything else aborts the solve (bosp::Error "device callback returned <s>").
+    using DeviceApplyFn = std::function<int(int device, const double* x, int64_t ldx, double* y, int64_t ldy,
+                                            int64_t ncols, cudaStream_t stream)>;
 
     LinearOperator() = default;
     static LinearOperator from_dense(const DenseMatrix& a);

@@ -66,7 +66,7 @@ BiorthOutcome biorth_common(const BlockVectors& x, const BlockVectors& y, const 
     DBlock p(x.dim(), std::max<int64_t>(x.cols(), 1)), q(x.dim(), std::max<int64_t>(x.cols(), 1));
     // small blocks: the reference's column-sequential recurrence itself (exact order, robust on
     // ill-conditioned input); wide blocks: the level-3 coefficient-space path of the solver
-    static const int64_t seq_max = std::getenv("BOSP_BIORTH_SEQ_MAX") ? std::atoll(std::getenv("BOSP_BIORTH_SEQ_MAX")) : 64;
+    constexpr int64_t seq_max = 64;
     DevBiorthOutcome o = x.cols() <= seq_max
         ? dev_gs_biorth_seq(dx.view(), dy.view(), p.view(), q.view(), ip, drop_tol, classical)
         : dev_mgs_biorth(dx.view(), dy.view(), p.view(), q.view(), ip, drop_tol, classical);

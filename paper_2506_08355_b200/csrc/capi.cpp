@@ -226,8 +226,8 @@ bosp_status bosp_op_callback(int64_t n, bosp_host_apply_fn fn, void* ctx, bosp_o
 bosp_status bosp_op_device_callback(int64_t n, bosp_device_apply_fn fn, void* ctx, bosp_op* out) {
     return guarded([&] {
         *out = wrap(bosp::LinearOperator::from_device_callback(
-            n, [fn, ctx, n](const double* x, int64_t ldx, double* y, int64_t ldy, int64_t m, cudaStream_t s) {
-                fn(ctx, x, ldx, y, ldy, n, m, static_cast<void*>(s));
+            n, [fn, ctx, n](int dev, const double* x, int64_t ldx, double* y, int64_t ldy, int64_t m, cudaStream_t s) {
+                return fn(ctx, dev, x, ldx, y, ldy, n, m, static_cast<void*>(s));
             }));
     });
 }

@@ -89,7 +89,7 @@ struct CgScalars {
     int* any_active;  // scalar: number of active columns (device)
     int* loops;       // scalar: batched iterations executed (device)
     unsigned long long* total = nullptr;  // running count of batched iterations over all solves
-    double* parts;    // scratch for per-block partial sums (cg_update_fused / fused SpMM dots)
+    double* parts;    // scratch for per-block partial sums (fused SpMM dots)
     int parts_cap;    // doubles available at `parts`
     // When the CG runs as a CUDA graph with a `while` conditional node, the start/update
     // epilogues set the loop condition to (any column still active).
@@ -109,13 +109,6 @@ void cg_start_x0(const DMat& b, const DMat& x0, const DMat& ax0, const DMat& x, 
                  const DMat& p, const CgScalars& s, double tol, int max_iter);
 // pap_j = p_j^T ap_j (active columns)
 void cg_pap(const DMat& p, const DMat& ap, const CgScalars& s);
-// One batched CG iteration after ap = A p, fused into one cooperative kernel:
-//   pap_j = sum of pap_parts[j * nparts + b] (fixed order; nparts = 1 for a ready value),
-//   x += a p, r -= a ap, rr_new (grid-wide barrier), beta, p = r + beta p, masks/scalars.
-// Same arithmetic as cg_update; half the passes and one launch instead of two.
-void cg_update_fused(const DMat& x, const DMat& r, const DMat& p, const DMat& ap,
-                     const CgScalars& s, const double* pap_parts, int nparts, double tol,
-                     int max_iter);
 // active & pap>0: x += a p, r -= a ap, rr_new; pap<=0 -> broken, inactive.  Then
 // p = r + beta p, rr = rr_new, active = sqrt(rr) > tol*bnorm && iters < max_iter.
 // pap_parts != nullptr: p^T A p is still in per-block partials (pap_parts[j * nparts + b], the

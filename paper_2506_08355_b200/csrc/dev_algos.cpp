@@ -157,7 +157,7 @@ DenseMatrix apply_coefs_gram(const DMat& x, const DMat& y, const DenseMatrix& a,
 void pair_grams(const DMat& x, const DMat& y, const InnerProduct& ip, DenseMatrix& gxx,
                 DenseMatrix& gxy, DenseMatrix& gyy) {
     const int64_t m = x.cols;
-    if (!ip.weighted() && !std::getenv("BOSP_PAIR_GRAM3")) {
+    if (!ip.weighted()) {
         // one symmetric Gram of Z = [X | Y]: X and Y streamed once, upper tiles only;
         // Z^T Z = [[X^T X, X^T Y], [., Y^T Y]]
         DBlock g(2 * m, 2 * m);
@@ -224,7 +224,6 @@ DevBiorthOutcome dev_mgs_biorth(const DMat& x, const DMat& y, const DMat& p, con
     DMat cx = x, cy = y;
     DBlock wx, wy;
     int64_t start = 0, kept = 0;
-    static const bool fused_off = std::getenv("BOSP_MGS_UNFUSED") != nullptr;
     DenseMatrix gpq_fused;
     bool have_fused = false;
     for (;;) {
@@ -236,8 +235,7 @@ DevBiorthOutcome dev_mgs_biorth(const DMat& x, const DMat& y, const DMat& p, con
         CoefBiorth cb = coef_mgs(gxx, gxy, gyy, drop_tol, classical, kCancel, &stop);
         const int64_t kb = static_cast<int64_t>(cb.kept.size());
         // whole block in one recurrence pass: the check Gram P^T Q comes out of the same kernel
-        const bool fuse = !classical && !ip.weighted() && start == 0 && stop >= mr && mr <= 32 && kb >= 2 &&
-                          !fused_off;
+        const bool fuse = !classical && !ip.weighted() && start == 0 && stop >= mr && mr <= 32 && kb >= 2;
         if (fuse) {
             gpq_fused = apply_coefs_gram(cx, cy, cb.a, cb.b, p.cols_range(0, kb), q.cols_range(0, kb));
             have_fused = true;
@@ -453,31 +451,32 @@ int64_t CgWorkspace::total_sweeps() {
 }
 
 CgWorkspace::~CgWorkspace() {
-    // owned device memory is returned with the pool at teardown; pinned/event handles leak
-    // intentionally when the workspace outlives the CUDA context at process exit.
+    // Every workspace (one per solve, per nullspace detection, per API CG call) returns what it
+    // owns.  At process exit the CUDA runtime may already be unloading: the calls then fail
+    // with cudaErrorCudartUnloading and are ignored (the driver reclaims everything).
+    drop_graphs(graphs);
+    Runtime& rt = Runtime::get();
+    if (cudaStreamQuery(rt.stream()) == cudaErrorCudartUnloading) return;
+    if (scal_) rt.free(scal_);
+    if (parts_) rt.free(parts_);
+    if (ticket_) rt.free(ticket_);
+    if (host_active) {
+        cudaStreamSynchronize(rt.stream());  // a pending publish() may still target it
+        cudaFreeHost(host_active);
+    }
+    for (cudaEvent_t& e : ev)
+        if (e) cudaEventDestroy(e);
+    cudaGetLastError();  // clear any teardown error
 }
 
 namespace {
 // One batched CG iteration: ap = A p with p^T A p fused into the operator when it can
 // (SELL / stencil), then the cooperative fused update; unfused kernels otherwise.
-// BOSP_CG_MODE: 0 = SpMM with fused p^T A p (masked) + update + direction (default);
-//               1 = separate p^T A p kernel; 2 = cooperative single-kernel update.
-// (A row-major "interleaved" CG layout was measured 15-20% slower on config 2 and dropped.)
-int cg_mode() {
-    static const int mode = std::getenv("BOSP_CG_MODE") ? std::atoi(std::getenv("BOSP_CG_MODE")) : 0;
-    return mode;
-}
-
+// (Measured and dropped: a row-major "interleaved" CG layout, 15-20 % slower on config 2, and
+// a cooperative single-kernel update with a grid barrier, slower than the 2-kernel form.)
 void cg_iteration(const LinearOperator& a, const DMat& x, const DMat& r, const DMat& p, const DMat& ap,
                   const CgScalars& sc, CgWorkspace& ws, double tol, int mi) {
-    const int mode = cg_mode();
-    if (mode == 2 && p.cols <= 160 && Runtime::get().nranks() == 1) {
-        a.apply_device(p, ap);
-        cg_pap(p, ap, sc);
-        cg_update_fused(x, r, p, ap, sc, sc.pap, 1, tol, mi);
-        return;
-    }
-    if (mode != 1 && Runtime::get().nranks() == 1) {
+    if (Runtime::get().nranks() == 1) {
         // the SpMM leaves p^T A p as per-block partials; each update block folds its column
         const SpmmDot dot{ws.pap_parts(), nullptr, sc.pap, sc.active, CgWorkspace::kPartsPerRegion};
         if (const int nparts = a.impl()->apply_dot(p, ap, dot)) {
@@ -486,7 +485,7 @@ void cg_iteration(const LinearOperator& a, const DMat& x, const DMat& r, const D
         }
     }
     const SpmmDot dot{ws.pap_parts(), ws.ticket(), sc.pap, sc.active, CgWorkspace::kPartsPerRegion};
-    if (mode != 1 && a.impl()->apply_dot(p, ap, dot) > 0) {
+    if (a.impl()->apply_dot(p, ap, dot) > 0) {
         Runtime::get().allreduce(sc.pap, p.cols);  // per-rank p^T A p -> global
         cg_update(x, r, p, ap, sc, tol, mi);
         return;
@@ -511,17 +510,15 @@ DevCgOutcome dev_cg(const LinearOperator& a, const DMat& rhs, const DMat& x, dou
     // communicator between kernels (host-synchronised for ThreadComm), so the loop is host-driven
     // Graphs pay off where launch overhead matters (config 2: 262144 x 20); on the large blocks
     // of configs 3/5 graph and host loop measured within run-to-run noise (config 3: 14.2-19.4 s
-    // vs 17.1-18.8 s over several boxes), so graphs stay the default.  BOSP_CG_GRAPHS=0 forces
-    // the host loop.
-    static const int graphs_env = std::getenv("BOSP_CG_GRAPHS") ? std::atoi(std::getenv("BOSP_CG_GRAPHS")) : 1;
-    const bool graphs_size_ok = graphs_env != 0;
-    if (!x0 && rt.nranks() == 1 && a.impl()->capturable() && !std::getenv("BOSP_NO_GRAPHS") && graphs_size_ok) {
+    // vs 17.1-18.8 s over several boxes), so graphs stay the default.  BOSP_NO_GRAPHS=1 forces
+    // the host loop (per-kernel ncu captures).
+    static const bool no_graphs = std::getenv("BOSP_NO_GRAPHS") != nullptr;
+    if (!x0 && rt.nranks() == 1 && a.impl()->capturable() && !no_graphs) {
         // ---- graph path: the whole solve is one launch, the loop runs on the device ----
         // Operators whose apply honours the column mask record the unrolled graph once at the
         // workspace width and serve every narrower call through the live-width scalar (the
         // solver's GS sweeps shrink 20 -> 19 -> 16 -> ... -> 1 as columns converge).
-        static const bool force_while = std::getenv("BOSP_CG_WHILE") != nullptr;
-        const bool unrolled = max_iter <= kCgUnrollMax && !force_while && a.impl()->has_masked_dot() && cg_mode() != 2;
+        const bool unrolled = max_iter <= kCgUnrollMax && a.impl()->has_masked_dot();
         // Recorded width: the next power of two (capped at the workspace width), so a graph
         // serves widths within 2x of its own and the kernels' grids stay sized for them
         // (recording at the full width for every call measured 8 % slower: narrow solves then
@@ -534,7 +531,7 @@ DevCgOutcome dev_cg(const LinearOperator& a, const DMat& rhs, const DMat& x, dou
         }
         CgGraph* g = nullptr;
         for (CgGraph& c : ws.graphs)
-            if (c.op == a.impl() && c.rhs == rhs.p && c.ldr == rhs.ld && c.x == x.p && c.ldx == x.ld &&
+            if (c.op == a.impl()->uid() && c.scratch_gen == rt.scratch_generation() && c.rhs == rhs.p && c.ldr == rhs.ld && c.x == x.p && c.ldx == x.ld &&
                 c.m == mg && c.tol == tol && c.max_iter == max_iter && c.prof_family == rt.prof_family())
                 g = &c;
         if (!g) {
@@ -542,7 +539,7 @@ DevCgOutcome dev_cg(const LinearOperator& a, const DMat& rhs, const DMat& x, dou
             if (ws.graphs.size() >= 16) drop_graphs(ws.graphs);
             ws.graphs.emplace_back();
             g = &ws.graphs.back();
-            g->op = a.impl();
+            g->op = a.impl()->uid();
             g->rhs = rhs.p;
             g->ldr = rhs.ld;
             g->x = x.p;
@@ -554,6 +551,7 @@ DevCgOutcome dev_cg(const LinearOperator& a, const DMat& rhs, const DMat& x, dou
             rt.set_capture_prof(&g->prof_pairs);
             rt.scratch(1 << 16);  // no pool growth while recording
             rt.tickets(64);
+            g->scratch_gen = rt.scratch_generation();
             rt.sync();
             BOSP_CUDA(cudaGraphCreate(&g->graph, 0));
             // Short solves (the solver's inner CG: max_iter 20) are unrolled into a straight

@@ -51,7 +51,8 @@ double dev_biorth_residual(const DMat& p, const DMat& q, const InnerProduct& ip)
 // One instantiated CUDA graph of a whole batched CG solve: [start] -> while(any active)
 // { A p; p^T A p; x, r update; p update }.  Keyed by everything the recorded launches capture.
 struct CgGraph {
-    const void* op = nullptr;
+    uint64_t op = 0;              // OperatorImpl::uid() (never reused, unlike an address)
+    uint64_t scratch_gen = 0;     // Runtime::scratch_generation() at recording
     const double *rhs = nullptr, *x = nullptr;
     int64_t ldr = 0, ldx = 0, m = 0, max_iter = 0;
     double tol = 0.0;

@@ -33,7 +33,6 @@ constexpr int kStages = BOSP_KSTAGES;
 #define BOSP_KBK 32
 #endif
 constexpr int kBK = BOSP_KBK;      // k-depth of one pipeline stage
-constexpr int kLdK = kBK + 4;     // padded k-contiguous smem stride
 
 __device__ __forceinline__ const double* colptr(const ColList& cl, int c) {
     int s = 0;
@@ -59,7 +58,7 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 }
 
 // Load a "k-contiguous" tile: R columns (from ColList starting at col0, total ncols), rows
-// [k0, k0+kBK) clipped to kmax, into smem[c * kLdK + k].  Missing data is zero-filled.
+// [k0, k0+kBK) clipped to kmax, into smem[c * (BK + 4) + k].  Missing data is zero-filled.
 template <int R, int NT, int BK = kBK>
 __device__ __forceinline__ void load_kcontig(double* smem, const ColList& cl, int col0, int ncols,
                                              int64_t k0, int64_t kmax) {
@@ -540,8 +539,7 @@ void launch_gram_regs(const GramJob* jobs, int njobs, int64_t n) {
                                                                 smem_need));
         resident[rt.device() & 63] = std::max(1, std::min(r, 2));
     }
-    static const int64_t waves_env = std::getenv("BOSP_GRAM_WAVES") ? std::atoi(std::getenv("BOSP_GRAM_WAVES")) : 0;
-    const int64_t waves = waves_env > 0 ? waves_env : resident[rt.device() & 63];
+    const int64_t waves = resident[rt.device() & 63];
     int splits = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(
         (waves * rt.sm_count() + njobs - 1) / njobs, steps / 8)));  // >= 8 steps of work per block
     const int64_t per = ((n + splits - 1) / splits + kStep - 1) / kStep;
@@ -701,123 +699,6 @@ k_product(ProductParams prm) {
     }
 }
 
-// Persistent product: a grid of resident CTAs walks the flattened (job, row tile, column tile)
-// list; the cp.async ring runs straight across tile boundaries (the next tile's first stages
-// load while the current tile's last stages compute) and the epilogue writes the accumulators
-// from registers (each warp store covers 8 rows x 4 columns: full 32-byte sectors), so no
-// per-tile pipeline fill/drain and no shared-memory transpose.
-template <int BM, int BN, int WM, int WN>
-__global__ void __launch_bounds__(WM * WN * 32)
-k_product_persist(ProductParams prm, int64_t total_tiles) {
-    constexpr int NT = WM * WN * 32;
-    constexpr int WTM = BM / WM, WTN = BN / WN;
-    constexpr int MT = WTM / 8, NTL = WTN / 8;
-    constexpr int LdM = BM + 4;
-    extern __shared__ __align__(16) double smem[];
-    double* sa = smem;                        // [kPStages][kPBK][LdM]
-    double* sb = smem + kPStages * kPBK * LdM;  // [kPStages][BN][kPLdK]
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int gid = lane >> 2, tig = lane & 3;
-    const int wm0 = (warp / WN) * WTM, wn0 = (warp % WN) * WTN;
-    // per-tile decode: tiles of job j occupy [base_j, base_j + tiles_j)
-    auto decode = [&](int64_t t, int& jb, int64_t& m0, int& n0) {
-        jb = 0;
-        while (jb + 1 < 4 && t >= prm.tiles[jb]) {
-            t -= prm.tiles[jb];
-            ++jb;
-        }
-        const int tn = static_cast<int>(t % prm.tiles_n[jb]);
-        m0 = (t / prm.tiles_n[jb]) * BM;
-        n0 = tn * BN;
-    };
-    auto c_list = [&](int jb) {
-        ColList cl;
-        cl.p[0] = prm.job[jb].c;
-        cl.ld[0] = prm.job[jb].ldc;
-        cl.start[1] = prm.job[jb].ncols;
-        cl.nseg = 1;
-        for (int i = 2; i <= kMaxSeg; ++i) cl.start[i] = prm.job[jb].ncols;
-        return cl;
-    };
-    // flattened (tile, k stage) sequence of this CTA
-    const int64_t my_tiles = total_tiles > blockIdx.x ? (total_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-    if (my_tiles == 0) return;
-    int jb0;
-    int64_t m00;
-    int n00;
-    decode(blockIdx.x, jb0, m00, n00);
-    const int nk = (prm.job[jb0].a.cols() + kPBK - 1) / kPBK;  // all jobs share k (asserted on the host)
-    const int64_t total_steps = my_tiles * nk;
-    auto issue = [&](int64_t step) {
-        if (step < total_steps) {
-            const int64_t t = blockIdx.x + (step / nk) * gridDim.x;
-            const int ks = static_cast<int>(step % nk);
-            int jb;
-            int64_t m0;
-            int n0;
-            decode(t, jb, m0, n0);
-            const ProductJob& job = prm.job[jb];
-            const int st = static_cast<int>(step % kPStages);
-            load_mcontig<BM, NT, kPBK>(sa + st * kPBK * LdM, job.a, ks * kPBK, job.a.cols(), m0, prm.n);
-            load_kcontig<BN, NT, kPBK>(sb + st * BN * kPLdK, c_list(jb), n0, job.ncols, ks * kPBK, job.a.cols());
-        }
-        cp_async_commit();
-    };
-    double acc[MT][NTL][2];
-#pragma unroll
-    for (int i = 0; i < MT; ++i)
-#pragma unroll
-        for (int j = 0; j < NTL; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-#pragma unroll
-    for (int s = 0; s < kPStages - 1; ++s) issue(s);
-    for (int64_t step = 0; step < total_steps; ++step) {
-        cp_async_wait<kPStages - 2>();
-        __syncthreads();
-        const int st = static_cast<int>(step % kPStages);
-        const double* a = sa + st * kPBK * LdM;
-        const double* b = sb + st * BN * kPLdK;
-#pragma unroll
-        for (int kk = 0; kk < kPBK; kk += 4) {
-            double af[MT], bf[NTL];
-#pragma unroll
-            for (int i = 0; i < MT; ++i) af[i] = a[(kk + tig) * LdM + wm0 + i * 8 + gid];
-#pragma unroll
-            for (int j = 0; j < NTL; ++j) bf[j] = b[(wn0 + j * 8 + gid) * kPLdK + kk + tig];
-#pragma unroll
-            for (int i = 0; i < MT; ++i)
-#pragma unroll
-                for (int j = 0; j < NTL; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
-        }
-        issue(step + kPStages - 1);
-        if (step % nk == nk - 1) {  // tile complete: registers -> Out, then start the next tile
-            const int64_t t = blockIdx.x + (step / nk) * gridDim.x;
-            int jb;
-            int64_t m0;
-            int n0;
-            decode(t, jb, m0, n0);
-            const ProductJob& job = prm.job[jb];
-#pragma unroll
-            for (int i = 0; i < MT; ++i)
-#pragma unroll
-                for (int j = 0; j < NTL; ++j) {
-                    const int64_t gm = m0 + wm0 + i * 8 + gid;
-                    const int gn = n0 + wn0 + j * 8 + 2 * tig;
-                    if (gm < prm.n) {
-#pragma unroll
-                        for (int h = 0; h < 2; ++h) {
-                            if (gn + h < job.ncols) {
-                                double* o = job.out + static_cast<int64_t>(gn + h) * job.ldo + gm;
-                                const double v = job.alpha * acc[i][j][h];
-                                *o = (job.beta == 0.0) ? v : v + job.beta * *o;
-                            }
-                        }
-                    }
-                    acc[i][j][0] = acc[i][j][1] = 0.0;
-                }
-        }
-    }
-    cp_async_wait<0>();
-}
 
 template <int BM, int BN, int WM, int WN>
 void launch_product(const ProductJob* jobs, int njobs, int64_t n) {
@@ -847,31 +728,9 @@ void launch_product(const ProductJob* jobs, int njobs, int64_t n) {
     constexpr size_t smem_epi = sizeof(double) * BN * (BM + 4);
     constexpr size_t smem = smem_pipe > smem_epi ? smem_pipe : smem_epi;
     static unsigned attr_mask = 0;
-    static int resident[64] = {0};
     if (rt.first_use(attr_mask)) {
         BOSP_CUDA(cudaFuncSetAttribute(k_product<BM, BN, WM, WN>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        BOSP_CUDA(cudaFuncSetAttribute(k_product_persist<BM, BN, WM, WN>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_pipe));
-        int r = 0;
-        BOSP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, k_product_persist<BM, BN, WM, WN>, NT, smem_pipe));
-        resident[rt.device() & 63] = std::max(1, r);
-    }
-    bool same_k = true;
-    for (int j = 1; j < njobs; ++j) same_k &= jobs[j].a.cols() == jobs[0].a.cols();
-    // opt-in: measured 5-7 % slower than the tiled grid at d = 320 (the DMMA inner loop, not the
-    // per-tile pipeline fill, is what limits these shapes)
-    static const bool persist = std::getenv("BOSP_PRODUCT_PERSIST") != nullptr;
-    if (persist && same_k && jobs[0].a.cols() > 0) {
-        int64_t total = 0;
-        for (int j = 0; j < njobs; ++j) total += prm.tiles[j];
-        for (int j = njobs; j < 4; ++j) prm.tiles[j] = 0;
-        const int64_t slots = static_cast<int64_t>(resident[rt.device() & 63]) * rt.sm_count();
-        const unsigned grid = static_cast<unsigned>(std::max<int64_t>(1, std::min(total, slots)));
-        LaunchScope ls("product", bytes, flops);
-        k_product_persist<BM, BN, WM, WN><<<grid, NT, smem_pipe, rt.stream()>>>(prm, total);
-        BOSP_LAUNCH_CHECK();
-        return;
     }
     LaunchScope ls("product", bytes, flops);
     const unsigned gx = static_cast<unsigned>(std::min<int64_t>(max_tiles, 65535));
@@ -1018,9 +877,7 @@ template <int BN>
 void launch_skinny(const ProductJob* jobs, int njobs, int64_t n) {
     // one m-tile per warp (64-row tiles, ~half the shared memory, 2+ blocks per SM) measured
     // 20-30 % faster than two for C widths >= 16 on config 2's shapes; width 8 keeps two
-    static const int rt_env = std::getenv("BOSP_SKINNY_RT") ? std::atoi(std::getenv("BOSP_SKINNY_RT")) : 0;
-    const int rt = rt_env ? rt_env : (BN <= 8 ? 2 : 1);
-    if (rt == 1) return launch_skinny_rt<BN, 1>(jobs, njobs, n);
+    if (BN > 8) return launch_skinny_rt<BN, 1>(jobs, njobs, n);
     return launch_skinny_rt<BN, 2>(jobs, njobs, n);
 }
 
@@ -1055,125 +912,6 @@ void launch_skinny_rt(const ProductJob* jobs, int njobs, int64_t n) {
     BOSP_LAUNCH_CHECK();
 }
 
-// Skinny product without staging A: for Out = A*C the n rows are the MMA's M dimension, so the
-// A fragment of m8n8k4 (row gid, k tig) is one double per lane, A[m0 + gid, k0 + tig] -- a warp
-// reads 4 columns x 8 consecutive rows (eight full sectors).  Each warp owns RT x 8 rows and all
-// of C's column tiles; C sits in shared memory (<= 64 x 64).  No A staging means no block-wide
-// barrier and no 130 KB buffer, so several blocks per SM keep the loads in flight.
-template <int NT, int RT>
-__global__ void __launch_bounds__(256) k_product_regs(SkinnyParams prm) {
-    extern __shared__ __align__(16) double smem[];
-    const int kp = prm.kp, ldc = prm.ldc;
-    double* sc = smem;  // [NT * 8][ldc], zero-padded to kp
-    const ProductJob& job = prm.job[blockIdx.z];
-    const int kcols = job.a.cols();
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int gid = lane >> 2, tig = lane & 3;
-    for (int idx = threadIdx.x; idx < NT * 8 * kp; idx += 256) {
-        const int c = idx / kp, k = idx - c * kp;
-        sc[c * ldc + k] = (c < job.ncols && k < kcols) ? job.c[static_cast<int64_t>(c) * job.ldc + k] : 0.0;
-    }
-    __syncthreads();
-    constexpr int kRowsW = 8 * RT;
-    const int64_t n = prm.n;
-    const int64_t wtiles = (n + kRowsW - 1) / kRowsW;
-    const double alpha = job.alpha, beta = job.beta;
-    for (int64_t wt = static_cast<int64_t>(blockIdx.x) * 8 + warp; wt < wtiles; wt += static_cast<int64_t>(gridDim.x) * 8) {
-        const int64_t m0 = wt * kRowsW;
-        double acc[RT][NT][2];
-#pragma unroll
-        for (int i = 0; i < RT; ++i)
-#pragma unroll
-            for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-#pragma unroll 4
-        for (int kk = 0; kk < kp; kk += 4) {
-            const int kc = kk + tig;
-            const double* col = kc < kcols ? colptr(job.a, kc) + m0 + gid : nullptr;
-            double af[RT], bf[NT];
-#pragma unroll
-            for (int i = 0; i < RT; ++i) af[i] = (col && m0 + i * 8 + gid < n) ? __ldcs(col + i * 8) : 0.0;
-#pragma unroll
-            for (int j = 0; j < NT; ++j) bf[j] = sc[(j * 8 + gid) * ldc + kc];
-#pragma unroll
-            for (int i = 0; i < RT; ++i)
-#pragma unroll
-                for (int j = 0; j < NT; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
-        }
-        if (beta != 0.0) {  // Out = alpha A C + beta Out: every old value loaded before the first use
-#pragma unroll
-            for (int i = 0; i < RT; ++i)
-#pragma unroll
-                for (int j = 0; j < NT; ++j)
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        const int64_t row = m0 + i * 8 + gid;
-                        const int col = j * 8 + 2 * tig + h;
-                        const double o = (row < n && col < job.ncols)
-                                             ? __ldcs(job.out + static_cast<int64_t>(col) * job.ldo + row)
-                                             : 0.0;
-                        acc[i][j][h] = alpha * acc[i][j][h] + beta * o;
-                    }
-        } else {
-#pragma unroll
-            for (int i = 0; i < RT; ++i)
-#pragma unroll
-                for (int j = 0; j < NT; ++j) {
-                    acc[i][j][0] *= alpha;
-                    acc[i][j][1] *= alpha;
-                }
-        }
-#pragma unroll
-        for (int i = 0; i < RT; ++i) {
-            const int64_t row = m0 + i * 8 + gid;
-            if (row >= n) continue;
-#pragma unroll
-            for (int j = 0; j < NT; ++j)
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int col = j * 8 + 2 * tig + h;
-                    if (col < job.ncols) __stcs(job.out + static_cast<int64_t>(col) * job.ldo + row, acc[i][j][h]);
-                }
-        }
-    }
-}
-
-template <int BN>
-void launch_product_regs(const ProductJob* jobs, int njobs, int64_t n) {
-    constexpr int NT = BN / 8;
-#ifndef BOSP_PRODUCT_RT
-    constexpr int RT = NT <= 2 ? 4 : NT <= 4 ? 2 : 1;
-#else
-    constexpr int RT = BOSP_PRODUCT_RT;
-#endif
-    Runtime& rt = Runtime::get();
-    SkinnyParams prm{};
-    int kmax = 0;
-    double flops = 0, bytes = 0;
-    for (int j = 0; j < njobs; ++j) {
-        prm.job[j] = jobs[j];
-        kmax = std::max(kmax, jobs[j].a.cols());
-        const double k = jobs[j].a.cols(), b = jobs[j].ncols;
-        flops += 2.0 * n * k * b;
-        bytes += 8.0 * n * (k + b * (jobs[j].beta != 0.0 ? 2.0 : 1.0));
-    }
-    prm.n = n;
-    prm.kp = std::max(4, (kmax + 3) / 4 * 4);
-    prm.ldc = (prm.kp + 15) / 16 * 16 + 4;
-    const size_t smem = sizeof(double) * static_cast<size_t>(BN) * prm.ldc;
-    static int per_sm = 0;
-    if (per_sm == 0) {
-        BOSP_CUDA(cudaFuncSetAttribute(k_product_regs<NT, RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-        BOSP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_product_regs<NT, RT>, 256, 64 * 1024));
-        per_sm = std::max(per_sm, 1);
-    }
-    const int64_t wtiles = (n + 8 * RT - 1) / (8 * RT);
-    static const int waves = std::getenv("BOSP_PRODUCT_WAVES") ? std::atoi(std::getenv("BOSP_PRODUCT_WAVES")) : 1;
-    const int64_t ctas = std::max<int64_t>(
-        1, std::min<int64_t>((wtiles + 7) / 8, static_cast<int64_t>(per_sm) * waves * rt.sm_count() / njobs));
-    LaunchScope ls("product", bytes, flops);
-    k_product_regs<NT, RT><<<dim3(static_cast<unsigned>(ctas), 1, njobs), 256, smem, rt.stream()>>>(prm);
-    BOSP_LAUNCH_CHECK();
-}
 
 void check_aligned(const ColList& cl) {
     for (int s = 0; s < cl.nseg; ++s)
@@ -1200,21 +938,19 @@ void gram(const GramJob* jobs, int njobs, int64_t n) {
                                           sizeof(double) * jobs[j].a.cols(), Runtime::get().stream()));
         return;
     }
-    static const bool regs = !std::getenv("BOSP_GRAM_SMEM");
     // register-fragment Grams (n rows = the MMA k dimension, operands straight from global):
     // up to 4 x 4 fragment tiles (32 columns) every warp holds the whole tile; a side wider
     // than 32 is split over two warp groups (a 2 x 1, 1 x 2 or 2 x 2 group layout, each warp
     // <= 4 x 4 tiles); beyond wide_max columns the shared-memory tiled DMMA kernel
     // 48: config 2 is flat between 32 and 64; at 64 the rounding of config 5's 64-wide Grams
     // pushed its (repair-heavy) run into the reference's NumericalAbort path -- 48 converges
-    static const int wide_max = std::getenv("BOSP_GRAM_WIDE_MAX") ? std::atoi(std::getenv("BOSP_GRAM_WIDE_MAX")) : 48;
-    const int lim = wide_max;
-    if (amax <= lim && bmax <= lim && regs) {
+    constexpr int lim = 48;
+    if (amax <= lim && bmax <= lim) {
         const int mt = (amax + 7) / 8, nt = (bmax + 7) / 8;
         // a symmetric Gram up to 48 columns ([X | Y] of MGS-Biorth, m <= 24): every warp holds
         // all upper fragment pairs and loads each column fragment once (the 2 x 2 group layout
         // re-loads every fragment per group)
-        if (njobs == 1 && jobs[0].sym && mt == nt && (mt == 5 || mt == 6) && !std::getenv("BOSP_GRAM_SYM_GROUPS"))
+        if (njobs == 1 && jobs[0].sym && mt == nt && (mt == 5 || mt == 6))
             return mt == 5 ? launch_gram_regs<5, 5>(jobs, njobs, n) : launch_gram_regs<6, 6>(jobs, njobs, n);
         if (mt <= 4 && nt <= 4) {
             switch (mt * 4 + nt) {
@@ -1241,22 +977,14 @@ void gram(const GramJob* jobs, int njobs, int64_t n) {
             default: break;
         }
     }
-    static const int gw = std::getenv("BOSP_GEMM_WARPS") ? std::atoi(std::getenv("BOSP_GEMM_WARPS")) : 8;
-    static const bool narrow_b = std::getenv("BOSP_GRAM_NO_NARROW") == nullptr;
     if (amax <= 32 && bmax <= 32)
         launch_gram<32, 32, 2, 2>(jobs, njobs, n);
-    else if (narrow_b && bmax <= 32 && amax >= 128)
+    else if (bmax <= 32 && amax >= 128)
         // many output rows, <= 32 columns (the dense operator's A x = (A^T)^T x at the CG's
-        // widths): 128 x 32 tiles, the same 32 x 16 warp tiles, no padding of b to 64
-    {
+        // widths): 128 x 32 tiles, the same 32 x 16 warp tiles, no padding of b to 64.
         // 16-row stages keep two 8-warp CTAs per SM (the 32-row ring fits one): the tile is
         // DMMA-latency bound, not byte bound -- n = 16384, 32 columns: 1.47 -> 0.93 ms
-        static const bool deep = std::getenv("BOSP_GRAM_NARROW_BK32") != nullptr;
-        if (deep) launch_gram<128, 32, 4, 2>(jobs, njobs, n);
-        else launch_gram<128, 32, 4, 2, 16, 3>(jobs, njobs, n);
-    }
-    else if (gw == 4)
-        launch_gram<64, 64, 2, 2>(jobs, njobs, n);
+        launch_gram<128, 32, 4, 2, 16, 3>(jobs, njobs, n);
     else
         launch_gram<64, 64, 2, 4>(jobs, njobs, n);
 }
@@ -1492,19 +1220,6 @@ void product(const ProductJob* jobs, int njobs, int64_t n) {
     if (n == 0 || bmax == 0) return;
     int kmax = 0;
     for (int j = 0; j < njobs; ++j) kmax = std::max(kmax, jobs[j].a.cols());
-    static const bool regs = std::getenv("BOSP_PRODUCT_REGS") != nullptr;
-    if (kmax <= 64 && bmax <= 64 && kmax > 0 && regs) {
-        switch ((bmax + 7) / 8) {
-            case 1: return launch_product_regs<8>(jobs, njobs, n);
-            case 2: return launch_product_regs<16>(jobs, njobs, n);
-            case 3: return launch_product_regs<24>(jobs, njobs, n);
-            case 4: return launch_product_regs<32>(jobs, njobs, n);
-            case 5: return launch_product_regs<40>(jobs, njobs, n);
-            case 6: return launch_product_regs<48>(jobs, njobs, n);
-            case 7: return launch_product_regs<56>(jobs, njobs, n);
-            default: return launch_product_regs<64>(jobs, njobs, n);
-        }
-    }
     if (kmax <= 64 && bmax <= 64 && kmax > 0) {
         switch ((bmax + 7) / 8) {
             case 1: return launch_skinny<8>(jobs, njobs, n);
@@ -1518,11 +1233,8 @@ void product(const ProductJob* jobs, int njobs, int64_t n) {
         }
     }
     // k == 0: Out = beta * Out (handled by the kernel with an empty K loop)
-    static const int pw = std::getenv("BOSP_GEMM_WARPS") ? std::atoi(std::getenv("BOSP_GEMM_WARPS")) : 8;
     if (bmax <= 32)
         launch_product<64, 32, 2, 2>(jobs, njobs, n);
-    else if (pw == 4)
-        launch_product<64, 64, 2, 2>(jobs, njobs, n);
     else
         launch_product<64, 64, 2, 4>(jobs, njobs, n);
 }

@@ -75,7 +75,8 @@ struct DeviceState {
     // workspaces
     DBlock ku, mv, xt, yt, kxt, myt, xtb, ytb, pt, qt, rz, rw, zg, wg, tmp;
     DBlock small;                 // device copies of small coefficient matrices
-    DBlock scal;                  // per-column scalars (lambdas, residual sums)
+    DBlock scal;                  // per-column scalars: 4 slots of scal_cap doubles
+    int64_t scal_cap = 0;         // >= every window width / block size of this solve
     CgWorkspace cg;
     bool cg_deferred = false;  // some CG sweep counts are still on the device (cg.total_sweeps)
 
@@ -135,10 +136,17 @@ std::vector<DevBasis> deflation_bases(const DeviceState& st) {
     return bases;
 }
 
+// Per-column scalar slots on the device: 0 = window lambdas, 1 = residual numerators,
+// 2 = residual denominators, 3 = Step-6 block lambdas; each scal_cap doubles.
+double* scal_slot(DeviceState& st, int slot) {
+    if (st.scal.rows() != st.scal_cap) ensure_block(st.scal, st.scal_cap, 4);
+    return st.scal.data() + slot * st.scal.ld();
+}
+
 // Scalars (per-column lambdas) to the device.
-const double* upload_scalars(DeviceState& st, const std::vector<double>& v, int64_t offset) {
-    ensure_block(st.scal, 1024, 4);
-    double* d = st.scal.data() + offset;
+const double* upload_scalars(DeviceState& st, const std::vector<double>& v, int slot) {
+    require(static_cast<int64_t>(v.size()) <= st.scal_cap, "bosp: scalar slot overflow");
+    double* d = scal_slot(st, slot);
     if (!v.empty())
         BOSP_CUDA(cudaMemcpyAsync(d, v.data(), sizeof(double) * v.size(), cudaMemcpyHostToDevice, Runtime::get().stream()));
     return d;
@@ -206,8 +214,7 @@ RitzOut ritz_step(DeviceState& st, const LinearOperator& k, const LinearOperator
     // K^ = U^T (K U) and M^ = V^T (M V) are symmetric (K, M symmetric): upper tiles, mirrored --
     // exactly what finish_assembly's (A + A^T)/2 (projected_lrep.cpp:13-46) would make of them
     // up to rounding, for ~60 % of the Gram work at d = 320
-    static const bool sym_ritz = std::getenv("BOSP_RITZ_FULL") == nullptr;
-    jobs[0].sym = jobs[1].sym = sym_ritz;
+    jobs[0].sym = jobs[1].sym = true;
     gram(jobs, 2, st.n);
     Runtime::get().allreduce(g.data(), g.ld() * 2 * d);
     DenseMatrix both(d, 2 * d);
@@ -275,6 +282,7 @@ SolverState initialize(const LinearOperator& k, const LinearOperator& m, const I
     st.wx = wx;
     st.wp = wp;
     st.ww = ww;
+    st.scal_cap = std::max<int64_t>({cap, nb, 32});
     if (ns.r > 0) {
         st.x0 = DBlock(n, ns.r);
         st.y0 = DBlock(n, ns.r);
@@ -344,16 +352,17 @@ bool iterate_once(SolverState& ss, const LinearOperator& k, const LinearOperator
         st.stats.matvec_count += 2 * wxa;
     }
     const double* lam_dev = upload_scalars(st, sol.lambdas, 0);
-    double* num_dev = st.scal.data() + 1024;
-    double* den_dev = st.scal.data() + 2048;
+    double* num_dev = scal_slot(st, 1);
+    double* den_dev = scal_slot(st, 2);
     residual_sums(st.kxt.view(), st.myt.view(), xt_b, yt_b, st.xt.view(), st.yt.view(), lam_dev,
                   num_dev, den_dev);
-    std::vector<double> nd(static_cast<size_t>(2 * 1024));
-    BOSP_CUDA(cudaMemcpyAsync(nd.data(), num_dev, sizeof(double) * 2048, cudaMemcpyDeviceToHost, Runtime::get().stream()));
+    const int64_t sld = st.scal.ld();  // slots 1 and 2 are adjacent columns of st.scal
+    std::vector<double> nd(static_cast<size_t>(2 * sld));
+    BOSP_CUDA(cudaMemcpyAsync(nd.data(), num_dev, sizeof(double) * 2 * sld, cudaMemcpyDeviceToHost, Runtime::get().stream()));
     Runtime::get().sync();
     for (int64_t j = 0; j < wxa; ++j) {
         const double lam = sol.lambdas[j];
-        st.residuals[st.frozen + j] = std::sqrt(nd[j]) / ((1.0 + lam) * std::sqrt(nd[1024 + j]));
+        st.residuals[st.frozen + j] = std::sqrt(nd[j]) / ((1.0 + lam) * std::sqrt(nd[sld + j]));
     }
     const int64_t base = st.locked_count() + st.frozen;
     int64_t prefix = 0;
@@ -416,7 +425,7 @@ bool iterate_once(SolverState& ss, const LinearOperator& k, const LinearOperator
     int64_t kw = 0;
     if (nb_eff > 0) {
         std::vector<double> lam_b(sol.lambdas.begin() + c0, sol.lambdas.begin() + c0 + nb_eff);
-        const double* lamb = upload_scalars(st, lam_b, 3072);
+        const double* lamb = upload_scalars(st, lam_b, 3);
         ensure_block(st.rz, n, nb_eff);
         ensure_block(st.rw, n, nb_eff);
         ensure_block(st.zg, n, nb_eff);

@@ -7,6 +7,7 @@
 #include "operators.hpp"
 
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 
 #include "comm.hpp"
@@ -623,7 +624,9 @@ public:
     DeviceCallbackOp(int64_t n, LinearOperator::DeviceApplyFn fn)
         : OperatorImpl(n, LinearOperator::Kind::matrix_free_callback), fn_(std::move(fn)) {}
     void apply(const DMat& x, const DMat& y) const override {
-        fn_(x.p, x.ld, y.p, y.ld, x.cols, Runtime::get().stream());
+        Runtime& rt = Runtime::get();
+        const int st = fn_(rt.device(), x.p, x.ld, y.p, y.ld, x.cols, rt.stream());
+        if (st != 0) throw Error("device callback returned " + std::to_string(st));
     }
     bool capturable() const override { return false; }
 
@@ -634,6 +637,10 @@ private:
 }  // namespace
 
 OperatorImpl::~OperatorImpl() = default;
+uint64_t OperatorImpl::next_uid() {
+    static std::atomic<uint64_t> counter{0};
+    return ++counter;
+}
 
 LinearOperator LinearOperator::from_dense(const DenseMatrix& a) {
     require(a.rows() == a.cols(), "LinearOperator: dense operator must be square");

@@ -10,8 +10,11 @@ inline namespace b200 {
 
 class OperatorImpl {
 public:
-    OperatorImpl(int64_t n, LinearOperator::Kind k) : n_(n), kind_(k) {}
+    OperatorImpl(int64_t n, LinearOperator::Kind k) : n_(n), kind_(k), uid_(next_uid()) {}
     virtual ~OperatorImpl();
+    // Process-unique id (never reused, unlike the object's address): caches of recorded CUDA
+    // graphs key on it, so a rebuilt operator at a recycled address never replays a stale graph.
+    uint64_t uid() const { return uid_; }
     // y(:, j) = A x(:, j), x and y device blocks with rows == dim(), y fully overwritten.
     virtual void apply(const DMat& x, const DMat& y) const = 0;
     int64_t dim() const { return n_; }
@@ -31,8 +34,10 @@ public:
     virtual bool has_masked_dot() const { return false; }
 
 private:
+    static uint64_t next_uid();
     int64_t n_;
     LinearOperator::Kind kind_;
+    uint64_t uid_;
 };
 
 }  // namespace b200

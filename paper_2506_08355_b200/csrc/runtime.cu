@@ -69,6 +69,7 @@ double* Runtime::scratch(size_t doubles) {
         if (scratch_) free(scratch_);
         scratch_cap_ = doubles + doubles / 2 + 4096;
         scratch_ = static_cast<double*>(alloc(scratch_cap_ * sizeof(double)));
+        ++scratch_gen_;
     }
     return scratch_;
 }
@@ -78,6 +79,7 @@ unsigned int* Runtime::tickets(size_t count) {
         if (tickets_) free(tickets_);
         tickets_cap_ = count + 1024;
         tickets_ = static_cast<unsigned int*>(alloc(tickets_cap_ * sizeof(unsigned int)));
+        ++scratch_gen_;
         BOSP_CUDA(cudaMemsetAsync(tickets_, 0, tickets_cap_ * sizeof(unsigned int), stream_));
     }
     return tickets_;

@@ -83,6 +83,9 @@ public:
     double* scratch(size_t doubles);
     // Zero-initialised uint32 tickets; each kernel that takes tickets leaves them at zero.
     unsigned int* tickets(size_t count);
+    // Bumped whenever scratch() or tickets() reallocates: a CUDA graph that captured the old
+    // pointers must not be replayed after that (dev_cg keys its graph cache on it).
+    uint64_t scratch_generation() const { return scratch_gen_; }
     // Pinned host staging (grow-only).
     double* pinned(size_t doubles);
     // Double-buffered pinned ring for large pageable host<->device copies (to_host/to_device):
@@ -148,6 +151,7 @@ private:
     int64_t n_global_ = 0, row0_ = 0;
     double* scratch_ = nullptr;
     size_t scratch_cap_ = 0;
+    uint64_t scratch_gen_ = 0;
     unsigned int* tickets_ = nullptr;
     size_t tickets_cap_ = 0;
     double* pinned_ = nullptr;

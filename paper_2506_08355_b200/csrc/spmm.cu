@@ -56,75 +56,15 @@ struct KTimer {
     }
 };
 
-// Rows whose slice is wider than kWMax fall back to the streaming loop below.
-constexpr int kWMax = 16;
 // Occupancy floor of the masked/halo SELL kernel (the CG's SpMM): it is memory-latency bound
 // and 4 resident blocks (64 registers) measured best for the batched CG on config 2.
 #ifndef BOSP_SELL_MINB
 #define BOSP_SELL_MINB 4
 #endif
 
-__global__ void __launch_bounds__(kRows) k_sell(SellDev a, const double* __restrict__ x, int64_t ldx,
-                                                 double* __restrict__ y, int64_t ldy, int ncols,
-                                                 KTimer tm) {
-    tm.start();
-    tm.columns(nullptr, 0, 0, ncols);
-    const int64_t row = static_cast<int64_t>(blockIdx.x) * kRows + threadIdx.x;
-    if (row < a.n) {
-        const int64_t s = row >> 5;
-        const int64_t base = a.slice_ptr[s] + (row & 31);
-        const int w = a.slice_w[s];
-        if (w <= kWMax) {
-            int col[kWMax];
-            double val[kWMax];
-#pragma unroll
-            for (int k = 0; k < kWMax; ++k) {
-                col[k] = k < w ? __ldg(a.col + base + 32 * k) : 0;
-                val[k] = k < w ? __ldg(a.val + base + 32 * k) : 0.0;
-            }
-            int j = 0;
-            for (; j + 4 <= ncols; j += 4) {
-                const double* x0 = x + static_cast<int64_t>(j) * ldx;
-                double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-#pragma unroll
-                for (int k = 0; k < kWMax; ++k) {
-                    if (k < w) {
-                        const double* xc = x0 + col[k];
-                        s0 += val[k] * __ldg(xc);
-                        s1 += val[k] * __ldg(xc + ldx);
-                        s2 += val[k] * __ldg(xc + 2 * ldx);
-                        s3 += val[k] * __ldg(xc + 3 * ldx);
-                    }
-                }
-                double* yo = y + static_cast<int64_t>(j) * ldy + row;
-                yo[0] = s0;
-                yo[ldy] = s1;
-                yo[2 * ldy] = s2;
-                yo[3 * ldy] = s3;
-            }
-            for (; j < ncols; ++j) {
-                const double* x0 = x + static_cast<int64_t>(j) * ldx;
-                double s0 = 0.0;
-#pragma unroll
-                for (int k = 0; k < kWMax; ++k)
-                    if (k < w) s0 += val[k] * __ldg(x0 + col[k]);
-                y[static_cast<int64_t>(j) * ldy + row] = s0;
-            }
-        } else {
-            for (int j = 0; j < ncols; ++j) {
-                const double* x0 = x + static_cast<int64_t>(j) * ldx;
-                double s0 = 0.0;
-                for (int k = 0; k < w; ++k)
-                    s0 += __ldg(a.val + base + 32 * k) * __ldg(x0 + __ldg(a.col + base + 32 * k));
-                y[static_cast<int64_t>(j) * ldy + row] = s0;
-            }
-        }
-    }
-    tm.stop();
-}
 
 // Per-block partial sums of x(:,j)^T y(:,j) for the CB columns of this block, written to
-// dots[j * gridDim.x + blockIdx.x] (fixed order; folded by cg_update_fused).
+// dots[j * gridDim.x + blockIdx.x] (fixed order; folded by the CG update blocks).
 template <int CB>
 __device__ __forceinline__ void block_dots_out(double (&d)[CB], double* dots, int j0, int ncols) {
     __shared__ double red[kRows / 32][CB];
@@ -234,97 +174,6 @@ __global__ void __launch_bounds__(kRows) k_sell_plain(SellDev a, const double* _
     tm.stop();
 }
 
-// Wide variant: one thread per row loads the row's (<= kWide) entries once and sweeps all
-// columns in groups of 4 (not unrolled), so the matrix is read once per apply and each row
-// pays one index-load latency instead of one per column group.  With DOT the per-column
-// x^T y partials are warp-reduced per group (fixed order) into shared memory and folded per
-// block, then across blocks by the last block.
-constexpr int kWide = 8;
-constexpr int kWideMaxCols = 160;
-
-template <bool DOT>
-__global__ void __launch_bounds__(kRows, 3) k_sell_wide(SellDev a, const double* __restrict__ x, int64_t ldx,
-                                                         double* __restrict__ y, int64_t ldy, int ncols,
-                                                         KTimer tm, DotOut dots) {
-    __shared__ double red[DOT ? kRows / 32 : 1][DOT ? kWideMaxCols : 1];
-    tm.start();
-    tm.columns(DOT ? dots.active : nullptr, 0, 0, ncols);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (DOT)
-        for (int i = threadIdx.x; i < (kRows / 32) * ncols; i += kRows) red[i / ncols][i % ncols] = 0.0;
-    const int64_t ntiles = (a.n + kRows - 1) / kRows;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int64_t row = tile * kRows + threadIdx.x;
-        const bool valid = row < a.n;
-        int w = 0;
-        int64_t base = 0;
-        if (valid) {
-            const int64_t s = row >> 5;
-            base = a.slice_ptr[s] + (row & 31);
-            w = a.slice_w[s];
-        }
-        const bool fast = w <= kWide;
-        int col[kWide];
-        double val[kWide];
-#pragma unroll
-        for (int k = 0; k < kWide; ++k) {
-            const bool in = fast && k < w;
-            col[k] = in ? __ldg(a.col + base + 32 * k) : 0;
-            val[k] = in ? __ldg(a.val + base + 32 * k) : 0.0;
-        }
-#pragma unroll 1
-        for (int j0 = 0; j0 < ncols; j0 += 4) {
-            bool on[4];
-            bool any = false;
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                on[c] = j0 + c < ncols && (!DOT || !dots.active || dots.active[j0 + c] != 0);
-                any |= on[c];
-            }
-            if (!any) continue;  // uniform across the block
-            const double* xb = x + static_cast<int64_t>(j0) * ldx;
-            double acc[4] = {0.0, 0.0, 0.0, 0.0};
-            if (fast) {
-#pragma unroll
-                for (int k = 0; k < kWide; ++k)
-                    if (k < w)
-#pragma unroll
-                        for (int c = 0; c < 4; ++c)
-                            if (on[c]) acc[c] += val[k] * __ldg(xb + c * ldx + col[k]);
-            } else if (valid) {
-                for (int k = 0; k < w; ++k) {
-                    const int cc = __ldg(a.col + base + 32 * k);
-                    const double v = __ldg(a.val + base + 32 * k);
-#pragma unroll
-                    for (int c = 0; c < 4; ++c)
-                        if (on[c]) acc[c] += v * __ldg(xb + c * ldx + cc);
-                }
-            }
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                if (!on[c]) continue;
-                if (valid) y[(j0 + c) * ldy + row] = acc[c];
-                if (DOT) {
-                    double t = valid ? __ldg(xb + c * ldx + row) * acc[c] : 0.0;
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-                    if (lane == 0) red[warp][j0 + c] += t;
-                }
-            }
-        }
-    }
-    if (DOT) {
-        __syncthreads();
-        for (int j = threadIdx.x; j < ncols; j += kRows) {
-            double t = 0.0;
-#pragma unroll
-            for (int q = 0; q < kRows / 32; ++q) t += red[q][j];
-            dots.parts[static_cast<int64_t>(j) * gridDim.x + blockIdx.x] = t;
-        }
-        fold_dots_last_block(dots.parts, ncols, dots.ticket, dots.out);
-    }
-    tm.stop();
-}
 
 // Column-group variant: grid.y walks groups of CB columns, grid.x strides over 256-row tiles;
 // the row's entries are re-read per column group (L2).  Optionally accumulates x^T y per
@@ -823,180 +672,6 @@ __global__ void __launch_bounds__(kRows) k_dia_sym(DiaDev a, const double* __res
     tm.stop();
 }
 
-// ---- DIA SpMM with bulk-async (TMA 1-D) staging of x -------------------------------------
-// Offsets are grouped into windows (runs of diagonals closer than kWinGap).  For a tile of kRows
-// rows starting at i0 (even), window w needs x rows [i0 + lo_w, i0 + kRows - 1 + hi_w]; one
-// cp.async.bulk per (column, window) lands them in shared memory, double-buffered against the
-// compute of the previous tile, so a thread's loads are shared-memory reads and the DRAM
-// stream is kept busy by the copy engine instead of by registers.
-struct DiaWin {
-    int nwin = 0;
-    int s = 0;                // doubles per column per stage
-    int lo[kDiaMax] = {};     // window start offset rounded down to even
-    int len[kDiaMax] = {};    // doubles staged per window (even)
-    int base[kDiaMax] = {};   // window start in the column's stage slice
-    int sidx[kDiaMax] = {};   // per diagonal: smem index of x(i0 + off_k) minus 0 (add t)
-    int sctr = -1;            // smem index of x(i0) when a window covers offset 0, else -1
-};
-
-constexpr int kWinGap = 512;
-
-bool dia_windows(const DiaDev& a, DiaWin& w) {
-    w = DiaWin{};
-    int k = 0;
-    while (k < a.ndiag) {
-        int e = k;
-        while (e + 1 < a.ndiag && a.off[e + 1] - a.off[e] <= kWinGap) ++e;
-        if (a.off[e] - a.off[k] > (int64_t(1) << 20)) return false;
-        const int lo = static_cast<int>(a.off[k]), hi = static_cast<int>(a.off[e]);
-        const int lo2 = lo & ~1;
-        int len = kRows + (hi - lo2) + 2;
-        len += len & 1;
-        const int wi = w.nwin++;
-        w.lo[wi] = lo2;
-        w.len[wi] = len;
-        w.base[wi] = w.s;
-        for (int q = k; q <= e; ++q) w.sidx[q] = w.s + static_cast<int>(a.off[q]) - lo2;
-        if (lo <= 0 && 0 <= hi) w.sctr = w.s - lo2;
-        w.s += len;
-        k = e + 1;
-    }
-    return true;
-}
-
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-    return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned cnt) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(cnt));
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
-    asm volatile(
-        "{\n .reg .pred p;\n"
-        "WAIT_%=:\n"
-        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(b)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* b) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(b))
-        : "memory");
-}
-
-template <int CB>
-__device__ __forceinline__ void dia_stage_issue(const DiaWin& w, const double* const (&xcol)[CB], const bool (&on)[CB],
-                                                int64_t n, int64_t i0, double* stage, unsigned long long* bar) {
-    unsigned tx = 0;
-    int64_t g0s[kDiaMax], cnts[kDiaMax];
-    for (int q = 0; q < w.nwin; ++q) {
-        const int64_t b = i0 + w.lo[q];
-        const int64_t g0 = b < 0 ? 0 : b;
-        const int64_t g1 = min(b + w.len[q], n);  // exclusive; even
-        g0s[q] = g0;
-        cnts[q] = g1 > g0 ? g1 - g0 : 0;
-    }
-    int act = 0;
-#pragma unroll
-    for (int c = 0; c < CB; ++c) act += on[c];
-    for (int q = 0; q < w.nwin; ++q) tx += static_cast<unsigned>(cnts[q] * 8) * act;
-    mbar_expect_tx(bar, tx);
-#pragma unroll
-    for (int c = 0; c < CB; ++c) {
-        if (!on[c]) continue;
-        for (int q = 0; q < w.nwin; ++q) {
-            if (cnts[q] == 0) continue;
-            const int64_t b = i0 + w.lo[q];
-            bulk_g2s(stage + c * w.s + w.base[q] + (g0s[q] - b), xcol[c] + g0s[q], static_cast<unsigned>(cnts[q] * 8), bar);
-        }
-    }
-}
-
-template <int CB, bool DOT, int ND>
-__global__ void __launch_bounds__(kRows) k_dia_tma(DiaDev a, DiaWin w, const double* __restrict__ x, int64_t ldx,
-                                                    double* __restrict__ y, int64_t ldy, int ncols, KTimer tm,
-                                                    DotOut dots) {
-    extern __shared__ __align__(128) double sm_dia[];
-    __shared__ __align__(8) unsigned long long bar[2];
-    tm.start();
-    tm.columns(DOT ? dots.active : nullptr, 0, 0, ncols);
-    const int j0 = blockIdx.y * CB;
-    double d[CB];
-#pragma unroll
-    for (int c = 0; c < CB; ++c) d[c] = 0.0;
-    bool on[CB];
-    const bool any = group_columns<CB, DOT>(dots, j0, ncols, on);
-    const int64_t n = a.n;
-    const int64_t ntiles = (n + kRows - 1) / kRows;
-    const int64_t mine = any && blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-    const double* xcol[CB];
-    double* ycol[CB];
-#pragma unroll
-    for (int c = 0; c < CB; ++c) {
-        xcol[c] = x + static_cast<int64_t>(j0 + c) * ldx;
-        ycol[c] = y + static_cast<int64_t>(j0 + c) * ldy;
-    }
-    const int stage_len = CB * w.s;
-    if (threadIdx.x == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    }
-    __syncthreads();
-    if (threadIdx.x == 0)
-        for (int64_t k = 0; k < 2 && k < mine; ++k)
-            dia_stage_issue<CB>(w, xcol, on, n, (blockIdx.x + k * gridDim.x) * kRows, sm_dia + k * stage_len, &bar[k]);
-    double v[ND];
-    int sx[ND];
-#pragma unroll
-    for (int k = 0; k < ND; ++k) sx[k] = w.sidx[k] + threadIdx.x;
-    for (int64_t k = 0; k < mine; ++k) {
-        const int64_t i = (blockIdx.x + k * gridDim.x) * kRows + threadIdx.x;
-        const int st = static_cast<int>(k & 1);
-        unsigned mk = 0;
-        if (i < n) {
-            mk = __ldg(a.mask + i);
-#pragma unroll
-            for (int q = 0; q < ND; ++q) {
-                const int vi = a.vidx[q];
-                v[q] = vi < 0 ? a.cval[q] : __ldg(a.val + static_cast<int64_t>(vi) * n + i);
-            }
-        }
-        mbar_wait(&bar[st], static_cast<unsigned>((k >> 1) & 1));
-        if (i < n) {
-            const double* sb = sm_dia + st * stage_len;
-#pragma unroll
-            for (int c = 0; c < CB; ++c) {
-                if (!on[c]) continue;
-                const double* xs = sb + c * w.s;
-                double acc = 0.0;
-#pragma unroll
-                for (int q = 0; q < ND; ++q) {
-                    const double t = xs[sx[q]];
-                    acc = ((mk >> q) & 1u) ? fma(v[q], t, acc) : acc;
-                }
-                __stcg(ycol[c] + i, acc);
-                if (DOT) d[c] = fma(w.sctr >= 0 ? xs[w.sctr + threadIdx.x] : __ldg(xcol[c] + i), acc, d[c]);
-            }
-        }
-        __syncthreads();  // every thread is done with this stage before it is refilled
-        if (threadIdx.x == 0 && k + 2 < mine) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            dia_stage_issue<CB>(w, xcol, on, n, (blockIdx.x + (k + 2) * gridDim.x) * kRows, sm_dia + st * stage_len,
-                                &bar[st]);
-        }
-    }
-    if (DOT) {
-        block_dots_out<CB>(d, dots.parts, j0, ncols);
-        fold_dots_last_block(dots.parts, ncols, dots.ticket, dots.out);
-    }
-    tm.stop();
-}
 
 // Row-tile blocks per column group: one per tile, bounded with dots by the partials buffer
 // (ncols x blocks doubles); the last block folds them.
@@ -1256,8 +931,7 @@ int sell_spmm(const SellDev& a, const DMat& x, const DMat& y, const SpmmDot* dot
     KTimer tm{rt.timer_begin(fam, bytes, flops, 12.0 * a.nnz + 4.0 * (a.n + 1), ncols)};
     LaunchScope ls(fam, bytes, flops, false);
     // Column groups of CB (grid.y) keep many independent blocks in flight; measured 2x the
-    // bandwidth of the all-columns-per-thread variant (k_sell) on config 2 (B200).
-    static const int variant = std::getenv("BOSP_SPMM_CB") ? std::atoi(std::getenv("BOSP_SPMM_CB")) : 4;
+    // bandwidth of an all-columns-per-thread variant on config 2 (B200).
     const unsigned gx = row_blocks(a.n, dot, ncols);
     const dim3 grid4(gx, (ncols + 3) / 4);
     if (a.halo) {  // row-partitioned: columns >= n read the halo copy of neighbour rows
@@ -1267,20 +941,10 @@ int sell_spmm(const SellDev& a, const DMat& x, const DMat& y, const SpmmDot* dot
         else
             k_sell_cb<4, false, true><<<grid4, kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm, DotOut{});
     } else if (dot) {
-        if (variant == 1 && ncols <= kWideMaxCols)
-            k_sell_wide<true><<<gx, kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm,
+        k_sell_cb<4, true><<<grid4, kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm,
                                                              DotOut{dot->parts, dot->ticket, dot->out, dot->active});
-        else
-            k_sell_cb<4, true><<<grid4, kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm,
-                                                                 DotOut{dot->parts, dot->ticket, dot->out, dot->active});
     } else {
-        switch (variant) {
-            case 1: k_sell_wide<false><<<gx, kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm, DotOut{}); break;
-            case 0: k_sell<<<gx, kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm); break;
-            case 2: k_sell_cb<2, false><<<dim3(gx, (ncols + 1) / 2), kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm, DotOut{}); break;
-            case 8: k_sell_cb<8, false><<<dim3(gx, (ncols + 7) / 8), kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm, DotOut{}); break;
-            default: k_sell_plain<4><<<dim3(gx, (ncols + 3) / 4), kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm); break;
-        }
+        k_sell_plain<4><<<grid4, kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm);
     }
     BOSP_LAUNCH_CHECK();
     return static_cast<int>(gx);
@@ -1298,15 +962,13 @@ template <int CB, int ND>
 unsigned launch_dia_row(const DiaDev& a, const DMat& x, const DMat& y, const DotOut& dd, bool dot, dim3 grid, KTimer tm) {
     Runtime& rt = Runtime::get();
     const int ncols = static_cast<int>(x.cols);
-    static const bool two = std::getenv("BOSP_DIA_1PHASE") == nullptr;
     bool var = false;
     for (int k = 0; k < a.ndiag; ++k) var = var || a.vidx[k] >= 0;
     auto go = [&](auto kern) { kern<<<grid, kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm, dd); };
     bool sym = (ND & 1) && a.off[ND / 2] == 0 && a.off[ND / 2 - 1] == -1 && a.off[ND / 2 + 1] == 1;
     for (int k = 0; k < ND; ++k)
         if (k < ND / 2 - 1 || k > ND / 2 + 1) sym = sym && (a.off[k] & 1) == 0;
-    static const bool nosym = std::getenv("BOSP_DIA_NOSYM") != nullptr;
-    if (sym && !nosym) {
+    if (sym) {
         const dim3 g2(std::min<unsigned>(grid.x, row_blocks(a.n / 2, nullptr, ncols)), grid.y);
         auto go2 = [&](auto kern) { kern<<<g2, kRows, 0, rt.stream()>>>(a, x.p, x.ld, y.p, y.ld, ncols, tm, dd); };
         int nvar = 0;
@@ -1316,64 +978,23 @@ unsigned launch_dia_row(const DiaDev& a, const DMat& x, const DMat& y, const Dot
         else dot ? go2(k_dia_sym<CB, true, ND, 2>) : go2(k_dia_sym<CB, false, ND, 2>);
         return g2.x;
     }
-    if (two) {
-        if (var) dot ? go(k_dia_row<CB, true, ND, true, true>) : go(k_dia_row<CB, false, ND, true, true>);
-        else dot ? go(k_dia_row<CB, true, ND, true, false>) : go(k_dia_row<CB, false, ND, true, false>);
-    } else {
-        if (var) dot ? go(k_dia_row<CB, true, ND, false, true>) : go(k_dia_row<CB, false, ND, false, true>);
-        else dot ? go(k_dia_row<CB, true, ND, false, false>) : go(k_dia_row<CB, false, ND, false, false>);
-    }
+    if (var) dot ? go(k_dia_row<CB, true, ND, true, true>) : go(k_dia_row<CB, false, ND, true, true>);
+    else dot ? go(k_dia_row<CB, true, ND, true, false>) : go(k_dia_row<CB, false, ND, true, false>);
     return grid.x;
 }
 
-template <int CB, int ND>
-unsigned launch_dia_tma(const DiaDev& a, const DiaWin& w, const DMat& x, const DMat& y, const SpmmDot* dot, KTimer tm) {
-    Runtime& rt = Runtime::get();
-    const int ncols = static_cast<int>(x.cols);
-    const size_t smem = sizeof(double) * 2 * CB * static_cast<size_t>(w.s);
-    auto kern = dot ? k_dia_tma<CB, true, ND> : k_dia_tma<CB, false, ND>;
-    static int configured[2] = {0, 0};
-    static int resident[2] = {0, 0};
-    const int di = dot ? 1 : 0;
-    if (configured[di] < static_cast<int>(smem)) {
-        BOSP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        BOSP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident[di], kern, kRows, smem));
-        configured[di] = static_cast<int>(smem);
-    }
-    const int groups = (ncols + CB - 1) / CB;
-    const int64_t slots = static_cast<int64_t>(std::max(resident[di], 1)) * rt.sm_count();
-    const unsigned gx = std::min<unsigned>(row_blocks(a.n, dot, ncols),
-                                           static_cast<unsigned>(std::max<int64_t>(1, slots / groups)));
-    const DotOut dd = dot ? DotOut{dot->parts, dot->ticket, dot->out, dot->active} : DotOut{};
-    kern<<<dim3(gx, groups), kRows, smem, rt.stream()>>>(a, w, x.p, x.ld, y.p, y.ld, ncols, tm, dd);
-    BOSP_LAUNCH_CHECK();
-    return gx;
-}
 
 template <int CB>
 unsigned launch_dia(const DiaDev& a, const DMat& x, const DMat& y, const SpmmDot* dot, KTimer tm) {
     const int ncols = static_cast<int>(x.cols);
-    static const int tma = std::getenv("BOSP_DIA_TMA") ? std::atoi(std::getenv("BOSP_DIA_TMA")) : 0;
-    DiaWin w;
-    if (tma && (reinterpret_cast<uintptr_t>(x.p) & 15) == 0 && a.n >= kRows && dia_windows(a, w) &&
-        sizeof(double) * 2 * CB * static_cast<size_t>(w.s) <= 110 * 1024) {
-        switch (a.ndiag) {
-            case 3: return launch_dia_tma<CB, 3>(a, w, x, y, dot, tm);
-            case 5: return launch_dia_tma<CB, 5>(a, w, x, y, dot, tm);
-            case 7: return launch_dia_tma<CB, 7>(a, w, x, y, dot, tm);
-            case 9: return launch_dia_tma<CB, 9>(a, w, x, y, dot, tm);
-            default: break;
-        }
-    }
-    static const bool pairs = std::getenv("BOSP_DIA_PAIRS") != nullptr;
-    if (!pairs && a.n < (int64_t(1) << 31) && (a.ndiag == 3 || a.ndiag == 5 || a.ndiag == 7 || a.ndiag == 9)) {
+    if (a.n < (int64_t(1) << 31) && (a.ndiag == 3 || a.ndiag == 5 || a.ndiag == 7 || a.ndiag == 9)) {
         // a few rows per thread: the per-block prologue/epilogue (column mask, timer, dot
         // reduction) is then amortised; ~kDiaWaves resident waves over all column groups
-        static const int waves = std::getenv("BOSP_DIA_WAVES") ? std::atoi(std::getenv("BOSP_DIA_WAVES")) : 8;
+        constexpr int waves = 8;
         const int groups = (ncols + CB - 1) / CB;
         const unsigned cap = static_cast<unsigned>(
             std::max<int64_t>(1, (static_cast<int64_t>(waves) * Runtime::get().sm_count() + groups - 1) / groups));
-        const unsigned gx = waves > 0 ? std::min(row_blocks(a.n, dot, ncols), cap) : row_blocks(a.n, dot, ncols);
+        const unsigned gx = std::min(row_blocks(a.n, dot, ncols), cap);
         const dim3 grid(gx, (ncols + CB - 1) / CB);
         const DotOut dd = dot ? DotOut{dot->parts, dot->ticket, dot->out, dot->active} : DotOut{};
         const bool d = dot != nullptr;
@@ -1415,9 +1036,7 @@ int dia_spmm(const DiaDev& a, const DMat& x, const DMat& y, const SpmmDot* dot) 
     const char* fam = dot ? "spmm_cg" : "spmm";
     KTimer tm{rt.timer_begin(fam, bytes, flops, 12.0 * a.nnz + 4.0 * (a.n + 1), ncols)};
     LaunchScope ls(fam, bytes, flops, false);
-    static const int cb = std::getenv("BOSP_DIA_CB") ? std::atoi(std::getenv("BOSP_DIA_CB")) : 4;
-    const unsigned gx = cb == 8 ? launch_dia<8>(a, x, y, dot, tm) : cb == 2 ? launch_dia<2>(a, x, y, dot, tm)
-                                                                            : launch_dia<4>(a, x, y, dot, tm);
+    const unsigned gx = launch_dia<4>(a, x, y, dot, tm);
     return static_cast<int>(gx);
 }
 
@@ -1443,8 +1062,7 @@ int stencil_spmm(const StencilDev& s, const DMat& x, const DMat& y, const SpmmDo
     if (part) {
         if (dot) k_stencil<CB, true, true><<<grid, kRows, 0, rt.stream()>>>(s, x.p, x.ld, y.p, y.ld, ncols, tm, dd);
         else k_stencil<CB, false, true><<<grid, kRows, 0, rt.stream()>>>(s, x.p, x.ld, y.p, y.ld, ncols, tm, dd);
-    } else if ((s.nx & 1) == 0 && (x.ld & 1) == 0 && (y.ld & 1) == 0 && n < (int64_t(1) << 32) &&
-               !std::getenv("BOSP_STENCIL_ROWS")) {
+    } else if ((s.nx & 1) == 0 && (x.ld & 1) == 0 && (y.ld & 1) == 0 && n < (int64_t(1) << 32)) {
         // row pairs: half the tiles
         const unsigned gx2 = row_blocks(n / 2, dot, ncols);
         const dim3 grid2(gx2, (ncols + CB - 1) / CB);

@@ -136,8 +136,7 @@ template <int K, class F>
 void launch_colred(const char* family, int64_t n, int ncols, const F& f, double bytes) {
     if (ncols <= 0) return;
     Runtime& rt = Runtime::get();
-    static const int64_t waves = std::getenv("BOSP_COLRED_WAVES") ? std::atoll(std::getenv("BOSP_COLRED_WAVES")) : 4;
-    const int64_t target = waves * rt.sm_count();  // 2..16 waves measured within 3% on config 2
+    const int64_t target = 4 * rt.sm_count();  // 4 waves: 2..16 measured within 3% on config 2
     // >= 1024 rows per chunk: narrow solves (1-8 live columns) still fill the machine
     int nchunks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n + 1023) / 1024,
                                                                             (target + ncols - 1) / ncols)));
@@ -473,124 +472,6 @@ struct CgDirF {  // p = r + beta p for still-active columns (cg.cpp:49)
     }
 };
 
-// ---- fused CG update (cooperative) ----------------------------------------------------------
-constexpr int kUpdMaxCols = 160;  // the reference's nb rule caps nb at 150
-constexpr int kUpdChunk = 8;      // columns reduced together
-
-__global__ void __launch_bounds__(kThreads) k_cg_update_fused(
-    int64_t n, int ncols, double* __restrict__ x, int64_t lx, double* __restrict__ r, int64_t lr,
-    double* __restrict__ p, int64_t lp, const double* __restrict__ ap, int64_t lap, CgScalars s,
-    const double* __restrict__ pap_parts, int nparts, double tol, int max_iter) {
-    __shared__ double s_alpha[kUpdMaxCols], s_beta[kUpdMaxCols], s_rr[kUpdMaxCols];
-    __shared__ int s_upd[kUpdMaxCols], s_act[kUpdMaxCols], s_new[kUpdMaxCols], s_it[kUpdMaxCols];
-    __shared__ double red[kThreads / 32][kUpdChunk];
-    const int nb = gridDim.x, b = blockIdx.x;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    constexpr int kWarps = kThreads / 32;
-    // phase 0: fold the p^T A p partials (one warp per column, lanes strided, fixed order) and
-    // snapshot the per-column state (block 0 rewrites it after the grid barrier)
-    for (int j = warp; j < ncols; j += kWarps) {
-        double t = 0.0;
-        for (int q = lane; q < nparts; q += 32) t += __ldcg(&pap_parts[static_cast<int64_t>(j) * nparts + q]);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-        if (lane == 0) {
-            const double pap = t;
-            const int act = s.active[j];
-            const int upd = act && pap > 0.0;
-            s_act[j] = act;
-            s_upd[j] = upd;
-            s_rr[j] = s.rr[j];
-            s_it[j] = s.iters[j];
-            s_alpha[j] = upd ? s.rr[j] / pap : 0.0;
-            if (b == 0 && act) s.pap[j] = pap;
-        }
-    }
-    __syncthreads();
-    const int64_t chunk = (n + nb - 1) / nb;
-    const int64_t r0 = b * chunk, r1 = min(n, r0 + chunk);
-    // phase 1: x += a p, r -= a ap, per-block partial r^T r
-    for (int c0 = 0; c0 < ncols; c0 += kUpdChunk) {
-        double acc[kUpdChunk];
-#pragma unroll
-        for (int jj = 0; jj < kUpdChunk; ++jj) acc[jj] = 0.0;
-        for (int64_t i = r0 + threadIdx.x; i < r1; i += kThreads) {
-#pragma unroll
-            for (int jj = 0; jj < kUpdChunk; ++jj) {
-                const int j = c0 + jj;
-                if (j < ncols && s_upd[j]) {
-                    const double a = s_alpha[j];
-                    const double xv = x[i + j * lx] + a * p[i + j * lp];
-                    const double rv = r[i + j * lr] - a * ap[i + j * lap];
-                    x[i + j * lx] = xv;
-                    r[i + j * lr] = rv;
-                    acc[jj] += rv * rv;
-                }
-            }
-        }
-#pragma unroll
-        for (int jj = 0; jj < kUpdChunk; ++jj)
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) acc[jj] += __shfl_xor_sync(0xffffffffu, acc[jj], o);
-        if (lane == 0)
-#pragma unroll
-            for (int jj = 0; jj < kUpdChunk; ++jj) red[warp][jj] = acc[jj];
-        __syncthreads();
-        if (threadIdx.x < kUpdChunk && c0 + threadIdx.x < ncols) {
-            double t = 0.0;
-            for (int w = 0; w < kThreads / 32; ++w) t += red[w][threadIdx.x];
-            s.parts[static_cast<int64_t>(c0 + threadIdx.x) * nb + b] = t;
-        }
-        __syncthreads();
-    }
-    __threadfence();
-    cooperative_groups::this_grid().sync();
-    // phase 2: every block folds the partials in the same order -> identical beta everywhere
-    for (int j = warp; j < ncols; j += kWarps) {
-        double rr = 0.0;
-        if (s_upd[j]) {
-            for (int q = lane; q < nb; q += 32) rr += __ldcg(&s.parts[static_cast<int64_t>(j) * nb + q]);
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) rr += __shfl_xor_sync(0xffffffffu, rr, o);
-        }
-        if (lane != 0) continue;
-        if (s_upd[j]) {
-            const double beta = rr / s_rr[j];
-            const int nit = s_it[j] + 1;
-            const int na = (sqrt(rr) > tol * s.bnorm[j] && nit < max_iter) ? 1 : 0;
-            s_beta[j] = beta;
-            s_new[j] = na;
-            if (b == 0) {
-                s.rr[j] = rr;
-                s.iters[j] = nit;
-                s.active[j] = na;
-                s.beta[j] = beta;
-            }
-        } else {
-            s_beta[j] = 0.0;
-            s_new[j] = 0;
-            if (b == 0 && s_act[j]) {  // p^T A p <= 0: breakdown keeps the iterate (cg.cpp:40-44)
-                s.broken[j] = 1;
-                s.active[j] = 0;
-            }
-        }
-    }
-    __syncthreads();
-    // p = r + beta p for the columns that continue
-    for (int64_t i = r0 + threadIdx.x; i < r1; i += kThreads)
-        for (int j = 0; j < ncols; ++j)
-            if (s_new[j]) p[i + j * lp] = r[i + j * lr] + s_beta[j] * p[i + j * lp];
-    if (b == 0 && threadIdx.x == 0) {
-        int c = 0;
-        for (int j = 0; j < ncols; ++j) c += s_new[j];
-        if (*s.any_active > 0) {
-            *s.loops += 1;
-            if (s.total) *s.total += 1;
-        }
-        *s.any_active = c;
-        if (s.has_cond) cudaGraphSetConditional(s.cond, c > 0 ? 1u : 0u);
-    }
-}
 
 __global__ void k_transpose(const double* __restrict__ a, int64_t lda, int64_t rows, int64_t cols,
                             double* __restrict__ t, int64_t ldt) {
@@ -608,37 +489,6 @@ __global__ void k_transpose(const double* __restrict__ a, int64_t lda, int64_t r
 }
 
 }  // namespace
-
-void cg_update_fused(const DMat& x, const DMat& r, const DMat& p, const DMat& ap, const CgScalars& s,
-                     const double* pap_parts, int nparts, double tol, int max_iter) {
-    const int ncols = static_cast<int>(x.cols);
-    if (ncols <= 0) return;
-    require(ncols <= kUpdMaxCols, "cg_update_fused: too many columns");
-    Runtime& rt = Runtime::get();
-    static int max_blocks = 0;
-    if (max_blocks == 0) {
-        int per_sm = 0;
-        BOSP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cg_update_fused, kThreads, 0));
-        max_blocks = std::max(1, per_sm) * rt.sm_count();
-    }
-    // two blocks per SM: enough to stream HBM, few enough that the redundant fold of the
-    // partials (ncols x blocks loads per block) stays cheap
-    const int nb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(
-        {static_cast<int64_t>(max_blocks), 2LL * rt.sm_count(), (x.rows + kThreads - 1) / kThreads})));
-    require(static_cast<int64_t>(nb) * ncols <= s.parts_cap, "cg_update_fused: partial buffer too small");
-    LaunchScope ls("cg_vec", 8.0 * x.rows * ncols * 8.0, 0.0);
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(nb);
-    cfg.blockDim = dim3(kThreads);
-    cfg.stream = rt.stream();
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;
-    attr[0].val.cooperative = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    BOSP_CUDA(cudaLaunchKernelEx(&cfg, k_cg_update_fused, x.rows, ncols, x.p, x.ld, r.p, r.ld, p.p, p.ld,
-                                 static_cast<const double*>(ap.p), ap.ld, s, pap_parts, nparts, tol, max_iter));
-}
 
 void transpose(const DMat& a, const DMat& t) {
     if (a.rows == 0 || a.cols == 0) return;
