@@ -62,6 +62,15 @@ class _Stats(C.Structure):
 _lib = None
 
 
+def use_library(path: str | None):
+    """Bind this module to another build of ref_shim.cpp -- tests/test_compat.py compiles the
+    same shim against the B200 library's reference-compatible headers and drives it through
+    these very wrappers.  None restores oracle/_ref."""
+    global _lib, LIB_PATH
+    LIB_PATH = path or os.path.join(_HERE, "_ref", "libbosp_ref.so")
+    _lib = None
+
+
 def available() -> bool:
     return os.path.exists(LIB_PATH)
 

@@ -11,7 +11,9 @@
 #include <memory>
 #include <optional>
 #include <random>
+#include <span>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "common.hpp"
@@ -61,8 +63,9 @@ public:
     double operator()(int64_t i, int64_t j) const { return data_[static_cast<size_t>(i + j * dim_)]; }
     double* data() { return data_.data(); }
     const double* data() const { return data_.data(); }
-    double* col(int64_t j) { return data_.data() + j * dim_; }
-    const double* col(int64_t j) const { return data_.data() + j * dim_; }
+    // Contiguous view of column j (block_vectors.hpp:23-24).
+    std::span<double> col(int64_t j) { return {data_.data() + j * dim_, static_cast<size_t>(dim_)}; }
+    std::span<const double> col(int64_t j) const { return {data_.data() + j * dim_, static_cast<size_t>(dim_)}; }
     BlockVectors columns(int64_t first, int64_t count) const;
     void assign_columns(int64_t first, const BlockVectors& src);
     void fill_zero();
@@ -74,14 +77,21 @@ private:
     std::vector<double, BigAlloc<double>> data_;
 };
 
-// CSR (sparse_csr.hpp:12-28); indices are int64 at the boundary, int32 on the device.
+// CSR (sparse_csr.hpp:12-28): the reference's size_t index vectors at the boundary, int32 on
+// the device.
 struct SparseMatrixCSR {
-    int64_t rows = 0, cols = 0;
-    std::vector<int64_t> row_offsets, col_indices;
+    std::size_t rows = 0, cols = 0;
+    std::vector<std::size_t> row_offsets, col_indices;
     std::vector<double> values;
-    int64_t nnz() const { return static_cast<int64_t>(values.size()); }
+    std::size_t nnz() const { return values.size(); }
     void check_invariants() const;
+    // y = A x for one column on the host (sparse_csr.hpp:24-25); the solver never calls it --
+    // its operators apply on the device.
+    void apply(std::span<const double> x, std::span<double> y) const;
 };
+// Unsorted triplets -> CSR, duplicates summed (sparse_csr.hpp:29-32).
+SparseMatrixCSR csr_from_triplets(std::size_t rows, std::size_t cols, std::vector<std::size_t> ti,
+                                  std::vector<std::size_t> tj, std::vector<double> tv);
 
 // Structured-grid Laplacian family applied matrix-free by the stencil kernel (new: the
 // reference reaches matrix-free operators only through from_callback).
@@ -161,6 +171,11 @@ public:
     explicit InnerProduct(LinearOperator weight) : weight_(std::make_shared<LinearOperator>(std::move(weight))) {}
     bool weighted() const { return weight_ != nullptr; }
     const LinearOperator* weight() const { return weight_.get(); }
+    // inner_product.hpp:20-27: B y (a copy when unweighted), x^T B y, sqrt(x^T B x) on host
+    // spans (each weighted call is one device apply).
+    BlockVectors apply_weight(const BlockVectors& y) const;
+    double dot(std::span<const double> x, std::span<const double> y) const;
+    double norm(std::span<const double> x) const;
 
 private:
     std::shared_ptr<const LinearOperator> weight_;
@@ -222,7 +237,11 @@ struct EigenResult {  // bosp_solver.hpp:71-81
     SolverStats stats;
 };
 
-struct DeviceState;  // HBM-resident SolverState (bosp_solver.hpp:53-69)
+struct DeviceState;  // HBM-resident blocks of the solve
+// SolverState (bosp_solver.hpp:53-69).  The n-length blocks x, y, p, q, w, z and the locked
+// bases live in HBM (dev()); the reference's host-side fields are public mirrors refreshed by
+// initialize / iterate_once, so code that reads st.iter, st.nev_conv, st.lambdas, ... compiles
+// and behaves as against the reference.
 class SolverState {
 public:
     SolverState();
@@ -231,8 +250,19 @@ public:
     SolverState& operator=(SolverState&&) noexcept;
     DeviceState& dev() { return *d_; }
     const DeviceState& dev() const { return *d_; }
-    int64_t iter() const;
-    int64_t nev_conv() const;
+
+    std::vector<double> lambdas;    // one per column of x
+    std::vector<double> residuals;  // last normalized residual per column of x
+    int64_t frozen = 0;
+    int64_t nev_conv = 0;           // global converged prefix, never decreases
+    std::vector<double> locked_lambdas;
+    std::vector<std::vector<double>> residual_history;  // [iteration][eigenindex]
+    std::vector<double> last_residual;                  // per global index
+    std::vector<int64_t> nevconv_history;
+    int64_t iter = 0;
+    bool leak_recovered = false;
+    SolverStats stats;
+    int64_t locked_count() const { return static_cast<int64_t>(locked_lambdas.size()); }
 
 private:
     std::unique_ptr<DeviceState> d_;
@@ -270,8 +300,9 @@ GeneralizedNullspace compute_nullspace(const LinearOperator& k, const LinearOper
                                        uint64_t seed = 777);
 
 // ---- kernel-level API on host blocks (each call runs on the device) -----------------------
-struct BiorthBasis {
+struct BiorthBasis {  // biorth.hpp:12-16
     BlockVectors p, q;
+    InnerProduct ip;
 };
 struct BiorthOutcome {
     BiorthBasis basis;
@@ -295,6 +326,33 @@ struct CgResult {
 };
 CgResult cg_solve(const LinearOperator& op, const BlockVectors& rhs, const BlockVectors& x0,
                   double tol, int64_t max_iter);
+
+// ---- the rest of the reference's public helpers (host side) -------------------------------
+// kernels.hpp:13-21: unit-stride vector helpers and the host kernel thread count (here: the
+// OpenMP threads of the host small dense algebra; the block kernels run on the GPU).
+double vdot(std::span<const double> x, std::span<const double> y);
+double vnorm2(std::span<const double> x);
+void vaxpy(double alpha, std::span<const double> x, std::span<double> y);
+void vscale(double alpha, std::span<double> x);
+void set_kernel_threads(int nthreads);
+int kernel_threads();
+// projected_lrep.hpp:27-36: K^ = U^T (K U), M^ = V^T (M V) (Grams on the device) + finish_assembly.
+ProjectedLrep assemble_projected(const LinearOperator& k, const LinearOperator& m, const BlockVectors& u,
+                                 const BlockVectors& v, const InnerProduct& ip);
+ProjectedLrep assemble_projected_applied(const BlockVectors& u, const BlockVectors& ku,
+                                         const BlockVectors& v, const BlockVectors& mv);
+// nullspace.hpp:21-23: power-iteration estimate of ||op||_2 (applies on the device).
+double estimate_operator_norm(const LinearOperator& op, int64_t iters = 50, uint64_t seed = 12345);
+// dense_kernels.hpp:24-40 (host small dense algebra).
+double condition_number_2(const DenseMatrix& a);
+struct LuFactors {
+    DenseMatrix lu;
+    std::vector<std::size_t> perm;
+};
+LuFactors lu_factor(DenseMatrix a);
+std::vector<double> lu_solve(const LuFactors& f, std::vector<double> b);
+DenseMatrix lu_solve(const LuFactors& f, const DenseMatrix& b);
+DenseMatrix transpose_times(const DenseMatrix& l, const DenseMatrix& r);
 
 }  // namespace b200
 }  // namespace bosp

@@ -206,7 +206,7 @@ bosp_status bosp_op_dense(int64_t n, const double* a, bosp_op* out) {
 bosp_status bosp_op_csr(int64_t n, const int64_t* rp, const int64_t* ci, const double* vv, bosp_op* out) {
     return guarded([&] {
         bosp::SparseMatrixCSR a;
-        a.rows = a.cols = n;
+        a.rows = a.cols = static_cast<size_t>(n);
         a.row_offsets.assign(rp, rp + n + 1);
         a.col_indices.assign(ci, ci + rp[n]);
         a.values.assign(vv, vv + rp[n]);
@@ -328,9 +328,9 @@ bosp_status bosp_read_matrix_market(const char* path, int64_t* rows, int64_t* co
             last = bosp::read_matrix_market(path);
             last_path = path;
         }
-        *rows = last.rows;
-        *cols = last.cols;
-        *nnz = last.nnz();
+        *rows = static_cast<int64_t>(last.rows);
+        *cols = static_cast<int64_t>(last.cols);
+        *nnz = static_cast<int64_t>(last.nnz());
         if (rowptr) std::memcpy(rowptr, last.row_offsets.data(), sizeof(int64_t) * last.row_offsets.size());
         if (colidx) std::memcpy(colidx, last.col_indices.data(), sizeof(int64_t) * last.col_indices.size());
         if (vals) std::memcpy(vals, last.values.data(), sizeof(double) * last.values.size());

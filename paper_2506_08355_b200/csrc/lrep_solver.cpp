@@ -90,8 +90,27 @@ SolverState::SolverState() : d_(std::make_unique<DeviceState>()) {}
 SolverState::~SolverState() = default;
 SolverState::SolverState(SolverState&&) noexcept = default;
 SolverState& SolverState::operator=(SolverState&&) noexcept = default;
-int64_t SolverState::iter() const { return d_->iter; }
-int64_t SolverState::nev_conv() const { return d_->nev_conv; }
+
+namespace {
+// Refresh the reference-visible host fields of SolverState from the device-side state
+// (histories grow by the rows added since the last refresh).
+void mirror_state(SolverState& ss) {
+    const DeviceState& st = ss.dev();
+    ss.lambdas = st.lambdas;
+    ss.residuals = st.residuals;
+    ss.frozen = st.frozen;
+    ss.nev_conv = st.nev_conv;
+    ss.locked_lambdas = st.locked_lambdas;
+    for (size_t i = ss.residual_history.size(); i < st.residual_history.size(); ++i)
+        ss.residual_history.push_back(st.residual_history[i]);
+    for (size_t i = ss.nevconv_history.size(); i < st.nevconv_history.size(); ++i)
+        ss.nevconv_history.push_back(st.nevconv_history[i]);
+    ss.last_residual = st.last_residual;
+    ss.iter = st.iter;
+    ss.leak_recovered = st.leak_recovered;
+    ss.stats = st.stats;
+}
+}  // namespace
 
 int64_t BospConfig::effective_nb() const {
     if (nb > 0) return std::min(nb, nev);
@@ -304,12 +323,13 @@ SolverState initialize(const LinearOperator& k, const LinearOperator& m, const I
     st.lambdas.assign(static_cast<size_t>(wx), std::numeric_limits<double>::infinity());
     st.residuals.assign(static_cast<size_t>(wx), 1.0);
     st.last_residual.assign(static_cast<size_t>(cfg.nev), 1.0);
+    mirror_state(ss);
     return ss;
 }
 
-bool iterate_once(SolverState& ss, const LinearOperator& k, const LinearOperator& m,
-                  const InnerProduct& ip, const GeneralizedNullspace& ns, const BospConfig& cfg) {
-    DeviceState& st = ss.dev();
+namespace {
+bool iterate_device(DeviceState& st, const LinearOperator& k, const LinearOperator& m,
+                    const InnerProduct& ip, const GeneralizedNullspace& ns, const BospConfig& cfg) {
     const int64_t n = st.n;
     const int64_t nb = cfg.effective_nb();
     const bool moving = cfg.effective_moving();
@@ -539,6 +559,14 @@ bool iterate_once(SolverState& ss, const LinearOperator& k, const LinearOperator
     }
     return false;
 }
+}  // namespace
+
+bool iterate_once(SolverState& ss, const LinearOperator& k, const LinearOperator& m,
+                  const InnerProduct& ip, const GeneralizedNullspace& ns, const BospConfig& cfg) {
+    const bool done = iterate_device(ss.dev(), k, m, ip, ns, cfg);
+    mirror_state(ss);
+    return done;
+}
 
 namespace {
 
@@ -646,7 +674,7 @@ EigenResult solve(const LinearOperator& k, const LinearOperator& m, const InnerP
     if (phases_enabled()) rt.sync();
     st.dev().phases.acc[PH_INIT] += secs(ti, Clock::now());
     bool converged = false;
-    while (st.iter() < cfg.max_outer_iter) {
+    while (st.iter < cfg.max_outer_iter) {
         if (iterate_once(st, k, m, ip, nullspace, cfg)) {
             converged = true;
             break;
@@ -660,7 +688,7 @@ EigenResult solve(const LinearOperator& k, const LinearOperator& m, const InnerP
                      (long long)rt.sync_count_, rt.sync_wait_s_, (long long)rt.graph_builds_, rt.graph_build_s_);
     if (phases_mode() != 0) {
         std::fprintf(stderr, "[bosp] phase %s times (s), %lld iterations:\n", phases_enabled() ? "wall" : "host",
-                     (long long)st.iter());
+                     (long long)st.iter);
         for (int i = 0; i < PH_COUNT; ++i)
             std::fprintf(stderr, "[bosp]   %-28s %9.4f\n", kPhaseNames[i], st.dev().phases.acc[i]);
     }

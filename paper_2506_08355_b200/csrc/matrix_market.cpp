@@ -160,8 +160,8 @@ SparseMatrixCSR read_matrix_market(const std::string& path) {
         }
     }
     SparseMatrixCSR m;
-    m.rows = static_cast<int64_t>(rows);
-    m.cols = static_cast<int64_t>(cols);
+    m.rows = static_cast<size_t>(rows);
+    m.cols = static_cast<size_t>(cols);
     m.row_offsets.assign(static_cast<size_t>(rows) + 1, 0);
     m.col_indices.reserve(nt);
     m.values.reserve(nt);
@@ -170,9 +170,9 @@ SparseMatrixCSR read_matrix_market(const std::string& path) {
         const int64_t r = ti[order[k]], c = tj[order[k]];
         double v = 0.0;
         while (k < nt && ti[order[k]] == r && tj[order[k]] == c) v += tv[order[k++]];
-        m.col_indices.push_back(c);
+        m.col_indices.push_back(static_cast<size_t>(c));
         m.values.push_back(v);
-        m.row_offsets[static_cast<size_t>(r) + 1] = static_cast<int64_t>(m.values.size());
+        m.row_offsets[static_cast<size_t>(r) + 1] = m.values.size();
     }
     for (size_t r = 1; r <= rows; ++r) m.row_offsets[r] = std::max(m.row_offsets[r], m.row_offsets[r - 1]);
     m.check_invariants();

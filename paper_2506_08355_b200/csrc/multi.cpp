@@ -89,8 +89,8 @@ EigenResult solve_multi(int nranks, int ngpus, const GlobalOp& k, const GlobalOp
                     nl->x0 = BlockVectors(s.n, ns->r);
                     nl->y0 = BlockVectors(s.n, ns->r);
                     for (int64_t c = 0; c < ns->r; ++c) {
-                        std::memcpy(nl->x0.col(c), ns->x0.col(c) + s.row0, sizeof(double) * s.n);
-                        std::memcpy(nl->y0.col(c), ns->y0.col(c) + s.row0, sizeof(double) * s.n);
+                        std::memcpy(nl->x0.col(c).data(), ns->x0.col(c).data() + s.row0, sizeof(double) * s.n);
+                        std::memcpy(nl->y0.col(c).data(), ns->y0.col(c).data() + s.row0, sizeof(double) * s.n);
                     }
                 }
                 res[r] = solve(kl, ml, InnerProduct{}, cfg, std::move(nl));
@@ -111,8 +111,8 @@ EigenResult solve_multi(int nranks, int ngpus, const GlobalOp& k, const GlobalOp
     out.y = BlockVectors(n, h);
     for (int r = 0; r < nranks; ++r)
         for (int64_t c = 0; c < h; ++c) {
-            std::memcpy(out.x.col(c) + slices[r].row0, res[r].x.col(c), sizeof(double) * slices[r].n);
-            std::memcpy(out.y.col(c) + slices[r].row0, res[r].y.col(c), sizeof(double) * slices[r].n);
+            std::memcpy(out.x.col(c).data() + slices[r].row0, res[r].x.col(c).data(), sizeof(double) * slices[r].n);
+            std::memcpy(out.y.col(c).data() + slices[r].row0, res[r].y.col(c).data(), sizeof(double) * slices[r].n);
         }
     for (int r = 1; r < nranks; ++r) {
         out.stats.wall_seconds = std::max(out.stats.wall_seconds, res[r].stats.wall_seconds);

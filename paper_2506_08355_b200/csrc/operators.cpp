@@ -83,15 +83,15 @@ BlockVectors BlockVectors::hcat(const std::vector<const BlockVectors*>& parts) {
 }
 
 void SparseMatrixCSR::check_invariants() const {
-    require(static_cast<int64_t>(row_offsets.size()) == rows + 1, "csr: row_offsets length must be rows+1");
+    require(row_offsets.size() == rows + 1, "csr: row_offsets length must be rows+1");
     require(row_offsets.front() == 0 && row_offsets.back() == nnz(), "csr: row_offsets endpoints invalid");
     require(col_indices.size() == values.size(), "csr: col_indices/values length mismatch");
-    for (int64_t r = 0; r < rows; ++r) {
+    for (size_t r = 0; r < rows; ++r) {
         require(row_offsets[r] <= row_offsets[r + 1], "csr: row_offsets must be nondecreasing");
-        for (int64_t k = row_offsets[r]; k + 1 < row_offsets[r + 1]; ++k)
+        for (size_t k = row_offsets[r]; k + 1 < row_offsets[r + 1]; ++k)
             require(col_indices[k] < col_indices[k + 1], "csr: column indices not strictly increasing");
-        for (int64_t k = row_offsets[r]; k < row_offsets[r + 1]; ++k)
-            require(col_indices[k] >= 0 && col_indices[k] < cols, "csr: column index out of range");
+        for (size_t k = row_offsets[r]; k < row_offsets[r + 1]; ++k)
+            require(col_indices[k] < cols, "csr: column index out of range");
     }
 }
 
@@ -652,7 +652,12 @@ LinearOperator LinearOperator::from_dense(const double* a, int64_t n) {
 LinearOperator LinearOperator::from_csr(const SparseMatrixCSR& a) {
     a.check_invariants();
     require(a.rows == a.cols, "LinearOperator: csr operator must be square");
-    return LinearOperator(std::make_shared<CsrOp>(a.rows, a.row_offsets.data(), a.col_indices.data(), a.values.data()));
+    // size_t and int64_t share width and representation for every valid index (< 2^63)
+    static_assert(sizeof(std::size_t) == sizeof(int64_t), "64-bit size_t expected");
+    return LinearOperator(std::make_shared<CsrOp>(static_cast<int64_t>(a.rows),
+                                                  reinterpret_cast<const int64_t*>(a.row_offsets.data()),
+                                                  reinterpret_cast<const int64_t*>(a.col_indices.data()),
+                                                  a.values.data()));
 }
 LinearOperator LinearOperator::from_csr(int64_t n, const int64_t* rp, const int64_t* ci, const double* vv) {
     return LinearOperator(std::make_shared<CsrOp>(n, rp, ci, vv));
