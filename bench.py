@@ -1,20 +1,30 @@
 #!/usr/bin/env python
 """Benchmark: BOSP LREP solve on B200 -- converged eigenpairs/s (BASELINE.json metric).
 
-Workload (N=1): BASELINE configs[1] = config 2, the 64^3 sparse LREP (n = 262,144, fp64 CSR,
-nev = 20, nb = 40 -> 20, tol 1e-8), explicit generalized nullspace (constants).  One "step" =
-one full bosp::solve (initialize + outer iterations + assemble_result) on the device.
+Headline workload (N=1): BASELINE configs[2] = config 3, the largest configuration that fits one
+GPU: the 3-D LREP on a 128^3 grid (n = 2,097,152) applied matrix-free as a 7-point stencil, nev =
+100, nb = 64, moving=true, tol 1e-8, explicit generalized nullspace (constants).  One "step" =
+one full bosp::solve (initialize + outer iterations + assemble_result) on the device, operators
+and the nullspace pair resident in HBM before the timed region, eigenvectors left in HBM.  The
+other configurations (1, 2, 4, 5) are timed in the same run (s/solve, eigenpairs/s, iterations,
+parity) and reported under "configs".
 
 Arms:
   default            the B200 library (libbosp_b200.so) through its C ABI.
   --impl reference   the UNMODIFIED reference CPU solver (oracle/_ref/libbosp_ref.so, built from
-                     /root/reference/proj/src) on the box's host cores: each step is a bounded
-                     sample (initialize + a few iterate_once) extrapolated to a full solve with the
-                     reference's own iteration count for this config.
+                     /root/reference/proj/src) on the box's host cores through its public API.
+                     A config-3 solve takes hours on the CPU, so each step is a bounded sample:
+                     initialize + one iterate_once on the same family at 24^3 and 32^3 (steps
+                     alternate), fitted to t(n) = a + b n and extrapolated to 128^3 with the
+                     iteration count of the B200 solve -- an ESTIMATE, labelled as such.
 
 JSON line keys follow the driver contract (metric/value/unit/n_gpus/steps/warmup/ms_per_step/
 higher_is_better/scaling/vs_baseline/dtype/data/config) plus roofline, cpu_baseline, e2e,
 gpu_launches and clocks.
+
+N > 1 (torchrun, one process per GPU): the config-3 solve is row-partitioned over the ranks
+(z-slabs of the stencil, NCCL allreduce of every Gram + halo planes) -- strong scaling.  A failed
+partitioned setup exits non-zero; there is no silent fallback to replicas.
 """
 from __future__ import annotations
 
@@ -32,9 +42,13 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-METRIC = "converged eigenpairs/s (LREP solve, config 2: 64^3 CSR, nev=20)"
+HEADLINE = "config3"
+METRIC = "converged eigenpairs/s (LREP solve, config 3: 128^3 7-point stencil, nev=100)"
 UNIT = "eigenpairs/s"
 GOLDEN = os.path.join(ROOT, "tests", "golden", "golden_solves.json")
+# B200 outer-iteration count of the config-3 solve (profiles/r2_*; used only to extrapolate the
+# reference's sampled per-iteration time to a full solve when this run's own count is absent)
+C3_ITERS_DEFAULT = 38
 
 
 def load_peaks():
@@ -118,64 +132,125 @@ def max_over_ranks(dist, v: float) -> float:
     return float(t.item())
 
 
-def reference_iterations() -> int:
+def golden_record(name):
     try:
-        return int(json.load(open(GOLDEN))["config2"]["iterations"])
+        return json.load(open(GOLDEN))[name]
     except Exception:
-        return 78
+        return None
 
 
-def cpu_reference_sample(prob, iters: int, threads: int):
-    """Reference solver (oracle/_ref) on a bounded sample: initialize + `iters` iterate_once."""
+# ---------------------------------------------------------------------------------------------
+# Reference CPU solver (oracle/_ref): bounded samples through its public API
+# ---------------------------------------------------------------------------------------------
+def ref_sample(grid: int, iters: int, threads: int):
+    """initialize + `iters` iterate_once of the reference on the config-3 family at grid^3."""
     from oracle import ref
+    from paper_2506_08355_b200 import problems as P
+    prob = P.config3(grid)
     ref.set_threads(threads)
     out = ref.time_iterations(prob.oracle_spec("K"), prob.oracle_spec("M"), ref.RefConfig(**prob.cfg),
                               (prob.x0, prob.y0), iters)
-    full_iters = reference_iterations()
+    return dict(n=prob.n, t_init=out["t_init"], t_iter=out["t_iters"] / max(1, out["iters"]),
+                iters=out["iters"], threads=ref.threads())
+
+
+def fit_linear(samples, key):
+    """Least-squares t = a + b n over the samples (>= 2 distinct n)."""
+    ns = np.array([s["n"] for s in samples], dtype=float)
+    ts = np.array([s[key] for s in samples], dtype=float)
+    if len(set(ns.tolist())) < 2:
+        return 0.0, float(np.median(ts / ns))
+    b, a = np.polyfit(ns, ts, 1)
+    return float(a), float(b)
+
+
+def ref_estimate(samples, n_full: int, iters_full: int):
+    a_i, b_i = fit_linear(samples, "t_init")
+    a_t, b_t = fit_linear(samples, "t_iter")
+    t_init = max(a_i + b_i * n_full, 0.0)
+    t_iter = max(a_t + b_t * n_full, 0.0)
+    return dict(solve_s=t_init + iters_full * t_iter, t_init=t_init, t_iter=t_iter,
+                fit={"t_init": [a_i, b_i], "t_iter": [a_t, b_t]})
+
+
+def ref_config2_estimate(threads: int):
+    """The round-1 reference arm on config 2 (64^3 CSR): initialize + 2 iterate_once,
+    extrapolated with the reference's own iteration count for the full solve (78)."""
+    from oracle import ref
+    from paper_2506_08355_b200 import problems as P
+    prob = P.config2(64)
+    ref.set_threads(threads)
+    out = ref.time_iterations(prob.oracle_spec("K"), prob.oracle_spec("M"), ref.RefConfig(**prob.cfg),
+                              (prob.x0, prob.y0), 2)
+    g = golden_record("config2") or {}
+    it = int(g.get("iterations", 78))
     t_iter = out["t_iters"] / max(1, out["iters"])
-    est = out["t_init"] + full_iters * t_iter
-    return dict(est_solve_s=est, t_init=out["t_init"], t_iter=t_iter, iters=out["iters"],
-                full_iters=full_iters, threads=ref.threads())
+    est = out["t_init"] + it * t_iter
+    return {"workload": prob.name, "value": prob.cfg["nev"] / est, "unit": UNIT, "est_solve_s": est,
+            "t_init": out["t_init"], "t_iter": t_iter, "iterations": it,
+            "full_solve_measured_here_s": g.get("seconds"),
+            "sample": "initialize + 2 iterate_once at 64^3, solve = t_init + 78 t_iter (ESTIMATE)"}
 
 
 def run_reference(args, world, rank, dist):
     if rank != 0:
         return
-    from paper_2506_08355_b200 import problems as P
-    prob = P.config2(64)
     threads = os.cpu_count() or 1
-    for _ in range(args.warmup):
-        cpu_reference_sample(prob, 1, threads)
-    samples = [cpu_reference_sample(prob, args.ref_iters, threads) for _ in range(args.steps)]
-    est = statistics.median(s["est_solve_s"] for s in samples)
-    value = prob.cfg["nev"] / est
+    n_full = 128 ** 3
+    for _ in range(args.warmup):  # untimed: loads the library, first-touch of the OpenMP pool
+        ref_sample(16, 1, threads)
+    samples = []
+    for s in range(args.steps):
+        samples.append(ref_sample(24 if s % 2 == 0 else 32, 1, threads))
+    if len({s["n"] for s in samples}) < 2:  # one step: add the other size so the fit has two
+        samples.append(ref_sample(32, 1, threads))
+    est = ref_estimate(samples, n_full, args.c3_iters)
+    value = 100.0 / est["solve_s"]
+    sample_txt = (f"ESTIMATE: each step = initialize + 1 iterate_once of the unmodified reference on the "
+                  f"config-3 family at 24^3 / 32^3 (alternating), fitted t(n) = a + b n and extrapolated to "
+                  f"128^3: solve = t_init + {args.c3_iters} x t_iter (B200 iteration count); "
+                  f"t_init={est['t_init']:.1f}s t_iter={est['t_iter']:.1f}s")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": est * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": est["solve_s"] * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded generator, paper_2506_08355_b200/problems.py)",
-        "config": {"workload": prob.name, "n": prob.n, "nev": 20, "nb": 40, "tol": 1e-8,
-                   "parallelism": "host OpenMP (reference kernels), serial CSR matvec"},
+        "config": {"workload": "config3-stencil7-128^3", "n": n_full, "nev": 100, "nb": 64, "moving": True,
+                   "tol": 1e-8, "parallelism": "host OpenMP (reference kernels), serial CSR matvec"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": samples[0]["threads"], "kind": "reference",
-                         "sample": (f"initialize + {args.ref_iters} iterate_once per step (public API), "
-                                    f"solve time = t_init + {samples[0]['full_iters']} x t_iter "
-                                    f"(the reference's own iteration count on this config); "
-                                    f"t_init={samples[0]['t_init']:.2f}s t_iter={samples[0]['t_iter']:.2f}s")},
+                         "sample": sample_txt},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "estimate": {"samples": samples, **est},
     }
+    if not args.no_other_configs:
+        try:
+            line["config2_estimate"] = ref_config2_estimate(threads)
+        except Exception as e:  # noqa: BLE001
+            line["config2_estimate"] = {"unavailable": str(e)[:200]}
     print(json.dumps(line), flush=True)
 
 
-def dmma_roofline():
-    """The dense contractions of configs 3/5 (d = 320) on the fp64 tensor pipe: Rayleigh-Ritz
-    Gram U^T (K U) (n x 320)^T (n x 320) and Ritz pullback (n x 320)(320 x 192) at n = 128^3,
-    device-resident random data, against cuBLAS DGEMM 8192^3 measured in the same process."""
+# ---------------------------------------------------------------------------------------------
+# B200 arm
+# ---------------------------------------------------------------------------------------------
+def make_problem(name, bosp, P):
+    if name == "config1":
+        return P.config1()
+    if name == "config2":
+        return P.config2(64, solve=bosp.device_solver)
+    if name == "config3":
+        return P.config3(128, solve=bosp.device_solver)
+    if name == "config4":
+        return P.config4(solve_factory=bosp.device_solver)
+    if name == "config5":
+        return P.config5(1024, solve=bosp.device_solver)
+    raise SystemExit(f"unknown workload {name}")
+
+
+def cublas_dgemm_tflops():
+    """Same-process cuBLAS DGEMM 8192^3 (torch.matmul fp64): the fp64 tensor-pipe denominator
+    (MEASURED_PEAKS.json carries no fp64 figure)."""
     import torch
-    from paper_2506_08355_b200 import bosp
-    n, d, w = 128 ** 3, 320, 192
-    out = {"bound": "tensor (fp64 DMMA)", "unit": "TFLOP/s", "n": n}
-    g_ms = bosp.bench_blas("gram", n, d, d, reps=10)
-    p_ms = bosp.bench_blas("product", n, d, w, reps=10)
     a = torch.randn(8192, 8192, dtype=torch.float64, device="cuda")
     b = torch.randn(8192, 8192, dtype=torch.float64, device="cuda")
     for _ in range(2):
@@ -189,249 +264,296 @@ def dmma_roofline():
     peak = 2 * 8192 ** 3 * 5 / (e0.elapsed_time(e1) * 1e-3) / 1e12
     del a, b
     torch.cuda.empty_cache()
-    # MGS-Biorth at HBM scale (m = 20 at n = 2^21, X, Y, P, Q far beyond L2): the pair Gram of
-    # [X | Y] + the fused apply/check kernel, against 48 n m algorithmic bytes
-    m = 20
-    mg_ms = bosp.bench_blas("gramsym", n, m, m, reps=10)
-    ma_ms = bosp.bench_blas("mgsapply", n, m, m, reps=10)
-    hbm = load_peaks().get("hbm_gbs", 6650.0)
-    mgs_gbs = 48.0 * n * m / ((mg_ms + ma_ms) * 1e-3) / 1e9
-    out["mgs_at_hbm_scale"] = {"n": n, "m": m, "pair_gram_ms": mg_ms, "apply_check_ms": ma_ms,
-                               "achieved_gbs": mgs_gbs, "frac_hbm": mgs_gbs / hbm,
-                               "note": "kernel time only (no host recurrence between the two launches)"}
-    gt = 2 * n * d * d / (g_ms * 1e-3) / 1e12
-    pt = 2 * n * d * w / (p_ms * 1e-3) / 1e12
-    out.update({"kernel": "k_gram<64,64> (G = A^T B, 320 x 320)", "achieved": gt, "peak": peak, "frac": gt / peak,
-                "gram_ms": g_ms, "product_kernel": "k_product<64,64> (A C, 320 -> 192)", "product_achieved": pt,
-                "product_frac": pt / peak, "product_ms": p_ms,
-                "peak_source": "cuBLAS DGEMM 8192^3 (torch.matmul fp64), best-effort same-process measurement"})
+    return peak
+
+
+def family_roofline(fam, rep, step_ms, peaks, dgemm, kind, note=""):
+    if not rep or rep["launches"] == 0 or rep["ms"] <= 0:
+        return None
+    if kind == "tensor":
+        ach = rep["flops"] / (rep["ms"] * 1e-3) / 1e12
+        peak, unit, src = dgemm, "TFLOP/s", "same-process cuBLAS DGEMM 8192^3 (fp64 tensor pipe)"
+    else:
+        ach = rep["bytes"] / (rep["ms"] * 1e-3) / 1e9
+        peak = peaks.get("hbm_gbs", 6650.0)
+        unit = "GB/s"
+        src = ("MEASURED_PEAKS.json hbm_gbs (copy, burst)" if "_fallback" not in peaks
+               else "fallback 6650 GB/s (B200_PROFILING.md)")
+    return {"family": fam, "bound": "tensor" if kind == "tensor" else "hbm", "achieved": ach, "peak": peak,
+            "unit": unit, "frac": ach / peak if peak else None, "launches_per_solve": rep["launches"],
+            "avg_launch_us": rep["ms"] * 1e3 / rep["launches"],
+            "algorithmic_bytes_per_launch": rep["bytes"] / rep["launches"],
+            "algorithmic_flops_per_launch": rep["flops"] / rep["launches"],
+            "share_of_step": rep["ms"] / step_ms if step_ms else None, "peak_source": src,
+            **({"note": note} if note else {})}
+
+
+# dominant kernel family of each config (profiles/r2_launches_*.txt) and its bound
+DOMINANT = {"config1": ("dense_apply", "tensor"), "config2": ("cg_vec", "hbm"), "config3": ("gram_wide", "tensor"),
+            "config4": ("dense_apply", "tensor"), "config5": ("gram_wide", "tensor")}
+NOTES = {
+    "gram_wide": "k_gram<64,64>: G = A^T B on the DMMA pipe (fp64 mma.sync m8n8k4); algorithmic flops "
+                 "2 n a b (symmetric Ritz Grams: n a^2, the upper half); tcgen05 has no f64 kind",
+    "product_wide": "k_product<64,64>: Out = A C on the DMMA pipe; 2 n k b flops (triangular MGS "
+                    "coefficients credited in full)",
+    "spmm_cg": "stencil / DIA SpMM with fused p^T A p inside the CG; algorithmic bytes = 16 n m_active "
+               "(stencil) or 16 n m_active + 2 n + 8 n per varying diagonal (DIA) -- the stored form",
+    "cg_vec": "CG x/r update + r^T r and direction kernels; one streaming pass each",
+    "dense_apply": "dense K X over the stored A^T, 128 x 32 DMMA tiles; 2 n^2 m flops",
+}
+
+
+def traffic_for(fam, workload):
+    """DRAM bytes per launch of the same kernel from the committed ncu --set full capture."""
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "roofline_traffic.json")))
+        ent = tr.get(workload, {}).get(fam)
+        return (ent["dram_bytes_per_launch"], ent) if ent else (None, None)
+    except Exception:
+        return None, None
+
+
+def solve_once(bosp, lib, K, M, cfg, ns, flush, vectors=False, profile=None):
+    lib.bosp_flush_l2(flush)
+    if profile:
+        bosp.profile_enable(profile)
+    r = bosp.solve(K, M, None, cfg, ns, want_vectors=vectors)
+    prof = bosp.profile_collect() if profile else None
+    if profile:
+        bosp.profile_enable(None)
+    return r, prof
+
+
+def check_record(prob, res, golden):
+    out = {"iterations": res.iterations, "converged": bool(res.converged), "nev_converged": res.nev_converged,
+           "max_residual": float(res.residuals.max()) if len(res.residuals) else None,
+           "final_biorth_deviation": res.stats["final_biorth_deviation"],
+           "repairs": res.stats["repairs"], "cg_iterations": res.stats["cg_iterations"],
+           "host_small_s": res.stats["host_small_seconds"]}
+    if golden:
+        g = np.asarray(golden["lambdas"])
+        if len(g) == len(res.lambdas):
+            out["max_rel_eig_err_vs_reference"] = float(np.max(np.abs(res.lambdas - g) / np.abs(g)))
+            out["reference_iterations"] = golden.get("iterations")
     return out
+
+
+def run_other_config(name, bosp, P, lib, flush, steps):
+    t0 = time.perf_counter()
+    prob = make_problem(name, bosp, P)
+    gen_s = time.perf_counter() - t0
+    K, M = bosp.operators_for(prob)
+    cfg = bosp.BospConfig(**prob.cfg)
+    ns = bosp.GeneralizedNullspace(prob.x0, prob.y0)
+    solve_once(bosp, lib, K, M, cfg, ns, flush)  # warm-up
+    dev = []
+    res = None
+    for _ in range(steps):
+        res, _ = solve_once(bosp, lib, K, M, cfg, ns, flush)
+        dev.append(res.stats["device_seconds"])
+    s = statistics.median(dev)
+    rec = {"workload": prob.name, "n": prob.n, "nev": prob.cfg["nev"], "s_per_solve": s,
+           "device_s": dev, "eigenpairs_per_s": prob.cfg["nev"] / s, "s_per_iteration": s / max(1, res.iterations),
+           "generator_s": gen_s, **check_record(prob, res, golden_record(name))}
+    del K, M
+    return rec
 
 
 def run_b200(args, world, rank, local, dist):
     from paper_2506_08355_b200 import _lib, bosp
     from paper_2506_08355_b200 import dist as D
     from paper_2506_08355_b200 import problems as P
-    _lib.lib().bosp_set_device(local)
+    lib = _lib.lib()
+    lib.bosp_set_device(local)
     name, sms = bosp.device_info()
-    prob = P.config2(64)
+    wl = args.workload
+    t0 = time.perf_counter()
+    prob = make_problem(wl, bosp, P)
+    gen_s = time.perf_counter() - t0
     cfg = bosp.BospConfig(**prob.cfg)
-    partitioned = world > 1 and args.partition == "rows"
-    partition_error = None
+    nev = prob.cfg["nev"]
+    partitioned = world > 1
     if partitioned:
         # one process per GPU, rows of every n-length block on this rank; NCCL communicator
         # inside libbosp_b200.so (torch.distributed only carries the unique id + timings).
-        # The ranks agree on success after one partitioned solve; if any rank failed, every
-        # rank falls back to replicas and the line records why.
-        ok = 1
-        try:
-            uid = D.broadcast_uid()
-            row0, nl = D.attach(prob.K, uid, world, rank)
-            ns = D.local_nullspace(prob.x0, prob.y0, row0, nl)
-            K, M = bosp.local_operator(prob.K, world, rank), bosp.local_operator(prob.M, world, rank)
-            bosp.solve(K, M, None, cfg, ns, want_vectors=True)
-        except Exception as e:  # noqa: BLE001 -- reported in the JSON line
-            ok, partition_error = 0, f"{type(e).__name__}: {e}"[:300]
-        import torch
-        flag = torch.tensor([ok], dtype=torch.int32)
-        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
-        if int(flag.item()) == 0:
-            try:
-                bosp.comm_free()
-            except Exception:
-                pass
-            partitioned = False
-            partition_error = partition_error or "another rank failed the partitioned setup"
-    if not partitioned:
+        uid = D.broadcast_uid()
+        row0, nl = D.attach(prob.K, uid, world, rank)
+        ns = D.local_nullspace(prob.x0, prob.y0, row0, nl)
+        K, M = bosp.local_operator(prob.K, world, rank), bosp.local_operator(prob.M, world, rank)
+    else:
         row0, nl = 0, prob.n
         ns = bosp.GeneralizedNullspace(prob.x0, prob.y0)
         K, M = bosp.operators_for(prob)   # resident in HBM before the timed region
-    flush = 512 << 20                  # 512 MB > 126 MB L2, written between steps
-    units = 1 if partitioned else world  # one shared problem vs. one replica per rank
-
-    def one_step(profile_family=None):
-        profile_family = profile_family or None
-        _lib.lib().bosp_flush_l2(flush)
-        if profile_family:
-            bosp.profile_enable(profile_family)
-        r = bosp.solve(K, M, None, cfg, ns, want_vectors=True)
-        prof = bosp.profile_collect() if profile_family else None
-        if profile_family:
-            bosp.profile_enable(None)
-        return r, prof
+    flush = 512 << 20                     # 512 MB > 126 MB L2, written between steps
 
     for _ in range(args.warmup):  # same configuration as the timed steps (graphs recorded here)
-        one_step(args.roofline_kernel)
+        solve_once(bosp, lib, K, M, cfg, ns, flush)
     barrier(dist)
     bosp.device_sync()
     bosp.launch_reset()
-    dev_s, wall_s, iters, profs = [], [], [], []
+    dev_s, wall_s, iters = [], [], []
     res = None
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
-            res, prof = one_step(args.roofline_kernel)
+            res, _ = solve_once(bosp, lib, K, M, cfg, ns, flush)
+            if not res.converged or res.nev_converged < nev:
+                raise SystemExit(f"bench: solve did not converge ({res.nev_converged}/{nev})")
             dev_s.append(res.stats["device_seconds"])
             wall_s.append(res.stats["wall_seconds"])
             iters.append(res.iterations)
-            profs.append(prof)
     bosp.device_sync()
     barrier(dist)
     launches = bosp.launch_count()
     families = bosp.launch_families()
     total = max_over_ranks(dist, float(sum(dev_s)))
     ms_per_step = total / args.steps * 1e3
-    value = prob.cfg["nev"] * args.steps * units / total
+    value = res.nev_converged * args.steps / total
 
-    # parity of the measured run against the reference's own eigenvalues (golden fixture)
-    parity = None
-    try:
-        g = json.load(open(GOLDEN))["config2"]["lambdas"]
-        parity = float(np.max(np.abs(res.lambdas - np.array(g)) / np.array(g)))
-    except Exception:
-        pass
-
-    # e2e: public API with host buffers -- operator construction from pinned host CSR, the solve,
-    # results back to host; all inside the timed region.
-    kc, mc = prob.K, prob.M
-    host = {}
-    for tag, c in (("k", kc), ("m", mc)):
-        rp = c.rowptr[row0:row0 + nl + 1]
-        host[tag] = (np.ascontiguousarray(rp), np.ascontiguousarray(c.colidx[rp[0]:rp[-1]]),
-                     np.ascontiguousarray(c.vals[rp[0]:rp[-1]]))
-    h2d = sum(a.nbytes for t in host.values() for a in t) + ns.x0.nbytes + ns.y0.nbytes
-    d2h = 2 * nl * prob.cfg["nev"] * 8 + 2 * prob.cfg["nev"] * 8
-    e2e_t = []
-    for _ in range(max(1, args.steps)):
-        _lib.lib().bosp_flush_l2(flush)
+    # e2e: the public API with host buffers -- operator construction from the host description,
+    # the nullspace pair H2D, the solve, eigenvalues + eigenvectors back into host buffers; all
+    # inside the timed region (wall clock, max over ranks).
+    e2e_t, h2d = [], 0
+    d2h = 2 * nl * nev * 8 + 2 * nev * 8
+    for _ in range(max(1, min(args.steps, args.e2e_steps))):
+        lib.bosp_flush_l2(flush)
         barrier(dist)
-        t0 = time.perf_counter()
+        t1 = time.perf_counter()
         if partitioned:
-            Ke = bosp.LinearOperator.from_csr_rows(prob.n, row0, *host["k"])
-            Me = bosp.LinearOperator.from_csr_rows(prob.n, row0, *host["m"])
+            Ke, Me = bosp.local_operator(prob.K, world, rank), bosp.local_operator(prob.M, world, rank)
         else:
-            Ke = bosp.LinearOperator.from_csr(*host["k"])
-            Me = bosp.LinearOperator.from_csr(*host["m"])
+            Ke, Me = bosp.operators_for(prob)
         r2 = bosp.solve(Ke, Me, None, cfg, ns, want_vectors=True)
         _ = float(r2.lambdas.sum())
-        e2e_t.append(time.perf_counter() - t0)
-        del Ke, Me
+        e2e_t.append(time.perf_counter() - t1)
+        h2d = host_bytes(prob, nl) + ns.x0.nbytes + ns.y0.nbytes
+        del Ke, Me, r2
     e2e_total = max_over_ranks(dist, float(sum(e2e_t)))
-    e2e_value = prob.cfg["nev"] * len(e2e_t) * units / e2e_total
-    if partitioned:
-        bosp.comm_free()
+    e2e_value = nev * len(e2e_t) / e2e_total
 
-    # roofline of the dominant kernel family (CUDA events on the solver stream, timed region)
+    # rooflines: one extra solve (outside the timed region) with every launch timed on the
+    # device, split by kernel family (CUDA events; device-clock slots inside the CG graphs)
     peaks = load_peaks()
-    roof = None
-    pr = [p for p in profs if p]
-    if pr:
-        launches_k = sum(p["launches"] for p in pr)
-        ms_k = sum(p["ms"] for p in pr)
-        bytes_k = sum(p["bytes"] for p in pr)
-        if launches_k and ms_k > 0:
-            achieved = bytes_k / (ms_k * 1e-3) / 1e9
-            traffic, traffic_note = None, None
-            try:  # DRAM bytes per launch of the same kernel from the committed ncu --set full capture
-                tr = json.load(open(os.path.join(ROOT, "profiles", "roofline_traffic.json")))
-                if args.roofline_kernel in tr.get("kernel", ""):
-                    traffic = tr["dram_bytes_per_launch"]
-                    traffic_note = {"algorithmic_bytes_per_launch_in_capture": tr["algorithmic_bytes_per_launch"],
-                                    "source": tr["capture"]}
-            except Exception:
-                pass
-            roof = {"kernel": args.roofline_kernel, "bound": "hbm", "achieved": achieved,
-                    "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
-                    "frac": achieved / peaks.get("hbm_gbs", 6650.0), "traffic": traffic,
-                    "traffic_capture": traffic_note,
-                    "launches_per_step": launches_k / len(pr),
-                    "avg_launch_us": ms_k * 1e3 / launches_k,
-                    "algorithmic_bytes_per_launch": bytes_k / launches_k,
-                    "share_of_step": ms_k / (sum(dev_s) * 1e3),
-                    "bytes_note": "CSR-equivalent algorithmic bytes (SURVEY 8d: 12 nnz + 4(n+1) + 16 n m_active); "
-                                  "the DIA form stored for config 2 moves 16 n m + 10 n, see DESIGN.md section 6",
-                    "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if "_fallback" not in peaks
-                    else "fallback 6650 GB/s (B200_PROFILING.md)"}
-
-    # MGS-Biorth as a unit (biorth.cpp:102-109): one extra profiled solve (outside the timed
-    # region) in which every launch issued inside an MGS-Biorth call is timed on the device.
+    roof, rooflines, prof_fams = None, {}, None
+    if not args.no_kernel_rooflines:
+        _, pm = solve_once(bosp, lib, K, M, cfg, ns, flush, profile="*")
+        prof_fams = pm["families"]
+        prof_ms = sum(f["ms"] for f in prof_fams.values())
+        dgemm = cublas_dgemm_tflops() if rank == 0 else None
+        for fam, kind in (("gram_wide", "tensor"), ("product_wide", "tensor"), ("dense_apply", "tensor"),
+                          ("spmm_cg", "hbm"), ("spmm", "hbm"), ("cg_vec", "hbm")):
+            r = family_roofline(fam, prof_fams.get(fam), prof_ms, peaks, dgemm, kind, NOTES.get(fam, ""))
+            if r:
+                rooflines[fam] = r
+        dom, _kind = DOMINANT.get(wl, ("gram_wide", "tensor"))
+        roof = dict(rooflines.get(dom) or {})
+        if roof:
+            traffic, ent = traffic_for(dom, wl)
+            roof["kernel"] = dom
+            roof["traffic"] = traffic
+            roof["traffic_capture"] = ent
+            roof["share_note"] = ("share_of_step = the family's summed launch time / all launches' time in the "
+                                  "profiled solve (kernel time, serialised per stream)")
+    # MGS-Biorth as a unit (biorth.cpp:102-109): every launch inside an MGS-Biorth call timed
     roof_mgs = None
     if not args.no_kernel_rooflines:
-        _lib.lib().bosp_flush_l2(flush)
-        _, pm = one_step("mgs")
+        _, pm = solve_once(bosp, lib, K, M, cfg, ns, flush, profile="mgs")
         if pm and pm["launches"] and pm["ms"] > 0:
             hbm = peaks.get("hbm_gbs", 6650.0)
             ach = pm["region_bytes"] / (pm["ms"] * 1e-3) / 1e9
-            roof_mgs = {"kernel": "mgs_biorth (Gram + coefficient product + P^T Q check kernels)",
+            roof_mgs = {"kernel": "mgs_biorth (pair Gram + coefficient products + P^T Q check)",
                         "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
                         "calls_per_solve": pm["region_calls"], "launches_per_solve": pm["launches"],
                         "avg_call_us": pm["ms"] * 1e3 / max(1, pm["region_calls"]),
                         "algorithmic_bytes_per_call": pm["region_bytes"] / max(1, pm["region_calls"]),
-                        "kernel_operand_gbs": pm["bytes"] / (pm["ms"] * 1e-3) / 1e9,
-                        "share_of_step": pm["ms"] / (ms_per_step),
+                        "share_of_step": pm["ms"] / ms_per_step,
                         "bytes_note": "48 n m per call (SURVEY 8d: X, Y read + P, Q written = 32 n m, + 16 n m "
-                                      "for the P^T Q Gram of the second-pass test); kernel_operand_gbs counts "
-                                      "every operand each kernel reads/writes (the Gram re-reads X, Y)"}
-    roof_dmma = None
-    if rank == 0 and not args.no_kernel_rooflines:
-        roof_dmma = dmma_roofline()
+                                      "for the P^T Q Gram of the second-pass test)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            s = cpu_reference_sample(prob, args.ref_iters, os.cpu_count() or 1)
-            cpu = {"value": prob.cfg["nev"] / s["est_solve_s"], "unit": UNIT, "cores": s["threads"],
-                   "kind": "reference",
-                   "sample": (f"oracle/_ref (unmodified reference) initialize + {s['iters']} iterate_once on "
-                              f"config 2; solve = t_init + {s['full_iters']} x t_iter "
-                              f"(t_init={s['t_init']:.2f}s, t_iter={s['t_iter']:.2f}s)")}
+            thr = os.cpu_count() or 1
+            smp = [ref_sample(24, 1, thr), ref_sample(32, 1, thr)]
+            est = ref_estimate(smp, prob.n, int(statistics.median(iters)))
+            cpu = {"value": nev / est["solve_s"], "unit": UNIT, "cores": smp[0]["threads"], "kind": "reference",
+                   "sample": (f"ESTIMATE: oracle/_ref (unmodified reference) initialize + 1 iterate_once on the "
+                              f"config-3 family at 24^3 and 32^3, t(n) = a + b n extrapolated to 128^3, "
+                              f"solve = t_init + {int(statistics.median(iters))} x t_iter "
+                              f"(t_init={est['t_init']:.1f}s, t_iter={est['t_iter']:.1f}s)")}
         except Exception as e:  # the checker is optional on a box without oracle/_ref
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
 
+    others = {}
+    if rank == 0 and world == 1 and not args.no_other_configs:
+        del K, M
+        for c in ("config1", "config2", "config4", "config5"):
+            if c == wl:
+                continue
+            try:
+                others[c] = run_other_config(c, bosp, P, lib, flush, 1 if c in ("config4", "config5") else 3)
+            except Exception as e:  # noqa: BLE001 -- reported, not hidden
+                others[c] = {"error": f"{type(e).__name__}: {e}"[:300]}
+
+    if partitioned:
+        bosp.comm_free()
+
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "metric": METRIC if wl == HEADLINE else f"converged eigenpairs/s (LREP solve, {wl})",
+            "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "strong" if partitioned else "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generator, paper_2506_08355_b200/problems.py; no dataset)",
-            "config": {"workload": prob.name, "n": prob.n, "nnz_K": kc.nnz, "nev": 20, "nb": 40,
-                       "tol": 1e-8,
-                       "parallelism": (f"row partition x{world} (NCCL allreduce + halo)" if partitioned
-                                       else "replicas" if world > 1 else "single GPU"),
-                       **({"partition_error": partition_error} if partition_error else {}),
-                       "l2": "flushed between steps (512 MB memset)", "device": name, "sms": sms},
+            "config": {"workload": {"config3": "config3-stencil7-128^3"}.get(wl, prob.name), "n": prob.n,
+                       "nev": nev, "nb": prob.cfg.get("nb"), "moving": prob.cfg.get("moving"),
+                       "tol": prob.cfg.get("tol"),
+                       "parallelism": (f"row partition x{world} (NCCL allreduce + halo planes)" if partitioned
+                                       else "single GPU"),
+                       "l2": "flushed between steps (512 MB memset); working set >> 126 MB L2",
+                       "device": name, "sms": sms, "generator_s": gen_s},
             "roofline": roof,
+            "rooflines": rooflines,
             "roofline_mgs": roof_mgs,
-            "roofline_dmma": roof_dmma,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "steps_s": [round(t, 4) for t in e2e_t]},
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "solve": {"iterations": iters, "device_s": dev_s, "wall_s": wall_s,
-                      "host_small_s": res.stats["host_small_seconds"], "repairs": res.stats["repairs"],
-                      "cg_iterations": res.stats["cg_iterations"],
-                      "max_rel_eig_err_vs_reference": parity,
-                      "max_residual": float(res.residuals.max()),
-                      "final_biorth_deviation": res.stats["final_biorth_deviation"],
-                      "launch_families": families},
+                      **check_record(prob, res, golden_record(wl)), "launch_families": families,
+                      "profiled_family_ms": ({k: round(v["ms"], 3) for k, v in prof_fams.items()}
+                                             if prof_fams else None)},
+            "configs": others,
         }
         print(json.dumps(line), flush=True)
+
+
+def host_bytes(prob, nl):
+    """Bytes of the host operator description handed to the library per e2e step."""
+    def one(op):
+        if isinstance(op, np.ndarray):
+            return op.nbytes * nl // max(1, op.shape[0])
+        if hasattr(op, "rowptr"):
+            return op.rowptr.nbytes + op.colidx.nbytes + op.vals.nbytes
+        v = getattr(op, "v", None)
+        return 0 if v is None else np.asarray(v).nbytes
+    return one(prob.K) + one(prob.M)
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--roofline-kernel", default="spmm_cg",
-                    help="kernel family timed for the roofline (default: the dominant one, the CG SpMM)")
-    ap.add_argument("--ref-iters", type=int, default=2)
+    ap.add_argument("--workload", default=HEADLINE, choices=["config1", "config2", "config3", "config4", "config5"])
+    ap.add_argument("--e2e-steps", type=int, default=3, help="e2e steps (<= --steps)")
+    ap.add_argument("--c3-iters", type=int, default=C3_ITERS_DEFAULT,
+                    help="reference arm: outer iterations assumed for the full config-3 solve")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-other-configs", action="store_true")
     ap.add_argument("--no-kernel-rooflines", action="store_true",
-                    help="skip the MGS-Biorth and fp64-DMMA kernel rooflines (extra, untimed work)")
-    ap.add_argument("--partition", default="rows", choices=["rows", "replicas"],
-                    help="N>1: row-partition one solve over the ranks (NCCL) or run N replicas")
+                    help="skip the profiled (untimed) solves behind the kernel rooflines")
     args = ap.parse_args()
     world, rank, local, dist = dist_setup()
     if args.impl == "reference":

@@ -265,6 +265,10 @@ void bosp_profile_collect(int64_t* launches, double* ms, double* bytes, double* 
  * P^T Q check of the second-pass test).  Either extra pointer may be NULL. */
 void bosp_profile_collect_regions(int64_t* launches, double* ms, double* bytes, double* flops,
                                   int64_t* region_calls, double* region_bytes);
+/* After bosp_profile_enable("*") (every launch timed) and a collect: the collected totals split
+ * by kernel family, one text line per family "<family> <launches> <ms> <bytes> <flops>\n"
+ * into buf (NUL-terminated, truncated to len); returns the length the full report needs. */
+int64_t bosp_profile_family_report(char* buf, int64_t len);
 /* Microbenchmark: apply `op` to a device-resident random n x ncols block `reps` times (after
  * one warm-up); returns the mean device time per apply in *ms (CUDA events). */
 bosp_status bosp_bench_apply(bosp_op op, int64_t ncols, int64_t reps, double* ms);

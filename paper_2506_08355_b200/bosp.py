@@ -612,8 +612,19 @@ def profile_collect():
     rc, rb = C.c_int64(), C.c_double()
     lib().bosp_profile_collect_regions(C.byref(n), C.byref(ms), C.byref(b), C.byref(f),
                                        C.byref(rc), C.byref(rb))
-    return dict(launches=n.value, ms=ms.value, bytes=b.value, flops=f.value,
-                region_calls=rc.value, region_bytes=rb.value)
+    out = dict(launches=n.value, ms=ms.value, bytes=b.value, flops=f.value,
+               region_calls=rc.value, region_bytes=rb.value)
+    L_ = lib()
+    L_.bosp_profile_family_report.restype = C.c_int64
+    need = L_.bosp_profile_family_report(None, C.c_int64(0))
+    buf = C.create_string_buffer(int(need))
+    L_.bosp_profile_family_report(buf, C.c_int64(need))
+    fams = {}
+    for line in buf.value.decode().splitlines():
+        f, l, m, by, fl = line.split()
+        fams[f] = dict(launches=int(l), ms=float(m), bytes=float(by), flops=float(fl))
+    out["families"] = fams
+    return out
 
 
 def launch_count():

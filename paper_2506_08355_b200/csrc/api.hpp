@@ -279,6 +279,7 @@ struct HostVectorsOut {
     double* x = nullptr;
     double* y = nullptr;
     int64_t cap = 0;
+    bool discard = false;  // the caller wants eigenvalues/residuals only: no vector copy-out
 };
 EigenResult solve(const LinearOperator& k, const LinearOperator& m, const InnerProduct& ip,
                   const BospConfig& cfg, std::optional<GeneralizedNullspace> ns = std::nullopt,

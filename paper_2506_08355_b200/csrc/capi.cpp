@@ -2,6 +2,8 @@
 // codes.  No exception crosses this boundary.
 #include "../../include/bosp_b200.h"
 
+#include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <string>
 
@@ -312,8 +314,9 @@ bosp_status bosp_solve(bosp_op K, bosp_op M, bosp_op B, const bosp_config* c, in
             g.y0 = host_block(y0, n, r);
             ns = std::move(g);
         }
-        const bosp::HostVectorsOut hv{x, y, cap};
-        bosp::EigenResult res = bosp::solve(K->op, M->op, ip_of(B), cfg, std::move(ns), (x && y) ? &hv : nullptr);
+        // null x / y: eigenvectors stay in HBM (no host copy); otherwise straight into x, y
+        const bosp::HostVectorsOut hv{x, y, cap, !(x && y)};
+        bosp::EigenResult res = bosp::solve(K->op, M->op, ip_of(B), cfg, std::move(ns), &hv);
         write_result(res, cfg, cap, lambdas, x, y, residuals, nout, stats, history, history_cap, history_rows);
     });
 }
@@ -602,6 +605,25 @@ void bosp_profile_enable(const char* family) {
         bosp::Runtime::get().prof_enable(family ? family : "");
     } catch (...) {
     }
+}
+
+int64_t bosp_profile_family_report(char* buf, int64_t len) {
+    std::string s;
+    try {
+        char line[256];
+        for (const auto& kv : bosp::Runtime::get().prof_by_family()) {
+            std::snprintf(line, sizeof(line), "%s %lld %.9g %.17g %.17g\n", kv.first.c_str(),
+                          (long long)kv.second.launches, kv.second.ms, kv.second.bytes, kv.second.flops);
+            s += line;
+        }
+    } catch (...) {
+    }
+    if (buf && len > 0) {
+        const size_t n = std::min<size_t>(s.size(), static_cast<size_t>(len - 1));
+        std::memcpy(buf, s.data(), n);
+        buf[n] = '\0';
+    }
+    return static_cast<int64_t>(s.size()) + 1;
 }
 
 void bosp_profile_collect(int64_t* launches, double* ms, double* bytes, double* flops) {

@@ -341,7 +341,10 @@ void launch_gram(const GramJob* jobs, int njobs, int64_t n) {
         bytes += 8.0 * n * (double)(same_columns(jobs[j].a, jobs[j].b) ? jobs[j].a.cols() : jobs[j].a.cols() + jobs[j].b.cols());
     }
     {
-        LaunchScope ls("gram", bytes, flops);
+        // families: the wide Rayleigh-Ritz / repair Grams (64 x 64 tiles), the dense operator's
+        // A x (128 x 32 tiles over the stored A^T), and the small tiled Grams
+        const char* fam = (BM == 64 && BN == 64) ? "gram_wide" : (BM == 128 && BN == 32) ? "dense_apply" : "gram";
+        LaunchScope ls(fam, bytes, flops);
         dim3 grid(max_tiles, prm.splits, njobs);
         k_gram<BM, BN, WM, WN, GBK, GST><<<grid, NT, smem, rt.stream()>>>(prm);
         BOSP_LAUNCH_CHECK();
@@ -732,7 +735,7 @@ void launch_product(const ProductJob* jobs, int njobs, int64_t n) {
         BOSP_CUDA(cudaFuncSetAttribute(k_product<BM, BN, WM, WN>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     }
-    LaunchScope ls("product", bytes, flops);
+    LaunchScope ls("product_wide", bytes, flops);
     const unsigned gx = static_cast<unsigned>(std::min<int64_t>(max_tiles, 65535));
     const unsigned gy = static_cast<unsigned>((max_tiles + gx - 1) / gx);
     dim3 grid(gx, gy, njobs);

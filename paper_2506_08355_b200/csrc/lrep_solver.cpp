@@ -640,6 +640,11 @@ EigenResult assemble_result(DeviceState& st, const LinearOperator& k, const Line
     DenseMatrix g = ip_gram_host(ip, rx.view(), ry.view());
     for (int64_t i = 0; i < g.rows(); ++i) g(i, i) -= 1.0;
     res.stats.final_biorth_deviation = g.max_abs();
+    if (out && out->discard) {
+        res.x = BlockVectors(n, 0);
+        res.y = BlockVectors(n, 0);
+        return res;
+    }
     if (out && out->x && out->y) {
         require(h <= out->cap, "solve: output capacity too small");
         to_host(rx.view(), out->x, n);

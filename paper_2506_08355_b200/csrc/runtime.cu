@@ -135,7 +135,7 @@ void Runtime::prof_enable(const std::string& family) {
 }
 
 bool Runtime::prof_on(const char* family) const {
-    return !prof_family_.empty() && (region_depth_ > 0 || prof_family_ == family);
+    return !prof_family_.empty() && (region_depth_ > 0 || prof_family_ == family || prof_family_ == "*");
 }
 
 bool Runtime::region_open(const char* name) {
@@ -164,9 +164,8 @@ cudaEvent_t Runtime::take_event() {
 }
 
 void Runtime::prof_begin(const char* family, double bytes, double flops) {
-    (void)family;
     if (capture_prof_) return;  // inside a graph only device-clock timers are possible
-    Ev ev{take_event(), take_event(), bytes, flops};
+    Ev ev{take_event(), take_event(), bytes, flops, family};
     BOSP_CUDA(cudaEventRecord(ev.a, stream_));
     prof_events_.push_back(ev);
 }
@@ -187,7 +186,7 @@ unsigned long long* Runtime::timer_begin(const char* family, double bytes, doubl
     unsigned long long* p = timer_slots_ + kSlotWords * slot;
     if (timer_reserved_ > 0) --timer_reserved_;
     else BOSP_CUDA(cudaMemsetAsync(p, 0, kSlotWords * sizeof(unsigned long long), stream_));
-    ProfPair pp{slot, bytes, flops, fixed_bytes, ncols};
+    ProfPair pp{slot, bytes, flops, fixed_bytes, ncols, family};
     if (capture_prof_) capture_prof_->push_back(pp);
     else timer_pending_.push_back(pp);
     return p;
@@ -229,10 +228,16 @@ void Runtime::read_timer_samples(const std::vector<ProfPair>& pairs) {
             if (act == 0) continue;  // nothing to do (converged columns): not a real apply
             frac = static_cast<double>(act) / static_cast<double>(p.ncols);
         }
+        const double ms = (e - s) * 1e-6, by = p.fixed_bytes + (p.bytes - p.fixed_bytes) * frac;
         graph_samples_.launches += 1;
-        graph_samples_.ms += (e - s) * 1e-6;
-        graph_samples_.bytes += p.fixed_bytes + (p.bytes - p.fixed_bytes) * frac;
+        graph_samples_.ms += ms;
+        graph_samples_.bytes += by;
         graph_samples_.flops += p.flops * frac;
+        ProfReport& f = by_family_[p.family ? p.family : "?"];
+        f.launches += 1;
+        f.ms += ms;
+        f.bytes += by;
+        f.flops += p.flops * frac;
     }
 }
 
@@ -254,10 +259,17 @@ Runtime::ProfReport Runtime::prof_collect() {
         r.bytes += e.bytes;
         r.flops += e.flops;
         ++r.launches;
+        ProfReport& f = by_family_[e.family ? e.family : "?"];
+        f.launches += 1;
+        f.ms += ms;
+        f.bytes += e.bytes;
+        f.flops += e.flops;
         event_pool_.push_back(e.a);
         event_pool_.push_back(e.b);
     }
     prof_events_.clear();
+    last_by_family_ = std::move(by_family_);
+    by_family_.clear();
     return r;
 }
 

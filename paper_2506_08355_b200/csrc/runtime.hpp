@@ -117,6 +117,8 @@ public:
         int64_t region_calls = 0; double region_bytes = 0.0;
     };
     ProfReport prof_collect();  // synchronises, sums elapsed times, resets
+    // prof_enable("*") times every launch; the last prof_collect() split by kernel family
+    const std::map<std::string, ProfReport>& prof_by_family() const { return last_by_family_; }
     // Composite-operation profiling: while a region named like the profiled family is open,
     // every launch inside it is timed (whatever its own family); at close the region credits
     // its algorithmic bytes once.  Nested regions of the same name count once (outermost).
@@ -129,7 +131,7 @@ public:
     // Slot words: [~earliest start, latest end, columns the launch actually applied (0 = none
     // reported)].  bytes/flops are the launch's algorithmic totals for all `ncols` columns; a
     // launch that reports fewer active columns is credited proportionally (fixed part kept).
-    struct ProfPair { int64_t slot; double bytes, flops, fixed_bytes; int64_t ncols; };
+    struct ProfPair { int64_t slot; double bytes, flops, fixed_bytes; int64_t ncols; const char* family; };
     static constexpr int kSlotWords = 4;
     unsigned long long* timer_begin(const char* family, double bytes, double flops, double fixed_bytes = 0.0,
                                     int64_t ncols = 0);
@@ -162,7 +164,9 @@ private:
     std::map<std::string, int64_t> family_launches_;
     std::map<std::string, int64_t>* capture_sink_ = nullptr;
     std::string prof_family_;
-    struct Ev { cudaEvent_t a, b; double bytes, flops; };
+    struct Ev { cudaEvent_t a, b; double bytes, flops; const char* family; };
+    // per-family split of the last prof_collect() (family names are string literals)
+    std::map<std::string, ProfReport> by_family_, last_by_family_;
     std::vector<Ev> prof_events_;
     std::vector<ProfPair>* capture_prof_ = nullptr;
     std::vector<ProfPair> timer_pending_;
