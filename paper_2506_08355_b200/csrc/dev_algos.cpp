@@ -153,6 +153,22 @@ DenseMatrix apply_coefs_gram(const DMat& x, const DMat& y, const DenseMatrix& a,
     return h;
 }
 
+// Gxx = X^T X and Gyy = Y^T Y only (unweighted): two symmetric jobs in one launch.
+void self_grams(const DMat& x, const DMat& y, DenseMatrix& gxx, DenseMatrix& gyy) {
+    const int64_t m = x.cols;
+    DBlock g(m, 2 * m);
+    GramJob jobs[2] = {{ColList(x), ColList(x), g.data(), g.ld()}, {ColList(y), ColList(y), g.data() + m * g.ld(), g.ld()}};
+    jobs[0].sym = jobs[1].sym = true;
+    gram(jobs, 2, x.rows);
+    Runtime::get().allreduce(g.data(), g.ld() * 2 * m);
+    DenseMatrix both(m, 2 * m);
+    to_host(g.view().cols_range(0, 2 * m), both.data(), m);
+    gxx = DenseMatrix(m, m);
+    gyy = DenseMatrix(m, m);
+    std::copy(both.data(), both.data() + m * m, gxx.data());
+    std::copy(both.data() + m * m, both.data() + 2 * m * m, gyy.data());
+}
+
 // Gxx, Gxy, Gyy of the pair under ip.
 void pair_grams(const DMat& x, const DMat& y, const InnerProduct& ip, DenseMatrix& gxx,
                 DenseMatrix& gxy, DenseMatrix& gyy) {
@@ -207,7 +223,8 @@ void pair_grams(const DMat& x, const DMat& y, const InnerProduct& ip, DenseMatri
 }  // namespace
 
 DevBiorthOutcome dev_mgs_biorth(const DMat& x, const DMat& y, const DMat& p, const DMat& q,
-                                const InnerProduct& ip, double drop_tol, bool classical) {
+                                const InnerProduct& ip, double drop_tol, bool classical,
+                                const DenseMatrix* gxy_hint) {
     require(x.rows == y.rows && x.cols == y.cols, "biorth: X and Y must have equal shape");
     DevBiorthOutcome out;
     const int64_t m = x.cols, n = x.rows;
@@ -230,7 +247,12 @@ DevBiorthOutcome dev_mgs_biorth(const DMat& x, const DMat& y, const DMat& p, con
         const int64_t mr = cx.cols;
         if (mr == 0) break;
         DenseMatrix gxx, gxy, gyy;
-        pair_grams(cx, cy, ip, gxx, gxy, gyy);
+        if (start == 0 && gxy_hint && !ip.weighted() && gxy_hint->rows() == mr && gxy_hint->cols() == mr) {
+            self_grams(cx, cy, gxx, gyy);
+            gxy = *gxy_hint;
+        } else {
+            pair_grams(cx, cy, ip, gxx, gxy, gyy);
+        }
         int64_t stop = mr;
         CoefBiorth cb = coef_mgs(gxx, gxy, gyy, drop_tol, classical, kCancel, &stop);
         const int64_t kb = static_cast<int64_t>(cb.kept.size());

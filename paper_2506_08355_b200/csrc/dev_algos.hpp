@@ -42,9 +42,11 @@ struct DevBiorthOutcome {
 // where ill-conditioned inputs (Table 1) need the n-space recurrence, not Grams.
 DevBiorthOutcome dev_gs_biorth_seq(const DMat& x, const DMat& y, const DMat& p, const DMat& q,
                                    const InnerProduct& ip, double drop_tol, bool classical);
+// gxy_hint: X^T Y already known on the host (unweighted only) -- the pair Grams then compute
+// only X^T X and Y^T Y (the drift repair reuses the invariant sample's U^T V, lrep_solver.cpp).
 DevBiorthOutcome dev_mgs_biorth(const DMat& x, const DMat& y, const DMat& p, const DMat& q,
                                 const InnerProduct& ip, double drop_tol = 1e-12,
-                                bool classical = false);
+                                bool classical = false, const DenseMatrix* gxy_hint = nullptr);
 // ||P^T Q - I||_2 (biorth.cpp:135-143).
 double dev_biorth_residual(const DMat& p, const DMat& q, const InnerProduct& ip);
 

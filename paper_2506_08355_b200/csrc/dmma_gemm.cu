@@ -79,6 +79,80 @@ __device__ __forceinline__ void load_kcontig(double* smem, const ColList& cl, in
     }
 }
 
+// The same k-contiguous tile load with every per-thread address computed once per CTA.  A thread
+// always copies the same row pair (2 kp) of the same kPer columns of every stage (NT is a
+// multiple of BK / 2), so the column pointers (ColList segment lookup) and shared offsets are
+// fixed; a stage only adds its first row k0.  (ncu on the per-chunk form: ~60 % of the Gram
+// kernel's issued instructions were this address arithmetic, DMMA only 10 %.)
+template <int R, int NT, int BK>
+struct KcontigLoader {
+    static_assert(NT % (BK / 2) == 0, "a thread keeps one row pair across stages");
+    static constexpr int kChunks = R * (BK / 2);
+    static constexpr int kPer = (kChunks + NT - 1) / NT;
+    const double* src[kPer];  // column base + this thread's row pair offset; nullptr: zero fill
+    int off[kPer];            // shared offset (c * (BK + 4) + 2 kp), -1: no chunk
+    int kp2;
+    const double* dummy;      // a valid address for zero-fill copies
+
+    __device__ __forceinline__ void init(const ColList& cl, int col0, int ncols) {
+        kp2 = 2 * (static_cast<int>(threadIdx.x) % (BK / 2));
+        dummy = cl.p[0];
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) {
+            const int ch = static_cast<int>(threadIdx.x) + i * NT;
+            const int c = ch / (BK / 2);
+            const bool have = (kChunks % NT == 0) || ch < kChunks;
+            off[i] = have ? c * (BK + 4) + kp2 : -1;
+            src[i] = (have && col0 + c < ncols) ? colptr(cl, col0 + c) + kp2 : nullptr;
+        }
+    }
+    // rows [k0, k0 + BK) of the tile, rows >= kmax zero-filled
+    __device__ __forceinline__ void load(double* smem, int64_t k0, int64_t kmax) const {
+        const int64_t k = k0 + kp2;
+        const int bytes = k + 2 <= kmax ? 16 : (k < kmax ? 8 : 0);
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) {
+            if ((kChunks % NT) != 0 && off[i] < 0) continue;
+            const bool v = src[i] != nullptr;
+            cp_async16(smem + off[i], v ? src[i] + k0 : dummy, v ? bytes : 0);
+        }
+    }
+};
+
+// m-contiguous tile load (BK columns x BM rows into smem[k * (BM + 4) + m]) for the product's A
+// operand with fixed per-thread rows: a thread always copies rows m0 + 2 mp of columns
+// k0 + kk0 + i * (NT / (BM / 2)); the column base pointers come from a shared table filled once
+// per CTA (no ColList segment search per chunk and stage).
+template <int BM, int NT, int BK>
+struct McontigLoader {
+    static_assert(NT % (BM / 2) == 0, "a thread keeps one row pair across stages");
+    static constexpr int kRowsPer = NT / (BM / 2);  // column stride between a thread's chunks
+    static constexpr int kPer = (BK * (BM / 2) + NT - 1) / NT;
+    int kk0, soff;
+    int64_t m;   // first row of this thread's pair
+    int bytes;   // rows of the pair inside the matrix (16, 8 or 0 bytes)
+    const double* dummy;
+    __device__ __forceinline__ void init(const double* any, int64_t m0, int64_t mmax) {
+        const int mp = static_cast<int>(threadIdx.x) % (BM / 2);
+        kk0 = static_cast<int>(threadIdx.x) / (BM / 2);
+        m = m0 + 2 * mp;
+        const int64_t rem = mmax - m;
+        bytes = rem >= 2 ? 16 : (rem == 1 ? 8 : 0);
+        soff = kk0 * (BM + 4) + 2 * mp;
+        dummy = any;
+    }
+    __device__ __forceinline__ void load(double* smem, const double* const* coltab, int k0, int kcols) const {
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) {
+            const int kk = kk0 + i * kRowsPer;
+            if ((BK * (BM / 2)) % NT != 0 && kk >= BK) continue;
+            const int gk = k0 + kk;
+            const bool v = gk < kcols && bytes > 0;
+            cp_async16(smem + soff + i * kRowsPer * (BM + 4), v ? coltab[gk] + m : dummy, v ? bytes : 0);
+        }
+    }
+};
+
 // Load an "m-contiguous" tile for the NN product: kBK columns (k0..k0+kBK of A, clipped to
 // kcols) x BM rows (m0.., clipped to mmax) into smem[k * (BM+4) + m].
 template <int BM, int NT, int BK = kBK>
@@ -185,11 +259,15 @@ k_gram(GramParams prm) {
         for (int j = 0; j < NTL; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
     const int nk = ke > kb ? static_cast<int>((ke - kb + kBK - 1) / kBK) : 0;
+    KcontigLoader<BM, NT, kBK> lda;
+    KcontigLoader<BN, NT, kBK> ldb;
+    lda.init(job.a, m0, acols);
+    ldb.init(job.b, n0, bcols);
 #pragma unroll
     for (int s = 0; s < kStages - 1; ++s) {
         if (s < nk) {
-            load_kcontig<BM, NT, kBK>(sa + s * BM * kLdK, job.a, m0, acols, kb + s * kBK, ke);
-            load_kcontig<BN, NT, kBK>(sb + s * BN * kLdK, job.b, n0, bcols, kb + s * kBK, ke);
+            lda.load(sa + s * BM * kLdK, kb + s * kBK, ke);
+            ldb.load(sb + s * BN * kLdK, kb + s * kBK, ke);
         }
         cp_async_commit();
     }
@@ -214,8 +292,8 @@ k_gram(GramParams prm) {
         const int nxt = it + kStages - 1;
         if (nxt < nk) {
             const int sn = nxt % kStages;
-            load_kcontig<BM, NT, kBK>(sa + sn * BM * kLdK, job.a, m0, acols, kb + nxt * kBK, ke);
-            load_kcontig<BN, NT, kBK>(sb + sn * BN * kLdK, job.b, n0, bcols, kb + nxt * kBK, ke);
+            lda.load(sa + sn * BM * kLdK, kb + nxt * kBK, ke);
+            ldb.load(sb + sn * BN * kLdK, kb + nxt * kBK, ke);
         }
         cp_async_commit();
     }
@@ -590,6 +668,7 @@ void launch_gram_regs(const GramJob* jobs, int njobs, int64_t n) {
 constexpr int kPStages = BOSP_PSTAGES;
 constexpr int kPBK = BOSP_PBK;
 constexpr int kPLdK = kPBK + 4;
+constexpr int kProdTab = 1024;  // A column pointers kept in shared memory (wider K: per-stage lookup)
 
 struct ProductParams {
     ProductJob job[4];
@@ -639,12 +718,26 @@ k_product(ProductParams prm) {
         for (int j = 0; j < NTL; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
     const int nk = (kcols + kPBK - 1) / kPBK;
+    // column base pointers of A for the whole K range (a table in shared memory, behind the
+    // pipeline buffers), so the stage loads never search the ColList segments
+    const double** coltab = reinterpret_cast<const double**>(smem + kPStages * (kPBK * LdM + BN * kPLdK));
+    const bool tab = kcols <= kProdTab;
+    if (tab) {
+        for (int c = threadIdx.x; c < kcols; c += NT) coltab[c] = colptr(job.a, c);
+        __syncthreads();
+    }
+    McontigLoader<BM, NT, kPBK> lda;
+    lda.init(job.a.p[0], m0, prm.n);
+    KcontigLoader<BN, NT, kPBK> ldb;
+    ldb.init(cl, n0, job.ncols);
+    auto load_stage = [&](int st, int s) {
+        if (tab) lda.load(sa + st * kPBK * LdM, coltab, s * kPBK, kcols);
+        else load_mcontig<BM, NT, kPBK>(sa + st * kPBK * LdM, job.a, s * kPBK, kcols, m0, prm.n);
+        ldb.load(sb + st * BN * kPLdK, s * kPBK, kcols);
+    };
 #pragma unroll
     for (int s = 0; s < kPStages - 1; ++s) {
-        if (s < nk) {
-            load_mcontig<BM, NT, kPBK>(sa + s * kPBK * LdM, job.a, s * kPBK, kcols, m0, prm.n);
-            load_kcontig<BN, NT, kPBK>(sb + s * BN * kPLdK, cl, n0, job.ncols, s * kPBK, kcols);
-        }
+        if (s < nk) load_stage(s, s);
         cp_async_commit();
     }
     for (int it = 0; it < nk; ++it) {
@@ -666,11 +759,7 @@ k_product(ProductParams prm) {
                 for (int j = 0; j < NTL; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
         }
         const int nxt = it + kPStages - 1;
-        if (nxt < nk) {
-            const int sn = nxt % kPStages;
-            load_mcontig<BM, NT, kPBK>(sa + sn * kPBK * LdM, job.a, nxt * kPBK, kcols, m0, prm.n);
-            load_kcontig<BN, NT, kPBK>(sb + sn * BN * kPLdK, cl, n0, job.ncols, nxt * kPBK, kcols);
-        }
+        if (nxt < nk) load_stage(nxt % kPStages, nxt);
         cp_async_commit();
     }
     cp_async_wait<0>();
@@ -727,7 +816,7 @@ void launch_product(const ProductJob* jobs, int njobs, int64_t n) {
     }
     prm.n = n;
     constexpr int NT = WM * WN * 32;
-    constexpr size_t smem_pipe = sizeof(double) * kPStages * (kPBK * (BM + 4) + BN * kPLdK);
+    constexpr size_t smem_pipe = sizeof(double) * (kPStages * (kPBK * (BM + 4) + BN * kPLdK) + kProdTab);
     constexpr size_t smem_epi = sizeof(double) * BN * (BM + 4);
     constexpr size_t smem = smem_pipe > smem_epi ? smem_pipe : smem_epi;
     static unsigned attr_mask = 0;

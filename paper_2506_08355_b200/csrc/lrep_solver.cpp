@@ -171,14 +171,15 @@ const double* upload_scalars(DeviceState& st, const std::vector<double>& v, int 
     return d;
 }
 
-// Full MGS repair of (U, V) (bosp_solver.cpp:79-95).
-void rebiorthogonalize_state(DeviceState& st, const InnerProduct& ip) {
+// Full MGS repair of (U, V) (bosp_solver.cpp:79-95).  gxy_hint: U^T V of the projected pair when
+// the caller already has it (see sample_invariants) -- the MGS then Grams only U^T U and V^T V.
+void rebiorthogonalize_state(DeviceState& st, const InnerProduct& ip, const DenseMatrix* gxy_hint = nullptr) {
     ++st.stats.repairs;
     const int64_t d = st.width();
     const DMat u = st.U.cols(0, d), v = st.V.cols(0, d);
     dev_biorth_against(deflation_bases(st), u, v, ip);
     DBlock nu(st.n, st.U.capacity()), nv(st.n, st.V.capacity());
-    DevBiorthOutcome out = dev_mgs_biorth(u, v, nu.cols(0, d), nv.cols(0, d), ip);
+    DevBiorthOutcome out = dev_mgs_biorth(u, v, nu.cols(0, d), nv.cols(0, d), ip, 1e-12, false, gxy_hint);
     if (!out.dropped_columns.empty())
         throw NumericalAbort("bosp: rebiorthogonalization dropped columns");
     nu.set_cols(st.U.ncols());
@@ -188,7 +189,11 @@ void rebiorthogonalize_state(DeviceState& st, const InnerProduct& ip) {
 }
 
 // Returns the max |U^T V - I| deviation and records cross-Gram statistics (:63-76).
-double sample_invariants(DeviceState& st, const InnerProduct& ip) {
+// projected_gxy (optional): U'^T V' of the pair after biorth_against(deflation bases), i.e. what
+// the drift repair's MGS would Gram first.  With U' = U - P_k (Q_k^T U), V' = V - Q_k (P_k^T V)
+// and P_k^T Q_k = I: U'^T V' = U^T V - sum_k (Q_k^T U)^T (P_k^T V) -- every term is one of the
+// Grams sampled here (cross terms between bases are products of two cross-Grams, ~1e-26).
+double sample_invariants(DeviceState& st, const InnerProduct& ip, DenseMatrix* projected_gxy = nullptr) {
     const int64_t d = st.width();
     const DMat u = st.U.cols(0, d), v = st.V.cols(0, d);
     // U^T V and every deflation cross-Gram in one batch, one device->host copy
@@ -198,6 +203,14 @@ double sample_invariants(DeviceState& st, const InnerProduct& ip) {
         pairs.push_back({b.p, v});
     }
     std::vector<DenseMatrix> gs = ip_grams_host(ip, pairs);
+    if (projected_gxy && !ip.weighted()) {
+        *projected_gxy = gs[0];
+        for (size_t i = 1; i + 1 < gs.size(); i += 2) {
+            const DenseMatrix corr = matmul_tn(gs[i], gs[i + 1]);
+            for (int64_t j = 0; j < d; ++j)
+                for (int64_t r = 0; r < d; ++r) (*projected_gxy)(r, j) -= corr(r, j);
+        }
+    }
     DenseMatrix& g = gs[0];
     for (int64_t i = 0; i < g.rows(); ++i) g(i, i) -= 1.0;
     const double dev = g.max_abs();
@@ -544,9 +557,10 @@ bool iterate_device(DeviceState& st, const LinearOperator& k, const LinearOperat
 
     // invariant sampling doubles as the drift monitor (:429-432)
     double dev;
+    DenseMatrix gxy;
     {
         auto ph = st.phases.scope(PH_SAMPLE);
-        dev = sample_invariants(st, ip);
+        dev = sample_invariants(st, ip, &gxy);
     }
     if (debug_enabled())
         std::fprintf(stderr, "[bosp] it=%lld wx=%lld wp=%lld ww=%lld frozen=%lld locked=%lld nev_conv=%lld "
@@ -555,7 +569,7 @@ bool iterate_device(DeviceState& st, const LinearOperator& k, const LinearOperat
                      (long long)st.nev_conv, (long long)nb_eff, (long long)c0, dev);
     if (dev > 5e-11) {
         auto ph = st.phases.scope(PH_REPAIR);
-        rebiorthogonalize_state(st, ip);
+        rebiorthogonalize_state(st, ip, gxy.rows() == st.width() ? &gxy : nullptr);
     }
     return false;
 }

@@ -4,9 +4,11 @@
 #include <immintrin.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <limits>
 #include <numeric>
 
 #ifdef _OPENMP
@@ -166,14 +168,14 @@ namespace {
 // squared column norms are carried in `nrm` (recomputed at every sweep start): after the
 // rotation that annihilates gamma they are exactly alpha - t*gamma and beta + t*gamma, so a pair
 // costs one dot product instead of three.
-inline bool jacobi_pair(DenseMatrix& a, DenseMatrix& v, double* nrm, int64_t p, int64_t q) {
+inline bool jacobi_pair(DenseMatrix& a, DenseMatrix& v, double* nrm, int64_t p, int64_t q, double tol = 1e-15) {
     const int64_t m = a.rows(), k = v.rows();
     double* ap = a.col(p);
     double* aq = a.col(q);
     const double alpha = nrm[p], beta = nrm[q];
     if (alpha == 0.0 || beta == 0.0) return false;
     const double gamma = dot_avx(ap, aq, m);
-    if (std::fabs(gamma) <= 1e-15 * std::sqrt(alpha * beta)) return false;
+    if (std::fabs(gamma) <= tol * std::sqrt(alpha * beta)) return false;
     const double zeta = (beta - alpha) / (2.0 * gamma);
     const double t = ((zeta >= 0.0) ? 1.0 : -1.0) / (std::fabs(zeta) + std::sqrt(1.0 + zeta * zeta));
     const double c = 1.0 / std::sqrt(1.0 + t * t);
@@ -191,7 +193,9 @@ void column_norms(const DenseMatrix& a, double* nrm) {
 
 }  // namespace
 
-JacobiSvdResult jacobi_svd(DenseMatrix a, int64_t max_sweeps) {
+JacobiSvdResult jacobi_svd(DenseMatrix a, int64_t max_sweeps) { return jacobi_svd_tol(std::move(a), max_sweeps, 1e-15); }
+
+JacobiSvdResult jacobi_svd_tol(DenseMatrix a, int64_t max_sweeps, double tol) {
     const int64_t m = a.rows(), k = a.cols();
     require(m >= k, "jacobi_svd: requires rows >= cols");
     JacobiSvdResult res;
@@ -206,15 +210,25 @@ JacobiSvdResult jacobi_svd(DenseMatrix a, int64_t max_sweeps) {
             ++sweep;
             column_norms(a, nrm.data());
             for (int64_t p = 0; p + 1 < k; ++p)
-                for (int64_t q = p + 1; q < k; ++q) rotated |= jacobi_pair(a, res.v, nrm.data(), p, q);
+                for (int64_t q = p + 1; q < k; ++q) rotated |= jacobi_pair(a, res.v, nrm.data(), p, q, tol);
         }
     } else {
-        // round-robin tournament: each round pairs disjoint columns, rotated in parallel
-        const int64_t kk = k + (k & 1);
-        std::vector<int64_t> pos(kk);
+        // Block round-robin: the columns are cut into nblk blocks (2 per thread) and every round
+        // of a block tournament gives each thread one disjoint block pair (I, J), whose column
+        // pairs it rotates in cyclic order (cross pairs p in I, q in J; in a sweep's first round
+        // also the pairs inside I and inside J), so every column pair is visited once per sweep
+        // as in the cyclic sweep.  nblk - 1 barriers per sweep instead of k - 1 (the per-column
+        // tournament spent as long in barriers as in rotations at d = 320).
+        const int nthr = std::max(1, omp_get_max_threads());
+        int64_t nblk = std::min<int64_t>(2 * nthr, k / 4);
+        nblk += nblk & 1;
+        const int64_t bs = (k + nblk - 1) / nblk;
+        nblk = (k + bs - 1) / bs;
+        nblk += nblk & 1;  // a trailing empty block when odd (a bye in the tournament)
+        auto blk_lo = [&](int64_t b) { return std::min(k, b * bs); };
+        auto blk_hi = [&](int64_t b) { return std::min(k, (b + 1) * bs); };
+        std::vector<int64_t> pos(static_cast<size_t>(nblk));
         std::iota(pos.begin(), pos.end(), 0);
-        // one parallel region per sweep; rounds are separated by barriers (the pair schedule
-        // of round r+1 depends only on r, so every thread can advance its own copy of `pos`)
         std::vector<double> nrm(static_cast<size_t>(k));
         while (rotated && sweep < max_sweeps) {
             ++sweep;
@@ -223,16 +237,23 @@ JacobiSvdResult jacobi_svd(DenseMatrix a, int64_t max_sweeps) {
 #pragma omp parallel reduction(| : any)
             {
                 std::vector<int64_t> lp(pos);
-                for (int64_t round = 0; round < kk - 1; ++round) {
-#pragma omp for schedule(static)
-                    for (int64_t i = 0; i < kk / 2; ++i) {
-                        int64_t p = lp[i], q = lp[kk - 1 - i];
-                        if (p >= k || q >= k) continue;
-                        if (p > q) std::swap(p, q);
-                        any |= jacobi_pair(a, res.v, nrm.data(), p, q) ? 1 : 0;
+                for (int64_t round = 0; round < nblk - 1; ++round) {
+#pragma omp for schedule(dynamic, 1)
+                    for (int64_t i = 0; i < nblk / 2; ++i) {
+                        int64_t bi = lp[i], bj = lp[nblk - 1 - i];
+                        if (bi > bj) std::swap(bi, bj);
+                        const int64_t i0 = blk_lo(bi), i1 = blk_hi(bi), j0 = blk_lo(bj), j1 = blk_hi(bj);
+                        if (round == 0) {
+                            for (int64_t p = i0; p + 1 < i1; ++p)
+                                for (int64_t q = p + 1; q < i1; ++q) any |= jacobi_pair(a, res.v, nrm.data(), p, q, tol);
+                            for (int64_t p = j0; p + 1 < j1; ++p)
+                                for (int64_t q = p + 1; q < j1; ++q) any |= jacobi_pair(a, res.v, nrm.data(), p, q, tol);
+                        }
+                        for (int64_t p = i0; p < i1; ++p)
+                            for (int64_t q = j0; q < j1; ++q) any |= jacobi_pair(a, res.v, nrm.data(), p, q, tol);
                     }  // implicit barrier
-                    const int64_t last = lp[kk - 1];
-                    for (int64_t i = kk - 1; i > 1; --i) lp[i] = lp[i - 1];
+                    const int64_t last = lp[nblk - 1];
+                    for (int64_t i = nblk - 1; i > 1; --i) lp[i] = lp[i - 1];
                     lp[1] = last;
                 }
 #pragma omp single
@@ -264,6 +285,110 @@ JacobiSvdResult jacobi_svd(DenseMatrix a, int64_t max_sweeps) {
         for (int64_t i = 0; i < k; ++i) vs(i, j) = res.v(i, src);
     }
     res.v = std::move(vs);
+    return res;
+}
+
+namespace {
+
+// Householder QR with column pivoting, W P = Q R (LAPACK dgeqp2 semantics: largest remaining
+// column norm first, norms downdated with the cancellation guard of dlaqp2).  On return `a`
+// holds R on and above the diagonal and the reflectors' tails below; tau / perm as in dgeqp2.
+void householder_qrcp(DenseMatrix& a, std::vector<double>& tau, std::vector<int64_t>& perm) {
+    const int64_t m = a.rows(), k = a.cols();
+    tau.assign(static_cast<size_t>(k), 0.0);
+    perm.resize(static_cast<size_t>(k));
+    std::iota(perm.begin(), perm.end(), 0);
+    std::vector<double> vn1(static_cast<size_t>(k)), vn2(static_cast<size_t>(k));
+    for (int64_t j = 0; j < k; ++j) vn1[j] = vn2[j] = std::sqrt(dot_avx(a.col(j), a.col(j), m));
+    const double tol3z = std::sqrt(std::numeric_limits<double>::epsilon());
+    for (int64_t j = 0; j < k && j < m; ++j) {
+        const int64_t pvt = j + (std::max_element(vn1.begin() + j, vn1.end()) - (vn1.begin() + j));
+        if (pvt != j) {
+            std::swap_ranges(a.col(pvt), a.col(pvt) + m, a.col(j));
+            std::swap(perm[pvt], perm[j]);
+            vn1[pvt] = vn1[j];
+            vn2[pvt] = vn2[j];
+        }
+        double* v = a.col(j) + j;  // v = [1; a(j+1:m, j)] after scaling
+        const int64_t len = m - j;
+        const double alpha = v[0];
+        const double xnorm = len > 1 ? std::sqrt(dot_avx(v + 1, v + 1, len - 1)) : 0.0;
+        double t = 0.0;
+        if (xnorm != 0.0) {
+            const double beta = -std::copysign(std::hypot(alpha, xnorm), alpha);
+            t = (beta - alpha) / beta;
+            const double sc = 1.0 / (alpha - beta);
+            for (int64_t i = 1; i < len; ++i) v[i] *= sc;
+            v[0] = beta;
+        }
+        tau[j] = t;
+        if (t != 0.0) {
+#pragma omp parallel for schedule(static) if ((k - j) * len > 16384)
+            for (int64_t c = j + 1; c < k; ++c) {
+                double* ac = a.col(c) + j;
+                const double w = t * (ac[0] + (len > 1 ? dot_avx(v + 1, ac + 1, len - 1) : 0.0));
+                ac[0] -= w;
+                for (int64_t i = 1; i < len; ++i) ac[i] -= w * v[i];
+            }
+        }
+        for (int64_t c = j + 1; c < k; ++c) {
+            if (vn1[c] == 0.0) continue;
+            double temp = std::fabs(a(j, c)) / vn1[c];
+            temp = std::max(0.0, 1.0 - temp * temp);
+            const double r = vn1[c] / vn2[c];
+            if (temp * r * r <= tol3z) {
+                const int64_t rest = m - j - 1;
+                vn1[c] = rest > 0 ? std::sqrt(dot_avx(a.col(c) + j + 1, a.col(c) + j + 1, rest)) : 0.0;
+                vn2[c] = vn1[c];
+            } else {
+                vn1[c] *= std::sqrt(temp);
+            }
+        }
+    }
+}
+
+}  // namespace
+
+// One-sided Jacobi SVD with QR preconditioning (Drmac & Veselic): W P = Q R, then the same
+// one-sided Jacobi (rotation formula, 1e-15 test, sweep cap) on X = R^T, whose columns are
+// graded and nearly orthogonal -- a few sweeps instead of ~15 at d = 320.  X V_x = U_x S gives
+// W = (Q V_x) S (P U_x)^T.  Same outputs as jacobi_svd (sigma ascending, u, v).
+JacobiSvdResult jacobi_svd_qr(const DenseMatrix& w, int64_t max_sweeps) {
+    const int64_t m = w.rows(), k = w.cols();
+    require(m == k, "jacobi_svd_qr: square input expected");
+    DenseMatrix a = w;
+    std::vector<double> tau;
+    std::vector<int64_t> perm;
+    householder_qrcp(a, tau, perm);
+    DenseMatrix x(k, k);  // X = R^T (lower triangular)
+    for (int64_t j = 0; j < k; ++j)
+        for (int64_t i = j; i < k; ++i) x(i, j) = a(j, i);
+    JacobiSvdResult jx = jacobi_svd_tol(std::move(x), max_sweeps, 1e-15);
+    // left vectors of W: Q V_x, Q = H_0 H_1 ... H_{k-1} applied to V_x (columns independent)
+    DenseMatrix u = std::move(jx.v);
+#pragma omp parallel for schedule(static)
+    for (int64_t c = 0; c < k; ++c) {
+        double* uc = u.col(c);
+        for (int64_t j = k - 1; j >= 0; --j) {
+            if (tau[j] == 0.0) continue;
+            const double* v = a.col(j) + j;
+            const int64_t len = m - j;
+            double s = uc[j];
+            for (int64_t i = 1; i < len; ++i) s += v[i] * uc[j + i];
+            s *= tau[j];
+            uc[j] -= s;
+            for (int64_t i = 1; i < len; ++i) uc[j + i] -= s * v[i];
+        }
+    }
+    // right vectors of W: P U_x (row perm[i] of the result is row i of U_x)
+    JacobiSvdResult res;
+    res.sigma = std::move(jx.sigma);
+    res.converged = jx.converged;
+    res.sweeps = jx.sweeps;
+    res.v = DenseMatrix(k, k);
+    for (int64_t j = 0; j < k; ++j)
+        for (int64_t i = 0; i < k; ++i) res.v(perm[i], j) = jx.u(i, j);
+    res.u = std::move(u);
     return res;
 }
 
@@ -328,7 +453,13 @@ SmallEigenSolution solve_small_lrep(const ProjectedLrep& p, int64_t k) {
     require(p.chol_k.rows() == p.d && p.chol_m.rows() == p.d, "solve_small_lrep: missing Cholesky factors");
     const DenseMatrix& l = p.chol_k;
     const DenseMatrix& r = p.chol_m;
-    JacobiSvdResult svd = jacobi_svd(matmul_tn(l, r));
+    // d >= 96 (configs 3/5: d = 320): QR-preconditioned Jacobi, a few sweeps instead of ~15
+    static const bool dbg = std::getenv("BOSP_DEBUG") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
+    JacobiSvdResult svd = p.d >= 96 ? jacobi_svd_qr(matmul_tn(l, r), 40) : jacobi_svd(matmul_tn(l, r));
+    if (dbg)
+        std::fprintf(stderr, "[bosp] small svd d=%lld sweeps=%lld %.2f ms\n", (long long)p.d, (long long)svd.sweeps,
+                     std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() * 1e3);
     const double smax = svd.sigma.empty() ? 0.0 : svd.sigma.back();
     for (double s : svd.sigma)
         if (s < 1e-14 * smax)

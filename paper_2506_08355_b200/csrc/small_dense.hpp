@@ -58,6 +58,11 @@ struct JacobiSvdResult {
 // dense_kernels.cpp:30-113; the sweep is executed in a parallel round-robin ordering so that
 // column pairs of one round rotate concurrently (threads when d is large).
 JacobiSvdResult jacobi_svd(DenseMatrix a, int64_t max_sweeps = 40);
+// The same with the orthogonality test |x^T y| <= tol ||x|| ||y|| (jacobi_svd: tol = 1e-15).
+JacobiSvdResult jacobi_svd_tol(DenseMatrix a, int64_t max_sweeps, double tol);
+// Square W: QR-preconditioned one-sided Jacobi (Householder QR with column pivoting, then the
+// same Jacobi on R^T); used by solve_small_lrep for d >= 96.
+JacobiSvdResult jacobi_svd_qr(const DenseMatrix& w, int64_t max_sweeps = 40);
 double spectral_norm(const DenseMatrix& a);
 DenseMatrix lu_inverse(const DenseMatrix& a);
 
