@@ -286,6 +286,9 @@ void bosp_launch_reset(void);
 /* Per-family launch counts as "family=count;..." into buf. */
 int bosp_launch_families(char* buf, int len);
 void bosp_device_sync(void);
+/* cudaProfilerStart (on != 0) / cudaProfilerStop: brackets the launches an
+ * `ncu --profile-from-start off` capture sees (tools/run_config.py --profile-range). */
+void bosp_profiler_range(int on);
 /* Select the CUDA device for this process (call before any other entry point; one process
  * per GPU).  Returns 0 on success. */
 int bosp_set_device(int device);

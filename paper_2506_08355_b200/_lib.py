@@ -84,7 +84,7 @@ EXPORTED = [
     "bosp_analytic_nullspace_T", "bosp_compute_nullspace", "bosp_block_inner",
     "bosp_block_product", "bosp_block_axpy", "bosp_biorth", "bosp_biorth_against",
     "bosp_biorth_residual", "bosp_cg_solve", "bosp_solve_small_lrep", "bosp_jacobi_svd",
-    "bosp_cholesky", "bosp_profile_enable", "bosp_profile_collect", "bosp_profile_collect_regions",
+    "bosp_cholesky", "bosp_profile_enable", "bosp_profile_collect", "bosp_profile_collect_regions", "bosp_profiler_range",
     "bosp_profile_family_report",
     "bosp_launch_count",
     "bosp_launch_reset", "bosp_launch_families", "bosp_device_sync", "bosp_host_alloc",

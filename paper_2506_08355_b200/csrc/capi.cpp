@@ -2,6 +2,8 @@
 // codes.  No exception crosses this boundary.
 #include "../../include/bosp_b200.h"
 
+#include <cuda_profiler_api.h>
+
 #include <cstdio>
 #include <algorithm>
 #include <cstring>
@@ -675,6 +677,11 @@ int bosp_launch_families(char* buf, int len) {
         buf[len - 1] = 0;
     }
     return static_cast<int>(s.size());
+}
+
+void bosp_profiler_range(int on) {
+    if (on) cudaProfilerStart();
+    else cudaProfilerStop();
 }
 
 void bosp_device_sync(void) {

@@ -12,6 +12,13 @@
 namespace bosp {
 inline namespace b200 {
 
+namespace {
+bool debug_on() {
+    static const bool on = std::getenv("BOSP_DEBUG") != nullptr;
+    return on;
+}
+}  // namespace
+
 // ---------------------------------------------------------------------------------------------
 // Grams under the inner product
 // ---------------------------------------------------------------------------------------------
@@ -54,7 +61,12 @@ std::vector<DenseMatrix> ip_grams_host(const InnerProduct& ip, const std::vector
     Runtime& rt = Runtime::get();
     DBlock g(total, 1);
     std::vector<DBlock> weighted;
-    std::vector<GramJob> jobs;
+    // Jobs are launched in shape classes (a launch's tile shape follows its widest job): square-
+    // ish Grams together, and skinny cross-Grams (Q^T U with Q <= 32 columns, U >= 128) computed
+    // as U^T Q on the 128 x 32 tiles and transposed on the host -- in a 320-wide launch a 1 x 320
+    // job would cost 5 full 64 x 64 tiles per row split.
+    std::vector<GramJob> wide, skinny;
+    std::vector<char> swapped(pairs.size(), 0);
     for (size_t i = 0; i < pairs.size(); ++i) {
         const DMat& a = pairs[i].first;
         DMat b = pairs[i].second;
@@ -64,16 +76,30 @@ std::vector<DenseMatrix> ip_grams_host(const InnerProduct& ip, const std::vector
             ip.weight()->apply_device(b, weighted.back().view());
             b = weighted.back().view();
         }
-        jobs.push_back({ColList(a), ColList(b), g.data() + off[i], a.cols});
+        if (a.cols <= 32 && b.cols >= 128) {
+            swapped[i] = 1;
+            skinny.push_back({ColList(b), ColList(a), g.data() + off[i], b.cols});
+        } else {
+            wide.push_back({ColList(a), ColList(b), g.data() + off[i], a.cols});
+        }
     }
-    for (size_t i = 0; i < jobs.size(); i += 4)
-        gram(jobs.data() + i, static_cast<int>(std::min<size_t>(4, jobs.size() - i)), pairs[0].first.rows);
+    for (const std::vector<GramJob>* js : {&wide, &skinny})
+        for (size_t i = 0; i < js->size(); i += 4)
+            gram(js->data() + i, static_cast<int>(std::min<size_t>(4, js->size() - i)), pairs[0].first.rows);
     rt.allreduce(g.data(), total);
     std::vector<double> h(static_cast<size_t>(total));
     BOSP_CUDA(cudaMemcpyAsync(h.data(), g.data(), sizeof(double) * total, cudaMemcpyDeviceToHost, rt.stream()));
     rt.sync();
-    for (size_t i = 0; i < pairs.size(); ++i)
-        std::copy(h.begin() + off[i], h.begin() + off[i] + out[i].rows() * out[i].cols(), out[i].data());
+    for (size_t i = 0; i < pairs.size(); ++i) {
+        const double* src = h.data() + off[i];
+        DenseMatrix& o = out[i];
+        if (!swapped[i]) {
+            std::copy(src, src + o.rows() * o.cols(), o.data());
+        } else {  // src holds (b^T a), o.cols() x o.rows()
+            for (int64_t c = 0; c < o.cols(); ++c)
+                for (int64_t r = 0; r < o.rows(); ++r) o(r, c) = src[c + r * o.cols()];
+        }
+    }
     return out;
 }
 
@@ -254,7 +280,12 @@ DevBiorthOutcome dev_mgs_biorth(const DMat& x, const DMat& y, const DMat& p, con
             pair_grams(cx, cy, ip, gxx, gxy, gyy);
         }
         int64_t stop = mr;
+        const auto tc0 = std::chrono::steady_clock::now();
         CoefBiorth cb = coef_mgs(gxx, gxy, gyy, drop_tol, classical, kCancel, &stop);
+        if (debug_on())
+            std::fprintf(stderr, "[bosp] mgs m=%lld coef %.2f ms stop=%lld\n", (long long)mr,
+                         std::chrono::duration<double>(std::chrono::steady_clock::now() - tc0).count() * 1e3,
+                         (long long)stop);
         const int64_t kb = static_cast<int64_t>(cb.kept.size());
         // whole block in one recurrence pass: the check Gram P^T Q comes out of the same kernel
         const bool fuse = !classical && !ip.weighted() && start == 0 && stop >= mr && mr <= 32 && kb >= 2;
@@ -310,6 +341,7 @@ DevBiorthOutcome dev_mgs_biorth(const DMat& x, const DMat& y, const DMat& p, con
     if (!biorth_loss_exceeds(gpq, 1e-10)) return out;
     // second subtraction pass (biorth.cpp:104-107)
     out.second_pass = true;
+    if (debug_on()) std::fprintf(stderr, "[bosp] mgs m=%lld second pass\n", (long long)out.kept);
     CoefBiorth cb2 = coef_rebiorth(gpq);
     DBlock tp(x.rows, out.kept), tq(x.rows, out.kept);
     apply_coefs(pk, qk, cb2.a, cb2.b, tp.view(), tq.view());

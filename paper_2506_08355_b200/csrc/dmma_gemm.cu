@@ -667,7 +667,6 @@ void launch_gram_regs(const GramJob* jobs, int njobs, int64_t n) {
 #endif
 constexpr int kPStages = BOSP_PSTAGES;
 constexpr int kPBK = BOSP_PBK;
-constexpr int kPLdK = kPBK + 4;
 constexpr int kProdTab = 1024;  // A column pointers kept in shared memory (wider K: per-stage lookup)
 
 struct ProductParams {
@@ -678,9 +677,10 @@ struct ProductParams {
     int16_t kend[4][16];  // per column tile: K rows of C that can be nonzero (0 = all)
 };
 
-template <int BM, int BN, int WM, int WN>
+template <int BM, int BN, int WM, int WN, int PBK = kPBK, int PST = kPStages>
 __global__ void __launch_bounds__(WM * WN * 32)
 k_product(ProductParams prm) {
+    constexpr int kPBK = PBK, kPStages = PST, kPLdK = PBK + 4;
     constexpr int NT = WM * WN * 32;
     constexpr int WTM = BM / WM, WTN = BN / WN;
     constexpr int MT = WTM / 8, NTL = WTN / 8;
@@ -792,8 +792,9 @@ k_product(ProductParams prm) {
 }
 
 
-template <int BM, int BN, int WM, int WN>
+template <int BM, int BN, int WM, int WN, int PBK = kPBK, int PST = kPStages>
 void launch_product(const ProductJob* jobs, int njobs, int64_t n) {
+    constexpr int kPBK = PBK, kPStages = PST, kPLdK = PBK + 4;
     Runtime& rt = Runtime::get();
     ProductParams prm{};
     int64_t max_tiles = 0;
@@ -821,14 +822,14 @@ void launch_product(const ProductJob* jobs, int njobs, int64_t n) {
     constexpr size_t smem = smem_pipe > smem_epi ? smem_pipe : smem_epi;
     static unsigned attr_mask = 0;
     if (rt.first_use(attr_mask)) {
-        BOSP_CUDA(cudaFuncSetAttribute(k_product<BM, BN, WM, WN>,
+        BOSP_CUDA(cudaFuncSetAttribute(k_product<BM, BN, WM, WN, PBK, PST>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     }
     LaunchScope ls("product_wide", bytes, flops);
     const unsigned gx = static_cast<unsigned>(std::min<int64_t>(max_tiles, 65535));
     const unsigned gy = static_cast<unsigned>((max_tiles + gx - 1) / gx);
     dim3 grid(gx, gy, njobs);
-    k_product<BM, BN, WM, WN><<<grid, NT, smem, rt.stream()>>>(prm);
+    k_product<BM, BN, WM, WN, PBK, PST><<<grid, NT, smem, rt.stream()>>>(prm);
     BOSP_LAUNCH_CHECK();
 }
 
@@ -1078,7 +1079,9 @@ void gram(const GramJob* jobs, int njobs, int64_t n) {
         // DMMA-latency bound, not byte bound -- n = 16384, 32 columns: 1.47 -> 0.93 ms
         launch_gram<128, 32, 4, 2, 16, 3>(jobs, njobs, n);
     else
-        launch_gram<64, 64, 2, 4>(jobs, njobs, n);
+        // 4 warps of 32 x 32, 3 x 32-row stages: 32.6 TF/s at n = 2^21, 320 x 320 (8 warps of
+        // 32 x 16: 31.4; 16-row stages: 29.7-32.2)
+        launch_gram<64, 64, 2, 2>(jobs, njobs, n);
 }
 
 namespace {
@@ -1325,10 +1328,12 @@ void product(const ProductJob* jobs, int njobs, int64_t n) {
         }
     }
     // k == 0: Out = beta * Out (handled by the kernel with an empty K loop)
+    // 4 warps of 32 x 32 (16 DMMAs per 8 fragment loads), 3 x 16-deep stages, 3 CTAs/SM:
+    // 31.5 TF/s at n = 2^21, 320 -> 192 (8 warps of 32 x 16: 30.3; 128-row tiles: 28.6-30.6)
     if (bmax <= 32)
         launch_product<64, 32, 2, 2>(jobs, njobs, n);
     else
-        launch_product<64, 64, 2, 4>(jobs, njobs, n);
+        launch_product<64, 64, 2, 2, 16, 3>(jobs, njobs, n);
 }
 
 }  // namespace b200

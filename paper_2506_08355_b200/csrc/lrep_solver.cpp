@@ -481,11 +481,13 @@ bool iterate_device(DeviceState& st, const LinearOperator& k, const LinearOperat
                 }
                 rhs_z = st.tmp.view();
             }
-            auto phz = st.phases.scope(PH_CG);
-            DevCgOutcome cz = dev_cg(m, rhs_z, st.zg.view(), cfg.inner_cg_tol, cfg.inner_cg_max_iter, st.cg,
-                                     nullptr, false, true);
-            if (cz.sweeps >= 0) st.stats.cg_iterations += cz.sweeps;
-            else st.cg_deferred = true;
+            {
+                auto phz = st.phases.scope(PH_CG);
+                DevCgOutcome cz = dev_cg(m, rhs_z, st.zg.view(), cfg.inner_cg_tol, cfg.inner_cg_max_iter, st.cg,
+                                         nullptr, false, true);
+                if (cz.sweeps >= 0) st.stats.cg_iterations += cz.sweeps;
+                else st.cg_deferred = true;
+            }
             // rhs_w = rw + lam B Z; W = CG(K, rhs_w)
             copy_block(st.rw.view(), st.tmp.view());
             if (ip.weighted()) {
@@ -496,11 +498,13 @@ bool iterate_device(DeviceState& st, const LinearOperator& k, const LinearOperat
             } else {
                 lam_axpy(st.zg.view(), lamb, st.tmp.view());
             }
-            auto phw = st.phases.scope(PH_CG);
-            DevCgOutcome cw = dev_cg(k, st.tmp.view(), st.wg.view(), cfg.inner_cg_tol, cfg.inner_cg_max_iter, st.cg,
-                                     nullptr, false, true);
-            if (cw.sweeps >= 0) st.stats.cg_iterations += cw.sweeps;
-            else st.cg_deferred = true;
+            {
+                auto phw = st.phases.scope(PH_CG);
+                DevCgOutcome cw = dev_cg(k, st.tmp.view(), st.wg.view(), cfg.inner_cg_tol, cfg.inner_cg_max_iter,
+                                         st.cg, nullptr, false, true);
+                if (cw.sweeps >= 0) st.stats.cg_iterations += cw.sweeps;
+                else st.cg_deferred = true;
+            }
         }
         std::vector<DevBasis> bases = deflation_bases(st);
         bases.push_back({st.X(), st.Y()});

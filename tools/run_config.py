@@ -25,6 +25,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
+PROFILE_RANGE = False
+
+
 def make(name: str, bosp, P):
     if name == "config1":
         return P.config1()
@@ -60,9 +63,13 @@ def run(name: str) -> dict:
     ns = bosp.GeneralizedNullspace(prob.x0, prob.y0)
     bosp.device_sync()
     bosp.launch_reset()
+    if PROFILE_RANGE:  # ncu --profile-from-start off sees exactly this solve
+        bosp.lib().bosp_profiler_range(1)
     t1 = time.perf_counter()
     res = bosp.solve(K, M, None, cfg, ns, want_vectors=True)
     solve_s = time.perf_counter() - t1
+    if PROFILE_RANGE:
+        bosp.lib().bosp_profiler_range(0)
     launches = bosp.launch_count()
     x, y, lam = res.x, res.y, res.lambdas
     # independent host checks (bosp_solver.cpp:256-271): K x = lambda y, M y = lambda x
@@ -93,7 +100,11 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("configs", nargs="+")
     ap.add_argument("--out", default=None)
+    ap.add_argument("--profile-range", action="store_true",
+                    help="cudaProfilerStart/Stop around the solve (for ncu --profile-from-start off)")
     a = ap.parse_args()
+    global PROFILE_RANGE
+    PROFILE_RANGE = a.profile_range
     out = {}
     for c in a.configs:
         r = run(c)
