@@ -540,9 +540,48 @@ double biorth_loss(const DenseMatrix& g) {
 
 bool biorth_loss_exceeds(const DenseMatrix& g, double thr) {
     DenseMatrix d = g;
-    for (int64_t i = 0; i < d.rows(); ++i) d(i, i) -= 1.0;
+    const int64_t m = d.rows(), k = d.cols();
+    for (int64_t i = 0; i < std::min(m, k); ++i) d(i, i) -= 1.0;
     if (d.frobenius_norm() <= thr) return false;  // ||.||_2 <= ||.||_F settles it exactly
-    return spectral_norm(d) > thr;
+    // ||D||_2 <= sqrt(||D||_1 ||D||_inf) settles "no" as exactly
+    double n1 = 0.0, ninf = 0.0;
+    std::vector<double> rows(static_cast<size_t>(m), 0.0);
+    for (int64_t j = 0; j < k; ++j) {
+        double c = 0.0;
+        for (int64_t i = 0; i < m; ++i) {
+            c += std::fabs(d(i, j));
+            rows[i] += std::fabs(d(i, j));
+        }
+        n1 = std::max(n1, c);
+    }
+    for (double r : rows) ninf = std::max(ninf, r);
+    if (std::sqrt(n1 * ninf) <= thr) return false;
+    // power iteration on D^T D: every ||D v|| / ||v|| is a lower bound of ||D||_2, so crossing
+    // thr proves "yes" (the common case: a clearly needed second pass) without the O(d^3) SVD
+    std::vector<double> v(static_cast<size_t>(k), 1.0), w(static_cast<size_t>(m));
+    for (int it = 0; it < 30; ++it) {
+        double vv = 0.0;
+        for (double x : v) vv += x * x;
+        if (vv == 0.0) break;
+        std::fill(w.begin(), w.end(), 0.0);
+        for (int64_t j = 0; j < k; ++j) {
+            const double vj = v[j];
+            for (int64_t i = 0; i < m; ++i) w[i] += d(i, j) * vj;
+        }
+        double ww = 0.0;
+        for (double x : w) ww += x * x;
+        if (std::sqrt(ww / vv) > thr) return true;
+        for (int64_t j = 0; j < k; ++j) {
+            double s = 0.0;
+            for (int64_t i = 0; i < m; ++i) s += d(i, j) * w[i];
+            v[j] = s;
+        }
+        double nv = 0.0;
+        for (double x : v) nv = std::max(nv, std::fabs(x));
+        if (nv == 0.0) break;
+        for (double& x : v) x /= nv;
+    }
+    return spectral_norm(d) > thr;  // undecided by the bounds: the exact Jacobi spectral norm
 }
 
 HostBiorth host_mgs_biorth(const DenseMatrix& x, const DenseMatrix& y, double drop_tol) {

@@ -348,8 +348,11 @@ __global__ void __launch_bounds__(kRows) k_stencil(StencilDev st, const double* 
 // Whole-grid stencil with nx even: one thread per pair of x-adjacent rows (i, i+1), i even --
 // half the index arithmetic (two 32-bit divisions per pair), 16-byte loads for the centre and the
 // y/z neighbours, 8-byte loads for the outer x neighbours, one 16-byte store.
-template <int CB, bool DOT>
-__global__ void __launch_bounds__(kRows) k_stencil2(StencilDev st, const double* __restrict__ x,
+// 6 resident blocks (40 registers): the kernel is load-latency bound, and occupancy beats
+// issuing all CB x 7 loads up front (measured: 616 -> 457 us per 64-column apply at 128^3, 4.7
+// TB/s; two-phase loads at 72-128 registers: 540-835 us).
+template <int CB, bool DOT, int MINB = 6>
+__global__ void __launch_bounds__(kRows, MINB) k_stencil2(StencilDev st, const double* __restrict__ x,
                                                      int64_t ldx, double* __restrict__ y, int64_t ldy,
                                                      int ncols, KTimer tm, DotOut dots) {
     tm.start();
