@@ -421,7 +421,7 @@ void launch_gram(const GramJob* jobs, int njobs, int64_t n) {
     {
         // families: the wide Rayleigh-Ritz / repair Grams (64 x 64 tiles), the dense operator's
         // A x (128 x 32 tiles over the stored A^T), and the small tiled Grams
-        const char* fam = (BM == 64 && BN == 64) ? "gram_wide" : (BM == 128 && BN == 32) ? "dense_apply" : "gram";
+        const char* fam = (BM == 64 && BN == 64) ? "gram_wide" : "gram";
         LaunchScope ls(fam, bytes, flops);
         dim3 grid(max_tiles, prm.splits, njobs);
         k_gram<BM, BN, WM, WN, GBK, GST><<<grid, NT, smem, rt.stream()>>>(prm);
@@ -1074,10 +1074,10 @@ void gram(const GramJob* jobs, int njobs, int64_t n) {
         launch_gram<32, 32, 2, 2>(jobs, njobs, n);
     else if (bmax <= 32 && amax >= 128)
         // many output rows, <= 32 columns (the dense operator's A x = (A^T)^T x at the CG's
-        // widths): 128 x 32 tiles, the same 32 x 16 warp tiles, no padding of b to 64.
-        // 16-row stages keep two 8-warp CTAs per SM (the 32-row ring fits one): the tile is
-        // DMMA-latency bound, not byte bound -- n = 16384, 32 columns: 1.47 -> 0.93 ms
-        launch_gram<128, 32, 4, 2, 16, 3>(jobs, njobs, n);
+        // widths): 128 x 32 tiles, 4 warps of 32 x 32, 2 x 32-row stages, no padding of b to
+        // 64 -- n = 16384, 32 columns: 0.73 ms (23.7 TF/s; 8 warps of 32 x 16: 23.0, 64 x 32
+        // tiles: 19-21)
+        launch_gram<128, 32, 4, 1, 32, 2>(jobs, njobs, n);
     else
         // 4 warps of 32 x 32, 3 x 32-row stages: 32.6 TF/s at n = 2^21, 320 x 320 (8 warps of
         // 32 x 16: 31.4; 16-row stages: 29.7-32.2)

@@ -133,6 +133,7 @@ public:
         Runtime::get().sync();
     }
     void apply(const DMat& x, const DMat& y) const override {
+        FamilyScope fs("dense_apply");
         gram(ColList(t_.view()), ColList(x), x.rows, y.p, y.ld);
     }
 

@@ -273,8 +273,14 @@ Runtime::ProfReport Runtime::prof_collect() {
     return r;
 }
 
+FamilyScope::FamilyScope(const char* fam) : prev(Runtime::get().family_override) {
+    Runtime::get().family_override = fam;
+}
+FamilyScope::~FamilyScope() { Runtime::get().family_override = prev; }
+
 LaunchScope::LaunchScope(const char* fam, double bytes, double flops, bool events) : family(fam) {
     Runtime& rt = Runtime::get();
+    if (rt.family_override) family = fam = rt.family_override;
     rt.count_launch(fam);
     timed = events && rt.prof_on(fam);
     if (timed) rt.prof_begin(fam, bytes, flops);

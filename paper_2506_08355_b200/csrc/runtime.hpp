@@ -96,6 +96,8 @@ public:
 
     // Kernel accounting (gpu_launches) and optional CUDA-event timing of one kernel family.
     void count_launch(const char* family);
+    // While set, every launch is attributed to this family (an operator's apply: "dense_apply")
+    const char* family_override = nullptr;
     int64_t launches() const { return launches_; }
     void reset_launches() { launches_ = 0; family_launches_.clear(); }
     const std::map<std::string, int64_t>& family_launches() const { return family_launches_; }
@@ -183,6 +185,13 @@ private:
 };
 
 // RAII: times one launch of `family` when profiling is on for it; always counts the launch.
+// RAII: attribute the launches of a scope (e.g. one operator apply) to one family.
+struct FamilyScope {
+    const char* prev;
+    explicit FamilyScope(const char* fam);
+    ~FamilyScope();
+};
+
 struct LaunchScope {
     const char* family;
     bool timed;
