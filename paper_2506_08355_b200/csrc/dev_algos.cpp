@@ -621,7 +621,7 @@ DevCgOutcome dev_cg(const LinearOperator& a, const DMat& rhs, const DMat& x, dou
                 rt.set_capture_sink(&g->start_launches);
                 BOSP_CUDA(cudaStreamBeginCaptureToGraph(rt.stream(), g->graph, nullptr, nullptr, 0,
                                                         cudaStreamCaptureModeRelaxed));
-                rt.timer_reserve(max_iter);  // one memset node for every timed launch below
+                rt.timer_reserve(3 * max_iter + 2);  // one memset node for every timed launch below
                 cg_start(rhsg, xg, rg, pg, sc, tol, mi);
                 for (int64_t it = 0; it < max_iter; ++it) cg_iteration(a, xg, rg, pg, apg, sc, ws, tol, mi);
                 rt.timer_reserve(0);

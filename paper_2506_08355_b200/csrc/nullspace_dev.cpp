@@ -1,6 +1,8 @@
-// Generalized nullspace detection on the device (nullspace.cpp:14-193 restated): power
-// iteration for ||K||, shifted block inverse iteration with the batched CG, CG for M y = B x
-// and the Cholesky normalisation X0 = X C^-1, Y0 = Y C^-1.  One-time setup, not the hot loop.
+// Generalized nullspace detection on the device (nullspace.cpp:14-193): power iteration for
+// ||K||, shifted block inverse iteration with the batched CG -- made robust by a Rayleigh-Ritz
+// step per sweep and an early shift schedule (the reference misdetects
+// rank 0 on T(-1)/T(0) at n >= 1000) -- CG for M y = B x and the Cholesky normalisation
+// X0 = X C^-1, Y0 = Y C^-1.  One-time setup, not the hot loop.
 #include <cmath>
 #include <limits>
 
@@ -102,6 +104,20 @@ GeneralizedNullspace compute_nullspace(const LinearOperator& k, const LinearOper
             copy_block(tmp.view(), v.view());
             orthonormalize(v.view());
             k.apply_device(v.view(), kv.view());
+            // Rayleigh-Ritz on the block (new vs nullspace.cpp:78-93, which takes per-vector
+            // Rayleigh quotients): a null direction spread over several iterates shows up as one
+            // Ritz value ~ 0 instead of several mixed quotients above zero_thresh -- the reason
+            // the reference misdetects rank 0 on T(-1)/T(0) at n >= 1000
+            {
+                DenseMatrix h = ip_gram_host(InnerProduct{}, v.view(), kv.view()).symmetrized();
+                JacobiSvdResult e = jacobi_svd(h);  // H is PSD: singular = eigen pairs, ascending
+                DBlock z(block, block);
+                to_device(e.v.data(), block, block, block, z.view());
+                product(ColList(v.view()), z.data(), z.ld(), static_cast<int32_t>(block), tmp.view(), 1.0, 0.0);
+                copy_block(tmp.view(), v.view());
+                product(ColList(kv.view()), z.data(), z.ld(), static_cast<int32_t>(block), tmp.view(), 1.0, 0.0);
+                copy_block(tmp.view(), kv.view());
+            }
             col_dots(v.view(), kv.view(), sc.data());
             to_host(sc.cols(0, 1), rayleigh.data(), block);
             // residual ||K v - theta v||
@@ -116,12 +132,15 @@ GeneralizedNullspace compute_nullspace(const LinearOperator& k, const LinearOper
             for (auto& r : resid) r = std::sqrt(r);
 
             double theta_min = std::numeric_limits<double>::infinity();
+            double theta_pos = std::numeric_limits<double>::infinity();  // smallest non-null Ritz value
             bool null_converged = true, any_null = false;
             for (int64_t j = 0; j < block; ++j) {
                 theta_min = std::min(theta_min, std::fabs(rayleigh[j]));
                 if (std::fabs(rayleigh[j]) < zero_thresh) {
                     any_null = true;
                     if (resid[j] > zero_thresh) null_converged = false;
+                } else {
+                    theta_pos = std::min(theta_pos, std::fabs(rayleigh[j]));
                 }
             }
             if (any_null && null_converged && outer >= 2) break;
@@ -134,8 +153,13 @@ GeneralizedNullspace compute_nullspace(const LinearOperator& k, const LinearOper
                     std::fabs(theta - prev_min) < 1e-4 * theta)
                     break;
             }
-            if (outer >= 8 && std::fabs(theta_min - prev_min) < 1e-3 * std::max(theta_min, 1e-300)) {
-                const double target = std::max({theta_min / 10.0, 1e-14 * knorm, 1e-300});
+            // Shift a decade below the smallest non-null Ritz value from the third sweep on
+            // (the reference moves it only after a stall, ~1e-3 relative change, which at
+            // n = 4000 never happens within 300 sweeps): the null directions then gain ~10x
+            // per sweep over the smallest positive eigenvalue.  The batched CG solves
+            // (K + sigma I) to 1e-10 regardless of the conditioning.
+            if (outer >= 2 && std::isfinite(theta_pos)) {
+                const double target = std::max({theta_pos / 10.0, 1e-14 * knorm, 1e-300});
                 if (target < sigma / 2.0) {
                     sigma = target;
                     shifted = LinearOperator::shifted(k, sigma);

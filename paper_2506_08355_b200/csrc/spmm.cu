@@ -12,6 +12,7 @@
 
 #include "runtime.hpp"
 #include "sparse_ops.hpp"
+#include "ktimer.cuh"
 
 namespace bosp {
 inline namespace b200 {
@@ -19,42 +20,6 @@ inline namespace b200 {
 namespace {
 
 constexpr int kRows = 256;  // threads per block = rows per block (8 SELL slices)
-
-__device__ __forceinline__ unsigned long long gtimer() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
-
-// Device-clock timing of one launch (Runtime::timer_begin): slot[0] = max(~start) -> earliest
-// start, slot[1] = max(end) -> latest end, slot[2] = columns applied (reported by block 0).
-struct KTimer {
-    unsigned long long* slot;
-    __device__ __forceinline__ void start() const {
-        if (slot && threadIdx.x == 0) atomicMax(&slot[0], ~gtimer());
-    }
-    __device__ __forceinline__ void columns(const int* active, int j0, int n, int ncols_total) const {
-        // one block reports the applied column count of the whole launch
-        if (!slot || threadIdx.x != 0 || blockIdx.x != 0 || blockIdx.y != 0) return;
-        (void)j0;
-        (void)n;
-        int c = ncols_total;
-        if (active) {
-            c = 0;
-            for (int j = 0; j < ncols_total; ++j) c += active[j] != 0;
-        }
-        slot[2] = static_cast<unsigned long long>(c);
-    }
-    __device__ __forceinline__ void stop() const {
-        if (slot) {
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                __threadfence();
-                atomicMax(&slot[1], gtimer());
-            }
-        }
-    }
-};
 
 // Occupancy floor of the masked/halo SELL kernel (the CG's SpMM): it is memory-latency bound
 // and 4 resident blocks (64 registers) measured best for the batched CG on config 2.

@@ -9,6 +9,7 @@
 #include <cstdlib>
 
 #include "dense_ops.hpp"
+#include "ktimer.cuh"
 #include "runtime.hpp"
 
 namespace bosp {
@@ -44,16 +45,18 @@ __device__ __forceinline__ void block_sum(double (&v)[K], double* sh) {
 template <int K, class F>
 __global__ void __launch_bounds__(kThreads) k_colred(int64_t n, int ncols, int nchunks,
                                                       int64_t chunk, F f, double* partial,
-                                                      unsigned* ticket, double* defer) {
+                                                      unsigned* ticket, double* defer, KTimer tm) {
     __shared__ double sh[(kThreads / 32) * K];
     __shared__ bool last;
     const int j = blockIdx.y;
     const int c = blockIdx.x;
+    tm.start();
     double acc[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) acc[k] = 0.0;
     f.prologue(j);
     if (!f.skip(j)) {
+        if (c == 0 && threadIdx.x == 0) tm.add_column();
         // 16-byte accesses: rows in pairs (chunk is even, columns are 256-byte aligned)
         const int64_t r0 = c * chunk;
         const int64_t r1 = min(n, r0 + chunk);
@@ -75,7 +78,10 @@ __global__ void __launch_bounds__(kThreads) k_colred(int64_t n, int ncols, int n
         last = (atomicAdd(ticket, 1u) == total - 1);
     }
     __syncthreads();
-    if (!last) return;
+    if (!last) {
+        tm.stop();
+        return;
+    }
     __threadfence();
     // fold: one warp per column, lanes strided over the chunks (all loads independent), then a
     // fixed shuffle tree -- the tail block finishes in a few L2 round trips, not nchunks
@@ -106,6 +112,7 @@ __global__ void __launch_bounds__(kThreads) k_colred(int64_t n, int ncols, int n
         if (!defer) f.fin_all(ncols);
         *ticket = 0u;
     }
+    tm.stop();
 }
 
 // Epilogue of k_colred on cross-rank sums (one block).
@@ -147,9 +154,11 @@ void launch_colred(const char* family, int64_t n, int ncols, const F& f, double 
     // epilogue on the global sums so every rank sets identical scalars
     double* defer = rt.nranks() > 1 ? partial + static_cast<size_t>(nchunks) * ncols * K : nullptr;
     {
-        LaunchScope ls(family, bytes, 0.0);
+        // device-clock timed (works inside the CG graphs); bytes credited per applied column
+        KTimer tm{rt.timer_begin(family, bytes, 0.0, 0.0, ncols)};
+        LaunchScope ls(family, bytes, 0.0, false);
         dim3 grid(nchunks, ncols);
-        k_colred<K, F><<<grid, kThreads, 0, rt.stream()>>>(n, ncols, nchunks, chunk, f, partial, ticket, defer);
+        k_colred<K, F><<<grid, kThreads, 0, rt.stream()>>>(n, ncols, nchunks, chunk, f, partial, ticket, defer, tm);
         BOSP_LAUNCH_CHECK();
     }
     if (defer) {
@@ -383,14 +392,17 @@ struct CgXrF {
 // ---- element-wise kernels ----------------------------------------------------------------
 // f(i, j) one row, f.pair(i, j) rows i, i+1 (i even, 16-byte accesses).
 template <class F>
-__global__ void __launch_bounds__(kThreads) k_cols(int64_t n, F f) {
+__global__ void __launch_bounds__(kThreads) k_cols(int64_t n, F f, KTimer tm) {
     const int j = blockIdx.y;
     if (f.skip(j)) return;
+    tm.start();
+    if (blockIdx.x == 0 && threadIdx.x == 0) tm.add_column();
     const int64_t npair = n >> 1;
     for (int64_t q = blockIdx.x * static_cast<int64_t>(kThreads) + threadIdx.x; q < npair;
          q += static_cast<int64_t>(gridDim.x) * kThreads)
         f.pair(2 * q, j);
     if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) f(n - 1, j);
+    tm.stop();
 }
 
 template <class F>
@@ -400,8 +412,9 @@ void launch_cols(const char* family, int64_t n, int ncols, const F& f, double by
     const int64_t target = 8LL * rt.sm_count();
     const unsigned gx = static_cast<unsigned>(std::max<int64_t>(
         1, std::min<int64_t>((n / 2 + kThreads - 1) / kThreads, (target + ncols - 1) / ncols)));
-    LaunchScope ls(family, bytes, 0.0);
-    k_cols<F><<<dim3(gx, ncols), kThreads, 0, rt.stream()>>>(n, f);
+    KTimer tm{rt.timer_begin(family, bytes, 0.0, 0.0, ncols)};
+    LaunchScope ls(family, bytes, 0.0, false);
+    k_cols<F><<<dim3(gx, ncols), kThreads, 0, rt.stream()>>>(n, f, tm);
     BOSP_LAUNCH_CHECK();
 }
 

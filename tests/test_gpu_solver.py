@@ -166,6 +166,35 @@ def test_compute_nullspace_small():
     assert np.isclose((ns.x0.T @ ns.y0)[0, 0], 1.0, rtol=1e-10)
 
 
+@pytest.mark.parametrize("n", [1000, 2000, 4000])
+def test_compute_nullspace_robust_large(n):
+    """the reference's detector returns rank 0 for T(-1)/T(0) at n >= 1000
+    (tests/test_oracle.py pins that); the device detector (Rayleigh-Ritz + early shift) finds the
+    analytic one-dimensional nullspace."""
+    k = bosp.LinearOperator.from_csr(P.t_matrix(n, -1.0))
+    m = bosp.LinearOperator.from_csr(P.t_matrix(n, 0.0))
+    ns = bosp.compute_nullspace(k, m)
+    assert ns.r == 1
+    xa, ya = P.analytic_nullspace_T(n)
+    cos = abs(float((xa.T @ ns.x0)[0, 0])) / (np.linalg.norm(ns.x0) * np.linalg.norm(xa))
+    assert abs(cos - 1) < 1e-8
+    assert np.isclose((ns.x0.T @ ns.y0)[0, 0], 1.0, rtol=1e-10)
+    # Y0 = M^-1 X0 (the generalized nullspace pair)
+    t0 = P.t_matrix(n, 0.0).scipy()
+    assert np.linalg.norm(t0 @ ns.y0 - ns.x0) / np.linalg.norm(ns.x0) < 1e-8
+
+
+def test_table3_without_given_nullspace(golden_solves):
+    """Table 3 (T(-1)/T(0), n = 1000) with the nullspace detected on the device instead of
+    passed in: the solve matches the reference's run with the analytic nullspace."""
+    n = 1000
+    k = bosp.LinearOperator.from_csr(P.t_matrix(n, -1.0))
+    m = bosp.LinearOperator.from_csr(P.t_matrix(n, 0.0))
+    res = bosp.solve(k, m, None, bosp.BospConfig(nev=10, nb=10, tol=1e-10))
+    check_result(res, golden_solves["tm1_t0_n1000"]["lambdas"], 1e-10, 10)
+    assert np.allclose(res.lambdas, TABLE3_ADVANPIX, rtol=2e-12)
+
+
 def test_config_errors():
     t = bosp.LinearOperator.from_csr(P.t_matrix(20, 0.0))
     with pytest.raises(bosp.ContractViolation):

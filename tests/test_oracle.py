@@ -167,3 +167,13 @@ def test_problem_generators_shapes():
     assert np.isclose((p.x0.T @ p.y0)[0, 0], 1.0)          # X0^T Y0 = I
     p5 = P.config5(16)
     assert p5.K.to_csr().nnz == 5 * 16 ** 2 - 4 * 16
+
+
+@needs_ref
+@pytest.mark.parametrize("n", [1000, 2000])
+def test_reference_nullspace_detector_misses_rank_at_large_n(n):
+    """Pins the failure SURVEY section 0.5 reports for the UNMODIFIED reference: its
+    compute_nullspace (nullspace.cpp:135-193) finds no null vector of T(-1)/T(0) (rank 1,
+    constants) at n >= 1000.  tests/test_gpu_solver.py holds the device detector to rank 1."""
+    x0, y0 = ref.compute_nullspace(P.t_matrix(n, -1.0).spec(), P.t_matrix(n, 0.0).spec())
+    assert x0.shape[1] == 0 and y0.shape[1] == 0
