@@ -83,6 +83,8 @@ struct CgScalars {
     double* bnorm;    // ||b||
     double* pap;      // p^T A p (this iteration)
     double* beta;     // rr_new / rr (this iteration)
+    double* alpha;    // rr / p^T A p of this iteration (0: column not updated), applied to x by
+                      // the direction kernel
     int* active;      // column still iterating
     int* broken;      // p^T A p <= 0 hit
     int* iters;       // iterations taken

@@ -24,6 +24,9 @@ void apply_weight(const InnerProduct& ip, const DMat& b, const DMat& out);
 
 struct DevBasis {
     DMat p, q;
+    // Consecutive bases flagged `group` are mutually biorthogonal (the solver's locked pairs)
+    // and are projected out in one concatenated pass (dev_biorth_against).
+    bool group = false;
 };
 
 // (I - sum P_k Q_k^T) W and (I - sum Q_k P_k^T) Z in place, bases in order (biorth.cpp:116-133).

@@ -151,7 +151,8 @@ void ensure_block(DBlock& b, int64_t rows, int64_t cols) {
 std::vector<DevBasis> deflation_bases(const DeviceState& st) {
     std::vector<DevBasis> bases;
     if (st.x0.ncols() > 0) bases.push_back({st.x0.view(), st.y0.view()});
-    for (size_t i = 0; i < st.locked_p.size(); ++i) bases.push_back({st.locked_p[i].view(), st.locked_q[i].view()});
+    for (size_t i = 0; i < st.locked_p.size(); ++i)
+        bases.push_back({st.locked_p[i].view(), st.locked_q[i].view(), true});
     return bases;
 }
 

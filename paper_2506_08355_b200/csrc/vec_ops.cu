@@ -351,36 +351,42 @@ struct CgXrF {
     }
     __device__ double pap(int j) const { return pap_parts ? xr_pap_slot() : s.pap[j]; }
     __device__ bool skip(int j) const { return s.active[j] == 0 || !(pap(j) > 0.0); }
+    // x += alpha p happens here (the host loop and the separate-update path) or, with defer_x,
+    // in the direction kernel (CgDirXF), which reads p anyway: 3 instead of 6 passes here
+    bool defer_x = false;
     __device__ void row(int64_t i, int j, double (&a)[1]) const {
         const double alpha = s.rr[j] / pap(j);
-        const double xv = x[i + j * lx] + alpha * p[i + j * lp];
+        if (!defer_x) x[i + j * lx] = x[i + j * lx] + alpha * p[i + j * lp];
         const double rv = r[i + j * lr] - alpha * ap[i + j * lap];
-        x[i + j * lx] = xv;
         r[i + j * lr] = rv;
         a[0] += rv * rv;
     }
     __device__ void row2(int64_t i, int j, double (&a)[1]) const {
         const double alpha = s.rr[j] / pap(j);
-        const double2 xv = ld2(x + i + j * lx), pv = ldg2(p + i + j * lp);
+        if (!defer_x) {
+            const double2 xv = ld2(x + i + j * lx), pv = ldg2(p + i + j * lp);
+            st2(x + i + j * lx, xv.x + alpha * pv.x, xv.y + alpha * pv.y);
+        }
         const double2 rv = ld2(r + i + j * lr), av = ldg2(ap + i + j * lap);
-        const double x0 = xv.x + alpha * pv.x, x1 = xv.y + alpha * pv.y;
         const double r0 = rv.x - alpha * av.x, r1 = rv.y - alpha * av.y;
-        st2(x + i + j * lx, x0, x1);
         st2(r + i + j * lr, r0, r1);
         a[0] += r0 * r0 + r1 * r1;
     }
     __device__ void fin(int j, const double (&sm)[1]) const {
         if (!s.active[j]) {
             beta[j] = 0.0;
+            s.alpha[j] = 0.0;
             return;
         }
         if (!(s.pap[j] > 0.0)) {  // cg.cpp:40-44: breakdown keeps the current iterate
             s.broken[j] = 1;
             s.active[j] = 0;
             beta[j] = 0.0;
+            s.alpha[j] = 0.0;
             return;
         }
         const double rr_new = sm[0];
+        s.alpha[j] = s.rr[j] / s.pap[j];  // the alpha the rows applied
         beta[j] = rr_new / s.rr[j];
         s.rr[j] = rr_new;
         s.iters[j] += 1;
@@ -474,14 +480,26 @@ struct DiagF {
         (*this)(i + 1, j);
     }
 };
-struct CgDirF {  // p = r + beta p for still-active columns (cg.cpp:49)
-    const double* r; double* p; int64_t lr, lp; const double* beta; const int* active;
-    __device__ bool skip(int j) const { return active[j] == 0; }
-    __device__ void operator()(int64_t i, int j) const { p[i + j * lp] = r[i + j * lr] + beta[j] * p[i + j * lp]; }
+// x += alpha p (the iteration's update, deferred from CgXrF) and p = r + beta p for columns still
+// active (cg.cpp:37, 49): x, p read once for both.  alpha == 0: the column did not move.
+struct CgDirXF {
+    double* x; const double* r; double* p; int64_t lx, lr, lp; const double* alpha; const double* beta;
+    const int* active;
+    __device__ bool skip(int j) const { return alpha[j] == 0.0; }
+    __device__ void operator()(int64_t i, int j) const {
+        const double pv = p[i + j * lp];
+        x[i + j * lx] = x[i + j * lx] + alpha[j] * pv;
+        if (active[j]) p[i + j * lp] = r[i + j * lr] + beta[j] * pv;
+    }
     __device__ void pair(int64_t i, int j) const {
-        const double bj = beta[j];
-        const double2 u = ldg2(r + i + j * lr), v = ld2(p + i + j * lp);
-        st2(p + i + j * lp, u.x + bj * v.x, u.y + bj * v.y);
+        const double aj = alpha[j];
+        const double2 pv = ld2(p + i + j * lp), xv = ld2(x + i + j * lx);
+        st2(x + i + j * lx, xv.x + aj * pv.x, xv.y + aj * pv.y);
+        if (active[j]) {
+            const double bj = beta[j];
+            const double2 u = ldg2(r + i + j * lr);
+            st2(p + i + j * lp, u.x + bj * pv.x, u.y + bj * pv.y);
+        }
     }
 };
 
@@ -593,9 +611,10 @@ void cg_update(const DMat& x, const DMat& r, const DMat& p, const DMat& ap, cons
     f.tol = tol; f.max_iter = max_iter;
     f.pap_parts = pap_parts;
     f.nparts = nparts;
-    launch_colred<1>("cg_vec", x.rows, static_cast<int>(x.cols), f, 48.0 * x.rows * x.cols);
-    CgDirF d{r.p, p.p, r.ld, p.ld, s.beta, s.active};
-    launch_cols("cg_vec", r.rows, static_cast<int>(r.cols), d, 24.0 * r.rows * r.cols);
+    f.defer_x = true;
+    launch_colred<1>("cg_vec", x.rows, static_cast<int>(x.cols), f, 24.0 * x.rows * x.cols);
+    CgDirXF d{x.p, r.p, p.p, x.ld, r.ld, p.ld, s.alpha, s.beta, s.active};
+    launch_cols("cg_vec", r.rows, static_cast<int>(r.cols), d, 40.0 * r.rows * r.cols);
 }
 
 }  // namespace b200

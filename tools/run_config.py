@@ -26,6 +26,7 @@ sys.path.insert(0, ROOT)
 
 
 PROFILE_RANGE = False
+REPEAT = 1
 
 
 def make(name: str, bosp, P):
@@ -65,6 +66,9 @@ def run(name: str) -> dict:
     bosp.launch_reset()
     if PROFILE_RANGE:  # ncu --profile-from-start off sees exactly this solve
         bosp.lib().bosp_profiler_range(1)
+    warm = []
+    for _ in range(REPEAT - 1):  # extra solves (eigenvectors stay in HBM), then the checked one
+        warm.append(bosp.solve(K, M, None, cfg, ns, want_vectors=False).stats["device_seconds"])
     t1 = time.perf_counter()
     res = bosp.solve(K, M, None, cfg, ns, want_vectors=True)
     solve_s = time.perf_counter() - t1
@@ -93,6 +97,7 @@ def run(name: str) -> dict:
         "max_width_u": res.stats["max_width_u"],
         "nullspace_crossgram": float(np.abs(prob.x0.T @ y).max()),
         "eigenpairs_per_s": prob.cfg["nev"] / res.stats["device_seconds"],
+        "device_s_all": warm + [res.stats["device_seconds"]],
     }
 
 
@@ -100,11 +105,13 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("configs", nargs="+")
     ap.add_argument("--out", default=None)
+    ap.add_argument("--repeat", type=int, default=1, help="solves per config (the last one is checked)")
     ap.add_argument("--profile-range", action="store_true",
                     help="cudaProfilerStart/Stop around the solve (for ncu --profile-from-start off)")
     a = ap.parse_args()
-    global PROFILE_RANGE
+    global PROFILE_RANGE, REPEAT
     PROFILE_RANGE = a.profile_range
+    REPEAT = max(1, a.repeat)
     out = {}
     for c in a.configs:
         r = run(c)
