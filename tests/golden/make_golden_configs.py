@@ -25,7 +25,24 @@ from paper_2506_08355_b200 import problems as P  # noqa: E402
 
 OUT = os.path.dirname(os.path.abspath(__file__))
 
+def _mass_1d(n):
+    """Linear-FEM mass matrix h/6 [1 4 1] with h = 1: a sparse SPD weight B."""
+    import numpy as np
+    import scipy.sparse as sp
+    e = np.ones(n)
+    return P.csr_from_scipy(sp.diags([e[:-1] / 6, 4 * e / 6, e[:-1] / 6], [-1, 0, 1]))
+
+
+def weighted_case(n):
+    """K = M = T(0), inner product weighted by the sparse mass matrix B: (K x = lambda B y,
+    M y = lambda B x), nev 6, nb 6, tol 1e-10 -- the reference detects the (empty) nullspace."""
+    t = P.t_matrix(n, 0.0)
+    return dict(K=t, M=t, B=_mass_1d(n), n=n, cfg=dict(nev=6, nb=6, tol=1e-10), name=f"weighted-T0-massB-n{n}")
+
+
 CASES = {
+    "weighted_massB_n400": lambda: weighted_case(400),
+    "weighted_massB_n2000": lambda: weighted_case(2000),
     "config4_n4096": lambda: P.config4(n=4096),
     "config5_m64": lambda: P.config5(64),
     "config3_m32": lambda: P.config3(32),
@@ -34,10 +51,17 @@ CASES = {
 
 def run(name: str):
     p = CASES[name]()
-    cfg = ref.RefConfig(**p.cfg)
-    t0 = time.time()
-    r = ref.solve(p.oracle_spec("K"), p.oracle_spec("M"), cfg, ns=(p.x0, p.y0), want_vectors=False)
-    dt = time.time() - t0
+    if isinstance(p, dict):  # B-weighted case: operators as CSR, nullspace detected by the reference
+        cfg = ref.RefConfig(**p["cfg"])
+        t0 = time.time()
+        r = ref.solve(p["K"].spec(), p["M"].spec(), cfg, B=p["B"].spec(), want_vectors=False)
+        dt = time.time() - t0
+        p = type("W", (), {"name": p["name"], "n": p["n"]})
+    else:
+        cfg = ref.RefConfig(**p.cfg)
+        t0 = time.time()
+        r = ref.solve(p.oracle_spec("K"), p.oracle_spec("M"), cfg, ns=(p.x0, p.y0), want_vectors=False)
+        dt = time.time() - t0
     rec = dict(lambdas=[float(v) for v in r.lambdas], residuals=[float(v) for v in r.residuals],
                iterations=int(r.stats["iterations"]), converged=bool(r.stats["converged"]),
                nev_converged=int(r.stats["nev_converged"]),

@@ -149,3 +149,30 @@ def test_config3_full_size_one_vs_two_ranks():
         assert r.residuals.max() < cfg.tol
         assert r.stats["final_biorth_deviation"] < 1e-10
     assert np.abs(one.lambdas - two.lambdas).max() / one.lambdas.max() < 1e-10
+
+
+# ---- generalized LREP: sparse SPD weight B ---------------------------------
+
+@pytest.mark.parametrize("n", [400, 2000])
+def test_weighted_sparse_mass_matrix(n):
+    """K x = lambda B y, M y = lambda B x with B the linear-FEM mass matrix (sparse, SPD,
+    inner_product.cpp:11-32, kernels.cpp:52-56), the nullspace detected under B -- against the
+    unmodified reference's run (tests/golden/golden_weighted_massB_n*.json)."""
+    from tests.golden.make_golden_configs import weighted_case
+    g = golden(f"weighted_massB_n{n}")
+    c = weighted_case(n)
+    K = bosp.LinearOperator.from_csr(c["K"])
+    M = bosp.LinearOperator.from_csr(c["M"])
+    B = bosp.LinearOperator.from_csr(c["B"])
+    res = bosp.solve(K, M, bosp.InnerProduct(B), bosp.BospConfig(**c["cfg"]))
+    assert res.converged and res.nev_converged == 6
+    lam, gl = np.asarray(res.lambdas), np.asarray(g["lambdas"])
+    assert np.max(np.abs(lam - gl) / gl) < 1e-10
+    assert res.residuals.max() < c["cfg"]["tol"]
+    bmat = c["B"].scipy()
+    gxy = res.x.T @ (bmat @ res.y)
+    assert np.abs(gxy - np.eye(6)).max() < 1e-10
+    # the pairs satisfy the generalized equations: K x = lambda B y, M y = lambda B x
+    kx = c["K"].scipy() @ res.x
+    by = bmat @ res.y
+    assert np.max(np.linalg.norm(kx - by * lam, axis=0) / np.linalg.norm(kx, axis=0)) < 1e-8
