@@ -172,7 +172,10 @@ def test_weighted_sparse_mass_matrix(n):
     bmat = c["B"].scipy()
     gxy = res.x.T @ (bmat @ res.y)
     assert np.abs(gxy - np.eye(6)).max() < 1e-10
-    # the pairs satisfy the generalized equations: K x = lambda B y, M y = lambda B x
-    kx = c["K"].scipy() @ res.x
-    by = bmat @ res.y
-    assert np.max(np.linalg.norm(kx - by * lam, axis=0) / np.linalg.norm(kx, axis=0)) < 1e-8
+    # the pairs satisfy the generalized equations K x = lambda B y, M y = lambda B x, with the
+    # solver's normalisation ||H z - lambda B z|| / ((1 + lambda) ||z||) (bosp_solver.cpp:271)
+    r1 = c["K"].scipy() @ res.x - (bmat @ res.y) * lam
+    r2 = c["M"].scipy() @ res.y - (bmat @ res.x) * lam
+    num = np.sqrt(np.sum(r1 ** 2, 0) + np.sum(r2 ** 2, 0))
+    den = (1 + lam) * np.sqrt(np.sum(res.x ** 2, 0) + np.sum(res.y ** 2, 0))
+    assert np.max(num / den) < 1e-9
