@@ -414,6 +414,9 @@ def run_b200(args, world, rank, local, dist):
     # inside the timed region (wall clock, max over ranks).
     e2e_t, h2d = [], 0
     d2h = 2 * nl * nev * 8 + 2 * nev * 8
+    # caller-owned page-locked result buffers, allocated once and reused by every step (what a
+    # serving loop does): the eigenvectors land there by DMA straight from HBM
+    xo, yo = bosp.pinned_empty((nl, nev)), bosp.pinned_empty((nl, nev))
     for _ in range(max(1, min(args.steps, args.e2e_steps))):
         lib.bosp_flush_l2(flush)
         barrier(dist)
@@ -422,7 +425,7 @@ def run_b200(args, world, rank, local, dist):
             Ke, Me = bosp.local_operator(prob.K, world, rank), bosp.local_operator(prob.M, world, rank)
         else:
             Ke, Me = bosp.operators_for(prob)
-        r2 = bosp.solve(Ke, Me, None, cfg, ns, want_vectors=True)
+        r2 = bosp.solve(Ke, Me, None, cfg, ns, out=(xo, yo))
         _ = float(r2.lambdas.sum())
         e2e_t.append(time.perf_counter() - t1)
         h2d = host_bytes(prob, nl) + ns.x0.nbytes + ns.y0.nbytes

@@ -247,16 +247,61 @@ class EigenResult:  # bosp_solver.hpp:71-81
     stats: dict = field(default_factory=dict)
 
 
+class _Pinned:
+    """Owner of a page-locked host buffer (bosp_host_alloc / cudaMallocHost)."""
+
+    def __init__(self, nbytes):
+        lib().bosp_host_alloc.restype = C.c_void_p
+        self.ptr = lib().bosp_host_alloc(C.c_int64(max(int(nbytes), 8)))
+        if not self.ptr:
+            raise CudaError("bosp_host_alloc failed")
+
+    def __del__(self):
+        try:
+            lib().bosp_host_free(C.c_void_p(self.ptr))
+        except Exception:
+            pass
+
+
+def pinned_empty(shape, order="F"):
+    """float64 array in page-locked host memory: eigenvector outputs written by DMA straight
+    from HBM (no staging through the pinned ring)."""
+    shape = tuple(int(v) for v in shape)
+    count = int(np.prod(shape))
+    owner = _Pinned(8 * count)
+    buf = (C.c_double * max(count, 1)).from_address(owner.ptr)
+    arr = np.frombuffer(buf, dtype=np.float64, count=count).reshape(shape, order=order)
+    return _PinnedArray(arr, owner)
+
+
+class _PinnedArray(np.ndarray):
+    def __new__(cls, arr, owner):
+        obj = arr.view(cls)
+        obj._owner = owner
+        return obj
+
+    def __array_finalize__(self, obj):
+        self._owner = getattr(obj, "_owner", None)
+
+
 def solve(K: LinearOperator, M: LinearOperator, ip: InnerProduct | None, cfg: BospConfig,
-          ns: GeneralizedNullspace | None = None, want_vectors=True, history_cap=2000) -> EigenResult:
-    """bosp::solve (bosp_solver.cpp:513-536) on the B200."""
+          ns: GeneralizedNullspace | None = None, want_vectors=True, history_cap=2000,
+          out=None) -> EigenResult:
+    """bosp::solve (bosp_solver.cpp:513-536) on the B200.  out=(x, y): caller-owned n x nev
+    Fortran-order float64 buffers for the eigenvectors (e.g. pinned_empty), reused across calls."""
     ip = ip or InnerProduct()
     n = K.dim
     cap = cfg.nev
     lam = np.zeros(cap)
     res = np.zeros(cap)
-    x = np.zeros((n, cap), order="F") if want_vectors else None
-    y = np.zeros((n, cap), order="F") if want_vectors else None
+    if out is not None:
+        x, y = out
+        for a in (x, y):
+            if a.shape != (n, cap) or a.dtype != np.float64 or not a.flags.f_contiguous:
+                raise ContractViolation("solve: out buffers must be n x nev float64, column-major")
+    else:
+        x = np.zeros((n, cap), order="F") if want_vectors else None
+        y = np.zeros((n, cap), order="F") if want_vectors else None
     hist = np.zeros((history_cap, cfg.nev))
     hrows, nout = C.c_int64(), C.c_int64()
     st = L.Stats()

@@ -271,23 +271,29 @@ k_gram(GramParams prm) {
         }
         cp_async_commit();
     }
+    // symmetric job, diagonal tile: a warp tile strictly below the diagonal only produces
+    // mirrored entries (never stored) -- it keeps the pipeline but leaves the DMMA pipe to the
+    // other warps (a quarter of a 2 x 2 diagonal tile's work)
+    const bool idle = prm.sym[jb] && tm == tn && wm0 >= wn0 + WTN;
     for (int it = 0; it < nk; ++it) {
         cp_async_wait<kStages - 2>();
         __syncthreads();
         const int st = it % kStages;
         const double* a = sa + st * BM * kLdK;
         const double* b = sb + st * BN * kLdK;
+        if (!idle) {
 #pragma unroll
-        for (int kk = 0; kk < kBK; kk += 4) {
-            double af[MT], bf[NTL];
+            for (int kk = 0; kk < kBK; kk += 4) {
+                double af[MT], bf[NTL];
 #pragma unroll
-            for (int i = 0; i < MT; ++i) af[i] = a[(wm0 + i * 8 + gid) * kLdK + kk + tig];
+                for (int i = 0; i < MT; ++i) af[i] = a[(wm0 + i * 8 + gid) * kLdK + kk + tig];
 #pragma unroll
-            for (int j = 0; j < NTL; ++j) bf[j] = b[(wn0 + j * 8 + gid) * kLdK + kk + tig];
+                for (int j = 0; j < NTL; ++j) bf[j] = b[(wn0 + j * 8 + gid) * kLdK + kk + tig];
 #pragma unroll
-            for (int i = 0; i < MT; ++i)
+                for (int i = 0; i < MT; ++i)
 #pragma unroll
-                for (int j = 0; j < NTL; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+                    for (int j = 0; j < NTL; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+            }
         }
         const int nxt = it + kStages - 1;
         if (nxt < nk) {
