@@ -78,7 +78,7 @@ def test_full_positive_spectrum_and_matrix_market(tmp_path):
         f.write(f"%%MatrixMarket matrix coordinate real general\n{t.n} {t.n} {t.nnz}\n")
         for i in range(t.n):
             for k in range(t.rowptr[i], t.rowptr[i + 1]):
-                f.write(f"{i + 1} {t.colidx[k] + 1} {t.vals[k]!r}\n")
+                f.write(f"{i + 1} {int(t.colidx[k]) + 1} {float(t.vals[k])!r}\n")
     out = tmp_path / "r.json"
     r = run_cli("solve", "--k-file", str(path), "--m-file", str(path), "--nev", "5", "--tol", "1e-10",
                 "--out", str(out))
