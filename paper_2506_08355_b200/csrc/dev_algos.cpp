@@ -271,7 +271,7 @@ void pair_grams(const DMat& x, const DMat& y, const InnerProduct& ip, DenseMatri
 
 DevBiorthOutcome dev_mgs_biorth(const DMat& x, const DMat& y, const DMat& p, const DMat& q,
                                 const InnerProduct& ip, double drop_tol, bool classical,
-                                const DenseMatrix* gxy_hint) {
+                                const DenseMatrix* gxy_hint, bool inputs_scratch) {
     require(x.rows == y.rows && x.cols == y.cols, "biorth: X and Y must have equal shape");
     DevBiorthOutcome out;
     const int64_t m = x.cols, n = x.rows;
@@ -364,6 +364,11 @@ DevBiorthOutcome dev_mgs_biorth(const DMat& x, const DMat& y, const DMat& p, con
     out.second_pass = true;
     if (debug_on()) std::fprintf(stderr, "[bosp] mgs m=%lld second pass\n", (long long)out.kept);
     CoefBiorth cb2 = coef_rebiorth(gpq);
+    if (inputs_scratch && start == 0) {  // X, Y (never re-pointed) take the result: no copy back
+        apply_coefs(pk, qk, cb2.a, cb2.b, x.cols_range(0, out.kept), y.cols_range(0, out.kept));
+        out.result_in_inputs = true;
+        return out;
+    }
     DBlock tp(x.rows, out.kept), tq(x.rows, out.kept);
     apply_coefs(pk, qk, cb2.a, cb2.b, tp.view(), tq.view());
     copy_block(tp.view(), pk);

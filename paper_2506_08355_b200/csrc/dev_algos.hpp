@@ -37,6 +37,9 @@ struct DevBiorthOutcome {
     int64_t kept = 0;
     std::vector<int64_t> kept_columns, dropped_columns;
     bool second_pass = false;
+    // inputs_scratch: the second pass wrote its result into the first `kept` columns of X, Y
+    // (instead of P, Q plus a copy back)
+    bool result_in_inputs = false;
 };
 // MGS-Biorth of (X, Y) into (P, Q) (first `kept` columns written; P/Q need >= m columns and
 // must not alias X/Y).  Semantics of mgs_biorth (biorth.cpp:102-109); classical -> cgs_biorth.
@@ -47,9 +50,12 @@ DevBiorthOutcome dev_gs_biorth_seq(const DMat& x, const DMat& y, const DMat& p, 
                                    const InnerProduct& ip, double drop_tol, bool classical);
 // gxy_hint: X^T Y already known on the host (unweighted only) -- the pair Grams then compute
 // only X^T X and Y^T Y (the drift repair reuses the invariant sample's U^T V, lrep_solver.cpp).
+// inputs_scratch: X, Y are dead after the call and may receive the result (see
+// DevBiorthOutcome::result_in_inputs).
 DevBiorthOutcome dev_mgs_biorth(const DMat& x, const DMat& y, const DMat& p, const DMat& q,
                                 const InnerProduct& ip, double drop_tol = 1e-12,
-                                bool classical = false, const DenseMatrix* gxy_hint = nullptr);
+                                bool classical = false, const DenseMatrix* gxy_hint = nullptr,
+                                bool inputs_scratch = false);
 // ||P^T Q - I||_2 (biorth.cpp:135-143).
 double dev_biorth_residual(const DMat& p, const DMat& q, const InnerProduct& ip);
 

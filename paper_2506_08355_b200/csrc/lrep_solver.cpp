@@ -180,9 +180,10 @@ void rebiorthogonalize_state(DeviceState& st, const InnerProduct& ip, const Dens
     const DMat u = st.U.cols(0, d), v = st.V.cols(0, d);
     dev_biorth_against(deflation_bases(st), u, v, ip);
     DBlock nu(st.n, st.U.capacity()), nv(st.n, st.V.capacity());
-    DevBiorthOutcome out = dev_mgs_biorth(u, v, nu.cols(0, d), nv.cols(0, d), ip, 1e-12, false, gxy_hint);
+    DevBiorthOutcome out = dev_mgs_biorth(u, v, nu.cols(0, d), nv.cols(0, d), ip, 1e-12, false, gxy_hint, true);
     if (!out.dropped_columns.empty())
         throw NumericalAbort("bosp: rebiorthogonalization dropped columns");
+    if (out.result_in_inputs) return;  // the second pass wrote U, V in place
     nu.set_cols(st.U.ncols());
     nv.set_cols(st.V.ncols());
     std::swap(st.U, nu);
@@ -256,6 +257,15 @@ RitzOut ritz_step(DeviceState& st, const LinearOperator& k, const LinearOperator
     std::copy(both.data(), both.data() + d * d, khat.data());
     std::copy(both.data() + d * d, both.data() + 2 * d * d, mhat.data());
 
+    static const char* dump = std::getenv("BOSP_DUMP_SMALL");  // diagnostics: "<path prefix>"
+    if (dump && d >= 96 && (st.iter == 5 || st.iter == 20)) {
+        const std::string path = std::string(dump) + "_it" + std::to_string(st.iter) + "_d" + std::to_string(d) + ".bin";
+        if (FILE* f = std::fopen(path.c_str(), "wb")) {
+            std::fwrite(khat.data(), sizeof(double), static_cast<size_t>(d * d), f);
+            std::fwrite(mhat.data(), sizeof(double), static_cast<size_t>(d * d), f);
+            std::fclose(f);
+        }
+    }
     const auto t0 = Clock::now();
     {
         auto ph = st.phases.scope(PH_SMALL);
@@ -457,6 +467,8 @@ bool iterate_device(DeviceState& st, const LinearOperator& k, const LinearOperat
 
     // Step 6 (:329-388): block Gauss-Seidel with batched inner CG, projection, MGS-Biorth
     int64_t kw = 0;
+    const DBlock* w_src = &st.rz;  // where W~, Z~ end up (the MGS output, or its inputs)
+    const DBlock* z_src = &st.rw;
     if (nb_eff > 0) {
         std::vector<double> lam_b(sol.lambdas.begin() + c0, sol.lambdas.begin() + c0 + nb_eff);
         const double* lamb = upload_scalars(st, lam_b, 3);
@@ -518,15 +530,20 @@ bool iterate_device(DeviceState& st, const LinearOperator& k, const LinearOperat
         ensure_block(st.rz, n, nb_eff);
         ensure_block(st.rw, n, nb_eff);
         auto phm = st.phases.scope(PH_MGS);
-        DevBiorthOutcome wz = dev_mgs_biorth(st.wg.view(), st.zg.view(), st.rz.view(), st.rw.view(), ip);
+        DevBiorthOutcome wz = dev_mgs_biorth(st.wg.view(), st.zg.view(), st.rz.view(), st.rw.view(), ip,
+                                             1e-12, false, nullptr, true);
         kw = wz.kept;
+        if (wz.result_in_inputs) {  // the second pass left W~, Z~ in the CG outputs
+            w_src = &st.wg;
+            z_src = &st.zg;
+        }
     }
 
     // Step 7 (:390-427): U = [X, P~, W~], V = [Y, Q~, Z~]
     copy_block(st.pt.cols(0, kp), st.U.cols(st.wx, kp));
     copy_block(st.qt.cols(0, kp), st.V.cols(st.wx, kp));
-    copy_block(st.rz.cols(0, kw), st.U.cols(st.wx + kp, kw));
-    copy_block(st.rw.cols(0, kw), st.V.cols(st.wx + kp, kw));
+    copy_block(w_src->cols(0, kw), st.U.cols(st.wx + kp, kw));
+    copy_block(z_src->cols(0, kw), st.V.cols(st.wx + kp, kw));
     st.wp = kp;
     st.ww = kw;
 

@@ -230,6 +230,24 @@ JacobiSvdResult jacobi_svd_tol(DenseMatrix a, int64_t max_sweeps, double tol) {
         std::vector<int64_t> pos(static_cast<size_t>(nblk));
         std::iota(pos.begin(), pos.end(), 0);
         std::vector<double> nrm(static_cast<size_t>(k));
+        // Pairs whose columns are unchanged since they last passed the orthogonality test are
+        // skipped: the test would recompute the same dot product from the same data (and the
+        // same norms: nrm is recomputed from the columns every sweep) and reach the same "no
+        // rotation" -- decision-exact, and most of the late sweeps' dot products disappear.
+        std::vector<uint32_t> ver(static_cast<size_t>(k), 0u);
+        std::vector<uint64_t> seen(static_cast<size_t>(k * k), ~uint64_t(0));
+        auto pair = [&](int64_t p, int64_t q) -> int {
+            const uint64_t key = (static_cast<uint64_t>(ver[p]) << 32) | ver[q];
+            uint64_t& sk = seen[p * k + q];
+            if (sk == key) return 0;
+            if (jacobi_pair(a, res.v, nrm.data(), p, q, tol)) {
+                ++ver[p];
+                ++ver[q];
+                return 1;
+            }
+            sk = key;
+            return 0;
+        };
         while (rotated && sweep < max_sweeps) {
             ++sweep;
             int any = 0;
@@ -245,12 +263,12 @@ JacobiSvdResult jacobi_svd_tol(DenseMatrix a, int64_t max_sweeps, double tol) {
                         const int64_t i0 = blk_lo(bi), i1 = blk_hi(bi), j0 = blk_lo(bj), j1 = blk_hi(bj);
                         if (round == 0) {
                             for (int64_t p = i0; p + 1 < i1; ++p)
-                                for (int64_t q = p + 1; q < i1; ++q) any |= jacobi_pair(a, res.v, nrm.data(), p, q, tol);
+                                for (int64_t q = p + 1; q < i1; ++q) any |= pair(p, q);
                             for (int64_t p = j0; p + 1 < j1; ++p)
-                                for (int64_t q = p + 1; q < j1; ++q) any |= jacobi_pair(a, res.v, nrm.data(), p, q, tol);
+                                for (int64_t q = p + 1; q < j1; ++q) any |= pair(p, q);
                         }
                         for (int64_t p = i0; p < i1; ++p)
-                            for (int64_t q = j0; q < j1; ++q) any |= jacobi_pair(a, res.v, nrm.data(), p, q, tol);
+                            for (int64_t q = j0; q < j1; ++q) any |= pair(p, q);
                     }  // implicit barrier
                     const int64_t last = lp[nblk - 1];
                     for (int64_t i = nblk - 1; i > 1; --i) lp[i] = lp[i - 1];
@@ -293,7 +311,7 @@ namespace {
 // Householder QR with column pivoting, W P = Q R (LAPACK dgeqp2 semantics: largest remaining
 // column norm first, norms downdated with the cancellation guard of dlaqp2).  On return `a`
 // holds R on and above the diagonal and the reflectors' tails below; tau / perm as in dgeqp2.
-void householder_qrcp(DenseMatrix& a, std::vector<double>& tau, std::vector<int64_t>& perm) {
+void householder_qrcp(DenseMatrix& a, std::vector<double>& tau, std::vector<int64_t>& perm, bool pivot = true) {
     const int64_t m = a.rows(), k = a.cols();
     tau.assign(static_cast<size_t>(k), 0.0);
     perm.resize(static_cast<size_t>(k));
@@ -302,7 +320,7 @@ void householder_qrcp(DenseMatrix& a, std::vector<double>& tau, std::vector<int6
     for (int64_t j = 0; j < k; ++j) vn1[j] = vn2[j] = std::sqrt(dot_avx(a.col(j), a.col(j), m));
     const double tol3z = std::sqrt(std::numeric_limits<double>::epsilon());
     for (int64_t j = 0; j < k && j < m; ++j) {
-        const int64_t pvt = j + (std::max_element(vn1.begin() + j, vn1.end()) - (vn1.begin() + j));
+        const int64_t pvt = pivot ? j + (std::max_element(vn1.begin() + j, vn1.end()) - (vn1.begin() + j)) : j;
         if (pvt != j) {
             std::swap_ranges(a.col(pvt), a.col(pvt) + m, a.col(j));
             std::swap(perm[pvt], perm[j]);
@@ -347,6 +365,26 @@ void householder_qrcp(DenseMatrix& a, std::vector<double>& tau, std::vector<int6
     }
 }
 
+// b <- Q b for Q = H_0 H_1 ... H_{k-1} (reflectors below the diagonal of `a`, dgeqp2 layout);
+// the columns of b are independent.
+void apply_q(const DenseMatrix& a, const std::vector<double>& tau, DenseMatrix& b) {
+    const int64_t m = a.rows(), k = static_cast<int64_t>(tau.size());
+#pragma omp parallel for schedule(static)
+    for (int64_t c = 0; c < b.cols(); ++c) {
+        double* bc = b.col(c);
+        for (int64_t j = k - 1; j >= 0; --j) {
+            if (tau[j] == 0.0) continue;
+            const double* v = a.col(j) + j;
+            const int64_t len = m - j;
+            double s = bc[j];
+            for (int64_t i = 1; i < len; ++i) s += v[i] * bc[j + i];
+            s *= tau[j];
+            bc[j] -= s;
+            for (int64_t i = 1; i < len; ++i) bc[j + i] -= s * v[i];
+        }
+    }
+}
+
 }  // namespace
 
 // One-sided Jacobi SVD with QR preconditioning (Drmac & Veselic): W P = Q R, then the same
@@ -366,20 +404,7 @@ JacobiSvdResult jacobi_svd_qr(const DenseMatrix& w, int64_t max_sweeps) {
     JacobiSvdResult jx = jacobi_svd_tol(std::move(x), max_sweeps, 1e-15);
     // left vectors of W: Q V_x, Q = H_0 H_1 ... H_{k-1} applied to V_x (columns independent)
     DenseMatrix u = std::move(jx.v);
-#pragma omp parallel for schedule(static)
-    for (int64_t c = 0; c < k; ++c) {
-        double* uc = u.col(c);
-        for (int64_t j = k - 1; j >= 0; --j) {
-            if (tau[j] == 0.0) continue;
-            const double* v = a.col(j) + j;
-            const int64_t len = m - j;
-            double s = uc[j];
-            for (int64_t i = 1; i < len; ++i) s += v[i] * uc[j + i];
-            s *= tau[j];
-            uc[j] -= s;
-            for (int64_t i = 1; i < len; ++i) uc[j + i] -= s * v[i];
-        }
-    }
+    apply_q(a, tau, u);
     // right vectors of W: P U_x (row perm[i] of the result is row i of U_x)
     JacobiSvdResult res;
     res.sigma = std::move(jx.sigma);
