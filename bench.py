@@ -463,14 +463,27 @@ def run_b200(args, world, rank, local, dist):
         if pm and pm["launches"] and pm["ms"] > 0:
             hbm = peaks.get("hbm_gbs", 6650.0)
             ach = pm["region_bytes"] / (pm["ms"] * 1e-3) / 1e9
+            fl = pm.get("region_flops", 0.0)
+            tf = fl / (pm["ms"] * 1e-3) / 1e12
+            intensity = fl / pm["region_bytes"] if pm["region_bytes"] else 0.0
+            dg = (rooflines.get("gram_wide") or {}).get("peak") or 35.5
+            # the bound follows the calls' arithmetic intensity (6 n m^2 flop / 48 n m B = m / 8):
+            # HBM below the DMMA ridge (~5.4 flop/B), the fp64 tensor pipe above it (d = 320 repairs)
+            tensor = intensity > dg * 1e12 / (hbm * 1e9)
             roof_mgs = {"kernel": "mgs_biorth (pair Gram + coefficient products + P^T Q check)",
-                        "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                        "bound": "tensor" if tensor else "hbm",
+                        "achieved": tf if tensor else ach, "peak": dg if tensor else hbm,
+                        "unit": "TFLOP/s" if tensor else "GB/s",
+                        "frac": (tf / dg) if tensor else (ach / hbm),
+                        "hbm_achieved_gbs": ach, "hbm_frac": ach / hbm, "tensor_achieved_tflops": tf,
+                        "tensor_frac": tf / dg, "intensity_flop_per_byte": intensity,
                         "calls_per_solve": pm["region_calls"], "launches_per_solve": pm["launches"],
                         "avg_call_us": pm["ms"] * 1e3 / max(1, pm["region_calls"]),
                         "algorithmic_bytes_per_call": pm["region_bytes"] / max(1, pm["region_calls"]),
                         "share_of_step": pm["ms"] / ms_per_step,
-                        "bytes_note": "48 n m per call (SURVEY 8d: X, Y read + P, Q written = 32 n m, + 16 n m "
-                                      "for the P^T Q Gram of the second-pass test)"}
+                        "bytes_note": "48 n m bytes and 6 n m^2 flops per call (SURVEY 8d: X, Y read + P, Q "
+                                      "written = 32 n m, + 16 n m for the P^T Q Gram of the second-pass test; "
+                                      "4 n m^2 recurrence + 2 n m^2 check)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -267,7 +267,8 @@ void bosp_profile_collect_regions(int64_t* launches, double* ms, double* bytes, 
                                   int64_t* region_calls, double* region_bytes);
 /* After bosp_profile_enable("*") (every launch timed) and a collect: the collected totals split
  * by kernel family, one text line per family "<family> <launches> <ms> <bytes> <flops>\n"
- * into buf (NUL-terminated, truncated to len); returns the length the full report needs. */
+ * into buf (NUL-terminated, truncated to len); returns the length the full report needs.  A
+ * composite-operation profile ("mgs") adds "@region <calls> 0 <bytes> <flops>". */
 int64_t bosp_profile_family_report(char* buf, int64_t len);
 /* Microbenchmark: apply `op` to a device-resident random n x ncols block `reps` times (after
  * one warm-up); returns the mean device time per apply in *ms (CUDA events). */

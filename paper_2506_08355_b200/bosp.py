@@ -667,6 +667,9 @@ def profile_collect():
     fams = {}
     for line in buf.value.decode().splitlines():
         f, l, m, by, fl = line.split()
+        if f == "@region":
+            out["region_flops"] = float(fl)
+            continue
         fams[f] = dict(launches=int(l), ms=float(m), bytes=float(by), flops=float(fl))
     out["families"] = fams
     return out

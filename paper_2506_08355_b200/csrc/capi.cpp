@@ -613,9 +613,15 @@ int64_t bosp_profile_family_report(char* buf, int64_t len) {
     std::string s;
     try {
         char line[256];
-        for (const auto& kv : bosp::Runtime::get().prof_by_family()) {
+        const bosp::Runtime& rt = bosp::Runtime::get();
+        for (const auto& kv : rt.prof_by_family()) {
             std::snprintf(line, sizeof(line), "%s %lld %.9g %.17g %.17g\n", kv.first.c_str(),
                           (long long)kv.second.launches, kv.second.ms, kv.second.bytes, kv.second.flops);
+            s += line;
+        }
+        if (rt.last_regions_.launches > 0) {  // composite operations: calls, -, bytes, flops
+            std::snprintf(line, sizeof(line), "@region %lld 0 %.17g %.17g\n", (long long)rt.last_regions_.launches,
+                          rt.last_regions_.bytes, rt.last_regions_.flops);
             s += line;
         }
     } catch (...) {

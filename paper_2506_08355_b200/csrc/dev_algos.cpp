@@ -277,7 +277,9 @@ DevBiorthOutcome dev_mgs_biorth(const DMat& x, const DMat& y, const DMat& p, con
     const int64_t m = x.cols, n = x.rows;
     if (m == 0) return out;
     // profiled as one unit ("mgs"): X, Y in and P, Q out (32 n m) + the P^T Q check (16 n m)
-    ProfRegion region("mgs", classical ? 32.0 * n * m : 48.0 * n * m);
+    // 4 n m^2 flops of the recurrence + 2 n m^2 for the P^T Q check
+    ProfRegion region("mgs", classical ? 32.0 * n * m : 48.0 * n * m,
+                      classical ? 4.0 * n * m * m : 6.0 * n * m * m);
     // Columns are processed in order.  Runs of well-conditioned columns go through the Gram /
     // coefficient recurrence (level-3 on the DMMA pipe); a column whose residual cancels
     // (nearly dependent on the kept pairs) is materialised in n-space and projected

@@ -144,11 +144,12 @@ bool Runtime::region_open(const char* name) {
     return true;
 }
 
-void Runtime::region_close(double algo_bytes) {
+void Runtime::region_close(double algo_bytes, double algo_flops) {
     if (region_depth_ > 0) --region_depth_;
     if (region_depth_ == 0) {
         graph_samples_.region_calls += 1;
         graph_samples_.region_bytes += algo_bytes;
+        graph_samples_.region_flops += algo_flops;
     }
 }
 
@@ -251,6 +252,7 @@ Runtime::ProfReport Runtime::prof_collect() {
     read_timer_samples(timer_pending_);
     timer_pending_.clear();
     ProfReport r = graph_samples_;
+    last_regions_ = ProfReport{r.region_calls, 0.0, r.region_bytes, r.region_flops};
     graph_samples_ = ProfReport{0, 0.0, 0.0, 0.0};
     for (auto& e : prof_events_) {
         float ms = 0.f;

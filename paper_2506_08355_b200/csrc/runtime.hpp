@@ -116,7 +116,7 @@ public:
     // region_calls/region_bytes: composite operations (ProfRegion) and their algorithmic bytes.
     struct ProfReport {
         int64_t launches; double ms; double bytes; double flops;
-        int64_t region_calls = 0; double region_bytes = 0.0;
+        int64_t region_calls = 0; double region_bytes = 0.0; double region_flops = 0.0;
     };
     ProfReport prof_collect();  // synchronises, sums elapsed times, resets
     // prof_enable("*") times every launch; the last prof_collect() split by kernel family
@@ -125,7 +125,9 @@ public:
     // every launch inside it is timed (whatever its own family); at close the region credits
     // its algorithmic bytes once.  Nested regions of the same name count once (outermost).
     bool region_open(const char* name);
-    void region_close(double algo_bytes);
+    void region_close(double algo_bytes, double algo_flops = 0.0);
+    // the last prof_collect()'s composite-operation totals (calls, bytes, flops)
+    ProfReport last_regions_{0, 0.0, 0.0, 0.0};
     // Device-clock timing for kernels that may run inside CUDA graphs (event nodes are not
     // allowed in conditional bodies): the kernel writes (max of ~start, max of end) %globaltimer
     // into a 2-word slot that a memset resets before each launch.  A launch recorded into a
@@ -204,10 +206,11 @@ struct LaunchScope {
 // profiled family; `algo_bytes` is the operation's algorithmic traffic.
 struct ProfRegion {
     bool open;
-    double algo_bytes;
-    ProfRegion(const char* name, double bytes) : open(Runtime::get().region_open(name)), algo_bytes(bytes) {}
+    double algo_bytes, algo_flops;
+    ProfRegion(const char* name, double bytes, double flops = 0.0)
+        : open(Runtime::get().region_open(name)), algo_bytes(bytes), algo_flops(flops) {}
     ~ProfRegion() {
-        if (open) Runtime::get().region_close(algo_bytes);
+        if (open) Runtime::get().region_close(algo_bytes, algo_flops);
     }
 };
 
