@@ -446,6 +446,7 @@ def run_b200(args, world, rank, local, dist):
                           ("spmm_cg", "hbm"), ("spmm", "hbm"), ("cg_vec", "hbm")):
             r = family_roofline(fam, prof_fams.get(fam), prof_ms, peaks, dgemm, kind, NOTES.get(fam, ""))
             if r:
+                r["traffic"] = traffic_for(fam, wl)[0]  # ncu DRAM bytes per launch (committed capture)
                 rooflines[fam] = r
         dom, _kind = DOMINANT.get(wl, ("gram_wide", "tensor"))
         roof = dict(rooflines.get(dom) or {})
