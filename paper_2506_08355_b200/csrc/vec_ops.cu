@@ -143,7 +143,7 @@ template <int K, class F>
 void launch_colred(const char* family, int64_t n, int ncols, const F& f, double bytes) {
     if (ncols <= 0) return;
     Runtime& rt = Runtime::get();
-    const int64_t target = 4 * rt.sm_count();  // 4 waves: 2..16 measured within 3% on config 2
+    const int64_t target = 4 * rt.sm_count();  // 4 waves: 2..32 within 3% on configs 2 and 3
     // >= 1024 rows per chunk: narrow solves (1-8 live columns) still fill the machine
     int nchunks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n + 1023) / 1024,
                                                                             (target + ncols - 1) / ncols)));
@@ -404,8 +404,8 @@ __global__ void __launch_bounds__(kThreads) k_cols(int64_t n, F f, KTimer tm) {
     tm.start();
     if (blockIdx.x == 0 && threadIdx.x == 0) tm.add_column();
     const int64_t npair = n >> 1;
-    for (int64_t q = blockIdx.x * static_cast<int64_t>(kThreads) + threadIdx.x; q < npair;
-         q += static_cast<int64_t>(gridDim.x) * kThreads)
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * kThreads;
+    for (int64_t q = blockIdx.x * static_cast<int64_t>(kThreads) + threadIdx.x; q < npair; q += stride)
         f.pair(2 * q, j);
     if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) f(n - 1, j);
     tm.stop();
@@ -415,7 +415,9 @@ template <class F>
 void launch_cols(const char* family, int64_t n, int ncols, const F& f, double bytes) {
     if (ncols <= 0 || n <= 0) return;
     Runtime& rt = Runtime::get();
-    const int64_t target = 8LL * rt.sm_count();
+    // 32 waves of blocks over all columns: the CG direction/x update (5 streams) went 1.08 ->
+    // ~0.9 ms per 64-column launch at 128^3 (8 waves: the grid-stride loop left HBM idle)
+    const int64_t target = 32LL * rt.sm_count();
     const unsigned gx = static_cast<unsigned>(std::max<int64_t>(
         1, std::min<int64_t>((n / 2 + kThreads - 1) / kThreads, (target + ncols - 1) / ncols)));
     KTimer tm{rt.timer_begin(family, bytes, 0.0, 0.0, ncols)};
