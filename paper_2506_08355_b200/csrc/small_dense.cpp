@@ -822,8 +822,67 @@ CoefBiorth coef_mgs(const DenseMatrix& gxx, const DenseMatrix& gxy, const DenseM
     return out;
 }
 
+namespace {
+// rebiorth_pass (biorth.cpp:72-98) for k >= 64 as the unpivoted LDU of Gpq -- the same
+// recurrence in exact arithmetic (the first pass's coef_mgs_ldu, without drop tests, which the
+// second pass does not apply): O(k^3) in threaded level-2/3 loops instead of ~50 ms of scalar
+// recurrence at k = 320.  Falls back (false) on a zero or non-finite pivot, whose column the
+// sequential form leaves unchanged (biorth.cpp:90).
+bool coef_rebiorth_ldu(const DenseMatrix& gpq, CoefBiorth& out) {
+    const int64_t m = gpq.rows();
+    DenseMatrix g = gpq;
+    std::vector<double> dpiv(static_cast<size_t>(m));
+    for (int64_t l = 0; l < m; ++l) {
+        const double d = g(l, l);
+        if (!(std::fabs(d) > 0.0) || !std::isfinite(d)) return false;
+        dpiv[l] = d;
+        const double inv = 1.0 / d;
+        for (int64_t i = l + 1; i < m; ++i) g(i, l) *= inv;
+#pragma omp parallel for schedule(static) if (m - l > 96)
+        for (int64_t j = l + 1; j < m; ++j) {
+            const double glj = g(l, j);
+            if (glj == 0.0) continue;
+            double* gj = g.col(j);
+            const double* gl = g.col(l);
+            for (int64_t i = l + 1; i < m; ++i) gj[i] -= gl[i] * glj;
+        }
+        for (int64_t j = l + 1; j < m; ++j) g(l, j) *= inv;
+    }
+    out.a = DenseMatrix(m, m);
+    out.b = DenseMatrix(m, m);
+#pragma omp parallel for schedule(dynamic, 8)
+    for (int64_t c = 0; c < m; ++c) {
+        double* a = out.a.col(c);  // L^T a = e_c
+        a[c] = 1.0;
+        for (int64_t i = c - 1; i >= 0; --i) {
+            double s = 0.0;
+            for (int64_t k = i + 1; k <= c; ++k) s += g(k, i) * a[k];
+            a[i] = -s;
+        }
+        double* b = out.b.col(c);  // U b = e_c
+        b[c] = 1.0;
+        for (int64_t i = c - 1; i >= 0; --i) {
+            double s = 0.0;
+            for (int64_t k = i + 1; k <= c; ++k) s += g(i, k) * b[k];
+            b[i] = -s;
+        }
+        const double sc = 1.0 / std::sqrt(std::fabs(dpiv[c])), sg = sign_or_plus(dpiv[c]);
+        for (int64_t i = 0; i <= c; ++i) {
+            a[i] *= sg * sc;
+            b[i] *= sc;
+        }
+    }
+    for (int64_t c = 0; c < m; ++c) out.kept.push_back(c);
+    return true;
+}
+}  // namespace
+
 CoefBiorth coef_rebiorth(const DenseMatrix& gpq) {
     const int64_t k = gpq.rows();
+    if (k >= 64) {
+        CoefBiorth fast;
+        if (coef_rebiorth_ldu(gpq, fast)) return fast;
+    }
     std::vector<std::vector<double>> av, bv, ua, ub;
     std::vector<double> al, be, ta, tb;
     for (int64_t l = 0; l < k; ++l) {
