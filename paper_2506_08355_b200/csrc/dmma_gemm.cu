@@ -416,9 +416,8 @@ void launch_gram(const GramJob* jobs, int njobs, int64_t n) {
     constexpr int NT = WM * WN * 32;
     constexpr size_t smem = sizeof(double) * kStages * (BM + BN) * kLdK;
     static unsigned attr_mask = 0;
-    if (rt.first_use(attr_mask))
-        BOSP_CUDA(cudaFuncSetAttribute(k_gram<BM, BN, WM, WN, GBK, GST>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    rt.once_per_device(attr_mask, [&] { BOSP_CUDA(cudaFuncSetAttribute(k_gram<BM, BN, WM, WN, GBK, GST>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); });
     double flops = 0.0, bytes = 0.0;
     for (int j = 0; j < njobs; ++j) {
         flops += 2.0 * n * (double)jobs[j].a.cols() * jobs[j].b.cols() * (prm.sym[j] ? 0.5 : 1.0);
@@ -637,9 +636,8 @@ void launch_gram_regs(const GramJob* jobs, int njobs, int64_t n) {
     prm.partial = rt.scratch(static_cast<size_t>(prm.job_stride) * njobs);
     constexpr size_t smem = sizeof(double) * (kGramSeqFold<GM * GN, MS, NS> ? 1 : kRegWarps) * MS * 8 * NS * 8;
     static unsigned attr_mask = 0;
-    if (rt.first_use(attr_mask))
-        BOSP_CUDA(cudaFuncSetAttribute(k_gram_regs<MT, NTL, GM, GN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem)));
+    rt.once_per_device(attr_mask, [&] { BOSP_CUDA(cudaFuncSetAttribute(k_gram_regs<MT, NTL, GM, GN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem))); });
     double flops = 0.0, bytes = 0.0;
     for (int j = 0; j < njobs; ++j) {
         flops += 2.0 * n * jobs[j].a.cols() * jobs[j].b.cols() * (prm.sym[j] ? 0.5 : 1.0);
@@ -827,10 +825,8 @@ void launch_product(const ProductJob* jobs, int njobs, int64_t n) {
     constexpr size_t smem_epi = sizeof(double) * BN * (BM + 4);
     constexpr size_t smem = smem_pipe > smem_epi ? smem_pipe : smem_epi;
     static unsigned attr_mask = 0;
-    if (rt.first_use(attr_mask)) {
-        BOSP_CUDA(cudaFuncSetAttribute(k_product<BM, BN, WM, WN, PBK, PST>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    }
+    rt.once_per_device(attr_mask, [&] { BOSP_CUDA(cudaFuncSetAttribute(k_product<BM, BN, WM, WN, PBK, PST>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); });
     LaunchScope ls("product_wide", bytes, flops);
     const unsigned gx = static_cast<unsigned>(std::min<int64_t>(max_tiles, 65535));
     const unsigned gy = static_cast<unsigned>((max_tiles + gx - 1) / gx);
@@ -1000,8 +996,7 @@ void launch_skinny_rt(const ProductJob* jobs, int njobs, int64_t n) {
     prm.ldc = (prm.kp + 15) / 16 * 16 + 4;
     const size_t smem = sizeof(double) * (static_cast<size_t>(BN) * prm.ldc + 2ull * prm.kp * kSkLdM);
     static unsigned attr_mask = 0;
-    if (rt.first_use(attr_mask))
-        BOSP_CUDA(cudaFuncSetAttribute(k_product_skinny<BN, RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    rt.once_per_device(attr_mask, [&] { BOSP_CUDA(cudaFuncSetAttribute(k_product_skinny<BN, RT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)); });
     int per_sm = 1;
     BOSP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_product_skinny<BN, RT>, 256, smem));
     const int64_t ctas = std::max<int64_t>(1, std::min<int64_t>(prm.tiles, int64_t(std::max(per_sm, 1)) * rt.sm_count()));
@@ -1080,10 +1075,10 @@ void gram(const GramJob* jobs, int njobs, int64_t n) {
         launch_gram<32, 32, 2, 2>(jobs, njobs, n);
     else if (bmax <= 32 && amax >= 128)
         // many output rows, <= 32 columns (the dense operator's A x = (A^T)^T x at the CG's
-        // widths): 128 x 32 tiles, 4 warps of 32 x 32, 2 x 32-row stages, no padding of b to
-        // 64 -- n = 16384, 32 columns: 0.73 ms (23.7 TF/s; 8 warps of 32 x 16: 23.0, 64 x 32
-        // tiles: 19-21)
-        launch_gram<128, 32, 4, 1, 32, 2>(jobs, njobs, n);
+        // widths): 128 x 32 tiles, 4 warps of 32 x 32, 4 x 16-row stages, no padding of b to
+        // 64 -- n = 16384, 32 columns: 0.71 ms (24.3 TF/s; 2 x 32-row stages 23.7, 8 warps of
+        // 32 x 16: 23.0, 256-row tiles 17-22, 64 x 32 tiles: 19-21)
+        launch_gram<128, 32, 4, 1, 16, 4>(jobs, njobs, n);
     else
         // 4 warps of 32 x 32, 3 x 32-row stages: 32.6 TF/s at n = 2^21, 320 x 320 (8 warps of
         // 32 x 16: 31.4; 16-row stages: 29.7-32.2)

@@ -5,6 +5,7 @@
 // rows, and the results are stitched back in rank order.
 #include <cstring>
 #include <exception>
+#include <string>
 #include <thread>
 
 #include "comm.hpp"
@@ -103,8 +104,18 @@ EigenResult solve_multi(int nranks, int ngpus, const GlobalOp& k, const GlobalOp
         });
     }
     for (auto& t : th) t.join();
-    for (auto& e : err)
-        if (e) std::rethrow_exception(e);
+    // rethrow the root cause: the other ranks only report that a peer aborted the group
+    std::exception_ptr first;
+    for (auto& e : err) {
+        if (!e) continue;
+        if (!first) first = e;
+        try {
+            std::rethrow_exception(e);
+        } catch (const std::exception& x) {
+            if (std::string(x.what()).find("another rank failed") == std::string::npos) throw;
+        }
+    }
+    if (first) std::rethrow_exception(first);
     EigenResult out = res[0];
     const int64_t h = static_cast<int64_t>(out.lambdas.size());
     out.x = BlockVectors(n, h);

@@ -17,6 +17,11 @@ void throw_cuda(cudaError_t e, const char* what, const char* file, int line) {
 
 Comm::~Comm() = default;
 
+std::mutex& Runtime::setup_mutex() {
+    static std::mutex mu;
+    return mu;
+}
+
 Runtime& Runtime::get() {
     thread_local Runtime rt;
     return rt;

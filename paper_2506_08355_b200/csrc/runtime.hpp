@@ -6,6 +6,7 @@
 
 #include <map>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -58,12 +59,19 @@ public:
         if (comm_ && comm_->size() > 1) comm_->allreduce_sum(dev, count, stream_);
     }
     // Per-device one-time kernel attribute setup (bit per device id).
-    bool first_use(unsigned& mask) {
+    // Per-device one-time setup (kernel attributes), thread-safe: ranks sharing a device (one
+    // thread each) wait until the first caller's setup is done -- publishing the bit before the
+    // attribute call let a second rank launch without it (cudaErrorInvalidValue).
+    template <class F>
+    void once_per_device(unsigned& mask, F&& setup) {
         const unsigned bit = 1u << (device_ & 31);
-        if (mask & bit) return false;
-        mask |= bit;
-        return true;
+        if (__atomic_load_n(&mask, __ATOMIC_ACQUIRE) & bit) return;
+        std::lock_guard<std::mutex> lk(setup_mutex());
+        if (mask & bit) return;
+        setup();
+        __atomic_fetch_or(&mask, bit, __ATOMIC_RELEASE);
     }
+    static std::mutex& setup_mutex();
 
     cudaStream_t stream() const { return stream_; }
     int device() const { return device_; }

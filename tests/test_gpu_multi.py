@@ -106,3 +106,34 @@ def test_nccl_single_rank_comm(golden_solves):
     finally:
         bosp.comm_free()
     check_result(res, golden_solves["tm1_t0_n300"]["lambdas"], 1e-10, 4)
+
+
+# ---- the round-2 config families under the row partition ----------------------------------
+
+def test_partitioned_config5_as_configured():
+    """Config 5 as configured (nev 500, nb 64, moving with repeated locking, d = 320) at 64^2 over
+    2 ranks (grid rows split, halo rows, allreduced Grams, grouped locked-basis projections)
+    against the unmodified reference's run (tests/golden/golden_config5_m64.json)."""
+    from tests.test_gpu_configs import golden
+    g = golden("config5_m64")
+    p = P.config5(64)
+    res = bosp.solve_multi(2, p.K, p.M, bosp.BospConfig(**p.cfg), bosp.GeneralizedNullspace(p.x0, p.y0))
+    check_result(res, g["lambdas"], 1e-8, 500)
+
+
+def test_partitioned_config4_dense():
+    """Config 4's dense BSE-like family at n = 4096 over 2 ranks (allgather of X, each rank's rows
+    of A^T) against the reference (tests/golden/golden_config4_n4096.json)."""
+    from tests.test_gpu_configs import golden
+    g = golden("config4_n4096")
+    p = P.config4(n=4096)
+    res = bosp.solve_multi(2, p.K, p.M, bosp.BospConfig(**p.cfg), bosp.GeneralizedNullspace(p.x0, p.y0))
+    check_result(res, g["lambdas"], 1e-8, 32)
+
+
+def test_partitioned_config3_as_configured_m32():
+    from tests.test_gpu_configs import golden
+    g = golden("config3_m32")
+    p = P.config3(32)
+    res = bosp.solve_multi(4, p.K, p.M, bosp.BospConfig(**p.cfg), bosp.GeneralizedNullspace(p.x0, p.y0))
+    check_result(res, g["lambdas"], 1e-8, 100)
