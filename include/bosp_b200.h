@@ -180,10 +180,11 @@ typedef struct {
 } bosp_global_op;
 
 /* nranks row-partitioned ranks as threads of this process over ngpus devices (round-robin;
- * <= 0: all visible).  Several ranks may share a GPU.  Outputs as bosp_solve, eigenvectors in
- * global row order; stats: max wall/device time over ranks. */
+ * <= 0: all visible).  Several ranks may share a GPU.  B (nullable): the inner-product weight,
+ * partitioned like K and M.  Outputs as bosp_solve, eigenvectors in global row order; stats:
+ * max wall/device time over ranks. */
 bosp_status bosp_solve_multi(int32_t nranks, int32_t ngpus, const bosp_global_op* K,
-                             const bosp_global_op* M, const bosp_config* cfg, int64_t r,
+                             const bosp_global_op* M, const bosp_global_op* B, const bosp_config* cfg, int64_t r,
                              const double* x0, const double* y0, int64_t cap, double* lambdas,
                              double* x, double* y, double* residuals, int64_t* nout,
                              bosp_stats* stats);

@@ -338,8 +338,17 @@ def read_matrix_market(path):
 
 
 # ---- row-partitioned ranks ---------------------------------------------------------------
+def _same_nccl_as_torch():
+    """Load torch's NCCL first (when torch is installed) so the library's dlopen reuses it."""
+    try:
+        import torch  # noqa: F401
+    except Exception:
+        pass
+
+
 def comm_nccl_unique_id() -> bytes:
     """ncclGetUniqueId: rank 0 creates it and broadcasts the 128 bytes (e.g. torch.distributed)."""
+    _same_nccl_as_torch()
     buf = (C.c_ubyte * 128)()
     check(lib().bosp_comm_nccl_unique_id(buf))
     return bytes(buf)
@@ -348,6 +357,7 @@ def comm_nccl_unique_id() -> bytes:
 def comm_init_nccl(uid: bytes, nranks: int, rank: int, n_global: int, row0: int):
     """Attach an NCCL communicator and this rank's row window [row0, ...) to the calling thread;
     afterwards solve() on partitioned operators returns this rank's rows of x, y."""
+    _same_nccl_as_torch()
     buf = (C.c_ubyte * 128).from_buffer_copy(uid)
     check(lib().bosp_comm_init_nccl(buf, C.c_int32(nranks), C.c_int32(rank), C.c_int64(n_global),
                                     C.c_int64(row0)))
@@ -412,11 +422,13 @@ def _global_op(op):
 
 
 def solve_multi(nranks, K, M, cfg: BospConfig, ns: GeneralizedNullspace | None = None, ngpus=0,
-                want_vectors=True) -> EigenResult:
+                want_vectors=True, B=None) -> EigenResult:
     """Row-partitioned solve: nranks ranks as threads of this process over ngpus devices
-    (several may share one GPU).  K, M: global problems.Csr / problems.Stencil / dense arrays."""
+    (several may share one GPU).  K, M (and the inner-product weight B): global problems.Csr /
+    problems.Stencil / dense arrays."""
     gk, kk = _global_op(K)
     gm, km = _global_op(M)
+    gb, kb = _global_op(B) if B is not None else (None, None)
     n = gk.n
     cap = cfg.nev
     lam, res = np.zeros(cap), np.zeros(cap)
@@ -428,7 +440,8 @@ def solve_multi(nranks, K, M, cfg: BospConfig, ns: GeneralizedNullspace | None =
     else:
         x0, y0 = _f(ns.x0), _f(ns.y0)
         r = x0.shape[1]
-    check(lib().bosp_solve_multi(C.c_int32(nranks), C.c_int32(ngpus), C.byref(gk), C.byref(gm), C.byref(cc),
+    check(lib().bosp_solve_multi(C.c_int32(nranks), C.c_int32(ngpus), C.byref(gk), C.byref(gm),
+                                 None if gb is None else C.byref(gb), C.byref(cc),
                                  C.c_int64(r), _p(x0), _p(y0), C.c_int64(cap), _p(lam), _p(x), _p(y), _p(res),
                                  C.byref(nout), C.byref(st)))
     del kk, km

@@ -383,6 +383,7 @@ bosp_status bosp_comm_free(void) {
 }
 
 bosp_status bosp_solve_multi(int32_t nranks, int32_t ngpus, const bosp_global_op* K, const bosp_global_op* M,
+                             const bosp_global_op* B,
                              const bosp_config* c, int64_t r, const double* x0, const double* y0, int64_t cap,
                              double* lambdas, double* x, double* y, double* residuals, int64_t* nout,
                              bosp_stats* stats) {
@@ -396,7 +397,9 @@ bosp_status bosp_solve_multi(int32_t nranks, int32_t ngpus, const bosp_global_op
             ns->x0 = host_block(x0, k.n, r);
             ns->y0 = host_block(y0, k.n, r);
         }
-        bosp::EigenResult res = bosp::solve_multi(nranks, ngpus, k, m, bosp::InnerProduct{}, cfg, ns);
+        bosp::GlobalOp bg;
+        if (B) bg = global_of(B);
+        bosp::EigenResult res = bosp::solve_multi(nranks, ngpus, k, m, B ? &bg : nullptr, cfg, ns);
         write_result(res, cfg, cap, lambdas, x, y, residuals, nout, stats, nullptr, 0, nullptr);
     });
 }

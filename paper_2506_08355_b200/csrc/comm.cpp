@@ -120,7 +120,11 @@ const NcclApi& nccl() {
     static NcclApi api = [] {
         NcclApi a;
         // prefer an already-loaded libnccl (e.g. torch's), else the system one
-        a.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        // Reuse an NCCL the process already loaded (e.g. torch's bundled one: loading the older
+        // system libnccl.so.2 first would make a later `import torch` resolve its NCCL symbols
+        // against it and fail); otherwise load it privately (RTLD_LOCAL).
+        a.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!a.h) a.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
         if (!a.h) throw CudaError("NcclComm: cannot dlopen libnccl.so.2");
         auto sym = [&](const char* n) {
             void* s = dlsym(a.h, n);

@@ -59,12 +59,12 @@ LinearOperator local_operator(const GlobalOp& op, const RowSlice& s) {
     throw ContractViolation("local_operator: unknown kind");
 }
 
-EigenResult solve_multi(int nranks, int ngpus, const GlobalOp& k, const GlobalOp& m, const InnerProduct& ip,
+EigenResult solve_multi(int nranks, int ngpus, const GlobalOp& k, const GlobalOp& m, const GlobalOp* b,
                         const BospConfig& cfg, const std::optional<GeneralizedNullspace>& ns,
                         std::vector<SolverStats>* rank_stats) {
     require(nranks >= 1 && nranks <= kMaxRanks, "solve_multi: 1..16 ranks");
-    require(!ip.weighted(), "solve_multi: B-weighted inner products are not partitioned yet");
     require(k.n == m.n, "solve_multi: K and M dimension mismatch");
+    require(!b || b->n == k.n, "solve_multi: B dimension mismatch");
     if (ngpus <= 0) BOSP_CUDA(cudaGetDeviceCount(&ngpus));
     const int64_t n = k.n;
     auto group = std::make_shared<ThreadGroup>(nranks);
@@ -83,6 +83,8 @@ EigenResult solve_multi(int nranks, int ngpus, const GlobalOp& k, const GlobalOp
                 slices[r] = s;
                 rt.set_rows(n, s.row0);
                 LinearOperator kl = local_operator(k, s), ml = local_operator(m, s);
+                // B's rows follow the same slice (a stencil slice is whole planes, still rows)
+                const InnerProduct ipl = b ? InnerProduct(local_operator(*b, s)) : InnerProduct{};
                 std::optional<GeneralizedNullspace> nl;
                 if (ns) {
                     nl.emplace();
@@ -94,7 +96,7 @@ EigenResult solve_multi(int nranks, int ngpus, const GlobalOp& k, const GlobalOp
                         std::memcpy(nl->y0.col(c).data(), ns->y0.col(c).data() + s.row0, sizeof(double) * s.n);
                     }
                 }
-                res[r] = solve(kl, ml, InnerProduct{}, cfg, std::move(nl));
+                res[r] = solve(kl, ml, ipl, cfg, std::move(nl));
                 rt.sync();
                 rt.set_comm(nullptr);
             } catch (...) {

@@ -32,7 +32,9 @@ LinearOperator local_operator(const GlobalOp& op, const RowSlice& s);
 // nranks ranks on ngpus devices (round-robin; ngpus <= 0 -> all visible).  Eigenvectors are
 // returned assembled in global row order; stats are rank 0's with max wall/device time.  No
 // nullspace -> each rank runs the partitioned compute_nullspace (as bosp::solve does).
-EigenResult solve_multi(int nranks, int ngpus, const GlobalOp& k, const GlobalOp& m, const InnerProduct& ip,
+// b (nullable): a B-weighted inner product (inner_product.hpp:12-29); each rank applies its rows
+// of B (halo rows / planes exchanged as for K and M).
+EigenResult solve_multi(int nranks, int ngpus, const GlobalOp& k, const GlobalOp& m, const GlobalOp* b,
                         const BospConfig& cfg, const std::optional<GeneralizedNullspace>& ns,
                         std::vector<SolverStats>* rank_stats = nullptr);
 

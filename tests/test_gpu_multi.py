@@ -137,3 +137,20 @@ def test_partitioned_config3_as_configured_m32():
     p = P.config3(32)
     res = bosp.solve_multi(4, p.K, p.M, bosp.BospConfig(**p.cfg), bosp.GeneralizedNullspace(p.x0, p.y0))
     check_result(res, g["lambdas"], 1e-8, 100)
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_partitioned_weighted_sparse_B(nranks):
+    """SURVEY 8(f)2 under the row partition: the sparse FEM mass matrix B applied per rank (halo
+    rows like K and M), nullspace detected by the partitioned detector under B, against the
+    unmodified reference's run (tests/golden/golden_weighted_massB_n2000.json)."""
+    from tests.golden.make_golden_configs import weighted_case
+    from tests.test_gpu_configs import golden
+    g = golden("weighted_massB_n2000")
+    c = weighted_case(2000)
+    res = bosp.solve_multi(nranks, c["K"], c["M"], bosp.BospConfig(**c["cfg"]), B=c["B"])
+    assert res.converged and res.nev_converged == 6
+    assert np.max(np.abs(res.lambdas - np.asarray(g["lambdas"])) / np.asarray(g["lambdas"])) < 1e-10
+    assert res.residuals.max() < c["cfg"]["tol"]
+    gxy = res.x.T @ (c["B"].scipy() @ res.y)
+    assert np.abs(gxy - np.eye(6)).max() < 1e-10
