@@ -151,6 +151,46 @@ void dev_biorth_against(const std::vector<DevBasis>& bases, const DMat& w, const
     }
 }
 
+void dev_project_sampled(const std::vector<DevBasis>& bases, const DMat& w, const DMat& z,
+                         const std::vector<DenseMatrix>& cross) {
+    const int64_t m = w.cols;
+    if (m == 0) return;
+    require(cross.size() == 2 * bases.size(), "project_sampled: one Gram pair per basis");
+    size_t i = 0;
+    while (i < bases.size()) {
+        ColList pl, ql;
+        std::vector<size_t> idx;
+        int64_t k = 0;
+        for (; i < bases.size() && pl.nseg < kMaxSeg; ++i) {
+            if (bases[i].p.cols == 0) continue;
+            pl.add(bases[i].p);
+            ql.add(bases[i].q);
+            idx.push_back(i);
+            k += bases[i].p.cols;
+        }
+        if (k == 0) continue;
+        DenseMatrix cw(k, m), cz(k, m);  // the bases' Grams stacked in segment order
+        int64_t r0 = 0;
+        for (size_t b : idx) {
+            const DenseMatrix& gw = cross[2 * b];
+            const DenseMatrix& gz = cross[2 * b + 1];
+            require(gw.cols() == m && gz.cols() == m, "project_sampled: Gram width mismatch");
+            for (int64_t c = 0; c < m; ++c)
+                for (int64_t r = 0; r < gw.rows(); ++r) {
+                    cw(r0 + r, c) = gw(r, c);
+                    cz(r0 + r, c) = gz(r, c);
+                }
+            r0 += gw.rows();
+        }
+        DBlock c(k, 2 * m);
+        to_device(cw.data(), k, m, k, c.cols(0, m));
+        to_device(cz.data(), k, m, k, c.cols(m, m));
+        ProductJob pj[2] = {{pl, c.data(), c.ld(), static_cast<int32_t>(m), w.p, w.ld, -1.0, 1.0},
+                            {ql, c.data() + m * c.ld(), c.ld(), static_cast<int32_t>(m), z.p, z.ld, -1.0, 1.0}};
+        product(pj, 2, w.rows);
+    }
+}
+
 // ---------------------------------------------------------------------------------------------
 // MGS-Biorth: Grams of the pair -> exact column recurrence on the host in coefficient space
 // -> P = X A, Q = Y B on the DMMA pipe -> conditional second pass from the Gram of (P, Q).

@@ -33,6 +33,12 @@ struct DevBasis {
 void dev_biorth_against(const std::vector<DevBasis>& bases, const DMat& w, const DMat& z,
                         const InnerProduct& ip);
 
+// biorth_against with the Grams already known: cross[2i] = Q_i^T W, cross[2i+1] = P_i^T Z for
+// bases[i] (unweighted), e.g. sampled by the drift monitor -- products only, up to kMaxSeg bases
+// per launch (one concatenated pass: the bases are mutually biorthogonal).
+void dev_project_sampled(const std::vector<DevBasis>& bases, const DMat& w, const DMat& z,
+                         const std::vector<DenseMatrix>& cross);
+
 struct DevBiorthOutcome {
     int64_t kept = 0;
     std::vector<int64_t> kept_columns, dropped_columns;

@@ -174,11 +174,16 @@ const double* upload_scalars(DeviceState& st, const std::vector<double>& v, int 
 
 // Full MGS repair of (U, V) (bosp_solver.cpp:79-95).  gxy_hint: U^T V of the projected pair when
 // the caller already has it (see sample_invariants) -- the MGS then Grams only U^T U and V^T V.
-void rebiorthogonalize_state(DeviceState& st, const InnerProduct& ip, const DenseMatrix* gxy_hint = nullptr) {
+// cross (optional): the sampled deflation cross-Grams Q_k^T U, P_k^T V of the same (U, V) --
+// the projection against the deflation bases then needs no Grams of its own (config 5: three
+// 128-column locked pairs per repair).
+void rebiorthogonalize_state(DeviceState& st, const InnerProduct& ip, const DenseMatrix* gxy_hint = nullptr,
+                             const std::vector<DenseMatrix>* cross = nullptr) {
     ++st.stats.repairs;
     const int64_t d = st.width();
     const DMat u = st.U.cols(0, d), v = st.V.cols(0, d);
-    dev_biorth_against(deflation_bases(st), u, v, ip);
+    if (cross && !ip.weighted()) dev_project_sampled(deflation_bases(st), u, v, *cross);
+    else dev_biorth_against(deflation_bases(st), u, v, ip);
     DBlock nu(st.n, st.U.capacity()), nv(st.n, st.V.capacity());
     DevBiorthOutcome out = dev_mgs_biorth(u, v, nu.cols(0, d), nv.cols(0, d), ip, 1e-12, false, gxy_hint, true);
     if (!out.dropped_columns.empty())
@@ -195,7 +200,8 @@ void rebiorthogonalize_state(DeviceState& st, const InnerProduct& ip, const Dens
 // the drift repair's MGS would Gram first.  With U' = U - P_k (Q_k^T U), V' = V - Q_k (P_k^T V)
 // and P_k^T Q_k = I: U'^T V' = U^T V - sum_k (Q_k^T U)^T (P_k^T V) -- every term is one of the
 // Grams sampled here (cross terms between bases are products of two cross-Grams, ~1e-26).
-double sample_invariants(DeviceState& st, const InnerProduct& ip, DenseMatrix* projected_gxy = nullptr) {
+double sample_invariants(DeviceState& st, const InnerProduct& ip, DenseMatrix* projected_gxy = nullptr,
+                         std::vector<DenseMatrix>* cross = nullptr) {
     const int64_t d = st.width();
     const DMat u = st.U.cols(0, d), v = st.V.cols(0, d);
     // U^T V and every deflation cross-Gram in one batch, one device->host copy
@@ -213,6 +219,7 @@ double sample_invariants(DeviceState& st, const InnerProduct& ip, DenseMatrix* p
                 for (int64_t r = 0; r < d; ++r) (*projected_gxy)(r, j) -= corr(r, j);
         }
     }
+    if (cross) cross->assign(gs.begin() + 1, gs.end());
     DenseMatrix& g = gs[0];
     for (int64_t i = 0; i < g.rows(); ++i) g(i, i) -= 1.0;
     const double dev = g.max_abs();
@@ -580,9 +587,10 @@ bool iterate_device(DeviceState& st, const LinearOperator& k, const LinearOperat
     // invariant sampling doubles as the drift monitor (:429-432)
     double dev;
     DenseMatrix gxy;
+    std::vector<DenseMatrix> cross;
     {
         auto ph = st.phases.scope(PH_SAMPLE);
-        dev = sample_invariants(st, ip, &gxy);
+        dev = sample_invariants(st, ip, &gxy, &cross);
     }
     if (debug_enabled())
         std::fprintf(stderr, "[bosp] it=%lld wx=%lld wp=%lld ww=%lld frozen=%lld locked=%lld nev_conv=%lld "
@@ -591,7 +599,7 @@ bool iterate_device(DeviceState& st, const LinearOperator& k, const LinearOperat
                      (long long)st.nev_conv, (long long)nb_eff, (long long)c0, dev);
     if (dev > 5e-11) {
         auto ph = st.phases.scope(PH_REPAIR);
-        rebiorthogonalize_state(st, ip, gxy.rows() == st.width() ? &gxy : nullptr);
+        rebiorthogonalize_state(st, ip, gxy.rows() == st.width() ? &gxy : nullptr, &cross);
     }
     return false;
 }
