@@ -296,7 +296,19 @@ RitzOut ritz_step(DeviceState& st, const LinearOperator& k, const LinearOperator
                         {ColList(v), yh, lds, w, st.yt.data(), st.yt.ld(), 1.0, 0.0},
                         {ColList(st.ku.view()), xh, lds, w, st.kxt.data(), st.kxt.ld(), 1.0, 0.0},
                         {ColList(st.mv.view()), yh, lds, w, st.myt.data(), st.myt.ld(), 1.0, 0.0}};
-    product(pj, 4, st.n);
+    // K X~ and M Y~: the reference pulls them back through linearity, (K U) X^ and (M V) Y^
+    // (bosp_solver.cpp:203-206, "no extra matvec").  For operators whose apply is one streaming
+    // pass (stencils, DIA-stored CSR) applying them to X~, Y~ is ~10x cheaper than the d-wide
+    // DMMA products at d >= 128 (configs 3 and 5: 2 x n x 320 x 192 per iteration) -- the same
+    // vectors up to rounding, with the true residual of the stored pairs.
+    if (d >= 128 && k.impl()->cheap_apply() && m.impl()->cheap_apply()) {
+        product(pj, 2, st.n);
+        k.apply_device(st.xt.view(), st.kxt.view());
+        m.apply_device(st.yt.view(), st.myt.view());
+        st.stats.matvec_count += 2 * wxa;
+    } else {
+        product(pj, 4, st.n);
+    }
     return ro;
 }
 

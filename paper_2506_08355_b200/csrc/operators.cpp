@@ -259,6 +259,7 @@ public:
         if (d_.ok && dia_fits(x, y)) dia_spmm(d_.dev, x, y);
         else sell_spmm(s_.dev, x, y);
     }
+    bool cheap_apply() const override { return d_.ok; }
     int apply_dot(const DMat& x, const DMat& y, const SpmmDot& dot) const override {
         if (d_.ok && dia_fits(x, y)) return dia_spmm(d_.dev, x, y, &dot);
         return sell_spmm(s_.dev, x, y, &dot);
@@ -518,6 +519,8 @@ public:
     bool has_masked_dot() const override { return true; }
     bool capturable() const override { return !partitioned_; }
 
+    bool cheap_apply() const override { return true; }
+
 private:
     // Slab partition along the slowest axis: exchange the first / last local plane of every
     // column with the ranks holding the neighbouring slabs (rank - 1 below, rank + 1 above).
@@ -569,6 +572,8 @@ public:
         else axpby(a_, x, 0.0, y);
     }
 
+    bool cheap_apply() const override { return true; }
+
 private:
     double a_;
 };
@@ -584,6 +589,8 @@ public:
         diag_scale(static_cast<const double*>(d_.p), x, y);
     }
 
+    bool cheap_apply() const override { return true; }
+
 private:
     DevFree d_{nullptr};
 };
@@ -597,6 +604,7 @@ public:
         axpby(sigma_, x, 1.0, y);  // y += sigma x (linear_operator.cpp:81-92)
     }
     bool capturable() const override { return base_->capturable(); }
+    bool cheap_apply() const override { return base_->cheap_apply(); }
 
 private:
     std::shared_ptr<const OperatorImpl> base_;

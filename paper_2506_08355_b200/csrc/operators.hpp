@@ -32,6 +32,10 @@ public:
     // apply_dot honours the column mask (converged CG columns cost nothing): unrolled CG graphs
     // are only worth it then -- otherwise every idle iteration would still pay a full apply.
     virtual bool has_masked_dot() const { return false; }
+    // An apply costs about one streaming pass over x and y (stencil, DIA-stored CSR, diagonal):
+    // cheaper than a d-wide DMMA product once d >= 128 (ritz_step then forms K X~ = K (U X^)
+    // instead of (K U) X^).
+    virtual bool cheap_apply() const { return false; }
 
 private:
     static uint64_t next_uid();
