@@ -48,7 +48,7 @@ UNIT = "eigenpairs/s"
 GOLDEN = os.path.join(ROOT, "tests", "golden", "golden_solves.json")
 # B200 outer-iteration count of the config-3 solve (profiles/r2_*; used only to extrapolate the
 # reference's sampled per-iteration time to a full solve when this run's own count is absent)
-C3_ITERS_DEFAULT = 38
+C3_ITERS_DEFAULT = 39
 
 
 def load_peaks():
