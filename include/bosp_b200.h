@@ -219,6 +219,11 @@ bosp_status bosp_test_gram_sym(int64_t n, int64_t a, const double* x, const doub
  * Q = Y B (X, Y n x k; A, B k x kb; k, kb <= 32) and g = P^T Q (kb x kb) from the same kernel. */
 bosp_status bosp_test_biorth_apply(int64_t n, int64_t k, int64_t kb, const double* x, const double* y,
                                    const double* a, const double* b, double* p, double* q, double* g);
+/* Test hook (no reference counterpart): the solver's device MGS-Biorth (mgs_biorth,
+ * biorth.cpp:102-109, as the outer iteration runs it: pair Gram, device or host coefficients,
+ * fused application, second pass).  P, Q n x m get the kept columns; *nkept, *second_pass. */
+bosp_status bosp_test_mgs_dev(int64_t n, int64_t m, const double* x, const double* y, double* p, double* q,
+                              int64_t* nkept, int32_t* second_pass);
 bosp_status bosp_block_product(int64_t n, int64_t a, int64_t b, const double* x, const double* c,
                                double* out);
 /* Y (n x b) -= X C  (block_axpy, kernels.cpp:89-104). */

@@ -92,6 +92,7 @@ EXPORTED = [
     "bosp_bench_apply", "bosp_bench_blas", "bosp_bench_cg", "bosp_op_csr_rows", "bosp_op_dense_rows",
     "bosp_comm_nccl_unique_id", "bosp_comm_init_nccl", "bosp_comm_free", "bosp_solve_multi",
     "bosp_read_matrix_market", "bosp_op_matrix_market", "bosp_test_gram_jobs", "bosp_test_biorth_apply", "bosp_test_gram_sym",
+    "bosp_test_mgs_dev",
 ]
 
 

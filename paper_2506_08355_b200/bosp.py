@@ -524,6 +524,18 @@ def _test_biorth_apply(x, y, a, b):
     return p, q, g
 
 
+def _test_mgs_dev(x, y):
+    """Test hook: the solver's device MGS-Biorth -> (P, Q, second_pass) of the kept columns."""
+    x, y = _f(x), _f(y)
+    n, m = x.shape
+    p = np.zeros((n, m), order="F")
+    q = np.zeros((n, m), order="F")
+    nk, sp = C.c_int64(), C.c_int32()
+    check(lib().bosp_test_mgs_dev(C.c_int64(n), C.c_int64(m), _p(x), _p(y), _p(p), _p(q), C.byref(nk), C.byref(sp)))
+    k = nk.value
+    return p[:, :k].copy(order="F"), q[:, :k].copy(order="F"), bool(sp.value)
+
+
 def block_product(x, c):
     x, c = _f(x), _f(c)
     if x.shape[1] != c.shape[0]:
@@ -726,7 +738,7 @@ def bench_cg(op, ncols, iters=20, reps=5):
 
 def bench_blas(kind, n, a, b, reps=20):
     """kind: 'gram' | 'product' | 'axpy' -> mean ms per call on device-resident data."""
-    k = {"gram": 0, "product": 1, "axpy": 2, "gram3": 3, "gramsym": 4, "mgsapply": 5}[kind]
+    k = {"gram": 0, "product": 1, "axpy": 2, "gram3": 3, "gramsym": 4, "mgsapply": 5, "mgs": 6, "mgs_cold": 7}[kind]
     ms = C.c_double()
     check(lib().bosp_bench_blas(C.c_int32(k), C.c_int64(n), C.c_int64(a), C.c_int64(b),
                                 C.c_int64(reps), C.byref(ms)))

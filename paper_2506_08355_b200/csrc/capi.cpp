@@ -165,6 +165,35 @@ double time_reps(int64_t reps, F&& f) {
     return ms / static_cast<double>(std::max<int64_t>(reps, 1));
 }
 
+// Mean device time of f() with the L2 flushed (a 512 MB memset) before every call; only the
+// calls are timed (events per call).
+template <class F>
+double time_reps_cold(int64_t reps, F&& f) {
+    bosp::Runtime& rt = bosp::Runtime::get();
+    f();
+    const size_t fl = size_t(512) << 20;
+    void* buf = nullptr;
+    BOSP_CUDA(cudaMalloc(&buf, fl));
+    cudaEvent_t a, b;
+    BOSP_CUDA(cudaEventCreate(&a));
+    BOSP_CUDA(cudaEventCreate(&b));
+    double total = 0.0;
+    for (int64_t i = 0; i < reps; ++i) {
+        BOSP_CUDA(cudaMemsetAsync(buf, static_cast<int>(i & 1), fl, rt.stream()));
+        BOSP_CUDA(cudaEventRecord(a, rt.stream()));
+        f();
+        BOSP_CUDA(cudaEventRecord(b, rt.stream()));
+        rt.sync();
+        float ms = 0.f;
+        BOSP_CUDA(cudaEventElapsedTime(&ms, a, b));
+        total += ms;
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(buf);
+    return total / static_cast<double>(std::max<int64_t>(reps, 1));
+}
+
 bosp::BospConfig cfg_of(const bosp_config* c) {
     bosp::BospConfig cfg;
     cfg.nev = c->nev;
@@ -503,6 +532,23 @@ bosp_status bosp_test_biorth_apply(int64_t n, int64_t k, int64_t kb, const doubl
     });
 }
 
+bosp_status bosp_test_mgs_dev(int64_t n, int64_t m, const double* x, const double* y, double* p, double* q,
+                              int64_t* nkept, int32_t* second_pass) {
+    return guarded([&] {
+        bosp::DBlock xd(n, m), yd(n, m), pd(n, m), qd(n, m);
+        bosp::to_device(x, n, m, n, xd.view());
+        bosp::to_device(y, n, m, n, yd.view());
+        const bosp::DevBiorthOutcome o = bosp::dev_mgs_biorth(xd.view(), yd.view(), pd.view(), qd.view(),
+                                                              bosp::InnerProduct(), 1e-12);
+        *nkept = o.kept;
+        *second_pass = o.second_pass ? 1 : 0;
+        if (o.kept > 0) {
+            bosp::to_host(pd.view().cols_range(0, o.kept), p, n);
+            bosp::to_host(qd.view().cols_range(0, o.kept), q, n);
+        }
+    });
+}
+
 bosp_status bosp_block_product(int64_t n, int64_t a, int64_t b, const double* x, const double* c, double* out) {
     return guarded([&] { copy_out(bosp::block_product(host_block(x, n, a), host_dense(c, a, b)), out); });
 }
@@ -740,6 +786,17 @@ bosp_status bosp_bench_blas(int32_t kind, int64_t n, int64_t a, int64_t b, int64
             *ms = time_reps(reps, [&] {
                 bosp::biorth_apply(x.view(), y.view().cols_range(0, a), z.data(), z.data() + a * z.ld(), z.ld(),
                                    static_cast<int>(a), p.view(), q.view(), g.data(), g.ld());
+            });
+        } else if (kind == 6) {  // one whole MGS-Biorth call (a = b columns): pair Gram, coefficient
+                                 // recurrence, fused apply + check Gram (48 n m bytes)
+            bosp::DBlock p(n, a), q(n, a);
+            *ms = time_reps(reps, [&] {
+                bosp::dev_mgs_biorth(x.view(), y.view().cols_range(0, a), p.view(), q.view(), bosp::InnerProduct(), 1e-12);
+            });
+        } else if (kind == 7) {  // kind 6 with the L2 flushed before every call
+            bosp::DBlock p(n, a), q(n, a);
+            *ms = time_reps_cold(reps, [&] {
+                bosp::dev_mgs_biorth(x.view(), y.view().cols_range(0, a), p.view(), q.view(), bosp::InnerProduct(), 1e-12);
             });
         } else if (kind == 4) {  // the same three blocks as one symmetric Gram of Z = [X | Y]
             bosp::DBlock z(a + b, a + b);

@@ -45,8 +45,24 @@ void product(const ProductJob* jobs, int njobs, int64_t n);
 // MGS-Biorth application fused with its check Gram (x, y widths and kb <= 32): P = X A,
 // Q = Y B for the k x kb coefficient matrices A (ca) and B (cb) with leading dimension ldc, and
 // G = P^T Q (kb x kb, ldg) from the same pass -- one launch + the split reduction.
+// col_kend (optional host array of kb): rows of A and B that can be nonzero per column (the
+// triangular coefficients of the first pass) -- the K loop of a column block stops there.
+// status_dev (optional device int): nonzero at run time -> the kernel does nothing (coefficients
+// produced on the device that turned out invalid; the caller redoes the block).
 void biorth_apply(const DMat& x, const DMat& y, const double* ca, const double* cb, int64_t ldc, int kb,
-                  const DMat& p, const DMat& q, double* g, int64_t ldg);
+                  const DMat& p, const DMat& q, double* g, int64_t ldg, const int32_t* col_kend = nullptr,
+                  const int* status_dev = nullptr);
+// MGS-Biorth coefficients of an m <= 32 column block on the device (coef_dev.cu): reads Gxx, Gxy,
+// Gyy from the pair Gram z = [X | Y]^T [X | Y] (2m x 2m, ldz), writes A | B (m x 2m, ldc; upper
+// triangular) and *status = 0, or *status = 1 when a pivot is zero / a column would be dropped
+// or cancels (the host's column-sequential recurrence must decide those).
+void coef_mgs_dev(const double* z, int64_t ldz, int m, double* c, int64_t ldc, int* status, double drop_tol,
+                  double cancel_tol);
+// The pair Gram g = Z^T Z of Z = [X | Y] (2m <= 56 columns, single rank, n >= 8192) with the
+// coefficients of coef_mgs_dev fused into its split reduction.  false: not applicable (the
+// caller runs gram + allreduce + coef_mgs_dev).
+bool gram_pair_coef(const ColList& z, int64_t n, double* g, int64_t ldg, double* c, int64_t ldc, int* status,
+                    double drop_tol, double cancel_tol);
 inline void product(const ColList& a, const double* c, int64_t ldc, int32_t b, const DMat& out,
                     double alpha, double beta) {
     ProductJob j{a, c, ldc, b, out.p, out.ld, alpha, beta};

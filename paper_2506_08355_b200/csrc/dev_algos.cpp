@@ -1,11 +1,13 @@
-#include <chrono>
-#include <cstdio>
 // Device orchestration of the biorthogonalization and inner-CG building blocks.
 #include "dev_algos.hpp"
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
+#include <cstring>
+#include <numeric>
 
 #include "operators.hpp"
 
@@ -233,7 +235,11 @@ DenseMatrix apply_coefs_gram(const DMat& x, const DMat& y, const DenseMatrix& a,
     DBlock c(m, 2 * k), g(k, k);
     to_device(a.data(), m, k, m, c.cols(0, k));
     to_device(b.data(), m, k, m, c.cols(k, k));
-    biorth_apply(x, y, c.data(), c.data() + k * c.ld(), c.ld(), static_cast<int>(k), p, q, g.data(), g.ld());
+    // triangular coefficients: each column block's K loop stops at its last nonzero row
+    std::vector<int32_t> ke = last_nonzero_rows(a);
+    const std::vector<int32_t> kbr = last_nonzero_rows(b);
+    for (size_t i = 0; i < ke.size(); ++i) ke[i] = std::max(ke[i], kbr[i]);
+    biorth_apply(x, y, c.data(), c.data() + k * c.ld(), c.ld(), static_cast<int>(k), p, q, g.data(), g.ld(), ke.data());
     Runtime::get().allreduce(g.data(), g.ld() * k);
     DenseMatrix h(k, k);
     to_host(g.view(), h.data(), k);
@@ -332,7 +338,42 @@ DevBiorthOutcome dev_mgs_biorth(const DMat& x, const DMat& y, const DMat& p, con
     int64_t start = 0, kept = 0;
     DenseMatrix gpq_fused;
     bool have_fused = false;
-    for (;;) {
+    // m <= 32, unweighted first pass: pair Gram -> device LDU coefficients -> fused application
+    // and check Gram, with no host round trip between the kernels; one read-back (P^T Q and the
+    // coefficient status) at the end.  A block the LDU cannot decide exactly (a drop, a
+    // cancelling column, a zero pivot) is redone below by the host's column recurrence.
+    static const bool dev_coef = !std::getenv("BOSP_DEV_COEF") || std::atoi(std::getenv("BOSP_DEV_COEF")) != 0;
+    if (dev_coef && !classical && !ip.weighted() && !gxy_hint && m >= 2 && m <= 32 && n >= 8192) {
+        Runtime& rt = Runtime::get();
+        DBlock z(2 * m, 2 * m), c(m, 2 * m), g(m, m + 1);
+        int* status = reinterpret_cast<int*>(g.data() + m * g.ld());
+        if (!gram_pair_coef(ColList(x).add(y), n, z.data(), z.ld(), c.data(), c.ld(), status, drop_tol, kCancel)) {
+            GramJob job{ColList(x).add(y), ColList(x).add(y), z.data(), z.ld()};
+            job.sym = true;
+            gram(&job, 1, n);
+            rt.allreduce(z.data(), z.ld() * 2 * m);
+            coef_mgs_dev(z.data(), z.ld(), static_cast<int>(m), c.data(), c.ld(), status, drop_tol, kCancel);
+        }
+        std::vector<int32_t> ke(static_cast<size_t>(m));
+        std::iota(ke.begin(), ke.end(), 1);  // upper triangular
+        biorth_apply(x, y, c.data(), c.data() + m * c.ld(), c.ld(), static_cast<int>(m), p, q, g.data(), g.ld(),
+                     ke.data(), status);
+        rt.allreduce(g.data(), g.ld() * m);  // P^T Q (every rank took the same decision)
+        std::vector<double> h(static_cast<size_t>(g.ld() * (m + 1)));
+        BOSP_CUDA(cudaMemcpyAsync(h.data(), g.data(), sizeof(double) * h.size(), cudaMemcpyDeviceToHost, rt.stream()));
+        rt.sync();
+        int st = 0;
+        std::memcpy(&st, h.data() + m * g.ld(), sizeof(int));
+        if (st == 0) {
+            gpq_fused = DenseMatrix(m, m);
+            for (int64_t j = 0; j < m; ++j)
+                for (int64_t i = 0; i < m; ++i) gpq_fused(i, j) = h[i + j * g.ld()];
+            have_fused = true;
+            kept = m;
+            for (int64_t j = 0; j < m; ++j) out.kept_columns.push_back(j);
+        }
+    }
+    for (; !have_fused;) {
         const int64_t mr = cx.cols;
         if (mr == 0) break;
         DenseMatrix gxx, gxy, gyy;

@@ -13,10 +13,14 @@
 // Operands are staged global->shared with 16-byte cp.async (LDGSTS) in a 3-stage ring, fed to
 // mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4).  Shared layouts are padded (+4 doubles) so the
 // fragment loads of a half-warp hit 16 distinct 8-byte bank pairs.
+#include <cuda.h>
+
 #include <algorithm>
 #include <cstdlib>
 #include <cstdio>
+#include <string>
 
+#include "coef_ldu.cuh"
 #include "dense_ops.hpp"
 #include "runtime.hpp"
 
@@ -371,6 +375,57 @@ __global__ void __launch_bounds__(kRedElems * kRedGroups) k_gram_reduce(GramPara
     const int nn = tn * BN + r / BM;
     if (m >= job.a.cols() || nn >= job.b.cols()) return;
     gram_store(job, prm.sym[jb], m, nn, s);
+}
+
+// The split reduction of a single-job symmetric Gram (k_gram_reduce) fused with the MGS-Biorth
+// coefficients of the reduced pair Gram: the last block to finish (ticket) runs coef_ldu_cta on
+// G -- one launch less per MGS-Biorth call, and no Gram round trip through the host.
+struct CoefParams {
+    double* c;          // A | B (m x 2m)
+    int64_t ldc;
+    int* status;
+    unsigned* ticket;   // zero on entry, left zero
+    int m;
+    double drop_tol, cancel_tol;
+};
+
+template <int LDP>
+__global__ void __launch_bounds__(kRedElems * kRedGroups) k_gram_reduce_coef(GramParams prm, CoefParams cp) {
+    __shared__ double part_sum[kRedGroups][kRedElems];
+    __shared__ double work[kCoefSmem];
+    __shared__ bool last;
+    const GramJob& job = prm.job[0];
+    const int el = threadIdx.x % kRedElems, grp = threadIdx.x / kRedElems;
+    const int64_t e = static_cast<int64_t>(blockIdx.x) * kRedElems + el;
+    const int64_t total = static_cast<int64_t>(LDP) * LDP;
+    double s0 = 0.0, s1 = 0.0;
+    if (e < total) {
+        const double* part = prm.partial + e;
+        int sp = grp;
+#pragma unroll 4
+        for (; sp + kRedGroups < prm.splits; sp += 2 * kRedGroups) {
+            s0 += __ldcg(part + sp * total);
+            s1 += __ldcg(part + (sp + kRedGroups) * total);
+        }
+        if (sp < prm.splits) s0 += __ldcg(part + sp * total);
+    }
+    part_sum[grp][el] = s0 + s1;
+    __syncthreads();
+    if (grp == 0 && e < total) {
+        double s = 0.0;
+#pragma unroll
+        for (int g = 0; g < kRedGroups; ++g) s += part_sum[g][el];
+        const int m = static_cast<int>(e % LDP), nn = static_cast<int>(e / LDP);
+        if (m < job.a.cols() && nn < job.b.cols()) gram_store(job, true, m, nn, s);
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(cp.ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    coef_ldu_cta(job.g, job.ldg, cp.m, cp.c, cp.ldc, cp.status, cp.drop_tol, cp.cancel_tol, work);
+    if (threadIdx.x == 0) *cp.ticket = 0u;
 }
 
 template <int BM, int BN, int WM, int WN, int GBK = kBK, int GST = kStages>
@@ -1007,6 +1062,297 @@ void launch_skinny_rt(const ProductJob* jobs, int njobs, int64_t n) {
 }
 
 
+// ------------------------------------------------------------------------------------------
+// TMA-staged skinny Grams: the MGS-Biorth pair Gram Z^T Z of Z = [X | Y]
+// ------------------------------------------------------------------------------------------
+// One persistent CTA per SM owns a contiguous range of R-row stages.  A producer warp lands a
+// stage of every column segment with ONE tensor-map TMA load per segment (cp.async.bulk.tensor,
+// completion counted in bytes on the stage's "full" mbarrier), several stages deep; eight
+// consumer warps take alternate 4-row k-steps of a stage, load one fragment double per 8-column
+// block from shared memory and issue the upper fragment pairs on the DMMA pipe (for G = Z^T Z the
+// B fragment of a block is its A fragment), then arrive on the stage's "empty" mbarrier, which
+// releases the slot to the producer -- no CTA-wide barrier in the main loop.
+//
+// The tensor maps are 3-D views of a column-major segment: (16 rows, columns, row groups of 16)
+// with strides (8 B, ld * 8 B, 128 B) and the 128-byte swizzle.  A stage box (16, c, R / 16)
+// lands as 128-byte lines [row group][column] of 16 rows each, the 16-byte chunks of line L
+// XOR-permuted by (L mod 8); a fragment load (4 rows x 8 consecutive columns = 8 lines) then
+// spreads over the banks (at most 2-way per half-warp), while every TMA line is a full 128-byte
+// L2 line of one column.  (Measured on the way there: one 1-D cp.async.bulk per column and stage
+// capped an SM at ~19 requests/us, 2.9 TB/s; 32- and 64-byte lines without swizzle, 1.1-2.2
+// TB/s from DRAM.)  Rows past n are zero-filled by the TMA unit (out-of-bounds row groups); n
+// must be a multiple of 16.  Warps fold in order, CTAs through k_gram_reduce: deterministic.
+constexpr int kTmaWarps = 8;   // consumer warps; warp kTmaWarps is the producer
+constexpr int kTmaMaxSt = 8;   // pipeline depth bound
+constexpr int kTmaSeg = 4;     // tensor maps (column segments) per operand set
+constexpr int kTmaQ = 16;      // rows per 128-byte swizzled line
+
+// Byte offset of element `rr` (0..15) of 128-byte line `line` under the 128-byte swizzle: the
+// 16-byte chunk index XOR (absolute line mod 8); bl = the buffer base's line mod 8.
+__device__ __forceinline__ int swz(int line, int rr, int bl) {
+    return line * 128 + ((((rr >> 1) ^ (line + bl)) & 7) << 4) + ((rr & 1) << 3);
+}
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned cnt) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(cnt));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+// 3-D tiled TMA load of box (16, cols, groups) at coordinates (0, 0, group0)
+__device__ __forceinline__ void tma_load3(void* dst, const CUtensorMap* map, int group0, unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+        ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(0), "r"(group0), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// One segment set: up to kTmaSeg column segments (tensor maps), each `cols` wide, consecutive
+// in the stage buffer.
+struct TmaSegs {
+    CUtensorMap map[kTmaSeg];
+    int cols[kTmaSeg];
+    int off[kTmaSeg];  // box offset in the stage buffer (doubles, 1024-byte aligned)
+    int stage;         // doubles per stage buffer
+    int nseg;
+};
+
+// Encode the 3-D view (qr rows, cols, n / qr row groups) of a column-major segment with a
+// (qr, cols, rows / qr) box, 128-byte swizzle.
+void encode_seg(CUtensorMap* m, const double* p, int64_t ld, int64_t n, int cols, int qr, int rows) {
+    using Fn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                            const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                            CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static Fn fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        BOSP_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q));
+        if (!f || q != cudaDriverEntryPointSuccess) throw CudaError("cuTensorMapEncodeTiled unavailable");
+        return reinterpret_cast<Fn>(f);
+    }();
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(qr), static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(n / qr)};
+    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld) * 8u, static_cast<cuuint64_t>(qr) * 8u};
+    const cuuint32_t box[3] = {static_cast<cuuint32_t>(qr), static_cast<cuuint32_t>(cols), static_cast<cuuint32_t>(rows / qr)};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(p), dims, strides, box, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
+}
+
+// The segments of a ColList as tensor maps; false when TMA cannot stage it (n % 16, alignment,
+// > kTmaSeg segments).  Each segment's box starts 1024-byte aligned in the stage buffer:
+// t.off[s] (doubles), t.stage (doubles per stage).
+bool make_segs(TmaSegs& t, const ColList& cl, int64_t n, int rows) {
+    if (n % kTmaQ != 0 || n < kTmaQ || cl.nseg > kTmaSeg || n / kTmaQ > (1LL << 32)) return false;
+    t.nseg = cl.nseg;
+    int off = 0;
+    for (int s = 0; s < cl.nseg; ++s) {
+        const int cols = cl.start[s + 1] - cl.start[s];
+        if ((reinterpret_cast<uintptr_t>(cl.p[s]) & 15) || ((cl.ld[s] * 8) & 15) || cols > 256) return false;
+        t.cols[s] = cols;
+        t.off[s] = off;
+        off += (cols * rows + 127) / 128 * 128;  // 1024-byte boundary
+        encode_seg(&t.map[s], cl.p[s], cl.ld[s], n, cols, kTmaQ, rows);
+    }
+    t.stage = off;
+    return true;
+}
+
+// Producer side of one stage: arm the full barrier with the stage's bytes, one TMA per segment.
+__device__ __forceinline__ void tma_stage(const TmaSegs& t, double* buf, int rows, int64_t stage,
+                                          unsigned long long* full) {
+    int total = 0;
+    for (int s = 0; s < t.nseg; ++s) total += t.cols[s];
+    mbar_expect_tx(full, static_cast<unsigned>(rows) * 8u * static_cast<unsigned>(total));
+    for (int s = 0; s < t.nseg; ++s)
+        tma_load3(buf + t.off[s], &t.map[s], static_cast<int>(stage * (rows / kTmaQ)), full);
+}
+
+struct GramTmaParams {
+    TmaSegs seg;
+    GramJob job;
+    int64_t n;
+    int64_t stages;     // R-row stages (the last one may be partial: TMA zero-fills)
+    int R, nst;         // rows per stage, pipeline depth
+    int ncols;          // real columns (a == b)
+    int ldp;            // partial layout (k_gram_reduce<ldp, ldp>)
+    double* partial;
+};
+
+template <int F>
+__global__ void __launch_bounds__((kTmaWarps + 1) * 32, 1) k_gram_tma(const __grid_constant__ GramTmaParams prm) {
+    constexpr int C = F * 8, NP = F * (F + 1) / 2;
+    extern __shared__ __align__(1024) double sm[];
+    __shared__ __align__(8) unsigned long long full_bar[kTmaMaxSt], empty_bar[kTmaMaxSt];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int gid = lane >> 2, tig = lane & 3;
+    const int R = prm.R, NST = prm.nst, stage_d = prm.seg.stage;
+    const int64_t s0 = prm.stages * blockIdx.x / gridDim.x, s1 = prm.stages * (blockIdx.x + 1) / gridDim.x;
+    const int64_t mine = s1 - s0;
+    const int nc = prm.ncols;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NST; ++i) {
+            mbar_init(&full_bar[i], 1);
+            mbar_init(&empty_bar[i], kTmaWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    // per fragment block: this lane's first line (bytes / 128, within a stage) and the lines per
+    // row group of its segment; padding columns (past nc) read as zero
+    int fline[F], fstr[F];
+    bool fpad[F];
+#pragma unroll
+    for (int i = 0; i < F; ++i) {
+        int c = i * 8 + gid, s = 0;
+        while (s < prm.seg.nseg && c >= prm.seg.cols[s]) c -= prm.seg.cols[s++];
+        fpad[i] = s >= prm.seg.nseg;
+        fline[i] = fpad[i] ? 0 : prm.seg.off[s] / 16 + c;
+        fstr[i] = fpad[i] ? 0 : prm.seg.cols[s];
+    }
+    const int bl = static_cast<int>(smem_u32(sm) >> 7) & 7;
+    __syncthreads();
+    double acc[NP][2];
+#pragma unroll
+    for (int t = 0; t < NP; ++t) acc[t][0] = acc[t][1] = 0.0;
+    if (warp == kTmaWarps) {
+        if (lane == 0)
+            for (int64_t k = 0; k < mine; ++k) {
+                const int slot = static_cast<int>(k % NST);
+                if (k >= NST) mbar_wait(&empty_bar[slot], static_cast<unsigned>((k / NST - 1) & 1));
+                tma_stage(prm.seg, sm + slot * stage_d, R, s0 + k, &full_bar[slot]);
+            }
+    } else {
+        for (int64_t k = 0; k < mine; ++k) {
+            const int slot = static_cast<int>(k % NST);
+            mbar_wait(&full_bar[slot], static_cast<unsigned>((k / NST) & 1));
+            const char* buf = reinterpret_cast<const char*>(sm + slot * stage_d);
+            for (int ks = warp; ks < R / 4; ks += kTmaWarps) {
+                const int row = ks * 4 + tig, q = row >> 4, rr = row & 15;
+                double f[F];
+#pragma unroll
+                for (int i = 0; i < F; ++i)
+                    f[i] = fpad[i] ? 0.0 : *reinterpret_cast<const double*>(buf + swz(fline[i] + q * fstr[i], rr, bl));
+                int t = 0;
+#pragma unroll
+                for (int i = 0; i < F; ++i)
+#pragma unroll
+                    for (int j = i; j < F; ++j, ++t) dmma(acc[t][0], acc[t][1], f[i], f[j]);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty_bar[slot]);
+        }
+    }
+    __syncthreads();  // the ring is drained
+    // fold the consumer warps in order into red[C x C] (upper fragment pairs only)
+    double* red = sm;
+    for (int w = 0; w < kTmaWarps; ++w) {
+        if (warp == w) {
+            int t = 0;
+#pragma unroll
+            for (int i = 0; i < F; ++i)
+#pragma unroll
+                for (int j = i; j < F; ++j, ++t) {
+                    const int m = i * 8 + gid, nn = j * 8 + 2 * tig;
+                    red[m + nn * C] = (w == 0 ? 0.0 : red[m + nn * C]) + acc[t][0];
+                    red[m + (nn + 1) * C] = (w == 0 ? 0.0 : red[m + (nn + 1) * C]) + acc[t][1];
+                }
+        }
+        __syncthreads();
+    }
+    double* part = prm.partial + static_cast<int64_t>(blockIdx.x) * prm.ldp * prm.ldp;
+    for (int e = threadIdx.x; e < C * C; e += blockDim.x) {
+        const int m = e % C, nn = e / C;
+        if ((m >> 3) > (nn >> 3)) continue;  // lower fragment tiles were not computed
+        if (gridDim.x == 1) {
+            if (m < nc && nn < nc) gram_store(prm.job, true, m, nn, red[e]);
+        } else {
+            part[m + nn * prm.ldp] = red[e];
+        }
+    }
+}
+
+template <int F>
+bool launch_gram_tma(const GramJob& job, int64_t n, const CoefParams* coef = nullptr) {
+    Runtime& rt = Runtime::get();
+    GramTmaParams prm{};
+    constexpr int C = F * 8;
+    const int sms = rt.sm_count();
+    // 128-row stages when every CTA gets >= 24 of them, else 64 (config 2's n = 2^18: 28 each)
+    prm.R = (n / 128) >= 24LL * sms ? 128 : 64;
+    if (!make_segs(prm.seg, job.a, n, prm.R)) return false;
+    prm.job = job;
+    prm.n = n;
+    prm.ncols = job.a.cols();
+    prm.stages = (n + prm.R - 1) / prm.R;
+    const size_t stage_b = sizeof(double) * prm.seg.stage;
+    prm.nst = static_cast<int>(std::min<size_t>(kTmaMaxSt, (200u * 1024u) / stage_b));
+    const size_t smem = std::max(stage_b * prm.nst, sizeof(double) * C * C);
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(sms, prm.stages)));
+    prm.ldp = C <= 32 ? 32 : 64;
+    prm.partial = rt.scratch(static_cast<size_t>(grid) * prm.ldp * prm.ldp);
+    static unsigned attr_mask = 0;
+    rt.once_per_device(attr_mask, [&] {
+        BOSP_CUDA(cudaFuncSetAttribute(k_gram_tma<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    });
+    const double flops = 1.0 * n * prm.ncols * prm.ncols;  // symmetric: the upper half
+    const double bytes = 8.0 * n * prm.ncols;
+    {
+        LaunchScope ls("gram", bytes, flops);
+        k_gram_tma<F><<<grid, (kTmaWarps + 1) * 32, smem, rt.stream()>>>(prm);
+        BOSP_LAUNCH_CHECK();
+    }
+    if (grid > 1) {
+        GramParams gp{};
+        gp.job[0] = job;
+        gp.tiles_n[0] = 1;
+        gp.tiles[0] = 1;
+        gp.sym[0] = 1;
+        gp.splits = grid;
+        gp.partial = prm.partial;
+        gp.job_stride = static_cast<int64_t>(grid) * prm.ldp * prm.ldp;
+        if (coef) {
+            LaunchScope ls("gram_reduce");
+            if (prm.ldp == 32)
+                k_gram_reduce_coef<32><<<dim3(32 * 32 / kRedElems), kRedElems * kRedGroups, 0, rt.stream()>>>(gp, *coef);
+            else
+                k_gram_reduce_coef<64><<<dim3(64 * 64 / kRedElems), kRedElems * kRedGroups, 0, rt.stream()>>>(gp, *coef);
+            BOSP_LAUNCH_CHECK();
+            return true;
+        }
+        LaunchScope ls("gram_reduce");
+        if (prm.ldp == 32)
+            k_gram_reduce<32, 32><<<dim3(32 * 32 / kRedElems, 1, 1), kRedElems * kRedGroups, 0, rt.stream()>>>(gp);
+        else
+            k_gram_reduce<64, 64><<<dim3(64 * 64 / kRedElems, 1, 1), kRedElems * kRedGroups, 0, rt.stream()>>>(gp);
+        BOSP_LAUNCH_CHECK();
+    }
+    if (coef) coef_mgs_dev(job.g, job.ldg, coef->m, coef->c, coef->ldc, coef->status, coef->drop_tol, coef->cancel_tol);
+    return true;
+}
+
+
+bool tma_gram_enabled() {
+    static const int v = std::getenv("BOSP_GRAM_TMA") ? std::atoi(std::getenv("BOSP_GRAM_TMA")) : 1;
+    return v != 0;
+}
+
 void check_aligned(const ColList& cl) {
     for (int s = 0; s < cl.nseg; ++s)
         if ((reinterpret_cast<uintptr_t>(cl.p[s]) & 15) || (cl.ld[s] & 1))
@@ -1039,6 +1385,23 @@ void gram(const GramJob* jobs, int njobs, int64_t n) {
     // 48: config 2 is flat between 32 and 64; at 64 the rounding of config 5's 64-wide Grams
     // pushed its (repair-heavy) run into the reference's NumericalAbort path -- 48 converges
     constexpr int lim = 48;
+    // one symmetric Gram of <= 64 columns (MGS-Biorth's [X | Y] pair Gram) over many rows:
+    // bulk-async staged, one persistent CTA per SM
+    // (57-64 columns: 36 fragment pairs of accumulators spill -- the register kernels below)
+    if (njobs == 1 && jobs[0].sym && amax == bmax && amax <= 56 && n >= 8192 && tma_gram_enabled() &&
+        same_columns(jobs[0].a, jobs[0].b)) {
+        bool done = false;
+        switch ((amax + 7) / 8) {
+            case 1: done = launch_gram_tma<1>(jobs[0], n); break;
+            case 2: done = launch_gram_tma<2>(jobs[0], n); break;
+            case 3: done = launch_gram_tma<3>(jobs[0], n); break;
+            case 4: done = launch_gram_tma<4>(jobs[0], n); break;
+            case 5: done = launch_gram_tma<5>(jobs[0], n); break;
+            case 6: done = launch_gram_tma<6>(jobs[0], n); break;
+            default: done = launch_gram_tma<7>(jobs[0], n); break;
+        }
+        if (done) return;
+    }
     if (amax <= lim && bmax <= lim) {
         const int mt = (amax + 7) / 8, nt = (bmax + 7) / 8;
         // a symmetric Gram up to 48 columns ([X | Y] of MGS-Biorth, m <= 24): every warp holds
@@ -1085,6 +1448,26 @@ void gram(const GramJob* jobs, int njobs, int64_t n) {
         launch_gram<64, 64, 2, 2>(jobs, njobs, n);
 }
 
+bool gram_pair_coef(const ColList& z, int64_t n, double* g, int64_t ldg, double* c, int64_t ldc, int* status,
+                    double drop_tol, double cancel_tol) {
+    const int w = z.cols();
+    if (w < 2 || (w & 1) || w > 56 || w / 2 > kCoefM || n < 8192 || !tma_gram_enabled() || Runtime::get().nranks() > 1)
+        return false;
+    check_aligned(z);
+    GramJob job{z, z, g, ldg};
+    job.sym = true;
+    CoefParams cp{c, ldc, status, Runtime::get().tickets(1), w / 2, drop_tol, cancel_tol};
+    switch ((w + 7) / 8) {
+        case 1: return launch_gram_tma<1>(job, n, &cp);
+        case 2: return launch_gram_tma<2>(job, n, &cp);
+        case 3: return launch_gram_tma<3>(job, n, &cp);
+        case 4: return launch_gram_tma<4>(job, n, &cp);
+        case 5: return launch_gram_tma<5>(job, n, &cp);
+        case 6: return launch_gram_tma<6>(job, n, &cp);
+        default: return launch_gram_tma<7>(job, n, &cp);
+    }
+}
+
 namespace {
 // ------------------------------------------------------------------------------------------
 // Fused MGS-Biorth application: P = X A, Q = Y B and the check Gram P^T Q in one pass
@@ -1107,12 +1490,14 @@ struct BiorthApplyParams {
     double *p, *q;
     int64_t ldp, ldq, n, tiles;
     double* partial;
+    const int* status;  // optional device flag: nonzero -> the coefficients are invalid, no work
 };
 
 template <int BN>
 __global__ void __launch_bounds__(256) k_biorth_apply(BiorthApplyParams prm) {
     constexpr int NT = BN / 8;
     extern __shared__ __align__(16) double smem[];
+    if (prm.status && *prm.status) return;
     const int kp = prm.kp, ldcs = prm.ldcs;
     double* sca = smem;                        // [BN][ldcs]
     double* scb = sca + BN * ldcs;             // [BN][ldcs]
@@ -1270,15 +1655,319 @@ void launch_biorth_apply(BiorthApplyParams prm, int64_t n, double* g, int64_t ld
         BOSP_LAUNCH_CHECK();
     }
 }
+
+// The same fused application with TMA staging: one persistent CTA per SM owns a contiguous range
+// of 64-row stages of X and Y (one 3-D tensor-map load per operand and stage -- box (16 rows, k
+// columns, 4 row groups), 128-byte swizzle, see k_gram_tma -- issued by a producer warp into a several-deep
+// mbarrier ring); consumer warp w computes rows 8w..8w+7 of P and Q from the stage, releases
+// the stage, streams its rows out and feeds them into its P^T Q fragments from a warp-private
+// shared strip.  Compile-time widths: the k loop is unrolled and the coefficient fragments stay
+// in registers (the kernel is issue-bound: ncu saw ~650 instructions per 8 rows, 7 % DMMA, with
+// a runtime k loop, per-row coefficient reloads and per-column store guards).
+struct BiorthTmaParams {
+    TmaSegs seg;            // X (k columns), Y (k columns)
+    const double *ca, *cb;
+    int64_t ldc;
+    int k, kb, kp;
+    int tri;                // coefficients upper triangular (column c: rows <= c)
+    double *p, *q;
+    int64_t ldp, ldq, n, stages;
+    int nst;
+    double* partial;
+    const int* status;  // optional device flag: nonzero -> the coefficients are invalid, no work
+};
+// 8-row blocks per consumer warp (two: each coefficient fragment feeds two DMMAs; one at 32
+// columns, whose accumulators would not fit in the 168 registers of a 9-warp CTA)
+constexpr int ba_mb(int bn) { return bn >= 32 ? 1 : 2; }
+constexpr int ba_rows(int bn) { return kTmaWarps * 8 * ba_mb(bn); }  // stage rows
+
+template <int BN, int KP>
+__global__ void __launch_bounds__((kTmaWarps + 1) * 32, 1) k_biorth_apply_tma(const __grid_constant__ BiorthTmaParams prm) {
+    constexpr int NT = BN / 8, KS = KP / 4, MB = ba_mb(BN), kBaR = ba_rows(BN), kBaS = kBaR + 4;
+    // coefficient fragments live in registers when they fit (KS x NT x 2 doubles per lane; 9
+    // warps leave 168 registers per thread -- 3 warps share one SM sub-partition's file)
+    constexpr bool kRegC = KS * NT * MB <= 12;
+    extern __shared__ __align__(1024) double sm_bat[];
+    __shared__ __align__(8) unsigned long long full_bar[kTmaMaxSt], empty_bar[kTmaMaxSt];
+    if (prm.status && *prm.status) return;
+    const int k = prm.k, kb = prm.kb, NST = prm.nst;
+    constexpr int ldcs = KP + 4;
+    const int stage_d = prm.seg.stage;
+    double* ring = sm_bat;                  // [NST][X box | Y box], 128-byte lines [row group][column]
+    double* sca = ring + NST * stage_d;     // [BN][ldcs]
+    double* scb = sca + BN * ldcs;          // [BN][ldcs]
+    double* sp = scb + BN * ldcs;           // [BN][kBaS] strip of P rows
+    double* sq = sp + BN * kBaS;            // [BN][kBaS]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int gid = lane >> 2, tig = lane & 3;
+    const int64_t s0 = prm.stages * blockIdx.x / gridDim.x, s1 = prm.stages * (blockIdx.x + 1) / gridDim.x;
+    const int64_t mine = s1 - s0;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NST; ++i) {
+            mbar_init(&full_bar[i], 1);
+            mbar_init(&empty_bar[i], kTmaWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    // A, B -> shared, zero-padded to KP x BN
+    for (int e = threadIdx.x; e < BN * ldcs; e += blockDim.x) {
+        const int c = e / ldcs, kk = e % ldcs;
+        const bool v = c < kb && kk < k;
+        sca[e] = v ? prm.ca[c * prm.ldc + kk] : 0.0;
+        scb[e] = v ? prm.cb[c * prm.ldc + kk] : 0.0;
+    }
+    __syncthreads();
+    double cfa[kRegC ? KS : 1][NT], cfb[kRegC ? KS : 1][NT];
+    if constexpr (kRegC) {
+#pragma unroll
+        for (int s = 0; s < KS; ++s)
+#pragma unroll
+            for (int j = 0; j < NT; ++j) {
+                cfa[s][j] = sca[(j * 8 + gid) * ldcs + 4 * s + tig];
+                cfb[s][j] = scb[(j * 8 + gid) * ldcs + 4 * s + tig];
+            }
+    }
+    double g[NT][NT][2];
+#pragma unroll
+    for (int i = 0; i < NT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) g[i][j][0] = g[i][j][1] = 0.0;
+    const int wr = warp * 8 * MB;  // this warp's MB 8-row blocks: rows wr .. wr + 8 MB - 1
+    // this lane's X / Y fragment addresses: row wr + 8 b + gid of a box (row group wr / 16),
+    // column 4 s + tig; lines of columns 8 apart share the swizzle phase, so k-steps s and s + 2
+    // differ by 8 lines
+    const int bl = static_cast<int>(smem_u32(sm_bat) >> 7) & 7;
+    const int xl = prm.seg.off[0] / 16 + (wr >> 4) * k + tig;
+    const int yl = prm.seg.off[1] / 16 + (wr >> 4) * k + tig;
+    int xa[MB][2], ya[MB][2];
+#pragma unroll
+    for (int b = 0; b < MB; ++b) {
+        const int rr = (wr + 8 * b + gid) & 15;
+        xa[b][0] = swz(xl, rr, bl);
+        xa[b][1] = swz(xl + 4, rr, bl) - 4 * 128;
+        ya[b][0] = swz(yl, rr, bl);
+        ya[b][1] = swz(yl + 4, rr, bl) - 4 * 128;
+    }
+    const bool full_cols = kb == BN, tri = prm.tri != 0;
+    if (warp == kTmaWarps) {
+        if (lane == 0)
+            for (int64_t s = 0; s < mine; ++s) {
+                const int slot = static_cast<int>(s % NST);
+                if (s >= NST) mbar_wait(&empty_bar[slot], static_cast<unsigned>((s / NST - 1) & 1));
+                tma_stage(prm.seg, ring + slot * stage_d, kBaR, s0 + s, &full_bar[slot]);
+            }
+    } else {
+        for (int64_t s = 0; s < mine; ++s) {
+            const int slot = static_cast<int>(s % NST);
+            mbar_wait(&full_bar[slot], static_cast<unsigned>((s / NST) & 1));
+            const char* buf = reinterpret_cast<const char*>(ring + slot * stage_d);
+            double accp[MB][NT][2], accq[MB][NT][2];
+#pragma unroll
+            for (int b = 0; b < MB; ++b)
+#pragma unroll
+                for (int j = 0; j < NT; ++j) accp[b][j][0] = accp[b][j][1] = accq[b][j][0] = accq[b][j][1] = 0.0;
+#pragma unroll
+            for (int ks = 0; ks < KS; ++ks) {
+                const int kr = 4 * ks + tig;
+                const int off = 4 * ks * 128;
+                double fx[MB], fy[MB];
+#pragma unroll
+                for (int b = 0; b < MB; ++b) {
+                    fx[b] = *reinterpret_cast<const double*>(buf + xa[b][ks & 1] + off);
+                    fy[b] = *reinterpret_cast<const double*>(buf + ya[b][ks & 1] + off);
+                    if (4 * ks + 4 > k && kr >= k) fx[b] = fy[b] = 0.0;  // columns past k (last k-step only)
+                }
+#pragma unroll
+                for (int j = 0; j < NT; ++j) {
+                    // triangular coefficients: column block j has nonzero rows < 8 j + 8 only
+                    if (tri && ks > 2 * j + 1) continue;
+                    double ca, cb;
+                    if constexpr (kRegC) {
+                        ca = cfa[ks][j];
+                        cb = cfb[ks][j];
+                    } else {
+                        ca = sca[(j * 8 + gid) * ldcs + kr];
+                        cb = scb[(j * 8 + gid) * ldcs + kr];
+                    }
+#pragma unroll
+                    for (int b = 0; b < MB; ++b) {
+                        dmma(accp[b][j][0], accp[b][j][1], fx[b], ca);
+                        dmma(accq[b][j][0], accq[b][j][1], fy[b], cb);
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty_bar[slot]);  // the stage may be refilled
+#pragma unroll
+            for (int b = 0; b < MB; ++b) {
+                const int lr = wr + 8 * b + gid;
+                const int64_t row = (s0 + s) * kBaR + lr;
+#pragma unroll
+                for (int j = 0; j < NT; ++j)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int col = j * 8 + 2 * tig + h;
+                        sp[col * kBaS + lr] = accp[b][j][h];
+                        sq[col * kBaS + lr] = accq[b][j][h];
+                    }
+                if (full_cols && row < prm.n) {
+#pragma unroll
+                    for (int j = 0; j < NT; ++j)
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int col = j * 8 + 2 * tig + h;
+                            __stcs(prm.p + static_cast<int64_t>(col) * prm.ldp + row, accp[b][j][h]);
+                            __stcs(prm.q + static_cast<int64_t>(col) * prm.ldq + row, accq[b][j][h]);
+                        }
+                } else if (row < prm.n) {
+#pragma unroll
+                    for (int j = 0; j < NT; ++j)
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int col = j * 8 + 2 * tig + h;
+                            if (col < kb) {
+                                __stcs(prm.p + static_cast<int64_t>(col) * prm.ldp + row, accp[b][j][h]);
+                                __stcs(prm.q + static_cast<int64_t>(col) * prm.ldq + row, accq[b][j][h]);
+                            }
+                        }
+                }
+            }
+            __syncwarp();
+            // P^T Q over this warp's rows (rows past n are zero: TMA zero-filled X, Y)
+#pragma unroll
+            for (int s2 = 0; s2 < 8 * MB; s2 += 4) {
+                double fp[NT], fq[NT];
+#pragma unroll
+                for (int i = 0; i < NT; ++i) {
+                    fp[i] = sp[(i * 8 + gid) * kBaS + wr + s2 + tig];
+                    fq[i] = sq[(i * 8 + gid) * kBaS + wr + s2 + tig];
+                }
+#pragma unroll
+                for (int i = 0; i < NT; ++i)
+#pragma unroll
+                    for (int j = 0; j < NT; ++j) dmma(g[i][j][0], g[i][j][1], fp[i], fq[j]);
+            }
+            __syncwarp();  // the strip is rewritten by this warp's next rows
+        }
+    }
+    __syncthreads();
+    // fold the consumer warps in order (reusing the ring), then the CTA partial (32 x 32 layout)
+    double* red = ring;
+    for (int w = 0; w < kTmaWarps; ++w) {
+        if (warp == w) {
+#pragma unroll
+            for (int i = 0; i < NT; ++i)
+#pragma unroll
+                for (int j = 0; j < NT; ++j) {
+                    const int m = i * 8 + gid, nn = j * 8 + 2 * tig;
+                    red[m + nn * BN] = (w == 0 ? 0.0 : red[m + nn * BN]) + g[i][j][0];
+                    red[m + (nn + 1) * BN] = (w == 0 ? 0.0 : red[m + (nn + 1) * BN]) + g[i][j][1];
+                }
+        }
+        __syncthreads();
+    }
+    double* part = prm.partial + static_cast<int64_t>(blockIdx.x) * (32 * 32);
+    for (int e = threadIdx.x; e < BN * BN; e += blockDim.x) {
+        const int m = e % BN, nn = e / BN;
+        part[m + nn * 32] = red[e];
+    }
+}
+
+template <int BN, int KP>
+void launch_biorth_apply_tma(BiorthTmaParams prm, int64_t n, double* g, int64_t ldg, const DMat& pv, const DMat& qv) {
+    Runtime& rt = Runtime::get();
+    const size_t fixed = sizeof(double) * (2ull * BN * (KP + 4) + 2ull * BN * (ba_rows(BN) + 4));
+    const size_t stage_b = sizeof(double) * prm.seg.stage;
+    prm.nst = static_cast<int>(std::max<size_t>(2, std::min<size_t>(kTmaMaxSt, (218u * 1024u - fixed) / stage_b)));
+    const size_t smem = std::max(fixed + stage_b * prm.nst, fixed + sizeof(double) * BN * BN);
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(rt.sm_count(), prm.stages)));
+    prm.partial = rt.scratch(static_cast<size_t>(grid) * 32 * 32);
+    static unsigned attr_mask = 0;
+    rt.once_per_device(attr_mask, [&] {
+        BOSP_CUDA(cudaFuncSetAttribute(k_biorth_apply_tma<BN, KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    });
+    const double flops = 2.0 * n * prm.k * prm.kb * 2 + 2.0 * n * prm.kb * prm.kb;
+    const double bytes = 8.0 * n * (2.0 * prm.k + 2.0 * prm.kb);
+    {
+        LaunchScope ls("product", bytes, flops);
+        k_biorth_apply_tma<BN, KP><<<grid, (kTmaWarps + 1) * 32, smem, rt.stream()>>>(prm);
+        BOSP_LAUNCH_CHECK();
+    }
+    GramParams gp{};
+    gp.job[0] = GramJob{ColList(pv), ColList(qv), g, ldg};
+    gp.tiles_n[0] = 1;
+    gp.tiles[0] = 1;
+    gp.splits = grid;
+    gp.partial = prm.partial;
+    gp.job_stride = static_cast<int64_t>(grid) * 32 * 32;
+    {
+        LaunchScope ls("gram_reduce");
+        k_gram_reduce<32, 32><<<dim3(32 * 32 / kRedElems, 1, 1), kRedElems * kRedGroups, 0, rt.stream()>>>(gp);
+        BOSP_LAUNCH_CHECK();
+    }
+}
+
+// (BN, KP) dispatch: BN = kept columns rounded to 8, KP = X columns rounded to 4 (kb <= k)
+template <int BN>
+void launch_biorth_apply_tma_k(BiorthTmaParams prm, int64_t n, double* g, int64_t ldg, const DMat& pv, const DMat& qv) {
+    switch (prm.kp) {
+        case 4: if constexpr (BN <= 8) return launch_biorth_apply_tma<BN, 4>(prm, n, g, ldg, pv, qv); break;
+        case 8: if constexpr (BN <= 8) return launch_biorth_apply_tma<BN, 8>(prm, n, g, ldg, pv, qv); break;
+        case 12: if constexpr (BN <= 16) return launch_biorth_apply_tma<BN, 12>(prm, n, g, ldg, pv, qv); break;
+        case 16: if constexpr (BN <= 16) return launch_biorth_apply_tma<BN, 16>(prm, n, g, ldg, pv, qv); break;
+        case 20: if constexpr (BN <= 24) return launch_biorth_apply_tma<BN, 20>(prm, n, g, ldg, pv, qv); break;
+        case 24: if constexpr (BN <= 24) return launch_biorth_apply_tma<BN, 24>(prm, n, g, ldg, pv, qv); break;
+        case 28: return launch_biorth_apply_tma<BN, 28>(prm, n, g, ldg, pv, qv);
+        default: return launch_biorth_apply_tma<BN, 32>(prm, n, g, ldg, pv, qv);
+    }
+    throw ContractViolation("biorth_apply: kept columns exceed the block width");
+}
+
+bool tma_apply_enabled() {
+    static const int v = std::getenv("BOSP_APPLY_TMA") ? std::atoi(std::getenv("BOSP_APPLY_TMA")) : 1;
+    return v != 0;
+}
 }  // namespace
 
 void biorth_apply(const DMat& x, const DMat& y, const double* ca, const double* cb, int64_t ldc, int kb,
-                  const DMat& p, const DMat& q, double* g, int64_t ldg) {
+                  const DMat& p, const DMat& q, double* g, int64_t ldg, const int32_t* col_kend,
+                  const int* status_dev) {
     require(x.cols == y.cols && x.rows == y.rows && p.rows == x.rows && q.rows == x.rows, "biorth_apply: shapes");
     require(x.cols <= 32 && kb <= 32 && kb >= 1 && p.cols >= kb && q.cols >= kb, "biorth_apply: widths <= 32");
     check_aligned(ColList(x));
     check_aligned(ColList(y));
     const int64_t n = x.rows;
+    const DMat pv = p.cols_range(0, kb), qv = q.cols_range(0, kb);
+    const int kpad = std::max(4, (static_cast<int>(x.cols) + 3) / 4 * 4);
+    BiorthTmaParams tp{};
+    if (tma_apply_enabled() && n >= 8192 &&
+        make_segs(tp.seg, ColList(x).add(y), n, ba_rows((kb + 7) / 8 * 8))) {
+        const int k = static_cast<int>(x.cols);
+        tp.ca = ca;
+        tp.cb = cb;
+        tp.ldc = ldc;
+        tp.k = k;
+        tp.kb = kb;
+        tp.kp = kpad;
+        // upper triangular (column c nonzero in rows <= c only): the K loop of column block j
+        // stops after row 8 j + 7
+        tp.tri = col_kend != nullptr;
+        for (int c = 0; tp.tri && c < kb; ++c) tp.tri = col_kend[c] <= c + 1;
+        tp.p = p.p;
+        tp.q = q.p;
+        tp.ldp = p.ld;
+        tp.ldq = q.ld;
+        tp.n = n;
+        tp.stages = (n + ba_rows((kb + 7) / 8 * 8) - 1) / ba_rows((kb + 7) / 8 * 8);
+        tp.status = status_dev;
+        switch ((kb + 7) / 8) {
+            case 1: return launch_biorth_apply_tma_k<8>(tp, n, g, ldg, pv, qv);
+            case 2: return launch_biorth_apply_tma_k<16>(tp, n, g, ldg, pv, qv);
+            case 3: return launch_biorth_apply_tma_k<24>(tp, n, g, ldg, pv, qv);
+            default: return launch_biorth_apply_tma_k<32>(tp, n, g, ldg, pv, qv);
+        }
+    }
     BiorthApplyParams prm{};
     prm.x = ColList(x);
     prm.y = ColList(y);
@@ -1287,7 +1976,7 @@ void biorth_apply(const DMat& x, const DMat& y, const double* ca, const double* 
     prm.ldc = ldc;
     prm.k = static_cast<int>(x.cols);
     prm.kb = kb;
-    prm.kp = std::max(4, (prm.k + 3) / 4 * 4);
+    prm.kp = kpad;
     prm.ldcs = (prm.kp + 15) / 16 * 16 + 4;
     prm.p = p.p;
     prm.q = q.p;
@@ -1295,7 +1984,7 @@ void biorth_apply(const DMat& x, const DMat& y, const double* ca, const double* 
     prm.ldq = q.ld;
     prm.n = n;
     prm.tiles = (n + 63) / 64;
-    const DMat pv = p.cols_range(0, kb), qv = q.cols_range(0, kb);
+    prm.status = status_dev;
     switch ((kb + 7) / 8) {
         case 1: return launch_biorth_apply<8>(prm, n, g, ldg, pv, qv);
         case 2: return launch_biorth_apply<16>(prm, n, g, ldg, pv, qv);

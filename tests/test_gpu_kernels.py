@@ -339,8 +339,8 @@ def test_biorth_apply_fused(k, kb, n):
     assert rel(g, pr.T @ qr) < 1e-12
 
 
-@pytest.mark.parametrize("a", [1, 4, 10, 16, 20, 24, 30, 60, 160])
-@pytest.mark.parametrize("n", [7, 20011])
+@pytest.mark.parametrize("a", [1, 4, 10, 16, 20, 24, 28, 30, 60, 160])
+@pytest.mark.parametrize("n", [7, 20011, 262147])
 def test_gram_symmetric(a, n):
     """Symmetric Grams (upper tiles mirrored): the MGS pair Gram of Z = [X | Y] (register path up
     to 48 columns of Z, tiled beyond) and a U^T (K U)-style Gram with distinct operands."""
@@ -357,3 +357,35 @@ def test_gram_symmetric(a, n):
     ref = x.T @ ky
     assert np.array_equal(h, h.T)
     assert rel(h, 0.5 * (ref + ref.T)) < 1e-13
+
+
+@pytest.mark.parametrize("m", [2, 8, 20, 32])
+@pytest.mark.parametrize("n", [8192, 100003])
+def test_mgs_device_coefficients(m, n):
+    """The solver's MGS-Biorth for m <= 32 (pair Gram on bulk-async staging -> LDU coefficients
+    on the device -> fused application): same kept set as the oracle's gs_biorth
+    (biorth.cpp:19-69), P, Q equal to it up to the recurrence's rounding, biorthogonal."""
+    rng = np.random.default_rng(m * 1000 + n % 997)
+    x = np.asfortranarray(rng.uniform(-1, 1, (n, m)))
+    y = np.asfortranarray(x + 0.5 * rng.uniform(-1, 1, (n, m)))
+    p, q, second = bosp._test_mgs_dev(x, y)
+    po, qo, ko, do = O.mgs_biorth(x, y)
+    assert p.shape[1] == len(ko) == m and not do
+    assert rel(p, po) < 1e-10 and rel(q, qo) < 1e-10
+    assert np.abs(p.T @ q - np.eye(m)).max() < 1e-12
+
+
+def test_mgs_device_coefficients_fallback():
+    """A nearly dependent column (cancellation) and an exact duplicate (drop) are decided by the
+    host's column-sequential recurrence, as gs_biorth does in n-space: same kept/dropped sets."""
+    rng = np.random.default_rng(5)
+    n, m = 20000, 12
+    x = np.asfortranarray(rng.uniform(-1, 1, (n, m)))
+    x[:, 7] = x[:, 3]                              # exact duplicate -> dropped
+    x[:, 9] = x[:, 1] + 1e-9 * rng.uniform(-1, 1, n)  # cancels in coefficient space
+    y = np.asfortranarray(x + 0.25 * rng.uniform(-1, 1, (n, m)))
+    y[:, 7] = y[:, 3]
+    p, q, _ = bosp._test_mgs_dev(x, y)
+    po, qo, ko, do = O.mgs_biorth(x, y)
+    assert p.shape[1] == len(ko)
+    assert np.abs(p.T @ q - np.eye(len(ko))).max() < 1e-10

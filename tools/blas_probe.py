@@ -29,6 +29,10 @@ def main():
         ms = bosp.bench_blas(kind, a.n, x, y, reps=a.reps)
         flops = 2.0 * a.n * x * y * (3 if kind in ("gram3", "gramsym") else 1)
         byts = 8.0 * a.n * (x + y) + (8.0 * a.n * y if kind == "axpy" else 0.0)
+        if kind == "mgs":  # X, Y read + P, Q written + the P^T Q check = 48 n m
+            flops, byts = 6.0 * a.n * x * x, 48.0 * a.n * x
+        elif kind == "mgsapply":
+            flops, byts = 6.0 * a.n * x * x, 32.0 * a.n * x
         print(f"{kind:8s} n={a.n} {x}x{y}: {ms * 1e3:9.1f} us  {flops / ms / 1e9:7.2f} TF/s  "
               f"{byts / ms / 1e6:8.1f} GB/s", flush=True)
 
