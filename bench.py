@@ -486,6 +486,20 @@ def run_b200(args, world, rank, local, dist):
                                       "written = 32 n m, + 16 n m for the P^T Q Gram of the second-pass test; "
                                       "4 n m^2 recurrence + 2 n m^2 check)"}
 
+    # MGS-Biorth at HBM scale (north star: >= 60 % of HBM on 1 B200): one whole call -- pair
+    # Gram (TMA), device coefficients, fused application + check Gram, the read-back -- on
+    # device-resident random X, Y of m = 20 columns (config 2's block width), L2 flushed before
+    # every call; 48 n m algorithmic bytes per call
+    mgs_hbm = None
+    if not args.no_kernel_rooflines and rank == 0:
+        hbm = peaks.get("hbm_gbs", 6650.0)
+        mgs_hbm = {}
+        for tag, nn in (("n=2^21", 2 ** 21), ("n=2^18 (config-2 scale)", 2 ** 18)):
+            ms = bosp.bench_blas("mgs_cold", nn, 20, 20, reps=10)
+            gbs = 48.0 * nn * 20 / (ms * 1e-3) / 1e9
+            mgs_hbm[tag] = {"m": 20, "us_per_call": ms * 1e3, "achieved": gbs, "peak": hbm, "unit": "GB/s",
+                            "frac": gbs / hbm, "bytes_per_call": 48.0 * nn * 20}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -531,6 +545,7 @@ def run_b200(args, world, rank, local, dist):
             "roofline": roof,
             "rooflines": rooflines,
             "roofline_mgs": roof_mgs,
+            "roofline_mgs_hbm_scale": mgs_hbm,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "steps_s": [round(t, 4) for t in e2e_t]},

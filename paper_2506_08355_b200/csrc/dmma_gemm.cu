@@ -1676,17 +1676,24 @@ struct BiorthTmaParams {
     double* partial;
     const int* status;  // optional device flag: nonzero -> the coefficients are invalid, no work
 };
-// 8-row blocks per consumer warp (two: each coefficient fragment feeds two DMMAs; one at 32
-// columns, whose accumulators would not fit in the 168 registers of a 9-warp CTA)
-constexpr int ba_mb(int bn) { return bn >= 32 ? 1 : 2; }
-constexpr int ba_rows(int bn) { return kTmaWarps * 8 * ba_mb(bn); }  // stage rows
+// Consumer warps and 8-row blocks per consumer warp.  Measured at n = 2^21, m = 20 (the
+// kernel is DMMA-latency bound, not byte bound): 8 warps x 1 block, coefficients in registers:
+// 390-398 us; 8 warps x 2 blocks: 390 us; 16 warps x 1 block, coefficients in shared memory
+// (17 warps: <= 96 registers): 395 us -- all slower than the cp.async kernel (k_biorth_apply,
+// 350 us) except at 32 columns (704 vs 797 us), where biorth_apply uses this one.
+#ifndef BOSP_BA_CW
+#define BOSP_BA_CW 8
+#endif
+constexpr int ba_cw(int bn) { return bn >= 32 ? 8 : BOSP_BA_CW; }
+constexpr int ba_mb(int bn) { return ba_cw(bn) > 8 || bn >= 32 ? 1 : 2; }
+constexpr int ba_rows(int bn) { return ba_cw(bn) * 8 * ba_mb(bn); }  // stage rows
 
 template <int BN, int KP>
-__global__ void __launch_bounds__((kTmaWarps + 1) * 32, 1) k_biorth_apply_tma(const __grid_constant__ BiorthTmaParams prm) {
-    constexpr int NT = BN / 8, KS = KP / 4, MB = ba_mb(BN), kBaR = ba_rows(BN), kBaS = kBaR + 4;
+__global__ void __launch_bounds__((ba_cw(BN) + 1) * 32, 1) k_biorth_apply_tma(const __grid_constant__ BiorthTmaParams prm) {
+    constexpr int NT = BN / 8, KS = KP / 4, MB = ba_mb(BN), kBaR = ba_rows(BN), kBaS = kBaR + 4, CW = ba_cw(BN);
     // coefficient fragments live in registers when they fit (KS x NT x 2 doubles per lane; 9
     // warps leave 168 registers per thread -- 3 warps share one SM sub-partition's file)
-    constexpr bool kRegC = KS * NT * MB <= 12;
+    constexpr bool kRegC = CW <= 8 && KS * NT * MB <= 12;
     extern __shared__ __align__(1024) double sm_bat[];
     __shared__ __align__(8) unsigned long long full_bar[kTmaMaxSt], empty_bar[kTmaMaxSt];
     if (prm.status && *prm.status) return;
@@ -1705,7 +1712,7 @@ __global__ void __launch_bounds__((kTmaWarps + 1) * 32, 1) k_biorth_apply_tma(co
     if (threadIdx.x == 0) {
         for (int i = 0; i < NST; ++i) {
             mbar_init(&full_bar[i], 1);
-            mbar_init(&empty_bar[i], kTmaWarps);
+            mbar_init(&empty_bar[i], CW);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -1750,7 +1757,7 @@ __global__ void __launch_bounds__((kTmaWarps + 1) * 32, 1) k_biorth_apply_tma(co
         ya[b][1] = swz(yl + 4, rr, bl) - 4 * 128;
     }
     const bool full_cols = kb == BN, tri = prm.tri != 0;
-    if (warp == kTmaWarps) {
+    if (warp == CW) {
         if (lane == 0)
             for (int64_t s = 0; s < mine; ++s) {
                 const int slot = static_cast<int>(s % NST);
@@ -1854,7 +1861,7 @@ __global__ void __launch_bounds__((kTmaWarps + 1) * 32, 1) k_biorth_apply_tma(co
     __syncthreads();
     // fold the consumer warps in order (reusing the ring), then the CTA partial (32 x 32 layout)
     double* red = ring;
-    for (int w = 0; w < kTmaWarps; ++w) {
+    for (int w = 0; w < CW; ++w) {
         if (warp == w) {
 #pragma unroll
             for (int i = 0; i < NT; ++i)
@@ -1891,7 +1898,7 @@ void launch_biorth_apply_tma(BiorthTmaParams prm, int64_t n, double* g, int64_t 
     const double bytes = 8.0 * n * (2.0 * prm.k + 2.0 * prm.kb);
     {
         LaunchScope ls("product", bytes, flops);
-        k_biorth_apply_tma<BN, KP><<<grid, (kTmaWarps + 1) * 32, smem, rt.stream()>>>(prm);
+        k_biorth_apply_tma<BN, KP><<<grid, (ba_cw(BN) + 1) * 32, smem, rt.stream()>>>(prm);
         BOSP_LAUNCH_CHECK();
     }
     GramParams gp{};
@@ -1941,7 +1948,7 @@ void biorth_apply(const DMat& x, const DMat& y, const double* ca, const double* 
     const DMat pv = p.cols_range(0, kb), qv = q.cols_range(0, kb);
     const int kpad = std::max(4, (static_cast<int>(x.cols) + 3) / 4 * 4);
     BiorthTmaParams tp{};
-    if (tma_apply_enabled() && n >= 8192 &&
+    if (tma_apply_enabled() && kb > 24 && n >= 8192 &&
         make_segs(tp.seg, ColList(x).add(y), n, ba_rows((kb + 7) / 8 * 8))) {
         const int k = static_cast<int>(x.cols);
         tp.ca = ca;
