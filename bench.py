@@ -267,6 +267,37 @@ def cublas_dgemm_tflops():
     return peak
 
 
+def cublas_same_shape(bosp, n=2 ** 21):
+    """cuBLAS DGEMM (torch fp64 matmul) on the solver's own dominant shapes next to the library's
+    DMMA kernels on the same device-resident shapes: Gram 320 x 320 over n rows (the Ritz /
+    invariant Grams) and product n x 320 -> 192 (the Ritz pullbacks)."""
+    import torch
+    out = {}
+    for kind, a, b in (("gram", 320, 320), ("product", 320, 192)):
+        x = torch.randn(a, n, dtype=torch.float64, device="cuda")
+        if kind == "gram":
+            y = torch.randn(b, n, dtype=torch.float64, device="cuda")
+            f = lambda: torch.mm(x, y.t())
+        else:
+            y = torch.randn(b, a, dtype=torch.float64, device="cuda")
+            f = lambda: torch.mm(y, x)
+        f()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(5):
+            f()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 5
+        del x, y
+        torch.cuda.empty_cache()
+        own = bosp.bench_blas(kind, n, a, b, reps=5)
+        fl = 2.0 * n * a * b
+        out[f"{kind} {a}x{b} n={n}"] = {"cublas_tflops": fl / ms / 1e9, "b200_kernels_tflops": fl / own / 1e9,
+                                        "ratio": ms / own}
+    return out
+
+
 def family_roofline(fam, rep, step_ms, peaks, dgemm, kind, note=""):
     if not rep or rep["launches"] == 0 or rep["ms"] <= 0:
         return None
@@ -448,8 +479,11 @@ def run_b200(args, world, rank, local, dist):
             if r:
                 r["traffic"] = traffic_for(fam, wl)[0]  # ncu DRAM bytes per launch (committed capture)
                 rooflines[fam] = r
+        same_shape = cublas_same_shape(bosp) if rank == 0 else None
         dom, _kind = DOMINANT.get(wl, ("gram_wide", "tensor"))
         roof = dict(rooflines.get(dom) or {})
+        if roof and roof.get("bound") == "tensor" and same_shape:
+            roof["cublas_same_shape"] = same_shape
         if roof:
             traffic, ent = traffic_for(dom, wl)
             roof["kernel"] = dom
