@@ -278,7 +278,29 @@ k_gram(GramParams prm) {
     // symmetric job, diagonal tile: a warp tile strictly below the diagonal only produces
     // mirrored entries (never stored) -- it keeps the pipeline but leaves the DMMA pipe to the
     // other warps (a quarter of a 2 x 2 diagonal tile's work)
-    const bool idle = prm.sym[jb] && tm == tn && wm0 >= wn0 + WTN;
+    bool idle = prm.sym[jb] && tm == tn && wm0 >= wn0 + WTN;
+    // masked B columns: a fragment group of 8 inactive columns issues no DMMAs; a CTA whose
+    // columns are all inactive does nothing at all (its G columns are never read)
+    bool live[NTL];
+#pragma unroll
+    for (int j = 0; j < NTL; ++j) live[j] = true;
+    if (job.b_active) {
+        bool any_cta = false;
+        for (int c = 0; c < BN && n0 + c < bcols; ++c) any_cta |= job.b_active[n0 + c] != 0;
+        if (!any_cta) return;
+        bool any_warp = false;
+#pragma unroll
+        for (int j = 0; j < NTL; ++j) {
+            bool a8 = false;
+            for (int c = 0; c < 8; ++c) {
+                const int col = n0 + wn0 + j * 8 + c;
+                a8 |= col < bcols && job.b_active[col] != 0;
+            }
+            live[j] = a8;
+            any_warp |= a8;
+        }
+        idle = idle || !any_warp;
+    }
     for (int it = 0; it < nk; ++it) {
         cp_async_wait<kStages - 2>();
         __syncthreads();
@@ -296,7 +318,8 @@ k_gram(GramParams prm) {
 #pragma unroll
                 for (int i = 0; i < MT; ++i)
 #pragma unroll
-                    for (int j = 0; j < NTL; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+                    for (int j = 0; j < NTL; ++j)
+                        if (live[j]) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
             }
         }
         const int nxt = it + kStages - 1;
@@ -316,9 +339,11 @@ k_gram(GramParams prm) {
             for (int j = 0; j < NTL; ++j) {
                 const int m = m0 + wm0 + i * 8 + gid;
                 const int nn = n0 + wn0 + j * 8 + 2 * tig;
-                if (m < acols) {
-                    if (nn < bcols) gram_store(job, prm.sym[jb], m, nn, acc[i][j][0]);
-                    if (nn + 1 < bcols) gram_store(job, prm.sym[jb], m, nn + 1, acc[i][j][1]);
+                if (m < acols && live[j]) {
+                    if (nn < bcols && (!job.b_active || job.b_active[nn]))
+                        gram_store(job, prm.sym[jb], m, nn, acc[i][j][0]);
+                    if (nn + 1 < bcols && (!job.b_active || job.b_active[nn + 1]))
+                        gram_store(job, prm.sym[jb], m, nn + 1, acc[i][j][1]);
                 }
             }
         return;
@@ -374,6 +399,7 @@ __global__ void __launch_bounds__(kRedElems * kRedGroups) k_gram_reduce(GramPara
     const int m = tm * BM + r % BM;
     const int nn = tn * BN + r / BM;
     if (m >= job.a.cols() || nn >= job.b.cols()) return;
+    if (job.b_active && !job.b_active[nn]) return;  // masked column: never computed
     gram_store(job, prm.sym[jb], m, nn, s);
 }
 
@@ -454,13 +480,36 @@ void launch_gram(const GramJob* jobs, int njobs, int64_t n) {
         resident[rt.device() & 63] = std::max(1, r);
     }
     const int kblocks = static_cast<int>((n + kBK - 1) / kBK);
-    // whole waves: tiles x splits just below a multiple of the resident CTA slots (a 1.5-wave
-    // grid leaves half the machine idle for the second wave)
+    // Split count by wave efficiency: tiles x splits CTAs over `slots` resident CTA slots run in
+    // ceil(total / slots) waves.  Among split counts giving at least ~2 waves of CTAs (more CTAs
+    // amortise the tail) with >= 4 stages of work per CTA, <= 16 waves and split partials <= 3 %
+    // of the operand bytes, take the one whose last wave is fullest (ties within 0.5 %: fewer
+    // splits).  (The previous rule, ~2 waves rounded down, gave the dense operator's 128 tiles
+    // 4 splits = 1.73 waves: 774 -> 687 us per apply; a 320 x 320 Gram 4 instead of 2 waves: +3 %.)
     const int slots = resident[rt.device() & 63] * rt.sm_count();
     const int per_split = max_tiles * njobs;
-    const int waves = std::max(1, (3 * rt.sm_count() + slots - 1) / slots);
-    int splits = std::max(1, waves * slots / per_split);
-    splits = std::min(splits, std::max(1, kblocks / 4));  // >= 4 stages of work per CTA
+    double opnd = 0.0;
+    for (int j = 0; j < njobs; ++j) opnd += 8.0 * n * (jobs[j].a.cols() + jobs[j].b.cols());
+    const int pcap = static_cast<int>(std::max(1.0, 0.03 * opnd / (8.0 * BM * BN * per_split)));
+    const int smax = std::max(1, std::min({kblocks / 4, 512, std::max(1, 16 * slots / per_split), pcap}));
+    const int smin = std::min(smax, std::max(1, (19 * slots / 10 + per_split - 1) / per_split));
+    int splits = smin;
+    double best = -1.0;
+    static const bool old_rule = std::getenv("BOSP_SPLIT_OLD") != nullptr;  // A/B switch (measurement)
+    if (old_rule) {
+        const int waves = std::max(1, (3 * rt.sm_count() + slots - 1) / slots);
+        splits = std::min(std::max(1, waves * slots / per_split), std::max(1, kblocks / 4));
+    } else {
+        for (int sp = smin; sp <= smax; ++sp) {
+            const int64_t total = static_cast<int64_t>(sp) * per_split;
+            const int64_t waves = (total + slots - 1) / slots;
+            const double eff = static_cast<double>(total) / static_cast<double>(waves * slots);
+            if (eff > best + 0.005) {
+                best = eff;
+                splits = sp;
+            }
+        }
+    }
     const int kb_per = (kblocks + splits - 1) / splits;
     prm.chunk = static_cast<int64_t>(kb_per) * kBK;
     splits = static_cast<int>((n + prm.chunk - 1) / prm.chunk);
