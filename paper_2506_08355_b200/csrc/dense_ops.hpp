@@ -18,10 +18,6 @@ struct GramJob {
     // are computed and G(i, j), i <= j, is mirrored to G(j, i) -- G exactly symmetric, ~half
     // the DMMA work.  Requires a.cols() == b.cols().
     bool sym = false;
-    // Optional device column mask of B (b.cols() ints): columns with a zero flag need not be
-    // computed -- the tiled kernel skips 8-column fragment groups that are wholly inactive and
-    // leaves their G columns untouched (the CG's dense apply with converged columns).
-    const int* b_active = nullptr;
 };
 void gram(const GramJob* jobs, int njobs, int64_t n);
 inline void gram(const ColList& a, const ColList& b, int64_t n, double* g, int64_t ldg) {
@@ -76,8 +72,6 @@ inline void product(const ColList& a, const double* c, int64_t ldc, int32_t b, c
 // ---- Column reductions (deterministic two-level, no atomics on values) ------------------------
 // out[j] = sum_i x[i,j] * y[i,j]
 void col_dots(const DMat& x, const DMat& y, double* out_dev);
-// per-block partials of x_j^T y_j (parts[j * nb + b], active columns only); returns nb
-int col_dot_parts(const DMat& x, const DMat& y, const int* active, double* parts, int64_t cap);
 // Normalised residuals of the Ritz window (bosp_solver.cpp:256-272, 487-497):
 // num_j = ||kx_j - lam_j yb_j||^2 + ||my_j - lam_j xb_j||^2,  den_j = ||x_j||^2 + ||y_j||^2
 void residual_sums(const DMat& kx, const DMat& my, const DMat& xb, const DMat& yb,

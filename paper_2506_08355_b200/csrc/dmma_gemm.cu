@@ -18,6 +18,8 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstdio>
+#include <mutex>
+#include <set>
 #include <string>
 
 #include "coef_ldu.cuh"
@@ -195,6 +197,18 @@ struct GramParams {
     int64_t job_stride;  // doubles per job in partial
 };
 
+// BOSP_PROF_SHAPES=1 (measurement): profile families split by launch shape, e.g.
+// "gram_wide:320x320s/2" (a x b, symmetric, jobs) -- interned, the profiler keeps the pointer.
+const char* shape_family(const char* fam, int a, int b, bool sym, int njobs) {
+    static const bool on = std::getenv("BOSP_PROF_SHAPES") != nullptr;
+    if (!on) return fam;
+    static std::mutex mu;
+    static std::set<std::string> names;
+    std::lock_guard<std::mutex> lk(mu);
+    return names.insert(std::string(fam) + ":" + std::to_string(a) + "x" + std::to_string(b) + (sym ? "s" : "") + "/" +
+                        std::to_string(njobs)).first->c_str();
+}
+
 bool same_columns(const ColList& a, const ColList& b) {
     if (a.nseg != b.nseg) return false;
     for (int s = 0; s < a.nseg; ++s)
@@ -278,29 +292,7 @@ k_gram(GramParams prm) {
     // symmetric job, diagonal tile: a warp tile strictly below the diagonal only produces
     // mirrored entries (never stored) -- it keeps the pipeline but leaves the DMMA pipe to the
     // other warps (a quarter of a 2 x 2 diagonal tile's work)
-    bool idle = prm.sym[jb] && tm == tn && wm0 >= wn0 + WTN;
-    // masked B columns: a fragment group of 8 inactive columns issues no DMMAs; a CTA whose
-    // columns are all inactive does nothing at all (its G columns are never read)
-    bool live[NTL];
-#pragma unroll
-    for (int j = 0; j < NTL; ++j) live[j] = true;
-    if (job.b_active) {
-        bool any_cta = false;
-        for (int c = 0; c < BN && n0 + c < bcols; ++c) any_cta |= job.b_active[n0 + c] != 0;
-        if (!any_cta) return;
-        bool any_warp = false;
-#pragma unroll
-        for (int j = 0; j < NTL; ++j) {
-            bool a8 = false;
-            for (int c = 0; c < 8; ++c) {
-                const int col = n0 + wn0 + j * 8 + c;
-                a8 |= col < bcols && job.b_active[col] != 0;
-            }
-            live[j] = a8;
-            any_warp |= a8;
-        }
-        idle = idle || !any_warp;
-    }
+    const bool idle = prm.sym[jb] && tm == tn && wm0 >= wn0 + WTN;
     for (int it = 0; it < nk; ++it) {
         cp_async_wait<kStages - 2>();
         __syncthreads();
@@ -318,8 +310,7 @@ k_gram(GramParams prm) {
 #pragma unroll
                 for (int i = 0; i < MT; ++i)
 #pragma unroll
-                    for (int j = 0; j < NTL; ++j)
-                        if (live[j]) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+                    for (int j = 0; j < NTL; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
             }
         }
         const int nxt = it + kStages - 1;
@@ -339,11 +330,9 @@ k_gram(GramParams prm) {
             for (int j = 0; j < NTL; ++j) {
                 const int m = m0 + wm0 + i * 8 + gid;
                 const int nn = n0 + wn0 + j * 8 + 2 * tig;
-                if (m < acols && live[j]) {
-                    if (nn < bcols && (!job.b_active || job.b_active[nn]))
-                        gram_store(job, prm.sym[jb], m, nn, acc[i][j][0]);
-                    if (nn + 1 < bcols && (!job.b_active || job.b_active[nn + 1]))
-                        gram_store(job, prm.sym[jb], m, nn + 1, acc[i][j][1]);
+                if (m < acols) {
+                    if (nn < bcols) gram_store(job, prm.sym[jb], m, nn, acc[i][j][0]);
+                    if (nn + 1 < bcols) gram_store(job, prm.sym[jb], m, nn + 1, acc[i][j][1]);
                 }
             }
         return;
@@ -399,7 +388,6 @@ __global__ void __launch_bounds__(kRedElems * kRedGroups) k_gram_reduce(GramPara
     const int m = tm * BM + r % BM;
     const int nn = tn * BN + r / BM;
     if (m >= job.a.cols() || nn >= job.b.cols()) return;
-    if (job.b_active && !job.b_active[nn]) return;  // masked column: never computed
     gram_store(job, prm.sym[jb], m, nn, s);
 }
 
@@ -530,7 +518,12 @@ void launch_gram(const GramJob* jobs, int njobs, int64_t n) {
     {
         // families: the wide Rayleigh-Ritz / repair Grams (64 x 64 tiles), the dense operator's
         // A x (128 x 32 tiles over the stored A^T), and the small tiled Grams
-        const char* fam = (BM == 64 && BN == 64) ? "gram_wide" : "gram";
+        int amx = 0, bmx = 0;
+        for (int j = 0; j < njobs; ++j) {
+            amx = std::max(amx, jobs[j].a.cols());
+            bmx = std::max(bmx, jobs[j].b.cols());
+        }
+        const char* fam = shape_family((BM == 64 && BN == 64) ? "gram_wide" : "gram", amx, bmx, prm.sym[0] != 0, njobs);
         LaunchScope ls(fam, bytes, flops);
         dim3 grid(max_tiles, prm.splits, njobs);
         k_gram<BM, BN, WM, WN, GBK, GST><<<grid, NT, smem, rt.stream()>>>(prm);
@@ -931,7 +924,12 @@ void launch_product(const ProductJob* jobs, int njobs, int64_t n) {
     static unsigned attr_mask = 0;
     rt.once_per_device(attr_mask, [&] { BOSP_CUDA(cudaFuncSetAttribute(k_product<BM, BN, WM, WN, PBK, PST>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); });
-    LaunchScope ls("product_wide", bytes, flops);
+    int kmx = 0, bmx = 0;
+    for (int j = 0; j < njobs; ++j) {
+        kmx = std::max(kmx, jobs[j].a.cols());
+        bmx = std::max(bmx, jobs[j].ncols);
+    }
+    LaunchScope ls(shape_family("product_wide", kmx, bmx, jobs[0].col_kend != nullptr, njobs), bytes, flops);
     const unsigned gx = static_cast<unsigned>(std::min<int64_t>(max_tiles, 65535));
     const unsigned gy = static_cast<unsigned>((max_tiles + gx - 1) / gx);
     dim3 grid(gx, gy, njobs);
@@ -2049,6 +2047,98 @@ void biorth_apply(const DMat& x, const DMat& y, const double* ca, const double* 
     }
 }
 
+namespace {
+// ------------------------------------------------------------------------------------------
+// Rank-k update Out = alpha A C + beta Out for k <= 8 and wide Out (the projection of a
+// 320-column block against the one-column null basis, biorth_against / the repair's sampled
+// projection): a streaming pass over Out (16-byte row pairs, coalesced per column), A's k
+// values of a row pair loaded once per column group, C broadcast from shared memory.  The tiled
+// DMMA kernel spent 14.7 ms on it at n = 2^21, d = 320 (a 16-deep K loop for k = 1).
+constexpr int kRkThreads = 256, kRkCols = 32;
+
+struct RankKParams {
+    ProductJob job[4];
+    int64_t n;
+    int groups[4];  // column groups per job
+};
+
+template <int K>
+__global__ void __launch_bounds__(kRkThreads) k_rankk(RankKParams prm) {
+    __shared__ double cs[8][kRkCols];
+    const int jb = blockIdx.z;
+    const ProductJob& job = prm.job[jb];
+    if (static_cast<int>(blockIdx.y) >= prm.groups[jb]) return;
+    const int c0 = blockIdx.y * kRkCols;
+    const int nc = min(kRkCols, job.ncols - c0);
+    const int k = job.a.cols();
+    for (int e = threadIdx.x; e < 8 * kRkCols; e += kRkThreads) {
+        const int t = e / kRkCols, c = e % kRkCols;
+        cs[t][c] = (t < k && c < nc) ? job.alpha * job.c[t + static_cast<int64_t>(c0 + c) * job.ldc] : 0.0;
+    }
+    __syncthreads();
+    const double* ap[K];
+#pragma unroll
+    for (int t = 0; t < K; ++t) ap[t] = t < k ? colptr(job.a, t) : nullptr;
+    const double beta = job.beta;
+    const int64_t npair = prm.n >> 1;
+    for (int64_t q = blockIdx.x * static_cast<int64_t>(kRkThreads) + threadIdx.x; q < npair;
+         q += static_cast<int64_t>(gridDim.x) * kRkThreads) {
+        const int64_t i = 2 * q;
+        double2 a[K];
+#pragma unroll
+        for (int t = 0; t < K; ++t) a[t] = ap[t] ? __ldg(reinterpret_cast<const double2*>(ap[t] + i)) : make_double2(0.0, 0.0);
+        double* out = job.out + static_cast<int64_t>(c0) * job.ldo + i;
+#pragma unroll 4
+        for (int c = 0; c < nc; ++c) {
+            double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+            for (int t = 0; t < K; ++t) {
+                s0 = fma(a[t].x, cs[t][c], s0);
+                s1 = fma(a[t].y, cs[t][c], s1);
+            }
+            double2* o = reinterpret_cast<double2*>(out + static_cast<int64_t>(c) * job.ldo);
+            if (beta != 0.0) {
+                const double2 v = *o;
+                s0 = fma(beta, v.x, s0);
+                s1 = fma(beta, v.y, s1);
+            }
+            *o = make_double2(s0, s1);
+        }
+    }
+    if ((prm.n & 1) && blockIdx.x == 0 && threadIdx.x < nc) {  // the last row of an odd n
+        const int64_t i = prm.n - 1;
+        const int c = threadIdx.x;
+        double s = 0.0;
+        for (int t = 0; t < k; ++t) s = fma(ap[t][i], cs[t][c], s);
+        double* o = job.out + static_cast<int64_t>(c0 + c) * job.ldo + i;
+        *o = beta != 0.0 ? fma(beta, *o, s) : s;
+    }
+}
+
+template <int K>
+void launch_rankk(const ProductJob* jobs, int njobs, int64_t n) {
+    Runtime& rt = Runtime::get();
+    RankKParams prm{};
+    int gmax = 0;
+    double bytes = 0.0, flops = 0.0;
+    for (int j = 0; j < njobs; ++j) {
+        prm.job[j] = jobs[j];
+        prm.groups[j] = (jobs[j].ncols + kRkCols - 1) / kRkCols;
+        gmax = std::max(gmax, prm.groups[j]);
+        bytes += 8.0 * n * (jobs[j].a.cols() + jobs[j].ncols * (jobs[j].beta != 0.0 ? 2.0 : 1.0));
+        flops += 2.0 * n * jobs[j].a.cols() * jobs[j].ncols;
+    }
+    prm.n = n;
+    const int64_t npair = std::max<int64_t>(1, n / 2);
+    const int64_t want = 8LL * rt.sm_count() * 2048 / kRkThreads;  // ~8 waves of resident blocks
+    const unsigned gx = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>((npair + kRkThreads - 1) / kRkThreads,
+                                                                                     want / std::max(1, gmax * njobs) + 1)));
+    LaunchScope ls("product", bytes, flops);
+    k_rankk<K><<<dim3(gx, gmax, njobs), kRkThreads, 0, rt.stream()>>>(prm);
+    BOSP_LAUNCH_CHECK();
+}
+}  // namespace
+
 void product(const ProductJob* jobs, int njobs, int64_t n) {
     require(njobs >= 1 && njobs <= 4, "product: 1..4 jobs per launch");
     int bmax = 0;
@@ -2072,6 +2162,15 @@ void product(const ProductJob* jobs, int njobs, int64_t n) {
             case 7: return launch_skinny<56>(jobs, njobs, n);
             default: return launch_skinny<64>(jobs, njobs, n);
         }
+    }
+    // rank-k updates of wide blocks (k <= 8, e.g. the projection against the null basis): a
+    // streaming pass, not a DMMA tile loop
+    if (kmax > 0 && kmax <= 8) {
+        bool aligned = true;
+        for (int j = 0; j < njobs; ++j) aligned = aligned && (jobs[j].ldo & 1) == 0 && (reinterpret_cast<uintptr_t>(jobs[j].out) & 15) == 0;
+        if (aligned) return kmax <= 1 ? launch_rankk<1>(jobs, njobs, n)
+                          : kmax <= 2 ? launch_rankk<2>(jobs, njobs, n)
+                          : kmax <= 4 ? launch_rankk<4>(jobs, njobs, n) : launch_rankk<8>(jobs, njobs, n);
     }
     // k == 0: Out = beta * Out (handled by the kernel with an empty K loop)
     // 4 warps of 32 x 32 (16 DMMAs per 8 fragment loads), 3 x 16-deep stages, 3 CTAs/SM:

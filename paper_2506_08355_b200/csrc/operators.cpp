@@ -137,25 +137,8 @@ public:
         FamilyScope fs("dense_apply");
         gram(ColList(t_.view()), ColList(x), x.rows, y.p, y.ld);
     }
-    // The CG's A p honouring the column mask: converged 8-column groups issue no DMMAs (the
-    // apply is DMMA-bound at the CG's widths), then p^T A p as per-block partials.
-    int apply_dot(const DMat& x, const DMat& y, const SpmmDot& dot) const override {
-        if (dot.ticket || !dot.active || !masked()) return 0;  // folded dots (row partition): generic path
-        {
-            FamilyScope fs("dense_apply");
-            GramJob job{ColList(t_.view()), ColList(x), y.p, y.ld};
-            job.b_active = dot.active;
-            gram(&job, 1, x.rows);
-        }
-        return col_dot_parts(x, y, dot.active, dot.parts, dot.parts_cap);
-    }
-    bool has_masked_dot() const override { return masked(); }
 
 private:
-    static bool masked() {  // BOSP_DENSE_MASK=0: the unmasked apply inside a while-loop CG graph (A/B)
-        static const bool on = !std::getenv("BOSP_DENSE_MASK") || std::atoi(std::getenv("BOSP_DENSE_MASK")) != 0;
-        return on;
-    }
     DBlock t_;
 };
 

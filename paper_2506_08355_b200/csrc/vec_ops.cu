@@ -619,41 +619,5 @@ void cg_update(const DMat& x, const DMat& r, const DMat& p, const DMat& ap, cons
     launch_cols("cg_vec", r.rows, static_cast<int>(r.cols), d, 40.0 * r.rows * r.cols);
 }
 
-// Per-block partials of x_j^T y_j for the active columns (parts[j * nb + b], the layout of the
-// SpMM-fused dots that cg_update folds); inactive columns are skipped.  Returns nb.
-namespace {
-__global__ void __launch_bounds__(kThreads) k_dot_parts(int64_t n, const double* __restrict__ x, int64_t ldx,
-                                                        const double* __restrict__ y, int64_t ldy,
-                                                        const int* active, double* parts) {
-    const int j = blockIdx.y;
-    if (active && !active[j]) return;
-    const int64_t per = (n + gridDim.x - 1) / gridDim.x;
-    const int64_t r0 = blockIdx.x * per, r1 = min(n, r0 + per);
-    double t = 0.0;
-    for (int64_t i = r0 + threadIdx.x; i < r1; i += kThreads) t += x[i + j * ldx] * y[i + j * ldy];
-    __shared__ double red[kThreads / 32];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = t;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double s = 0.0;
-        for (int w = 0; w < kThreads / 32; ++w) s += red[w];
-        parts[static_cast<int64_t>(j) * gridDim.x + blockIdx.x] = s;
-    }
-}
-}  // namespace
-
-int col_dot_parts(const DMat& x, const DMat& y, const int* active, double* parts, int64_t cap) {
-    if (x.cols == 0 || x.rows == 0) return 0;
-    const int nb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>({64, cap / x.cols, (x.rows + 1023) / 1024})));
-    Runtime& rt = Runtime::get();
-    LaunchScope ls("cg_vec", 16.0 * x.rows * x.cols);
-    k_dot_parts<<<dim3(nb, static_cast<unsigned>(x.cols)), kThreads, 0, rt.stream()>>>(x.rows, x.p, x.ld, y.p, y.ld,
-                                                                                       active, parts);
-    BOSP_LAUNCH_CHECK();
-    return nb;
-}
-
 }  // namespace b200
 }  // namespace bosp

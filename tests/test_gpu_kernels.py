@@ -389,3 +389,18 @@ def test_mgs_device_coefficients_fallback():
     po, qo, ko, do = O.mgs_biorth(x, y)
     assert p.shape[1] == len(ko)
     assert np.abs(p.T @ q - np.eye(len(ko))).max() < 1e-10
+
+
+@pytest.mark.parametrize("k", [1, 3, 8])
+@pytest.mark.parametrize("b", [65, 320])
+@pytest.mark.parametrize("n", [7, 20011])
+def test_rank_k_product_and_axpy(k, b, n):
+    """Rank-k updates of wide blocks (the streaming k <= 8 path: the projection of a d-column
+    block against the null basis) against numpy: block_product (kernels.cpp:70-87) and
+    block_axpy (:89-104), odd n included."""
+    rng = np.random.default_rng(100 * k + b + n)
+    x = np.asfortranarray(rng.uniform(-1, 1, (n, k)))
+    c = np.asfortranarray(rng.uniform(-1, 1, (k, b)))
+    y = np.asfortranarray(rng.uniform(-1, 1, (n, b)))
+    assert rel(bosp.block_product(x, c), x @ c) < 1e-14
+    assert rel(bosp.block_axpy(x, c, y), y - x @ c) < 1e-14
