@@ -16,11 +16,13 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstdio>
 #include <mutex>
 #include <set>
 #include <string>
+#include <vector>
 
 #include "coef_ldu.cuh"
 #include "dense_ops.hpp"
@@ -2165,7 +2167,8 @@ void product(const ProductJob* jobs, int njobs, int64_t n) {
     }
     // rank-k updates of wide blocks (k <= 8, e.g. the projection against the null basis): a
     // streaming pass, not a DMMA tile loop
-    if (kmax > 0 && kmax <= 8) {
+    static const bool rankk_on = !std::getenv("BOSP_RANKK") || std::atoi(std::getenv("BOSP_RANKK")) != 0;
+    if (rankk_on && kmax > 0 && kmax <= 8) {
         bool aligned = true;
         for (int j = 0; j < njobs; ++j) aligned = aligned && (jobs[j].ldo & 1) == 0 && (reinterpret_cast<uintptr_t>(jobs[j].out) & 15) == 0;
         if (aligned) return kmax <= 1 ? launch_rankk<1>(jobs, njobs, n)

@@ -404,3 +404,4 @@ def test_rank_k_product_and_axpy(k, b, n):
     y = np.asfortranarray(rng.uniform(-1, 1, (n, b)))
     assert rel(bosp.block_product(x, c), x @ c) < 1e-14
     assert rel(bosp.block_axpy(x, c, y), y - x @ c) < 1e-14
+
