@@ -882,6 +882,44 @@ k_product(ProductParams prm) {
         }
     __syncthreads();
     const double alpha = job.alpha, beta = job.beta;
+    if ((job.ldo & 1) == 0 && (reinterpret_cast<uintptr_t>(job.out) & 15) == 0) {
+        // row pairs as 16-byte accesses, 4 pairs per thread and round with every load of Out
+        // (beta != 0) issued before the first store (a scalar load -> store chain per element
+        // left the epilogue latency bound)
+        constexpr int kPairs = BM * BN / 2, kU = 4;
+        for (int q0 = threadIdx.x; q0 < kPairs; q0 += NT * kU) {
+            double2 old[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const int q = q0 + u * NT;
+                const int m = 2 * (q % (BM / 2)), nn = q / (BM / 2);
+                const int64_t gm = m0 + m;
+                const int gn = n0 + nn;
+                old[u] = make_double2(0.0, 0.0);
+                if (beta != 0.0 && q < kPairs && gn < job.ncols) {
+                    const double* o = job.out + gn * job.ldo + gm;
+                    if (gm + 1 < prm.n) old[u] = *reinterpret_cast<const double2*>(o);
+                    else if (gm < prm.n) old[u].x = *o;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const int q = q0 + u * NT;
+                if (q >= kPairs) continue;
+                const int m = 2 * (q % (BM / 2)), nn = q / (BM / 2);
+                const int64_t gm = m0 + m;
+                const int gn = n0 + nn;
+                if (gn >= job.ncols || gm >= prm.n) continue;
+                double* o = job.out + gn * job.ldo + gm;
+                const double v0 = alpha * so[nn * LdM + m], v1 = alpha * so[nn * LdM + m + 1];
+                const double r0 = beta == 0.0 ? v0 : v0 + beta * old[u].x;
+                const double r1 = beta == 0.0 ? v1 : v1 + beta * old[u].y;
+                if (gm + 1 < prm.n) *reinterpret_cast<double2*>(o) = make_double2(r0, r1);
+                else *o = r0;
+            }
+        }
+        return;
+    }
     for (int e = threadIdx.x; e < BM * BN; e += NT) {
         const int m = e % BM, nn = e / BM;
         const int64_t gm = m0 + m;
