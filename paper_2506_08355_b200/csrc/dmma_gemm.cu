@@ -473,14 +473,15 @@ void launch_gram(const GramJob* jobs, int njobs, int64_t n) {
     // Split count by wave efficiency: tiles x splits CTAs over `slots` resident CTA slots run in
     // ceil(total / slots) waves.  Among split counts giving at least ~2 waves of CTAs (more CTAs
     // amortise the tail) with >= 4 stages of work per CTA, <= 16 waves and split partials <= 3 %
-    // of the operand bytes, take the one whose last wave is fullest (ties within 0.5 %: fewer
+    // of the operand bytes (>= 32 MB), take the one whose last wave is fullest (ties within 0.5 %: fewer
     // splits).  (The previous rule, ~2 waves rounded down, gave the dense operator's 128 tiles
     // 4 splits = 1.73 waves: 774 -> 687 us per apply; a 320 x 320 Gram 4 instead of 2 waves: +3 %.)
     const int slots = resident[rt.device() & 63] * rt.sm_count();
     const int per_split = max_tiles * njobs;
     double opnd = 0.0;
     for (int j = 0; j < njobs; ++j) opnd += 8.0 * n * (jobs[j].a.cols() + jobs[j].b.cols());
-    const int pcap = static_cast<int>(std::max(1.0, 0.03 * opnd / (8.0 * BM * BN * per_split)));
+    // (small problems: a 32 MB floor, or config 1's n = 2000 dense apply would get one split)
+    const int pcap = static_cast<int>(std::max(1.0, std::max(0.03 * opnd, 32.0 * (1 << 20)) / (8.0 * BM * BN * per_split)));
     const int smax = std::max(1, std::min({kblocks / 4, 512, std::max(1, 16 * slots / per_split), pcap}));
     const int smin = std::min(smax, std::max(1, (19 * slots / 10 + per_split - 1) / per_split));
     int splits = smin;
