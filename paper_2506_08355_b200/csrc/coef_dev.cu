@@ -11,7 +11,7 @@ inline namespace b200 {
 
 namespace {
 
-__global__ void __launch_bounds__(64) k_coef_ldu(const double* __restrict__ z, int64_t ldz, int m, double* c,
+__global__ void __launch_bounds__(kCoefThreads) k_coef_ldu(const double* __restrict__ z, int64_t ldz, int m, double* c,
                                                  int64_t ldc, int* status, double drop_tol, double cancel_tol) {
     __shared__ double work[kCoefSmem];
     coef_ldu_cta(z, ldz, m, c, ldc, status, drop_tol, cancel_tol, work);
@@ -24,7 +24,7 @@ void coef_mgs_dev(const double* z, int64_t ldz, int m, double* c, int64_t ldc, i
     require(m >= 1 && m <= kCoefM, "coef_mgs_dev: 1..32 columns");
     Runtime& rt = Runtime::get();
     LaunchScope ls("coef");
-    k_coef_ldu<<<1, 64, 0, rt.stream()>>>(z, ldz, m, c, ldc, status, drop_tol, cancel_tol);
+    k_coef_ldu<<<1, kCoefThreads, 0, rt.stream()>>>(z, ldz, m, c, ldc, status, drop_tol, cancel_tol);
     BOSP_LAUNCH_CHECK();
 }
 

@@ -406,22 +406,23 @@ struct CoefParams {
 };
 
 template <int LDP>
-__global__ void __launch_bounds__(kRedElems * kRedGroups) k_gram_reduce_coef(GramParams prm, CoefParams cp) {
-    __shared__ double part_sum[kRedGroups][kRedElems];
+__global__ void __launch_bounds__(kCoefThreads) k_gram_reduce_coef(GramParams prm, CoefParams cp) {
+    constexpr int kE = 32, kG = kCoefThreads / kE;  // 32 outputs x 32 split groups per block
+    __shared__ double part_sum[kG][kE];
     __shared__ double work[kCoefSmem];
     __shared__ bool last;
     const GramJob& job = prm.job[0];
-    const int el = threadIdx.x % kRedElems, grp = threadIdx.x / kRedElems;
-    const int64_t e = static_cast<int64_t>(blockIdx.x) * kRedElems + el;
+    const int el = threadIdx.x % kE, grp = threadIdx.x / kE;
+    const int64_t e = static_cast<int64_t>(blockIdx.x) * kE + el;
     const int64_t total = static_cast<int64_t>(LDP) * LDP;
     double s0 = 0.0, s1 = 0.0;
     if (e < total) {
         const double* part = prm.partial + e;
         int sp = grp;
 #pragma unroll 4
-        for (; sp + kRedGroups < prm.splits; sp += 2 * kRedGroups) {
+        for (; sp + kG < prm.splits; sp += 2 * kG) {
             s0 += __ldcg(part + sp * total);
-            s1 += __ldcg(part + (sp + kRedGroups) * total);
+            s1 += __ldcg(part + (sp + kG) * total);
         }
         if (sp < prm.splits) s0 += __ldcg(part + sp * total);
     }
@@ -430,7 +431,7 @@ __global__ void __launch_bounds__(kRedElems * kRedGroups) k_gram_reduce_coef(Gra
     if (grp == 0 && e < total) {
         double s = 0.0;
 #pragma unroll
-        for (int g = 0; g < kRedGroups; ++g) s += part_sum[g][el];
+        for (int g = 0; g < kG; ++g) s += part_sum[g][el];
         const int m = static_cast<int>(e % LDP), nn = static_cast<int>(e / LDP);
         if (m < job.a.cols() && nn < job.b.cols()) gram_store(job, true, m, nn, s);
     }
@@ -1418,9 +1419,9 @@ bool launch_gram_tma(const GramJob& job, int64_t n, const CoefParams* coef = nul
         if (coef) {
             LaunchScope ls("gram_reduce");
             if (prm.ldp == 32)
-                k_gram_reduce_coef<32><<<dim3(32 * 32 / kRedElems), kRedElems * kRedGroups, 0, rt.stream()>>>(gp, *coef);
+                k_gram_reduce_coef<32><<<dim3(32 * 32 / 32), kCoefThreads, 0, rt.stream()>>>(gp, *coef);
             else
-                k_gram_reduce_coef<64><<<dim3(64 * 64 / kRedElems), kRedElems * kRedGroups, 0, rt.stream()>>>(gp, *coef);
+                k_gram_reduce_coef<64><<<dim3(64 * 64 / 32), kCoefThreads, 0, rt.stream()>>>(gp, *coef);
             BOSP_LAUNCH_CHECK();
             return true;
         }
@@ -1539,7 +1540,8 @@ void gram(const GramJob* jobs, int njobs, int64_t n) {
 bool gram_pair_coef(const ColList& z, int64_t n, double* g, int64_t ldg, double* c, int64_t ldc, int* status,
                     double drop_tol, double cancel_tol) {
     const int w = z.cols();
-    if (w < 2 || (w & 1) || w > 56 || w / 2 > kCoefM || n < 8192 || !tma_gram_enabled() || Runtime::get().nranks() > 1)
+    static const bool fuse = !std::getenv("BOSP_COEF_FUSE") || std::atoi(std::getenv("BOSP_COEF_FUSE")) != 0;
+    if (!fuse || w < 2 || (w & 1) || w > 56 || w / 2 > kCoefM || n < 8192 || !tma_gram_enabled() || Runtime::get().nranks() > 1)
         return false;
     check_aligned(z);
     GramJob job{z, z, g, ldg};
