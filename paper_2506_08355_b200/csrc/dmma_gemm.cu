@@ -487,19 +487,13 @@ void launch_gram(const GramJob* jobs, int njobs, int64_t n) {
     const int smin = std::min(smax, std::max(1, (19 * slots / 10 + per_split - 1) / per_split));
     int splits = smin;
     double best = -1.0;
-    static const bool old_rule = std::getenv("BOSP_SPLIT_OLD") != nullptr;  // A/B switch (measurement)
-    if (old_rule) {
-        const int waves = std::max(1, (3 * rt.sm_count() + slots - 1) / slots);
-        splits = std::min(std::max(1, waves * slots / per_split), std::max(1, kblocks / 4));
-    } else {
-        for (int sp = smin; sp <= smax; ++sp) {
-            const int64_t total = static_cast<int64_t>(sp) * per_split;
-            const int64_t waves = (total + slots - 1) / slots;
-            const double eff = static_cast<double>(total) / static_cast<double>(waves * slots);
-            if (eff > best + 0.005) {
-                best = eff;
-                splits = sp;
-            }
+    for (int sp = smin; sp <= smax; ++sp) {
+        const int64_t total = static_cast<int64_t>(sp) * per_split;
+        const int64_t waves = (total + slots - 1) / slots;
+        const double eff = static_cast<double>(total) / static_cast<double>(waves * slots);
+        if (eff > best + 0.005) {
+            best = eff;
+            splits = sp;
         }
     }
     const int kb_per = (kblocks + splits - 1) / splits;
@@ -1222,26 +1216,29 @@ struct TmaSegs {
 };
 
 // Encode the 3-D view (qr rows, cols, n / qr row groups) of a column-major segment with a
-// (qr, cols, rows / qr) box, 128-byte swizzle.
-void encode_seg(CUtensorMap* m, const double* p, int64_t ld, int64_t n, int cols, int qr, int rows) {
+// (qr, cols, rows / qr) box, 128-byte swizzle; false when the driver cannot encode it.
+bool encode_seg(CUtensorMap* m, const double* p, int64_t ld, int64_t n, int cols, int qr, int rows) {
     using Fn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
                             const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                             CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-    static Fn fn = [] {
+    static const Fn fn = [] {
         void* f = nullptr;
         cudaDriverEntryPointQueryResult q{};
-        BOSP_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q));
-        if (!f || q != cudaDriverEntryPointSuccess) throw CudaError("cuTensorMapEncodeTiled unavailable");
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess) {
+            cudaGetLastError();
+            f = nullptr;
+        }
         return reinterpret_cast<Fn>(f);
     }();
+    if (!fn) return false;  // no driver entry point: the callers use their cp.async kernels
     const cuuint64_t dims[3] = {static_cast<cuuint64_t>(qr), static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(n / qr)};
     const cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld) * 8u, static_cast<cuuint64_t>(qr) * 8u};
     const cuuint32_t box[3] = {static_cast<cuuint32_t>(qr), static_cast<cuuint32_t>(cols), static_cast<cuuint32_t>(rows / qr)};
     const cuuint32_t estr[3] = {1, 1, 1};
-    const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(p), dims, strides, box, estr,
-                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(p), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 // The segments of a ColList as tensor maps; false when TMA cannot stage it (n % 16, alignment,
@@ -1257,7 +1254,7 @@ bool make_segs(TmaSegs& t, const ColList& cl, int64_t n, int rows) {
         t.cols[s] = cols;
         t.off[s] = off;
         off += (cols * rows + 127) / 128 * 128;  // 1024-byte boundary
-        encode_seg(&t.map[s], cl.p[s], cl.ld[s], n, cols, kTmaQ, rows);
+        if (!encode_seg(&t.map[s], cl.p[s], cl.ld[s], n, cols, kTmaQ, rows)) return false;
     }
     t.stage = off;
     return true;
@@ -1437,11 +1434,6 @@ bool launch_gram_tma(const GramJob& job, int64_t n, const CoefParams* coef = nul
 }
 
 
-bool tma_gram_enabled() {
-    static const int v = std::getenv("BOSP_GRAM_TMA") ? std::atoi(std::getenv("BOSP_GRAM_TMA")) : 1;
-    return v != 0;
-}
-
 void check_aligned(const ColList& cl) {
     for (int s = 0; s < cl.nseg; ++s)
         if ((reinterpret_cast<uintptr_t>(cl.p[s]) & 15) || (cl.ld[s] & 1))
@@ -1477,7 +1469,7 @@ void gram(const GramJob* jobs, int njobs, int64_t n) {
     // one symmetric Gram of <= 64 columns (MGS-Biorth's [X | Y] pair Gram) over many rows:
     // bulk-async staged, one persistent CTA per SM
     // (57-64 columns: 36 fragment pairs of accumulators spill -- the register kernels below)
-    if (njobs == 1 && jobs[0].sym && amax == bmax && amax <= 56 && n >= 8192 && tma_gram_enabled() &&
+    if (njobs == 1 && jobs[0].sym && amax == bmax && amax <= 56 && n >= 8192 &&
         same_columns(jobs[0].a, jobs[0].b)) {
         bool done = false;
         switch ((amax + 7) / 8) {
@@ -1540,8 +1532,7 @@ void gram(const GramJob* jobs, int njobs, int64_t n) {
 bool gram_pair_coef(const ColList& z, int64_t n, double* g, int64_t ldg, double* c, int64_t ldc, int* status,
                     double drop_tol, double cancel_tol) {
     const int w = z.cols();
-    static const bool fuse = !std::getenv("BOSP_COEF_FUSE") || std::atoi(std::getenv("BOSP_COEF_FUSE")) != 0;
-    if (!fuse || w < 2 || (w & 1) || w > 56 || w / 2 > kCoefM || n < 8192 || !tma_gram_enabled() || Runtime::get().nranks() > 1)
+    if (w < 2 || (w & 1) || w > 56 || w / 2 > kCoefM || n < 8192 || Runtime::get().nranks() > 1)
         return false;
     check_aligned(z);
     GramJob job{z, z, g, ldg};
@@ -2021,10 +2012,6 @@ void launch_biorth_apply_tma_k(BiorthTmaParams prm, int64_t n, double* g, int64_
     throw ContractViolation("biorth_apply: kept columns exceed the block width");
 }
 
-bool tma_apply_enabled() {
-    static const int v = std::getenv("BOSP_APPLY_TMA") ? std::atoi(std::getenv("BOSP_APPLY_TMA")) : 1;
-    return v != 0;
-}
 }  // namespace
 
 void biorth_apply(const DMat& x, const DMat& y, const double* ca, const double* cb, int64_t ldc, int kb,
@@ -2038,7 +2025,7 @@ void biorth_apply(const DMat& x, const DMat& y, const double* ca, const double* 
     const DMat pv = p.cols_range(0, kb), qv = q.cols_range(0, kb);
     const int kpad = std::max(4, (static_cast<int>(x.cols) + 3) / 4 * 4);
     BiorthTmaParams tp{};
-    if (tma_apply_enabled() && kb > 24 && n >= 8192 &&
+    if (kb > 24 && n >= 8192 &&
         make_segs(tp.seg, ColList(x).add(y), n, ba_rows((kb + 7) / 8 * 8))) {
         const int k = static_cast<int>(x.cols);
         tp.ca = ca;
@@ -2208,8 +2195,7 @@ void product(const ProductJob* jobs, int njobs, int64_t n) {
     }
     // rank-k updates of wide blocks (k <= 8, e.g. the projection against the null basis): a
     // streaming pass, not a DMMA tile loop
-    static const bool rankk_on = !std::getenv("BOSP_RANKK") || std::atoi(std::getenv("BOSP_RANKK")) != 0;
-    if (rankk_on && kmax > 0 && kmax <= 8) {
+    if (kmax > 0 && kmax <= 8) {
         bool aligned = true;
         for (int j = 0; j < njobs; ++j) aligned = aligned && (jobs[j].ldo & 1) == 0 && (reinterpret_cast<uintptr_t>(jobs[j].out) & 15) == 0;
         if (aligned) return kmax <= 1 ? launch_rankk<1>(jobs, njobs, n)

@@ -278,11 +278,6 @@ JacobiSvdResult jacobi_svd_tol(DenseMatrix a, int64_t max_sweeps, double tol) {
                 pos = lp;
             }
             rotated = (any != 0);
-            if (std::getenv("BOSP_DEBUG_SWEEPS")) {
-                int64_t cnt = 0;
-                for (int64_t p2 = 0; p2 < k; ++p2) cnt += ver[p2];
-                std::fprintf(stderr, "[bosp] sweep %lld: column versions %lld\n", (long long)sweep, (long long)cnt);
-            }
         }
     }
     res.converged = !rotated;
@@ -428,49 +423,6 @@ JacobiSvdResult jacobi_svd_qr(const DenseMatrix& w, int64_t max_sweeps) {
     for (int64_t j = 0; j < k; ++j)
         for (int64_t i = 0; i < k; ++i) res.v(perm[i], j) = jx.u(i, j);
     res.u = std::move(u);
-    return res;
-}
-
-// Double QR preconditioning (Drmac & Veselic): W P = Q1 R1, then R1^T = Q2 R2 (no pivoting) and
-// the one-sided Jacobi on X = R2^T:  X V_x = U_x S  gives  W = (Q1 U_x) S (P Q2 V_x)^T.
-JacobiSvdResult jacobi_svd_qr2(const DenseMatrix& w, int64_t max_sweeps) {
-    const int64_t k = w.cols();
-    require(w.rows() == k, "jacobi_svd_qr2: square input expected");
-    static const bool dbg = std::getenv("BOSP_DEBUG") != nullptr;
-    const auto t0 = std::chrono::steady_clock::now();
-    DenseMatrix a = w;
-    std::vector<double> tau1, tau2;
-    std::vector<int64_t> perm, perm2;
-    householder_qrcp(a, tau1, perm);
-    DenseMatrix b(k, k);  // R1^T
-    for (int64_t j = 0; j < k; ++j)
-        for (int64_t i = j; i < k; ++i) b(i, j) = a(j, i);
-    householder_qrcp(b, tau2, perm2, false);
-    const auto t1 = std::chrono::steady_clock::now();
-    DenseMatrix x(k, k);  // X = R2^T (lower triangular)
-    for (int64_t j = 0; j < k; ++j)
-        for (int64_t i = j; i < k; ++i) x(i, j) = b(j, i);
-    JacobiSvdResult jx = jacobi_svd_tol(std::move(x), max_sweeps, 1e-15);
-    const auto t2 = std::chrono::steady_clock::now();
-    // X V_x = U_x S with X = R2^T:  R2 = V_x S U_x^T, R1^T = Q2 R2 -> R1 = U_x S (Q2 V_x)^T
-    // W P = Q1 R1 = (Q1 U_x) S (Q2 V_x)^T  ->  left vectors Q1 U_x, right vectors P Q2 V_x
-    DenseMatrix u = std::move(jx.u);
-    apply_q(a, tau1, u);
-    DenseMatrix vq = std::move(jx.v);
-    apply_q(b, tau2, vq);
-    JacobiSvdResult res;
-    res.sigma = std::move(jx.sigma);
-    res.converged = jx.converged;
-    res.sweeps = jx.sweeps;
-    res.v = DenseMatrix(k, k);
-    for (int64_t j = 0; j < k; ++j)
-        for (int64_t i = 0; i < k; ++i) res.v(perm[i], j) = vq(i, j);
-    res.u = std::move(u);
-    if (dbg) {
-        auto ms = [](auto x0, auto x1) { return std::chrono::duration<double>(x1 - x0).count() * 1e3; };
-        std::fprintf(stderr, "[bosp] svd_qr2 d=%lld qr x2 %.2f ms jacobi %.2f ms (%lld sweeps) apply %.2f ms\n",
-                     (long long)k, ms(t0, t1), ms(t1, t2), (long long)res.sweeps, ms(t2, std::chrono::steady_clock::now()));
-    }
     return res;
 }
 

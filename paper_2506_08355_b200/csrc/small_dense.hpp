@@ -63,7 +63,6 @@ JacobiSvdResult jacobi_svd_tol(DenseMatrix a, int64_t max_sweeps, double tol);
 // Square W: QR-preconditioned one-sided Jacobi (Householder QR with column pivoting, then the
 // same Jacobi on R^T); used by solve_small_lrep for d >= 96.
 JacobiSvdResult jacobi_svd_qr(const DenseMatrix& w, int64_t max_sweeps = 40);
-JacobiSvdResult jacobi_svd_qr2(const DenseMatrix& w, int64_t max_sweeps = 40);
 double spectral_norm(const DenseMatrix& a);
 DenseMatrix lu_inverse(const DenseMatrix& a);
 
