@@ -1138,7 +1138,9 @@ void launch_skinny_rt(const ProductJob* jobs, int njobs, int64_t n) {
     int per_sm = 1;
     BOSP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_product_skinny<BN, RT>, 256, smem));
     const int64_t ctas = std::max<int64_t>(1, std::min<int64_t>(prm.tiles, int64_t(std::max(per_sm, 1)) * rt.sm_count()));
-    LaunchScope ls("product", bytes, flops);
+    int bmx = 0;
+    for (int j = 0; j < njobs; ++j) bmx = std::max(bmx, jobs[j].ncols);
+    LaunchScope ls(shape_family("product", kmax, bmx, jobs[0].beta != 0.0, njobs), bytes, flops);
     dim3 grid(static_cast<unsigned>(ctas), 1, njobs);
     k_product_skinny<BN, RT><<<grid, 256, smem, rt.stream()>>>(prm);
     BOSP_LAUNCH_CHECK();
@@ -2163,7 +2165,7 @@ void launch_rankk(const ProductJob* jobs, int njobs, int64_t n) {
     const int64_t want = 8LL * rt.sm_count() * 2048 / kRkThreads;  // ~8 waves of resident blocks
     const unsigned gx = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>((npair + kRkThreads - 1) / kRkThreads,
                                                                                      want / std::max(1, gmax * njobs) + 1)));
-    LaunchScope ls("product", bytes, flops);
+    LaunchScope ls(shape_family("product", K, jobs[0].ncols, jobs[0].beta != 0.0, njobs), bytes, flops);
     k_rankk<K><<<dim3(gx, gmax, njobs), kRkThreads, 0, rt.stream()>>>(prm);
     BOSP_LAUNCH_CHECK();
 }
