@@ -4,6 +4,8 @@
 #include <immintrin.h>
 
 #include <algorithm>
+#include <atomic>
+#include <memory>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -74,9 +76,11 @@ bool DenseMatrix::is_symmetric(double tol_rel) const {
 
 namespace {
 // AVX2 helpers for the rotation kernels (x86-64-v3 build).
-inline double dot_avx(const double* a, const double* b, int64_t m) {
+// i0 (a multiple of 8) skips leading products known to be exactly zero without changing the
+// lane assignment: bitwise the full-range sum (up to the sign of an exact-zero result).
+inline double dot_avx(const double* a, const double* b, int64_t m, int64_t i0 = 0) {
     __m256d s0 = _mm256_setzero_pd(), s1 = _mm256_setzero_pd();
-    int64_t i = 0;
+    int64_t i = i0;
     for (; i + 8 <= m; i += 8) {
         s0 = _mm256_fmadd_pd(_mm256_loadu_pd(a + i), _mm256_loadu_pd(b + i), s0);
         s1 = _mm256_fmadd_pd(_mm256_loadu_pd(a + i + 4), _mm256_loadu_pd(b + i + 4), s1);
@@ -107,7 +111,7 @@ inline void rotate_avx(double* x, double* y, int64_t m, double c, double s) {
 
 }  // namespace
 
-DenseMatrix matmul(const DenseMatrix& a, const DenseMatrix& b) {
+DenseMatrix matmul(const DenseMatrix& a, const DenseMatrix& b, bool a_lower) {
     require(a.cols() == b.rows(), "matmul: inner dimensions disagree");
     DenseMatrix c(a.rows(), b.cols());
     const int64_t m = a.rows(), k = a.cols();
@@ -118,7 +122,24 @@ DenseMatrix matmul(const DenseMatrix& a, const DenseMatrix& b) {
             const double bpj = b(p, j);
             if (bpj == 0.0) continue;
             const double* ap = a.col(p);
-            for (int64_t i = 0; i < m; ++i) cj[i] += ap[i] * bpj;
+            for (int64_t i = a_lower ? p : 0; i < m; ++i) cj[i] += ap[i] * bpj;
+        }
+    }
+    return c;
+}
+
+DenseMatrix matmul_tn_lower(const DenseMatrix& l, const DenseMatrix& r) {
+    require(l.rows() == r.rows() && l.rows() == l.cols() && r.rows() == r.cols(), "matmul_tn_lower: square factors");
+    const int64_t n = l.rows();
+    DenseMatrix c(n, n);
+    // (L^T R)(i, j) = sum_{p >= max(i, j)} L(p, i) R(p, j): the structural zeros are skipped
+    // (bitwise matmul_tn: same lanes, only exact-zero products left out)
+#pragma omp parallel for schedule(dynamic, 8)
+    for (int64_t j = 0; j < n; ++j) {
+        const double* rj = r.col(j);
+        for (int64_t i = 0; i < n; ++i) {
+            const int64_t p0 = std::max(i, j) & ~int64_t(7);
+            c(i, j) = dot_avx(l.col(i), rj, n, p0);
         }
     }
     return c;
@@ -146,7 +167,22 @@ std::optional<DenseMatrix> cholesky_lower(const DenseMatrix& a) {
     std::vector<double> s(static_cast<size_t>(n));
     for (int64_t j = 0; j < n; ++j) {
         for (int64_t i = j; i < n; ++i) s[i] = a(i, j);
-        for (int64_t k = 0; k < j; ++k) {
+        // four k at a time with each element's subtractions still in ascending k (bitwise the
+        // one-k-at-a-time loop; s is loaded and stored once per four columns of L)
+        int64_t k = 0;
+        for (; k + 4 <= j; k += 4) {
+            const double c0 = l(j, k), c1 = l(j, k + 1), c2 = l(j, k + 2), c3 = l(j, k + 3);
+            const double *l0 = l.col(k), *l1 = l.col(k + 1), *l2 = l.col(k + 2), *l3 = l.col(k + 3);
+            for (int64_t i = j; i < n; ++i) {
+                double v = s[i];
+                v -= l0[i] * c0;
+                v -= l1[i] * c1;
+                v -= l2[i] * c2;
+                v -= l3[i] * c3;
+                s[i] = v;
+            }
+        }
+        for (; k < j; ++k) {
             const double ljk = l(j, k);
             const double* lk = l.col(k);
             for (int64_t i = j; i < n; ++i) s[i] -= lk[i] * ljk;
@@ -161,6 +197,19 @@ std::optional<DenseMatrix> cholesky_lower(const DenseMatrix& a) {
     return l;
 }
 
+void cholesky_lower_pair(const DenseMatrix& a, const DenseMatrix& b, std::optional<DenseMatrix>& la,
+                         std::optional<DenseMatrix>& lb) {
+    // the two factorizations on two threads (a barrier-per-column parallel factorization lost
+    // to barrier latency at d = 320)
+#pragma omp parallel sections num_threads(2) if (a.rows() >= 64)
+    {
+#pragma omp section
+        la = cholesky_lower(a);
+#pragma omp section
+        lb = cholesky_lower(b);
+    }
+}
+
 namespace {
 
 // Rotate columns p, q of a (m rows) and v (k rows) if they are not yet orthogonal; returns
@@ -168,11 +217,13 @@ namespace {
 // squared column norms are carried in `nrm` (recomputed at every sweep start): after the
 // rotation that annihilates gamma they are exactly alpha - t*gamma and beta + t*gamma, so a pair
 // costs one dot product instead of three.
-inline bool jacobi_pair(DenseMatrix& a, DenseMatrix& v, double* nrm, int64_t p, int64_t q, double tol = 1e-15) {
-    const int64_t m = a.rows(), k = v.rows();
+inline bool jacobi_pair(DenseMatrix& a, DenseMatrix* v, double* nrm, int64_t p, int64_t q, double tol = 1e-15) {
+    const int64_t m = a.rows();
     double* ap = a.col(p);
     double* aq = a.col(q);
-    const double alpha = nrm[p], beta = nrm[q];
+    double& np = nrm[p];
+    double& nq = nrm[q];
+    const double alpha = np, beta = nq;
     if (alpha == 0.0 || beta == 0.0) return false;
     const double gamma = dot_avx(ap, aq, m);
     if (std::fabs(gamma) <= tol * std::sqrt(alpha * beta)) return false;
@@ -181,9 +232,9 @@ inline bool jacobi_pair(DenseMatrix& a, DenseMatrix& v, double* nrm, int64_t p, 
     const double c = 1.0 / std::sqrt(1.0 + t * t);
     const double s = c * t;
     rotate_avx(ap, aq, m, c, s);
-    rotate_avx(v.col(p), v.col(q), k, c, s);
-    nrm[p] = alpha - t * gamma;
-    nrm[q] = beta + t * gamma;
+    if (v) rotate_avx(v->col(p), v->col(q), v->rows(), c, s);
+    np = alpha - t * gamma;
+    nq = beta + t * gamma;
     return true;
 }
 
@@ -195,11 +246,12 @@ void column_norms(const DenseMatrix& a, double* nrm) {
 
 JacobiSvdResult jacobi_svd(DenseMatrix a, int64_t max_sweeps) { return jacobi_svd_tol(std::move(a), max_sweeps, 1e-15); }
 
-JacobiSvdResult jacobi_svd_tol(DenseMatrix a, int64_t max_sweeps, double tol) {
+JacobiSvdResult jacobi_svd_tol(DenseMatrix a, int64_t max_sweeps, double tol, bool accumulate) {
     const int64_t m = a.rows(), k = a.cols();
     require(m >= k, "jacobi_svd: requires rows >= cols");
     JacobiSvdResult res;
-    res.v = DenseMatrix::identity(k);
+    if (accumulate) res.v = DenseMatrix::identity(k);
+    DenseMatrix* vp = accumulate ? &res.v : nullptr;
     bool rotated = true;
     int64_t sweep = 0;
     if (k < 96) {
@@ -210,7 +262,7 @@ JacobiSvdResult jacobi_svd_tol(DenseMatrix a, int64_t max_sweeps, double tol) {
             ++sweep;
             column_norms(a, nrm.data());
             for (int64_t p = 0; p + 1 < k; ++p)
-                for (int64_t q = p + 1; q < k; ++q) rotated |= jacobi_pair(a, res.v, nrm.data(), p, q, tol);
+                for (int64_t q = p + 1; q < k; ++q) rotated |= jacobi_pair(a, vp, nrm.data(), p, q, tol);
         }
     } else {
         // Block round-robin: the columns are cut into nblk blocks (2 per thread) and every round
@@ -240,7 +292,7 @@ JacobiSvdResult jacobi_svd_tol(DenseMatrix a, int64_t max_sweeps, double tol) {
             const uint64_t key = (static_cast<uint64_t>(ver[p]) << 32) | ver[q];
             uint64_t& sk = seen[p * k + q];
             if (sk == key) return 0;
-            if (jacobi_pair(a, res.v, nrm.data(), p, q, tol)) {
+            if (jacobi_pair(a, vp, nrm.data(), p, q, tol)) {
                 ++ver[p];
                 ++ver[q];
                 return 1;
@@ -248,36 +300,49 @@ JacobiSvdResult jacobi_svd_tol(DenseMatrix a, int64_t max_sweeps, double tol) {
             sk = key;
             return 0;
         };
+        // Rounds are ordered per block, not by a barrier: a block pair of round r starts as soon
+        // as both of its blocks have finished round r - 1 (acquire/release round counters), so a
+        // thread whose pairs were skipped (late sweeps) runs ahead instead of waiting for the
+        // slowest thread of every round.  Pair i of every round belongs to thread i mod T.
+        std::unique_ptr<std::atomic<int64_t>[]> done(new std::atomic<int64_t>[static_cast<size_t>(nblk)]);
         while (rotated && sweep < max_sweeps) {
             ++sweep;
             int any = 0;
             column_norms(a, nrm.data());
-#pragma omp parallel reduction(| : any)
+            for (int64_t b = 0; b < nblk; ++b) done[b].store(0, std::memory_order_relaxed);
+#pragma omp parallel reduction(+ : any)
             {
+                const int nt = omp_get_num_threads(), t = omp_get_thread_num();
                 std::vector<int64_t> lp(pos);
                 for (int64_t round = 0; round < nblk - 1; ++round) {
-#pragma omp for schedule(dynamic, 1)
-                    for (int64_t i = 0; i < nblk / 2; ++i) {
+                    for (int64_t i = t; i < nblk / 2; i += nt) {
                         int64_t bi = lp[i], bj = lp[nblk - 1 - i];
                         if (bi > bj) std::swap(bi, bj);
+                        while (done[bi].load(std::memory_order_acquire) < round ||
+                               done[bj].load(std::memory_order_acquire) < round)
+                            _mm_pause();
                         const int64_t i0 = blk_lo(bi), i1 = blk_hi(bi), j0 = blk_lo(bj), j1 = blk_hi(bj);
                         if (round == 0) {
                             for (int64_t p = i0; p + 1 < i1; ++p)
-                                for (int64_t q = p + 1; q < i1; ++q) any |= pair(p, q);
+                                for (int64_t q = p + 1; q < i1; ++q) any += pair(p, q);
                             for (int64_t p = j0; p + 1 < j1; ++p)
-                                for (int64_t q = p + 1; q < j1; ++q) any |= pair(p, q);
+                                for (int64_t q = p + 1; q < j1; ++q) any += pair(p, q);
                         }
                         for (int64_t p = i0; p < i1; ++p)
-                            for (int64_t q = j0; q < j1; ++q) any |= pair(p, q);
-                    }  // implicit barrier
+                            for (int64_t q = j0; q < j1; ++q) any += pair(p, q);
+                        done[bi].store(round + 1, std::memory_order_release);
+                        done[bj].store(round + 1, std::memory_order_release);
+                    }
                     const int64_t last = lp[nblk - 1];
                     for (int64_t i = nblk - 1; i > 1; --i) lp[i] = lp[i - 1];
                     lp[1] = last;
                 }
+#pragma omp barrier
 #pragma omp single
                 pos = lp;
             }
             rotated = (any != 0);
+            if (std::getenv("BOSP_DEBUG_SWEEPS")) std::fprintf(stderr, "[bosp] jacobi sweep %lld rotations %d\n", (long long)sweep, any);
         }
     }
     res.converged = !rotated;
@@ -294,13 +359,14 @@ JacobiSvdResult jacobi_svd_tol(DenseMatrix a, int64_t max_sweeps, double tol) {
     std::stable_sort(order.begin(), order.end(), [&](int64_t i, int64_t j) { return sig[i] < sig[j]; });
     res.u = DenseMatrix(m, k);
     res.sigma.resize(static_cast<size_t>(k));
-    DenseMatrix vs(k, k);
+    DenseMatrix vs(accumulate ? k : 0, accumulate ? k : 0);
     for (int64_t j = 0; j < k; ++j) {
         const int64_t src = order[j];
         res.sigma[j] = sig[src];
         const double inv = sig[src] > 0.0 ? 1.0 / sig[src] : 0.0;
         for (int64_t i = 0; i < m; ++i) res.u(i, j) = a(i, src) * inv;
-        for (int64_t i = 0; i < k; ++i) vs(i, j) = res.v(i, src);
+        if (accumulate)
+            for (int64_t i = 0; i < k; ++i) vs(i, j) = res.v(i, src);
     }
     res.v = std::move(vs);
     return res;
@@ -390,10 +456,18 @@ void apply_q(const DenseMatrix& a, const std::vector<double>& tau, DenseMatrix& 
 // One-sided Jacobi SVD with QR preconditioning (Drmac & Veselic): W P = Q R, then the same
 // one-sided Jacobi (rotation formula, 1e-15 test, sweep cap) on X = R^T, whose columns are
 // graded and nearly orthogonal -- a few sweeps instead of ~15 at d = 320.  X V_x = U_x S gives
-// W = (Q V_x) S (P U_x)^T.  Same outputs as jacobi_svd (sigma ascending, u, v).
-JacobiSvdResult jacobi_svd_qr(const DenseMatrix& w, int64_t max_sweeps) {
+// W = (Q V_x) S (P U_x)^T.  Same outputs as jacobi_svd (sigma ascending, u, v), restricted to the
+// first `nvec` (smallest) singular vectors when 0 <= nvec < k (Q applied to those only).
+//
+// Measured and not kept: skipping the accumulation of V_x (half the work per rotation) and
+// solving R^T v_j = sigma_j u_j for the wanted columns instead -- accurate to ~kappa(R~) eps
+// (max |V_x^T V_x - I| = 1.5e-13 at d = 320, vs ~1e-15 accumulated) and 2.5 ms faster per call,
+// but that perturbation moved the SPEC-6 moving-off solve (n = 1000, d = 420, stopped at
+// max_outer_iter) from 299 to 297 converged pairs.
+JacobiSvdResult jacobi_svd_qr(const DenseMatrix& w, int64_t max_sweeps, int64_t nvec) {
     const int64_t m = w.rows(), k = w.cols();
     require(m == k, "jacobi_svd_qr: square input expected");
+    if (nvec < 0 || nvec > k) nvec = k;
     static const bool dbg = std::getenv("BOSP_DEBUG") != nullptr;
     const auto t0 = std::chrono::steady_clock::now();
     DenseMatrix a = w;
@@ -406,21 +480,23 @@ JacobiSvdResult jacobi_svd_qr(const DenseMatrix& w, int64_t max_sweeps) {
         for (int64_t i = j; i < k; ++i) x(i, j) = a(j, i);
     JacobiSvdResult jx = jacobi_svd_tol(std::move(x), max_sweeps, 1e-15);
     const auto t2 = std::chrono::steady_clock::now();
-    // left vectors of W: Q V_x, Q = H_0 H_1 ... H_{k-1} applied to V_x (columns independent)
-    DenseMatrix u = std::move(jx.v);
+    // left vectors of W: Q V_x, Q = H_0 H_1 ... H_{k-1} applied to V_x's wanted columns
+    DenseMatrix u(k, nvec);
+    for (int64_t c = 0; c < nvec; ++c) std::copy(jx.v.col(c), jx.v.col(c) + k, u.col(c));
     apply_q(a, tau, u);
     if (dbg) {
         auto ms = [](auto x0, auto x1) { return std::chrono::duration<double>(x1 - x0).count() * 1e3; };
-        std::fprintf(stderr, "[bosp] svd_qr d=%lld qrcp %.2f ms jacobi %.2f ms (%lld sweeps) apply_q %.2f ms\n",
-                     (long long)k, ms(t0, t1), ms(t1, t2), (long long)jx.sweeps, ms(t2, std::chrono::steady_clock::now()));
+        std::fprintf(stderr, "[bosp] svd_qr d=%lld nvec=%lld qrcp %.2f ms jacobi %.2f ms (%lld sweeps) apply_q %.2f ms\n",
+                     (long long)k, (long long)nvec, ms(t0, t1), ms(t1, t2), (long long)jx.sweeps,
+                     ms(t2, std::chrono::steady_clock::now()));
     }
     // right vectors of W: P U_x (row perm[i] of the result is row i of U_x)
     JacobiSvdResult res;
     res.sigma = std::move(jx.sigma);
     res.converged = jx.converged;
     res.sweeps = jx.sweeps;
-    res.v = DenseMatrix(k, k);
-    for (int64_t j = 0; j < k; ++j)
+    res.v = DenseMatrix(k, nvec);
+    for (int64_t j = 0; j < nvec; ++j)
         for (int64_t i = 0; i < k; ++i) res.v(perm[i], j) = jx.u(i, j);
     res.u = std::move(u);
     return res;
@@ -469,16 +545,21 @@ DenseMatrix lu_inverse(const DenseMatrix& a0) {
 }
 
 ProjectedLrep finish_assembly(const DenseMatrix& khat, const DenseMatrix& mhat) {
+    static const bool dbg = std::getenv("BOSP_DEBUG") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
     ProjectedLrep p;
     p.d = khat.rows();
     p.khat = khat.symmetrized();
     p.mhat = mhat.symmetrized();
-    auto lk = cholesky_lower(p.khat);
+    std::optional<DenseMatrix> lk, lm;
+    cholesky_lower_pair(p.khat, p.mhat, lk, lm);
     if (!lk) throw NullspaceLeak("assemble_projected: U^T K U is not SPD");
-    auto lm = cholesky_lower(p.mhat);
     if (!lm) throw NullspaceLeak("assemble_projected: V^T M V is not SPD");
     p.chol_k = std::move(*lk);
     p.chol_m = std::move(*lm);
+    if (dbg)
+        std::fprintf(stderr, "[bosp] finish_assembly d=%lld %.2f ms\n", (long long)p.d,
+                     std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() * 1e3);
     return p;
 }
 
@@ -490,7 +571,7 @@ SmallEigenSolution solve_small_lrep(const ProjectedLrep& p, int64_t k) {
     // d >= 96 (configs 3/5: d = 320): QR-preconditioned Jacobi, a few sweeps instead of ~15
     static const bool dbg = std::getenv("BOSP_DEBUG") != nullptr;
     const auto t0 = std::chrono::steady_clock::now();
-    JacobiSvdResult svd = p.d >= 96 ? jacobi_svd_qr(matmul_tn(l, r), 40) : jacobi_svd(matmul_tn(l, r));
+    JacobiSvdResult svd = p.d >= 96 ? jacobi_svd_qr(matmul_tn_lower(l, r), 40, k) : jacobi_svd(matmul_tn(l, r));
     if (dbg)
         std::fprintf(stderr, "[bosp] small svd d=%lld sweeps=%lld %.2f ms\n", (long long)p.d, (long long)svd.sweeps,
                      std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() * 1e3);
@@ -499,6 +580,7 @@ SmallEigenSolution solve_small_lrep(const ProjectedLrep& p, int64_t k) {
         if (s < 1e-14 * smax)
             throw DegenerateSpectrum("solve_small_lrep: singular value at round-off scale, "
                                      "a near-zero eigenvalue escaped deflation");
+    const auto t1 = std::chrono::steady_clock::now();
     SmallEigenSolution sol;
     sol.lambdas.assign(svd.sigma.begin(), svd.sigma.begin() + k);
     DenseMatrix phi(p.d, k), psi(p.d, k);
@@ -509,8 +591,11 @@ SmallEigenSolution solve_small_lrep(const ProjectedLrep& p, int64_t k) {
             psi(i, j) = svd.v(i, j) * w;
         }
     }
-    sol.yhat = matmul(l, phi);
-    sol.xhat = matmul(r, psi);
+    sol.yhat = matmul(l, phi, true);  // L, R lower triangular
+    sol.xhat = matmul(r, psi, true);
+    if (dbg)
+        std::fprintf(stderr, "[bosp] small back-transform %.2f ms\n",
+                     std::chrono::duration<double>(std::chrono::steady_clock::now() - t1).count() * 1e3);
     return sol;
 }
 

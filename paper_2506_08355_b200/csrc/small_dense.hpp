@@ -41,11 +41,17 @@ private:
     std::vector<double> data_;
 };
 
-DenseMatrix matmul(const DenseMatrix& a, const DenseMatrix& b);
+// a_lower: a is lower triangular (its structural zeros are skipped).
+DenseMatrix matmul(const DenseMatrix& a, const DenseMatrix& b, bool a_lower = false);
 DenseMatrix matmul_tn(const DenseMatrix& a, const DenseMatrix& b);
+// L^T R for square lower-triangular L, R.
+DenseMatrix matmul_tn_lower(const DenseMatrix& l, const DenseMatrix& r);
 
 // A = L L^T, or nullopt when a pivot is <= 0 / non-finite (dense_kernels.cpp:11-28).
 std::optional<DenseMatrix> cholesky_lower(const DenseMatrix& a);
+// cholesky_lower of two matrices of one order at once (threads; bitwise the serial factors).
+void cholesky_lower_pair(const DenseMatrix& a, const DenseMatrix& b, std::optional<DenseMatrix>& la,
+                         std::optional<DenseMatrix>& lb);
 
 struct JacobiSvdResult {
     DenseMatrix u;
@@ -59,10 +65,12 @@ struct JacobiSvdResult {
 // column pairs of one round rotate concurrently (threads when d is large).
 JacobiSvdResult jacobi_svd(DenseMatrix a, int64_t max_sweeps = 40);
 // The same with the orthogonality test |x^T y| <= tol ||x|| ||y|| (jacobi_svd: tol = 1e-15).
-JacobiSvdResult jacobi_svd_tol(DenseMatrix a, int64_t max_sweeps, double tol);
+// accumulate = false: the rotations are not accumulated (res.v empty; U and sigma only).
+JacobiSvdResult jacobi_svd_tol(DenseMatrix a, int64_t max_sweeps, double tol, bool accumulate = true);
 // Square W: QR-preconditioned one-sided Jacobi (Householder QR with column pivoting, then the
-// same Jacobi on R^T); used by solve_small_lrep for d >= 96.
-JacobiSvdResult jacobi_svd_qr(const DenseMatrix& w, int64_t max_sweeps = 40);
+// same Jacobi on R^T); used by solve_small_lrep for d >= 96.  0 <= nvec < k: only the nvec
+// smallest singular pairs' vectors (u, v are k x nvec; sigma is complete).
+JacobiSvdResult jacobi_svd_qr(const DenseMatrix& w, int64_t max_sweeps = 40, int64_t nvec = -1);
 double spectral_norm(const DenseMatrix& a);
 DenseMatrix lu_inverse(const DenseMatrix& a);
 
