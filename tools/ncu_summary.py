@@ -26,6 +26,10 @@ WANT = [
     ("launch__grid_size", "grid"),
     ("launch__block_size", "block"),
     ("lts__t_sector_hit_rate.pct", "L2 hit rate %"),
+    ("l1tex__t_sector_hit_rate.pct", "L1 hit rate %"),
+    ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active %"),
+    ("smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio", "long-scoreboard stall / issue"),
+    ("launch__occupancy_limit_registers", "occupancy limit (registers), blocks"),
 ]
 
 
