@@ -68,6 +68,7 @@ public:
     void exchange(const std::vector<HaloMsg>& sends, const std::vector<HaloMsg>& recvs,
                   cudaStream_t stream) override;
     void allgather(const double* sdev, int64_t count, double* rdev, cudaStream_t stream) override;
+    bool stream_capturable() const override { return true; }
 
 private:
     void* comm_ = nullptr;

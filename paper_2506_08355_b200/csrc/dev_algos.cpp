@@ -1,6 +1,8 @@
 // Device orchestration of the biorthogonalization and inner-CG building blocks.
 #include "dev_algos.hpp"
 
+#include <atomic>
+
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -670,19 +672,25 @@ DevCgOutcome dev_cg(const LinearOperator& a, const DMat& rhs, const DMat& x, dou
     ws.ensure(rhs.rows, m);
     const DMat r = ws.r.view(), p = ws.p.view(), ap = ws.ap.view();
     const int mi = static_cast<int>(std::min<int64_t>(max_iter, 1 << 30));
-    // one rank: the whole solve is a CUDA graph; several ranks exchange through the
-    // communicator between kernels (host-synchronised for ThreadComm), so the loop is host-driven
+    // one rank: the whole solve is a CUDA graph.  Several ranks: also a graph when the
+    // communicator is stream-ordered (NCCL: the allreduces of p^T A p / r^T r and the halo
+    // send/recv are recorded with the kernels); ThreadComm's host barriers keep the loop
+    // host-driven.  A multi-rank capture that fails falls back to the host loop for good.
     // Graphs pay off where launch overhead matters (config 2: 262144 x 20); on the large blocks
     // of configs 3/5 graph and host loop measured within run-to-run noise (config 3: 14.2-19.4 s
     // vs 17.1-18.8 s over several boxes), so graphs stay the default.  BOSP_NO_GRAPHS=1 forces
     // the host loop (per-kernel ncu captures).
     static const bool no_graphs = std::getenv("BOSP_NO_GRAPHS") != nullptr;
-    if (!x0 && rt.nranks() == 1 && a.impl()->capturable() && !no_graphs) {
+    static std::atomic<bool> multi_capture_failed{false};
+    const bool multi = rt.nranks() > 1;
+    const bool comm_ok = !multi || (rt.comm()->stream_capturable() && !multi_capture_failed.load());
+    CgGraph* g = nullptr;
+    const bool unrolled = max_iter <= kCgUnrollMax && a.impl()->has_masked_dot();
+    if (!x0 && comm_ok && a.impl()->capturable() && !no_graphs) {
         // ---- graph path: the whole solve is one launch, the loop runs on the device ----
         // Operators whose apply honours the column mask record the unrolled graph once at the
         // workspace width and serve every narrower call through the live-width scalar (the
         // solver's GS sweeps shrink 20 -> 19 -> 16 -> ... -> 1 as columns converge).
-        const bool unrolled = max_iter <= kCgUnrollMax && a.impl()->has_masked_dot();
         // Recorded width: the next power of two (capped at the workspace width), so a graph
         // serves widths within 2x of its own and the kernels' grids stay sized for them
         // (recording at the full width for every call measured 8 % slower: narrow solves then
@@ -693,7 +701,6 @@ DevCgOutcome dev_cg(const LinearOperator& a, const DMat& rhs, const DMat& x, dou
             while (mg < m) mg *= 2;
             mg = std::max<int64_t>(m, std::min<int64_t>(mg, ws.r.capacity()));
         }
-        CgGraph* g = nullptr;
         for (CgGraph& c : ws.graphs)
             if (c.op == a.impl()->uid() && c.scratch_gen == rt.scratch_generation() && c.rhs == rhs.p && c.ldr == rhs.ld && c.x == x.p && c.ldx == x.ld &&
                 c.m == mg && c.tol == tol && c.max_iter == max_iter && c.prof_family == rt.prof_family())
@@ -716,7 +723,9 @@ DevCgOutcome dev_cg(const LinearOperator& a, const DMat& rhs, const DMat& x, dou
             rt.scratch(1 << 16);  // no pool growth while recording
             rt.tickets(64);
             g->scratch_gen = rt.scratch_generation();
+            a.impl()->reserve(unrolled ? mg : m);  // halo buffers exist before the capture
             rt.sync();
+            try {
             BOSP_CUDA(cudaGraphCreate(&g->graph, 0));
             // Short solves (the solver's inner CG: max_iter 20) are unrolled into a straight
             // graph -- every kernel early-outs once its columns are done, no conditional node,
@@ -769,13 +778,36 @@ DevCgOutcome dev_cg(const LinearOperator& a, const DMat& rhs, const DMat& x, dou
             rt.set_capture_sink(nullptr);
             rt.set_capture_prof(nullptr);
             BOSP_CUDA(cudaGraphInstantiate(&g->exec, g->graph, 0));
+            } catch (const std::exception& e) {
+                // end the (invalidated) capture, drop the half-built graph; one rank re-throws,
+                // several ranks run the host loop from now on
+                cudaGraph_t tmp = nullptr;
+                cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+                if (cudaStreamIsCapturing(rt.stream(), &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone)
+                    cudaStreamEndCapture(rt.stream(), &tmp);
+                if (tmp) cudaGraphDestroy(tmp);
+                cudaGetLastError();
+                rt.set_capture_sink(nullptr);
+                rt.set_capture_prof(nullptr);
+                rt.timer_reserve(0);
+                if (g->graph) cudaGraphDestroy(g->graph);
+                ws.graphs.pop_back();
+                g = nullptr;
+                if (!multi) throw;
+                multi_capture_failed.store(true);
+                std::fprintf(stderr, "[bosp] cg graph capture over %d ranks failed (%s): host loop\n", rt.nranks(), e.what());
+            }
+            if (g) {
             rt.graph_builds_ += 1;
             rt.graph_build_s_ += std::chrono::duration<double>(std::chrono::steady_clock::now() - tb).count();
             if (std::getenv("BOSP_SYNC_STATS"))
                 std::fprintf(stderr, "[bosp] cg graph: op %p rhs %p x %p m %lld tol %g max_iter %lld (cache %zu)\n",
                              (const void*)a.impl(), (const void*)rhs.p, (const void*)x.p, (long long)m, tol,
                              (long long)max_iter, ws.graphs.size());
+            }
         }
+    }
+    if (g) {
         if (unrolled) set_device_int(ws.m_live, static_cast<int>(m));
         BOSP_CUDA(cudaGraphLaunch(g->exec, rt.stream()));
         if (defer_sweeps && g->body_launches.empty() && g->prof_pairs.empty() && !want_stats) {

@@ -398,7 +398,8 @@ public:
         return sell_spmm(with_halo(x), x, y, &dot);
     }
     bool has_masked_dot() const override { return true; }
-    bool capturable() const override { return false; }
+    bool capturable() const override { return comm_capturable(); }
+    void reserve(int64_t m) const override { buffers(m); }
 
 private:
     struct SendPlan {
@@ -410,9 +411,7 @@ private:
         int peer;
         int64_t cnt, off;
     };
-    SellDev with_halo(const DMat& x) const {
-        Runtime& rt = Runtime::get();
-        const int64_t m = x.cols;
+    void buffers(int64_t m) const {
         if (!halo_ || halo_->capacity() < m) {
             halo_ = std::make_unique<DBlock>(std::max<int64_t>(n_halo_, 1), m);
             sbuf_.clear();
@@ -420,6 +419,11 @@ private:
             for (const SendPlan& s : send_) sbuf_.emplace_back(s.cnt, m);
             for (const RecvPlan& r : recv_) rbuf_.emplace_back(r.cnt, m);
         }
+    }
+    SellDev with_halo(const DMat& x) const {
+        Runtime& rt = Runtime::get();
+        const int64_t m = x.cols;
+        buffers(m);
         std::vector<HaloMsg> sends, recvs;
         for (size_t i = 0; i < send_.size(); ++i) {
             gather_rows(x.p, x.ld, static_cast<const int32_t*>(send_[i].idx.p), send_[i].cnt, m, sbuf_[i].data(),
@@ -460,14 +464,17 @@ public:
         for (const RankRange& r : rg_) nmax_ = std::max(nmax_, r.n);
         Runtime::get().sync();
     }
-    void apply(const DMat& x, const DMat& y) const override {
-        Runtime& rt = Runtime::get();
-        const int64_t m = x.cols, P = static_cast<int64_t>(rg_.size());
+    void reserve(int64_t m) const override {
         if (!full_ || full_->capacity() < m) {
             full_ = std::make_unique<DBlock>(ng_, m);
             send_ = std::make_unique<DBlock>(nmax_ * m, 1);
-            recv_ = std::make_unique<DBlock>(P * nmax_ * m, 1);
+            recv_ = std::make_unique<DBlock>(static_cast<int64_t>(rg_.size()) * nmax_ * m, 1);
         }
+    }
+    void apply(const DMat& x, const DMat& y) const override {
+        Runtime& rt = Runtime::get();
+        const int64_t m = x.cols, P = static_cast<int64_t>(rg_.size());
+        reserve(m);
         BOSP_CUDA(cudaMemcpy2DAsync(send_->data(), nmax_ * sizeof(double), x.p, x.ld * sizeof(double),
                                     x.rows * sizeof(double), m, cudaMemcpyDeviceToDevice, rt.stream()));
         rt.comm()->allgather(send_->data(), nmax_ * m, recv_->data(), rt.stream());
@@ -478,7 +485,7 @@ public:
                                             rg_[r].n * sizeof(double), m, cudaMemcpyDeviceToDevice, rt.stream()));
         gram(ColList(t_.view()), ColList(full_->cols(0, m)), ng_, y.p, y.ld);
     }
-    bool capturable() const override { return false; }
+    bool capturable() const override { return comm_capturable(); }
 
 private:
     DBlock t_;
@@ -518,13 +525,25 @@ public:
         return stencil_spmm(with_halo(x), x, y, &dot);
     }
     bool has_masked_dot() const override { return true; }
-    bool capturable() const override { return !partitioned_; }
+    bool capturable() const override { return !partitioned_ || comm_capturable(); }
+    void reserve(int64_t m) const override {
+        if (partitioned_) buffers(m);
+    }
 
     bool cheap_apply() const override { return true; }
 
 private:
     // Slab partition along the slowest axis: exchange the first / last local plane of every
     // column with the ranks holding the neighbouring slabs (rank - 1 below, rank + 1 above).
+    void buffers(int64_t m) const {
+        const int64_t plane = dev_.dims == 3 ? dev_.nx * dev_.ny : dev_.nx;
+        if (!lo_ || lo_->capacity() < m) {
+            lo_ = std::make_unique<DBlock>(plane, m);
+            hi_ = std::make_unique<DBlock>(plane, m);
+            slo_ = std::make_unique<DBlock>(plane, m);
+            shi_ = std::make_unique<DBlock>(plane, m);
+        }
+    }
     StencilDev with_halo(const DMat& x) const {
         if (!partitioned_) return dev_;
         Runtime& rt = Runtime::get();
@@ -532,12 +551,7 @@ private:
         const int64_t plane = dev_.dims == 3 ? dev_.nx * dev_.ny : dev_.nx;
         const int64_t snl = dev_.dims == 3 ? dev_.nz : dev_.ny;
         const int64_t m = x.cols;
-        if (!lo_ || lo_->capacity() < m) {
-            lo_ = std::make_unique<DBlock>(plane, m);
-            hi_ = std::make_unique<DBlock>(plane, m);
-            slo_ = std::make_unique<DBlock>(plane, m);
-            shi_ = std::make_unique<DBlock>(plane, m);
-        }
+        buffers(m);
         const bool has_lo = dev_.s0 > 0, has_hi = dev_.s0 + snl < dev_.s_global;
         std::vector<HaloMsg> sends, recvs;
         const size_t pb = plane * sizeof(double);
@@ -605,6 +619,7 @@ public:
         axpby(sigma_, x, 1.0, y);  // y += sigma x (linear_operator.cpp:81-92)
     }
     bool capturable() const override { return base_->capturable(); }
+    void reserve(int64_t m) const override { base_->reserve(m); }
     bool cheap_apply() const override { return base_->cheap_apply(); }
 
 private:
@@ -647,6 +662,10 @@ private:
 }  // namespace
 
 OperatorImpl::~OperatorImpl() = default;
+bool comm_capturable() {
+    const Comm* c = Runtime::get().comm();
+    return c && c->stream_capturable();
+}
 uint64_t OperatorImpl::next_uid() {
     static std::atomic<uint64_t> counter{0};
     return ++counter;

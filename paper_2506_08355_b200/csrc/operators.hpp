@@ -22,6 +22,9 @@ public:
     // Whether apply() only enqueues device work on the solver stream (so it can be recorded
     // into a CUDA graph); host callbacks cannot.
     virtual bool capturable() const { return true; }
+    // Allocate whatever apply() of an m-column block allocates lazily (halo / gather buffers),
+    // so that a CUDA graph recorded afterwards never allocates during capture.
+    virtual void reserve(int64_t m) const { (void)m; }
     // y = A x with x(:,j)^T y(:,j) (the CG's p^T A p) fused into the apply: per-block partials
     // (dot.parts[j * blocks + b]) and, with a ticket, folded into dot.out.  Returns the number of
     // partial blocks per column, 0 when unsupported (nothing done).
@@ -43,6 +46,10 @@ private:
     LinearOperator::Kind kind_;
     uint64_t uid_;
 };
+
+// Row-partitioned operators exchange through the communicator inside apply(): recordable into a
+// CUDA graph only when the communicator's calls are stream-ordered (NCCL).
+bool comm_capturable();
 
 }  // namespace b200
 }  // namespace bosp

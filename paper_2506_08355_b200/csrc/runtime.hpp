@@ -38,6 +38,10 @@ public:
                           cudaStream_t stream) = 0;
     // every rank contributes `count` doubles; recv holds size()*count, rank-major
     virtual void allgather(const double* sdev, int64_t count, double* rdev, cudaStream_t stream) = 0;
+    // Every call only enqueues work on `stream` (no host synchronisation), so it can be recorded
+    // into a CUDA graph: NCCL (collectives and grouped send/recv are capturable), not ThreadComm
+    // (its ranks meet at host barriers).
+    virtual bool stream_capturable() const { return false; }
 };
 
 class Runtime {
