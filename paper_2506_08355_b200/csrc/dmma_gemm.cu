@@ -1704,6 +1704,210 @@ __global__ void __launch_bounds__(256) k_biorth_apply(BiorthApplyParams prm) {
     }
 }
 
+// Compile-time variant for the common widths (<= 24 kept columns, KP = X columns rounded to 4):
+// the K loop is unrolled, upper-triangular coefficients (TRI) stop the K loop of column block j
+// after row 8 j + 7 at compile time, a warp owns RG groups of 8 rows (each coefficient fragment
+// read from shared memory feeds RG DMMAs: the kernel is bound by the shared-memory data pipe
+// next to the DMMA pipe, ncu: 67 % / 52 %), and the warp-private P, Q strips alias the warp's own
+// rows of the X, Y stage (completely consumed before the strip is written).
+template <int BN, int KP, bool TRI, int RG>
+__global__ void __launch_bounds__(256, 2) k_biorth_apply4(BiorthApplyParams prm) {
+    constexpr int NT = BN / 8;
+    constexpr int TR = 64 * RG;           // rows per tile
+    constexpr int LD = TR + 4;            // smem stride of a stage column
+    constexpr int LDCS = (KP + 15) / 16 * 16 + 4;
+    extern __shared__ __align__(16) double smem[];
+    if (prm.status && *prm.status) return;
+    double* sca = smem;                   // [BN][LDCS]
+    double* scb = sca + BN * LDCS;        // [BN][LDCS]
+    double* sx = scb + BN * LDCS;         // [2][KP][LD]
+    double* sy = sx + 2 * KP * LD;        // [2][KP][LD]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int gid = lane >> 2, tig = lane & 3;
+    const int k = prm.k, kb = prm.kb;
+    for (int e = threadIdx.x; e < BN * (KP / 2); e += 256) {
+        const int c = e / (KP / 2), k2 = 2 * (e % (KP / 2));
+        int bytes = 0;
+        const double *srca = prm.ca, *srcb = prm.cb;
+        if (c < kb && k2 < k) {
+            bytes = (k - k2) >= 2 ? 16 : 8;
+            srca = prm.ca + c * prm.ldc + k2;
+            srcb = prm.cb + c * prm.ldc + k2;
+        }
+        cp_async16(sca + c * LDCS + k2, srca, bytes);
+        cp_async16(scb + c * LDCS + k2, srcb, bytes);
+    }
+    auto load = [&](int buf, int64_t tile) {
+        const int64_t m0 = tile * TR;
+#pragma unroll
+        for (int e0 = 0; e0 < KP * (TR / 2); e0 += 256) {
+            const int e = e0 + threadIdx.x;
+            if ((KP * (TR / 2)) % 256 != 0 && e >= KP * (TR / 2)) break;
+            const int kk = e / (TR / 2), m2 = 2 * (e % (TR / 2));
+            const int64_t m = m0 + m2;
+            int bytes = 0;
+            const double *srcx = prm.ca, *srcy = prm.ca;
+            if (kk < k && m < prm.n) {
+                bytes = (prm.n - m) >= 2 ? 16 : 8;
+                srcx = colptr(prm.x, kk) + m;
+                srcy = colptr(prm.y, kk) + m;
+            }
+            cp_async16(sx + (buf * KP + kk) * LD + m2, srcx, bytes);
+            cp_async16(sy + (buf * KP + kk) * LD + m2, srcy, bytes);
+        }
+    };
+    double g[NT][NT][2];
+#pragma unroll
+    for (int i = 0; i < NT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) g[i][j][0] = g[i][j][1] = 0.0;
+    int64_t tile = blockIdx.x;
+    if (tile < prm.tiles) load(0, tile);
+    cp_async_commit();
+    int buf = 0;
+    const int wr = warp * 8 * RG;
+    for (; tile < prm.tiles; tile += gridDim.x, buf ^= 1) {
+        const int64_t next = tile + gridDim.x;
+        if (next < prm.tiles) load(buf ^ 1, next);
+        cp_async_commit();
+        cp_async_wait<1>();
+        __syncthreads();
+        double* ax = sx + buf * KP * LD + wr;
+        double* ay = sy + buf * KP * LD + wr;
+        double accp[RG][NT][2], accq[RG][NT][2];
+#pragma unroll
+        for (int r = 0; r < RG; ++r)
+#pragma unroll
+            for (int j = 0; j < NT; ++j) accp[r][j][0] = accp[r][j][1] = accq[r][j][0] = accq[r][j][1] = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < KP; kk += 4) {
+            double fx[RG], fy[RG];
+#pragma unroll
+            for (int r = 0; r < RG; ++r) {
+                fx[r] = ax[(kk + tig) * LD + 8 * r + gid];
+                fy[r] = ay[(kk + tig) * LD + 8 * r + gid];
+            }
+#pragma unroll
+            for (int j = 0; j < NT; ++j) {
+                if (TRI && kk >= 8 * (j + 1)) continue;
+                const double ca = sca[(j * 8 + gid) * LDCS + kk + tig];
+                const double cb = scb[(j * 8 + gid) * LDCS + kk + tig];
+#pragma unroll
+                for (int r = 0; r < RG; ++r) {
+                    dmma(accp[r][j][0], accp[r][j][1], fx[r], ca);
+                    dmma(accq[r][j][0], accq[r][j][1], fy[r], cb);
+                }
+            }
+        }
+        __syncwarp();  // every lane has consumed its X, Y fragments: the rows become the strip
+#pragma unroll
+        for (int r = 0; r < RG; ++r) {
+            const int64_t row = tile * TR + wr + 8 * r + gid;
+#pragma unroll
+            for (int j = 0; j < NT; ++j)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int col = j * 8 + 2 * tig + h;
+                    if (col < KP) {  // columns kb..KP-1 are exact zeros (zero-padded coefficients)
+                        ax[col * LD + 8 * r + gid] = accp[r][j][h];
+                        ay[col * LD + 8 * r + gid] = accq[r][j][h];
+                    }
+                    if (row < prm.n && col < kb) {
+                        __stcs(prm.p + static_cast<int64_t>(col) * prm.ldp + row, accp[r][j][h]);
+                        __stcs(prm.q + static_cast<int64_t>(col) * prm.ldq + row, accq[r][j][h]);
+                    }
+                }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int s2 = 0; s2 < 8 * RG; s2 += 4) {
+            double fp[NT], fq[NT];
+#pragma unroll
+            for (int i = 0; i < NT; ++i) {
+                const bool in = i * 8 + gid < KP;
+                fp[i] = in ? ax[(i * 8 + gid) * LD + s2 + tig] : 0.0;
+                fq[i] = in ? ay[(i * 8 + gid) * LD + s2 + tig] : 0.0;
+            }
+#pragma unroll
+            for (int i = 0; i < NT; ++i)
+#pragma unroll
+                for (int j = 0; j < NT; ++j) dmma(g[i][j][0], g[i][j][1], fp[i], fq[j]);
+        }
+        __syncthreads();  // everyone is done with `buf` before it is refilled
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+    double* red = smem;
+    for (int w = 0; w < 8; ++w) {
+        if (warp == w) {
+#pragma unroll
+            for (int i = 0; i < NT; ++i)
+#pragma unroll
+                for (int j = 0; j < NT; ++j) {
+                    const int m = i * 8 + gid, nn = j * 8 + 2 * tig;
+                    red[m + nn * BN] = (w == 0 ? 0.0 : red[m + nn * BN]) + g[i][j][0];
+                    red[m + (nn + 1) * BN] = (w == 0 ? 0.0 : red[m + (nn + 1) * BN]) + g[i][j][1];
+                }
+        }
+        __syncthreads();
+    }
+    double* part = prm.partial + static_cast<int64_t>(blockIdx.x) * (32 * 32);
+    for (int e = threadIdx.x; e < BN * BN; e += 256) {
+        const int m = e % BN, nn = e / BN;
+        part[m + nn * 32] = red[e];
+    }
+}
+
+template <int BN, int KP, bool TRI, int RG>
+void launch_biorth_apply4(BiorthApplyParams prm, int64_t n, double* g, int64_t ldg, const DMat& pv, const DMat& qv) {
+    Runtime& rt = Runtime::get();
+    constexpr int TR = 64 * RG, LD = TR + 4, LDCS = (KP + 15) / 16 * 16 + 4;
+    constexpr size_t smem = sizeof(double) * (2ull * BN * LDCS + 4ull * KP * LD);
+    static int per_sm[64] = {0};
+    if (per_sm[rt.device() & 63] == 0) {
+        BOSP_CUDA(cudaFuncSetAttribute(k_biorth_apply4<BN, KP, TRI, RG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(232448)));
+        int r = 0;
+        BOSP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, k_biorth_apply4<BN, KP, TRI, RG>, 256, smem));
+        per_sm[rt.device() & 63] = std::max(1, r);
+    }
+    prm.tiles = (n + TR - 1) / TR;
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(prm.tiles, per_sm[rt.device() & 63] * rt.sm_count())));
+    prm.partial = rt.scratch(static_cast<size_t>(grid) * 32 * 32);
+    const double flops = 2.0 * n * prm.k * prm.kb * 2 + 2.0 * n * prm.kb * prm.kb;
+    const double bytes = 8.0 * n * (2.0 * prm.k + 2.0 * prm.kb);
+    {
+        LaunchScope ls("product", bytes, flops);
+        k_biorth_apply4<BN, KP, TRI, RG><<<grid, 256, smem, rt.stream()>>>(prm);
+        BOSP_LAUNCH_CHECK();
+    }
+    GramParams gp{};
+    gp.job[0] = GramJob{ColList(pv), ColList(qv), g, ldg};
+    gp.tiles_n[0] = 1;
+    gp.tiles[0] = 1;
+    gp.splits = grid;
+    gp.partial = prm.partial;
+    gp.job_stride = static_cast<int64_t>(grid) * 32 * 32;
+    {
+        LaunchScope ls("gram_reduce");
+        k_gram_reduce<32, 32><<<dim3(32 * 32 / kRedElems, 1, 1), kRedElems * kRedGroups, 0, rt.stream()>>>(gp);
+        BOSP_LAUNCH_CHECK();
+    }
+}
+
+template <int BN, int KP>
+bool dispatch_biorth_apply4(const BiorthApplyParams& prm, int tri, int rg, int64_t n, double* g, int64_t ldg,
+                            const DMat& pv, const DMat& qv) {
+    if (tri) {
+        if (rg == 2) launch_biorth_apply4<BN, KP, true, 2>(prm, n, g, ldg, pv, qv);
+        else launch_biorth_apply4<BN, KP, true, 1>(prm, n, g, ldg, pv, qv);
+    } else {
+        if (rg == 2) launch_biorth_apply4<BN, KP, false, 2>(prm, n, g, ldg, pv, qv);
+        else launch_biorth_apply4<BN, KP, false, 1>(prm, n, g, ldg, pv, qv);
+    }
+    return true;
+}
+
 template <int BN>
 void launch_biorth_apply(BiorthApplyParams prm, int64_t n, double* g, int64_t ldg, const DMat& pv, const DMat& qv) {
     Runtime& rt = Runtime::get();
@@ -2071,6 +2275,18 @@ void biorth_apply(const DMat& x, const DMat& y, const double* ca, const double* 
     prm.n = n;
     prm.tiles = (n + 63) / 64;
     prm.status = status_dev;
+    int tri = col_kend != nullptr;
+    for (int c = 0; tri && c < kb; ++c) tri = col_kend[c] <= c + 1;
+    // the common widths run the compile-time kernel (BOSP_APPLY4=0: the runtime-width one;
+    // =1 / =2: 8 / 16 rows per warp)
+    static const int v4 = std::getenv("BOSP_APPLY4") ? std::atoi(std::getenv("BOSP_APPLY4")) : 2;
+    if (v4 > 0 && n >= 8192) {
+        const int bn = (kb + 7) / 8 * 8;
+#define BOSP_A4(BN_, KP_) \
+    if (bn == BN_ && kpad == KP_ && dispatch_biorth_apply4<BN_, KP_>(prm, tri, v4, n, g, ldg, pv, qv)) return;
+        BOSP_A4(24, 20) BOSP_A4(24, 24) BOSP_A4(16, 12) BOSP_A4(16, 16) BOSP_A4(8, 4) BOSP_A4(8, 8)
+#undef BOSP_A4
+    }
     switch ((kb + 7) / 8) {
         case 1: return launch_biorth_apply<8>(prm, n, g, ldg, pv, qv);
         case 2: return launch_biorth_apply<16>(prm, n, g, ldg, pv, qv);
