@@ -1806,15 +1806,21 @@ __global__ void __launch_bounds__(256, 2) k_biorth_apply4(BiorthApplyParams prm)
 #pragma unroll
             for (int j = 0; j < NT; ++j)
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
+                for (int s = 0; s < 2; ++s) {
+                    // lanes tig = 0..3 store columns 0, 2, 5, 7 (then 1, 3, 4, 6) of the block:
+                    // distinct mod 4, so the strip stores (stride LD = 4 mod 16) hit 16
+                    // distinct banks per half-warp (same-h stores were 2-way conflicts)
+                    const int h = (tig >> 1) ^ s;
                     const int col = j * 8 + 2 * tig + h;
+                    const double vp = h ? accp[r][j][1] : accp[r][j][0];
+                    const double vq = h ? accq[r][j][1] : accq[r][j][0];
                     if (col < KP) {  // columns kb..KP-1 are exact zeros (zero-padded coefficients)
-                        ax[col * LD + 8 * r + gid] = accp[r][j][h];
-                        ay[col * LD + 8 * r + gid] = accq[r][j][h];
+                        ax[col * LD + 8 * r + gid] = vp;
+                        ay[col * LD + 8 * r + gid] = vq;
                     }
                     if (row < prm.n && col < kb) {
-                        __stcs(prm.p + static_cast<int64_t>(col) * prm.ldp + row, accp[r][j][h]);
-                        __stcs(prm.q + static_cast<int64_t>(col) * prm.ldq + row, accq[r][j][h]);
+                        __stcs(prm.p + static_cast<int64_t>(col) * prm.ldp + row, vp);
+                        __stcs(prm.q + static_cast<int64_t>(col) * prm.ldq + row, vq);
                     }
                 }
         }
