@@ -92,8 +92,11 @@ def test_mgs_biorth_golden(golden_small, tag, seed, n, m):
     x, y = kernel_inputs(seed, n, m)
     p, q, kept, dropped = bosp.mgs_biorth(x, y)
     assert list(kept) == list(golden_small[f"mgs_{tag}_kept"])
-    assert np.allclose(p, golden_small[f"mgs_{tag}_p"], rtol=1e-7, atol=1e-8)
-    assert np.allclose(q, golden_small[f"mgs_{tag}_q"], rtol=1e-7, atol=1e-8)
+    # the coefficient-space recurrence differs from the reference's column recurrence by
+    # rounding only: measured 1.4e-13 / 3.2e-13 of max|P| (cond(X^T Y) = 25 / 233)
+    for got, tag2 in ((p, "p"), (q, "q")):
+        want = golden_small[f"mgs_{tag}_{tag2}"]
+        assert np.abs(got - want).max() <= 1e-11 * np.abs(want).max()
     assert bosp.biorth_residual(p, q) < 1e-10
 
 
