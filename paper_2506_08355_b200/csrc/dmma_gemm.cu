@@ -1737,23 +1737,32 @@ __global__ void __launch_bounds__(256, 2) k_biorth_apply4(BiorthApplyParams prm)
         cp_async16(sca + c * LDCS + k2, srca, bytes);
         cp_async16(scb + c * LDCS + k2, srcb, bytes);
     }
+    // column base pointers once per CTA (the ColList segment search per cp.async was ~55 % of
+    // the kernel's instructions); columns past k stay null and are zero-filled
+    __shared__ const double* colx[KP];
+    __shared__ const double* coly[KP];
+    if (threadIdx.x < KP) {
+        const int kk = threadIdx.x;
+        colx[kk] = kk < k ? colptr(prm.x, kk) : nullptr;
+        coly[kk] = kk < k ? colptr(prm.y, kk) : nullptr;
+    }
+    __syncthreads();
+    constexpr int CPI = 256 / (TR / 2);   // columns per pass of the 256 threads
+    const int lm2 = 2 * (threadIdx.x % (TR / 2)), lk0 = threadIdx.x / (TR / 2);
     auto load = [&](int buf, int64_t tile) {
-        const int64_t m0 = tile * TR;
+        const int64_t m = tile * TR + lm2;
+        const int rb = m < prm.n ? ((prm.n - m) >= 2 ? 16 : 8) : 0;
+        double* dx = sx + (buf * KP + lk0) * LD + lm2;
+        double* dy = sy + (buf * KP + lk0) * LD + lm2;
 #pragma unroll
-        for (int e0 = 0; e0 < KP * (TR / 2); e0 += 256) {
-            const int e = e0 + threadIdx.x;
-            if ((KP * (TR / 2)) % 256 != 0 && e >= KP * (TR / 2)) break;
-            const int kk = e / (TR / 2), m2 = 2 * (e % (TR / 2));
-            const int64_t m = m0 + m2;
-            int bytes = 0;
-            const double *srcx = prm.ca, *srcy = prm.ca;
-            if (kk < k && m < prm.n) {
-                bytes = (prm.n - m) >= 2 ? 16 : 8;
-                srcx = colptr(prm.x, kk) + m;
-                srcy = colptr(prm.y, kk) + m;
-            }
-            cp_async16(sx + (buf * KP + kk) * LD + m2, srcx, bytes);
-            cp_async16(sy + (buf * KP + kk) * LD + m2, srcy, bytes);
+        for (int it = 0; it < (KP + CPI - 1) / CPI; ++it) {
+            const int kk = it * CPI + lk0;
+            if (KP % CPI != 0 && kk >= KP) break;
+            const double* px = colx[kk];
+            const double* py = coly[kk];
+            const int bytes = px ? rb : 0;
+            cp_async16(dx + it * CPI * LD, bytes ? px + m : prm.ca, bytes);
+            cp_async16(dy + it * CPI * LD, bytes ? py + m : prm.ca, bytes);
         }
     };
     double g[NT][NT][2];
@@ -1872,7 +1881,7 @@ void launch_biorth_apply4(BiorthApplyParams prm, int64_t n, double* g, int64_t l
     static int per_sm[64] = {0};
     if (per_sm[rt.device() & 63] == 0) {
         BOSP_CUDA(cudaFuncSetAttribute(k_biorth_apply4<BN, KP, TRI, RG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(232448)));
+                                       static_cast<int>(smem)));
         int r = 0;
         BOSP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, k_biorth_apply4<BN, KP, TRI, RG>, 256, smem));
         per_sm[rt.device() & 63] = std::max(1, r);
