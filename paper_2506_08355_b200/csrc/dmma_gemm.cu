@@ -1604,20 +1604,25 @@ __global__ void __launch_bounds__(256) k_biorth_apply(BiorthApplyParams prm) {
         cp_async16(sca + c * ldcs + k2, srca, bytes);
         cp_async16(scb + c * ldcs + k2, srcb, bytes);
     }
+    // column base pointers once per CTA (see k_biorth_apply4); null past k: zero fill
+    __shared__ const double* colx[32];
+    __shared__ const double* coly[32];
+    if (threadIdx.x < 32) {
+        const int kk = threadIdx.x;
+        colx[kk] = kk < k ? colptr(prm.x, kk) : nullptr;
+        coly[kk] = kk < k ? colptr(prm.y, kk) : nullptr;
+    }
+    __syncthreads();
+    const int lm2 = 2 * (threadIdx.x & 31), lk0 = threadIdx.x >> 5;
     auto load = [&](int buf, int64_t tile) {
-        const int64_t m0 = tile * 64;
-        for (int e = threadIdx.x; e < kp * 32; e += 256) {
-            const int kk = e / 32, m2 = 2 * (e % 32);
-            const int64_t m = m0 + m2;
-            int bytes = 0;
-            const double *srcx = prm.ca, *srcy = prm.ca;
-            if (kk < k && m < prm.n) {
-                bytes = (prm.n - m) >= 2 ? 16 : 8;
-                srcx = colptr(prm.x, kk) + m;
-                srcy = colptr(prm.y, kk) + m;
-            }
-            cp_async16(sx + (buf * kp + kk) * kBaLd + m2, srcx, bytes);
-            cp_async16(sy + (buf * kp + kk) * kBaLd + m2, srcy, bytes);
+        const int64_t m = tile * 64 + lm2;
+        const int rb = m < prm.n ? ((prm.n - m) >= 2 ? 16 : 8) : 0;
+        for (int kk = lk0; kk < kp; kk += 8) {
+            const double* px = colx[kk];
+            const double* py = coly[kk];
+            const int bytes = px ? rb : 0;
+            cp_async16(sx + (buf * kp + kk) * kBaLd + lm2, bytes ? px + m : prm.ca, bytes);
+            cp_async16(sy + (buf * kp + kk) * kBaLd + lm2, bytes ? py + m : prm.ca, bytes);
         }
     };
     double g[NT][NT][2];
@@ -1930,7 +1935,7 @@ void launch_biorth_apply(BiorthApplyParams prm, int64_t n, double* g, int64_t ld
     static int per_sm[64] = {0};
     if (per_sm[rt.device() & 63] == 0) {
         BOSP_CUDA(cudaFuncSetAttribute(k_biorth_apply<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(232448)));
+                                       static_cast<int>(232448 - 1024)));
         int r = 0;
         BOSP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, k_biorth_apply<BN>, 256, smem));
         per_sm[rt.device() & 63] = std::max(1, r);
