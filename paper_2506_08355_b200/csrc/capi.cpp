@@ -524,8 +524,14 @@ bosp_status bosp_test_biorth_apply(int64_t n, int64_t k, int64_t kb, const doubl
         bosp::to_device(y, n, k, n, yd.view());
         bosp::to_device(a, k, kb, k, cd.cols(0, kb));
         bosp::to_device(b, k, kb, k, cd.cols(kb, kb));
+        // K bound of every coefficient column (its last nonzero row in A or B): upper-triangular
+        // inputs take the kernels' triangular K loops, as the solver's calls do
+        std::vector<int32_t> ke(static_cast<size_t>(kb), 0);
+        for (int64_t c = 0; c < kb; ++c)
+            for (int64_t r = 0; r < k; ++r)
+                if (a[r + c * k] != 0.0 || b[r + c * k] != 0.0) ke[c] = static_cast<int32_t>(r + 1);
         bosp::biorth_apply(xd.view(), yd.view(), cd.data(), cd.data() + kb * cd.ld(), cd.ld(), static_cast<int>(kb),
-                           pd.view(), qd.view(), gd.data(), gd.ld());
+                           pd.view(), qd.view(), gd.data(), gd.ld(), ke.data());
         bosp::to_host(pd.view(), p, n);
         bosp::to_host(qd.view(), q, n);
         bosp::to_host(gd.view(), g, kb);

@@ -326,16 +326,22 @@ def test_gram_multi_job_segments(a, b, nseg):
             assert rel(g3, y.T @ y) < 1e-13, (njobs, "yy")
 
 
-@pytest.mark.parametrize("k,kb", [(1, 1), (7, 5), (20, 20), (24, 17), (32, 32), (20, 2)])
-@pytest.mark.parametrize("n", [1, 63, 5003, 262147])
-def test_biorth_apply_fused(k, kb, n):
+@pytest.mark.parametrize("full", [False, True])
+@pytest.mark.parametrize("k,kb", [(1, 1), (4, 4), (7, 5), (8, 8), (12, 9), (12, 12), (16, 16), (20, 20), (24, 17),
+                                  (24, 24), (32, 32), (20, 2)])
+@pytest.mark.parametrize("n", [1, 63, 5003, 8192, 8321, 262147])
+def test_biorth_apply_fused(k, kb, n, full):
     """MGS-Biorth application fused with its check Gram: P = X A, Q = Y B, P^T Q in one kernel
-    (biorth.cpp:19-69 / :104-107) against numpy; row counts with a partial last 64-row tile."""
+    (biorth.cpp:19-69 / :104-107) against numpy; row counts with a partial last 64- / 128-row
+    tile, upper-triangular coefficients (the kernels' triangular K loops) and full ones, every
+    compile-time width pair of k_biorth_apply4 plus the runtime-width and TMA kernels."""
     rng = np.random.default_rng(7 * k + kb + n)
     x = np.asfortranarray(rng.uniform(-1, 1, (n, k)))
     y = np.asfortranarray(rng.uniform(-1, 1, (n, k)))
-    a = np.asfortranarray(np.triu(rng.uniform(-1, 1, (k, kb))))
-    b = np.asfortranarray(np.triu(rng.uniform(-1, 1, (k, kb))))
+    a = np.asfortranarray(rng.uniform(-1, 1, (k, kb)))
+    b = np.asfortranarray(rng.uniform(-1, 1, (k, kb)))
+    if not full:
+        a, b = np.asfortranarray(np.triu(a)), np.asfortranarray(np.triu(b))
     p, q, g = bosp._test_biorth_apply(x, y, a, b)
     pr, qr = x @ a, y @ b
     assert rel(p, pr) < 1e-13 and rel(q, qr) < 1e-13
