@@ -1907,16 +1907,17 @@ void launch_biorth_apply4(BiorthApplyParams prm, int64_t n, double* g, int64_t l
     Runtime& rt = Runtime::get();
     constexpr int TR = 64 * RG, LD = TR + 4, LDCS = (KP + 15) / 16 * 16 + 4;
     constexpr size_t smem = sizeof(double) * (2ull * BN * LDCS + 4ull * KP * LD);
-    static int per_sm[64] = {0};
-    if (per_sm[rt.device() & 63] == 0) {
+    static int per_sm[32] = {0};
+    static unsigned attr_mask = 0;
+    rt.once_per_device(attr_mask, [&] {  // ranks sharing a GPU (ThreadComm) set it up once
         BOSP_CUDA(cudaFuncSetAttribute(k_biorth_apply4<BN, KP, TRI, RG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem)));
         int r = 0;
         BOSP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, k_biorth_apply4<BN, KP, TRI, RG>, 256, smem));
-        per_sm[rt.device() & 63] = std::max(1, r);
-    }
+        per_sm[rt.device() & 31] = std::max(1, r);
+    });
     prm.tiles = (n + TR - 1) / TR;
-    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(prm.tiles, per_sm[rt.device() & 63] * rt.sm_count())));
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(prm.tiles, per_sm[rt.device() & 31] * rt.sm_count())));
     prm.partial = rt.scratch(static_cast<size_t>(grid) * 32 * 32);
     const double flops = 2.0 * n * prm.k * prm.kb * 2 + 2.0 * n * prm.kb * prm.kb;
     const double bytes = 8.0 * n * (2.0 * prm.k + 2.0 * prm.kb);
