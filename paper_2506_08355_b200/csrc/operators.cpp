@@ -520,14 +520,21 @@ public:
         const int64_t snl = dev_.dims == 3 ? s.nz : s.ny;
         partitioned_ = s.s_global > 0 && (s.s0 > 0 || s.s0 + snl < s.s_global);
     }
-    void apply(const DMat& x, const DMat& y) const override { stencil_spmm(with_halo(x), x, y); }
-    int apply_dot(const DMat& x, const DMat& y, const SpmmDot& dot) const override {
-        return stencil_spmm(with_halo(x), x, y, &dot);
-    }
+    void apply(const DMat& x, const DMat& y) const override { run(x, y, nullptr); }
+    int apply_dot(const DMat& x, const DMat& y, const SpmmDot& dot) const override { return run(x, y, &dot); }
     bool has_masked_dot() const override { return true; }
     bool capturable() const override { return !partitioned_ || comm_capturable(); }
     void reserve(int64_t m) const override {
-        if (partitioned_) buffers(m);
+        if (partitioned_) {
+            buffers(m);
+            side();
+        }
+    }
+    ~StencilOp() override {
+        if (ev_pack_) cudaEventDestroy(ev_pack_);
+        if (ev_halo_) cudaEventDestroy(ev_halo_);
+        if (side_) cudaStreamDestroy(side_);
+        cudaGetLastError();
     }
 
     bool cheap_apply() const override { return true; }
@@ -543,6 +550,60 @@ private:
             slo_ = std::make_unique<DBlock>(plane, m);
             shi_ = std::make_unique<DBlock>(plane, m);
         }
+    }
+    // side stream + events of the halo overlap, created on first use (before any graph capture:
+    // reserve() runs ahead of the CG's capture)
+    cudaStream_t side() const {
+        if (!side_) {
+            BOSP_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
+            BOSP_CUDA(cudaEventCreateWithFlags(&ev_pack_, cudaEventDisableTiming));
+            BOSP_CUDA(cudaEventCreateWithFlags(&ev_halo_, cudaEventDisableTiming));
+        }
+        return side_;
+    }
+    // Slab-partitioned apply with the halo exchange overlapped with the interior planes
+    // (SURVEY 8e): pack the two boundary planes on the apply stream, launch the interior, run the
+    // exchange on the side stream behind the pack, apply the boundary planes behind the exchange.
+    // BOSP_HALO_OVERLAP=0: exchange first, one launch.
+    int run(const DMat& x, const DMat& y, const SpmmDot* dot) const {
+        static const bool overlap = !std::getenv("BOSP_HALO_OVERLAP") || std::atoi(std::getenv("BOSP_HALO_OVERLAP")) != 0;
+        if (!partitioned_ || !overlap) return stencil_spmm(with_halo(x), x, y, dot);
+        Runtime& rt = Runtime::get();
+        const int me = rt.comm()->rank();
+        const int64_t plane = dev_.dims == 3 ? dev_.nx * dev_.ny : dev_.nx;
+        const int64_t snl = dev_.dims == 3 ? dev_.nz : dev_.ny;
+        const int64_t m = x.cols;
+        buffers(m);
+        const cudaStream_t sd = side();
+        StencilOverlap ov;
+        ov.plane = plane;
+        ov.has_lo = dev_.s0 > 0;
+        ov.has_hi = dev_.s0 + snl < dev_.s_global;
+        std::vector<HaloMsg> sends, recvs;
+        const size_t pb = plane * sizeof(double);
+        if (ov.has_lo) {
+            BOSP_CUDA(cudaMemcpy2DAsync(slo_->data(), pb, x.p, x.ld * sizeof(double), pb, m,
+                                        cudaMemcpyDeviceToDevice, rt.stream()));
+            sends.push_back({me - 1, slo_->data(), plane * m});
+            recvs.push_back({me - 1, lo_->data(), plane * m});
+        }
+        if (ov.has_hi) {
+            BOSP_CUDA(cudaMemcpy2DAsync(shi_->data(), pb, x.p + (snl - 1) * plane, x.ld * sizeof(double), pb, m,
+                                        cudaMemcpyDeviceToDevice, rt.stream()));
+            sends.push_back({me + 1, shi_->data(), plane * m});
+            recvs.push_back({me + 1, hi_->data(), plane * m});
+        }
+        BOSP_CUDA(cudaEventRecord(ev_pack_, rt.stream()));
+        ov.exchange = [&] {
+            BOSP_CUDA(cudaStreamWaitEvent(sd, ev_pack_, 0));
+            rt.comm()->exchange(sends, recvs, sd);
+            BOSP_CUDA(cudaEventRecord(ev_halo_, sd));
+            BOSP_CUDA(cudaStreamWaitEvent(rt.stream(), ev_halo_, 0));
+        };
+        StencilDev d = dev_;
+        d.halo_lo = ov.has_lo ? lo_->data() : nullptr;
+        d.halo_hi = ov.has_hi ? hi_->data() : nullptr;
+        return stencil_spmm(d, x, y, dot, &ov);
     }
     StencilDev with_halo(const DMat& x) const {
         if (!partitioned_) return dev_;
@@ -577,6 +638,8 @@ private:
     StencilDev dev_;
     bool partitioned_ = false;
     mutable std::unique_ptr<DBlock> lo_, hi_, slo_, shi_;
+    mutable cudaStream_t side_ = nullptr;
+    mutable cudaEvent_t ev_pack_ = nullptr, ev_halo_ = nullptr;
 };
 
 class ScaledIdentityOp final : public OperatorImpl {

@@ -1,6 +1,8 @@
 // Block sparse-matrix x multi-vector on sm_100a: SELL-32 CSR and matrix-free 5/7-point stencils.
 #pragma once
 
+#include <functional>
+
 #include "common.hpp"
 
 namespace bosp {
@@ -94,7 +96,16 @@ struct StencilDev {
     const double* halo_lo = nullptr;
     const double* halo_hi = nullptr;
 };
-int stencil_spmm(const StencilDev& s, const DMat& x, const DMat& y, const SpmmDot* dot = nullptr);
+// Halo overlap of a slab-partitioned stencil: `exchange` posts the halo exchange (on its own
+// stream) and makes the apply stream wait for it; stencil_spmm calls it after launching the
+// interior planes, then applies the boundary plane(s) (plane values each, below / above).
+struct StencilOverlap {
+    int64_t plane = 0;
+    bool has_lo = false, has_hi = false;
+    std::function<void()> exchange;
+};
+int stencil_spmm(const StencilDev& s, const DMat& x, const DMat& y, const SpmmDot* dot = nullptr,
+                 const StencilOverlap* ov = nullptr);
 
 }  // namespace b200
 }  // namespace bosp

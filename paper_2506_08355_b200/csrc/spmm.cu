@@ -6,6 +6,7 @@
 // once per column (16 B per row per column).  Neighbour re-reads of x hit L1/L2.  Reference:
 // SparseMatrixCSR::apply (sparse_csr.cpp:29-36) via from_csr (linear_operator.cpp:33-43), and
 // the matrix-free from_callback path (linear_operator.cpp:45-47) for the stencils.
+#include <cstdio>
 #include <algorithm>
 #include <cstdlib>
 #include <vector>
@@ -31,7 +32,9 @@ constexpr int kRows = 256;  // threads per block = rows per block (8 SELL slices
 // Per-block partial sums of x(:,j)^T y(:,j) for the CB columns of this block, written to
 // dots[j * gridDim.x + blockIdx.x] (fixed order; folded by the CG update blocks).
 template <int CB>
-__device__ __forceinline__ void block_dots_out(double (&d)[CB], double* dots, int j0, int ncols) {
+__device__ __forceinline__ void block_dots_out(double (&d)[CB], double* dots, int j0, int ncols, int nb = 0,
+                                               int boff = 0) {
+    if (nb == 0) nb = static_cast<int>(gridDim.x);  // nb, boff: a launch that writes a slice of the partials
     __shared__ double red[kRows / 32][CB];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #pragma unroll
@@ -45,14 +48,14 @@ __device__ __forceinline__ void block_dots_out(double (&d)[CB], double* dots, in
     if (threadIdx.x < CB && j0 + static_cast<int>(threadIdx.x) < ncols) {
         double t = 0.0;
         for (int w = 0; w < kRows / 32; ++w) t += red[w][threadIdx.x];
-        dots[static_cast<int64_t>(j0 + threadIdx.x) * gridDim.x + blockIdx.x] = t;
+        dots[static_cast<int64_t>(j0 + threadIdx.x) * nb + boff + blockIdx.x] = t;
     }
 }
 
 // Last block of the grid (ticket) folds the per-block partials of every column in a fixed order
 // (one warp per column, lanes strided) into out[j]; leaves the ticket at zero.
 __device__ __forceinline__ void fold_dots_last_block(const double* dots, int ncols, unsigned* ticket,
-                                                     double* out) {
+                                                     double* out, int nb_total = 0) {
     if (!ticket) return;  // partials left for the consumer
     __shared__ bool last;
     __syncthreads();
@@ -64,7 +67,7 @@ __device__ __forceinline__ void fold_dots_last_block(const double* dots, int nco
     if (!last) return;
     __threadfence();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nb = static_cast<int>(gridDim.x);
+    const int nb = nb_total ? nb_total : static_cast<int>(gridDim.x);
     for (int j = warp; j < ncols; j += kRows / 32) {
         // four independent accumulators keep several L2 loads in flight per lane
         const double* pj = dots + static_cast<int64_t>(j) * nb;
@@ -90,6 +93,8 @@ struct DotOut {
     unsigned* ticket;    // zero on entry, left at zero
     double* out;         // folded x^T y per column
     const int* active;   // optional mask: skip inactive columns entirely
+    int nb_total = 0;    // partials per column when several launches share the buffer (0: gridDim.x)
+    int b_off = 0;       // this launch's first partial
 };
 
 // Columns this block applies: in range and (with a mask) still active.
@@ -197,19 +202,22 @@ __global__ void __launch_bounds__(kRows, BOSP_SELL_MINB) k_sell_cb(SellDev a, co
 template <int CB, bool DOT, bool PART>
 __global__ void __launch_bounds__(kRows) k_stencil(StencilDev st, const double* __restrict__ x,
                                                     int64_t ldx, double* __restrict__ y,
-                                                    int64_t ldy, int ncols, KTimer tm, DotOut dots) {
+                                                    int64_t ldy, int ncols, KTimer tm, DotOut dots,
+                                                    int64_t r0 = 0, int64_t r1 = -1) {
     tm.start();
     tm.columns(DOT ? dots.active : nullptr, 0, 0, ncols);
-    const int64_t n = st.nx * st.ny * st.nz;
+    // rows [r0, r1) of the local grid (default: all) -- the halo overlap applies the interior
+    // planes and the boundary planes in separate launches
+    const int64_t n = r1 < 0 ? st.nx * st.ny * st.nz : r1;
     const int j0 = blockIdx.y * CB;
     double d[CB];
 #pragma unroll
     for (int c = 0; c < CB; ++c) d[c] = 0.0;
     bool on[CB];
     const bool any = group_columns<CB, DOT>(dots, j0, ncols, on);
-    const int64_t ntiles = any ? (n + kRows - 1) / kRows : 0;
+    const int64_t ntiles = any ? (n - r0 + kRows - 1) / kRows : 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int64_t idx = tile * kRows + threadIdx.x;
+        const int64_t idx = r0 + tile * kRows + threadIdx.x;
         if (idx >= n) continue;
         const int64_t nxy = st.nx * st.ny;
         const int64_t i = idx % st.nx;
@@ -304,8 +312,8 @@ __global__ void __launch_bounds__(kRows) k_stencil(StencilDev st, const double* 
         }
     }
     if (DOT) {
-        block_dots_out<CB>(d, dots.parts, j0, ncols);
-        fold_dots_last_block(dots.parts, ncols, dots.ticket, dots.out);
+        block_dots_out<CB>(d, dots.parts, j0, ncols, dots.nb_total, dots.b_off);
+        fold_dots_last_block(dots.parts, ncols, dots.ticket, dots.out, dots.nb_total);
     }
     tm.stop();
 }
@@ -1014,7 +1022,7 @@ int dia_spmm(const DiaDev& a, const DMat& x, const DMat& y, const SpmmDot* dot) 
     return static_cast<int>(gx);
 }
 
-int stencil_spmm(const StencilDev& s, const DMat& x, const DMat& y, const SpmmDot* dot) {
+int stencil_spmm(const StencilDev& s, const DMat& x, const DMat& y, const SpmmDot* dot, const StencilOverlap* ov) {
     const int64_t n = s.nx * s.ny * s.nz;
     if (n == 0 || x.cols == 0) return 0;
     Runtime& rt = Runtime::get();
@@ -1033,7 +1041,46 @@ int stencil_spmm(const StencilDev& s, const DMat& x, const DMat& y, const SpmmDo
     const int64_t snl = s.dims == 3 ? s.nz : s.ny;
     const bool part = s.s_global > 0 && (s.s0 > 0 || s.s0 + snl < s.s_global);
     const DotOut dd = dot ? DotOut{dot->parts, dot->ticket, dot->out, dot->active} : DotOut{};
+    if (part && ov && snl >= 3) {
+        // Halo overlap: the interior planes need no halo, so they are applied while
+        // the boundary planes travel (ov->exchange posts the exchange on its own stream after
+        // the interior launch and makes this stream wait for it); the one or two boundary
+        // planes follow.  The launches share the dot partials (slices b_off.. of nb_total per
+        // column); the last launch folds them.
+        const int64_t lo_n = ov->has_lo ? ov->plane : 0, hi_n = ov->has_hi ? ov->plane : 0;
+        const int64_t cap = dot ? std::max<int64_t>(4, dot->parts_cap / std::max(ncols, 1)) : (int64_t(1) << 30);
+        auto tiles_of = [&](int64_t rows) {
+            return static_cast<unsigned>(std::min<int64_t>((rows + kRows - 1) / kRows, cap / 4));
+        };
+        const unsigned g_lo = lo_n ? tiles_of(lo_n) : 0u, g_hi = hi_n ? tiles_of(hi_n) : 0u;
+        unsigned g_in = row_blocks(n - lo_n - hi_n, dot, ncols);
+        g_in = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(g_in, cap - g_lo - g_hi)));
+        const int nbt = static_cast<int>(g_in + g_lo + g_hi);
+        auto launch = [&](int64_t r0, int64_t r1, unsigned gxr, unsigned boff, bool fold) {
+            DotOut d2 = dd;
+            d2.nb_total = nbt;
+            d2.b_off = static_cast<int>(boff);
+            if (!fold) d2.ticket = nullptr;
+            const double frac = static_cast<double>(r1 - r0) / static_cast<double>(n);
+            KTimer tr{rt.timer_begin(fam, bytes * frac, flops * frac, 0.0, ncols)};
+            LaunchScope lr(fam, bytes * frac, flops * frac, false);
+            const dim3 g(gxr, (ncols + CB - 1) / CB);
+            if (dot) k_stencil<CB, true, true><<<g, kRows, 0, rt.stream()>>>(s, x.p, x.ld, y.p, y.ld, ncols, tr, d2, r0, r1);
+            else k_stencil<CB, false, true><<<g, kRows, 0, rt.stream()>>>(s, x.p, x.ld, y.p, y.ld, ncols, tr, d2, r0, r1);
+            BOSP_LAUNCH_CHECK();
+        };
+        static const bool dbg = std::getenv("BOSP_DEBUG_HALO") != nullptr;
+        if (dbg)
+            std::fprintf(stderr, "[bosp] stencil halo overlap: interior rows [%lld, %lld) in %u blocks, boundary %u + %u blocks, %d columns%s\n",
+                         (long long)lo_n, (long long)(n - hi_n), g_in, g_lo, g_hi, ncols, dot ? ", dots" : "");
+        launch(lo_n, n - hi_n, g_in, 0u, false);
+        ov->exchange();
+        if (lo_n) launch(0, lo_n, g_lo, g_in, hi_n == 0);
+        if (hi_n) launch(n - hi_n, n, g_hi, g_in + g_lo, true);
+        return nbt;
+    }
     if (part) {
+        if (ov) ov->exchange();  // a slab of one or two planes: no interior to overlap with
         if (dot) k_stencil<CB, true, true><<<grid, kRows, 0, rt.stream()>>>(s, x.p, x.ld, y.p, y.ld, ncols, tm, dd);
         else k_stencil<CB, false, true><<<grid, kRows, 0, rt.stream()>>>(s, x.p, x.ld, y.p, y.ld, ncols, tm, dd);
     } else if ((s.nx & 1) == 0 && (x.ld & 1) == 0 && (y.ld & 1) == 0 && n < (int64_t(1) << 32)) {
