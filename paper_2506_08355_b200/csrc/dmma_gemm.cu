@@ -416,7 +416,12 @@ __global__ void __launch_bounds__(kCoefThreads) k_gram_reduce_coef(GramParams pr
     const int64_t e = static_cast<int64_t>(blockIdx.x) * kE + el;
     const int64_t total = static_cast<int64_t>(LDP) * LDP;
     double s0 = 0.0, s1 = 0.0;
-    if (e < total) {
+    // symmetric: only the upper triangle of the real columns is stored (and mirrored) -- the
+    // rest of the LDP x LDP partial (padding, the uncomputed lower tiles) is not even read
+    // (m = 20: 820 of 4096 elements)
+    const int em = static_cast<int>(e % LDP), en = static_cast<int>(e / LDP);
+    const bool need = e < total && em <= en && en < job.b.cols();
+    if (need) {
         const double* part = prm.partial + e;
         int sp = grp;
 #pragma unroll 4
@@ -428,12 +433,11 @@ __global__ void __launch_bounds__(kCoefThreads) k_gram_reduce_coef(GramParams pr
     }
     part_sum[grp][el] = s0 + s1;
     __syncthreads();
-    if (grp == 0 && e < total) {
+    if (grp == 0 && need) {
         double s = 0.0;
 #pragma unroll
         for (int g = 0; g < kG; ++g) s += part_sum[g][el];
-        const int m = static_cast<int>(e % LDP), nn = static_cast<int>(e / LDP);
-        if (m < job.a.cols() && nn < job.b.cols()) gram_store(job, true, m, nn, s);
+        gram_store(job, true, em, en, s);
     }
     __threadfence();
     __syncthreads();
